@@ -1,0 +1,157 @@
+/*
+ * bkfac.h — C ABI of the B200-native B-KFAC hot path (arxiv 2210.08494).
+ *
+ * What it computes (BASELINE.json north_star; PAPER.md = /root/reference/PAPER.md):
+ *   - bkfac_brand_update: the per-step symmetric Brand low-rank eigen-update of an
+ *     exponential-average (EA) K-factor: the top-r eigendecomposition of
+ *         alpha * U_in diag(D_in) U_in^T + beta * M M^T
+ *     (Alg 3; Alg 4, :536-552, which passes (U, rho*D, sqrt(1-rho)*A);
+ *     the B-process Eq.(10), :580-589).  Per step alpha = rho, beta = 1 - rho; at the
+ *     first step alpha = 0, beta = 1 (Mtilde_{B,0} = M_0 M_0^T, :584; kappa(0) = 1, :362).
+ *     When r + c >= n the B-update is "not applicable" (:457, :493); the library then
+ *     forms the n x n sum densely and eigendecomposes it (same result, SURVEY §8(a) a6').
+ *   - bkfac_ea_accumulate: the dense EA update K <- rho K + (1 - rho) M M^T
+ *     (Alg 1 lines 5/9, :381, :390; Eq.(8) :563-568).  rho = 0 gives K = M M^T (k = 0).
+ *   - bkfac_rsvd_overwrite: the B-R-KFAC overwrite (Alg 5, :641-646): randomized range
+ *     finder on the dense EA factor (Alg 1 line 13, :397): Gaussian sketch + power
+ *     iterations, symmetric projection, small EVD, top-r.
+ *   - bkfac_precondition: S = Gamma~^{-1} J A~^{-1} with the regularised low-rank
+ *     inverses of Alg 1 lines 16-17 (:403-405), J = Mat(g) (:359, :401), optionally with
+ *     spectrum continuation (:711) and relative lambda (lambda = lambda * max D, :940).
+ *
+ * Conventions
+ *   - All float buffers are DEVICE memory owned by the caller, fp32.
+ *   - "col-major a x b" = each length-a column is contiguous (a PyTorch tensor of
+ *     shape (b, a)).  U (n x r), M (n x c), K_dense (n x n, symmetric) are col-major.
+ *     J and S are row-major d_G x d_A (PyTorch weight.grad layout).
+ *   - D arrays have length r, are non-increasing and >= 0 on output.
+ *   - The library never allocates device memory: the caller allocates the workspace
+ *     (bkfac_workspace_bytes) and registers it (bkfac_set_workspace).  The context
+ *     retains no caller pointer beyond a call except that workspace.
+ *   - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t, passed
+ *     as void* so this header needs no CUDA include).  Argument validation is
+ *     synchronous and returns immediately with an error code; no work is enqueued
+ *     on error.  Device-side numeric trouble (non-finite inputs, eigensolver
+ *     failure) sets a per-factor status word reported by bkfac_check.
+ *   - A context is not thread-safe; use one per device/thread.
+ */
+#ifndef BKFAC_H
+#define BKFAC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bkfac_ctx_s* bkfac_ctx;
+
+typedef enum {
+  BKFAC_OK = 0,
+  BKFAC_ERR_INVALID_ARG = 1,  /* null pointer, alpha < 0, beta <= 0, lambda <= 0, bad index */
+  BKFAC_ERR_DIM = 2,          /* c > c_max, r > n, dimension mismatch with the descriptor    */
+  BKFAC_ERR_RANK = 3,         /* r + oversample > n (RSVD)                                    */
+  BKFAC_ERR_ALIAS = 4,        /* U_out aliases U_in (or D_out aliases D_in)                   */
+  BKFAC_ERR_WORKSPACE = 5,    /* workspace missing or too small                               */
+  BKFAC_ERR_CUDA = 6,         /* a CUDA runtime call failed                                   */
+  BKFAC_ERR_NUMERIC = 7,      /* device status word reports non-finite data / no convergence  */
+  BKFAC_ERR_UNSUPPORTED = 8   /* shape outside what this build supports                       */
+} bkfac_status;
+
+/* bkfac_factor_desc.flags */
+#define BKFAC_FACTOR_DENSE_EA 1   /* the factor may be RSVD-overwritten: reserve RSVD workspace */
+
+/* bkfac_brand_args.flags */
+#define BKFAC_BRAND_NO_REORTH 1   /* skip the second (CGS2) projection against U           */
+
+/* bkfac_precond_args.flags */
+#define BKFAC_PRECOND_CONTINUATION 1    /* lambda <- lambda + min D, D <- D - min D (:711)  */
+#define BKFAC_PRECOND_LAMBDA_RELATIVE 2 /* lambda <- lambda * max D (phi_lambda, :940)      */
+
+/* One K-factor: dimension n, target rank r (1 <= r <= n), largest batch c_max.       */
+typedef struct { int n; int r; int c_max; int flags; } bkfac_factor_desc;
+
+/* One preconditioned layer: gradient J is d_G x d_A (row-major); ranks of its factors. */
+typedef struct { int d_G; int d_A; int r_G; int r_A; } bkfac_layer_desc;
+
+/* Creates a context on CUDA device `device` for `nfactors` factors and `nlayers`
+ * layers.  Descriptors are copied.  Returns BKFAC_ERR_DIM on invalid shapes. */
+bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nfactors,
+                        const bkfac_layer_desc* layers, int nlayers, int device);
+
+/* Bytes of device workspace needed so that every factor and layer can be processed
+ * in a single batched call (all of them concurrently). */
+size_t bkfac_workspace_bytes(bkfac_ctx ctx);
+
+/* Registers caller-owned device memory (>= bkfac_workspace_bytes, 256-B aligned).
+ * Also holds the per-factor status words; they are cleared here. */
+bkfac_status bkfac_set_workspace(bkfac_ctx ctx, void* dev_ptr, size_t bytes);
+
+bkfac_status bkfac_destroy(bkfac_ctx ctx);
+
+/* U_out (n x r col-major), D_out (r) = top_r( alpha U_in diag(D_in) U_in^T + beta M M^T ).
+ * U_in must have orthonormal columns (any orthonormal basis with D_in = 0 at init).
+ * M is col-major n x c, c <= c_max.  U_out must not alias U_in (BKFAC_ERR_ALIAS); the
+ * caller ping-pongs two buffers.  Eigenvector signs are unspecified.  `count`
+ * updates (distinct factors) run as one batch. */
+typedef struct {
+  int factor;
+  const float* U_in; const float* D_in;
+  const float* M; int c;
+  float* U_out; float* D_out;
+  float alpha; float beta;
+  int flags;
+} bkfac_brand_args;
+bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int count,
+                                void* stream);
+
+/* K_dense (n x n) <- rho K_dense + (1 - rho) M M^T.  Requires BKFAC_FACTOR_DENSE_EA. */
+bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K_dense, const float* M,
+                                 int c, float rho, void* stream);
+
+/* U_out (n x r), D_out (r) <- RSVD of K_dense with l = r + oversample sketch columns and
+ * `power_iters` re-orthonormalised power iterations.  The Gaussian sketch is
+ * Philox4x32-10 keyed by `seed`, stream `counter`. */
+bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K_dense,
+                                  int oversample, int power_iters, uint64_t seed,
+                                  uint64_t counter, float* U_out, float* D_out, void* stream);
+
+/* Omega (n x l col-major) <- the RSVD Gaussian test matrix for (seed, counter): the
+ * sketch step of bkfac_rsvd_overwrite exposed on its own (Philox4x32-10, key = seed,
+ * counter words (e/4 lo, e/4 hi, counter lo, counter hi) for element e = j*n + i;
+ * Box-Muller in fp64 on the word pair ((e%4)/2)*2, cos for even e, sin for odd e). */
+bkfac_status bkfac_gaussian_sketch(float* Omega, int n, int l, uint64_t seed, uint64_t counter,
+                                   void* stream);
+
+/* S (d_G x d_A row-major) = Gamma~^{-1} J A~^{-1}, with
+ *   A~^{-1} = U_A diag((D_A + lambda_A)^{-1} - 1/lambda_A) U_A^T + I/lambda_A  (and Gamma).
+ * S must not alias J.  `layer` indexes the layer descriptors given to bkfac_init. */
+typedef struct {
+  int layer;
+  const float* U_G; const float* D_G; float lambda_G;
+  const float* U_A; const float* D_A; float lambda_A;
+  const float* J; float* S;
+  int flags;
+} bkfac_precond_args;
+bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, int count,
+                                void* stream);
+
+/* Synchronises `stream`, reads the per-factor status words.  Returns BKFAC_OK or
+ * BKFAC_ERR_NUMERIC (first offending factor in *first_bad_factor, else -1).
+ * Informational bits (e.g. a Cholesky pivot dropped for a rank-deficient residual)
+ * are returned in *info_bits (OR over factors) without failing. */
+bkfac_status bkfac_check(bkfac_ctx ctx, void* stream, int* first_bad_factor, int* info_bits);
+
+/* Number of kernels this context has launched since creation (host-side counter). */
+uint64_t bkfac_launch_count(bkfac_ctx ctx);
+
+const char* bkfac_status_string(bkfac_status s);
+
+/* Build identification string (compile flags / arch). */
+const char* bkfac_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BKFAC_H */

@@ -1,0 +1,212 @@
+"""ctypes binding of the bkfac C ABI (include/bkfac.h).  Argument marshalling only:
+every step of the hot path runs in the CUDA kernels of ``libbkfac.so``.
+
+Tensor conventions (PyTorch, all fp32, CUDA, contiguous):
+  U: shape (r, n)   == col-major n x r          M: shape (c, n) == col-major n x c
+  D: shape (r,)                                  K_dense: shape (n, n) (symmetric)
+  J, S: shape (d_G, d_A)  == row-major d_G x d_A (weight.grad layout)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbkfac.so")
+
+BKFAC_FACTOR_DENSE_EA = 1
+BKFAC_BRAND_NO_REORTH = 1
+BKFAC_PRECOND_CONTINUATION = 1
+BKFAC_PRECOND_LAMBDA_RELATIVE = 2
+
+STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKFAC_ERR_RANK",
+          4: "BKFAC_ERR_ALIAS", 5: "BKFAC_ERR_WORKSPACE", 6: "BKFAC_ERR_CUDA",
+          7: "BKFAC_ERR_NUMERIC", 8: "BKFAC_ERR_UNSUPPORTED"}
+
+EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac_destroy",
+            "bkfac_brand_update", "bkfac_ea_accumulate", "bkfac_rsvd_overwrite",
+            "bkfac_precondition", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count", "bkfac_status_string",
+            "bkfac_build_info"]
+
+
+class BkfacError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {STATUS.get(code, code)}")
+        self.code = code
+
+
+class FactorDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("r", ctypes.c_int), ("c_max", ctypes.c_int),
+                ("flags", ctypes.c_int)]
+
+
+class LayerDesc(ctypes.Structure):
+    _fields_ = [("d_G", ctypes.c_int), ("d_A", ctypes.c_int), ("r_G", ctypes.c_int),
+                ("r_A", ctypes.c_int)]
+
+
+class BrandArgs(ctypes.Structure):
+    _fields_ = [("factor", ctypes.c_int), ("U_in", ctypes.c_void_p), ("D_in", ctypes.c_void_p),
+                ("M", ctypes.c_void_p), ("c", ctypes.c_int), ("U_out", ctypes.c_void_p),
+                ("D_out", ctypes.c_void_p), ("alpha", ctypes.c_float), ("beta", ctypes.c_float),
+                ("flags", ctypes.c_int)]
+
+
+class PrecondArgs(ctypes.Structure):
+    _fields_ = [("layer", ctypes.c_int), ("U_G", ctypes.c_void_p), ("D_G", ctypes.c_void_p),
+                ("lambda_G", ctypes.c_float), ("U_A", ctypes.c_void_p), ("D_A", ctypes.c_void_p),
+                ("lambda_A", ctypes.c_float), ("J", ctypes.c_void_p), ("S", ctypes.c_void_p),
+                ("flags", ctypes.c_int)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libbkfac.so.  Raises loudly if it is missing: there is no fallback path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"bkfac CUDA library not built: {path} is missing "
+                           "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
+    lib = ctypes.CDLL(path)
+    vp, ci, cf, sz, u64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_size_t, ctypes.c_uint64
+    lib.bkfac_init.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(FactorDesc), ci,
+                               ctypes.POINTER(LayerDesc), ci, ci]
+    lib.bkfac_init.restype = ci
+    lib.bkfac_workspace_bytes.argtypes = [vp]
+    lib.bkfac_workspace_bytes.restype = sz
+    lib.bkfac_set_workspace.argtypes = [vp, vp, sz]
+    lib.bkfac_set_workspace.restype = ci
+    lib.bkfac_destroy.argtypes = [vp]
+    lib.bkfac_destroy.restype = ci
+    lib.bkfac_brand_update.argtypes = [vp, ctypes.POINTER(BrandArgs), ci, vp]
+    lib.bkfac_brand_update.restype = ci
+    lib.bkfac_ea_accumulate.argtypes = [vp, ci, vp, vp, ci, cf, vp]
+    lib.bkfac_ea_accumulate.restype = ci
+    lib.bkfac_rsvd_overwrite.argtypes = [vp, ci, vp, ci, ci, u64, u64, vp, vp, vp]
+    lib.bkfac_rsvd_overwrite.restype = ci
+    lib.bkfac_gaussian_sketch.argtypes = [vp, ci, ci, u64, u64, vp]
+    lib.bkfac_gaussian_sketch.restype = ci
+    lib.bkfac_precondition.argtypes = [vp, ctypes.POINTER(PrecondArgs), ci, vp]
+    lib.bkfac_precondition.restype = ci
+    lib.bkfac_check.argtypes = [vp, vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
+    lib.bkfac_check.restype = ci
+    lib.bkfac_launch_count.argtypes = [vp]
+    lib.bkfac_launch_count.restype = u64
+    lib.bkfac_status_string.argtypes = [ci]
+    lib.bkfac_status_string.restype = ctypes.c_char_p
+    lib.bkfac_build_info.argtypes = []
+    lib.bkfac_build_info.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(code: int, where: str) -> None:
+    if code != 0:
+        raise BkfacError(code, where)
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch.Tensor")
+    if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError("bkfac expects contiguous float32 CUDA tensors")
+    return t.data_ptr()
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Context:
+    """Owns a bkfac_ctx and its device workspace (a torch uint8 tensor)."""
+
+    def __init__(self, factors: Sequence[tuple], layers: Sequence[tuple] = (), device: int = 0):
+        import torch
+        self.lib = load()
+        self.device = device
+        fd = (FactorDesc * max(1, len(factors)))(*[FactorDesc(*f) for f in factors])
+        ld = (LayerDesc * max(1, len(layers)))(*[LayerDesc(*l) for l in layers])
+        h = ctypes.c_void_p()
+        _check(self.lib.bkfac_init(ctypes.byref(h), fd, len(factors), ld, len(layers), device),
+               "bkfac_init")
+        self.h = h
+        self.factors = [tuple(f) for f in factors]
+        self.layers = [tuple(l) for l in layers]
+        nbytes = int(self.lib.bkfac_workspace_bytes(h))
+        self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8,
+                                     device=f"cuda:{device}")
+        _check(self.lib.bkfac_set_workspace(h, self.workspace.data_ptr(), self.workspace.numel()),
+               "bkfac_set_workspace")
+
+    def close(self) -> None:
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.bkfac_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- calls with the C names --------------------------------------------------------
+    def bkfac_brand_update(self, updates: List[dict], stream=None) -> None:
+        arr = (BrandArgs * len(updates))()
+        for i, u in enumerate(updates):
+            arr[i] = BrandArgs(u["factor"], _ptr(u["U_in"]), _ptr(u["D_in"]), _ptr(u["M"]),
+                               int(u["M"].shape[0]), _ptr(u["U_out"]), _ptr(u["D_out"]),
+                               float(u["alpha"]), float(u["beta"]), int(u.get("flags", 0)))
+        _check(self.lib.bkfac_brand_update(self.h, arr, len(updates), _stream_ptr(stream)),
+               "bkfac_brand_update")
+
+    def bkfac_ea_accumulate(self, factor: int, K, M, rho: float, stream=None) -> None:
+        _check(self.lib.bkfac_ea_accumulate(self.h, factor, _ptr(K), _ptr(M), int(M.shape[0]),
+                                            float(rho), _stream_ptr(stream)),
+               "bkfac_ea_accumulate")
+
+    def bkfac_rsvd_overwrite(self, factor: int, K, oversample: int, power_iters: int,
+                             seed: int, counter: int, U_out, D_out, stream=None) -> None:
+        _check(self.lib.bkfac_rsvd_overwrite(self.h, factor, _ptr(K), oversample, power_iters,
+                                             seed, counter, _ptr(U_out), _ptr(D_out),
+                                             _stream_ptr(stream)),
+               "bkfac_rsvd_overwrite")
+
+    def bkfac_precondition(self, items: List[dict], stream=None) -> None:
+        arr = (PrecondArgs * len(items))()
+        for i, a in enumerate(items):
+            arr[i] = PrecondArgs(a["layer"], _ptr(a["U_G"]), _ptr(a["D_G"]), float(a["lambda_G"]),
+                                 _ptr(a["U_A"]), _ptr(a["D_A"]), float(a["lambda_A"]),
+                                 _ptr(a["J"]), _ptr(a["S"]), int(a.get("flags", 0)))
+        _check(self.lib.bkfac_precondition(self.h, arr, len(items), _stream_ptr(stream)),
+               "bkfac_precondition")
+
+    def bkfac_check(self, stream=None):
+        bad = ctypes.c_int(-1)
+        info = ctypes.c_int(0)
+        code = self.lib.bkfac_check(self.h, _stream_ptr(stream), ctypes.byref(bad),
+                                    ctypes.byref(info))
+        return code, bad.value, info.value
+
+    def bkfac_launch_count(self) -> int:
+        return int(self.lib.bkfac_launch_count(self.h))
+
+
+def bkfac_gaussian_sketch(Omega, seed: int, counter: int, stream=None) -> None:
+    """Omega: tensor of shape (l, n) (col-major n x l) filled with the RSVD sketch."""
+    l, n = Omega.shape
+    _check(load().bkfac_gaussian_sketch(_ptr(Omega), n, l, seed, counter, _stream_ptr(stream)),
+           "bkfac_gaussian_sketch")
+
+
+def bkfac_status_string(code: int) -> str:
+    return load().bkfac_status_string(code).decode()

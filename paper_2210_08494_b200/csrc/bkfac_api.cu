@@ -1,0 +1,887 @@
+// C ABI of the B-KFAC hot path (include/bkfac.h): workspace planning, validation and
+// the stream-ordered stage sequence of each call.  All arithmetic runs in the kernels
+// of gemm_*.cuh, chol.cuh, eig.cuh and misc.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "bkfac.h"
+#include "chol.cuh"
+#include "common.cuh"
+#include "eig.cuh"
+#include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
+#include "misc.cuh"
+
+using namespace bkfac;
+
+namespace {
+
+constexpr int kSplitMax = 16;
+constexpr int kNumSM = 148;
+constexpr int kRsvdOversampleMax = 32;
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Arena {
+  size_t cur = 0;
+  size_t take(size_t bytes) {
+    size_t o = cur;
+    cur += align256(bytes ? bytes : 1);
+    return o;
+  }
+};
+
+struct EigWs {  // workspace of one eigen problem of order <= m with <= r outputs
+  size_t K, d, e, tau, lam, Y, scr, piv, V;
+  int m, r;
+};
+
+void plan_eig(Arena& a, EigWs& w, int m, int r) {
+  w.m = m; w.r = r;
+  w.K = a.take(sizeof(float) * (size_t)m * m);
+  w.d = a.take(sizeof(float) * m);
+  w.e = a.take(sizeof(float) * m);
+  w.tau = a.take(sizeof(float) * m);
+  w.lam = a.take(sizeof(double) * r);
+  w.Y = a.take(sizeof(double) * (size_t)m * r);
+  w.scr = a.take(sizeof(double) * 4 * (size_t)m * r);
+  w.piv = a.take((size_t)m * r);
+  w.V = a.take(sizeof(float) * (size_t)m * r);
+}
+
+struct FactorPlan {
+  bkfac_factor_desc d;
+  bool dense = false;  // r + c_max >= n: form the n x n sum densely (a6')
+  int m = 0;           // core order (r + c_max, or n on the dense path)
+  // Brand path
+  size_t W, P2, R, Qb, G, L1, L1i, L2, L2i, cscr, ws;
+  size_t ws_elems = 0;
+  // dense path
+  size_t T;
+  EigWs eig;
+  // RSVD
+  bool rsvd = false;
+  int lmax = 0;
+  size_t Yr, Qr, Q2r, Tr, Gr, L1r, L1ir, L2r, L2ir, Br, cscr_r, ws_r;
+  size_t ws_r_elems = 0;
+  EigWs eig_r;
+};
+
+struct LayerPlan {
+  bkfac_layer_desc d;
+  size_t Y, Xt, Z, sA, sG, lam, ws;  // lam: [lamA, lamG, coef]
+  size_t ws_elems = 0;
+};
+
+}  // namespace
+
+struct bkfac_ctx_s {
+  int device = 0;
+  std::vector<FactorPlan> f;
+  std::vector<LayerPlan> l;
+  size_t ws_bytes = 0;
+  size_t status_off = 0;
+  char* ws = nullptr;
+  size_t ws_cap = 0;
+  uint64_t launches = 0;
+  int* host_status = nullptr;
+  bool use_tc = true;
+};
+
+namespace {
+
+template <typename T>
+T* at(bkfac_ctx c, size_t off) { return reinterpret_cast<T*>(c->ws + off); }
+
+int* status_ptr(bkfac_ctx c, int factor) { return at<int>(c, c->status_off) + factor; }
+
+bool cuda_ok(cudaError_t e) {
+  if (e != cudaSuccess) {
+    fprintf(stderr, "bkfac: CUDA error %s\n", cudaGetErrorString(e));
+    return false;
+  }
+  return true;
+}
+
+#define LAUNCH_CHECK(ctx)                                   \
+  do {                                                      \
+    (ctx)->launches++;                                      \
+    if (!cuda_ok(cudaGetLastError())) return BKFAC_ERR_CUDA; \
+  } while (0)
+
+// ------------------------------------------------------------------ GEMM stage
+struct GemmStage {
+  std::vector<GemmProb> probs[4];
+  std::vector<long> caps[4];
+  void add(bool ta, bool tb, const GemmProb& p, long ws_cap_elems) {
+    const int v = (ta ? 2 : 0) + (tb ? 1 : 0);
+    probs[v].push_back(p);
+    caps[v].push_back(ws_cap_elems);
+  }
+  bool empty() const {
+    return probs[0].empty() && probs[1].empty() && probs[2].empty() && probs[3].empty();
+  }
+};
+
+GemmProb gp(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N,
+            int K, float alpha, const float* C0 = nullptr, int ldc0 = 0, float beta = 0.f) {
+  GemmProb p;
+  memset(&p, 0, sizeof(p));
+  p.A = A; p.lda = lda; p.A2 = A; p.lda2 = lda;
+  p.B = B; p.ldb = ldb; p.B2 = B; p.ldb2 = ldb;
+  p.C = C; p.ldc = ldc; p.C0 = C0 ? C0 : C; p.ldc0 = C0 ? ldc0 : ldc;
+  p.M = M; p.N = N; p.K = K; p.k1 = K;
+  p.alpha = alpha; p.beta = beta;
+  return p;
+}
+
+template <bool TA, bool TB>
+bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_t st) {
+  size_t i0 = 0;
+  while (i0 < v.size()) {
+    const size_t n = std::min(v.size() - i0, (size_t)GEMM_MAXP);
+    static GemmBatch b;  // host staging (large); kernel params are copied at launch
+    b.nprob = (int)n;
+    int tiles = 0;
+    bool any_split = false;
+    for (size_t i = 0; i < n; ++i) {
+      GemmProb p = v[i0 + i];
+      p.tile_start = tiles;
+      tiles += p.tiles_m * p.tiles_n * p.splits;
+      any_split |= p.splits > 1;
+      b.p[i] = p;
+    }
+    b.total_tiles = tiles;
+    if (tiles > 0) {
+      gemm_simt_kernel<TA, TB><<<tiles, 256, 0, st>>>(b);
+      LAUNCH_CHECK(ctx);
+      if (any_split) {
+        gemm_splitk_reduce_kernel<<<dim3(64, (unsigned)n), 256, 0, st>>>(b);
+        LAUNCH_CHECK(ctx);
+      }
+    }
+    i0 += n;
+  }
+  return BKFAC_OK;
+}
+
+bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
+  // split-K: aim for ~2 waves of CTAs over the whole stage
+  long base_tiles = 0;
+  for (int v = 0; v < 4; ++v)
+    for (auto& p : s.probs[v]) {
+      p.tiles_m = ceil_div(std::max(p.M, 1), SG_BM);
+      p.tiles_n = ceil_div(std::max(p.N, 1), SG_BN);
+      if (p.M <= 0 || p.N <= 0) p.tiles_m = p.tiles_n = 0;
+      base_tiles += (long)p.tiles_m * p.tiles_n;
+    }
+  const long target = 2L * kNumSM;
+  for (int v = 0; v < 4; ++v)
+    for (size_t i = 0; i < s.probs[v].size(); ++i) {
+      GemmProb& p = s.probs[v][i];
+      int splits = 1;
+      if (p.K >= 1024 && base_tiles > 0 && base_tiles < target && p.ws != nullptr) {
+        splits = (int)std::min<long>(kSplitMax, (target + base_tiles - 1) / base_tiles);
+        splits = std::min(splits, p.K / 256);
+        const long mn = (long)p.M * p.N;
+        if (mn > 0) splits = (int)std::min<long>(splits, s.caps[v][i] / mn);
+        splits = std::max(splits, 1);
+      }
+      int kchunk = p.K;
+      if (splits > 1) {
+        kchunk = ceil_div(p.K, splits);
+        kchunk = (kchunk + SG_BK - 1) / SG_BK * SG_BK;
+        splits = ceil_div(p.K, kchunk);
+      }
+      p.splits = splits;
+      p.kchunk = std::max(kchunk, 1);
+    }
+  bkfac_status r;
+  if ((r = launch_variant<false, false>(ctx, s.probs[0], st)) != BKFAC_OK) return r;
+  if ((r = launch_variant<false, true>(ctx, s.probs[1], st)) != BKFAC_OK) return r;
+  if ((r = launch_variant<true, false>(ctx, s.probs[2], st)) != BKFAC_OK) return r;
+  if ((r = launch_variant<true, true>(ctx, s.probs[3], st)) != BKFAC_OK) return r;
+  for (int v = 0; v < 4; ++v) { s.probs[v].clear(); s.caps[v].clear(); }
+  return BKFAC_OK;
+}
+
+// ------------------------------------------------------------------ small stages
+bkfac_status run_ew(bkfac_ctx ctx, std::vector<EwProb>& v, cudaStream_t st) {
+  size_t i0 = 0;
+  while (i0 < v.size()) {
+    const size_t n = std::min(v.size() - i0, (size_t)EW_MAXP);
+    static EwBatch b;
+    b.nprob = (int)n;
+    for (size_t i = 0; i < n; ++i) b.p[i] = v[i0 + i];
+    ew_kernel<<<dim3(128, (unsigned)n), 256, 0, st>>>(b);
+    LAUNCH_CHECK(ctx);
+    i0 += n;
+  }
+  v.clear();
+  return BKFAC_OK;
+}
+
+bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) {
+  std::vector<CholProb> small, big;
+  int cmax_small = 0;
+  for (auto& p : v) {
+    if (p.c <= CHOL_SMEM_MAX) { small.push_back(p); cmax_small = std::max(cmax_small, p.c); }
+    else big.push_back(p);
+  }
+  static CholBatch b;
+  for (int pass = 0; pass < 2; ++pass) {
+    auto& list = pass == 0 ? small : big;
+    size_t i0 = 0;
+    while (i0 < list.size()) {
+      const size_t n = std::min(list.size() - i0, (size_t)CHOL_MAXP);
+      b.nprob = (int)n;
+      int cmax = 0;
+      for (size_t i = 0; i < n; ++i) { b.p[i] = list[i0 + i]; cmax = std::max(cmax, b.p[i].c); }
+      if (pass == 0) {
+        const size_t smem = sizeof(float) * ((size_t)cmax * (cmax + 1) / 2 + cmax + 32);
+        chol_inv_kernel<true><<<(unsigned)n, 1024, smem, st>>>(b);
+      } else {
+        const size_t smem = sizeof(float) * ((size_t)cmax + 32);
+        chol_inv_kernel<false><<<(unsigned)n, 1024, smem, st>>>(b);
+      }
+      LAUNCH_CHECK(ctx);
+      i0 += n;
+    }
+  }
+  v.clear();
+  return BKFAC_OK;
+}
+
+bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
+  size_t i0 = 0;
+  static EigBatch b;
+  while (i0 < v.size()) {
+    const size_t n = std::min(v.size() - i0, (size_t)EIG_MAXP);
+    b.nprob = (int)n;
+    int mmax = 0, rmax = 0;
+    for (size_t i = 0; i < n; ++i) {
+      b.p[i] = v[i0 + i];
+      mmax = std::max(mmax, b.p[i].m);
+      rmax = std::max(rmax, b.p[i].r);
+    }
+    sytrd_kernel<<<(unsigned)n, 1024, sizeof(float) * (4 * (size_t)mmax + 32), st>>>(b);
+    LAUNCH_CHECK(ctx);
+    bisect_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, BIS_WARPS)), BIS_WARPS * 32,
+                    sizeof(double) * 2 * (size_t)mmax, st>>>(b);
+    LAUNCH_CHECK(ctx);
+    invit_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, 128)), 128, 0, st>>>(b);
+    LAUNCH_CHECK(ctx);
+    cluster_kernel<<<(unsigned)n, 1024, 0, st>>>(b);
+    LAUNCH_CHECK(ctx);
+    backtr_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, 32)), 1024,
+                    sizeof(float) * 33 * (size_t)mmax, st>>>(b);
+    LAUNCH_CHECK(ctx);
+    i0 += n;
+  }
+  v.clear();
+  return BKFAC_OK;
+}
+
+EigProb eig_prob(bkfac_ctx ctx, const EigWs& w, int m, int r, float* V, int ldv, float* Dout,
+                 int* status) {
+  EigProb p;
+  p.K = at<float>(ctx, w.K); p.ldk = m;
+  p.m = m; p.r = r;
+  p.d = at<float>(ctx, w.d); p.e = at<float>(ctx, w.e); p.tau = at<float>(ctx, w.tau);
+  p.lam = at<double>(ctx, w.lam);
+  p.Y = at<double>(ctx, w.Y);
+  p.scr = at<double>(ctx, w.scr);
+  p.piv = at<unsigned char>(ctx, w.piv);
+  p.V = V; p.ldv = ldv;
+  p.Dout = Dout;
+  p.status = status;
+  return p;
+}
+
+CholProb chol_prob(bkfac_ctx ctx, const float* G, int c, size_t L, size_t Li, size_t scr,
+                   int* status) {
+  CholProb p;
+  p.G = G; p.ldg = c;
+  p.L = at<float>(ctx, L); p.Linv = at<float>(ctx, Li);
+  p.scratch = at<float>(ctx, scr);
+  p.status = status;
+  p.c = c;
+  return p;
+}
+
+void gemm_ws(GemmProb& p, float* ws) { p.ws = ws; }
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char* bkfac_status_string(bkfac_status s) {
+  switch (s) {
+    case BKFAC_OK: return "ok";
+    case BKFAC_ERR_INVALID_ARG: return "invalid argument";
+    case BKFAC_ERR_DIM: return "dimension error";
+    case BKFAC_ERR_RANK: return "rank too large";
+    case BKFAC_ERR_ALIAS: return "output aliases input";
+    case BKFAC_ERR_WORKSPACE: return "workspace missing or too small";
+    case BKFAC_ERR_CUDA: return "CUDA error";
+    case BKFAC_ERR_NUMERIC: return "numeric failure on device";
+    case BKFAC_ERR_UNSUPPORTED: return "unsupported shape";
+  }
+  return "unknown status";
+}
+
+const char* bkfac_build_info(void) {
+  return "bkfac sm_100a; SIMT fp32 GEMM + tcgen05 3xTF32 GEMM; CholeskyQR2; Householder "
+         "tridiagonalisation + fp64 multisection/inverse iteration";
+}
+
+bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nfactors,
+                        const bkfac_layer_desc* layers, int nlayers, int device) {
+  if (!out || nfactors < 0 || nlayers < 0 || (nfactors > 0 && !factors) ||
+      (nlayers > 0 && !layers))
+    return BKFAC_ERR_INVALID_ARG;
+  *out = nullptr;
+  bkfac_ctx c = new (std::nothrow) bkfac_ctx_s();
+  if (!c) return BKFAC_ERR_INVALID_ARG;
+  c->device = device;
+  Arena a;
+  c->status_off = a.take(sizeof(int) * (size_t)(nfactors + nlayers + 1));
+  for (int i = 0; i < nfactors; ++i) {
+    FactorPlan fp;
+    fp.d = factors[i];
+    const int n = fp.d.n, r = fp.d.r, cm = fp.d.c_max;
+    if (n <= 0 || r <= 0 || r > n || cm <= 0) { delete c; return BKFAC_ERR_DIM; }
+    fp.dense = (r + cm >= n);
+    if (fp.dense) {
+      fp.m = n;
+      fp.T = a.take(sizeof(float) * (size_t)n * r);
+      plan_eig(a, fp.eig, n, r);
+    } else {
+      const int m = r + cm;
+      fp.m = m;
+      fp.W = a.take(sizeof(float) * (size_t)m * cm);
+      fp.P2 = a.take(sizeof(float) * (size_t)r * cm);
+      fp.R = a.take(sizeof(float) * (size_t)n * cm);
+      fp.Qb = a.take(sizeof(float) * (size_t)n * cm);
+      const size_t cc = sizeof(float) * (size_t)cm * cm;
+      fp.G = a.take(cc); fp.L1 = a.take(cc); fp.L1i = a.take(cc); fp.L2 = a.take(cc); fp.L2i = a.take(cc);
+      fp.cscr = a.take(cm > CHOL_SMEM_MAX ? sizeof(float) * (size_t)cm * (cm + 1) / 2 : 4);
+      fp.ws_elems = (long)kSplitMax * std::max(r, cm) * (long)cm;
+      fp.ws = a.take(sizeof(float) * fp.ws_elems);
+      plan_eig(a, fp.eig, m, r);
+    }
+    if (fp.d.flags & BKFAC_FACTOR_DENSE_EA) {
+      fp.rsvd = true;
+      const int l = std::min(n, r + kRsvdOversampleMax);
+      fp.lmax = l;
+      const size_t nl = sizeof(float) * (size_t)n * l;
+      fp.Yr = a.take(nl); fp.Qr = a.take(nl); fp.Q2r = a.take(nl); fp.Tr = a.take(nl);
+      const size_t ll = sizeof(float) * (size_t)l * l;
+      fp.Gr = a.take(ll); fp.L1r = a.take(ll); fp.L1ir = a.take(ll); fp.L2r = a.take(ll);
+      fp.L2ir = a.take(ll); fp.Br = a.take(ll);
+      fp.cscr_r = a.take(l > CHOL_SMEM_MAX ? sizeof(float) * (size_t)l * (l + 1) / 2 : 4);
+      fp.ws_r_elems = (long)kSplitMax * l * (long)l;
+      fp.ws_r = a.take(sizeof(float) * fp.ws_r_elems);
+      plan_eig(a, fp.eig_r, l, r);
+    }
+    c->f.push_back(fp);
+  }
+  for (int i = 0; i < nlayers; ++i) {
+    LayerPlan lp;
+    lp.d = layers[i];
+    const auto& d = lp.d;
+    if (d.d_G <= 0 || d.d_A <= 0 || d.r_G < 0 || d.r_A < 0 || d.r_G > d.d_G || d.r_A > d.d_A) {
+      delete c;
+      return BKFAC_ERR_DIM;
+    }
+    lp.Y = a.take(sizeof(float) * (size_t)d.d_G * std::max(d.r_A, 1));
+    lp.Xt = a.take(sizeof(float) * (size_t)d.d_A * std::max(d.r_G, 1));
+    lp.Z = a.take(sizeof(float) * (size_t)std::max(d.r_G, 1) * std::max(d.r_A, 1));
+    lp.sA = a.take(sizeof(float) * std::max(d.r_A, 1));
+    lp.sG = a.take(sizeof(float) * std::max(d.r_G, 1));
+    lp.lam = a.take(sizeof(float) * 4);
+    lp.ws_elems = (long)kSplitMax * std::max((long)d.d_G * d.r_A, (long)d.d_A * d.r_G);
+    lp.ws = a.take(sizeof(float) * std::max<long>(lp.ws_elems, 1));
+    c->l.push_back(lp);
+  }
+  c->ws_bytes = a.cur;
+  cudaError_t e = cudaMallocHost(&c->host_status, sizeof(int) * (size_t)(nfactors + nlayers + 1));
+  if (e != cudaSuccess) { delete c; return BKFAC_ERR_CUDA; }
+  // opt-in shared memory sizes
+  int dev_prev = 0;
+  cudaGetDevice(&dev_prev);
+  cudaSetDevice(device);
+  cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncSetAttribute(backtr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  tc_init_attributes();
+  cudaSetDevice(dev_prev);
+  const char* env = getenv("BKFAC_GEMM");
+  c->use_tc = !(env && strcmp(env, "simt") == 0);
+  *out = c;
+  return BKFAC_OK;
+}
+
+size_t bkfac_workspace_bytes(bkfac_ctx c) { return c ? c->ws_bytes : 0; }
+
+bkfac_status bkfac_set_workspace(bkfac_ctx c, void* p, size_t bytes) {
+  if (!c || !p) return BKFAC_ERR_INVALID_ARG;
+  if (bytes < c->ws_bytes || (reinterpret_cast<uintptr_t>(p) & 255)) return BKFAC_ERR_WORKSPACE;
+  c->ws = static_cast<char*>(p);
+  c->ws_cap = bytes;
+  if (!cuda_ok(cudaMemset(c->ws + c->status_off, 0, sizeof(int) * (c->f.size() + c->l.size() + 1))))
+    return BKFAC_ERR_CUDA;
+  return BKFAC_OK;
+}
+
+bkfac_status bkfac_destroy(bkfac_ctx c) {
+  if (!c) return BKFAC_ERR_INVALID_ARG;
+  if (c->host_status) cudaFreeHost(c->host_status);
+  delete c;
+  return BKFAC_OK;
+}
+
+uint64_t bkfac_launch_count(bkfac_ctx c) { return c ? c->launches : 0; }
+
+// ------------------------------------------------------------------------- Brand
+bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int count,
+                                void* stream) {
+  if (!ctx || (count > 0 && !args) || count < 0) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    if (a.factor < 0 || a.factor >= (int)ctx->f.size()) return BKFAC_ERR_INVALID_ARG;
+    const auto& fp = ctx->f[a.factor];
+    if (!a.U_in || !a.D_in || !a.M || !a.U_out || !a.D_out) return BKFAC_ERR_INVALID_ARG;
+    if (!(a.alpha >= 0.f) || !(a.beta > 0.f) || !std::isfinite(a.alpha) || !std::isfinite(a.beta))
+      return BKFAC_ERR_INVALID_ARG;
+    if (a.c <= 0 || a.c > fp.d.c_max) return BKFAC_ERR_DIM;
+    if (a.U_out == a.U_in || a.D_out == a.D_in) return BKFAC_ERR_ALIAS;
+    for (int j = 0; j < i; ++j)
+      if (args[j].factor == a.factor) return BKFAC_ERR_INVALID_ARG;  // one update per factor per batch
+  }
+  if (count == 0) return BKFAC_OK;
+  int dev_prev = 0;
+  cudaGetDevice(&dev_prev);
+  if (dev_prev != ctx->device) cudaSetDevice(ctx->device);
+
+  bkfac_status rs = BKFAC_OK;
+  GemmStage gs;
+  std::vector<EwProb> ew;
+  std::vector<CholProb> ch;
+  std::vector<EigProb> eg;
+  std::vector<int> brand, dense;
+  for (int i = 0; i < count; ++i) (ctx->f[args[i].factor].dense ? dense : brand).push_back(i);
+
+  auto run = [&](void) -> bkfac_status { return run_gemms(ctx, gs, st); };
+#define STAGE(x) do { if ((rs = (x)) != BKFAC_OK) goto done; } while (0)
+
+  // ---------------- dense path (r + c >= n): K = alpha U diag(D) U^T + beta M M^T
+  if (!dense.empty()) {
+    for (int i : dense) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      if (a.alpha != 0.f) {
+        EwProb e{};
+        e.Y = at<float>(ctx, fp.T); e.ldy = fp.d.n; e.X = a.U_in; e.ldx = fp.d.n;
+        e.vec = a.D_in; e.rows = fp.d.n; e.cols = fp.d.r; e.op = EW_SCALE_COLS;
+        ew.push_back(e);
+      }
+    }
+    STAGE(run_ew(ctx, ew, st));
+    for (int i : dense) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      if (a.alpha != 0.f) {
+        const int n = fp.d.n;
+        gs.add(false, true, gp(at<float>(ctx, fp.T), n, a.U_in, n, at<float>(ctx, fp.eig.K), n, n, n,
+                               fp.d.r, a.alpha), 0);
+      }
+    }
+    STAGE(run());
+    for (int i : dense) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      const int n = fp.d.n;
+      float* K = at<float>(ctx, fp.eig.K);
+      gs.add(false, true, gp(a.M, n, a.M, n, K, n, n, n, a.c, a.beta, K, n, a.alpha != 0.f ? 1.f : 0.f), 0);
+    }
+    STAGE(run());
+    for (int i : dense) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      eg.push_back(eig_prob(ctx, fp.eig, fp.d.n, fp.d.r, a.U_out, fp.d.n, a.D_out,
+                            status_ptr(ctx, a.factor)));
+    }
+  }
+
+  // ---------------- Brand path
+  if (!brand.empty()) {
+    // A: P = U^T M  -> W rows [0, r)
+    for (int i : brand) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      const int n = fp.d.n, r = fp.d.r;
+      GemmProb p = gp(a.U_in, n, a.M, n, at<float>(ctx, fp.W), fp.m, r, a.c, n, 1.f);
+      gemm_ws(p, at<float>(ctx, fp.ws));
+      gs.add(true, false, p, fp.ws_elems);
+    }
+    STAGE(run());
+    // B: R = M - U P
+    for (int i : brand) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      const int n = fp.d.n, r = fp.d.r;
+      gs.add(false, false, gp(a.U_in, n, at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), n, n, a.c,
+                              r, -1.f, a.M, n, 1.f), 0);
+    }
+    STAGE(run());
+    // CGS2 re-projection: P2 = U^T R; R -= U P2; P += P2
+    bool any_reorth = false;
+    for (int i : brand) {
+      const auto& a = args[i];
+      if (a.flags & BKFAC_BRAND_NO_REORTH) continue;
+      any_reorth = true;
+      const auto& fp = ctx->f[a.factor];
+      const int n = fp.d.n, r = fp.d.r;
+      GemmProb p = gp(a.U_in, n, at<float>(ctx, fp.R), n, at<float>(ctx, fp.P2), r, r, a.c, n, 1.f);
+      gemm_ws(p, at<float>(ctx, fp.ws));
+      gs.add(true, false, p, fp.ws_elems);
+    }
+    if (any_reorth) {
+      STAGE(run());
+      for (int i : brand) {
+        const auto& a = args[i];
+        if (a.flags & BKFAC_BRAND_NO_REORTH) continue;
+        const auto& fp = ctx->f[a.factor];
+        const int n = fp.d.n, r = fp.d.r;
+        float* R = at<float>(ctx, fp.R);
+        gs.add(false, false, gp(a.U_in, n, at<float>(ctx, fp.P2), r, R, n, n, a.c, r, -1.f, R, n, 1.f), 0);
+        EwProb e{};
+        e.Y = at<float>(ctx, fp.W); e.ldy = fp.m; e.X = at<float>(ctx, fp.P2); e.ldx = r;
+        e.rows = r; e.cols = a.c; e.a = 1.f; e.op = EW_ADD;
+        ew.push_back(e);
+      }
+      STAGE(run());
+      STAGE(run_ew(ctx, ew, st));
+    }
+    // CholeskyQR2 of R:  G = R^T R; L1; Q1 = R L1^{-T}; G = Q1^T Q1; L2; Q = Q1 L2^{-T}
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i : brand) {
+        const auto& a = args[i];
+        const auto& fp = ctx->f[a.factor];
+        const int n = fp.d.n, c = a.c;
+        const float* X = at<float>(ctx, pass == 0 ? fp.R : fp.Qb);
+        GemmProb p = gp(X, n, X, n, at<float>(ctx, fp.G), c, c, c, n, 1.f);
+        gemm_ws(p, at<float>(ctx, fp.ws));
+        gs.add(true, false, p, fp.ws_elems);
+      }
+      STAGE(run());
+      for (int i : brand) {
+        const auto& a = args[i];
+        const auto& fp = ctx->f[a.factor];
+        ch.push_back(chol_prob(ctx, at<float>(ctx, fp.G), a.c, pass == 0 ? fp.L1 : fp.L2,
+                               pass == 0 ? fp.L1i : fp.L2i, fp.cscr, status_ptr(ctx, a.factor)));
+      }
+      STAGE(run_chol(ctx, ch, st));
+      for (int i : brand) {
+        const auto& a = args[i];
+        const auto& fp = ctx->f[a.factor];
+        const int n = fp.d.n, c = a.c;
+        const float* X = at<float>(ctx, pass == 0 ? fp.R : fp.Qb);
+        float* Y = at<float>(ctx, pass == 0 ? fp.Qb : fp.R);
+        const float* Li = at<float>(ctx, pass == 0 ? fp.L1i : fp.L2i);
+        gs.add(false, true, gp(X, n, Li, c, Y, n, n, c, c, 1.f), 0);
+      }
+      STAGE(run());
+    }
+    // R_Q = L2^T L1^T -> W rows [r, r+c); then core K = beta W W^T (+ alpha D on the diagonal)
+    for (int i : brand) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      const int c = a.c, r = fp.d.r;
+      gs.add(true, true, gp(at<float>(ctx, fp.L2), c, at<float>(ctx, fp.L1), c,
+                            at<float>(ctx, fp.W) + r, fp.m, c, c, c, 1.f), 0);
+    }
+    STAGE(run());
+    for (int i : brand) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      const int mm = fp.d.r + a.c;
+      const float* W = at<float>(ctx, fp.W);
+      gs.add(false, true, gp(W, fp.m, W, fp.m, at<float>(ctx, fp.eig.K), mm, mm, mm, a.c, a.beta), 0);
+      if (a.alpha != 0.f) {
+        EwProb e{};
+        e.Y = at<float>(ctx, fp.eig.K); e.ldy = mm; e.X = nullptr; e.vec = a.D_in;
+        e.rows = fp.d.r; e.cols = 1; e.a = a.alpha; e.op = EW_ADD_DIAG;
+        ew.push_back(e);
+      }
+    }
+    STAGE(run());
+    STAGE(run_ew(ctx, ew, st));
+    for (int i : brand) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      const int mm = fp.d.r + a.c;
+      eg.push_back(eig_prob(ctx, fp.eig, mm, fp.d.r, at<float>(ctx, fp.eig.V), mm, a.D_out,
+                            status_ptr(ctx, a.factor)));
+    }
+  }
+  STAGE(run_eig(ctx, eg, st));
+  // rotation: U_out = [U Q] V
+  for (int i : brand) {
+    const auto& a = args[i];
+    const auto& fp = ctx->f[a.factor];
+    const int n = fp.d.n, r = fp.d.r, mm = r + a.c;
+    const float* V = at<float>(ctx, fp.eig.V);
+    GemmProb p = gp(a.U_in, n, V, mm, a.U_out, n, n, r, mm, 1.f);
+    p.A2 = at<float>(ctx, fp.R); p.lda2 = n;
+    p.B2 = V + r; p.ldb2 = mm;
+    p.k1 = r;
+    gs.add(false, false, p, 0);
+  }
+  STAGE(run());
+done:
+#undef STAGE
+  if (dev_prev != ctx->device) cudaSetDevice(dev_prev);
+  return rs;
+}
+
+// ------------------------------------------------------------------------- dense EA
+bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K, const float* M, int c,
+                                 float rho, void* stream) {
+  if (!ctx || !K || !M) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  if (factor < 0 || factor >= (int)ctx->f.size()) return BKFAC_ERR_INVALID_ARG;
+  const auto& fp = ctx->f[factor];
+  if (!(fp.d.flags & BKFAC_FACTOR_DENSE_EA)) return BKFAC_ERR_INVALID_ARG;
+  if (c <= 0 || c > fp.d.c_max) return BKFAC_ERR_DIM;
+  if (!(rho >= 0.f && rho < 1.f)) return BKFAC_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int n = fp.d.n;
+  GemmStage gs;
+  gs.add(false, true, gp(M, n, M, n, K, n, n, n, c, 1.f - rho, K, n, rho), 0);
+  return run_gemms(ctx, gs, st);
+}
+
+// ------------------------------------------------------------------------- RSVD
+bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K, int oversample,
+                                  int power_iters, uint64_t seed, uint64_t counter, float* U_out,
+                                  float* D_out, void* stream) {
+  if (!ctx || !K || !U_out || !D_out) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  if (factor < 0 || factor >= (int)ctx->f.size()) return BKFAC_ERR_INVALID_ARG;
+  const auto& fp = ctx->f[factor];
+  if (!fp.rsvd) return BKFAC_ERR_INVALID_ARG;
+  if (oversample < 0 || power_iters < 0 || power_iters > 64) return BKFAC_ERR_INVALID_ARG;
+  const int n = fp.d.n, r = fp.d.r, l = r + oversample;
+  if (l > n) return BKFAC_ERR_RANK;
+  if (l > fp.lmax) return BKFAC_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* status = status_ptr(ctx, factor);
+  float* Y = at<float>(ctx, fp.Yr);
+  float* Q = at<float>(ctx, fp.Qr);
+  float* Q2 = at<float>(ctx, fp.Q2r);
+  float* T = at<float>(ctx, fp.Tr);
+  float* ws = at<float>(ctx, fp.ws_r);
+  GemmStage gs;
+  std::vector<CholProb> ch;
+  std::vector<EigProb> eg;
+  bkfac_status rs;
+  // Omega -> Q ; Y = K Omega
+  philox_sketch_kernel<<<1024, 256, 0, st>>>(Q, (long)n * l, seed, counter);
+  LAUNCH_CHECK(ctx);
+  gs.add(false, false, gp(K, n, Q, n, Y, n, n, l, n, 1.f), 0);
+  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  auto orth = [&](const float* X, float* Qout) -> bkfac_status {
+    // CholeskyQR2: Q2 = X L1^{-T}, Qout = Q2 L2^{-T}
+    for (int pass = 0; pass < 2; ++pass) {
+      const float* In = pass == 0 ? X : Q2;
+      float* Out = pass == 0 ? Q2 : Qout;
+      GemmProb p = gp(In, n, In, n, at<float>(ctx, fp.Gr), l, l, l, n, 1.f);
+      gemm_ws(p, ws);
+      gs.add(true, false, p, fp.ws_r_elems);
+      bkfac_status s2 = run_gemms(ctx, gs, st);
+      if (s2 != BKFAC_OK) return s2;
+      ch.push_back(chol_prob(ctx, at<float>(ctx, fp.Gr), l, pass == 0 ? fp.L1r : fp.L2r,
+                             pass == 0 ? fp.L1ir : fp.L2ir, fp.cscr_r, status));
+      if ((s2 = run_chol(ctx, ch, st)) != BKFAC_OK) return s2;
+      gs.add(false, true, gp(In, n, at<float>(ctx, pass == 0 ? fp.L1ir : fp.L2ir), l, Out, n, n, l, l, 1.f), 0);
+      if ((s2 = run_gemms(ctx, gs, st)) != BKFAC_OK) return s2;
+    }
+    return BKFAC_OK;
+  };
+  for (int q = 0; q < power_iters; ++q) {
+    if ((rs = orth(Y, Q)) != BKFAC_OK) return rs;
+    gs.add(false, false, gp(K, n, Q, n, Y, n, n, l, n, 1.f), 0);
+    if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  }
+  if ((rs = orth(Y, Q)) != BKFAC_OK) return rs;
+  // B = Q^T K Q
+  gs.add(false, false, gp(K, n, Q, n, T, n, n, l, n, 1.f), 0);
+  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  {
+    GemmProb p = gp(Q, n, T, n, at<float>(ctx, fp.eig_r.K), l, l, l, n, 1.f);
+    gemm_ws(p, ws);
+    gs.add(true, false, p, fp.ws_r_elems);
+    if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  }
+  eg.push_back(eig_prob(ctx, fp.eig_r, l, r, at<float>(ctx, fp.eig_r.V), l, D_out, status));
+  if ((rs = run_eig(ctx, eg, st)) != BKFAC_OK) return rs;
+  gs.add(false, false, gp(Q, n, at<float>(ctx, fp.eig_r.V), l, U_out, n, n, r, l, 1.f), 0);
+  return run_gemms(ctx, gs, st);
+}
+
+bkfac_status bkfac_gaussian_sketch(float* Om, int n, int l, uint64_t seed, uint64_t counter,
+                                   void* stream) {
+  if (!Om || n <= 0 || l <= 0) return BKFAC_ERR_INVALID_ARG;
+  philox_sketch_kernel<<<1024, 256, 0, static_cast<cudaStream_t>(stream)>>>(Om, (long)n * l, seed,
+                                                                            counter);
+  if (!cuda_ok(cudaGetLastError())) return BKFAC_ERR_CUDA;
+  return BKFAC_OK;
+}
+
+// ------------------------------------------------------------------------- precondition
+bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, int count,
+                                void* stream) {
+  if (!ctx || (count > 0 && !args) || count < 0) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    if (a.layer < 0 || a.layer >= (int)ctx->l.size()) return BKFAC_ERR_INVALID_ARG;
+    const auto& d = ctx->l[a.layer].d;
+    if (!a.J || !a.S) return BKFAC_ERR_INVALID_ARG;
+    if ((d.r_A > 0 && (!a.U_A || !a.D_A)) || (d.r_G > 0 && (!a.U_G || !a.D_G)))
+      return BKFAC_ERR_INVALID_ARG;
+    if (!(a.lambda_A > 0.f) || !(a.lambda_G > 0.f)) return BKFAC_ERR_INVALID_ARG;
+    if (a.S == a.J) return BKFAC_ERR_ALIAS;
+    for (int j = 0; j < i; ++j)
+      if (args[j].layer == a.layer) return BKFAC_ERR_INVALID_ARG;
+  }
+  if (count == 0) return BKFAC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static PrecScalBatch psb;
+  static PrecScaleBatch pcb;
+  bkfac_status rs;
+  GemmStage gs;
+  // S1: scalars
+  for (int i0 = 0; i0 < count; i0 += PS_MAXP / 2) {
+    const int n = std::min(count - i0, PS_MAXP / 2);
+    psb.nprob = 0;
+    for (int i = i0; i < i0 + n; ++i) {
+      const auto& a = args[i];
+      const auto& lp = ctx->l[a.layer];
+      float* lam = at<float>(ctx, lp.lam);
+      psb.p[psb.nprob++] = PrecScalProb{a.D_A, lp.d.r_A, a.lambda_A, a.flags, at<float>(ctx, lp.sA), lam + 0};
+      psb.p[psb.nprob++] = PrecScalProb{a.D_G, lp.d.r_G, a.lambda_G, a.flags, at<float>(ctx, lp.sG), lam + 1};
+    }
+    prec_scalars_kernel<<<psb.nprob, 256, 0, st>>>(psb);
+    LAUNCH_CHECK(ctx);
+  }
+  for (int i0 = 0; i0 < count; ++i0) {
+    const auto& lp = ctx->l[args[i0].layer];
+    float* lam = at<float>(ctx, lp.lam);
+    prec_coef_kernel<<<1, 1, 0, st>>>(lam + 1, lam + 0, lam + 2);
+    LAUNCH_CHECK(ctx);
+  }
+  // S2: Y = J U_A (d_G x r_A), Xt = J^T U_G (d_A x r_G)
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    const auto& lp = ctx->l[a.layer];
+    const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G;
+    if (rA > 0) {
+      GemmProb p = gp(a.J, dA, a.U_A, dA, at<float>(ctx, lp.Y), dG, dG, rA, dA, 1.f);
+      gemm_ws(p, at<float>(ctx, lp.ws));
+      gs.add(true, false, p, lp.ws_elems);
+    }
+    if (rG > 0) gs.add(false, false, gp(a.J, dA, a.U_G, dG, at<float>(ctx, lp.Xt), dA, dA, rG, dG, 1.f), 0);
+  }
+  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  // S3: Z = U_G^T Y (r_G x r_A)
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    const auto& lp = ctx->l[a.layer];
+    const int dG = lp.d.d_G, rA = lp.d.r_A, rG = lp.d.r_G;
+    if (rA > 0 && rG > 0)
+      gs.add(true, false, gp(a.U_G, dG, at<float>(ctx, lp.Y), dG, at<float>(ctx, lp.Z), rG, rG, rA, dG, 1.f), 0);
+  }
+  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  // S4: Y' = Y diag(sA)/lamG ; Z' = diag(sG) Z diag(sA) ; Xt' = Xt diag(sG)/lamA
+  for (int i0 = 0; i0 < count; i0 += PS_MAXP / 3) {
+    const int n = std::min(count - i0, PS_MAXP / 3);
+    pcb.nprob = 0;
+    for (int i = i0; i < i0 + n; ++i) {
+      const auto& lp = ctx->l[args[i].layer];
+      const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G;
+      float* lam = at<float>(ctx, lp.lam);
+      if (rA > 0)
+        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.Y), dG, dG, rA, at<float>(ctx, lp.sA), nullptr, lam + 1, 0};
+      if (rA > 0 && rG > 0)
+        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.Z), rG, rG, rA, at<float>(ctx, lp.sA), at<float>(ctx, lp.sG), nullptr, 1};
+      if (rG > 0)
+        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.Xt), dA, dA, rG, at<float>(ctx, lp.sG), nullptr, lam + 0, 0};
+    }
+    if (pcb.nprob) {
+      prec_scale_kernel<<<dim3(64, pcb.nprob), 256, 0, st>>>(pcb);
+      LAUNCH_CHECK(ctx);
+    }
+  }
+  // S5: Y' += U_G Z'
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    const auto& lp = ctx->l[a.layer];
+    const int dG = lp.d.d_G, rA = lp.d.r_A, rG = lp.d.r_G;
+    if (rA > 0 && rG > 0) {
+      float* Y = at<float>(ctx, lp.Y);
+      gs.add(false, false, gp(a.U_G, dG, at<float>(ctx, lp.Z), rG, Y, dG, dG, rA, rG, 1.f, Y, dG, 1.f), 0);
+    }
+  }
+  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  // S7: S^T (d_A x d_G) = [U_A | Xt'] [Y'^T ; U_G^T] + coef J^T
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    const auto& lp = ctx->l[a.layer];
+    const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G;
+    float* lam = at<float>(ctx, lp.lam);
+    GemmProb p = gp(rA > 0 ? a.U_A : at<float>(ctx, lp.Xt), dA,
+                    rA > 0 ? at<float>(ctx, lp.Y) : a.U_G, dG, a.S, dA, dA, dG, rA + rG, 1.f,
+                    a.J, dA, 1.f);
+    p.A2 = at<float>(ctx, lp.Xt); p.lda2 = dA;
+    p.B2 = a.U_G ? a.U_G : at<float>(ctx, lp.Y); p.ldb2 = dG;
+    p.k1 = rA;
+    p.beta_dev = lam + 2;
+    gs.add(false, true, p, 0);
+  }
+  return run_gemms(ctx, gs, st);
+}
+
+// ------------------------------------------------------------------------- check
+bkfac_status bkfac_check(bkfac_ctx ctx, void* stream, int* first_bad, int* info_bits) {
+  if (!ctx) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t n = ctx->f.size() + ctx->l.size() + 1;
+  if (!cuda_ok(cudaMemcpyAsync(ctx->host_status, ctx->ws + ctx->status_off, sizeof(int) * n,
+                               cudaMemcpyDeviceToHost, st)))
+    return BKFAC_ERR_CUDA;
+  if (!cuda_ok(cudaStreamSynchronize(st))) return BKFAC_ERR_CUDA;
+  int bad = -1, info = 0;
+  for (size_t i = 0; i < n; ++i) {
+    info |= ctx->host_status[i];
+    if (bad < 0 && (ctx->host_status[i] & ST_ERROR_MASK)) bad = (int)i;
+  }
+  if (first_bad) *first_bad = bad;
+  if (info_bits) *info_bits = info;
+  return bad >= 0 ? BKFAC_ERR_NUMERIC : BKFAC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,405 @@
+// Batched symmetric eigensolver for the Brand core K (m x m, m = r + c) and for the
+// dense-path / RSVD projected matrices: "EVD(M_S)" of Alg 3, of which
+// only the top-r eigenpairs are kept (truncation, Alg 4 :540-543).
+//
+//   1. sytrd_kernel     Householder tridiagonalisation T = H^T K H (one CTA per factor,
+//                       lower triangle, rank-2 update fused with the next symv).
+//   2. bisect_kernel    top-r eigenvalues of T by Sturm-count multisection in fp64
+//                       (one warp per eigenvalue, 32 probes per round).
+//   3. invit_kernel     eigenvectors of T by inverse iteration in fp64 (one thread per
+//                       eigenvector, tridiagonal LU with partial pivoting).
+//   4. cluster_kernel   modified Gram-Schmidt inside clusters of (near-)equal eigenvalues.
+//   5. backtr_kernel    V = H Y (apply the m-2 reflectors to the r eigenvectors).
+// See DESIGN.md "Eigensolver" for why stage 2/3 replace implicit QL on sm_100a.
+#pragma once
+#include "common.cuh"
+
+namespace bkfac {
+
+struct EigProb {
+  float* K; int ldk;       // m x m symmetric (lower used); overwritten with reflectors
+  int m, r;                // order, number of wanted (largest) eigenpairs
+  float* d; float* e; float* tau;   // m, m, m (fp32 tridiagonal + reflector scalars)
+  double* lam;             // r eigenvalues, descending
+  double* Y;               // m x r eigenvectors of T, layout Y[i*r + j]
+  double* scr;             // 4*m*r doubles scratch (LU factors)
+  unsigned char* piv;      // m*r pivot flags
+  float* V; int ldv;       // output eigenvectors of K, m x r col-major
+  float* Dout;             // output eigenvalues (r), clamped >= 0
+  int* status;
+};
+constexpr int EIG_MAXP = 100;
+struct EigBatch { int nprob; EigProb p[EIG_MAXP]; };
+
+// ------------------------------------------------------------------ 1. sytrd
+__global__ void __launch_bounds__(1024) sytrd_kernel(const __grid_constant__ EigBatch b) {
+  const EigProb& p = b.p[blockIdx.x];
+  const int m = p.m;
+  const int ld = p.ldk;
+  float* K = p.K;
+  extern __shared__ __align__(16) float ssm[];
+  float* v = ssm;
+  float* vp = v + m;
+  float* wp = vp + m;
+  float* y = wp + m;
+  float* red = y + m;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+
+  // non-finite guard on the input (lower triangle)
+  {
+    int bad = 0;
+    for (int j = warp; j < m; j += nw)
+      for (int i = j + lane; i < m; i += 32) bad |= !isfinite(K[i + (long)j * ld]);
+    bad = __syncthreads_or(bad);
+    if (bad) {
+      if (tid == 0 && p.status) atomicOr(p.status, ST_NONFINITE);
+      for (int i = tid; i < m; i += nt) { p.d[i] = 0.f; p.e[i] = 0.f; p.tau[i] = 0.f; }
+      return;
+    }
+  }
+  if (m == 1) {
+    if (tid == 0) { p.d[0] = K[0]; p.e[0] = 0.f; p.tau[0] = 0.f; }
+    return;
+  }
+  bool have_prev = false;
+  for (int k = 0; k < m - 2; ++k) {
+    if (have_prev)
+      for (int i = k + tid; i < m; i += nt)
+        K[i + (long)k * ld] -= vp[i] * wp[k] + wp[i] * vp[k];
+    __syncthreads();
+    const float alpha = K[k + 1 + (long)k * ld];
+    float ss = 0.f;
+    for (int i = k + 2 + tid; i < m; i += nt) {
+      const float t = K[i + (long)k * ld];
+      ss += t * t;
+    }
+    ss = block_sum(ss, red);
+    float tau, beta, scale;
+    if (ss == 0.f) {
+      tau = 0.f; beta = alpha; scale = 0.f;
+    } else {
+      const float nrm = sqrtf(alpha * alpha + ss);
+      beta = alpha >= 0.f ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scale = 1.f / (alpha - beta);
+    }
+    for (int i = k + 1 + tid; i < m; i += nt) {
+      float vi = 1.f;
+      if (i >= k + 2) {
+        vi = K[i + (long)k * ld] * scale;
+        K[i + (long)k * ld] = vi;
+      }
+      v[i] = vi;
+      y[i] = 0.f;
+    }
+    if (tid == 0) {
+      p.d[k] = K[k + (long)k * ld];
+      p.e[k] = beta;
+      p.tau[k] = tau;
+    }
+    __syncthreads();
+    // fused: apply the previous rank-2 update to columns j >= k+1 (rows i >= j)
+    // and accumulate y = K22 v from the lower triangle.
+    for (int j = k + 1 + warp; j < m; j += nw) {
+      const float vj = v[j];
+      const float wpj = have_prev ? wp[j] : 0.f, vpj = have_prev ? vp[j] : 0.f;
+      float acc = 0.f;
+      for (int i = j + lane; i < m; i += 32) {
+        float a = K[i + (long)j * ld];
+        if (have_prev) {
+          a -= vp[i] * wpj + wp[i] * vpj;
+          K[i + (long)j * ld] = a;
+        }
+        acc = fmaf(a, v[i], acc);
+        if (i > j) atomicAdd(&y[i], a * vj);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) atomicAdd(&y[j], acc);
+    }
+    __syncthreads();
+    float pv = 0.f;
+    for (int i = k + 1 + tid; i < m; i += nt) pv += y[i] * v[i];
+    pv = block_sum(pv, red);
+    const float gamma = 0.5f * tau * tau * pv;
+    for (int i = k + 1 + tid; i < m; i += nt) {
+      wp[i] = tau * y[i] - gamma * v[i];
+      vp[i] = v[i];
+    }
+    have_prev = true;
+    __syncthreads();
+  }
+  if (have_prev) {
+    if (tid < 3) {
+      const int j = m - 2 + (tid == 2);
+      const int i = m - 2 + (tid >= 1);
+      K[i + (long)j * ld] -= vp[i] * wp[j] + wp[i] * vp[j];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    p.d[m - 2] = K[(m - 2) + (long)(m - 2) * ld];
+    p.d[m - 1] = K[(m - 1) + (long)(m - 1) * ld];
+    p.e[m - 2] = K[(m - 1) + (long)(m - 2) * ld];
+    p.e[m - 1] = 0.f;
+    p.tau[m - 2] = 0.f;
+    p.tau[m - 1] = 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ 2. bisection
+// Number of eigenvalues of T strictly below x (Sturm sequence of the LDL^T pivots).
+BKFAC_DEV int sturm_count(const double* dd, const double* e2, int m, double x, double pivmin) {
+  int cnt = 0;
+  double q = dd[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += (q < 0.0);
+  for (int i = 1; i < m; ++i) {
+    q = (dd[i] - x) - e2[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += (q < 0.0);
+  }
+  return cnt;
+}
+
+constexpr int BIS_WARPS = 8;
+
+// grid: (nprob, ceil(rmax / BIS_WARPS)); smem: 2*m doubles
+__global__ void __launch_bounds__(BIS_WARPS * 32) bisect_kernel(const __grid_constant__ EigBatch b) {
+  const EigProb& p = b.p[blockIdx.x];
+  const int m = p.m;
+  extern __shared__ __align__(16) double dsm[];
+  double* dd = dsm;
+  double* e2 = dd + m;
+  __shared__ double s_lo, s_hi, s_pivmin;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < m; i += blockDim.x) {
+    dd[i] = (double)p.d[i];
+    const double ee = (i < m - 1) ? (double)p.e[i] : 0.0;
+    e2[i] = ee * ee;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double lo = 1e300, hi = -1e300, emax = 0.0;
+    for (int i = 0; i < m; ++i) {
+      const double r = (i > 0 ? fabs((double)p.e[i - 1]) : 0.0) + (i < m - 1 ? fabs((double)p.e[i]) : 0.0);
+      lo = fmin(lo, dd[i] - r);
+      hi = fmax(hi, dd[i] + r);
+      emax = fmax(emax, e2[i]);
+    }
+    const double span = fmax(fabs(lo), fabs(hi));
+    const double pad = 2.2e-16 * span * 4.0 + 1e-300;
+    s_lo = lo - pad;
+    s_hi = hi + pad;
+    s_pivmin = 2.3e-308 * fmax(1.0, emax);
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int j = blockIdx.y * BIS_WARPS + warp;   // descending index
+  if (j >= p.r) return;
+  const int kasc = m - 1 - j;                     // ascending index
+  double lo = s_lo, hi = s_hi;
+  const double pivmin = s_pivmin;
+  // invariant: count(lo) <= kasc < count(hi)
+  for (int round = 0; round < 14; ++round) {
+    const double w = hi - lo;
+    if (w <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) * 2.0 + pivmin) break;
+    const double x = lo + w * (double)(lane + 1) / 33.0;
+    const int cnt = sturm_count(dd, e2, m, x, pivmin);
+    const unsigned above = __ballot_sync(0xffffffffu, cnt >= kasc + 1);
+    const int first = above ? __ffs(above) - 1 : 32;
+    const double nlo = (first == 0) ? lo : lo + w * (double)first / 33.0;
+    const double nhi = (first == 32) ? hi : lo + w * (double)(first + 1) / 33.0;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) p.lam[j] = 0.5 * (lo + hi);
+}
+
+// ------------------------------------------------------------------ 3. inverse iteration
+BKFAC_DEV double hash_unit(unsigned a, unsigned b) {
+  unsigned h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u;
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+  return ((double)h / 4294967296.0) - 0.5;
+}
+
+// grid: (nprob, ceil(rmax/128)), block 128: thread = eigenvector j.
+__global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigBatch b) {
+  const EigProb& p = b.p[blockIdx.x];
+  const int m = p.m, r = p.r;
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;
+  if (j >= r) return;
+  // scratch arrays, interleaved by eigenvector: a[i*r + j]
+  double* dU = p.scr;                  // U diagonal
+  double* du = dU + (long)m * r;       // U first superdiagonal
+  double* du2 = du + (long)m * r;      // U second superdiagonal
+  double* dl = du2 + (long)m * r;      // multipliers
+  unsigned char* pv = p.piv;
+  double* x = p.Y;
+#define AT(a, i) (a)[(long)(i) * r + j]
+  const double lam = p.lam[j];
+  // ||T||_1 estimate for the zero-pivot replacement
+  double tn = 0.0;
+  for (int i = 0; i < m; ++i) {
+    const double t = fabs((double)p.d[i]) + (i > 0 ? fabs((double)p.e[i - 1]) : 0.0) +
+                     (i < m - 1 ? fabs((double)p.e[i]) : 0.0);
+    tn = fmax(tn, t);
+  }
+  const double tiny = fmax(tn, 1e-300) * 2.2e-16;
+  if (m == 1) { AT(x, 0) = 1.0; return; }
+  // LU with partial pivoting of T - lam I (LAPACK dgttrf recurrence)
+  double dcur = (double)p.d[0] - lam;
+  double dufcur = (double)p.e[0];
+  for (int i = 0; i < m - 1; ++i) {
+    const double sub = (double)p.e[i];
+    const double dnext = (double)p.d[i + 1] - lam;
+    const double dunext = (i + 1 < m - 1) ? (double)p.e[i + 1] : 0.0;
+    if (fabs(dcur) >= fabs(sub)) {
+      double piv = dcur;
+      if (fabs(piv) < tiny) piv = (piv >= 0.0) ? tiny : -tiny;
+      const double f = sub / piv;
+      AT(dU, i) = piv; AT(du, i) = dufcur; AT(du2, i) = 0.0; AT(dl, i) = f; AT(pv, i) = 0;
+      dcur = dnext - f * dufcur;
+      dufcur = dunext;
+    } else {
+      const double f = dcur / sub;
+      AT(dU, i) = sub; AT(du, i) = dnext; AT(du2, i) = dunext; AT(dl, i) = f; AT(pv, i) = 1;
+      dcur = dufcur - f * dnext;
+      dufcur = -f * dunext;
+    }
+  }
+  if (fabs(dcur) < tiny) dcur = (dcur >= 0.0) ? tiny : -tiny;
+  AT(dU, m - 1) = dcur;
+  // start vector
+  for (int i = 0; i < m; ++i) AT(x, i) = hash_unit((unsigned)i, (unsigned)j) + 0.5;
+  for (int it = 0; it < 3; ++it) {
+    // forward: apply L^{-1} with row interchanges
+    for (int i = 0; i < m - 1; ++i) {
+      const double xi = AT(x, i), xn = AT(x, i + 1);
+      if (AT(pv, i) == 0) {
+        AT(x, i + 1) = xn - AT(dl, i) * xi;
+      } else {
+        AT(x, i) = xn;
+        AT(x, i + 1) = xi - AT(dl, i) * xn;
+      }
+    }
+    // back substitution with U (bandwidth 2)
+    double x2 = 0.0, x1 = AT(x, m - 1) / AT(dU, m - 1);
+    AT(x, m - 1) = x1;
+    double amax = fabs(x1);
+    for (int i = m - 2; i >= 0; --i) {
+      const double xi = (AT(x, i) - AT(du, i) * x1 - AT(du2, i) * x2) / AT(dU, i);
+      AT(x, i) = xi;
+      x2 = x1;
+      x1 = xi;
+      amax = fmax(amax, fabs(xi));
+    }
+    // normalise (scale by max first, then 2-norm)
+    const double s1 = (amax > 0.0 && isfinite(amax)) ? 1.0 / amax : 1.0;
+    double nrm = 0.0;
+    for (int i = 0; i < m; ++i) {
+      const double t = AT(x, i) * s1;
+      AT(x, i) = t;
+      nrm += t * t;
+    }
+    const double s2 = (nrm > 0.0) ? 1.0 / sqrt(nrm) : 0.0;
+    for (int i = 0; i < m; ++i) AT(x, i) *= s2;
+  }
+#undef AT
+}
+
+// ------------------------------------------------------------------ 4. clusters
+// One CTA (32 warps) per problem; clusters are runs of eigenvalues whose consecutive
+// gaps are <= 1e-9 * ||T|| (beyond that, fp64 inverse iteration is orthogonal to
+// ~1e-7).  Each warp orthonormalises one cluster by modified Gram-Schmidt.
+__global__ void __launch_bounds__(1024) cluster_kernel(const __grid_constant__ EigBatch b) {
+  const EigProb& p = b.p[blockIdx.x];
+  const int m = p.m, r = p.r;
+  __shared__ int s_start[1024], s_len[1024], s_n;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    double tn = 0.0;
+    for (int j = 0; j < r; ++j) tn = fmax(tn, fabs(p.lam[j]));
+    for (int i = 0; i < m; ++i) tn = fmax(tn, fabs((double)p.d[i]));
+    const double tol = 1e-9 * fmax(tn, 1e-300);
+    int n = 0, st = 0;
+    for (int j = 1; j <= r; ++j) {
+      if (j == r || p.lam[j - 1] - p.lam[j] > tol) {
+        if (j - st > 1 && n < 1024) { s_start[n] = st; s_len[n] = j - st; ++n; }
+        st = j;
+      }
+    }
+    s_n = n;
+    s_bad = 0;
+  }
+  __syncthreads();
+  double* Y = p.Y;
+  for (int cl = warp; cl < s_n; cl += 32) {
+    const int st = s_start[cl], len = s_len[cl];
+    for (int t = st; t < st + len; ++t) {
+      for (int s = st; s < t; ++s) {
+        double dot = 0.0;
+        for (int i = lane; i < m; i += 32) dot += Y[(long)i * r + s] * Y[(long)i * r + t];
+        dot = warp_sum_d(dot);
+        for (int i = lane; i < m; i += 32) Y[(long)i * r + t] -= dot * Y[(long)i * r + s];
+      }
+      double nrm = 0.0;
+      for (int i = lane; i < m; i += 32) nrm += Y[(long)i * r + t] * Y[(long)i * r + t];
+      nrm = warp_sum_d(nrm);
+      const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+      for (int i = lane; i < m; i += 32) Y[(long)i * r + t] *= inv;
+    }
+  }
+  __syncthreads();
+  // eigenvalues out (clamped at 0: the core is PSD) + finiteness check
+  for (int j = tid; j < r; j += blockDim.x) {
+    const double l = p.lam[j];
+    if (!isfinite(l)) s_bad = 1;
+    p.Dout[j] = (float)fmax(l, 0.0);
+  }
+  __syncthreads();
+  if (tid == 0 && s_bad && p.status) atomicOr(p.status, ST_EIG_FAIL);
+}
+
+// ------------------------------------------------------------------ 5. back-transform
+// V(:, cols) = H_0 H_1 ... H_{m-3} Y(:, cols); one CTA per (problem, 32 columns);
+// warp w owns column w, kept in shared memory (m floats).  smem: 33*m floats.
+__global__ void __launch_bounds__(1024) backtr_kernel(const __grid_constant__ EigBatch b) {
+  const EigProb& p = b.p[blockIdx.x];
+  const int m = p.m, r = p.r;
+  const int col0 = blockIdx.y * 32;
+  if (col0 >= r) return;
+  extern __shared__ __align__(16) float bsm[];
+  float* vs = bsm;              // m
+  float* Ys = vs + m;           // 32 * m, column w at Ys + w*m
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int j = col0 + warp;
+  const bool act = j < r;
+  float* yc = Ys + warp * m;
+  int bad = 0;
+  for (int i = lane; i < m; i += 32) {
+    const float v = act ? (float)p.Y[(long)i * r + j] : 0.f;
+    bad |= !isfinite(v);
+    yc[i] = v;
+  }
+  for (int k = m - 3; k >= 0; --k) {
+    const float tau = p.tau[k];
+    __syncthreads();
+    if (tau == 0.f) continue;
+    for (int i = k + 1 + tid; i < m; i += blockDim.x)
+      vs[i] = (i == k + 1) ? 1.f : p.K[i + (long)k * p.ldk];
+    __syncthreads();
+    float dot = 0.f;
+    for (int i = k + 1 + lane; i < m; i += 32) dot = fmaf(vs[i], yc[i], dot);
+    dot = warp_sum(dot) * tau;
+    for (int i = k + 1 + lane; i < m; i += 32) yc[i] -= dot * vs[i];
+  }
+  __syncthreads();
+  if (act)
+    for (int i = lane; i < m; i += 32) p.V[i + (long)j * p.ldv] = yc[i];
+  bad = __syncthreads_or(bad);
+  if (bad && tid == 0 && p.status) atomicOr(p.status, ST_EIG_FAIL);
+}
+
+}  // namespace bkfac

@@ -1,0 +1,148 @@
+// Small fused elementwise kernels of the hot path (epilogue-class work).
+#pragma once
+#include "common.cuh"
+
+namespace bkfac {
+
+// ---- generic batched "axpy-like" ops on col-major blocks -----------------------------
+struct EwProb {
+  float* Y; int ldy;          // destination block (rows x cols)
+  const float* X; int ldx;    // source block
+  const float* vec;           // optional per-column (or diagonal) vector
+  int rows, cols;
+  float a, b;
+  int op;
+};
+enum : int {
+  EW_ADD = 0,        // Y += a * X
+  EW_SCALE_COLS = 1, // Y(:,j) = X(:,j) * vec[j]
+  EW_ADD_DIAG = 2,   // Y(i,i) += a * vec[i], i < rows
+  EW_COPY = 3,       // Y = X
+  EW_SCALE_ROWSCOLS = 4, // Y(i,j) = X(i,j) * a * vec[i]... (unused)
+};
+constexpr int EW_MAXP = 100;
+struct EwBatch { int nprob; EwProb p[EW_MAXP]; };
+
+__global__ void ew_kernel(const __grid_constant__ EwBatch b) {
+  const EwProb& p = b.p[blockIdx.y];
+  if (p.op == EW_ADD_DIAG) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.rows; i += gridDim.x * blockDim.x)
+      p.Y[i + (long)i * p.ldy] += p.a * p.vec[i];
+    return;
+  }
+  const long total = (long)p.rows * p.cols;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % p.rows), j = (int)(e / p.rows);
+    float* y = p.Y + i + (long)j * p.ldy;
+    const float x = p.X[i + (long)j * p.ldx];
+    switch (p.op) {
+      case EW_ADD: *y += p.a * x; break;
+      case EW_SCALE_COLS: *y = x * p.vec[j]; break;
+      case EW_COPY: *y = x; break;
+      default: break;
+    }
+  }
+}
+
+// ---- preconditioner scalars (Alg 1 lines 16-17) ---------------------
+// For each layer side: effective lambda (relative mode :940, continuation :711) and
+// s_i = (D_i + lambda)^{-1} - 1/lambda.  Writes s (r floats) and lambda_eff (1 float).
+struct PrecScalProb {
+  const float* D; int r; float lam; int flags;
+  float* s; float* lam_out;
+};
+constexpr int PS_MAXP = 200;
+struct PrecScalBatch { int nprob; PrecScalProb p[PS_MAXP]; };
+
+__global__ void prec_scalars_kernel(const __grid_constant__ PrecScalBatch b) {
+  const PrecScalProb& p = b.p[blockIdx.x];
+  __shared__ float s_min, s_max;
+  if (threadIdx.x == 0) {
+    float mn = 3.4e38f, mx = 0.f;
+    for (int i = 0; i < p.r; ++i) { mn = fminf(mn, p.D[i]); mx = fmaxf(mx, p.D[i]); }
+    if (p.r == 0) mn = 0.f;
+    s_min = mn; s_max = mx;
+  }
+  __syncthreads();
+  float lam = p.lam;
+  if (p.flags & 2) lam = lam * s_max;          // relative: lambda = phi * max D
+  float shift = 0.f;
+  if (p.flags & 1) { shift = s_min; lam += shift; }  // continuation
+  for (int i = threadIdx.x; i < p.r; i += blockDim.x) {
+    const float dd = p.D[i] - shift;
+    p.s[i] = 1.f / (dd + lam) - 1.f / lam;
+  }
+  if (threadIdx.x == 0) *p.lam_out = lam;
+}
+
+// Scale rows/cols of small blocks by the preconditioner vectors:
+//   mode 0: Y(:, j) *= s[j] * c            (c = 1/lambda_other read from device)
+//   mode 1: Z(i, j) *= sG[i] * sA[j]
+struct PrecScaleProb {
+  float* Y; int ld; int rows, cols;
+  const float* s_col; const float* s_row; const float* lam_div;
+  int mode;
+};
+struct PrecScaleBatch { int nprob; PrecScaleProb p[PS_MAXP]; };
+
+__global__ void prec_scale_kernel(const __grid_constant__ PrecScaleBatch b) {
+  const PrecScaleProb& p = b.p[blockIdx.y];
+  const long total = (long)p.rows * p.cols;
+  const float inv = p.lam_div ? 1.f / *p.lam_div : 1.f;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % p.rows), j = (int)(e / p.rows);
+    float f = p.s_col[j];
+    if (p.mode == 0) f *= inv;
+    else f *= p.s_row[i];
+    p.Y[i + (long)j * p.ld] *= f;
+  }
+}
+
+// Final coefficient of J in S: 1 / (lambda_G lambda_A), written to a device scalar.
+__global__ void prec_coef_kernel(const float* lamG, const float* lamA, float* coef) {
+  *coef = 1.f / (*lamG * *lamA);
+}
+
+// ---- Philox4x32-10 Gaussian sketch -------------------------------------
+// Omega (n x l col-major), element e = j*n + i; counter block e/4, word pair by e%4;
+// uniforms (x + 0.5) 2^-32; Box-Muller in fp64; rounded to fp32.
+BKFAC_DEV void philox_round(unsigned& c0, unsigned& c1, unsigned& c2, unsigned& c3,
+                            unsigned k0, unsigned k1) {
+  const unsigned long long p0 = 0xD2511F53ull * c0;
+  const unsigned long long p1 = 0xCD9E8D57ull * c2;
+  const unsigned hi0 = (unsigned)(p0 >> 32), lo0 = (unsigned)p0;
+  const unsigned hi1 = (unsigned)(p1 >> 32), lo1 = (unsigned)p1;
+  const unsigned n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+  c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+}
+
+BKFAC_DEV void philox4x32_10(unsigned c[4], unsigned k0, unsigned k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    philox_round(c[0], c[1], c[2], c[3], k0, k1);
+  }
+}
+
+__global__ void philox_sketch_kernel(float* Om, long total, unsigned long long seed,
+                                     unsigned long long counter) {
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const unsigned long long blk = (unsigned long long)e >> 2;
+    unsigned c[4] = {(unsigned)blk, (unsigned)(blk >> 32), (unsigned)counter,
+                     (unsigned)(counter >> 32)};
+    philox4x32_10(c, (unsigned)seed, (unsigned)(seed >> 32));
+    const int t = (int)(e & 3);
+    const int pp = t >> 1;
+    const double ua = ((double)c[2 * pp] + 0.5) * 2.3283064365386963e-10;
+    const double ub = ((double)c[2 * pp + 1] + 0.5) * 2.3283064365386963e-10;
+    const double rad = sqrt(-2.0 * log(ua));
+    const double th = 6.283185307179586 * ub;
+    const double z = (t & 1) ? rad * sin(th) : rad * cos(th);
+    Om[e] = (float)z;
+  }
+}
+
+}  // namespace bkfac

@@ -1,0 +1,206 @@
+"""Stack driver: B-KFAC / B-R-KFAC over many K-factors and layers.
+
+Per step k (Alg 4 / Alg 5; Alg 1 lines 16-17, :401-405):
+  * k == 0: Mtilde_{B,0} = M_0 M_0^T -> top-r  (alpha = 0, beta = 1, phantom basis)
+  * k >= 1: if RSVD is due (k % T_RSVD == 0): (U, D) <- RSVD(Mcal_{k-1}), then
+            Brand update with (alpha, beta) = (rho, 1 - rho)
+  * dense EA factor Mcal_k (only when RSVD is enabled)
+  * S = Gamma~^{-1} J A~^{-1} for every layer whose factors this rank owns.
+Every call goes through the C ABI; this module only owns buffers and the schedule.
+
+Multi-GPU: whole layers are assigned to ranks by greedy LPT on
+n_A^3 + n_Gamma^3 (``shard_layers``); each rank updates its own factors and
+preconditions its own layers; preconditioned gradients are all-gathered per slot.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from . import binding
+
+
+def shard_layers(layer_costs: Sequence[float], world: int) -> List[List[int]]:
+    """Greedy LPT: layers sorted by decreasing cost, each to the least-loaded rank
+    (ties: lowest rank).  Deterministic; returns per-rank lists in ascending order."""
+    order = sorted(range(len(layer_costs)), key=lambda i: (-layer_costs[i], i))
+    loads = [0.0] * world
+    owned: List[List[int]] = [[] for _ in range(world)]
+    for i in order:
+        r = min(range(world), key=lambda q: (loads[q], q))
+        loads[r] += layer_costs[i]
+        owned[r].append(i)
+    return [sorted(o) for o in owned]
+
+
+def layer_cost(n_A: int, n_G: int) -> float:
+    return float(n_A) ** 3 + float(n_G) ** 3
+
+
+class BKFACStack:
+    """Owns the per-factor state (ping-pong U/D buffers, optional dense EA factor) of
+    the factors a rank owns and runs whole steps through the bkfac C ABI."""
+
+    def __init__(self, factors: Sequence[Tuple[int, int, int]],
+                 layers: Sequence[Tuple[int, int, int, int]],
+                 rho: float, lam: float, rsvd_every: int = 0, oversample: int = 10,
+                 power_iters: int = 2, precond_flags: int = 0, brand_flags: int = 0,
+                 device: int = 0, rank: int = 0, world: int = 1, rsvd_seed: int = 20221015):
+        """factors: (n, r, c_max) per global factor; layers: (d_G, d_A, g_index, a_index)."""
+        import torch
+        self.torch = torch
+        self.rho, self.lam = float(rho), float(lam)
+        self.rsvd_every, self.oversample, self.power_iters = rsvd_every, oversample, power_iters
+        self.precond_flags, self.brand_flags = precond_flags, brand_flags
+        self.rsvd_seed = rsvd_seed
+        self.device = device
+        self.rank, self.world = rank, world
+        self.factors = [tuple(f) for f in factors]
+        self.layers = [tuple(l) for l in layers]
+        costs = [layer_cost(self.factors[a][0], self.factors[g][0]) for (_, _, g, a) in self.layers]
+        self.owned_layers_all = shard_layers(costs, world) if self.layers else [[] for _ in range(world)]
+        self.my_layers = self.owned_layers_all[rank]
+        owned_f = set()
+        for li in self.my_layers:
+            _, _, g, a = self.layers[li]
+            owned_f.update([g, a])
+        if not self.layers:   # factor-only workloads: round-robin on n^3
+            fo = shard_layers([float(f[0]) ** 3 for f in self.factors], world)[rank]
+            owned_f.update(fo)
+        self.my_factors = sorted(owned_f)
+        self.local = {g: i for i, g in enumerate(self.my_factors)}
+        dense_flag = binding.BKFAC_FACTOR_DENSE_EA if rsvd_every > 0 else 0
+        fdesc = [(self.factors[g][0], self.factors[g][1], self.factors[g][2], dense_flag)
+                 for g in self.my_factors]
+        ldesc = []
+        for li in self.my_layers:
+            dG, dA, g, a = self.layers[li]
+            ldesc.append((dG, dA, self.factors[g][1], self.factors[a][1]))
+        self.ctx = binding.Context(fdesc, ldesc, device=device)
+        dev = f"cuda:{device}"
+        self.U = []
+        self.D = []
+        self.K = []
+        for g in self.my_factors:
+            n, r, _ = self.factors[g]
+            self.U.append([torch.zeros((r, n), dtype=torch.float32, device=dev) for _ in range(2)])
+            self.D.append([torch.zeros((r,), dtype=torch.float32, device=dev) for _ in range(2)])
+            self.K.append(torch.zeros((n, n), dtype=torch.float32, device=dev) if rsvd_every > 0 else None)
+        self.cur = [0] * len(self.my_factors)
+        self.k = 0
+        self.n_overwrites = 0
+        self.S: Dict[int, "torch.Tensor"] = {}
+        for li in self.my_layers:
+            dG, dA, _, _ = self.layers[li]
+            self.S[li] = torch.empty((dG, dA), dtype=torch.float32, device=dev)
+
+    # ---------------------------------------------------------------------------------
+    def state(self, g: int):
+        i = self.local[g]
+        return self.U[i][self.cur[i]], self.D[i][self.cur[i]]
+
+    def set_state(self, g: int, U, D) -> None:
+        i = self.local[g]
+        self.U[i][self.cur[i]].copy_(U)
+        self.D[i][self.cur[i]].copy_(D)
+
+    def _phantom(self, i: int):
+        U = self.U[i][self.cur[i]]
+        U.zero_()
+        r = U.shape[0]
+        U[self.torch.arange(r), self.torch.arange(r)] = 1.0
+        self.D[i][self.cur[i]].zero_()
+
+    def step(self, M: Dict[int, "torch.Tensor"], J: Optional[Dict[int, "torch.Tensor"]] = None,
+             stream=None) -> Dict[int, "torch.Tensor"]:
+        """One step over the owned factors (M keyed by global factor index, each (c, n))
+        and owned layers (J keyed by global layer index, each (d_G, d_A))."""
+        k = self.k
+        if k == 0:
+            for i in range(len(self.my_factors)):
+                self._phantom(i)
+            alpha, beta = 0.0, 1.0
+        else:
+            alpha, beta = self.rho, 1.0 - self.rho
+            if self.rsvd_every and k % self.rsvd_every == 0:
+                for i, g in enumerate(self.my_factors):
+                    self.ctx.bkfac_rsvd_overwrite(i, self.K[i], self.oversample, self.power_iters,
+                                                  self.rsvd_seed + g, self.n_overwrites,
+                                                  self.U[i][self.cur[i]], self.D[i][self.cur[i]],
+                                                  stream)
+                self.n_overwrites += 1
+        ups = []
+        for i, g in enumerate(self.my_factors):
+            c, nx = self.cur[i], 1 - self.cur[i]
+            ups.append(dict(factor=i, U_in=self.U[i][c], D_in=self.D[i][c], M=M[g],
+                            U_out=self.U[i][nx], D_out=self.D[i][nx], alpha=alpha, beta=beta,
+                            flags=self.brand_flags))
+        if ups:
+            self.ctx.bkfac_brand_update(ups, stream)
+        if self.rsvd_every:
+            for i, g in enumerate(self.my_factors):
+                self.ctx.bkfac_ea_accumulate(i, self.K[i], M[g], self.rho if k > 0 else 0.0, stream)
+        for i in range(len(self.my_factors)):
+            self.cur[i] = 1 - self.cur[i]
+        out = {}
+        if J is not None and self.my_layers:
+            items = []
+            for lj, li in enumerate(self.my_layers):
+                dG, dA, g, a = self.layers[li]
+                UG, DG = self.state(g)
+                UA, DA = self.state(a)
+                items.append(dict(layer=lj, U_G=UG, D_G=DG, lambda_G=self.lam, U_A=UA, D_A=DA,
+                                  lambda_A=self.lam, J=J[li], S=self.S[li],
+                                  flags=self.precond_flags))
+            self.ctx.bkfac_precondition(items, stream)
+            out = {li: self.S[li] for li in self.my_layers}
+        self.k += 1
+        return out
+
+    def check(self, stream=None):
+        return self.ctx.bkfac_check(stream)
+
+    def launches(self) -> int:
+        return self.ctx.bkfac_launch_count()
+
+
+class SlotGather:
+    """All-gather of the preconditioned gradients: slot s holds each
+    rank's s-th owned layer, packed fp32 and padded to the slot maximum; one
+    ``all_gather_into_tensor`` per slot (NCCL over NVLink on the GPU box, gloo in tests)."""
+
+    def __init__(self, layers: Sequence[Tuple[int, int, int, int]], owned: List[List[int]],
+                 rank: int, device):
+        import torch
+        self.torch = torch
+        self.layers = layers
+        self.owned = owned
+        self.rank = rank
+        self.world = len(owned)
+        self.nslots = max((len(o) for o in owned), default=0)
+        self.slot_numel = []
+        for s in range(self.nslots):
+            sizes = [layers[o[s]][0] * layers[o[s]][1] if s < len(o) else 0 for o in owned]
+            self.slot_numel.append(max(sizes))
+        self.send = [torch.zeros(n, dtype=torch.float32, device=device) for n in self.slot_numel]
+        self.recv = [torch.zeros(n * self.world, dtype=torch.float32, device=device)
+                     for n in self.slot_numel]
+
+    def bytes_per_step(self) -> int:
+        return sum(4 * n * (self.world - 1) for n in self.slot_numel)
+
+    def gather(self, S_local: Dict[int, "torch.Tensor"], group=None) -> Dict[int, "torch.Tensor"]:
+        import torch.distributed as dist
+        out: Dict[int, "torch.Tensor"] = {}
+        mine = self.owned[self.rank]
+        for s in range(self.nslots):
+            if s < len(mine):
+                t = S_local[mine[s]].reshape(-1)
+                self.send[s][: t.numel()].copy_(t)
+            dist.all_gather_into_tensor(self.recv[s], self.send[s], group=group)
+            for q in range(self.world):
+                if s < len(self.owned[q]):
+                    li = self.owned[q][s]
+                    dG, dA = self.layers[li][0], self.layers[li][1]
+                    base = q * self.slot_numel[s]
+                    out[li] = self.recv[s][base: base + dG * dA].view(dG, dA)
+        return out

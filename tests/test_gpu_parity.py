@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same
+seeded fp32 inputs.  Tolerances from BASELINE.json north_star: relative Frobenius error
+of U_r D_r U_r^T <= 1e-4 after one step and <= 1e-3 after 20 chained steps; eigenvalues
+<= 1e-4 (normwise); preconditioned gradients <= 1e-3."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from tests._util import eig_rel_err, lowrank_rel_err
+from tests.gpu_helpers import from_dev_cols, gpu_brand, to_dev, to_dev_cols
+
+pytestmark = pytest.mark.gpu
+
+TOL_STEP = 1e-4
+TOL_CHAIN = 1e-3
+TOL_EIG = 1e-4
+TOL_PREC = 1e-3
+
+
+def _ctx(factors, layers=()):
+    from paper_2210_08494_b200 import binding
+    return binding.Context(factors, layers, device=0)
+
+
+def _orth_check(U, tol=1e-5):
+    G = U.T @ U
+    return float(np.abs(G - np.eye(G.shape[0])).max()) < tol
+
+
+# ------------------------------------------------------------------ single steps
+
+SHAPES = [  # (n, c, r): several tiles and ragged tails, c = 1, r = 1
+    (96, 8, 16), (200, 13, 37), (300, 32, 64), (700, 64, 100), (130, 1, 5),
+    (64, 16, 1), (1000, 96, 150), (577, 256, 220)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_brand_init_and_step(cuda_lib, shape):
+    n, c, r = shape
+    f = synth.random_case(n, c, r, seed=1000 + n + c + r, k=min(n, 2 * c), decay=0.9)
+    M0, M1 = f.batch(0).astype(np.float64), f.batch(1).astype(np.float64)
+    ctx = _ctx([(n, r, c, 0)])
+    U0 = synth.phantom_basis(n, r)
+    # init step: alpha = 0, beta = 1 (Mtilde_{B,0} = M_0 M_0^T)
+    Ug, Dg = gpu_brand(ctx, 0, U0, np.zeros(r), M0, 0.0, 1.0)
+    Uo, Do = O.brand_update(U0, np.zeros(r), M0, 0.0, 1.0, r)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    assert eig_rel_err(Do, Dg) < TOL_EIG
+    # regular step from the oracle's state cast to fp32 (both sides same inputs)
+    U32 = Uo.astype(np.float32).astype(np.float64)
+    D32 = Do.astype(np.float32).astype(np.float64)
+    Ug, Dg = gpu_brand(ctx, 0, U32, D32, M1, 0.95, 0.05)
+    Uo, Do = O.brand_update(U32, D32, M1, 0.95, 0.05, r)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    assert eig_rel_err(Do, Dg) < TOL_EIG
+    assert np.all(np.diff(Dg) <= 0) and np.all(Dg >= 0)
+    assert _orth_check(Ug)
+    code, bad, info = ctx.bkfac_check()
+    assert code == 0
+
+
+@pytest.mark.parametrize("shape", [(48, 40, 20), (256, 256, 220), (10, 256, 10), (128, 32, 128)])
+def test_dense_path(cuda_lib, shape):
+    """r + c >= n: the library forms alpha U D U^T + beta M M^T densely (a6')."""
+    n, c, r = shape
+    f = synth.random_case(n, c, r, seed=77 + n, k=min(n, c), decay=0.9)
+    M0, M1 = f.batch(0).astype(np.float64), f.batch(1).astype(np.float64)
+    ctx = _ctx([(n, r, c, 0)])
+    Ug, Dg = gpu_brand(ctx, 0, synth.phantom_basis(n, r), np.zeros(r), M0, 0.0, 1.0)
+    Uo, Do = O.brand_update(synth.phantom_basis(n, r), np.zeros(r), M0, 0.0, 1.0, r)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    U32, D32 = Uo.astype(np.float32), Do.astype(np.float32)
+    Ug, Dg = gpu_brand(ctx, 0, U32, D32, M1, 0.95, 0.05)
+    Uo, Do = O.brand_update(U32.astype(np.float64), D32.astype(np.float64), M1, 0.95, 0.05, r)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    assert eig_rel_err(Do, Dg) < TOL_EIG
+
+
+def test_zero_update_keeps_rep(cuda_lib):
+    """A = 0 leaves the representation unchanged (here scaled by alpha)."""
+    n, c, r = 200, 16, 24
+    rng = np.random.default_rng(3)
+    U, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    D = np.sort(rng.random(r) * 3 + 0.1)[::-1]
+    ctx = _ctx([(n, r, c, 0)])
+    Ug, Dg = gpu_brand(ctx, 0, U, D, np.zeros((n, c)), 0.9, 0.1)
+    U32 = U.astype(np.float32).astype(np.float64)
+    assert lowrank_rel_err(U32, 0.9 * D, Ug, Dg) < TOL_STEP
+    code, bad, info = ctx.bkfac_check()
+    assert code == 0 and (info & 1)  # all residual columns dropped (informational)
+
+
+# ------------------------------------------------------------------ chained (config 1)
+
+def test_cfg1_chain_20_steps(cuda_lib):
+    """BASELINE configs[0]: both factors, 20 chained Brand steps on the GPU vs the
+    oracle's own chain; then the 256x128 gradient preconditioned (G10)."""
+    cfg = synth.cfg1_toy()
+    import torch
+    from paper_2210_08494_b200 import BKFACStack
+    factors = [(f.n, f.r, f.c) for f in cfg.factors]
+    layers = [(l.d_G, l.d_A, l.g_index, l.a_index) for l in cfg.layers]
+    st = BKFACStack(factors, layers, cfg.rho, cfg.lam)
+    chains = [O.FactorChain(f.n, f.r, cfg.rho) for f in cfg.factors]
+    for k in range(cfg.steps):
+        Ms = {i: f.batch(k) for i, f in enumerate(cfg.factors)}
+        J = {0: cfg.layers[0].grad(k)}
+        S = st.step({i: to_dev_cols(m) for i, m in Ms.items()}, {0: to_dev(J[0])})
+        torch.cuda.synchronize()
+        reps = [ch.step(Ms[i].astype(np.float64), synth.phantom_basis(f.n, f.r))
+                for i, (ch, f) in enumerate(zip(chains, cfg.factors))]
+        tol = TOL_STEP if k == 0 else TOL_CHAIN
+        for i, f in enumerate(cfg.factors):
+            Ug, Dg = st.state(i)
+            Ug, Dg = from_dev_cols(Ug), Dg.double().cpu().numpy()
+            e = lowrank_rel_err(reps[i][0], reps[i][1], Ug, Dg)
+            assert e < tol, f"step {k} factor {i}: {e:.2e}"
+            assert eig_rel_err(reps[i][1], Dg) < TOL_EIG * (10 if k > 0 else 1)
+        (UG, DG), (UA, DA) = reps[1], reps[0]
+        So = O.precondition(J[0].astype(np.float64), UG, DG, cfg.lam, UA, DA, cfg.lam)
+        Sg = S[0].double().cpu().numpy()
+        assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC
+    code, bad, info = st.check()
+    assert code == 0
+
+
+# ------------------------------------------------------------------ preconditioning
+
+@pytest.mark.parametrize("dims", [(128, 256, 64, 64), (512, 4609, 220, 220), (10, 513, 10, 220),
+                                  (77, 301, 13, 29)])
+@pytest.mark.parametrize("flags", [0, 1, 2, 3])
+def test_precondition_kernel_only(cuda_lib, dims, flags):
+    dG, dA, rG, rA = dims
+    rng = np.random.default_rng(dG * 7 + dA + flags)
+    UG, _ = np.linalg.qr(rng.standard_normal((dG, rG)))
+    UA, _ = np.linalg.qr(rng.standard_normal((dA, rA)))
+    DG = np.sort(rng.random(rG) * 5)[::-1]
+    DA = np.sort(rng.random(rA) * 5)[::-1]
+    J = (0.1 * rng.standard_normal((dG, dA))).astype(np.float32)
+    lG, lA = 0.1, 0.05
+    ctx = _ctx([], [(dG, dA, rG, rA)])
+    import torch
+    S = torch.empty((dG, dA), dtype=torch.float32, device="cuda")
+    tUG, tUA = to_dev_cols(UG), to_dev_cols(UA)
+    tDG, tDA = to_dev(DG), to_dev(DA)
+    ctx.bkfac_precondition([dict(layer=0, U_G=tUG, D_G=tDG, lambda_G=lG, U_A=tUA, D_A=tDA,
+                                 lambda_A=lA, J=to_dev(J), S=S, flags=flags)])
+    torch.cuda.synchronize()
+    f32 = lambda x: x.astype(np.float32).astype(np.float64)
+    So = O.precondition(J.astype(np.float64), f32(UG), f32(DG), lG, f32(UA), f32(DA), lA,
+                        continuation=bool(flags & 1), lam_relative=bool(flags & 2))
+    Sg = S.double().cpu().numpy()
+    assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC
+
+
+# ------------------------------------------------------------------ RSVD / EA / sketch
+
+def test_gaussian_sketch_matches_oracle(cuda_lib):
+    import torch
+    from paper_2210_08494_b200 import binding
+    n, l = 4609, 230
+    Om = torch.empty((l, n), dtype=torch.float32, device="cuda")
+    binding.bkfac_gaussian_sketch(Om, seed=20221015 * 7 + 3, counter=5)
+    torch.cuda.synchronize()
+    g = Om.cpu().numpy().T.astype(np.float32)
+    o = O.gaussian_sketch(n, l, 20221015 * 7 + 3, 5).astype(np.float32)
+    ulp = np.abs(g.view(np.int32).astype(np.int64) - o.view(np.int32).astype(np.int64))
+    assert ulp.max() <= 1
+
+
+def test_ea_accumulate_and_rsvd(cuda_lib):
+    """a8 (dense EA) and a7 (RSVD overwrite on the same Omega) vs the oracle."""
+    import torch
+    n, c, r, ro, q = 700, 64, 40, 10, 2
+    f = synth.random_case(n, c, r, seed=901, k=48, decay=0.93)
+    ctx = _ctx([(n, r, c, 1)])
+    K = torch.zeros((n, n), dtype=torch.float32, device="cuda")
+    Mc = None
+    for k in range(3):
+        M = f.batch(k)
+        ctx.bkfac_ea_accumulate(0, K, to_dev_cols(M), 0.95 if k > 0 else 0.0)
+        Mc = O.ea_update(Mc, M.astype(np.float64), 0.95)
+    torch.cuda.synchronize()
+    Kg = K.double().cpu().numpy()
+    assert np.abs(Kg - Mc).max() / np.abs(Mc).max() < 1e-5
+    U = torch.empty((r, n), dtype=torch.float32, device="cuda")
+    D = torch.empty((r,), dtype=torch.float32, device="cuda")
+    ctx.bkfac_rsvd_overwrite(0, K, ro, q, 1234, 0, U, D)
+    torch.cuda.synchronize()
+    Uo, Do = O.rsvd_overwrite(Kg.astype(np.float32).astype(np.float64), r, ro, q, 1234, 0)
+    assert lowrank_rel_err(Uo, Do, from_dev_cols(U), D.double().cpu().numpy()) < TOL_STEP
+    assert ctx.bkfac_check()[0] == 0
+
+
+# ------------------------------------------------------------------ full size (sampled)
+
+def test_cfg2_full_size_step(cuda_lib):
+    """BASELINE configs[1] shape (n = 4609, c = 256, r = 220): init + one step."""
+    cfg = synth.cfg2_conv()
+    f = cfg.factors[0]
+    M0, M1 = f.batch(0).astype(np.float64), f.batch(1).astype(np.float64)
+    ctx = _ctx([(f.n, f.r, f.c, 0)])
+    U0 = synth.phantom_basis(f.n, f.r)
+    Uo, Do = O.brand_update(U0, np.zeros(f.r), M0, 0.0, 1.0, f.r)
+    Ug, Dg = gpu_brand(ctx, 0, U0, np.zeros(f.r), M0, 0.0, 1.0)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    U32, D32 = Uo.astype(np.float32).astype(np.float64), Do.astype(np.float32).astype(np.float64)
+    Uo, Do = O.brand_update(U32, D32, M1, cfg.rho, 1 - cfg.rho, f.r)
+    Ug, Dg = gpu_brand(ctx, 0, U32, D32, M1, cfg.rho, 1 - cfg.rho)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    assert eig_rel_err(Do, Dg) < TOL_EIG
+
+
+def test_cfg5_factor_shape_step(cuda_lib):
+    """BASELINE configs[4] factor shape (n = 4097, c = 1024, r = 512, m = 1536): one step."""
+    cfg = synth.cfg5_transformer(blocks=1)
+    f = cfg.factors[0]
+    M0 = f.batch(0).astype(np.float64)
+    ctx = _ctx([(f.n, f.r, f.c, 0)])
+    U0 = synth.phantom_basis(f.n, f.r)
+    Uo, Do = O.brand_update(U0, np.zeros(f.r), M0, 0.0, 1.0, f.r)
+    Ug, Dg = gpu_brand(ctx, 0, U0, np.zeros(f.r), M0, 0.0, 1.0)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    assert eig_rel_err(Do, Dg) < TOL_EIG
+
+
+# ------------------------------------------------------------------ errors / status
+
+def test_errors_and_status(cuda_lib):
+    import torch
+    from paper_2210_08494_b200 import binding
+    n, c, r = 100, 8, 10
+    ctx = _ctx([(n, r, c, 0)])
+    U = torch.zeros((r, n), device="cuda"); D = torch.zeros(r, device="cuda")
+    M = torch.zeros((c, n), device="cuda")
+    Uo = torch.zeros_like(U); Do = torch.zeros_like(D)
+    with pytest.raises(binding.BkfacError) as e:
+        ctx.bkfac_brand_update([dict(factor=0, U_in=U, D_in=D, M=M, U_out=U, D_out=Do,
+                                     alpha=0.9, beta=0.1)])
+    assert e.value.code == 4
+    with pytest.raises(binding.BkfacError) as e:
+        ctx.bkfac_brand_update([dict(factor=0, U_in=U, D_in=D, M=torch.zeros((c + 1, n), device="cuda"),
+                                     U_out=Uo, D_out=Do, alpha=0.9, beta=0.1)])
+    assert e.value.code == 2
+    with pytest.raises(binding.BkfacError) as e:
+        ctx.bkfac_brand_update([dict(factor=0, U_in=U, D_in=D, M=M, U_out=Uo, D_out=Do,
+                                     alpha=0.9, beta=0.0)])
+    assert e.value.code == 1
+    # non-finite input -> device status NUMERIC
+    Mn = torch.full((c, n), float("nan"), device="cuda")
+    U[torch.arange(r), torch.arange(r)] = 1.0
+    ctx.bkfac_brand_update([dict(factor=0, U_in=U, D_in=D, M=Mn, U_out=Uo, D_out=Do,
+                                 alpha=0.0, beta=1.0)])
+    code, bad, info = ctx.bkfac_check()
+    assert code == 7 and bad == 0
