@@ -418,11 +418,15 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   int dev_prev = 0;
   cudaGetDevice(&dev_prev);
   cudaSetDevice(device);
-  cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  cudaFuncSetAttribute(backtr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  tc_init_attributes();
+  const int big = 220 * 1024;  // below the 227 KB opt-in limit minus static smem
+  bool attr_ok = true;
+  attr_ok &= cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(backtr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= tc_init_attributes();
+  if (!attr_ok) fprintf(stderr, "bkfac: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
+  cudaGetLastError();  // never leave a sticky error behind
   cudaSetDevice(dev_prev);
   const char* env = getenv("BKFAC_GEMM");
   c->use_tc = !(env && strcmp(env, "simt") == 0);
