@@ -1,0 +1,520 @@
+#!/usr/bin/env python
+"""B-KFAC hot-path benchmark (driver contract).
+
+A "step" is one pass of the whole hot path over one batch of synthetic input: the
+Brand update of every K-factor the rank owns (SURVEY §8(a) a0-a6, a6'), the dense EA
+accumulate and -- every T_RSVD steps -- the RSVD overwrite (a7, a8), the
+preconditioning of every owned layer (a9), and for N > 1 the NCCL all-gather of the
+preconditioned gradients (§8(e)).
+
+Default workload: BASELINE.json configs[3] semantics on the configs[2] VGG16_bn stack
+(32 K-factors, 16 layers, n_BS = 256, r = min(220, n), rho = 0.95, lambda = 0.1, dense
+EA + RSVD overwrite every 25 steps), the same workload at every GPU count.
+``--config cfg1|cfg2|cfg3|cfg4|cfg5`` selects another BASELINE config.
+
+value = Brand factor-updates/s over the whole job (all ranks); the line also carries
+preconditioned layers/s.  ``--impl reference`` times the fp64 oracle (the reference arm
+of this tier) on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Brand factor-updates/s + preconditioned layers/s, % roofline, 1/2/4/8 B200"
+UNIT = "factor-updates/s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=25)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=25.0)
+    ap.add_argument("--pool", type=int, default=2, help="distinct input batches kept on device")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ helpers
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        d["_source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0, "_source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(self.NAMES, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(name: str):
+    import synth
+    if name not in synth.CONFIGS:
+        raise SystemExit(f"unknown config {name}")
+    return synth.CONFIGS[name]()
+
+
+def device_inputs(cfg, my_factors, my_layers, pool: int, device):
+    """Per-step inputs generated ON DEVICE outside the timed region, same recipe as
+    synth.FactorSpec.batch (L diag(s) W + sigma N) but drawn with torch's CUDA RNG."""
+    import torch
+    M_pool = [dict() for _ in range(pool)]
+    J_pool = [dict() for _ in range(pool)]
+    for g in my_factors:
+        f = cfg.factors[g]
+        gen = torch.Generator(device=device)
+        gen.manual_seed(f.seed)
+        G = torch.randn((f.n, f.k), generator=gen, device=device, dtype=torch.float32)
+        L, R = torch.linalg.qr(G)
+        L = L * torch.sign(torch.diagonal(R))[None, :]
+        s = f.decay ** torch.arange(f.k, device=device, dtype=torch.float32)
+        for p in range(pool):
+            W = torch.randn((f.k, f.c), generator=gen, device=device)
+            N = torch.randn((f.n, f.c), generator=gen, device=device)
+            M = (L * s[None, :]) @ W + f.sigma * N            # n x c
+            M_pool[p][g] = M.t().contiguous()                   # (c, n) == col-major n x c
+        del G, L, R
+    for li in my_layers:
+        l = cfg.layers[li]
+        gen = torch.Generator(device=device)
+        gen.manual_seed(l.seed)
+        for p in range(pool):
+            J_pool[p][li] = (l.grad_std * torch.randn((l.d_G, l.d_A), generator=gen,
+                                                      device=device)).contiguous()
+    torch.cuda.synchronize()
+    return M_pool, J_pool
+
+
+def roofline_from_stages(stages, peaks, clocks):
+    """Dominant stage (largest event-timed share of the step) against its bound."""
+    if not stages:
+        return None, []
+    total = sum(s["ms"] for s in stages)
+    stages = sorted(stages, key=lambda s: -s["ms"])
+    top = stages[0]
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12          # TFLOP/s, FFMA on CUDA cores
+    name = top["name"]
+    sec = top["ms"] / 1e3
+    if name.startswith("gemm_") and top.get("path") == "tc":
+        tf32 = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))) * 0.5
+        bound, peak, unit, achieved = "tensor", tf32 / 3.0, "TFLOP/s", top["flops"] / sec / 1e12
+    elif name.startswith("gemm_") or name.startswith("eig_") or name.startswith("chol"):
+        bound, peak, unit, achieved = "alu", fp32_peak, "TFLOP/s", top["flops"] / sec / 1e12
+    else:
+        bound, peak, unit, achieved = "hbm", float(peaks["hbm_gbs"]), "GB/s", top["bytes"] / sec / 1e9
+    roof = {"bound": bound, "achieved": round(achieved, 4), "peak": round(peak, 3), "unit": unit,
+            "frac": round(achieved / peak, 5) if peak else None, "traffic": None,
+            "kernel": name, "share_of_step": round(top["ms"] / total, 4) if total else None,
+            "launches_per_step": None, "peak_source": peaks["_source"] +
+            ("; fp32 CUDA-core peak = 148 SM x 128 FMA x 2 x sm_max" if bound == "alu" else "")}
+    table = [{"stage": s["name"], "ms": round(s["ms"], 4), "share": round(s["ms"] / total, 4),
+              "gflop": round(s["flops"] / 1e9, 3), "gbytes": round(s["bytes"] / 1e9, 4),
+              "launches": s["launches"]} for s in stages]
+    return roof, table
+
+
+def traffic_lookup(kernel_stage: str):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(kernel_stage)
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------------------------ CPU oracle
+
+def oracle_sample(cfg, budget_s: float):
+    """Time the fp64 oracle as it stands on a bounded sample of the workload: one layer per
+    distinct layer shape (smallest first) -- its A and Gamma Brand updates and its
+    preconditioning -- until the time budget is spent.  Input generation is not timed.
+    Returns (factor_updates, layers, seconds, extrapolated full-step seconds, description)."""
+    import numpy as np
+    import oracle as O
+    rng = np.random.default_rng(0)
+
+    def inputs(f):
+        U, _ = np.linalg.qr(rng.standard_normal((f.n, f.r)))
+        return U, np.sort(rng.random(f.r))[::-1], f.batch(1).astype(np.float64)
+
+    layers = list(cfg.layers)
+    if not layers:   # factor-only workload (cfg2)
+        f = cfg.factors[0]
+        U, D, M = inputs(f)
+        t0 = time.perf_counter()
+        O.brand_update(U, D, M, cfg.rho, 1 - cfg.rho, f.r)
+        dt = time.perf_counter() - t0
+        return 1, 0, dt, dt * len(cfg.factors), f"1 Brand update of n={f.n}, fp64 numpy"
+    shapes = {}
+    for li, l in enumerate(layers):
+        key = (cfg.factors[l.a_index].n, cfg.factors[l.g_index].n, l.d_G, l.d_A)
+        shapes.setdefault(key, []).append(li)
+    times = {}
+    spent = 0.0
+    for key, lis in sorted(shapes.items(), key=lambda kv: kv[0][0] + kv[0][1]):
+        if spent > budget_s and times:
+            break
+        l = layers[lis[0]]
+        fa, fg = cfg.factors[l.a_index], cfg.factors[l.g_index]
+        ia, ig = inputs(fa), inputs(fg)
+        J = l.grad(1).astype(np.float64)
+        t0 = time.perf_counter()
+        UA, DA = O.brand_update(*ia, cfg.rho, 1 - cfg.rho, fa.r)
+        UG, DG = O.brand_update(*ig, cfg.rho, 1 - cfg.rho, fg.r)
+        O.precondition(J, UG, DG, cfg.lam, UA, DA, cfg.lam)
+        dt = time.perf_counter() - t0
+        times[key] = dt
+        spent += dt
+    step_s = 0.0
+    kref, tref = max(times.items(), key=lambda kv: kv[1])
+    for key, lis in shapes.items():
+        if key in times:
+            step_s += times[key] * len(lis)
+        else:   # unsampled shapes: O(n^2 (r + c)) model relative to the slowest sample
+            scale = (key[0] ** 2 + key[1] ** 2) / max(kref[0] ** 2 + kref[1] ** 2, 1)
+            step_s += tref * scale * len(lis)
+    lay = len(times)
+    desc = (f"{lay} of {len(layers)} layers (one per distinct shape, smallest first, "
+            f"~{budget_s:.0f}s budget): 2 Brand updates + 1 preconditioning each, fp64 numpy "
+            f"oracle; full-step time extrapolated by layer counts"
+            + ("" if lay == len(shapes) else "; unsampled shapes scaled by n^2"))
+    return 2 * lay, lay, sum(times.values()), step_s, desc
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d.get("num_threads", 1) for d in threadpool_info() if d.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return 1
+
+
+# ------------------------------------------------------------------------------ arms
+
+def run_reference(args, rank, world):
+    """Reference arm of this tier: the fp64 oracle as it stands on the host cores."""
+    if rank != 0:
+        return
+    cfg = make_workload(args.config)
+    import numpy as np
+    import oracle as O
+    layers = list(cfg.layers)
+    n_f = len(cfg.factors)
+    n_l = len(layers)
+    per_step = []
+    upd_total = 0
+    t_total = 0.0
+    rng = np.random.default_rng(1)
+    for step in range(args.warmup + args.steps):
+        # one layer per step (cycling): its 2 Brand updates + its preconditioning
+        if layers:
+            l = layers[step % n_l]
+            fis = (l.a_index, l.g_index)
+        else:
+            l = None
+            fis = (step % n_f,)
+        inputs = []
+        for fi in fis:
+            f = cfg.factors[fi]
+            U, _ = np.linalg.qr(rng.standard_normal((f.n, f.r)))
+            inputs.append((U, np.sort(rng.random(f.r))[::-1], f.batch(step).astype(np.float64), f.r))
+        J = l.grad(step).astype(np.float64) if l is not None else None
+        t0 = time.perf_counter()
+        reps = [O.brand_update(U, D, M, cfg.rho, 1 - cfg.rho, r) for (U, D, M, r) in inputs]
+        if l is not None:
+            O.precondition(J, reps[1][0], reps[1][1], cfg.lam, reps[0][0], reps[0][1], cfg.lam)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            per_step.append(dt)
+            upd_total += len(fis)
+            t_total += dt
+    value = upd_total / t_total
+    cores = blas_threads()
+    sample = (f"per step: one layer of the {cfg.name} stack (cycling) = {len(fis)} Brand "
+              f"update(s) + {'1 preconditioning' if layers else 'no layer'}, fp64 numpy oracle")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * t_total / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "factors": n_f, "layers": n_l,
+                       "sample": "one layer (2 factor updates + preconditioning) per step"},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2210_08494_b200 import BKFACStack, SlotGather
+
+    device = torch.device(f"cuda:{local_rank}")
+    torch.cuda.set_device(device)
+    cfg = make_workload(args.config)
+    factors = [(f.n, f.r, f.c) for f in cfg.factors]
+    layers = [(l.d_G, l.d_A, l.g_index, l.a_index) for l in cfg.layers]
+    stack = BKFACStack(factors, layers, cfg.rho, cfg.lam, rsvd_every=cfg.rsvd_every,
+                       oversample=cfg.oversample, power_iters=cfg.power_iters,
+                       device=local_rank, rank=rank, world=world)
+    gather = SlotGather(layers, stack.owned_layers_all, rank, device) if world > 1 and layers else None
+    M_pool, J_pool = device_inputs(cfg, stack.my_factors, stack.my_layers, args.pool, device)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream()
+
+    def one_step(i):
+        S = stack.step(M_pool[i % args.pool], J_pool[i % args.pool])
+        if gather is not None:
+            gather.gather(S)
+
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+    code, bad, info = stack.check()
+    if code != 0:
+        raise SystemExit(f"device status error after warm-up (factor {bad})")
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sampler = ClockSampler(local_rank)
+    stack.ctx.bkfac_profile_enable(True)
+    l0 = stack.launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for i in range(args.steps):
+        flush.zero_()                       # L2 flush between timed steps (not timed)
+        ev[i][0].record(stream)
+        one_step(args.warmup + i)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = stack.launches() - l0
+    stages = stack.ctx.bkfac_profile_read()
+    stack.ctx.bkfac_profile_enable(False)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([ms, float(launches)], dtype=torch.float64, device=device)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms, launches = float(tmax[0]), int(tsum[1])
+    code, bad, info = stack.check()
+    if code != 0:
+        raise SystemExit(f"device status error in the timed region (factor {bad})")
+
+    n_f, n_l = len(cfg.factors), len(cfg.layers)
+    sec = ms / 1e3
+    value = n_f * args.steps / sec
+    layers_per_s = n_l * args.steps / sec
+
+    # ---- e2e through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, stack, gather, cfg, device, stream, world)
+
+    if rank != 0:
+        return
+    peaks = load_peaks()
+    for s in stages:
+        s["path"] = "tc" if os.environ.get("BKFAC_GEMM", "tc") != "simt" and stack_uses_tc(stack) else "simt"
+    roof, table = roofline_from_stages(stages, peaks, clocks)
+    if roof is not None:
+        roof["traffic"] = traffic_lookup(roof["kernel"])
+        roof["launches_per_step"] = round(next(s["launches"] for s in stages
+                                               if s["name"] == roof["kernel"]) / args.steps, 2)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        upd, lay, ssec, step_s, desc = oracle_sample(cfg, args.cpu_budget_s)
+        cpu = {"value": round(n_f / step_s, 4), "unit": UNIT, "cores": blas_threads(),
+               "kind": "oracle", "sample": desc + f"; sample took {ssec:.1f}s",
+               "measured_updates_per_s_on_sample": round(upd / ssec, 4)}
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak" if not layers else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "layers_per_s": round(layers_per_s, 3),
+            "config": {"workload": cfg.name, "factors": n_f, "layers": n_l,
+                       "n_BS": cfg.factors[0].c, "rho": cfg.rho, "lambda": cfg.lam,
+                       "rsvd_every": cfg.rsvd_every, "parallelism": f"layer-shard x{world}",
+                       "l2": "flushed between timed steps (512 MiB write)",
+                       "inputs": "device-resident pool of %d synthetic batches" % args.pool},
+            "roofline": roof, "stages": table, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks}
+    print(json.dumps(line), flush=True)
+
+
+def stack_uses_tc(stack) -> bool:
+    try:
+        return b"tcgen05" in stack.ctx.lib.bkfac_build_info() and os.environ.get("BKFAC_GEMM") != "simt"
+    except Exception:
+        return False
+
+
+def run_e2e(args, stack, gather, cfg, device, stream, world):
+    """Same metric through the public API with HOST inputs: per step, pinned host -> device
+    copies of the step's M and J, the step, and a device -> host read of S."""
+    import torch
+    import torch.distributed as dist
+    steps = max(1, min(args.e2e_steps, args.steps))
+    host_M = {}
+    for g in stack.my_factors:
+        f = cfg.factors[g]
+        key = (f.c, f.n)
+        if key not in host_M:
+            host_M[key] = torch.randn(key, dtype=torch.float32).pin_memory()
+    host_J, host_S = {}, {}
+    for li in stack.my_layers:
+        l = cfg.layers[li]
+        key = (l.d_G, l.d_A)
+        if key not in host_J:
+            host_J[key] = (l.grad_std * torch.randn(key, dtype=torch.float32)).pin_memory()
+            host_S[key] = torch.empty(key, dtype=torch.float32).pin_memory()
+    dev_M = {g: torch.empty((cfg.factors[g].c, cfg.factors[g].n), dtype=torch.float32, device=device)
+             for g in stack.my_factors}
+    dev_J = {li: torch.empty((cfg.layers[li].d_G, cfg.layers[li].d_A), dtype=torch.float32,
+                             device=device) for li in stack.my_layers}
+    h2d = sum(4 * t.numel() for t in dev_M.values()) + sum(4 * t.numel() for t in dev_J.values())
+    d2h = sum(4 * cfg.layers[li].d_G * cfg.layers[li].d_A for li in stack.my_layers)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        for g, t in dev_M.items():
+            f = cfg.factors[g]
+            t.copy_(host_M[(f.c, f.n)], non_blocking=True)
+        for li, t in dev_J.items():
+            l = cfg.layers[li]
+            t.copy_(host_J[(l.d_G, l.d_A)], non_blocking=True)
+        S = stack.step(dev_M, dev_J)
+        if gather is not None:
+            gather.gather(S)
+        for li, s in S.items():
+            l = cfg.layers[li]
+            host_S[(l.d_G, l.d_A)].copy_(s, non_blocking=True)
+        stream.synchronize()
+    sec = time.perf_counter() - t0
+    t = torch.tensor([sec], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t[0])
+        hd = torch.tensor([h2d, d2h], dtype=torch.float64, device=device)
+        dist.all_reduce(hd, op=dist.ReduceOp.SUM)
+        h2d, d2h = int(hd[0]), int(hd[1])
+    return {"value": round(len(cfg.factors) * steps / sec, 3), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "timing": "wall clock around the pinned-host copies + step + D2H read, max over ranks"}
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run (one rank per GPU)")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,22 @@ bkfac_status bkfac_check(bkfac_ctx ctx, void* stream, int* first_bad_factor, int
 /* Number of kernels this context has launched since creation (host-side counter). */
 uint64_t bkfac_launch_count(bkfac_ctx ctx);
 
+/* Optional per-stage timing: when enabled, every stage (a group of launches of one
+ * kernel family) is bracketed by CUDA events recorded on the launching stream, with
+ * its algorithmic flop and byte counts. */
+typedef struct {
+  char name[32];
+  long long calls;      /* stage executions                */
+  long long launches;   /* kernel launches inside them      */
+  double ms;            /* summed event-timed duration      */
+  double flops;         /* algorithmic flops                */
+  double bytes;         /* algorithmic bytes                */
+} bkfac_stage_stat;
+bkfac_status bkfac_profile_enable(bkfac_ctx ctx, int enable);   /* also clears records */
+/* Synchronises the recorded events, aggregates per stage name into out[0..max_out),
+ * clears the records and returns the number of distinct stages (-1 on error). */
+int bkfac_profile_read(bkfac_ctx ctx, bkfac_stage_stat* out, int max_out);
+
 const char* bkfac_status_string(bkfac_status s);
 
 /* Build identification string (compile flags / arch). */

@@ -26,7 +26,8 @@ STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKF
 
 EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac_destroy",
             "bkfac_brand_update", "bkfac_ea_accumulate", "bkfac_rsvd_overwrite",
-            "bkfac_precondition", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count", "bkfac_status_string",
+            "bkfac_precondition", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
+            "bkfac_profile_enable", "bkfac_profile_read", "bkfac_status_string",
             "bkfac_build_info"]
 
 
@@ -51,6 +52,12 @@ class BrandArgs(ctypes.Structure):
                 ("M", ctypes.c_void_p), ("c", ctypes.c_int), ("U_out", ctypes.c_void_p),
                 ("D_out", ctypes.c_void_p), ("alpha", ctypes.c_float), ("beta", ctypes.c_float),
                 ("flags", ctypes.c_int)]
+
+
+class StageStat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("calls", ctypes.c_longlong),
+                ("launches", ctypes.c_longlong), ("ms", ctypes.c_double),
+                ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
 class PrecondArgs(ctypes.Structure):
@@ -96,6 +103,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.bkfac_check.restype = ci
     lib.bkfac_launch_count.argtypes = [vp]
     lib.bkfac_launch_count.restype = u64
+    lib.bkfac_profile_enable.argtypes = [vp, ci]
+    lib.bkfac_profile_enable.restype = ci
+    lib.bkfac_profile_read.argtypes = [vp, ctypes.POINTER(StageStat), ci]
+    lib.bkfac_profile_read.restype = ci
     lib.bkfac_status_string.argtypes = [ci]
     lib.bkfac_status_string.restype = ctypes.c_char_p
     lib.bkfac_build_info.argtypes = []
@@ -199,6 +210,17 @@ class Context:
 
     def bkfac_launch_count(self) -> int:
         return int(self.lib.bkfac_launch_count(self.h))
+
+    def bkfac_profile_enable(self, on: bool = True) -> None:
+        _check(self.lib.bkfac_profile_enable(self.h, 1 if on else 0), "bkfac_profile_enable")
+
+    def bkfac_profile_read(self) -> List[dict]:
+        arr = (StageStat * 128)()
+        n = self.lib.bkfac_profile_read(self.h, arr, 128)
+        if n < 0:
+            raise BkfacError(6, "bkfac_profile_read")
+        return [dict(name=arr[i].name.decode(), calls=arr[i].calls, launches=arr[i].launches,
+                     ms=arr[i].ms, flops=arr[i].flops, bytes=arr[i].bytes) for i in range(min(n, 128))]
 
 
 def bkfac_gaussian_sketch(Omega, seed: int, counter: int, stream=None) -> None:

@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <map>
+#include <string>
 #include <vector>
 
 #include "bkfac.h"
@@ -92,6 +94,13 @@ struct bkfac_ctx_s {
   uint64_t launches = 0;
   int* host_status = nullptr;
   bool use_tc = true;
+  // optional per-stage CUDA-event profiling (bkfac_profile_enable)
+  bool prof = false;
+  struct Rec { std::string tag; cudaEvent_t a, b; double flops, bytes; uint64_t launches; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  int open_rec = -1;
 };
 
 namespace {
@@ -107,6 +116,33 @@ bool cuda_ok(cudaError_t e) {
     return false;
   }
   return true;
+}
+
+cudaEvent_t prof_event(bkfac_ctx c) {
+  if (c->pool_used == c->pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->pool.push_back(e);
+  }
+  return c->pool[c->pool_used++];
+}
+
+// Brackets one stage (one or more kernel launches on `st`) with CUDA events.
+void prof_begin(bkfac_ctx c, const char* tag, cudaStream_t st, double flops, double bytes) {
+  if (!c->prof) return;
+  bkfac_ctx_s::Rec r;
+  r.tag = tag; r.flops = flops; r.bytes = bytes; r.launches = c->launches;
+  r.a = prof_event(c); r.b = prof_event(c);
+  cudaEventRecord(r.a, st);
+  c->recs.push_back(r);
+  c->open_rec = (int)c->recs.size() - 1;
+}
+void prof_end(bkfac_ctx c, cudaStream_t st) {
+  if (!c->prof || c->open_rec < 0) return;
+  auto& r = c->recs[c->open_rec];
+  cudaEventRecord(r.b, st);
+  r.launches = c->launches - r.launches;
+  c->open_rec = -1;
 }
 
 #define LAUNCH_CHECK(ctx)                                   \
@@ -171,7 +207,22 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
   return BKFAC_OK;
 }
 
-bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
+bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st);
+bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char* tag) {
+  double flops = 0.0, bytes = 0.0;
+  for (int v = 0; v < 4; ++v)
+    for (auto& p : s.probs[v]) {
+      flops += 2.0 * p.M * (double)p.N * p.K;
+      bytes += 4.0 * ((double)p.M * p.K + (double)p.K * p.N + (double)p.M * p.N *
+                      ((p.beta != 0.f || p.beta_dev) ? 2.0 : 1.0));
+    }
+  prof_begin(ctx, tag, st, flops, bytes);
+  bkfac_status rr = run_gemms_impl(ctx, s, st);
+  prof_end(ctx, st);
+  return rr;
+}
+
+bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
   // split-K: aim for ~2 waves of CTAs over the whole stage
   long base_tiles = 0;
   for (int v = 0; v < 4; ++v)
@@ -212,7 +263,10 @@ bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ small stages
-bkfac_status run_ew(bkfac_ctx ctx, std::vector<EwProb>& v, cudaStream_t st) {
+bkfac_status run_ew(bkfac_ctx ctx, std::vector<EwProb>& v, cudaStream_t st, const char* tag) {
+  double bytes = 0.0;
+  for (auto& p : v) bytes += (p.op == EW_ADD_DIAG) ? 8.0 * p.rows : 12.0 * p.rows * (double)p.cols;
+  prof_begin(ctx, tag, st, 0.0, bytes);
   size_t i0 = 0;
   while (i0 < v.size()) {
     const size_t n = std::min(v.size() - i0, (size_t)EW_MAXP);
@@ -224,10 +278,14 @@ bkfac_status run_ew(bkfac_ctx ctx, std::vector<EwProb>& v, cudaStream_t st) {
     i0 += n;
   }
   v.clear();
+  prof_end(ctx, st);
   return BKFAC_OK;
 }
 
 bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) {
+  double flops = 0.0, bytes = 0.0;
+  for (auto& p : v) { flops += 2.0 * p.c * (double)p.c * p.c / 3.0; bytes += 12.0 * p.c * (double)p.c; }
+  prof_begin(ctx, "chol_inv", st, flops, bytes);
   std::vector<CholProb> small, big;
   int cmax_small = 0;
   for (auto& p : v) {
@@ -255,6 +313,7 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
     }
   }
   v.clear();
+  prof_end(ctx, st);
   return BKFAC_OK;
 }
 
@@ -270,18 +329,35 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
       mmax = std::max(mmax, b.p[i].m);
       rmax = std::max(rmax, b.p[i].r);
     }
+    double m3 = 0.0, m2 = 0.0, m2r = 0.0, mr = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      const double m = b.p[i].m, r = b.p[i].r;
+      m3 += m * m * m; m2 += m * m; m2r += m * m * r; mr += m * r;
+    }
+    // sytrd: 4/3 m^3 flops; algorithmic bytes: read K (lower), write reflectors + T
+    prof_begin(ctx, "eig_sytrd", st, 4.0 / 3.0 * m3, 4.0 * m2);
     sytrd_kernel<<<(unsigned)n, 1024, sizeof(float) * (4 * (size_t)mmax + 32), st>>>(b);
     LAUNCH_CHECK(ctx);
+    prof_end(ctx, st);
+    prof_begin(ctx, "eig_bisect", st, 0.0, 0.0);
     bisect_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, BIS_WARPS)), BIS_WARPS * 32,
                     sizeof(double) * 2 * (size_t)mmax, st>>>(b);
     LAUNCH_CHECK(ctx);
+    prof_end(ctx, st);
+    prof_begin(ctx, "eig_invit", st, 0.0, 8.0 * mr);
     invit_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, 128)), 128, 0, st>>>(b);
     LAUNCH_CHECK(ctx);
+    prof_end(ctx, st);
+    prof_begin(ctx, "eig_cluster", st, 0.0, 0.0);
     cluster_kernel<<<(unsigned)n, 1024, 0, st>>>(b);
     LAUNCH_CHECK(ctx);
+    prof_end(ctx, st);
+    // back-transform: 2 m^2 r flops (m-2 reflectors on r columns); bytes: reflectors + Y + V
+    prof_begin(ctx, "eig_backtr", st, 2.0 * m2r, 2.0 * m2 + 12.0 * mr);
     backtr_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, 32)), 1024,
                     sizeof(float) * 33 * (size_t)mmax, st>>>(b);
     LAUNCH_CHECK(ctx);
+    prof_end(ctx, st);
     i0 += n;
   }
   v.clear();
@@ -338,7 +414,7 @@ const char* bkfac_status_string(bkfac_status s) {
 }
 
 const char* bkfac_build_info(void) {
-  return "bkfac sm_100a; SIMT fp32 GEMM + tcgen05 3xTF32 GEMM; CholeskyQR2; Householder "
+  return "bkfac sm_100a; GEMM: " BKFAC_GEMM_PATH "; CholeskyQR2; Householder "
          "tridiagonalisation + fp64 multisection/inverse iteration";
 }
 
@@ -449,11 +525,53 @@ bkfac_status bkfac_set_workspace(bkfac_ctx c, void* p, size_t bytes) {
 bkfac_status bkfac_destroy(bkfac_ctx c) {
   if (!c) return BKFAC_ERR_INVALID_ARG;
   if (c->host_status) cudaFreeHost(c->host_status);
+  for (auto e : c->pool) cudaEventDestroy(e);
   delete c;
   return BKFAC_OK;
 }
 
 uint64_t bkfac_launch_count(bkfac_ctx c) { return c ? c->launches : 0; }
+
+bkfac_status bkfac_profile_enable(bkfac_ctx c, int enable) {
+  if (!c) return BKFAC_ERR_INVALID_ARG;
+  c->prof = enable != 0;
+  c->recs.clear();
+  c->pool_used = 0;
+  c->open_rec = -1;
+  return BKFAC_OK;
+}
+
+int bkfac_profile_read(bkfac_ctx c, bkfac_stage_stat* out, int max_out) {
+  if (!c) return -1;
+  std::map<std::string, bkfac_stage_stat> agg;
+  std::vector<std::string> order;
+  for (auto& r : c->recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto it = agg.find(r.tag);
+    if (it == agg.end()) {
+      bkfac_stage_stat z;
+      memset(&z, 0, sizeof(z));
+      strncpy(z.name, r.tag.c_str(), sizeof(z.name) - 1);
+      it = agg.emplace(r.tag, z).first;
+      order.push_back(r.tag);
+    }
+    it->second.calls += 1;
+    it->second.launches += (long long)r.launches;
+    it->second.ms += ms;
+    it->second.flops += r.flops;
+    it->second.bytes += r.bytes;
+  }
+  int n = 0;
+  for (auto& t : order) {
+    if (out && n < max_out) out[n] = agg[t];
+    ++n;
+  }
+  c->recs.clear();
+  c->pool_used = 0;
+  return n;
+}
 
 // ------------------------------------------------------------------------- Brand
 bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int count,
@@ -486,7 +604,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
   std::vector<int> brand, dense;
   for (int i = 0; i < count; ++i) (ctx->f[args[i].factor].dense ? dense : brand).push_back(i);
 
-  auto run = [&](void) -> bkfac_status { return run_gemms(ctx, gs, st); };
+  auto run = [&](const char* tag) -> bkfac_status { return run_gemms(ctx, gs, st, tag); };
 #define STAGE(x) do { if ((rs = (x)) != BKFAC_OK) goto done; } while (0)
 
   // ---------------- dense path (r + c >= n): K = alpha U diag(D) U^T + beta M M^T
@@ -501,7 +619,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         ew.push_back(e);
       }
     }
-    STAGE(run_ew(ctx, ew, st));
+    STAGE(run_ew(ctx, ew, st, "ew_dense_scale"));
     for (int i : dense) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
@@ -511,7 +629,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
                                fp.d.r, a.alpha), 0);
       }
     }
-    STAGE(run());
+    STAGE(run("gemm_dense_core"));
     for (int i : dense) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
@@ -519,7 +637,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       float* K = at<float>(ctx, fp.eig.K);
       gs.add(false, true, gp(a.M, n, a.M, n, K, n, n, n, a.c, a.beta, K, n, a.alpha != 0.f ? 1.f : 0.f), 0);
     }
-    STAGE(run());
+    STAGE(run("gemm_dense_core"));
     for (int i : dense) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
@@ -539,7 +657,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       gemm_ws(p, at<float>(ctx, fp.ws));
       gs.add(true, false, p, fp.ws_elems);
     }
-    STAGE(run());
+    STAGE(run("gemm_proj"));
     // B: R = M - U P
     for (int i : brand) {
       const auto& a = args[i];
@@ -548,7 +666,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       gs.add(false, false, gp(a.U_in, n, at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), n, n, a.c,
                               r, -1.f, a.M, n, 1.f), 0);
     }
-    STAGE(run());
+    STAGE(run("gemm_resid"));
     // CGS2 re-projection: P2 = U^T R; R -= U P2; P += P2
     bool any_reorth = false;
     for (int i : brand) {
@@ -562,7 +680,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       gs.add(true, false, p, fp.ws_elems);
     }
     if (any_reorth) {
-      STAGE(run());
+      STAGE(run("gemm_cgs2_proj"));
       for (int i : brand) {
         const auto& a = args[i];
         if (a.flags & BKFAC_BRAND_NO_REORTH) continue;
@@ -575,8 +693,8 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         e.rows = r; e.cols = a.c; e.a = 1.f; e.op = EW_ADD;
         ew.push_back(e);
       }
-      STAGE(run());
-      STAGE(run_ew(ctx, ew, st));
+      STAGE(run("gemm_cgs2_resid"));
+      STAGE(run_ew(ctx, ew, st, "ew_cgs2"));
     }
     // CholeskyQR2 of R:  G = R^T R; L1; Q1 = R L1^{-T}; G = Q1^T Q1; L2; Q = Q1 L2^{-T}
     for (int pass = 0; pass < 2; ++pass) {
@@ -589,7 +707,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         gemm_ws(p, at<float>(ctx, fp.ws));
         gs.add(true, false, p, fp.ws_elems);
       }
-      STAGE(run());
+      STAGE(run("gemm_gram"));
       for (int i : brand) {
         const auto& a = args[i];
         const auto& fp = ctx->f[a.factor];
@@ -606,7 +724,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         const float* Li = at<float>(ctx, pass == 0 ? fp.L1i : fp.L2i);
         gs.add(false, true, gp(X, n, Li, c, Y, n, n, c, c, 1.f), 0);
       }
-      STAGE(run());
+      STAGE(run("gemm_qmul"));
     }
     // R_Q = L2^T L1^T -> W rows [r, r+c); then core K = beta W W^T (+ alpha D on the diagonal)
     for (int i : brand) {
@@ -616,7 +734,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       gs.add(true, true, gp(at<float>(ctx, fp.L2), c, at<float>(ctx, fp.L1), c,
                             at<float>(ctx, fp.W) + r, fp.m, c, c, c, 1.f), 0);
     }
-    STAGE(run());
+    STAGE(run("gemm_rq"));
     for (int i : brand) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
@@ -630,8 +748,8 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         ew.push_back(e);
       }
     }
-    STAGE(run());
-    STAGE(run_ew(ctx, ew, st));
+    STAGE(run("gemm_core"));
+    STAGE(run_ew(ctx, ew, st, "ew_core_diag"));
     for (int i : brand) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
@@ -653,7 +771,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     p.k1 = r;
     gs.add(false, false, p, 0);
   }
-  STAGE(run());
+  STAGE(run("gemm_rotate"));
 done:
 #undef STAGE
   if (dev_prev != ctx->device) cudaSetDevice(dev_prev);
@@ -674,7 +792,7 @@ bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K, const floa
   const int n = fp.d.n;
   GemmStage gs;
   gs.add(false, true, gp(M, n, M, n, K, n, n, n, c, 1.f - rho, K, n, rho), 0);
-  return run_gemms(ctx, gs, st);
+  return run_gemms(ctx, gs, st, "gemm_ea");
 }
 
 // ------------------------------------------------------------------------- RSVD
@@ -702,10 +820,12 @@ bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K, int
   std::vector<EigProb> eg;
   bkfac_status rs;
   // Omega -> Q ; Y = K Omega
+  prof_begin(ctx, "rsvd_sketch", st, 0.0, 4.0 * n * (double)l);
   philox_sketch_kernel<<<1024, 256, 0, st>>>(Q, (long)n * l, seed, counter);
   LAUNCH_CHECK(ctx);
+  prof_end(ctx, st);
   gs.add(false, false, gp(K, n, Q, n, Y, n, n, l, n, 1.f), 0);
-  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
   auto orth = [&](const float* X, float* Qout) -> bkfac_status {
     // CholeskyQR2: Q2 = X L1^{-T}, Qout = Q2 L2^{-T}
     for (int pass = 0; pass < 2; ++pass) {
@@ -714,35 +834,35 @@ bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K, int
       GemmProb p = gp(In, n, In, n, at<float>(ctx, fp.Gr), l, l, l, n, 1.f);
       gemm_ws(p, ws);
       gs.add(true, false, p, fp.ws_r_elems);
-      bkfac_status s2 = run_gemms(ctx, gs, st);
+      bkfac_status s2 = run_gemms(ctx, gs, st, "gemm_rsvd_gram");
       if (s2 != BKFAC_OK) return s2;
       ch.push_back(chol_prob(ctx, at<float>(ctx, fp.Gr), l, pass == 0 ? fp.L1r : fp.L2r,
                              pass == 0 ? fp.L1ir : fp.L2ir, fp.cscr_r, status));
       if ((s2 = run_chol(ctx, ch, st)) != BKFAC_OK) return s2;
       gs.add(false, true, gp(In, n, at<float>(ctx, pass == 0 ? fp.L1ir : fp.L2ir), l, Out, n, n, l, l, 1.f), 0);
-      if ((s2 = run_gemms(ctx, gs, st)) != BKFAC_OK) return s2;
+      if ((s2 = run_gemms(ctx, gs, st, "gemm_rsvd_qmul")) != BKFAC_OK) return s2;
     }
     return BKFAC_OK;
   };
   for (int q = 0; q < power_iters; ++q) {
     if ((rs = orth(Y, Q)) != BKFAC_OK) return rs;
     gs.add(false, false, gp(K, n, Q, n, Y, n, n, l, n, 1.f), 0);
-    if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+    if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
   }
   if ((rs = orth(Y, Q)) != BKFAC_OK) return rs;
   // B = Q^T K Q
   gs.add(false, false, gp(K, n, Q, n, T, n, n, l, n, 1.f), 0);
-  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
   {
     GemmProb p = gp(Q, n, T, n, at<float>(ctx, fp.eig_r.K), l, l, l, n, 1.f);
     gemm_ws(p, ws);
     gs.add(true, false, p, fp.ws_r_elems);
-    if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+    if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_proj")) != BKFAC_OK) return rs;
   }
   eg.push_back(eig_prob(ctx, fp.eig_r, l, r, at<float>(ctx, fp.eig_r.V), l, D_out, status));
   if ((rs = run_eig(ctx, eg, st)) != BKFAC_OK) return rs;
   gs.add(false, false, gp(Q, n, at<float>(ctx, fp.eig_r.V), l, U_out, n, n, r, l, 1.f), 0);
-  return run_gemms(ctx, gs, st);
+  return run_gemms(ctx, gs, st, "gemm_rsvd_rot");
 }
 
 bkfac_status bkfac_gaussian_sketch(float* Om, int n, int l, uint64_t seed, uint64_t counter,
@@ -778,6 +898,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
   bkfac_status rs;
   GemmStage gs;
   // S1: scalars
+  prof_begin(ctx, "prec_scalars", st, 0.0, 0.0);
   for (int i0 = 0; i0 < count; i0 += PS_MAXP / 2) {
     const int n = std::min(count - i0, PS_MAXP / 2);
     psb.nprob = 0;
@@ -797,6 +918,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     prec_coef_kernel<<<1, 1, 0, st>>>(lam + 1, lam + 0, lam + 2);
     LAUNCH_CHECK(ctx);
   }
+  prof_end(ctx, st);
   // S2: Y = J U_A (d_G x r_A), Xt = J^T U_G (d_A x r_G)
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
@@ -809,7 +931,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     }
     if (rG > 0) gs.add(false, false, gp(a.J, dA, a.U_G, dG, at<float>(ctx, lp.Xt), dA, dA, rG, dG, 1.f), 0);
   }
-  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  if ((rs = run_gemms(ctx, gs, st, "gemm_prec_proj")) != BKFAC_OK) return rs;
   // S3: Z = U_G^T Y (r_G x r_A)
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
@@ -818,8 +940,9 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     if (rA > 0 && rG > 0)
       gs.add(true, false, gp(a.U_G, dG, at<float>(ctx, lp.Y), dG, at<float>(ctx, lp.Z), rG, rG, rA, dG, 1.f), 0);
   }
-  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  if ((rs = run_gemms(ctx, gs, st, "gemm_prec_z")) != BKFAC_OK) return rs;
   // S4: Y' = Y diag(sA)/lamG ; Z' = diag(sG) Z diag(sA) ; Xt' = Xt diag(sG)/lamA
+  prof_begin(ctx, "prec_scale", st, 0.0, 0.0);
   for (int i0 = 0; i0 < count; i0 += PS_MAXP / 3) {
     const int n = std::min(count - i0, PS_MAXP / 3);
     pcb.nprob = 0;
@@ -839,6 +962,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
       LAUNCH_CHECK(ctx);
     }
   }
+  prof_end(ctx, st);
   // S5: Y' += U_G Z'
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
@@ -849,7 +973,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
       gs.add(false, false, gp(a.U_G, dG, at<float>(ctx, lp.Z), rG, Y, dG, dG, rA, rG, 1.f, Y, dG, 1.f), 0);
     }
   }
-  if ((rs = run_gemms(ctx, gs, st)) != BKFAC_OK) return rs;
+  if ((rs = run_gemms(ctx, gs, st, "gemm_prec_small")) != BKFAC_OK) return rs;
   // S7: S^T (d_A x d_G) = [U_A | Xt'] [Y'^T ; U_G^T] + coef J^T
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
@@ -865,7 +989,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     p.beta_dev = lam + 2;
     gs.add(false, true, p, 0);
   }
-  return run_gemms(ctx, gs, st);
+  return run_gemms(ctx, gs, st, "gemm_prec_out");
 }
 
 // ------------------------------------------------------------------------- check

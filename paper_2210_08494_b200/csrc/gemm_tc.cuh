@@ -2,4 +2,5 @@
 #pragma once
 namespace bkfac {
 inline bool tc_init_attributes() { return true; }
+#define BKFAC_GEMM_PATH "SIMT fp32 (CUDA cores)"
 }
