@@ -379,7 +379,10 @@ class FactorChain:
         else:
             if self.rsvd_every and k % self.rsvd_every == 0:
                 # Alg 5 (:641-646): overwrite with RSVD(Mcal_{k-1}), then B-update.
-                self.U, self.D = rsvd_overwrite(self.Mcal, self.r, self.oversample,
+                # sketch width l = r + r_o capped at n (reading R7: l = n is the
+                # exact EVD of Mcal_{k-1}, the limit of the range finder)
+                ro = min(self.oversample, self.n - self.r)
+                self.U, self.D = rsvd_overwrite(self.Mcal, self.r, ro,
                                                 self.power_iters, self.rsvd_seed,
                                                 self.n_overwrites)
                 self.n_overwrites += 1

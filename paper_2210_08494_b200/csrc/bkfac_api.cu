@@ -19,6 +19,7 @@
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "misc.cuh"
+#include "sytrd_cluster.cuh"
 
 using namespace bkfac;
 
@@ -301,13 +302,10 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
       b.nprob = (int)n;
       int cmax = 0;
       for (size_t i = 0; i < n; ++i) { b.p[i] = list[i0 + i]; cmax = std::max(cmax, b.p[i].c); }
-      if (pass == 0) {
-        const size_t smem = sizeof(float) * ((size_t)cmax * (cmax + 1) / 2 + cmax + 32);
-        chol_inv_kernel<true><<<(unsigned)n, 1024, smem, st>>>(b);
-      } else {
-        const size_t smem = sizeof(float) * ((size_t)cmax + 32);
-        chol_inv_kernel<false><<<(unsigned)n, 1024, smem, st>>>(b);
-      }
+      if (pass == 0)
+        chol_inv_kernel<true><<<(unsigned)n, 1024, chol_smem_bytes(cmax, true), st>>>(b);
+      else
+        chol_inv_kernel<false><<<(unsigned)n, 1024, chol_smem_bytes(cmax, false), st>>>(b);
       LAUNCH_CHECK(ctx);
       i0 += n;
     }
@@ -336,8 +334,37 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     }
     // sytrd: 4/3 m^3 flops; algorithmic bytes: read K (lower), write reflectors + T
     prof_begin(ctx, "eig_sytrd", st, 4.0 / 3.0 * m3, 4.0 * m2);
-    sytrd_kernel<<<(unsigned)n, 1024, sizeof(float) * (4 * (size_t)mmax + 32), st>>>(b);
-    LAUNCH_CHECK(ctx);
+    {
+      static EigBatch sub;
+      for (int C : {0, 1, 2, 4, 8}) {
+        sub.nprob = 0;
+        int msub = 0;
+        for (size_t i = 0; i < n; ++i)
+          if (sytrd_cluster_size(b.p[i].m) == C) {
+            sub.p[sub.nprob++] = b.p[i];
+            msub = std::max(msub, b.p[i].m);
+          }
+        if (sub.nprob == 0) continue;
+        if (C == 0) {
+          sytrd_kernel<<<(unsigned)sub.nprob, 1024, sizeof(float) * (4 * (size_t)msub + 32), st>>>(sub);
+        } else {
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3((unsigned)(C * sub.nprob), 1, 1);
+          cfg.blockDim = dim3(1024, 1, 1);
+          cfg.dynamicSmemBytes = sytrd_cluster_smem_bytes(msub, C);
+          cfg.stream = st;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeClusterDimension;
+          attr[0].val.clusterDim.x = (unsigned)C;
+          attr[0].val.clusterDim.y = 1;
+          attr[0].val.clusterDim.z = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel, sub, C))) return BKFAC_ERR_CUDA;
+        }
+        LAUNCH_CHECK(ctx);
+      }
+    }
     prof_end(ctx, st);
     prof_begin(ctx, "eig_bisect", st, 0.0, 0.0);
     bisect_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, BIS_WARPS)), BIS_WARPS * 32,
@@ -345,7 +372,8 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
     prof_begin(ctx, "eig_invit", st, 0.0, 8.0 * mr);
-    invit_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, 128)), 128, 0, st>>>(b);
+    invit_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, 128)), 128,
+                   sizeof(double) * 2 * (size_t)mmax, st>>>(b);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
     prof_begin(ctx, "eig_cluster", st, 0.0, 0.0);
@@ -497,8 +525,12 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   const int big = 220 * 1024;  // below the 227 KB opt-in limit minus static smem
   bool attr_ok = true;
   attr_ok &= cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(chol_inv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(backtr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= tc_init_attributes();
   if (!attr_ok) fprintf(stderr, "bkfac: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));

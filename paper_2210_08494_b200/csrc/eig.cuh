@@ -223,13 +223,32 @@ BKFAC_DEV double hash_unit(unsigned a, unsigned b) {
   return ((double)h / 4294967296.0) - 0.5;
 }
 
-// grid: (nprob, ceil(rmax/128)), block 128: thread = eigenvector j.
+// grid: (nprob, ceil(rmax/128)), block 128: thread = eigenvector j.  smem: 2m doubles.
+// Chains (pivot recurrence, forward and back substitution) are carried in registers;
+// the per-vector arrays are written once per pass and read back in the next pass
+// (interleaved a[i*r + j] so a warp's accesses are coalesced).
 __global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   const int m = p.m, r = p.r;
+  extern __shared__ __align__(16) double ism[];
+  double* dd = ism;        // diagonal
+  double* ee = dd + m;     // off-diagonal (ee[m-1] = 0)
+  __shared__ double s_tiny;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    dd[i] = (double)p.d[i];
+    ee[i] = (i < m - 1) ? (double)p.e[i] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tn = 0.0;
+    for (int i = 0; i < m; ++i)
+      tn = fmax(tn, fabs(dd[i]) + fabs(ee[i]) + (i > 0 ? fabs(ee[i - 1]) : 0.0));
+    s_tiny = fmax(tn, 1e-300) * 2.2e-16;
+  }
+  __syncthreads();
   const int j = blockIdx.y * blockDim.x + threadIdx.x;
   if (j >= r) return;
-  // scratch arrays, interleaved by eigenvector: a[i*r + j]
+  const double tiny = s_tiny;
   double* dU = p.scr;                  // U diagonal
   double* du = dU + (long)m * r;       // U first superdiagonal
   double* du2 = du + (long)m * r;      // U second superdiagonal
@@ -237,23 +256,15 @@ __global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigB
   unsigned char* pv = p.piv;
   double* x = p.Y;
 #define AT(a, i) (a)[(long)(i) * r + j]
-  const double lam = p.lam[j];
-  // ||T||_1 estimate for the zero-pivot replacement
-  double tn = 0.0;
-  for (int i = 0; i < m; ++i) {
-    const double t = fabs((double)p.d[i]) + (i > 0 ? fabs((double)p.e[i - 1]) : 0.0) +
-                     (i < m - 1 ? fabs((double)p.e[i]) : 0.0);
-    tn = fmax(tn, t);
-  }
-  const double tiny = fmax(tn, 1e-300) * 2.2e-16;
   if (m == 1) { AT(x, 0) = 1.0; return; }
+  const double lam = p.lam[j];
   // LU with partial pivoting of T - lam I (LAPACK dgttrf recurrence)
-  double dcur = (double)p.d[0] - lam;
-  double dufcur = (double)p.e[0];
+  double dcur = dd[0] - lam;
+  double dufcur = ee[0];
   for (int i = 0; i < m - 1; ++i) {
-    const double sub = (double)p.e[i];
-    const double dnext = (double)p.d[i + 1] - lam;
-    const double dunext = (i + 1 < m - 1) ? (double)p.e[i + 1] : 0.0;
+    const double sub = ee[i];
+    const double dnext = dd[i + 1] - lam;
+    const double dunext = ee[i + 1];
     if (fabs(dcur) >= fabs(sub)) {
       double piv = dcur;
       if (fabs(piv) < tiny) piv = (piv >= 0.0) ? tiny : -tiny;
@@ -270,23 +281,27 @@ __global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigB
   }
   if (fabs(dcur) < tiny) dcur = (dcur >= 0.0) ? tiny : -tiny;
   AT(dU, m - 1) = dcur;
-  // start vector
+  // start vector (deterministic, distinct per eigenvector)
   for (int i = 0; i < m; ++i) AT(x, i) = hash_unit((unsigned)i, (unsigned)j) + 0.5;
   for (int it = 0; it < 3; ++it) {
-    // forward: apply L^{-1} with row interchanges
+    // forward: apply L^{-1} with row interchanges; the running entry is carried
+    double carry = AT(x, 0);
     for (int i = 0; i < m - 1; ++i) {
-      const double xi = AT(x, i), xn = AT(x, i + 1);
+      const double xn = AT(x, i + 1);
+      const double f = AT(dl, i);
       if (AT(pv, i) == 0) {
-        AT(x, i + 1) = xn - AT(dl, i) * xi;
+        AT(x, i) = carry;
+        carry = xn - f * carry;
       } else {
         AT(x, i) = xn;
-        AT(x, i + 1) = xi - AT(dl, i) * xn;
+        carry = carry - f * xn;
       }
     }
-    // back substitution with U (bandwidth 2)
-    double x2 = 0.0, x1 = AT(x, m - 1) / AT(dU, m - 1);
-    AT(x, m - 1) = x1;
+    // back substitution with U (bandwidth 2); x1, x2 carried
+    double x1 = carry / AT(dU, m - 1);
+    double x2 = 0.0;
     double amax = fabs(x1);
+    AT(x, m - 1) = x1;
     for (int i = m - 2; i >= 0; --i) {
       const double xi = (AT(x, i) - AT(du, i) * x1 - AT(du2, i) * x2) / AT(dU, i);
       AT(x, i) = xi;
@@ -294,15 +309,14 @@ __global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigB
       x1 = xi;
       amax = fmax(amax, fabs(xi));
     }
-    // normalise (scale by max first, then 2-norm)
+    // normalise: scale by 1/max, then by 1/||x||_2 (two streaming passes)
     const double s1 = (amax > 0.0 && isfinite(amax)) ? 1.0 / amax : 1.0;
     double nrm = 0.0;
     for (int i = 0; i < m; ++i) {
       const double t = AT(x, i) * s1;
-      AT(x, i) = t;
       nrm += t * t;
     }
-    const double s2 = (nrm > 0.0) ? 1.0 / sqrt(nrm) : 0.0;
+    const double s2 = (nrm > 0.0) ? s1 / sqrt(nrm) : 0.0;
     for (int i = 0; i < m; ++i) AT(x, i) *= s2;
   }
 #undef AT

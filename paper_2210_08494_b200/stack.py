@@ -123,7 +123,10 @@ class BKFACStack:
             alpha, beta = self.rho, 1.0 - self.rho
             if self.rsvd_every and k % self.rsvd_every == 0:
                 for i, g in enumerate(self.my_factors):
-                    self.ctx.bkfac_rsvd_overwrite(i, self.K[i], self.oversample, self.power_iters,
+                    n_g, r_g, _ = self.factors[g]
+                    # sketch width l = r + r_o is capped at n (l = n is the exact EVD)
+                    ro = min(self.oversample, n_g - r_g)
+                    self.ctx.bkfac_rsvd_overwrite(i, self.K[i], ro, self.power_iters,
                                                   self.rsvd_seed + g, self.n_overwrites,
                                                   self.U[i][self.cur[i]], self.D[i][self.cur[i]],
                                                   stream)

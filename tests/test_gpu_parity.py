@@ -34,7 +34,9 @@ def _orth_check(U, tol=1e-5):
 
 SHAPES = [  # (n, c, r): several tiles and ragged tails, c = 1, r = 1
     (96, 8, 16), (200, 13, 37), (300, 32, 64), (700, 64, 100), (130, 1, 5),
-    (64, 16, 1), (1000, 96, 150), (577, 256, 220)]
+    (64, 16, 1), (1000, 96, 150), (577, 256, 220),
+    (900, 128, 250),    # core m = 378: 2-CTA cluster tridiagonalisation
+    (2000, 300, 450)]   # core m = 750: 8-CTA cluster tridiagonalisation
 
 
 @pytest.mark.parametrize("shape", SHAPES)
