@@ -110,6 +110,11 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
 bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K_dense, const float* M,
                                  int c, float rho, void* stream);
 
+/* Batched form of bkfac_ea_accumulate: `count` distinct factors in one grouped launch. */
+typedef struct { int factor; float* K_dense; const float* M; int c; float rho; } bkfac_ea_args;
+bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args, int count,
+                                       void* stream);
+
 /* U_out (n x r), D_out (r) <- RSVD of K_dense with l = r + oversample sketch columns and
  * `power_iters` re-orthonormalised power iterations.  The Gaussian sketch is
  * Philox4x32-10 keyed by `seed`, stream `counter`. */

@@ -25,7 +25,8 @@ STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKF
           7: "BKFAC_ERR_NUMERIC", 8: "BKFAC_ERR_UNSUPPORTED"}
 
 EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac_destroy",
-            "bkfac_brand_update", "bkfac_ea_accumulate", "bkfac_rsvd_overwrite",
+            "bkfac_brand_update", "bkfac_ea_accumulate", "bkfac_ea_accumulate_batch",
+            "bkfac_rsvd_overwrite",
             "bkfac_precondition", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
             "bkfac_profile_enable", "bkfac_profile_read", "bkfac_status_string",
             "bkfac_build_info"]
@@ -52,6 +53,11 @@ class BrandArgs(ctypes.Structure):
                 ("M", ctypes.c_void_p), ("c", ctypes.c_int), ("U_out", ctypes.c_void_p),
                 ("D_out", ctypes.c_void_p), ("alpha", ctypes.c_float), ("beta", ctypes.c_float),
                 ("flags", ctypes.c_int)]
+
+
+class EaArgs(ctypes.Structure):
+    _fields_ = [("factor", ctypes.c_int), ("K_dense", ctypes.c_void_p), ("M", ctypes.c_void_p),
+                ("c", ctypes.c_int), ("rho", ctypes.c_float)]
 
 
 class StageStat(ctypes.Structure):
@@ -93,6 +99,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.bkfac_brand_update.restype = ci
     lib.bkfac_ea_accumulate.argtypes = [vp, ci, vp, vp, ci, cf, vp]
     lib.bkfac_ea_accumulate.restype = ci
+    lib.bkfac_ea_accumulate_batch.argtypes = [vp, ctypes.POINTER(EaArgs), ci, vp]
+    lib.bkfac_ea_accumulate_batch.restype = ci
     lib.bkfac_rsvd_overwrite.argtypes = [vp, ci, vp, ci, ci, u64, u64, vp, vp, vp]
     lib.bkfac_rsvd_overwrite.restype = ci
     lib.bkfac_gaussian_sketch.argtypes = [vp, ci, ci, u64, u64, vp]
@@ -184,6 +192,15 @@ class Context:
         _check(self.lib.bkfac_ea_accumulate(self.h, factor, _ptr(K), _ptr(M), int(M.shape[0]),
                                             float(rho), _stream_ptr(stream)),
                "bkfac_ea_accumulate")
+
+    def bkfac_ea_batch(self, items: List[dict], stream=None) -> None:
+        """bkfac_ea_accumulate_batch: items of dict(factor, K, M, rho)."""
+        arr = (EaArgs * len(items))()
+        for i, a in enumerate(items):
+            arr[i] = EaArgs(a["factor"], _ptr(a["K"]), _ptr(a["M"]), int(a["M"].shape[0]),
+                            float(a["rho"]))
+        _check(self.lib.bkfac_ea_accumulate_batch(self.h, arr, len(items), _stream_ptr(stream)),
+               "bkfac_ea_accumulate_batch")
 
     def bkfac_rsvd_overwrite(self, factor: int, K, oversample: int, power_iters: int,
                              seed: int, counter: int, U_out, D_out, stream=None) -> None:

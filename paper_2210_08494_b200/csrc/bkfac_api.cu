@@ -346,7 +346,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
           }
         if (sub.nprob == 0) continue;
         if (C == 0) {
-          sytrd_kernel<<<(unsigned)sub.nprob, 1024, sizeof(float) * (4 * (size_t)msub + 32), st>>>(sub);
+          sytrd_kernel<<<(unsigned)sub.nprob, 1024, sizeof(float) * (36 * (size_t)msub + 64), st>>>(sub);
         } else {
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3((unsigned)(C * sub.nprob), 1, 1);
@@ -409,13 +409,14 @@ EigProb eig_prob(bkfac_ctx ctx, const EigWs& w, int m, int r, float* V, int ldv,
 }
 
 CholProb chol_prob(bkfac_ctx ctx, const float* G, int c, size_t L, size_t Li, size_t scr,
-                   int* status) {
+                   int* status, float shift = 0.f) {
   CholProb p;
   p.G = G; p.ldg = c;
   p.L = at<float>(ctx, L); p.Linv = at<float>(ctx, Li);
   p.scratch = at<float>(ctx, scr);
   p.status = status;
   p.c = c;
+  p.shift = shift;
   return p;
 }
 
@@ -529,7 +530,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   attr_ok &= cudaFuncSetAttribute(sytrd_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sytrd_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(backtr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
-  attr_ok &= cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= tc_init_attributes();
@@ -743,8 +744,10 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       for (int i : brand) {
         const auto& a = args[i];
         const auto& fp = ctx->f[a.factor];
+        // pass 0 is shifted (shift = c u tr(G)): shifted CholeskyQR2 (see chol.cuh)
         ch.push_back(chol_prob(ctx, at<float>(ctx, fp.G), a.c, pass == 0 ? fp.L1 : fp.L2,
-                               pass == 0 ? fp.L1i : fp.L2i, fp.cscr, status_ptr(ctx, a.factor)));
+                               pass == 0 ? fp.L1i : fp.L2i, fp.cscr, status_ptr(ctx, a.factor),
+                               pass == 0 ? (float)a.c * 1.1920929e-7f : 0.f));
       }
       STAGE(run_chol(ctx, ch, st));
       for (int i : brand) {
@@ -827,6 +830,26 @@ bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K, const floa
   return run_gemms(ctx, gs, st, "gemm_ea");
 }
 
+bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args, int count,
+                                       void* stream) {
+  if (!ctx || count < 0 || (count > 0 && !args)) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  GemmStage gs;
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    if (a.factor < 0 || a.factor >= (int)ctx->f.size() || !a.K_dense || !a.M)
+      return BKFAC_ERR_INVALID_ARG;
+    const auto& fp = ctx->f[a.factor];
+    if (!(fp.d.flags & BKFAC_FACTOR_DENSE_EA)) return BKFAC_ERR_INVALID_ARG;
+    if (a.c <= 0 || a.c > fp.d.c_max) return BKFAC_ERR_DIM;
+    if (!(a.rho >= 0.f && a.rho < 1.f)) return BKFAC_ERR_INVALID_ARG;
+    const int n = fp.d.n;
+    gs.add(false, true, gp(a.M, n, a.M, n, a.K_dense, n, n, n, a.c, 1.f - a.rho, a.K_dense, n, a.rho), 0);
+  }
+  if (count == 0) return BKFAC_OK;
+  return run_gemms(ctx, gs, static_cast<cudaStream_t>(stream), "gemm_ea");
+}
+
 // ------------------------------------------------------------------------- RSVD
 bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K, int oversample,
                                   int power_iters, uint64_t seed, uint64_t counter, float* U_out,
@@ -859,19 +882,20 @@ bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K, int
   gs.add(false, false, gp(K, n, Q, n, Y, n, n, l, n, 1.f), 0);
   if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
   auto orth = [&](const float* X, float* Qout) -> bkfac_status {
-    // CholeskyQR2: Q2 = X L1^{-T}, Qout = Q2 L2^{-T}
-    for (int pass = 0; pass < 2; ++pass) {
-      const float* In = pass == 0 ? X : Q2;
-      float* Out = pass == 0 ? Q2 : Qout;
+    // shifted CholeskyQR3 (the power-iteration block K Q is ill-conditioned by design):
+    // X -> Qout (shifted) -> Q2 -> Qout
+    for (int pass = 0; pass < 3; ++pass) {
+      const float* In = pass == 0 ? X : (pass == 1 ? Qout : Q2);
+      float* Out = pass == 1 ? Q2 : Qout;
       GemmProb p = gp(In, n, In, n, at<float>(ctx, fp.Gr), l, l, l, n, 1.f);
       gemm_ws(p, ws);
       gs.add(true, false, p, fp.ws_r_elems);
       bkfac_status s2 = run_gemms(ctx, gs, st, "gemm_rsvd_gram");
       if (s2 != BKFAC_OK) return s2;
-      ch.push_back(chol_prob(ctx, at<float>(ctx, fp.Gr), l, pass == 0 ? fp.L1r : fp.L2r,
-                             pass == 0 ? fp.L1ir : fp.L2ir, fp.cscr_r, status));
+      ch.push_back(chol_prob(ctx, at<float>(ctx, fp.Gr), l, fp.L1r, fp.L1ir, fp.cscr_r, status,
+                             pass == 0 ? (float)l * 1.1920929e-7f : 0.f));
       if ((s2 = run_chol(ctx, ch, st)) != BKFAC_OK) return s2;
-      gs.add(false, true, gp(In, n, at<float>(ctx, pass == 0 ? fp.L1ir : fp.L2ir), l, Out, n, n, l, l, 1.f), 0);
+      gs.add(false, true, gp(In, n, at<float>(ctx, fp.L1ir), l, Out, n, n, l, l, 1.f), 0);
       if ((s2 = run_gemms(ctx, gs, st, "gemm_rsvd_qmul")) != BKFAC_OK) return s2;
     }
     return BKFAC_OK;

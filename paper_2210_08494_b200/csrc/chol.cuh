@@ -24,6 +24,7 @@ struct CholProb {
   float* scratch;          // packed c(c+1)/2 floats (global path only)
   int* status;
   int c;
+  float shift;             // shifted CholeskyQR: G_ii += shift * trace(G) (0 = plain)
 };
 constexpr int CHOL_MAXP = 100;
 struct CholBatch { int nprob; CholProb p[CHOL_MAXP]; };
@@ -43,24 +44,29 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const __grid_constant__ 
   const int tid = threadIdx.x, nt = blockDim.x;
   const int tx = tid & 31, ty = tid >> 5;
 
-  float dmax = 0.f;
+  float dsum = 0.f, dmax = 0.f;
   for (int i = ty; i < c; i += 32)
     for (int k = tx; k <= i; k += 32) {
       const float g = p.G[i + (long)k * p.ldg];
       P[pidx(i, k)] = g;
-      if (k == i) dmax = fmaxf(dmax, g);
+      if (k == i) { dsum += g; dmax = fmaxf(dmax, g); }
     }
+  const float trace = block_sum(dsum, red);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if (tx == 0) red[ty] = dmax;
   __syncthreads();
-  if (tid == 0) {
-    float m = 0.f;
-    for (int w = 0; w < (nt + 31) / 32; ++w) m = fmaxf(m, red[w]);
-    red[0] = m;
-  }
+  float gmax = 0.f;
+  for (int w = 0; w < (nt + 31) / 32; ++w) gmax = fmaxf(gmax, red[w]);
+  // shifted first pass (sCQR, Fukaya et al. 2020): keeps the factorisation defined
+  // for ill-conditioned inputs; R = Q R_Q stays exact, later passes restore Q^T Q = I.
+  const float sh = (p.shift > 0.f) ? p.shift * trace : 0.f;
   __syncthreads();
-  const float tol = 8.0f * (float)c * 1.1920929e-7f * red[0];
+  if (sh > 0.f)
+    for (int i = tid; i < c; i += nt) P[pidx(i, i)] += sh;
+  __syncthreads();
+  // pivots at the rounding level of the largest diagonal entry = rank deficiency
+  const float tol = 4.0f * 1.1920929e-7f * (gmax + sh);
   int dropped = 0;
 
   // ---- phase 1: right-looking Cholesky

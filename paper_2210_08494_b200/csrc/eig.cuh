@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(1024) sytrd_kernel(const __grid_constant__ Eig
   float* wp = vp + m;
   float* y = wp + m;
   float* red = y + m;
+  float* ywarp = red + 32;    // per-warp partial y (32 * m floats), no atomics
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
 
@@ -91,8 +92,8 @@ __global__ void __launch_bounds__(1024) sytrd_kernel(const __grid_constant__ Eig
         K[i + (long)k * ld] = vi;
       }
       v[i] = vi;
-      y[i] = 0.f;
     }
+    for (int i = k + 1 + lane; i < m; i += 32) ywarp[warp * m + i] = 0.f;
     if (tid == 0) {
       p.d[k] = K[k + (long)k * ld];
       p.e[k] = beta;
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(1024) sytrd_kernel(const __grid_constant__ Eig
     __syncthreads();
     // fused: apply the previous rank-2 update to columns j >= k+1 (rows i >= j)
     // and accumulate y = K22 v from the lower triangle.
+    float* yw = ywarp + warp * m;
     for (int j = k + 1 + warp; j < m; j += nw) {
       const float vj = v[j];
       const float wpj = have_prev ? wp[j] : 0.f, vpj = have_prev ? vp[j] : 0.f;
@@ -112,10 +114,19 @@ __global__ void __launch_bounds__(1024) sytrd_kernel(const __grid_constant__ Eig
           K[i + (long)j * ld] = a;
         }
         acc = fmaf(a, v[i], acc);
-        if (i > j) atomicAdd(&y[i], a * vj);
+        if (i > j) yw[i] = fmaf(a, vj, yw[i]);
       }
       acc = warp_sum(acc);
-      if (lane == 0) atomicAdd(&y[j], acc);
+      __syncwarp();
+      if (lane == 0) yw[j] += acc;
+      __syncwarp();
+    }
+    __syncthreads();
+    for (int i = k + 1 + tid; i < m; i += nt) {
+      float s = 0.f;
+#pragma unroll 8
+      for (int w = 0; w < nw; ++w) s += ywarp[w * m + i];
+      y[i] = s;
     }
     __syncthreads();
     float pv = 0.f;

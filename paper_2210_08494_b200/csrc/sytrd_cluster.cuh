@@ -35,14 +35,14 @@ constexpr int SYTRD_CLUSTER_SMEM_FLOATS = 53 * 1024;  // 212 KB budget per CTA
 inline int sytrd_cluster_size(int m) {
   for (int C = 1; C <= 8; C *= 2) {
     const long own = ((long)m * (m + 1) / 2 + (long)C * m) / C;  // upper bound per CTA
-    const long extra = 6L * m + 64;
+    const long extra = 38L * m + 64;
     if (own + extra <= SYTRD_CLUSTER_SMEM_FLOATS) return C;
   }
   return 0;
 }
 inline size_t sytrd_cluster_smem_bytes(int m, int C) {
   const long own = ((long)m * (m + 1) / 2 + (long)C * m) / C;
-  return sizeof(float) * (size_t)(own + 6L * m + 64);
+  return sizeof(float) * (size_t)(own + 38L * m + 64);
 }
 
 __global__ void __launch_bounds__(1024, 1) sytrd_cluster_kernel(const __grid_constant__ EigBatch b,
@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(1024, 1) sytrd_cluster_kernel(const __grid_con
   float* ys = y + m;          // m    (summed y, local)
   float* scal = ys + m;       // 32   [0..1]: tau by parity, [2]: bad flag
   float* red = scal + 32;     // 32
-  float* col = red + 32;      // owned columns, packed
+  float* ywarp = red + 32;    // 32 * m  (per-warp partial y)
+  float* col = ywarp + 32 * m;  // owned columns, packed
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int nown = (q < m) ? (m - q + C - 1) / C : 0;
@@ -139,8 +140,9 @@ __global__ void __launch_bounds__(1024, 1) sytrd_cluster_kernel(const __grid_con
     }
     cluster.sync();                                              // (1) v_k, tau_k everywhere
     const float tau = scal[k & 1];
-    for (int i = k + 1 + tid; i < m; i += nt) y[i] = 0.f;
-    __syncthreads();
+    float* yw = ywarp + warp * m;     // this warp's private partial of y (no atomics)
+    for (int i = k + 1 + lane; i < m; i += 32) yw[i] = 0.f;
+    __syncwarp();
     // (b) fused update (v_{k-1}, w_{k-1}) + partial symv with v_k on owned columns j > k
     const int t0 = (k + 1 - q + C - 1) / C > 0 ? (k + 1 - q + C - 1) / C : 0;
     for (int t = t0 + warp; t < nown; t += nw) {
@@ -156,10 +158,20 @@ __global__ void __launch_bounds__(1024, 1) sytrd_cluster_kernel(const __grid_con
           cj[i - j] = a;
         }
         acc = fmaf(a, v[i], acc);
-        if (i > j) atomicAdd(&y[i], a * vj);
+        if (i > j) yw[i] = fmaf(a, vj, yw[i]);
       }
       acc = warp_sum(acc);
-      if (lane == 0) atomicAdd(&y[j], acc);
+      __syncwarp();
+      if (lane == 0) yw[j] += acc;
+      __syncwarp();
+    }
+    __syncthreads();
+    // CTA partial: y[i] = sum over warps
+    for (int i = k + 1 + tid; i < m; i += nt) {
+      float s = 0.f;
+#pragma unroll 8
+      for (int w = 0; w < nw; ++w) s += ywarp[w * m + i];
+      y[i] = s;
     }
     __syncthreads();
     cluster.sync();                                              // (2) partial y ready

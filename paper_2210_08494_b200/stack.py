@@ -140,8 +140,9 @@ class BKFACStack:
         if ups:
             self.ctx.bkfac_brand_update(ups, stream)
         if self.rsvd_every:
-            for i, g in enumerate(self.my_factors):
-                self.ctx.bkfac_ea_accumulate(i, self.K[i], M[g], self.rho if k > 0 else 0.0, stream)
+            self.ctx.bkfac_ea_batch([dict(factor=i, K=self.K[i], M=M[g],
+                                          rho=self.rho if k > 0 else 0.0)
+                                     for i, g in enumerate(self.my_factors)], stream)
         for i in range(len(self.my_factors)):
             self.cur[i] = 1 - self.cur[i]
         out = {}

@@ -36,7 +36,8 @@ SHAPES = [  # (n, c, r): several tiles and ragged tails, c = 1, r = 1
     (96, 8, 16), (200, 13, 37), (300, 32, 64), (700, 64, 100), (130, 1, 5),
     (64, 16, 1), (1000, 96, 150), (577, 256, 220),
     (900, 128, 250),    # core m = 378: 2-CTA cluster tridiagonalisation
-    (2000, 300, 450)]   # core m = 750: 8-CTA cluster tridiagonalisation
+    (2000, 250, 350),   # core m = 600: 8-CTA cluster tridiagonalisation
+    (2000, 300, 450)]   # core m = 750: global-memory tridiagonalisation
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -258,3 +259,32 @@ def test_errors_and_status(cuda_lib):
                                  alpha=0.0, beta=1.0)])
     code, bad, info = ctx.bkfac_check()
     assert code == 7 and bad == 0
+
+
+def test_rsvd_ill_conditioned_cfg4_factor(cuda_lib):
+    """configs[3] factor shape n = 577, r = 220, l = 230, q = 2 after 25 EA steps: the
+    power-iteration block K Q has condition ~1e3, which plain CholeskyQR2 cannot
+    orthonormalise in fp32 (regression: needs the shifted first pass)."""
+    import torch
+    cfg = synth.cfg4_vgg_sharded()
+    f = cfg.factors[2]
+    assert (f.n, f.r) == (577, 220)
+    ctx = _ctx([(f.n, f.r, f.c, 1)])
+    K = torch.zeros((f.n, f.n), dtype=torch.float32, device="cuda")
+    Ms = [f.batch(k) for k in range(25)]
+    ctx.bkfac_ea_batch([dict(factor=0, K=K, M=to_dev_cols(Ms[0]), rho=0.0)])
+    for k in range(1, 25):
+        ctx.bkfac_ea_batch([dict(factor=0, K=K, M=to_dev_cols(Ms[k]), rho=cfg.rho)])
+    U = torch.empty((f.r, f.n), dtype=torch.float32, device="cuda")
+    D = torch.empty((f.r,), dtype=torch.float32, device="cuda")
+    ctx.bkfac_rsvd_overwrite(0, K, 10, 2, 99, 3, U, D)
+    torch.cuda.synchronize()
+    Kg = K.double().cpu().numpy()
+    Mc = O.ea_process([m.astype(np.float64) for m in Ms], cfg.rho)[-1]
+    assert np.abs(Kg - Mc).max() / np.abs(Mc).max() < 1e-5
+    Uo, Do = O.rsvd_overwrite(Kg, f.r, 10, 2, 99, 3)
+    Dg = D.double().cpu().numpy()
+    assert lowrank_rel_err(Uo, Do, from_dev_cols(U), Dg) < TOL_STEP
+    assert eig_rel_err(Do, Dg) < TOL_EIG
+    assert Dg[-1] > 0
+    assert ctx.bkfac_check()[0] == 0
