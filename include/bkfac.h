@@ -122,6 +122,14 @@ bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K_dens
                                   int oversample, int power_iters, uint64_t seed,
                                   uint64_t counter, float* U_out, float* D_out, void* stream);
 
+/* Batched form of bkfac_rsvd_overwrite: `count` distinct factors, stage by stage. */
+typedef struct {
+  int factor; const float* K_dense; int oversample; int power_iters;
+  uint64_t seed; uint64_t counter; float* U_out; float* D_out;
+} bkfac_rsvd_args;
+bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* args, int count,
+                                        void* stream);
+
 /* Omega (n x l col-major) <- the RSVD Gaussian test matrix for (seed, counter): the
  * sketch step of bkfac_rsvd_overwrite exposed on its own (Philox4x32-10, key = seed,
  * counter words (e/4 lo, e/4 hi, counter lo, counter hi) for element e = j*n + i;

@@ -26,7 +26,7 @@ STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKF
 
 EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac_destroy",
             "bkfac_brand_update", "bkfac_ea_accumulate", "bkfac_ea_accumulate_batch",
-            "bkfac_rsvd_overwrite",
+            "bkfac_rsvd_overwrite", "bkfac_rsvd_overwrite_batch",
             "bkfac_precondition", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
             "bkfac_profile_enable", "bkfac_profile_read", "bkfac_status_string",
             "bkfac_build_info"]
@@ -58,6 +58,12 @@ class BrandArgs(ctypes.Structure):
 class EaArgs(ctypes.Structure):
     _fields_ = [("factor", ctypes.c_int), ("K_dense", ctypes.c_void_p), ("M", ctypes.c_void_p),
                 ("c", ctypes.c_int), ("rho", ctypes.c_float)]
+
+
+class RsvdArgs(ctypes.Structure):
+    _fields_ = [("factor", ctypes.c_int), ("K_dense", ctypes.c_void_p), ("oversample", ctypes.c_int),
+                ("power_iters", ctypes.c_int), ("seed", ctypes.c_uint64), ("counter", ctypes.c_uint64),
+                ("U_out", ctypes.c_void_p), ("D_out", ctypes.c_void_p)]
 
 
 class StageStat(ctypes.Structure):
@@ -103,6 +109,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.bkfac_ea_accumulate_batch.restype = ci
     lib.bkfac_rsvd_overwrite.argtypes = [vp, ci, vp, ci, ci, u64, u64, vp, vp, vp]
     lib.bkfac_rsvd_overwrite.restype = ci
+    lib.bkfac_rsvd_overwrite_batch.argtypes = [vp, ctypes.POINTER(RsvdArgs), ci, vp]
+    lib.bkfac_rsvd_overwrite_batch.restype = ci
     lib.bkfac_gaussian_sketch.argtypes = [vp, ci, ci, u64, u64, vp]
     lib.bkfac_gaussian_sketch.restype = ci
     lib.bkfac_precondition.argtypes = [vp, ctypes.POINTER(PrecondArgs), ci, vp]
@@ -208,6 +216,16 @@ class Context:
                                              seed, counter, _ptr(U_out), _ptr(D_out),
                                              _stream_ptr(stream)),
                "bkfac_rsvd_overwrite")
+
+    def bkfac_rsvd_batch(self, items: List[dict], stream=None) -> None:
+        """bkfac_rsvd_overwrite_batch: dict(factor, K, oversample, power_iters, seed, counter,
+        U_out, D_out)."""
+        arr = (RsvdArgs * len(items))()
+        for i, a in enumerate(items):
+            arr[i] = RsvdArgs(a["factor"], _ptr(a["K"]), int(a["oversample"]), int(a["power_iters"]),
+                              int(a["seed"]), int(a["counter"]), _ptr(a["U_out"]), _ptr(a["D_out"]))
+        _check(self.lib.bkfac_rsvd_overwrite_batch(self.h, arr, len(items), _stream_ptr(stream)),
+               "bkfac_rsvd_overwrite_batch")
 
     def bkfac_precondition(self, items: List[dict], stream=None) -> None:
         arr = (PrecondArgs * len(items))()

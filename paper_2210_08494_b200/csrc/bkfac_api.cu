@@ -851,74 +851,126 @@ bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args,
 }
 
 // ------------------------------------------------------------------------- RSVD
-bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K, int oversample,
-                                  int power_iters, uint64_t seed, uint64_t counter, float* U_out,
-                                  float* D_out, void* stream) {
-  if (!ctx || !K || !U_out || !D_out) return BKFAC_ERR_INVALID_ARG;
+bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* args, int count,
+                                        void* stream) {
+  if (!ctx || count < 0 || (count > 0 && !args)) return BKFAC_ERR_INVALID_ARG;
   if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
-  if (factor < 0 || factor >= (int)ctx->f.size()) return BKFAC_ERR_INVALID_ARG;
-  const auto& fp = ctx->f[factor];
-  if (!fp.rsvd) return BKFAC_ERR_INVALID_ARG;
-  if (oversample < 0 || power_iters < 0 || power_iters > 64) return BKFAC_ERR_INVALID_ARG;
-  const int n = fp.d.n, r = fp.d.r, l = r + oversample;
-  if (l > n) return BKFAC_ERR_RANK;
-  if (l > fp.lmax) return BKFAC_ERR_UNSUPPORTED;
+  int qmax = 0;
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    if (!a.K_dense || !a.U_out || !a.D_out) return BKFAC_ERR_INVALID_ARG;
+    if (a.factor < 0 || a.factor >= (int)ctx->f.size()) return BKFAC_ERR_INVALID_ARG;
+    const auto& fp = ctx->f[a.factor];
+    if (!fp.rsvd) return BKFAC_ERR_INVALID_ARG;
+    if (a.oversample < 0 || a.power_iters < 0 || a.power_iters > 64) return BKFAC_ERR_INVALID_ARG;
+    const int l = fp.d.r + a.oversample;
+    if (l > fp.d.n) return BKFAC_ERR_RANK;
+    if (l > fp.lmax) return BKFAC_ERR_UNSUPPORTED;
+    for (int j = 0; j < i; ++j)
+      if (args[j].factor == a.factor) return BKFAC_ERR_INVALID_ARG;
+    qmax = std::max(qmax, a.power_iters);
+  }
+  if (count == 0) return BKFAC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int* status = status_ptr(ctx, factor);
-  float* Y = at<float>(ctx, fp.Yr);
-  float* Q = at<float>(ctx, fp.Qr);
-  float* Q2 = at<float>(ctx, fp.Q2r);
-  float* T = at<float>(ctx, fp.Tr);
-  float* ws = at<float>(ctx, fp.ws_r);
   GemmStage gs;
   std::vector<CholProb> ch;
   std::vector<EigProb> eg;
   bkfac_status rs;
-  // Omega -> Q ; Y = K Omega
-  prof_begin(ctx, "rsvd_sketch", st, 0.0, 4.0 * n * (double)l);
-  philox_sketch_kernel<<<1024, 256, 0, st>>>(Q, (long)n * l, seed, counter);
-  LAUNCH_CHECK(ctx);
-  prof_end(ctx, st);
-  gs.add(false, false, gp(K, n, Q, n, Y, n, n, l, n, 1.f), 0);
+  struct Loc { int n, r, l; int* status; float *Y, *Q, *Q2, *T, *ws; const FactorPlan* fp; };
+  std::vector<Loc> L(count);
+  for (int i = 0; i < count; ++i) {
+    const auto& fp = ctx->f[args[i].factor];
+    L[i] = Loc{fp.d.n, fp.d.r, fp.d.r + args[i].oversample, status_ptr(ctx, args[i].factor),
+               at<float>(ctx, fp.Yr), at<float>(ctx, fp.Qr), at<float>(ctx, fp.Q2r),
+               at<float>(ctx, fp.Tr), at<float>(ctx, fp.ws_r), &fp};
+  }
+  // Omega -> Q (Philox sketch); Y = K Omega
+  {
+    double bytes = 0.0;
+    for (auto& x : L) bytes += 4.0 * x.n * (double)x.l;
+    prof_begin(ctx, "rsvd_sketch", st, 0.0, bytes);
+    for (int i = 0; i < count; ++i) {
+      philox_sketch_kernel<<<256, 256, 0, st>>>(L[i].Q, (long)L[i].n * L[i].l, args[i].seed,
+                                               args[i].counter);
+      LAUNCH_CHECK(ctx);
+    }
+    prof_end(ctx, st);
+  }
+  for (int i = 0; i < count; ++i)
+    gs.add(false, false, gp(args[i].K_dense, L[i].n, L[i].Q, L[i].n, L[i].Y, L[i].n, L[i].n, L[i].l,
+                            L[i].n, 1.f), 0);
   if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
-  auto orth = [&](const float* X, float* Qout) -> bkfac_status {
-    // shifted CholeskyQR3 (the power-iteration block K Q is ill-conditioned by design):
-    // X -> Qout (shifted) -> Q2 -> Qout
+  // shifted CholeskyQR3 of X (the power-iteration block K Q is ill-conditioned by
+  // design): X -> Qout (shifted) -> Q2 -> Qout, for the factors in `act`
+  auto orth = [&](const std::vector<int>& act, bool fromY) -> bkfac_status {
     for (int pass = 0; pass < 3; ++pass) {
-      const float* In = pass == 0 ? X : (pass == 1 ? Qout : Q2);
-      float* Out = pass == 1 ? Q2 : Qout;
-      GemmProb p = gp(In, n, In, n, at<float>(ctx, fp.Gr), l, l, l, n, 1.f);
-      gemm_ws(p, ws);
-      gs.add(true, false, p, fp.ws_r_elems);
+      for (int i : act) {
+        const float* In = pass == 0 ? (fromY ? L[i].Y : L[i].Q) : (pass == 1 ? L[i].Q : L[i].Q2);
+        GemmProb p = gp(In, L[i].n, In, L[i].n, at<float>(ctx, L[i].fp->Gr), L[i].l, L[i].l, L[i].l,
+                        L[i].n, 1.f);
+        gemm_ws(p, L[i].ws);
+        gs.add(true, false, p, L[i].fp->ws_r_elems);
+      }
       bkfac_status s2 = run_gemms(ctx, gs, st, "gemm_rsvd_gram");
       if (s2 != BKFAC_OK) return s2;
-      ch.push_back(chol_prob(ctx, at<float>(ctx, fp.Gr), l, fp.L1r, fp.L1ir, fp.cscr_r, status,
-                             pass == 0 ? (float)l * 1.1920929e-7f : 0.f));
+      for (int i : act)
+        ch.push_back(chol_prob(ctx, at<float>(ctx, L[i].fp->Gr), L[i].l, L[i].fp->L1r, L[i].fp->L1ir,
+                               L[i].fp->cscr_r, L[i].status,
+                               pass == 0 ? (float)L[i].l * 1.1920929e-7f : 0.f));
       if ((s2 = run_chol(ctx, ch, st)) != BKFAC_OK) return s2;
-      gs.add(false, true, gp(In, n, at<float>(ctx, fp.L1ir), l, Out, n, n, l, l, 1.f), 0);
+      for (int i : act) {
+        const float* In = pass == 0 ? (fromY ? L[i].Y : L[i].Q) : (pass == 1 ? L[i].Q : L[i].Q2);
+        float* Out = pass == 1 ? L[i].Q2 : L[i].Q;
+        gs.add(false, true, gp(In, L[i].n, at<float>(ctx, L[i].fp->L1ir), L[i].l, Out, L[i].n, L[i].n,
+                               L[i].l, L[i].l, 1.f), 0);
+      }
       if ((s2 = run_gemms(ctx, gs, st, "gemm_rsvd_qmul")) != BKFAC_OK) return s2;
     }
     return BKFAC_OK;
   };
-  for (int q = 0; q < power_iters; ++q) {
-    if ((rs = orth(Y, Q)) != BKFAC_OK) return rs;
-    gs.add(false, false, gp(K, n, Q, n, Y, n, n, l, n, 1.f), 0);
+  // note: pass 0 reads Y and writes Q, so X and Qout never alias
+  for (int q = 0; q < qmax; ++q) {
+    std::vector<int> act;
+    for (int i = 0; i < count; ++i)
+      if (q < args[i].power_iters) act.push_back(i);
+    if ((rs = orth(act, true)) != BKFAC_OK) return rs;
+    for (int i : act)
+      gs.add(false, false, gp(args[i].K_dense, L[i].n, L[i].Q, L[i].n, L[i].Y, L[i].n, L[i].n,
+                              L[i].l, L[i].n, 1.f), 0);
     if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
   }
-  if ((rs = orth(Y, Q)) != BKFAC_OK) return rs;
-  // B = Q^T K Q
-  gs.add(false, false, gp(K, n, Q, n, T, n, n, l, n, 1.f), 0);
-  if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
   {
-    GemmProb p = gp(Q, n, T, n, at<float>(ctx, fp.eig_r.K), l, l, l, n, 1.f);
-    gemm_ws(p, ws);
-    gs.add(true, false, p, fp.ws_r_elems);
-    if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_proj")) != BKFAC_OK) return rs;
+    std::vector<int> all(count);
+    for (int i = 0; i < count; ++i) all[i] = i;
+    if ((rs = orth(all, true)) != BKFAC_OK) return rs;
   }
-  eg.push_back(eig_prob(ctx, fp.eig_r, l, r, at<float>(ctx, fp.eig_r.V), l, D_out, status));
+  // B = Q^T K Q ; EVD(B) ; U = Q V_r
+  for (int i = 0; i < count; ++i)
+    gs.add(false, false, gp(args[i].K_dense, L[i].n, L[i].Q, L[i].n, L[i].T, L[i].n, L[i].n, L[i].l,
+                            L[i].n, 1.f), 0);
+  if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
+  for (int i = 0; i < count; ++i) {
+    GemmProb p = gp(L[i].Q, L[i].n, L[i].T, L[i].n, at<float>(ctx, L[i].fp->eig_r.K), L[i].l, L[i].l,
+                    L[i].l, L[i].n, 1.f);
+    gemm_ws(p, L[i].ws);
+    gs.add(true, false, p, L[i].fp->ws_r_elems);
+  }
+  if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_proj")) != BKFAC_OK) return rs;
+  for (int i = 0; i < count; ++i)
+    eg.push_back(eig_prob(ctx, L[i].fp->eig_r, L[i].l, L[i].r, at<float>(ctx, L[i].fp->eig_r.V),
+                          L[i].l, args[i].D_out, L[i].status));
   if ((rs = run_eig(ctx, eg, st)) != BKFAC_OK) return rs;
-  gs.add(false, false, gp(Q, n, at<float>(ctx, fp.eig_r.V), l, U_out, n, n, r, l, 1.f), 0);
+  for (int i = 0; i < count; ++i)
+    gs.add(false, false, gp(L[i].Q, L[i].n, at<float>(ctx, L[i].fp->eig_r.V), L[i].l, args[i].U_out,
+                            L[i].n, L[i].n, L[i].r, L[i].l, 1.f), 0);
   return run_gemms(ctx, gs, st, "gemm_rsvd_rot");
+}
+
+bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K, int oversample,
+                                  int power_iters, uint64_t seed, uint64_t counter, float* U_out,
+                                  float* D_out, void* stream) {
+  bkfac_rsvd_args a{factor, K, oversample, power_iters, seed, counter, U_out, D_out};
+  return bkfac_rsvd_overwrite_batch(ctx, &a, 1, stream);
 }
 
 bkfac_status bkfac_gaussian_sketch(float* Om, int n, int l, uint64_t seed, uint64_t counter,

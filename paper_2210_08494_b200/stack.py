@@ -122,14 +122,15 @@ class BKFACStack:
         else:
             alpha, beta = self.rho, 1.0 - self.rho
             if self.rsvd_every and k % self.rsvd_every == 0:
+                items = []
                 for i, g in enumerate(self.my_factors):
                     n_g, r_g, _ = self.factors[g]
                     # sketch width l = r + r_o is capped at n (l = n is the exact EVD)
-                    ro = min(self.oversample, n_g - r_g)
-                    self.ctx.bkfac_rsvd_overwrite(i, self.K[i], ro, self.power_iters,
-                                                  self.rsvd_seed + g, self.n_overwrites,
-                                                  self.U[i][self.cur[i]], self.D[i][self.cur[i]],
-                                                  stream)
+                    items.append(dict(factor=i, K=self.K[i], oversample=min(self.oversample, n_g - r_g),
+                                      power_iters=self.power_iters, seed=self.rsvd_seed + g,
+                                      counter=self.n_overwrites, U_out=self.U[i][self.cur[i]],
+                                      D_out=self.D[i][self.cur[i]]))
+                self.ctx.bkfac_rsvd_batch(items, stream)
                 self.n_overwrites += 1
         ups = []
         for i, g in enumerate(self.my_factors):

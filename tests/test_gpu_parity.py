@@ -288,3 +288,27 @@ def test_rsvd_ill_conditioned_cfg4_factor(cuda_lib):
     assert eig_rel_err(Do, Dg) < TOL_EIG
     assert Dg[-1] > 0
     assert ctx.bkfac_check()[0] == 0
+
+
+def test_rsvd_batch_mixed_shapes(cuda_lib):
+    """bkfac_rsvd_overwrite_batch over factors of different n, r, l (incl. l = n)."""
+    import torch
+    shapes = [(300, 40, 10), (64, 64, 0), (900, 100, 10)]     # (n, r, oversample)
+    ctx = _ctx([(n, r, 32, 1) for (n, r, _) in shapes])
+    Ks, items, outs = [], [], []
+    for i, (n, r, ro) in enumerate(shapes):
+        f = synth.random_case(n, 32, r, seed=500 + i, k=min(n, 24), decay=0.9)
+        K = torch.zeros((n, n), dtype=torch.float32, device="cuda")
+        for k in range(6):
+            ctx.bkfac_ea_batch([dict(factor=i, K=K, M=to_dev_cols(f.batch(k)), rho=0.9 if k else 0.0)])
+        U = torch.empty((r, n), device="cuda"); D = torch.empty((r,), device="cuda")
+        items.append(dict(factor=i, K=K, oversample=ro, power_iters=2, seed=7 + i, counter=1,
+                          U_out=U, D_out=D))
+        Ks.append(K); outs.append((U, D))
+    ctx.bkfac_rsvd_batch(items)
+    torch.cuda.synchronize()
+    for (n, r, ro), K, (U, D), it in zip(shapes, Ks, outs, items):
+        Kg = K.double().cpu().numpy()
+        Uo, Do = O.rsvd_overwrite(Kg, r, ro, 2, it["seed"], 1)
+        assert lowrank_rel_err(Uo, Do, from_dev_cols(U), D.double().cpu().numpy()) < TOL_STEP
+    assert ctx.bkfac_check()[0] == 0
