@@ -150,6 +150,19 @@ typedef struct {
 bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, int count,
                                 void* stream);
 
+/* The fp32-accurate GEMM every contraction above runs on, exposed for testing and for
+ * callers that need the same arithmetic:  C = alpha op(A) op(B) + beta C  (BLAS col-major;
+ * op(X) = X^T when trans* != 0; C is M x N with leading dimension ldc >= M).
+ * path BKFAC_GEMM_TCGEN05: 3xTF32 on tcgen05 tensor cores (the hot-path kernel);
+ * path BKFAC_GEMM_SIMT: fp32 FFMA on CUDA cores (comparison baseline).
+ * ws (device, optional, ws_bytes) enables deterministic split-K when K is long and the
+ * output small; without it the product runs unsplit.  Asynchronous on `stream`. */
+#define BKFAC_GEMM_TCGEN05 0
+#define BKFAC_GEMM_SIMT 1
+bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha, const float* A,
+                        int lda, const float* B, int ldb, float beta, float* C, int ldc, float* ws,
+                        size_t ws_bytes, int path, void* stream);
+
 /* Synchronises `stream`, reads the per-factor status words.  Returns BKFAC_OK or
  * BKFAC_ERR_NUMERIC (first offending factor in *first_bad_factor, else -1).
  * Informational bits (e.g. a Cholesky pivot dropped for a rank-deficient residual)

@@ -19,6 +19,8 @@ BKFAC_FACTOR_DENSE_EA = 1
 BKFAC_BRAND_NO_REORTH = 1
 BKFAC_PRECOND_CONTINUATION = 1
 BKFAC_PRECOND_LAMBDA_RELATIVE = 2
+BKFAC_GEMM_TCGEN05 = 0
+BKFAC_GEMM_SIMT = 1
 
 STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKFAC_ERR_RANK",
           4: "BKFAC_ERR_ALIAS", 5: "BKFAC_ERR_WORKSPACE", 6: "BKFAC_ERR_CUDA",
@@ -29,7 +31,7 @@ EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac
             "bkfac_rsvd_overwrite", "bkfac_rsvd_overwrite_batch",
             "bkfac_precondition", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
             "bkfac_profile_enable", "bkfac_profile_read", "bkfac_status_string",
-            "bkfac_build_info"]
+            "bkfac_build_info", "bkfac_gemm"]
 
 
 class BkfacError(RuntimeError):
@@ -127,6 +129,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.bkfac_status_string.restype = ctypes.c_char_p
     lib.bkfac_build_info.argtypes = []
     lib.bkfac_build_info.restype = ctypes.c_char_p
+    lib.bkfac_gemm.argtypes = [ci, ci, ci, ci, ci, cf, vp, ci, vp, ci, cf, vp, ci, vp, sz, ci, vp]
+    lib.bkfac_gemm.restype = ci
     _lib = lib
     return lib
 
@@ -263,6 +267,21 @@ def bkfac_gaussian_sketch(Omega, seed: int, counter: int, stream=None) -> None:
     l, n = Omega.shape
     _check(load().bkfac_gaussian_sketch(_ptr(Omega), n, l, seed, counter, _stream_ptr(stream)),
            "bkfac_gaussian_sketch")
+
+
+def bkfac_gemm(transA: bool, transB: bool, alpha: float, A, B, beta: float, C, ws=None,
+               path: int = BKFAC_GEMM_TCGEN05, stream=None) -> None:
+    """C = alpha op(A) op(B) + beta C in BLAS col-major terms.  Tensors are PyTorch
+    row-major, so a (cols, rows) tensor is a col-major rows x cols matrix:
+    C has shape (N, M); A has shape (K, M) (or (M, K) if transA); B has shape (N, K)
+    (or (K, N) if transB)."""
+    N, M = C.shape
+    K = A.shape[1] if transA else A.shape[0]
+    lda, ldb, ldc = A.shape[1], B.shape[1], C.shape[1]
+    wsb = 0 if ws is None else ws.numel() * ws.element_size()
+    _check(load().bkfac_gemm(int(transA), int(transB), M, N, K, alpha, _ptr(A), lda, _ptr(B), ldb,
+                             beta, _ptr(C), ldc, _ptr(ws), wsb, path, _stream_ptr(stream)),
+           "bkfac_gemm")
 
 
 def bkfac_status_string(code: int) -> str:

@@ -179,7 +179,7 @@ GemmProb gp(const float* A, int lda, const float* B, int ldb, float* C, int ldc,
 }
 
 template <bool TA, bool TB>
-bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_t st) {
+bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_t st, bool tc) {
   size_t i0 = 0;
   while (i0 < v.size()) {
     const size_t n = std::min(v.size() - i0, (size_t)GEMM_MAXP);
@@ -196,7 +196,12 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
     }
     b.total_tiles = tiles;
     if (tiles > 0) {
-      gemm_simt_kernel<TA, TB><<<tiles, 256, 0, st>>>(b);
+      if (tc) {
+        const int grid = std::min(tiles, kNumSM);
+        gemm_tc_kernel<TA, TB, 128><<<grid, TC_THREADS, TcCfg<128>::SMEM_BYTES, st>>>(b);
+      } else {
+        gemm_simt_kernel<TA, TB><<<tiles, 256, 0, st>>>(b);
+      }
       LAUNCH_CHECK(ctx);
       if (any_split) {
         gemm_splitk_reduce_kernel<<<dim3(64, (unsigned)n), 256, 0, st>>>(b);
@@ -223,26 +228,46 @@ bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char*
   return rr;
 }
 
+// Split-K planning.  SIMT: K units, 64x64 tiles.  tcgen05: 32-wide K chunks, 128 x 128
+// tiles, one persistent CTA per SM.  Splits only when a stage has fewer tiles than the
+// machine has SMs (x2 for SIMT); the reduction order is fixed (deterministic).
 bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
-  // split-K: aim for ~2 waves of CTAs over the whole stage
+  const bool tc = ctx->use_tc;
+  const int bm = tc ? TC_BM : SG_BM, bn = tc ? 128 : SG_BN;
   long base_tiles = 0;
   for (int v = 0; v < 4; ++v)
     for (auto& p : s.probs[v]) {
-      p.tiles_m = ceil_div(std::max(p.M, 1), SG_BM);
-      p.tiles_n = ceil_div(std::max(p.N, 1), SG_BN);
+      p.tiles_m = ceil_div(std::max(p.M, 1), bm);
+      p.tiles_n = ceil_div(std::max(p.N, 1), bn);
       if (p.M <= 0 || p.N <= 0) p.tiles_m = p.tiles_n = 0;
       base_tiles += (long)p.tiles_m * p.tiles_n;
     }
-  const long target = 2L * kNumSM;
+  const long target = tc ? (long)kNumSM : 2L * kNumSM;
   for (int v = 0; v < 4; ++v)
     for (size_t i = 0; i < s.probs[v].size(); ++i) {
       GemmProb& p = s.probs[v][i];
+      const long mn = (long)p.M * p.N;
+      const long cap = (p.ws != nullptr && mn > 0) ? s.caps[v][i] / mn : 1;
+      if (tc) {
+        const int nc = ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK);
+        int splits = 1;
+        if (nc >= 8 && base_tiles > 0 && base_tiles < target && p.ws != nullptr) {
+          splits = (int)std::min<long>(kSplitMax, (target + base_tiles - 1) / base_tiles);
+          splits = std::min(splits, nc / 4);
+          splits = (int)std::min<long>(splits, cap);
+          splits = std::max(splits, 1);
+        }
+        int cps = std::max(ceil_div(nc, splits), 1);
+        splits = std::max(ceil_div(nc, cps), 1);
+        p.splits = splits;
+        p.kchunk = cps;
+        continue;
+      }
       int splits = 1;
       if (p.K >= 1024 && base_tiles > 0 && base_tiles < target && p.ws != nullptr) {
         splits = (int)std::min<long>(kSplitMax, (target + base_tiles - 1) / base_tiles);
         splits = std::min(splits, p.K / 256);
-        const long mn = (long)p.M * p.N;
-        if (mn > 0) splits = (int)std::min<long>(splits, s.caps[v][i] / mn);
+        splits = (int)std::min<long>(splits, cap);
         splits = std::max(splits, 1);
       }
       int kchunk = p.K;
@@ -255,10 +280,10 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       p.kchunk = std::max(kchunk, 1);
     }
   bkfac_status r;
-  if ((r = launch_variant<false, false>(ctx, s.probs[0], st)) != BKFAC_OK) return r;
-  if ((r = launch_variant<false, true>(ctx, s.probs[1], st)) != BKFAC_OK) return r;
-  if ((r = launch_variant<true, false>(ctx, s.probs[2], st)) != BKFAC_OK) return r;
-  if ((r = launch_variant<true, true>(ctx, s.probs[3], st)) != BKFAC_OK) return r;
+  if ((r = launch_variant<false, false>(ctx, s.probs[0], st, tc)) != BKFAC_OK) return r;
+  if ((r = launch_variant<false, true>(ctx, s.probs[1], st, tc)) != BKFAC_OK) return r;
+  if ((r = launch_variant<true, false>(ctx, s.probs[2], st, tc)) != BKFAC_OK) return r;
+  if ((r = launch_variant<true, true>(ctx, s.probs[3], st, tc)) != BKFAC_OK) return r;
   for (int v = 0; v < 4; ++v) { s.probs[v].clear(); s.caps[v].clear(); }
   return BKFAC_OK;
 }
@@ -875,28 +900,33 @@ bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* ar
   GemmStage gs;
   std::vector<CholProb> ch;
   std::vector<EigProb> eg;
+  std::vector<EwProb> ew;
   bkfac_status rs;
   struct Loc { int n, r, l; int* status; float *Y, *Q, *Q2, *T, *ws; const FactorPlan* fp; };
   std::vector<Loc> L(count);
+  // sketch width l = n: the range is all of R^n, Q = I and the RSVD is the exact EVD of
+  // K (Alg 5 with nothing to sketch); those factors skip the range finder entirely.
+  std::vector<int> rf, exact;
   for (int i = 0; i < count; ++i) {
     const auto& fp = ctx->f[args[i].factor];
     L[i] = Loc{fp.d.n, fp.d.r, fp.d.r + args[i].oversample, status_ptr(ctx, args[i].factor),
                at<float>(ctx, fp.Yr), at<float>(ctx, fp.Qr), at<float>(ctx, fp.Q2r),
                at<float>(ctx, fp.Tr), at<float>(ctx, fp.ws_r), &fp};
+    (L[i].l == L[i].n ? exact : rf).push_back(i);
   }
   // Omega -> Q (Philox sketch); Y = K Omega
   {
     double bytes = 0.0;
-    for (auto& x : L) bytes += 4.0 * x.n * (double)x.l;
+    for (int i : rf) bytes += 4.0 * L[i].n * (double)L[i].l;
     prof_begin(ctx, "rsvd_sketch", st, 0.0, bytes);
-    for (int i = 0; i < count; ++i) {
+    for (int i : rf) {
       philox_sketch_kernel<<<256, 256, 0, st>>>(L[i].Q, (long)L[i].n * L[i].l, args[i].seed,
                                                args[i].counter);
       LAUNCH_CHECK(ctx);
     }
     prof_end(ctx, st);
   }
-  for (int i = 0; i < count; ++i)
+  for (int i : rf)
     gs.add(false, false, gp(args[i].K_dense, L[i].n, L[i].Q, L[i].n, L[i].Y, L[i].n, L[i].n, L[i].l,
                             L[i].n, 1.f), 0);
   if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
@@ -931,36 +961,43 @@ bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* ar
   // note: pass 0 reads Y and writes Q, so X and Qout never alias
   for (int q = 0; q < qmax; ++q) {
     std::vector<int> act;
-    for (int i = 0; i < count; ++i)
+    for (int i : rf)
       if (q < args[i].power_iters) act.push_back(i);
+    if (act.empty()) continue;
     if ((rs = orth(act, true)) != BKFAC_OK) return rs;
     for (int i : act)
       gs.add(false, false, gp(args[i].K_dense, L[i].n, L[i].Q, L[i].n, L[i].Y, L[i].n, L[i].n,
                               L[i].l, L[i].n, 1.f), 0);
     if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
   }
-  {
-    std::vector<int> all(count);
-    for (int i = 0; i < count; ++i) all[i] = i;
-    if ((rs = orth(all, true)) != BKFAC_OK) return rs;
-  }
+  if (!rf.empty() && (rs = orth(rf, true)) != BKFAC_OK) return rs;
   // B = Q^T K Q ; EVD(B) ; U = Q V_r
-  for (int i = 0; i < count; ++i)
+  for (int i : rf)
     gs.add(false, false, gp(args[i].K_dense, L[i].n, L[i].Q, L[i].n, L[i].T, L[i].n, L[i].n, L[i].l,
                             L[i].n, 1.f), 0);
   if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
-  for (int i = 0; i < count; ++i) {
+  for (int i : rf) {
     GemmProb p = gp(L[i].Q, L[i].n, L[i].T, L[i].n, at<float>(ctx, L[i].fp->eig_r.K), L[i].l, L[i].l,
                     L[i].l, L[i].n, 1.f);
     gemm_ws(p, L[i].ws);
     gs.add(true, false, p, L[i].fp->ws_r_elems);
   }
   if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_proj")) != BKFAC_OK) return rs;
-  for (int i = 0; i < count; ++i)
-    eg.push_back(eig_prob(ctx, L[i].fp->eig_r, L[i].l, L[i].r, at<float>(ctx, L[i].fp->eig_r.V),
-                          L[i].l, args[i].D_out, L[i].status));
+  for (int i : exact) {   // B = K itself
+    EwProb e{};
+    e.Y = at<float>(ctx, L[i].fp->eig_r.K); e.ldy = L[i].n; e.X = args[i].K_dense; e.ldx = L[i].n;
+    e.rows = L[i].n; e.cols = L[i].n; e.op = EW_COPY;
+    ew.push_back(e);
+  }
+  if (!ew.empty() && (rs = run_ew(ctx, ew, st, "ew_rsvd_exact")) != BKFAC_OK) return rs;
+  for (int i = 0; i < count; ++i) {
+    const bool ex = L[i].l == L[i].n;
+    eg.push_back(eig_prob(ctx, L[i].fp->eig_r, L[i].l, L[i].r,
+                          ex ? args[i].U_out : at<float>(ctx, L[i].fp->eig_r.V),
+                          ex ? L[i].n : L[i].l, args[i].D_out, L[i].status));
+  }
   if ((rs = run_eig(ctx, eg, st)) != BKFAC_OK) return rs;
-  for (int i = 0; i < count; ++i)
+  for (int i : rf)
     gs.add(false, false, gp(L[i].Q, L[i].n, at<float>(ctx, L[i].fp->eig_r.V), L[i].l, args[i].U_out,
                             L[i].n, L[i].n, L[i].r, L[i].l, 1.f), 0);
   return run_gemms(ctx, gs, st, "gemm_rsvd_rot");
@@ -1098,6 +1135,28 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     gs.add(false, true, p, 0);
   }
   return run_gemms(ctx, gs, st, "gemm_prec_out");
+}
+
+// ------------------------------------------------------------------------- GEMM primitive
+bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha, const float* A,
+                        int lda, const float* B, int ldb, float beta, float* C, int ldc, float* ws,
+                        size_t ws_bytes, int path, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || !C || (K > 0 && (!A || !B))) return BKFAC_ERR_INVALID_ARG;
+  if (path != BKFAC_GEMM_TCGEN05 && path != BKFAC_GEMM_SIMT) return BKFAC_ERR_INVALID_ARG;
+  if (ldc < std::max(M, 1) || lda < 1 || ldb < 1) return BKFAC_ERR_DIM;
+  if (M == 0 || N == 0) return BKFAC_OK;
+  bkfac_ctx_s tmp;   // launch bookkeeping only; no workspace
+  tmp.use_tc = path == BKFAC_GEMM_TCGEN05;
+  if (tmp.use_tc) {
+    static bool attrs = false;
+    if (!attrs) { attrs = tc_init_attributes(); cudaGetLastError(); }
+  }
+  GemmStage gs;
+  GemmProb p = gp(A, lda, B, ldb, C, ldc, M, N, K, alpha, C, ldc, beta);
+  const long cap = ws ? (long)(ws_bytes / sizeof(float)) : 0;
+  if (ws && cap > 0) gemm_ws(p, ws);
+  gs.add(transA != 0, transB != 0, p, cap);
+  return run_gemms(&tmp, gs, static_cast<cudaStream_t>(stream), "gemm_user");
 }
 
 // ------------------------------------------------------------------------- check

@@ -1,6 +1,479 @@
-// tcgen05 3xTF32 GEMM (placeholder until the kernel lands).
+// Grouped fp32-accurate GEMM on the 5th-generation tensor cores (tcgen05, sm_100a):
+// 3xTF32 splitting, operands staged in swizzled shared memory, accumulators in TMEM.
+//
+// Same problem description as gemm_simt.cuh (GemmProb / GemmBatch, BLAS col-major,
+// optional second K segment, deterministic split-K through the same reduce kernel):
+//     C = alpha * op(A) op(B) + beta * C0
+//
+// Why 3xTF32 (SURVEY §8(c) survey probe; BASELINE north_star): every contraction of the
+// Brand update, the RSVD and the preconditioner must meet fp32 tolerances; single-pass
+// TF32 fails them.  Each fp32 operand x is split as x = hi + lo with hi = rna_tf32(x),
+// lo = x - hi (exact in fp32) and the product is accumulated in fp32 TMEM as
+//     hi_A hi_B + hi_A lo_B + lo_A hi_B       (the lo_A lo_B term is O(2^-22)).
+//
+// Accumulator promotion.  The tensor core's fp32 accumulate is not round-to-nearest: a
+// measured 3xTF32 product with K = 4609 drifted by 3.2e-5 relative (error linear in K,
+// i.e. a bias, 25x the SIMT fp32 kernel).  So the MMA accumulates only TC_PROMO chunks
+// (TC_PROMO * 32 of K) into a TMEM buffer; the epilogue warps add each such block into a
+// running sum (fp32 FADD, round-to-nearest; the running sum itself lives in a third TMEM
+// region, tcgen05.ld/st) while the MMA fills the other buffer.  The bias is then bounded
+// by one block's length instead of K.
+//
+// Kernel anatomy (one CTA per SM, persistent over the tiles of all problems):
+//   warps 0-3  epilogue: thread = tile row = TMEM lane; promotes each K-block into the
+//              running sum, then alpha/beta and stores coalesced along M (the contiguous
+//              dimension of col-major C)
+//   warp  4    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 5-12 loaders: coalesced global loads of 128-byte lines (32 fp32 along the
+//              contiguous dimension of the operand), hi/lo split in registers, stores of
+//              both halves into the 128B-swizzled canonical UMMA layouts.  A line is a
+//              K-run of one row for a K-major operand (A transposed, B not transposed)
+//              and an MN-run of one k for an MN-major operand; tcgen05 reads either major
+//              order for kind::tf32, so no operand is ever transposed.
+//   Loaders keep the next chunk's loads in flight while they split and store the current
+//   one.  Loaders and the MMA warp hand shared-memory stages over with mbarriers
+//   (full: 8 loader warps arrive after fence.proxy.async; empty: tcgen05.commit);
+//   the MMA warp and the epilogue hand the two TMEM block buffers over with a second pair.
+//
+// Why loaders instead of TMA: the leading dimensions on this path are odd (n = 4609,
+// 4097, 16385, d_A = 4097 ...), which cuTensorMapEncodeTiled cannot describe (global
+// strides must be multiples of 16 bytes), and the split pass has to touch every element
+// in registers anyway.  Loading straight from global into the split registers costs one
+// shared-memory write per half instead of TMA write + read + write.
 #pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "gemm_simt.cuh"
+
 namespace bkfac {
-inline bool tc_init_attributes() { return true; }
-#define BKFAC_GEMM_PATH "SIMT fp32 (CUDA cores)"
+
+#define BKFAC_GEMM_PATH "tcgen05 kind::tf32 3xTF32 (TMEM accumulators, mbarrier pipeline)"
+
+constexpr int TC_BM = 128;            // UMMA M (TMEM lanes)
+constexpr int TC_BK = 32;             // one 128-byte swizzle line of fp32
+constexpr int TC_EPI_WARPS = 4;
+constexpr int TC_MMA_WARP = 4;
+constexpr int TC_LOAD_WARPS = 8;
+constexpr int TC_PROMO = 2;           // K chunks accumulated in TMEM before promotion
+constexpr int TC_THREADS = (TC_EPI_WARPS + 1 + TC_LOAD_WARPS) * 32;
+
+template <int BN>
+struct TcCfg {
+  static constexpr int A_BYTES = TC_BM * TC_BK * 4;          // one half (hi or lo)
+  static constexpr int B_BYTES = BN * TC_BK * 4;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = (BN >= 256) ? 2 : 3;
+  static constexpr int TMEM_COLS = 4 * BN;                   // 2 K-block buffers + running sum
+  static constexpr int LINES = TC_BM + BN;                   // 128-byte lines per stage half
+  static constexpr int LPW = LINES / TC_LOAD_WARPS;          // lines per loader warp
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// ----------------------------------------------------------------------- PTX helpers
+BKFAC_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+BKFAC_DEV void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+BKFAC_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+BKFAC_DEV void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+BKFAC_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+BKFAC_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+BKFAC_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+BKFAC_DEV void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+BKFAC_DEV void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+BKFAC_DEV float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// 32 consecutive fp32 TMEM columns of this thread's lane
+BKFAC_DEV void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 16 consecutive fp32 TMEM columns of this thread's lane
+BKFAC_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+BKFAC_DEV void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// UMMA shared-memory descriptor (SM100 "version 1").  layout: 2 = SWIZZLE_128B (K-major
+// operands: 8 rows x 128 B atoms, 16-byte chunks XOR row%8), 1 = SWIZZLE_128B_BASE32B
+// (MN-major tf32 operands -- the only MN-major layout kind::tf32 accepts: 4 k-rows x 128 B
+// atoms, 32-byte chunks XOR k%4).
+BKFAC_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // version (sm_100)
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+// Byte offset of element e (0..31) of 128-byte line l inside one operand buffer of R
+// MN-rows.  K-major: line = MN row (32 consecutive k).  MN-major: line = (k-line kk,
+// MN atom a) with l = a*32 + kk (32 consecutive MN indices at fixed k).
+template <bool MN, int R>
+BKFAC_DEV uint32_t tc_line_off(int l, int e) {
+  if (!MN) return l * 128u + (((uint32_t)(e >> 2) ^ (uint32_t)(l & 7)) << 4) + ((e & 3) << 2);
+  const int kk = l & 31, a = l >> 5;
+  return (uint32_t)(kk >> 2) * (uint32_t)(R / 32 * 512) + a * 512u + (kk & 3) * 128u +
+         (((uint32_t)(e >> 3) ^ (uint32_t)(kk & 3)) << 5) + ((e & 7) << 2);
+}
+// Descriptor of k-step ks (8 k = one tf32 MMA) of an operand buffer at saddr.
+template <bool MN, int R>
+BKFAC_DEV uint64_t tc_op_desc(uint32_t saddr, int ks) {
+  if (!MN) return umma_desc(saddr + ks * 32u, 16u, 1024u, 2u);
+  return umma_desc(saddr + ks * 2u * (R / 32 * 512), 512u, R / 32 * 512, 1u);
+}
+// Instruction descriptor: kind::tf32, fp32 accumulate, M = 128, N = BN.
+template <int BN>
+BKFAC_DEV constexpr uint32_t umma_idesc_tf32(bool a_mn_major, bool b_mn_major) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn_major ? 1u : 0u) << 15) |
+         ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(TC_BM >> 4) << 24);
+}
+
+// ----------------------------------------------------------------------- tile walk
+struct TcTile {
+  int pi, m0, n0, split, c_beg, c_end, nc1;
+};
+
+BKFAC_DEV int tc_find_prob(const GemmBatch& b, int t) {
+  int lo = 0, hi = b.nprob - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (b.p[mid].tile_start <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int BN>
+BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
+  TcTile x;
+  x.pi = tc_find_prob(b, t);
+  const GemmProb& p = b.p[x.pi];
+  const int lt = t - p.tile_start;
+  const int per_split = p.tiles_m * p.tiles_n;
+  x.split = lt / per_split;
+  const int rem = lt - x.split * per_split;
+  x.m0 = (rem % p.tiles_m) * TC_BM;
+  x.n0 = (rem / p.tiles_m) * BN;
+  x.nc1 = (p.k1 + TC_BK - 1) / TC_BK;
+  const int nc = x.nc1 + (p.K - p.k1 + TC_BK - 1) / TC_BK;
+  x.c_beg = min(nc, x.split * p.kchunk);     // kchunk = chunks per split on this path
+  x.c_end = min(nc, x.c_beg + p.kchunk);
+  return x;
+}
+
+// ----------------------------------------------------------------------- kernel
+template <bool TA, bool TB, int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
+  using Cfg = TcCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  // bars: full[S], empty[S], tfull[2], tempty[2]; then the TMEM base address
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = smem_u32(bars);
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (Cfg::STAGES + s); };
+  auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + a); };
+  auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + 2 + a); };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == TC_MMA_WARP) {
+    if (lane == 0) {
+      for (int s = 0; s < Cfg::STAGES; ++s) {
+        mbar_init(full_bar(s), TC_LOAD_WARPS);
+        mbar_init(empty_bar(s), 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(tfull_bar(a), 1);
+        mbar_init(tempty_bar(a), TC_EPI_WARPS);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == TC_MMA_WARP) {
+    // ------------------------------------------------------------- MMA issuer
+    constexpr uint32_t IDESC = umma_idesc_tf32<BN>(!TA, TB);
+    int stage = 0; uint32_t phase = 0;
+    int kb = 0;   // K-block counter over all tiles of this CTA (TMEM buffer = kb & 1)
+    for (int t = blockIdx.x; t < b.total_tiles; t += gridDim.x) {
+      const TcTile x = tc_tile<BN>(b, t);
+      for (int c0 = x.c_beg; c0 < x.c_end; c0 += TC_PROMO, ++kb) {
+        const int buf = kb & 1;
+        mbar_wait(tempty_bar(buf), ((kb >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
+        const int c1 = min(x.c_end, c0 + TC_PROMO);
+        for (int c = c0; c < c1; ++c) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sA = sbase + stage * Cfg::STAGE_BYTES;
+            const uint32_t sAlo = sA + Cfg::A_BYTES;
+            const uint32_t sB = sA + 2 * Cfg::A_BYTES;
+            const uint32_t sBlo = sB + Cfg::B_BYTES;
+#pragma unroll
+            for (int ks = 0; ks < TC_BK / 8; ++ks) {
+              const uint64_t aH = tc_op_desc<!TA, TC_BM>(sA, ks);
+              const uint64_t aL = tc_op_desc<!TA, TC_BM>(sAlo, ks);
+              const uint64_t bH = tc_op_desc<TB, BN>(sB, ks);
+              const uint64_t bL = tc_op_desc<TB, BN>(sBlo, ks);
+              const uint32_t first = (c == c0 && ks == 0) ? 0u : 1u;
+              tc_mma_tf32(tmem_d, aL, bH, IDESC, first);   // small terms first
+              tc_mma_tf32(tmem_d, aH, bL, IDESC, 1u);
+              tc_mma_tf32(tmem_d, aH, bH, IDESC, 1u);
+            }
+            tc_commit(empty_bar(stage));
+          }
+          __syncwarp();
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) tc_commit(tfull_bar(buf));
+        __syncwarp();
+      }
+    }
+  } else if (warp > TC_MMA_WARP) {
+    // ------------------------------------------------------------- loaders
+    const int lw = warp - TC_MMA_WARP - 1;
+    int stage = 0; uint32_t phase = 0;
+    // the (tile, chunk) sequence of this CTA, walked one step ahead of the stores
+    int t = blockIdx.x, c = 0;
+    TcTile x;
+    auto seek = [&]() {   // advance (t, c) to the next existing chunk; false when done
+      while (t < b.total_tiles) {
+        if (c == 0) { x = tc_tile<BN>(b, t); c = x.c_beg; }
+        if (c < x.c_end) return true;
+        t += gridDim.x; c = 0;
+      }
+      return false;
+    };
+    auto load = [&](float (&v)[Cfg::LPW]) {
+      const GemmProb& p = b.p[x.pi];
+      const int seg = c < x.nc1 ? 0 : 1;
+      const int ks = (seg ? c - x.nc1 : c) * TC_BK;
+      const int klen = seg ? p.K - p.k1 : p.k1;
+      const float* Ap = seg ? p.A2 : p.A;
+      const float* Bp = seg ? p.B2 : p.B;
+      const long lda = seg ? p.lda2 : p.lda;
+      const long ldb = seg ? p.ldb2 : p.ldb;
+#pragma unroll
+      for (int q = 0; q < Cfg::LPW; ++q) {
+        const int l = lw + q * TC_LOAD_WARPS;
+        float val = 0.f;
+        if (l < TC_BM) {
+          if (TA) {            // K-major line: row m0+l, k = ks + lane
+            const int i = x.m0 + l, k = ks + lane;
+            if (i < p.M && k < klen) val = __ldg(Ap + k + (long)i * lda);
+          } else {             // MN-major line: k = ks + (l & 31), rows m0 + 32*(l>>5) + lane
+            const int k = ks + (l & 31), i = x.m0 + ((l >> 5) << 5) + lane;
+            if (i < p.M && k < klen) val = __ldg(Ap + i + (long)k * lda);
+          }
+        } else {
+          const int lb = l - TC_BM;
+          if (!TB) {           // K-major line: column n0+lb, k = ks + lane
+            const int j = x.n0 + lb, k = ks + lane;
+            if (j < p.N && k < klen) val = __ldg(Bp + k + (long)j * ldb);
+          } else {             // MN-major line: k = ks + (lb & 31), cols n0 + 32*(lb>>5) + lane
+            const int k = ks + (lb & 31), j = x.n0 + ((lb >> 5) << 5) + lane;
+            if (j < p.N && k < klen) val = __ldg(Bp + j + (long)k * ldb);
+          }
+        }
+        v[q] = val;
+      }
+    };
+    auto store = [&](const float (&v)[Cfg::LPW]) {
+      mbar_wait(empty_bar(stage), phase ^ 1);
+      uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
+#pragma unroll
+      for (int q = 0; q < Cfg::LPW; ++q) {
+        const int l = lw + q * TC_LOAD_WARPS;
+        const float hi = tf32_rna(v[q]);
+        const float lo = v[q] - hi;
+        uint32_t off;
+        uint8_t *dh, *dl;
+        if (l < TC_BM) {
+          off = tc_line_off<!TA, TC_BM>(l, lane);
+          dh = st; dl = st + Cfg::A_BYTES;
+        } else {
+          off = tc_line_off<TB, BN>(l - TC_BM, lane);
+          dh = st + 2 * Cfg::A_BYTES; dl = dh + Cfg::B_BYTES;
+        }
+        *reinterpret_cast<float*>(dh + off) = hi;
+        *reinterpret_cast<float*>(dl + off) = lo;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full_bar(stage));
+      if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+    };
+    float va[Cfg::LPW], vb[Cfg::LPW];
+    bool have = seek();
+    if (have) { load(va); ++c; }
+    while (have) {
+      const bool more = seek();
+      if (more) { load(vb); ++c; }
+      store(va);
+      if (!more) break;
+      const bool more2 = seek();
+      if (more2) { load(va); ++c; }
+      store(vb);
+      have = more2;
+    }
+  } else {
+    // ------------------------------------------------------------- epilogue
+    const int row = warp * 32 + lane;                         // TMEM lane = tile row
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t run = tmem_base + lane_off + 2 * BN;       // running-sum columns
+    int kb = 0;
+    for (int t = blockIdx.x; t < b.total_tiles; t += gridDim.x) {
+      const TcTile x = tc_tile<BN>(b, t);
+      const GemmProb& p = b.p[x.pi];
+      const int nblk = (x.c_end - x.c_beg + TC_PROMO - 1) / TC_PROMO;
+      const int i = x.m0 + row;
+      const float beta = p.beta_dev ? *p.beta_dev : p.beta;
+      float* w = p.splits > 1 ? p.ws + (long)x.split * p.M * p.N : nullptr;
+      for (int blk = 0; blk < nblk; ++blk, ++kb) {
+        const int buf = kb & 1;
+        const bool last = blk == nblk - 1;
+        mbar_wait(tfull_bar(buf), (kb >> 1) & 1);
+        tc_fence_after();
+        const uint32_t src = tmem_base + lane_off + (uint32_t)(buf * BN);
+#pragma unroll 1
+        for (int g = 0; g < BN / 16; ++g) {
+          if (last && x.n0 + g * 16 >= p.N) break;      // warp-uniform
+          float v[16];
+          tmem_ld16(src + g * 16, v);
+          if (blk > 0) {
+            float r[16];
+            tmem_ld16(run + g * 16, r);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] += r[j];
+          }
+          if (!last) {
+            tmem_st16(run + g * 16, v);
+          } else if (i < p.M) {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int j = x.n0 + g * 16 + jj;
+              if (j < p.N) {
+                if (w) {
+                  w[i + (long)j * p.M] = v[jj];
+                } else {
+                  float o = p.alpha * v[jj];
+                  if (beta != 0.f) o += beta * p.C0[i + (long)j * p.ldc0];
+                  p.C[i + (long)j * p.ldc] = o;
+                }
+              }
+            }
+          }
+        }
+        if (!last) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_bar(buf));
+      }
+      if (nblk == 0 && i < p.M) {     // empty K range (split beyond K or K = 0)
+        for (int j = x.n0; j < min(p.N, x.n0 + BN); ++j) {
+          if (w) {
+            w[i + (long)j * p.M] = 0.f;
+          } else {
+            float o = 0.f;
+            if (beta != 0.f) o += beta * p.C0[i + (long)j * p.ldc0];
+            p.C[i + (long)j * p.ldc] = o;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == TC_MMA_WARP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)Cfg::TMEM_COLS));
+  }
+}
+
+template <bool TA, bool TB, int BN>
+inline bool tc_set_attr() {
+  return cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              TcCfg<BN>::SMEM_BYTES) == cudaSuccess;
+}
+
+inline bool tc_init_attributes() {
+  bool ok = true;
+  ok &= tc_set_attr<false, false, 128>();
+  ok &= tc_set_attr<false, true, 128>();
+  ok &= tc_set_attr<true, false, 128>();
+  ok &= tc_set_attr<true, true, 128>();
+  return ok;
+}
+
+}  // namespace bkfac
