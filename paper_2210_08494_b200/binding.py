@@ -84,11 +84,13 @@ class PrecondArgs(ctypes.Structure):
 _lib = None
 
 
-def load(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load libbkfac.so.  Raises loudly if it is missing: there is no fallback path."""
+def load(path: str = None) -> ctypes.CDLL:
+    """Load libbkfac.so.  Raises loudly if it is missing: there is no fallback path.
+    ``BKFAC_LIB`` may point at another in-tree build of the same library (tuning runs)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("BKFAC_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"bkfac CUDA library not built: {path} is missing "
                            "(run `python -c 'import __graft_entry__ as g; g.build()'`)")

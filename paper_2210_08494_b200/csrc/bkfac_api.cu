@@ -198,7 +198,7 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
     if (tiles > 0) {
       if (tc) {
         const int grid = std::min(tiles, kNumSM);
-        gemm_tc_kernel<TA, TB, 128><<<grid, TC_THREADS, TcCfg<128>::SMEM_BYTES, st>>>(b);
+        tc_launch<TA, TB>(b, grid, st);
       } else {
         gemm_simt_kernel<TA, TB><<<tiles, 256, 0, st>>>(b);
       }
@@ -233,7 +233,7 @@ bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char*
 // machine has SMs (x2 for SIMT); the reduction order is fixed (deterministic).
 bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
   const bool tc = ctx->use_tc;
-  const int bm = tc ? TC_BM : SG_BM, bn = tc ? 128 : SG_BN;
+  const int bm = tc ? TC_BM : SG_BM, bn = tc ? TC_BN : SG_BN;
   long base_tiles = 0;
   for (int v = 0; v < 4; ++v)
     for (auto& p : s.probs[v]) {

@@ -55,19 +55,34 @@ constexpr int TC_BM = 128;            // UMMA M (TMEM lanes)
 constexpr int TC_BK = 32;             // one 128-byte swizzle line of fp32
 constexpr int TC_EPI_WARPS = 4;
 constexpr int TC_MMA_WARP = 4;
-constexpr int TC_LOAD_WARPS = 8;
-constexpr int TC_PROMO = 2;           // K chunks accumulated in TMEM before promotion
-constexpr int TC_THREADS = (TC_EPI_WARPS + 1 + TC_LOAD_WARPS) * 32;
+#ifndef BKFAC_TC_PROMO
+#define BKFAC_TC_PROMO 4
+#endif
+#ifndef BKFAC_TC_NLW
+#define BKFAC_TC_NLW 16
+#endif
+#ifndef BKFAC_TC_DEPTH
+#define BKFAC_TC_DEPTH 1
+#endif
+#ifdef BKFAC_TC_DEBUG_NOLOAD          // tuning only: loaders skip global memory
+#define TC_LDG(ptr) (1.0f + (float)lane)
+#else
+#define TC_LDG(ptr) __ldg(ptr)
+#endif
+constexpr int TC_PROMO = BKFAC_TC_PROMO;   // K chunks accumulated in TMEM before promotion
 
-template <int BN>
+// NLW loader warps, each keeping DEPTH chunks of loads in flight ahead of its stores.
+template <int BN, int NLW = 16, int DEPTH = 2>
 struct TcCfg {
+  static constexpr int LOAD_WARPS = NLW;
+  static constexpr int THREADS = (TC_EPI_WARPS + 1 + NLW) * 32;
   static constexpr int A_BYTES = TC_BM * TC_BK * 4;          // one half (hi or lo)
   static constexpr int B_BYTES = BN * TC_BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = (BN >= 256) ? 2 : 3;
   static constexpr int TMEM_COLS = 4 * BN;                   // 2 K-block buffers + running sum
   static constexpr int LINES = TC_BM + BN;                   // 128-byte lines per stage half
-  static constexpr int LPW = LINES / TC_LOAD_WARPS;          // lines per loader warp
+  static constexpr int LPW = LINES / NLW;                    // lines per loader warp
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -90,6 +105,21 @@ BKFAC_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
 BKFAC_DEV void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// Waiter that does not need to react within tens of cycles (the epilogue): the thread is
+// suspended until the phase completes or ~the hint (ns) elapses instead of spinning, so
+// it does not steal issue slots from the loader warps.
+BKFAC_DEV void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAITS_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+BKFAC_DEV void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v));
+}
 BKFAC_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 BKFAC_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 BKFAC_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -105,6 +135,11 @@ BKFAC_DEV void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+// Round to the nearest tf32 (ties away from zero) in two integer ops; non-finite values
+// stay non-finite (NaN stays NaN, +-inf stays +-inf) so status checks still see them.
+BKFAC_DEV float tf32_round(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 BKFAC_DEV float tf32_rna(float x) {
   uint32_t r;
@@ -220,9 +255,11 @@ BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
 }
 
 // ----------------------------------------------------------------------- kernel
-template <bool TA, bool TB, int BN>
-__global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
-  using Cfg = TcCfg<BN>;
+template <bool TA, bool TB, int BN, int NLW, int DEPTH>
+__global__ void __launch_bounds__(TcCfg<BN, NLW, DEPTH>::THREADS, 1)
+gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
+  using Cfg = TcCfg<BN, NLW, DEPTH>;
+  constexpr int TC_LOAD_WARPS = NLW;
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -286,9 +323,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
               const uint64_t bH = tc_op_desc<TB, BN>(sB, ks);
               const uint64_t bL = tc_op_desc<TB, BN>(sBlo, ks);
               const uint32_t first = (c == c0 && ks == 0) ? 0u : 1u;
+#ifndef BKFAC_TC_DEBUG_ONEPASS
               tc_mma_tf32(tmem_d, aL, bH, IDESC, first);   // small terms first
               tc_mma_tf32(tmem_d, aH, bL, IDESC, 1u);
               tc_mma_tf32(tmem_d, aH, bH, IDESC, 1u);
+#else                                     // tuning only: 1xTF32 (MMA-rate probe)
+              tc_mma_tf32(tmem_d, aH, bH, IDESC, first);
+#endif
             }
             tc_commit(empty_bar(stage));
           }
@@ -330,19 +371,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         if (l < TC_BM) {
           if (TA) {            // K-major line: row m0+l, k = ks + lane
             const int i = x.m0 + l, k = ks + lane;
-            if (i < p.M && k < klen) val = __ldg(Ap + k + (long)i * lda);
+            if (i < p.M && k < klen) val = TC_LDG(Ap + k + (long)i * lda);
           } else {             // MN-major line: k = ks + (l & 31), rows m0 + 32*(l>>5) + lane
             const int k = ks + (l & 31), i = x.m0 + ((l >> 5) << 5) + lane;
-            if (i < p.M && k < klen) val = __ldg(Ap + i + (long)k * lda);
+            if (i < p.M && k < klen) val = TC_LDG(Ap + i + (long)k * lda);
           }
         } else {
           const int lb = l - TC_BM;
           if (!TB) {           // K-major line: column n0+lb, k = ks + lane
             const int j = x.n0 + lb, k = ks + lane;
-            if (j < p.N && k < klen) val = __ldg(Bp + k + (long)j * ldb);
+            if (j < p.N && k < klen) val = TC_LDG(Bp + k + (long)j * ldb);
           } else {             // MN-major line: k = ks + (lb & 31), cols n0 + 32*(lb>>5) + lane
             const int k = ks + (lb & 31), j = x.n0 + ((lb >> 5) << 5) + lane;
-            if (j < p.N && k < klen) val = __ldg(Bp + j + (long)k * ldb);
+            if (j < p.N && k < klen) val = TC_LDG(Bp + j + (long)k * ldb);
           }
         }
         v[q] = val;
@@ -350,41 +391,63 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     };
     auto store = [&](const float (&v)[Cfg::LPW]) {
       mbar_wait(empty_bar(stage), phase ^ 1);
-      uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
+      const uint32_t st = sbase + stage * Cfg::STAGE_BYTES;
 #pragma unroll
       for (int q = 0; q < Cfg::LPW; ++q) {
         const int l = lw + q * TC_LOAD_WARPS;
-        const float hi = tf32_rna(v[q]);
+        const float hi = tf32_round(v[q]);
         const float lo = v[q] - hi;
-        uint32_t off;
-        uint8_t *dh, *dl;
+        uint32_t dh, dl;
         if (l < TC_BM) {
-          off = tc_line_off<!TA, TC_BM>(l, lane);
-          dh = st; dl = st + Cfg::A_BYTES;
+          dh = st + tc_line_off<!TA, TC_BM>(l, lane);
+          dl = dh + Cfg::A_BYTES;
         } else {
-          off = tc_line_off<TB, BN>(l - TC_BM, lane);
-          dh = st + 2 * Cfg::A_BYTES; dl = dh + Cfg::B_BYTES;
+          dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, lane);
+          dl = dh + Cfg::B_BYTES;
         }
-        *reinterpret_cast<float*>(dh + off) = hi;
-        *reinterpret_cast<float*>(dl + off) = lo;
+        sts_f32(dh, hi);
+        sts_f32(dl, lo);
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(full_bar(stage));
       if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
     };
-    float va[Cfg::LPW], vb[Cfg::LPW];
-    bool have = seek();
-    if (have) { load(va); ++c; }
-    while (have) {
-      const bool more = seek();
-      if (more) { load(vb); ++c; }
-      store(va);
-      if (!more) break;
-      const bool more2 = seek();
-      if (more2) { load(va); ++c; }
-      store(vb);
-      have = more2;
+    if constexpr (DEPTH == 1) {
+      float va[Cfg::LPW], vb[Cfg::LPW];
+      bool have = seek();
+      if (have) { load(va); ++c; }
+      while (have) {
+        const bool more = seek();
+        if (more) { load(vb); ++c; }
+        store(va);
+        if (!more) break;
+        const bool more2 = seek();
+        if (more2) { load(va); ++c; }
+        store(vb);
+        have = more2;
+      }
+    } else {
+      // three register buffers, two chunks of loads in flight while one is stored
+      float v0[Cfg::LPW], v1[Cfg::LPW], v2[Cfg::LPW];
+      bool h0 = seek();
+      if (h0) { load(v0); ++c; }
+      bool h1 = h0 && seek();
+      if (h1) { load(v1); ++c; }
+      while (h0) {
+        const bool h2 = h1 && seek();
+        if (h2) { load(v2); ++c; }
+        store(v0);
+        if (!h1) break;
+        const bool h3 = h2 && seek();
+        if (h3) { load(v0); ++c; }
+        store(v1);
+        if (!h2) break;
+        const bool h4 = h3 && seek();
+        if (h4) { load(v1); ++c; }
+        store(v2);
+        h0 = h3; h1 = h4;
+      }
     }
   } else {
     // ------------------------------------------------------------- epilogue
@@ -402,7 +465,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
       for (int blk = 0; blk < nblk; ++blk, ++kb) {
         const int buf = kb & 1;
         const bool last = blk == nblk - 1;
-        mbar_wait(tfull_bar(buf), (kb >> 1) & 1);
+        mbar_wait_sleep(tfull_bar(buf), (kb >> 1) & 1);
         tc_fence_after();
         const uint32_t src = tmem_base + lane_off + (uint32_t)(buf * BN);
 #pragma unroll 1
@@ -461,19 +524,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   }
 }
 
-template <bool TA, bool TB, int BN>
+// Launch configuration of the hot-path GEMM (BN = 128 tiles, 16 loader warps, two
+// chunks of loads in flight per loader).
+constexpr int TC_BN = 128, TC_NLW = BKFAC_TC_NLW, TC_DEPTH = BKFAC_TC_DEPTH;
+using TcMain = TcCfg<TC_BN, TC_NLW, TC_DEPTH>;
+
+template <bool TA, bool TB>
 inline bool tc_set_attr() {
-  return cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              TcCfg<BN>::SMEM_BYTES) == cudaSuccess;
+  return cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, TcMain::SMEM_BYTES) == cudaSuccess;
 }
 
 inline bool tc_init_attributes() {
   bool ok = true;
-  ok &= tc_set_attr<false, false, 128>();
-  ok &= tc_set_attr<false, true, 128>();
-  ok &= tc_set_attr<true, false, 128>();
-  ok &= tc_set_attr<true, true, 128>();
+  ok &= tc_set_attr<false, false>();
+  ok &= tc_set_attr<false, true>();
+  ok &= tc_set_attr<true, false>();
+  ok &= tc_set_attr<true, true>();
   return ok;
+}
+
+template <bool TA, bool TB>
+inline void tc_launch(const GemmBatch& b, int grid, cudaStream_t st) {
+  gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH><<<grid, TcMain::THREADS, TcMain::SMEM_BYTES, st>>>(b);
 }
 
 }  // namespace bkfac

@@ -37,7 +37,7 @@ out = []
 for name, ta, tb, M, N, K in SHAPES:
     row = {"shape": name, "M": M, "N": N, "K": K}
     for path, key in ((binding.BKFAC_GEMM_TCGEN05, "tc"), (binding.BKFAC_GEMM_SIMT, "simt")):
-        if key == "simt" and M * N * K > 3e11:
+        if key == "simt" and (M * N * K > 3e11 or "--tc-only" in sys.argv):
             continue
         ms, tf = run(path, ta, tb, M, N, K)
         row[key + "_ms"] = round(ms, 4); row[key + "_tflops"] = round(tf, 2)
