@@ -14,12 +14,13 @@
 
 #include "bkfac.h"
 #include "chol.cuh"
+#include "chol_tiled.cuh"
 #include "common.cuh"
 #include "eig.cuh"
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "misc.cuh"
-#include "sytrd_cluster.cuh"
+#include "sytrd_tiled.cuh"
 
 using namespace bkfac;
 
@@ -312,28 +313,18 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
   double flops = 0.0, bytes = 0.0;
   for (auto& p : v) { flops += 2.0 * p.c * (double)p.c * p.c / 3.0; bytes += 12.0 * p.c * (double)p.c; }
   prof_begin(ctx, "chol_inv", st, flops, bytes);
-  std::vector<CholProb> small, big;
-  int cmax_small = 0;
-  for (auto& p : v) {
-    if (p.c <= CHOL_SMEM_MAX) { small.push_back(p); cmax_small = std::max(cmax_small, p.c); }
-    else big.push_back(p);
-  }
-  static CholBatch b;
-  for (int pass = 0; pass < 2; ++pass) {
-    auto& list = pass == 0 ? small : big;
-    size_t i0 = 0;
-    while (i0 < list.size()) {
-      const size_t n = std::min(list.size() - i0, (size_t)CHOL_MAXP);
-      b.nprob = (int)n;
-      int cmax = 0;
-      for (size_t i = 0; i < n; ++i) { b.p[i] = list[i0 + i]; cmax = std::max(cmax, b.p[i].c); }
-      if (pass == 0)
-        chol_inv_kernel<true><<<(unsigned)n, 1024, chol_smem_bytes(cmax, true), st>>>(b);
-      else
-        chol_inv_kernel<false><<<(unsigned)n, 1024, chol_smem_bytes(cmax, false), st>>>(b);
-      LAUNCH_CHECK(ctx);
-      i0 += n;
+  static CholTiledBatch b;
+  size_t i0 = 0;
+  while (i0 < v.size()) {
+    const size_t n = std::min(v.size() - i0, (size_t)CT_MAXP);
+    b.nprob = (int)n;
+    for (size_t i = 0; i < n; ++i) {
+      const CholProb& q = v[i0 + i];
+      b.p[i] = CholTiledProb{q.G, q.ldg, q.L, q.Linv, q.scratch, q.status, q.c, q.shift};
     }
+    chol_tiled_kernel<<<(unsigned)n, CT_THREADS, CT_SMEM_BYTES, st>>>(b);
+    LAUNCH_CHECK(ctx);
+    i0 += n;
   }
   v.clear();
   prof_end(ctx, st);
@@ -365,7 +356,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         sub.nprob = 0;
         int msub = 0;
         for (size_t i = 0; i < n; ++i)
-          if (sytrd_cluster_size(b.p[i].m) == C) {
+          if (sytrd_tiled_cluster(b.p[i].m) == C) {
             sub.p[sub.nprob++] = b.p[i];
             msub = std::max(msub, b.p[i].m);
           }
@@ -375,8 +366,8 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         } else {
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3((unsigned)(C * sub.nprob), 1, 1);
-          cfg.blockDim = dim3(1024, 1, 1);
-          cfg.dynamicSmemBytes = sytrd_cluster_smem_bytes(msub, C);
+          cfg.blockDim = dim3(SYT_THREADS, 1, 1);
+          cfg.dynamicSmemBytes = sytrd_tiled_smem_bytes(msub, C);
           cfg.stream = st;
           cudaLaunchAttribute attr[1];
           attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -385,7 +376,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
           attr[0].val.clusterDim.z = 1;
           cfg.attrs = attr;
           cfg.numAttrs = 1;
-          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel, sub, C))) return BKFAC_ERR_CUDA;
+          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_tiled_kernel, sub, C))) return BKFAC_ERR_CUDA;
         }
         LAUNCH_CHECK(ctx);
       }
@@ -502,7 +493,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
       fp.Qb = a.take(sizeof(float) * (size_t)n * cm);
       const size_t cc = sizeof(float) * (size_t)cm * cm;
       fp.G = a.take(cc); fp.L1 = a.take(cc); fp.L1i = a.take(cc); fp.L2 = a.take(cc); fp.L2i = a.take(cc);
-      fp.cscr = a.take(cm > CHOL_SMEM_MAX ? sizeof(float) * (size_t)cm * (cm + 1) / 2 : 4);
+      fp.cscr = a.take(sizeof(float) * chol_tiled_scratch_floats(cm));
       fp.ws_elems = (long)kSplitMax * std::max(r, cm) * (long)cm;
       fp.ws = a.take(sizeof(float) * fp.ws_elems);
       plan_eig(a, fp.eig, m, r);
@@ -516,7 +507,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
       const size_t ll = sizeof(float) * (size_t)l * l;
       fp.Gr = a.take(ll); fp.L1r = a.take(ll); fp.L1ir = a.take(ll); fp.L2r = a.take(ll);
       fp.L2ir = a.take(ll); fp.Br = a.take(ll);
-      fp.cscr_r = a.take(l > CHOL_SMEM_MAX ? sizeof(float) * (size_t)l * (l + 1) / 2 : 4);
+      fp.cscr_r = a.take(sizeof(float) * chol_tiled_scratch_floats(l));
       fp.ws_r_elems = (long)kSplitMax * l * (long)l;
       fp.ws_r = a.take(sizeof(float) * fp.ws_r_elems);
       plan_eig(a, fp.eig_r, l, r);
@@ -550,14 +541,13 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   cudaSetDevice(device);
   const int big = 220 * 1024;  // below the 227 KB opt-in limit minus static smem
   bool attr_ok = true;
-  attr_ok &= cudaFuncSetAttribute(chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
-  attr_ok &= cudaFuncSetAttribute(chol_inv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
-  attr_ok &= cudaFuncSetAttribute(sytrd_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
-  attr_ok &= cudaFuncSetAttribute(sytrd_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(backtr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(chol_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT_SMEM_BYTES) == cudaSuccess;
   attr_ok &= tc_init_attributes();
   if (!attr_ok) fprintf(stderr, "bkfac: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
   cudaGetLastError();  // never leave a sticky error behind

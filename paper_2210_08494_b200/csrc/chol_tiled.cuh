@@ -1,0 +1,324 @@
+// Blocked Cholesky factorisation and triangular inverse of the c x c Gram matrix
+// G = R^T R of CholeskyQR (Alg 3 line 2 "QR_decomp(A_perp)"; footnote :451
+// allows any orthonormal decomposition) -- one CTA per factor, 32 x 32 register tiles.
+//
+// G is split into NB = ceil(c/32) block rows/columns (padding: identity), tiles packed
+// lower-triangular in a global scratch (L1/L2 resident):
+//   L tiles  col-major (element (i,j) at j*32 + i),  T(I,J) = I(I+1)/2 + J, I >= J
+//   X tiles  row-major (element (i,j) at i*32 + j),  X = L^{-1}
+// Right-looking Cholesky, for each block column J:
+//   (1) one warp factors the diagonal tile (lane = row, rows in registers, shuffles)
+//       and inverts it (lane = column);                                         barrier
+//   (2) every warp takes below-diagonal tiles: L_IJ = G_IJ X_JJ^T;              barrier
+//   (3) every warp takes trailing tiles (I >= K > J): G_IK -= L_IJ L_KJ^T;     barrier
+// then X = L^{-1} right-looking by block rows K (X_KJ = X_KK A_KJ, then A_IJ -= L_IK X_KJ
+// for all I > K in parallel), A_IJ = -sum_{M<I} L_IM X_MJ accumulated in place.
+// The tile products run on FP32 FFMA with the B tile read as broadcast float4 loads.
+// A pivot <= tol * max_i G_ii (rank-deficient residual) is dropped: its column of L and
+// row of X are zero and ST_CHOL_DROP is reported (informational, as before).
+// Outputs: L and Linv = L^{-1} (c x c col-major, zeros above the diagonal).
+#pragma once
+#include "chol.cuh"
+#include "common.cuh"
+
+namespace bkfac {
+
+constexpr int CT_THREADS = 512;
+
+BKFAC_DEV int ctix(int I, int J) { return I * (I + 1) / 2 + J; }
+
+// acc[j] -= (or +=) sum_k A(lane, k) * B(j, k); A, B col-major 32 x 32 tiles
+template <bool SUB>
+BKFAC_DEV void tile_abt(float (&acc)[32], const float* A, const float* B, int lane) {
+#pragma unroll 2
+  for (int k = 0; k < 32; ++k) {
+    const float a = A[k * 32 + lane];
+    const float4* b4 = reinterpret_cast<const float4*>(B + k * 32);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 bb = b4[q];
+      if (SUB) {
+        acc[4 * q + 0] = fmaf(-a, bb.x, acc[4 * q + 0]);
+        acc[4 * q + 1] = fmaf(-a, bb.y, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(-a, bb.z, acc[4 * q + 2]);
+        acc[4 * q + 3] = fmaf(-a, bb.w, acc[4 * q + 3]);
+      } else {
+        acc[4 * q + 0] = fmaf(a, bb.x, acc[4 * q + 0]);
+        acc[4 * q + 1] = fmaf(a, bb.y, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(a, bb.z, acc[4 * q + 2]);
+        acc[4 * q + 3] = fmaf(a, bb.w, acc[4 * q + 3]);
+      }
+    }
+  }
+}
+// acc[j] += sum_k A(lane, k) * B(k, j); A col-major, B row-major 32 x 32 tiles
+BKFAC_DEV void tile_ab(float (&acc)[32], const float* A, const float* Brm, int lane) {
+#pragma unroll 2
+  for (int k = 0; k < 32; ++k) {
+    const float a = A[k * 32 + lane];
+    const float4* b4 = reinterpret_cast<const float4*>(Brm + k * 32);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 bb = b4[q];
+      acc[4 * q + 0] = fmaf(a, bb.x, acc[4 * q + 0]);
+      acc[4 * q + 1] = fmaf(a, bb.y, acc[4 * q + 1]);
+      acc[4 * q + 2] = fmaf(a, bb.z, acc[4 * q + 2]);
+      acc[4 * q + 3] = fmaf(a, bb.w, acc[4 * q + 3]);
+    }
+  }
+}
+
+// Copy one 32 x 32 tile (1024 floats, 16-byte aligned) global -> this warp's shared
+// buffer with all loads in flight at once (one L2 round trip instead of one per column).
+BKFAC_DEV void tile_stage(float* dst, const float* src, int lane) {
+  float4 r[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) r[q] = reinterpret_cast<const float4*>(src)[q * 32 + lane];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) reinterpret_cast<float4*>(dst)[q * 32 + lane] = r[q];
+}
+
+// ---- 32 x 32 diagonal tile on one warp, fully unrolled by templates (compile-time
+// register indices: no local memory).  Factor: lane = row i, a[j] = A(i, j).
+template <int K, int J>
+BKFAC_DEV void ct_upd(float (&a)[32], float lik, int lane) {
+  if constexpr (J < 32) {
+    const float ljk = __shfl_sync(0xffffffffu, lik, J);
+    if (lane >= J) a[J] = fmaf(-lik, ljk, a[J]);
+    ct_upd<K, J + 1>(a, lik, lane);
+  }
+}
+template <int K>
+BKFAC_DEV void ct_factor(float (&a)[32], int lane, int nreal, float tol, int& dropped) {
+  if constexpr (K < 32) {
+    const float akk = __shfl_sync(0xffffffffu, a[K], K);
+    const bool drop = (K < nreal) && !(akk > tol);
+    const float rs = drop ? 0.f : rsqrtf(fmaxf(akk, 1e-38f));   // 1 / l_kk (MUFU)
+    const float lkk = drop ? 0.f : fmaxf(akk, 1e-38f) * rs;
+    dropped |= drop;
+    const float lik = (lane > K) ? a[K] * rs : (lane == K ? lkk : 0.f);
+    a[K] = lik;
+    ct_upd<K, K + 1>(a, lik, lane);
+    ct_factor<K + 1>(a, lane, nreal, tol, dropped);
+  }
+}
+// Inverse of the lower-triangular tile held as a (lane = row): lane j computes column j
+// of X = L^{-1}: x[i] = X(i, j).
+template <int I, int Kk>
+BKFAC_DEV void ct_inv_dot(const float (&a)[32], const float (&x)[32], float& s, int lane) {
+  if constexpr (Kk < I) {
+    const float lik = __shfl_sync(0xffffffffu, a[Kk], I);
+    if (Kk >= lane) s = fmaf(lik, x[Kk], s);
+    ct_inv_dot<I, Kk + 1>(a, x, s, lane);
+  }
+}
+template <int I>
+BKFAC_DEV void ct_inverse(const float (&a)[32], float (&x)[32], int lane) {
+  if constexpr (I < 32) {
+    float s = 0.f;
+    ct_inv_dot<I, 0>(a, x, s, lane);
+    const float lii = __shfl_sync(0xffffffffu, a[I], I);
+    const float rinv = (lii > 0.f) ? __frcp_rn(lii) : 0.f;
+    x[I] = (I < lane) ? 0.f : (I == lane ? rinv : -s * rinv);
+    ct_inverse<I + 1>(a, x, lane);
+  }
+}
+
+struct CholTiledProb {
+  const float* G; int ldg;
+  float* L; float* Linv;   // c x c col-major, ld = c
+  float* tiles;            // chol_tiled_scratch_floats(c) floats of scratch
+  int* status;
+  int c;
+  float shift;
+};
+constexpr int CT_MAXP = 100;
+struct CholTiledBatch { int nprob; CholTiledProb p[CT_MAXP]; };
+
+constexpr size_t CT_SMEM_BYTES = (size_t)(CT_THREADS / 32) * 2048 * sizeof(float);
+inline size_t chol_tiled_scratch_floats(int c) {
+  const size_t NB = (size_t)(c + 31) / 32;
+  return 2 * NB * (NB + 1) / 2 * 1024 + NB * 1024;
+}
+
+__global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_constant__ CholTiledBatch b) {
+  const CholTiledProb& p = b.p[blockIdx.x];
+  const int c = p.c, NB = (c + 31) >> 5;
+  const int ntile = NB * (NB + 1) / 2;
+  float* Lt = p.tiles;                       // L tiles (col-major)
+  float* Xt = Lt + (size_t)ntile * 1024;     // X tiles (row-major)
+  float* Xd = Xt + (size_t)ntile * 1024;     // col-major copies of the diagonal X_JJ
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = CT_THREADS / 32;
+  __shared__ float red[32];
+  __shared__ int s_drop;
+  extern __shared__ __align__(16) float ctsm[];
+  float* sA = ctsm + warp * 2048;     // per-warp staging: A tile, B tile
+  float* sB = sA + 1024;
+
+  // ---- load G (lower) into tiles, identity padding; trace and max diagonal
+  float dsum = 0.f, dmax = 0.f;
+  for (int t = warp; t < ntile; t += NW) {
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    const int J = t - I * (I + 1) / 2;
+    float* T = Lt + (size_t)t * 1024;
+    for (int jj = 0; jj < 32; ++jj) {
+      const int i = 32 * I + lane, j = 32 * J + jj;
+      float g;
+      if (i < c && j < c) g = (i >= j) ? p.G[i + (long)j * p.ldg] : 0.f;
+      else g = (i == j) ? 1.f : 0.f;
+      T[jj * 32 + lane] = g;
+      if (i == j && i < c) { dsum += g; dmax = fmaxf(dmax, g); }
+    }
+  }
+  const float trace = block_sum(dsum, red);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if (lane == 0) red[warp] = dmax;
+  __syncthreads();
+  float gmax = 0.f;
+  for (int w = 0; w < NW; ++w) gmax = fmaxf(gmax, red[w]);
+  if (tid == 0) s_drop = 0;
+  // shifted first pass (sCQR, Fukaya et al. 2020): G_ii += shift * tr(G)
+  const float sh = (p.shift > 0.f) ? p.shift * trace : 0.f;
+  const float tol = 4.0f * 1.1920929e-7f * (gmax + sh);
+  __syncthreads();
+
+  for (int J = 0; J < NB; ++J) {
+    // (1) diagonal tile: one warp factors it (lane = row, register rows, shuffles; fully
+    //     unrolled by templates) and inverts it (lane = column).
+    if (warp == 0) {
+      float* T = Lt + (size_t)ctix(J, J) * 1024;
+      float a[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) a[j] = T[j * 32 + lane];
+      const bool real = 32 * J + lane < c;
+      if (sh > 0.f && real) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) if (j == lane) a[j] += sh;
+      }
+      int dropped = 0;
+      ct_factor<0>(a, lane, c - 32 * J, tol, dropped);
+      // write L_JJ (lower), zero the upper part
+#pragma unroll
+      for (int j = 0; j < 32; ++j) T[j * 32 + lane] = (lane >= j) ? a[j] : 0.f;
+      float x[32];
+      ct_inverse<0>(a, x, lane);
+      // X_JJ: row-major into the X tiles, col-major copy into Xd
+      float* XJ = Xt + (size_t)ctix(J, J) * 1024;
+      float* XJc = Xd + (size_t)J * 1024;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        XJ[i * 32 + lane] = x[i];       // element (i, lane)
+        XJc[lane * 32 + i] = x[i];      // col-major: column lane
+      }
+      if (dropped && lane == 0) s_drop = 1;
+    }
+    __syncthreads();
+    // (2) L_IJ = G_IJ X_JJ^T for I > J (X_JJ^T(k, j) = X_JJ(j, k) -> col-major copy as B)
+    for (int I = J + 1 + warp; I < NB; I += NW) {
+      float* T = Lt + (size_t)ctix(I, J) * 1024;
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+      // acc(i, j) = sum_k G(i, k) X_JJ(j, k): B = X_JJ col-major
+      tile_stage(sA, T, lane);
+      tile_stage(sB, Xd + (size_t)J * 1024, lane);
+      __syncwarp();
+      tile_abt<false>(acc, sA, sB, lane);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) T[j * 32 + lane] = acc[j];
+    }
+    __syncthreads();
+    // (3) trailing update G_IK -= L_IJ L_KJ^T for I >= K > J
+    {
+      const int n = NB - J - 1;
+      const int npairs = n * (n + 1) / 2;
+      for (int t = warp; t < npairs; t += NW) {
+        int a = 0;
+        while ((a + 1) * (a + 2) / 2 <= t) ++a;
+        const int I = J + 1 + a, K = J + 1 + (t - a * (a + 1) / 2);
+        float* T = Lt + (size_t)ctix(I, K) * 1024;
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = T[j * 32 + lane];
+        // B(j, k) = L_KJ(j, k): col-major L tile is element (j,k) at k*32 + j -- we need
+        // B rows contiguous in j for fixed k: that is exactly the col-major layout.
+        tile_stage(sA, Lt + (size_t)ctix(I, J) * 1024, lane);
+        tile_stage(sB, Lt + (size_t)ctix(K, J) * 1024, lane);
+        __syncwarp();
+        tile_abt<true>(acc, sA, sB, lane);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) T[j * 32 + lane] = acc[j];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- X = L^{-1}, right-looking by block rows K: the off-diagonal X tiles first hold
+  // the accumulators A_IJ = -sum_{M<I} L_IM X_MJ (zero-initialised), then
+  //   (1) X_KJ = X_KK A_KJ for J < K;     (2) A_IJ -= L_IK X_KJ for I > K, J <= K.
+  for (int t = warp; t < ntile; t += NW) {
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    if (t - I * (I + 1) / 2 == I) continue;            // diagonal X_II already set
+    float4* T4 = reinterpret_cast<float4*>(Xt + (size_t)t * 1024);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) T4[q * 32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  for (int K = 0; K < NB; ++K) {
+    for (int J = warp; J < K; J += NW) {               // (1)
+      float* XK = Xt + (size_t)ctix(K, J) * 1024;
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+      tile_stage(sA, Xd + (size_t)K * 1024, lane);     // X_KK col-major
+      tile_stage(sB, XK, lane);                        // A_KJ row-major
+      __syncwarp();
+      tile_ab(acc, sA, sB, lane);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) XK[lane * 32 + j] = acc[j];
+    }
+    __syncthreads();
+    const int nI = NB - K - 1, nJ = K + 1;
+    for (int t = warp; t < nI * nJ; t += NW) {         // (2)
+      const int I = K + 1 + t / nJ, J = t % nJ;
+      float* XI = Xt + (size_t)ctix(I, J) * 1024;
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+      tile_stage(sA, Lt + (size_t)ctix(I, K) * 1024, lane);   // L_IK col-major
+      tile_stage(sB, Xt + (size_t)ctix(K, J) * 1024, lane);   // X_KJ row-major
+      __syncwarp();
+      tile_ab(acc, sA, sB, lane);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) XI[lane * 32 + j] -= acc[j];
+    }
+    __syncthreads();
+  }
+  // ---- outputs: L and Linv, c x c col-major, zeros above the diagonal
+  for (int t = warp; t < NB * NB; t += NW) {
+    const int I = t % NB, J = t / NB;
+    const int i = 32 * I + lane;
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = 32 * J + jj;
+      if (i >= c || j >= c) continue;
+      float lv = 0.f, xv = 0.f;
+      if (I >= J) {
+        lv = Lt[(size_t)ctix(I, J) * 1024 + jj * 32 + lane];
+        xv = Xt[(size_t)ctix(I, J) * 1024 + lane * 32 + jj];
+        if (I == J && lane < jj) { lv = 0.f; xv = 0.f; }
+      }
+      p.L[i + (long)j * c] = lv;
+      p.Linv[i + (long)j * c] = xv;
+    }
+  }
+  if (tid == 0 && s_drop && p.status) atomicOr(p.status, ST_CHOL_DROP);
+}
+
+}  // namespace bkfac

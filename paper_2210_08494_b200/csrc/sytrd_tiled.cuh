@@ -1,0 +1,306 @@
+// Householder tridiagonalisation of the Brand core K (Alg 3 line 4 "EVD(M_S)",
+// PAPER.md:505) with the lower triangle resident in the distributed shared memory of a
+// thread-block cluster, processed in 32 x 32 register tiles.
+//
+// Storage.  K is padded to m_pad = 32*NB rows/cols (zeros).  Block-column J (columns
+// 32J..32J+31, rows 32J..m_pad-1, col-major) lives in the shared memory of CTA
+// owner(J) of the cluster; block-columns are dealt to the C CTAs in boustrophedon order
+// (0..C-1, C-1..0, ...), which balances the triangular sizes.
+//
+// Step k (reflector H_k = I - tau v v^T zeroing column k below the subdiagonal):
+//   (a) the owner of column k applies the pending rank-2 update of step k-1 to it
+//       (A <- A - v w^T - w v^T), forms v_k, tau_k (dlarfg) and broadcasts v_k into every
+//       CTA (st.shared::cluster);                                     cluster barrier
+//   (b) every CTA walks its tiles (I >= J) of the trailing matrix with one warp per tile,
+//       lane = row: applies the pending update in registers, writes the tile back, and
+//       accumulates its partial y = A v_k both ways from the lower triangle -- row sums
+//       in a register, column sums by a 31-shuffle transpose-reduce; both go to the
+//       CTA's partial y with shared-memory atomics;                  cluster barrier
+//   (c) every CTA sums the C partial y through DSMEM and forms
+//       w_k = tau y - (tau^2/2)(y.v) v locally.
+// Per element of the trailing matrix and step: one LDS, one STS and five FP32 ops (the
+// column-cyclic first version of this kernel needed seven shared-memory accesses).
+// v and y are double-buffered by step parity.  Outputs as sytrd_kernel: d, e, tau and
+// the reflectors (rows >= k+2 of column k) in K's lower triangle for the back-transform.
+#pragma once
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "eig.cuh"
+
+namespace bkfac {
+
+namespace cgt = cooperative_groups;
+
+constexpr int SYT_THREADS = 512;
+constexpr int SYT_SMEM_FLOATS = 55 * 1024;   // per-CTA budget (220 KB)
+
+__host__ __device__ inline int syt_owner(int J, int C) {
+  const int t = J / C, pos = J % C;
+  return (t & 1) ? C - 1 - pos : pos;
+}
+// floats of tile storage owned by CTA q
+inline long syt_own_floats(int NB, int C, int q) {
+  long s = 0;
+  for (int J = 0; J < NB; ++J)
+    if (syt_owner(J, C) == q) s += 1024L * (NB - J);
+  return s;
+}
+inline int syt_vec_floats(int m_pad) { return 7 * m_pad + 64 + 64; }
+// smallest cluster size whose largest per-CTA share fits; 0 = does not fit
+inline int sytrd_tiled_cluster(int m) {
+  const int NB = (m + 31) / 32, m_pad = NB * 32;
+  for (int C = 1; C <= 8; C *= 2) {
+    long mx = 0;
+    for (int q = 0; q < C; ++q) mx = std::max(mx, syt_own_floats(NB, C, q));
+    if (mx + syt_vec_floats(m_pad) <= SYT_SMEM_FLOATS) return C;
+  }
+  return 0;
+}
+inline size_t sytrd_tiled_smem_bytes(int m, int C) {
+  const int NB = (m + 31) / 32, m_pad = NB * 32;
+  long mx = 0;
+  for (int q = 0; q < C; ++q) mx = std::max(mx, syt_own_floats(NB, C, q));
+  return sizeof(float) * (size_t)(mx + syt_vec_floats(m_pad));
+}
+
+__global__ void __launch_bounds__(SYT_THREADS, 1)
+sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
+  cgt::cluster_group cluster = cgt::this_cluster();
+  const int q = (int)cluster.block_rank();
+  const EigProb& p = b.p[blockIdx.x / C];
+  const int m = p.m;
+  const int ld = p.ldk;
+  float* K = p.K;
+  const int NB = (m + 31) >> 5, m_pad = NB << 5;
+  extern __shared__ __align__(16) float tsm[];
+  float* vbuf = tsm;                 // 2 * m_pad  (v_k by parity, broadcast by the owner)
+  float* ybuf = vbuf + 2 * m_pad;    // 2 * m_pad  (partial y by parity, read remotely)
+  float* ys = ybuf + 2 * m_pad;      // m_pad      (summed y)
+  float* wp = ys + m_pad;            // m_pad      (w_{k-1})
+  float* scal = wp + m_pad;          // 64: [0..1] tau by parity, [2] bad flag, [4..] reduce
+  int* boff = reinterpret_cast<int*>(scal + 64);   // 64: storage offset of block-column J
+  float* tiles = scal + 128;         // owned block-columns
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = SYT_THREADS / 32;
+  float* red = scal + 4;
+
+  if (tid == 0) {
+    int off = 0;
+    for (int J = 0; J < NB; ++J) {
+      if (syt_owner(J, C) == q) { boff[J] = off; off += 1024 * (NB - J); }
+      else boff[J] = -1;
+    }
+  }
+  for (int i = tid; i < 4 * m_pad; i += SYT_THREADS) vbuf[i] = 0.f;   // vbuf + ybuf
+  for (int i = tid; i < 2 * m_pad; i += SYT_THREADS) ys[i] = 0.f;     // ys + wp
+  __syncthreads();
+  // load owned block-columns (zero padding) + finiteness check
+  int bad = 0;
+  for (int J = 0; J < NB; ++J) {
+    if (boff[J] < 0) continue;
+    const int rows = m_pad - 32 * J;
+    float* blk = tiles + boff[J];
+    for (int jj = warp; jj < 32; jj += NW) {
+      const int j = 32 * J + jj;
+      for (int ii = lane; ii < rows; ii += 32) {
+        const int i = 32 * J + ii;
+        float a = 0.f;
+        if (i < m && j < m && i >= j) { a = K[i + (long)j * ld]; bad |= !isfinite(a); }
+        blk[jj * rows + ii] = a;
+      }
+    }
+  }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) scal[2] = bad ? 1.f : 0.f;
+  cluster.sync();
+  float anybad = 0.f;
+  for (int r = 0; r < C; ++r) anybad += *cluster.map_shared_rank(scal + 2, r);
+  cluster.sync();
+  if (anybad != 0.f) {
+    if (q == 0) {
+      if (tid == 0 && p.status) atomicOr(p.status, ST_NONFINITE);
+      for (int i = tid; i < m; i += SYT_THREADS) { p.d[i] = 0.f; p.e[i] = 0.f; p.tau[i] = 0.f; }
+    }
+    return;
+  }
+  if (m <= 2) {
+    if (q == 0 && tid == 0) {
+      p.d[0] = K[0];
+      p.e[0] = (m == 2) ? K[1] : 0.f;
+      p.tau[0] = 0.f;
+      if (m == 2) { p.d[1] = K[1 + (long)ld]; p.e[1] = 0.f; p.tau[1] = 0.f; }
+    }
+    return;
+  }
+
+  for (int k = 0; k < m - 2; ++k) {
+    float* v = vbuf + (k & 1) * m_pad;            // v_k (written by the owner)
+    const float* vp = vbuf + ((k + 1) & 1) * m_pad;   // v_{k-1} (zero at k = 0)
+    float* y = ybuf + (k & 1) * m_pad;
+    const bool have_prev = k > 0;
+    const int kb = k >> 5, jk = k & 31;
+    // (a) owner of column k
+    if (boff[kb] >= 0) {
+      const int rows = m_pad - 32 * kb;
+      float* ck = tiles + boff[kb] + jk * rows - 32 * kb;   // ck[i], i >= k
+      if (have_prev) {
+        const float wk = wp[k], vk = vp[k];
+        for (int i = k + tid; i < m; i += SYT_THREADS) ck[i] -= vp[i] * wk + wp[i] * vk;
+      }
+      __syncthreads();
+      const float alpha = ck[k + 1];
+      float ss = 0.f;
+      for (int i = k + 2 + tid; i < m; i += SYT_THREADS) ss += ck[i] * ck[i];
+      ss = block_sum(ss, red);
+      float tau, beta, scale;
+      if (ss == 0.f) {
+        tau = 0.f; beta = alpha; scale = 0.f;
+      } else {
+        const float nrm = sqrtf(alpha * alpha + ss);
+        beta = alpha >= 0.f ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.f / (alpha - beta);
+      }
+      for (int i = tid; i < m_pad; i += SYT_THREADS) {
+        float vi = 0.f;
+        if (i == k + 1) vi = 1.f;
+        else if (i >= k + 2 && i < m) { vi = ck[i] * scale; ck[i] = vi; }
+        for (int r = 0; r < C; ++r) *cluster.map_shared_rank(v + i, r) = vi;
+      }
+      if (tid == 0) {
+        p.d[k] = ck[k];
+        p.e[k] = beta;
+        p.tau[k] = tau;
+        for (int r = 0; r < C; ++r) *cluster.map_shared_rank(scal + (k & 1), r) = tau;
+      }
+    }
+    cluster.sync();                                              // (1) v_k, tau_k everywhere
+    const float tau = scal[k & 1];
+    for (int i = tid; i < m_pad; i += SYT_THREADS) y[i] = 0.f;
+    __syncthreads();
+    // (b) tiles (I >= J) of owned block-columns that have columns j > k
+    int tcount = 0;
+    for (int J = kb; J < NB; ++J) {
+      if (boff[J] < 0) continue;
+      const int rows = m_pad - 32 * J;
+      const float* blkc = tiles + boff[J];
+      const float cv = v[32 * J + lane], cvp = vp[32 * J + lane], cwp = wp[32 * J + lane];
+      for (int I = J; I < NB; ++I, ++tcount) {
+        if ((tcount % NW) != warp) continue;
+        float* tcol = const_cast<float*>(blkc) + 32 * (I - J) + lane;   // + jj * rows
+        const int i = 32 * I + lane;
+        const float vi = v[i], vpi = vp[i], wpi = wp[i];
+        float rowacc = 0.f;
+        float colv[32];
+        const bool full = (32 * J > k) && (I > J);
+        if (full) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            float a = tcol[jj * rows];
+            if (have_prev) {
+              a -= vpi * __shfl_sync(0xffffffffu, cwp, jj) + wpi * __shfl_sync(0xffffffffu, cvp, jj);
+              tcol[jj * rows] = a;
+            }
+            rowacc = fmaf(a, __shfl_sync(0xffffffffu, cv, jj), rowacc);
+            colv[jj] = a * vi;
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const int j = 32 * J + jj;
+            const bool valid = (j > k) && (i >= j);
+            float a = tcol[jj * rows];
+            const float cwpj = __shfl_sync(0xffffffffu, cwp, jj);
+            const float cvpj = __shfl_sync(0xffffffffu, cvp, jj);
+            const float cvj = __shfl_sync(0xffffffffu, cv, jj);
+            if (valid && have_prev) {
+              a -= vpi * cwpj + wpi * cvpj;
+              tcol[jj * rows] = a;
+            }
+            const float ae = valid ? a : 0.f;
+            rowacc = fmaf(ae, cvj, rowacc);
+            colv[jj] = (i > j) ? ae * vi : 0.f;
+          }
+        }
+        // transpose-reduce: lane l ends with sum over lanes of colv[l]
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          const bool upper = (lane & s) != 0;
+#pragma unroll
+          for (int t = 0; t < s; ++t) {
+            const float send = upper ? colv[t] : colv[t + s];
+            const float keep = upper ? colv[t + s] : colv[t];
+            colv[t] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+          }
+        }
+        atomicAdd(&y[i], rowacc);
+        atomicAdd(&y[32 * J + lane], colv[0]);
+      }
+    }
+    __syncthreads();
+    cluster.sync();                                              // (2) partial y ready
+    float pv = 0.f;
+    for (int i = k + 1 + tid; i < m; i += SYT_THREADS) {
+      float s = 0.f;
+      for (int r = 0; r < C; ++r) s += *cluster.map_shared_rank(y + i, r);
+      ys[i] = s;
+      pv = fmaf(s, v[i], pv);
+    }
+    pv = block_sum(pv, red);
+    const float gamma = 0.5f * tau * tau * pv;
+    for (int i = tid; i < m_pad; i += SYT_THREADS)
+      wp[i] = (i > k && i < m) ? tau * ys[i] - gamma * v[i] : 0.f;
+    __syncthreads();
+  }
+  // trailing 2x2 block: the pending update of step m-3, then d, e
+  {
+    const int k = m - 2;
+    const float* vp = vbuf + ((k + 1) & 1) * m_pad;
+    const int b2 = (m - 2) >> 5, b1 = (m - 1) >> 5;
+    if (boff[b2] >= 0 && tid < 2) {
+      const int rows = m_pad - 32 * b2;
+      float* c2 = tiles + boff[b2] + ((m - 2) & 31) * rows - 32 * b2;
+      const int i = m - 2 + tid;
+      c2[i] -= vp[i] * wp[m - 2] + wp[i] * vp[m - 2];
+    }
+    if (boff[b1] >= 0 && tid == 32) {
+      const int rows = m_pad - 32 * b1;
+      float* c1 = tiles + boff[b1] + ((m - 1) & 31) * rows - 32 * b1;
+      c1[m - 1] -= 2.f * vp[m - 1] * wp[m - 1];
+    }
+    __syncthreads();
+    if (boff[b2] >= 0 && tid == 0) {
+      const int rows = m_pad - 32 * b2;
+      const float* c2 = tiles + boff[b2] + ((m - 2) & 31) * rows - 32 * b2;
+      p.d[m - 2] = c2[m - 2];
+      p.e[m - 2] = c2[m - 1];
+      p.e[m - 1] = 0.f;
+      p.tau[m - 2] = 0.f;
+      p.tau[m - 1] = 0.f;
+    }
+    if (boff[b1] >= 0 && tid == 0) {
+      const int rows = m_pad - 32 * b1;
+      p.d[m - 1] = tiles[boff[b1] + ((m - 1) & 31) * rows - 32 * b1 + m - 1];
+    }
+  }
+  // reflectors back to K's lower triangle (rows >= j) for the back-transform
+  for (int J = 0; J < NB; ++J) {
+    if (boff[J] < 0) continue;
+    const int rows = m_pad - 32 * J;
+    const float* blk = tiles + boff[J];
+    for (int jj = warp; jj < 32; jj += NW) {
+      const int j = 32 * J + jj;
+      if (j >= m) continue;
+      for (int ii = lane; ii < rows; ii += 32) {
+        const int i = 32 * J + ii;
+        if (i >= j && i < m) K[i + (long)j * ld] = blk[jj * rows + ii];
+      }
+    }
+  }
+  cluster.sync();   // no CTA exits while others may still address its shared memory
+}
+
+}  // namespace bkfac
