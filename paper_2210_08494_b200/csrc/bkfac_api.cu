@@ -191,7 +191,7 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
     for (size_t i = 0; i < n; ++i) {
       GemmProb p = v[i0 + i];
       p.tile_start = tiles;
-      tiles += p.tiles_m * p.tiles_n * p.splits;
+      tiles += (p.sym ? p.tiles_m * (p.tiles_m + 1) / 2 : p.tiles_m * p.tiles_n) * p.splits;
       any_split |= p.splits > 1;
       b.p[i] = p;
     }
@@ -241,7 +241,8 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       p.tiles_m = ceil_div(std::max(p.M, 1), bm);
       p.tiles_n = ceil_div(std::max(p.N, 1), bn);
       if (p.M <= 0 || p.N <= 0) p.tiles_m = p.tiles_n = 0;
-      base_tiles += (long)p.tiles_m * p.tiles_n;
+      if (!tc || p.M != p.N || bm != bn) p.sym = 0;   // mirrored tiles: tcgen05 square tiles only
+      base_tiles += p.sym ? (long)p.tiles_m * (p.tiles_m + 1) / 2 : (long)p.tiles_m * p.tiles_n;
     }
   const long target = tc ? (long)kNumSM : 2L * kNumSM;
   for (int v = 0; v < 4; ++v)
@@ -252,7 +253,7 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       if (tc) {
         const int nc = ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK);
         int splits = 1;
-        if (nc >= 8 && base_tiles > 0 && base_tiles < target && p.ws != nullptr) {
+        if (nc >= 8 && base_tiles > 0 && base_tiles < target && p.ws != nullptr && !p.sym) {
           splits = (int)std::min<long>(kSplitMax, (target + base_tiles - 1) / base_tiles);
           splits = std::min(splits, nc / 4);
           splits = (int)std::min<long>(splits, cap);
@@ -841,7 +842,9 @@ bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K, const floa
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int n = fp.d.n;
   GemmStage gs;
-  gs.add(false, true, gp(M, n, M, n, K, n, n, n, c, 1.f - rho, K, n, rho), 0);
+  GemmProb pe = gp(M, n, M, n, K, n, n, n, c, 1.f - rho, K, n, rho);
+  pe.sym = 1;   // K and M M^T are symmetric: lower tiles computed, mirrored
+  gs.add(false, true, pe, 0);
   return run_gemms(ctx, gs, st, "gemm_ea");
 }
 
@@ -859,7 +862,9 @@ bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args,
     if (a.c <= 0 || a.c > fp.d.c_max) return BKFAC_ERR_DIM;
     if (!(a.rho >= 0.f && a.rho < 1.f)) return BKFAC_ERR_INVALID_ARG;
     const int n = fp.d.n;
-    gs.add(false, true, gp(a.M, n, a.M, n, a.K_dense, n, n, n, a.c, 1.f - a.rho, a.K_dense, n, a.rho), 0);
+    GemmProb pe = gp(a.M, n, a.M, n, a.K_dense, n, n, n, a.c, 1.f - a.rho, a.K_dense, n, a.rho);
+    pe.sym = 1;   // K and M M^T are symmetric: lower tiles computed, mirrored
+    gs.add(false, true, pe, 0);
   }
   if (count == 0) return BKFAC_OK;
   return run_gemms(ctx, gs, static_cast<cudaStream_t>(stream), "gemm_ea");

@@ -19,6 +19,7 @@ struct GemmProb {
   float alpha, beta;
   const float* beta_dev;   // if non-null, beta = *beta_dev (device scalar)
   int splits, kchunk, tiles_m, tiles_n, tile_start;
+  int sym;                 // tcgen05 path: C = C^T known (e.g. M M^T): lower tiles only, mirrored
 };
 
 constexpr int GEMM_MAXP = 100;

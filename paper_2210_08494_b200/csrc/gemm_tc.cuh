@@ -242,11 +242,19 @@ BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
   x.pi = tc_find_prob(b, t);
   const GemmProb& p = b.p[x.pi];
   const int lt = t - p.tile_start;
-  const int per_split = p.tiles_m * p.tiles_n;
+  const int per_split = p.sym ? p.tiles_m * (p.tiles_m + 1) / 2 : p.tiles_m * p.tiles_n;
   x.split = lt / per_split;
   const int rem = lt - x.split * per_split;
-  x.m0 = (rem % p.tiles_m) * TC_BM;
-  x.n0 = (rem / p.tiles_m) * BN;
+  if (p.sym) {   // lower-triangular tile (tm >= tn), rem = tm (tm + 1) / 2 + tn
+    int tm = (int)((sqrtf(8.f * rem + 1.f) - 1.f) * 0.5f);
+    while (tm * (tm + 1) / 2 > rem) --tm;
+    while ((tm + 1) * (tm + 2) / 2 <= rem) ++tm;
+    x.m0 = tm * TC_BM;
+    x.n0 = (rem - tm * (tm + 1) / 2) * BN;
+  } else {
+    x.m0 = (rem % p.tiles_m) * TC_BM;
+    x.n0 = (rem / p.tiles_m) * BN;
+  }
   x.nc1 = (p.k1 + TC_BK - 1) / TC_BK;
   const int nc = x.nc1 + (p.K - p.k1 + TC_BK - 1) / TC_BK;
   x.c_beg = min(nc, x.split * p.kchunk);     // kchunk = chunks per split on this path
@@ -492,6 +500,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
                   float o = p.alpha * v[jj];
                   if (beta != 0.f) o += beta * p.C0[i + (long)j * p.ldc0];
                   p.C[i + (long)j * p.ldc] = o;
+                  if (p.sym && x.m0 != x.n0) p.C[j + (long)i * p.ldc] = o;   // mirror tile
                 }
               }
             }
