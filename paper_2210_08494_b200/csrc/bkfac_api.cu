@@ -42,13 +42,14 @@ struct Arena {
 };
 
 struct EigWs {  // workspace of one eigen problem of order <= m with <= r outputs
-  size_t K, d, e, tau, lam, Y, scr, piv, V;
+  size_t K, d, e, tau, lam, Y, scr, piv, V, gt;
   int m, r;
 };
 
 void plan_eig(Arena& a, EigWs& w, int m, int r) {
   w.m = m; w.r = r;
   w.K = a.take(sizeof(float) * (size_t)m * m);
+  w.gt = sytrd_tiled_cluster(m) == 0 ? a.take(sizeof(float) * syt_global_tile_floats(m)) : 0;
   w.d = a.take(sizeof(float) * m);
   w.e = a.take(sizeof(float) * m);
   w.tau = a.take(sizeof(float) * m);
@@ -362,8 +363,10 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
             msub = std::max(msub, b.p[i].m);
           }
         if (sub.nprob == 0) continue;
-        if (C == 0) {
-          sytrd_kernel<<<(unsigned)sub.nprob, 1024, sizeof(float) * (36 * (size_t)msub + 64), st>>>(sub);
+        if (C == 0) {   // tiles in global memory, one CTA per factor
+          const int mp = (msub + 31) / 32 * 32;
+          sytrd_tiled_kernel<true><<<(unsigned)sub.nprob, SYT_THREADS,
+                                     sizeof(float) * (size_t)syt_vec_floats(mp), st>>>(sub, 1);
         } else {
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3((unsigned)(C * sub.nprob), 1, 1);
@@ -377,12 +380,16 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
           attr[0].val.clusterDim.z = 1;
           cfg.attrs = attr;
           cfg.numAttrs = 1;
-          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_tiled_kernel, sub, C))) return BKFAC_ERR_CUDA;
+          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_tiled_kernel<false>, sub, C))) return BKFAC_ERR_CUDA;
         }
         LAUNCH_CHECK(ctx);
       }
     }
     prof_end(ctx, st);
+#ifdef BKFAC_SYT_TIMING
+    i0 += n;
+    continue;   // tuning builds: keep the sytrd timing sums in Y
+#endif
     prof_begin(ctx, "eig_bisect", st, 0.0, 0.0);
     bisect_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, BIS_WARPS)), BIS_WARPS * 32,
                     sizeof(double) * 2 * (size_t)mmax, st>>>(b);
@@ -422,6 +429,7 @@ EigProb eig_prob(bkfac_ctx ctx, const EigWs& w, int m, int r, float* V, int ldv,
   p.V = V; p.ldv = ldv;
   p.Dout = Dout;
   p.status = status;
+  p.gtiles = w.gt ? at<float>(ctx, w.gt) : nullptr;
   return p;
 }
 
@@ -542,10 +550,10 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   cudaSetDevice(device);
   const int big = 220 * 1024;  // below the 227 KB opt-in limit minus static smem
   bool attr_ok = true;
-  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
-  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(backtr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
-  attr_ok &= cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(chol_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT_SMEM_BYTES) == cudaSuccess;
@@ -1153,6 +1161,17 @@ bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha
   gs.add(transA != 0, transB != 0, p, cap);
   return run_gemms(&tmp, gs, static_cast<cudaStream_t>(stream), "gemm_user");
 }
+
+#ifdef BKFAC_SYT_TIMING
+// tuning builds only (not part of the ABI): device address of a factor's eigensolver
+// scratch, where BKFAC_SYT_TIMING kernels leave per-phase cycle sums.
+void* bkfac_debug_eig_scratch(bkfac_ctx ctx, int factor) {
+  return at<double>(ctx, ctx->f[factor].eig.Y);
+}
+void bkfac_debug_d2h(void* dst, const void* src, size_t bytes) {
+  cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+}
+#endif
 
 // ------------------------------------------------------------------------- check
 bkfac_status bkfac_check(bkfac_ctx ctx, void* stream, int* first_bad, int* info_bits) {

@@ -2,8 +2,7 @@
 // dense-path / RSVD projected matrices: "EVD(M_S)" of Alg 3, of which
 // only the top-r eigenpairs are kept (truncation, Alg 4 :540-543).
 //
-//   1. sytrd_kernel     Householder tridiagonalisation T = H^T K H (one CTA per factor,
-//                       lower triangle, rank-2 update fused with the next symv).
+//   1. sytrd_tiled_kernel (sytrd_tiled.cuh) Householder tridiagonalisation T = H^T K H.
 //   2. bisect_kernel    top-r eigenvalues of T by Sturm-count multisection in fp64
 //                       (one warp per eigenvalue, 32 probes per round).
 //   3. invit_kernel     eigenvectors of T by inverse iteration in fp64 (one thread per
@@ -27,136 +26,10 @@ struct EigProb {
   float* V; int ldv;       // output eigenvectors of K, m x r col-major
   float* Dout;             // output eigenvalues (r), clamped >= 0
   int* status;
+  float* gtiles;           // tridiagonalisation tiles in global memory (large m), else null
 };
 constexpr int EIG_MAXP = 100;
 struct EigBatch { int nprob; EigProb p[EIG_MAXP]; };
-
-// ------------------------------------------------------------------ 1. sytrd
-__global__ void __launch_bounds__(1024) sytrd_kernel(const __grid_constant__ EigBatch b) {
-  const EigProb& p = b.p[blockIdx.x];
-  const int m = p.m;
-  const int ld = p.ldk;
-  float* K = p.K;
-  extern __shared__ __align__(16) float ssm[];
-  float* v = ssm;
-  float* vp = v + m;
-  float* wp = vp + m;
-  float* y = wp + m;
-  float* red = y + m;
-  float* ywarp = red + 32;    // per-warp partial y (32 * m floats), no atomics
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-
-  // non-finite guard on the input (lower triangle)
-  {
-    int bad = 0;
-    for (int j = warp; j < m; j += nw)
-      for (int i = j + lane; i < m; i += 32) bad |= !isfinite(K[i + (long)j * ld]);
-    bad = __syncthreads_or(bad);
-    if (bad) {
-      if (tid == 0 && p.status) atomicOr(p.status, ST_NONFINITE);
-      for (int i = tid; i < m; i += nt) { p.d[i] = 0.f; p.e[i] = 0.f; p.tau[i] = 0.f; }
-      return;
-    }
-  }
-  if (m == 1) {
-    if (tid == 0) { p.d[0] = K[0]; p.e[0] = 0.f; p.tau[0] = 0.f; }
-    return;
-  }
-  bool have_prev = false;
-  for (int k = 0; k < m - 2; ++k) {
-    if (have_prev)
-      for (int i = k + tid; i < m; i += nt)
-        K[i + (long)k * ld] -= vp[i] * wp[k] + wp[i] * vp[k];
-    __syncthreads();
-    const float alpha = K[k + 1 + (long)k * ld];
-    float ss = 0.f;
-    for (int i = k + 2 + tid; i < m; i += nt) {
-      const float t = K[i + (long)k * ld];
-      ss += t * t;
-    }
-    ss = block_sum(ss, red);
-    float tau, beta, scale;
-    if (ss == 0.f) {
-      tau = 0.f; beta = alpha; scale = 0.f;
-    } else {
-      const float nrm = sqrtf(alpha * alpha + ss);
-      beta = alpha >= 0.f ? -nrm : nrm;
-      tau = (beta - alpha) / beta;
-      scale = 1.f / (alpha - beta);
-    }
-    for (int i = k + 1 + tid; i < m; i += nt) {
-      float vi = 1.f;
-      if (i >= k + 2) {
-        vi = K[i + (long)k * ld] * scale;
-        K[i + (long)k * ld] = vi;
-      }
-      v[i] = vi;
-    }
-    for (int i = k + 1 + lane; i < m; i += 32) ywarp[warp * m + i] = 0.f;
-    if (tid == 0) {
-      p.d[k] = K[k + (long)k * ld];
-      p.e[k] = beta;
-      p.tau[k] = tau;
-    }
-    __syncthreads();
-    // fused: apply the previous rank-2 update to columns j >= k+1 (rows i >= j)
-    // and accumulate y = K22 v from the lower triangle.
-    float* yw = ywarp + warp * m;
-    for (int j = k + 1 + warp; j < m; j += nw) {
-      const float vj = v[j];
-      const float wpj = have_prev ? wp[j] : 0.f, vpj = have_prev ? vp[j] : 0.f;
-      float acc = 0.f;
-      for (int i = j + lane; i < m; i += 32) {
-        float a = K[i + (long)j * ld];
-        if (have_prev) {
-          a -= vp[i] * wpj + wp[i] * vpj;
-          K[i + (long)j * ld] = a;
-        }
-        acc = fmaf(a, v[i], acc);
-        if (i > j) yw[i] = fmaf(a, vj, yw[i]);
-      }
-      acc = warp_sum(acc);
-      __syncwarp();
-      if (lane == 0) yw[j] += acc;
-      __syncwarp();
-    }
-    __syncthreads();
-    for (int i = k + 1 + tid; i < m; i += nt) {
-      float s = 0.f;
-#pragma unroll 8
-      for (int w = 0; w < nw; ++w) s += ywarp[w * m + i];
-      y[i] = s;
-    }
-    __syncthreads();
-    float pv = 0.f;
-    for (int i = k + 1 + tid; i < m; i += nt) pv += y[i] * v[i];
-    pv = block_sum(pv, red);
-    const float gamma = 0.5f * tau * tau * pv;
-    for (int i = k + 1 + tid; i < m; i += nt) {
-      wp[i] = tau * y[i] - gamma * v[i];
-      vp[i] = v[i];
-    }
-    have_prev = true;
-    __syncthreads();
-  }
-  if (have_prev) {
-    if (tid < 3) {
-      const int j = m - 2 + (tid == 2);
-      const int i = m - 2 + (tid >= 1);
-      K[i + (long)j * ld] -= vp[i] * wp[j] + wp[i] * vp[j];
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    p.d[m - 2] = K[(m - 2) + (long)(m - 2) * ld];
-    p.d[m - 1] = K[(m - 1) + (long)(m - 1) * ld];
-    p.e[m - 2] = K[(m - 1) + (long)(m - 2) * ld];
-    p.e[m - 1] = 0.f;
-    p.tau[m - 2] = 0.f;
-    p.tau[m - 1] = 0.f;
-  }
-}
 
 // ------------------------------------------------------------------ 2. bisection
 // Number of eigenvalues of T strictly below x (Sturm sequence of the LDL^T pivots).

@@ -66,6 +66,14 @@ inline size_t sytrd_tiled_smem_bytes(int m, int C) {
   return sizeof(float) * (size_t)(mx + syt_vec_floats(m_pad));
 }
 
+// Tile storage of one factor when the tiles do not fit the cluster's shared memory
+// (GT = true: one CTA per factor, tiles in global memory / L2).
+inline size_t syt_global_tile_floats(int m) {
+  const size_t NB = (size_t)(m + 31) / 32;
+  return NB * (NB + 1) / 2 * 1024;
+}
+
+template <bool GT>
 __global__ void __launch_bounds__(SYT_THREADS, 1)
 sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   cgt::cluster_group cluster = cgt::this_cluster();
@@ -82,10 +90,12 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   float* wp = ys + m_pad;            // m_pad      (w_{k-1})
   float* scal = wp + m_pad;          // 64: [0..1] tau by parity, [2] bad flag, [4..] reduce
   int* boff = reinterpret_cast<int*>(scal + 64);   // 64: storage offset of block-column J
-  float* tiles = scal + 128;         // owned block-columns
+  float* tiles = GT ? p.gtiles : scal + 128;   // owned block-columns
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = SYT_THREADS / 32;
   float* red = scal + 4;
+  // address of `ptr` in CTA r of the cluster (plain local pointer for 1-CTA launches)
+  auto rptr = [&](float* ptr, int r) -> float* { return C == 1 ? ptr : cluster.map_shared_rank(ptr, r); };
 
   if (tid == 0) {
     int off = 0;
@@ -115,10 +125,10 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   }
   bad = __syncthreads_or(bad);
   if (tid == 0) scal[2] = bad ? 1.f : 0.f;
-  cluster.sync();
+  if (C > 1) cluster.sync(); else __syncthreads();
   float anybad = 0.f;
-  for (int r = 0; r < C; ++r) anybad += *cluster.map_shared_rank(scal + 2, r);
-  cluster.sync();
+  for (int r = 0; r < C; ++r) anybad += *rptr(scal + 2, r);
+  if (C > 1) cluster.sync(); else __syncthreads();
   if (anybad != 0.f) {
     if (q == 0) {
       if (tid == 0 && p.status) atomicOr(p.status, ST_NONFINITE);
@@ -136,6 +146,12 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     return;
   }
 
+#ifdef BKFAC_SYT_TIMING
+  unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0}, tprev = clock64();
+#define SYT_T(i) do { if (tid == 0) { unsigned long long tn = clock64(); tacc[i] += tn - tprev; tprev = tn; } } while (0)
+#else
+#define SYT_T(i) do {} while (0)
+#endif
   for (int k = 0; k < m - 2; ++k) {
     float* v = vbuf + (k & 1) * m_pad;            // v_k (written by the owner)
     const float* vp = vbuf + ((k + 1) & 1) * m_pad;   // v_{k-1} (zero at k = 0)
@@ -168,61 +184,66 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
         float vi = 0.f;
         if (i == k + 1) vi = 1.f;
         else if (i >= k + 2 && i < m) { vi = ck[i] * scale; ck[i] = vi; }
-        for (int r = 0; r < C; ++r) *cluster.map_shared_rank(v + i, r) = vi;
+        for (int r = 0; r < C; ++r) *rptr(v + i, r) = vi;
       }
       if (tid == 0) {
         p.d[k] = ck[k];
         p.e[k] = beta;
         p.tau[k] = tau;
-        for (int r = 0; r < C; ++r) *cluster.map_shared_rank(scal + (k & 1), r) = tau;
+        for (int r = 0; r < C; ++r) *rptr(scal + (k & 1), r) = tau;
       }
     }
-    cluster.sync();                                              // (1) v_k, tau_k everywhere
+    SYT_T(0);
+    if (C > 1) cluster.sync(); else __syncthreads();             // (1) v_k, tau_k everywhere
+    SYT_T(1);
     const float tau = scal[k & 1];
     for (int i = tid; i < m_pad; i += SYT_THREADS) y[i] = 0.f;
     __syncthreads();
-    // (b) tiles (I >= J) of owned block-columns that have columns j > k
+    // (b) tiles (I >= J) of owned block-columns that have columns j > k, one per warp
     int tcount = 0;
     for (int J = kb; J < NB; ++J) {
       if (boff[J] < 0) continue;
       const int rows = m_pad - 32 * J;
-      const float* blkc = tiles + boff[J];
+      float* blkc = tiles + boff[J];
       const float cv = v[32 * J + lane], cvp = vp[32 * J + lane], cwp = wp[32 * J + lane];
       for (int I = J; I < NB; ++I, ++tcount) {
         if ((tcount % NW) != warp) continue;
-        float* tcol = const_cast<float*>(blkc) + 32 * (I - J) + lane;   // + jj * rows
+        float* tcol = blkc + 32 * (I - J) + lane;   // + jj * rows
         const int i = 32 * I + lane;
         const float vi = v[i], vpi = vp[i], wpi = wp[i];
-        float rowacc = 0.f;
+        // all 32 loads first: a store to column jj must not order the load of column
+        // jj+1 behind it (the compiler cannot prove they differ)
         float colv[32];
-        const bool full = (32 * J > k) && (I > J);
-        if (full) {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) colv[jj] = tcol[jj * rows];
+        float racc[4] = {0.f, 0.f, 0.f, 0.f};
+        if ((32 * J > k) && (I > J)) {
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
-            float a = tcol[jj * rows];
+            float x = colv[jj];
             if (have_prev) {
-              a -= vpi * __shfl_sync(0xffffffffu, cwp, jj) + wpi * __shfl_sync(0xffffffffu, cvp, jj);
-              tcol[jj * rows] = a;
+              x -= vpi * __shfl_sync(0xffffffffu, cwp, jj) + wpi * __shfl_sync(0xffffffffu, cvp, jj);
+              tcol[jj * rows] = x;
             }
-            rowacc = fmaf(a, __shfl_sync(0xffffffffu, cv, jj), rowacc);
-            colv[jj] = a * vi;
+            racc[jj & 3] = fmaf(x, __shfl_sync(0xffffffffu, cv, jj), racc[jj & 3]);
+            colv[jj] = x * vi;
           }
         } else {
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
             const int j = 32 * J + jj;
             const bool valid = (j > k) && (i >= j);
-            float a = tcol[jj * rows];
             const float cwpj = __shfl_sync(0xffffffffu, cwp, jj);
             const float cvpj = __shfl_sync(0xffffffffu, cvp, jj);
             const float cvj = __shfl_sync(0xffffffffu, cv, jj);
+            float x = colv[jj];
             if (valid && have_prev) {
-              a -= vpi * cwpj + wpi * cvpj;
-              tcol[jj * rows] = a;
+              x -= vpi * cwpj + wpi * cvpj;
+              tcol[jj * rows] = x;
             }
-            const float ae = valid ? a : 0.f;
-            rowacc = fmaf(ae, cvj, rowacc);
-            colv[jj] = (i > j) ? ae * vi : 0.f;
+            const float xe = valid ? x : 0.f;
+            racc[jj & 3] = fmaf(xe, cvj, racc[jj & 3]);
+            colv[jj] = (i > j) ? xe * vi : 0.f;
           }
         }
         // transpose-reduce: lane l ends with sum over lanes of colv[l]
@@ -236,16 +257,18 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
             colv[t] = keep + __shfl_xor_sync(0xffffffffu, send, s);
           }
         }
-        atomicAdd(&y[i], rowacc);
+        atomicAdd(&y[i], (racc[0] + racc[1]) + (racc[2] + racc[3]));
         atomicAdd(&y[32 * J + lane], colv[0]);
       }
     }
     __syncthreads();
-    cluster.sync();                                              // (2) partial y ready
+    SYT_T(2);
+    if (C > 1) cluster.sync();                                   // (2) partial y ready
+    SYT_T(3);
     float pv = 0.f;
     for (int i = k + 1 + tid; i < m; i += SYT_THREADS) {
       float s = 0.f;
-      for (int r = 0; r < C; ++r) s += *cluster.map_shared_rank(y + i, r);
+      for (int r = 0; r < C; ++r) s += *rptr(y + i, r);
       ys[i] = s;
       pv = fmaf(s, v[i], pv);
     }
@@ -254,7 +277,14 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     for (int i = tid; i < m_pad; i += SYT_THREADS)
       wp[i] = (i > k && i < m) ? tau * ys[i] - gamma * v[i] : 0.f;
     __syncthreads();
+    SYT_T(4);
   }
+#ifdef BKFAC_SYT_TIMING
+  if (tid == 0 && p.status) {   // tuning builds: per-phase cycle sums of CTA q
+    unsigned long long* o = reinterpret_cast<unsigned long long*>(p.Y) + 8 * q;
+    for (int i = 0; i < 5; ++i) o[i] = tacc[i];
+  }
+#endif
   // trailing 2x2 block: the pending update of step m-3, then d, e
   {
     const int k = m - 2;
@@ -300,7 +330,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       }
     }
   }
-  cluster.sync();   // no CTA exits while others may still address its shared memory
+  if (C > 1) cluster.sync();   // no CTA exits while others may still address its smem
 }
 
 }  // namespace bkfac
