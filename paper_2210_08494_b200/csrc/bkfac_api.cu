@@ -97,6 +97,9 @@ struct bkfac_ctx_s {
   uint64_t launches = 0;
   int* host_status = nullptr;
   bool use_tc = true;
+  // side streams for independent launch groups inside one call (fork/join with events)
+  cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
   // optional per-stage CUDA-event profiling (bkfac_profile_enable)
   bool prof = false;
   struct Rec { std::string tag; cudaEvent_t a, b; double flops, bytes; uint64_t launches; };
@@ -353,26 +356,40 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     // sytrd: 4/3 m^3 flops; algorithmic bytes: read K (lower), write reflectors + T
     prof_begin(ctx, "eig_sytrd", st, 4.0 / 3.0 * m3, 4.0 * m2);
     {
-      static EigBatch sub;
-      for (int C : {0, 1, 2, 4, 8}) {
-        sub.nprob = 0;
+      // one launch per cluster size; the launches are independent problems, so all but
+      // the first run on side streams (fork/join) and overlap on the GPU
+      static EigBatch sub[5];
+      int ngroups = 0;
+      const int Cs[5] = {0, 1, 2, 4, 8};
+      int gC[5], gm[5];
+      for (int ci = 0; ci < 5; ++ci) {
+        EigBatch& sb = sub[ngroups];
+        sb.nprob = 0;
         int msub = 0;
         for (size_t i = 0; i < n; ++i)
-          if (sytrd_tiled_cluster(b.p[i].m) == C) {
-            sub.p[sub.nprob++] = b.p[i];
+          if (sytrd_tiled_cluster(b.p[i].m) == Cs[ci]) {
+            sb.p[sb.nprob++] = b.p[i];
             msub = std::max(msub, b.p[i].m);
           }
-        if (sub.nprob == 0) continue;
+        if (sb.nprob == 0) continue;
+        gC[ngroups] = Cs[ci]; gm[ngroups] = msub; ++ngroups;
+      }
+      const bool fork = ngroups > 1 && ctx->ev_fork != nullptr;
+      if (fork && !cuda_ok(cudaEventRecord(ctx->ev_fork, st))) return BKFAC_ERR_CUDA;
+      for (int g = 0; g < ngroups; ++g) {
+        cudaStream_t sg = (fork && g > 0) ? ctx->side[g - 1] : st;
+        if (sg != st && !cuda_ok(cudaStreamWaitEvent(sg, ctx->ev_fork, 0))) return BKFAC_ERR_CUDA;
+        const int C = gC[g], msub = gm[g];
         if (C == 0) {   // tiles in global memory, one CTA per factor
           const int mp = (msub + 31) / 32 * 32;
-          sytrd_tiled_kernel<true><<<(unsigned)sub.nprob, SYT_THREADS,
-                                     sizeof(float) * (size_t)syt_vec_floats(mp), st>>>(sub, 1);
+          sytrd_tiled_kernel<true><<<(unsigned)sub[g].nprob, SYT_THREADS,
+                                     sizeof(float) * (size_t)syt_vec_floats(mp), sg>>>(sub[g], 1);
         } else {
           cudaLaunchConfig_t cfg = {};
-          cfg.gridDim = dim3((unsigned)(C * sub.nprob), 1, 1);
+          cfg.gridDim = dim3((unsigned)(C * sub[g].nprob), 1, 1);
           cfg.blockDim = dim3(SYT_THREADS, 1, 1);
           cfg.dynamicSmemBytes = sytrd_tiled_smem_bytes(msub, C);
-          cfg.stream = st;
+          cfg.stream = sg;
           cudaLaunchAttribute attr[1];
           attr[0].id = cudaLaunchAttributeClusterDimension;
           attr[0].val.clusterDim.x = (unsigned)C;
@@ -380,10 +397,14 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
           attr[0].val.clusterDim.z = 1;
           cfg.attrs = attr;
           cfg.numAttrs = 1;
-          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_tiled_kernel<false>, sub, C))) return BKFAC_ERR_CUDA;
+          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_tiled_kernel<false>, sub[g], C))) return BKFAC_ERR_CUDA;
         }
         LAUNCH_CHECK(ctx);
+        if (sg != st && !cuda_ok(cudaEventRecord(ctx->ev_join[g - 1], sg))) return BKFAC_ERR_CUDA;
       }
+      if (fork)
+        for (int g = 1; g < ngroups; ++g)
+          if (!cuda_ok(cudaStreamWaitEvent(st, ctx->ev_join[g - 1], 0))) return BKFAC_ERR_CUDA;
     }
     prof_end(ctx, st);
 #ifdef BKFAC_SYT_TIMING
@@ -561,6 +582,16 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   if (!attr_ok) fprintf(stderr, "bkfac: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
   cudaGetLastError();  // never leave a sticky error behind
   cudaSetDevice(dev_prev);
+  cudaSetDevice(device);
+  for (int i = 0; i < 4; ++i) {
+    if (cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking) != cudaSuccess) c->side[i] = nullptr;
+    if (cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) != cudaSuccess) c->ev_join[i] = nullptr;
+  }
+  if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess) c->ev_fork = nullptr;
+  for (int i = 0; i < 4; ++i)
+    if (!c->side[i] || !c->ev_join[i]) { if (c->ev_fork) cudaEventDestroy(c->ev_fork); c->ev_fork = nullptr; }
+  cudaGetLastError();
+  cudaSetDevice(dev_prev);
   const char* env = getenv("BKFAC_GEMM");
   c->use_tc = !(env && strcmp(env, "simt") == 0);
   *out = c;
@@ -583,6 +614,11 @@ bkfac_status bkfac_destroy(bkfac_ctx c) {
   if (!c) return BKFAC_ERR_INVALID_ARG;
   if (c->host_status) cudaFreeHost(c->host_status);
   for (auto e : c->pool) cudaEventDestroy(e);
+  for (int i = 0; i < 4; ++i) {
+    if (c->side[i]) cudaStreamDestroy(c->side[i]);
+    if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   delete c;
   return BKFAC_OK;
 }

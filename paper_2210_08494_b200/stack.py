@@ -88,6 +88,7 @@ class BKFACStack:
         self.cur = [0] * len(self.my_factors)
         self.k = 0
         self.n_overwrites = 0
+        self.side = None   # side stream for the dense EA accumulate
         self.S: Dict[int, "torch.Tensor"] = {}
         for li in self.my_layers:
             dG, dA, _, _ = self.layers[li]
@@ -115,6 +116,8 @@ class BKFACStack:
         """One step over the owned factors (M keyed by global factor index, each (c, n))
         and owned layers (J keyed by global layer index, each (d_G, d_A))."""
         k = self.k
+        torch = self.torch
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
         if k == 0:
             for i in range(len(self.my_factors)):
                 self._phantom(i)
@@ -130,8 +133,24 @@ class BKFACStack:
                                       power_iters=self.power_iters, seed=self.rsvd_seed + g,
                                       counter=self.n_overwrites, U_out=self.U[i][self.cur[i]],
                                       D_out=self.D[i][self.cur[i]]))
-                self.ctx.bkfac_rsvd_batch(items, stream)
+                self.ctx.bkfac_rsvd_batch(items, main)
                 self.n_overwrites += 1
+        ea_done = None
+        if self.rsvd_every:
+            # the dense EA accumulate (a8) needs only M_k and must follow this step's RSVD
+            # read of Mcal_{k-1}: it runs on a side stream, overlapped with the Brand update
+            if self.side is None:
+                self.side = torch.cuda.Stream(device=self.device)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self.side.wait_event(ev)
+            for g in self.my_factors:
+                M[g].record_stream(self.side)
+            self.ctx.bkfac_ea_batch([dict(factor=i, K=self.K[i], M=M[g],
+                                          rho=self.rho if k > 0 else 0.0)
+                                     for i, g in enumerate(self.my_factors)], self.side)
+            ea_done = torch.cuda.Event()
+            ea_done.record(self.side)
         ups = []
         for i, g in enumerate(self.my_factors):
             c, nx = self.cur[i], 1 - self.cur[i]
@@ -139,11 +158,7 @@ class BKFACStack:
                             U_out=self.U[i][nx], D_out=self.D[i][nx], alpha=alpha, beta=beta,
                             flags=self.brand_flags))
         if ups:
-            self.ctx.bkfac_brand_update(ups, stream)
-        if self.rsvd_every:
-            self.ctx.bkfac_ea_batch([dict(factor=i, K=self.K[i], M=M[g],
-                                          rho=self.rho if k > 0 else 0.0)
-                                     for i, g in enumerate(self.my_factors)], stream)
+            self.ctx.bkfac_brand_update(ups, main)
         for i in range(len(self.my_factors)):
             self.cur[i] = 1 - self.cur[i]
         out = {}
@@ -156,8 +171,10 @@ class BKFACStack:
                 items.append(dict(layer=lj, U_G=UG, D_G=DG, lambda_G=self.lam, U_A=UA, D_A=DA,
                                   lambda_A=self.lam, J=J[li], S=self.S[li],
                                   flags=self.precond_flags))
-            self.ctx.bkfac_precondition(items, stream)
+            self.ctx.bkfac_precondition(items, main)
             out = {li: self.S[li] for li in self.my_layers}
+        if ea_done is not None:
+            main.wait_event(ea_done)
         self.k += 1
         return out
 
