@@ -413,7 +413,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
 #endif
     prof_begin(ctx, "eig_bisect", st, 0.0, 0.0);
     bisect_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, BIS_WARPS)), BIS_WARPS * 32,
-                    sizeof(double) * 2 * (size_t)mmax, st>>>(b);
+                    sizeof(double) * 3 * (size_t)mmax, st>>>(b);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
     prof_begin(ctx, "eig_invit", st, 0.0, 8.0 * mr);

@@ -46,6 +46,19 @@ BKFAC_DEV int sturm_count(const double* dd, const double* e2, int m, double x, d
   return cnt;
 }
 
+BKFAC_DEV int sturm_count_f32(const float* dd, const float* e2, int m, float x, float pivmin) {
+  int cnt = 0;
+  float q = dd[0] - x;
+  if (fabsf(q) < pivmin) q = -pivmin;
+  cnt += (q < 0.f);
+  for (int i = 1; i < m; ++i) {
+    q = (dd[i] - x) - __fdividef(e2[i - 1], q);
+    if (fabsf(q) < pivmin) q = -pivmin;
+    cnt += (q < 0.f);
+  }
+  return cnt;
+}
+
 constexpr int BIS_WARPS = 8;
 
 // grid: (nprob, ceil(rmax / BIS_WARPS)); smem: 2*m doubles
@@ -55,12 +68,16 @@ __global__ void __launch_bounds__(BIS_WARPS * 32) bisect_kernel(const __grid_con
   extern __shared__ __align__(16) double dsm[];
   double* dd = dsm;
   double* e2 = dd + m;
+  float* ddf = reinterpret_cast<float*>(e2 + m);
+  float* e2f = ddf + m;
   __shared__ double s_lo, s_hi, s_pivmin;
   const int tid = threadIdx.x;
   for (int i = tid; i < m; i += blockDim.x) {
     dd[i] = (double)p.d[i];
     const double ee = (i < m - 1) ? (double)p.e[i] : 0.0;
     e2[i] = ee * ee;
+    ddf[i] = p.d[i];
+    e2f[i] = (float)(ee * ee);
   }
   __syncthreads();
   if (tid == 0) {
@@ -84,10 +101,31 @@ __global__ void __launch_bounds__(BIS_WARPS * 32) bisect_kernel(const __grid_con
   const int kasc = m - 1 - j;                     // ascending index
   double lo = s_lo, hi = s_hi;
   const double pivmin = s_pivmin;
-  // invariant: count(lo) <= kasc < count(hi)
-  for (int round = 0; round < 14; ++round) {
+  // invariant: count(lo) <= kasc < count(hi).  Phase 1: 32-way multisection with fp32
+  // Sturm counts (fast reciprocal) down to ~1e-6 of the spectrum's span; phase 2: the
+  // bracket, widened by the fp32 counts' backward error, refined with fp64 counts.
+  const double span = fmax(fabs(lo), fabs(hi));
+  {
+    const float pivf = 1e-30f;
+    for (int round = 0; round < 8; ++round) {
+      const double w = hi - lo;
+      if (w <= 1e-6 * span) break;
+      const float xf = (float)(lo + w * (double)(lane + 1) / 33.0);
+      const int cnt = sturm_count_f32(ddf, e2f, m, xf, pivf);
+      const unsigned above = __ballot_sync(0xffffffffu, cnt >= kasc + 1);
+      const int first = above ? __ffs(above) - 1 : 32;
+      const double nlo = (first == 0) ? lo : lo + w * (double)first / 33.0;
+      const double nhi = (first == 32) ? hi : lo + w * (double)(first + 1) / 33.0;
+      lo = nlo;
+      hi = nhi;
+    }
+    const double widen = 4e-7 * span * (1.0 + 0.01 * m);
+    lo = fmax(lo - widen, s_lo);
+    hi = fmin(hi + widen, s_hi);
+  }
+  for (int round = 0; round < 10; ++round) {
     const double w = hi - lo;
-    if (w <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) * 2.0 + pivmin) break;
+    if (w <= 1e-12 * span + pivmin) break;
     const double x = lo + w * (double)(lane + 1) / 33.0;
     const int cnt = sturm_count(dd, e2, m, x, pivmin);
     const unsigned above = __ballot_sync(0xffffffffu, cnt >= kasc + 1);
@@ -167,18 +205,34 @@ __global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigB
   AT(dU, m - 1) = dcur;
   // start vector (deterministic, distinct per eigenvector)
   for (int i = 0; i < m; ++i) AT(x, i) = hash_unit((unsigned)i, (unsigned)j) + 0.5;
+  // The passes below stream the per-vector arrays; every dependent chain (carry, x1/x2)
+  // is in registers, and the array loads of a batch of IB entries are issued before the
+  // batch's stores (the compiler cannot reorder a load past a store to x it cannot prove
+  // distinct), so one memory latency is exposed per batch instead of per entry.
+  constexpr int IB = 16;
   for (int it = 0; it < 3; ++it) {
     // forward: apply L^{-1} with row interchanges; the running entry is carried
     double carry = AT(x, 0);
-    for (int i = 0; i < m - 1; ++i) {
-      const double xn = AT(x, i + 1);
-      const double f = AT(dl, i);
-      if (AT(pv, i) == 0) {
-        AT(x, i) = carry;
-        carry = xn - f * carry;
-      } else {
-        AT(x, i) = xn;
-        carry = carry - f * xn;
+    for (int i0 = 0; i0 < m - 1; i0 += IB) {
+      double xn[IB], f[IB];
+      unsigned char pw[IB];
+#pragma unroll
+      for (int u = 0; u < IB; ++u) {
+        const int i = i0 + u;
+        if (i < m - 1) { xn[u] = AT(x, i + 1); f[u] = AT(dl, i); pw[u] = AT(pv, i); }
+      }
+#pragma unroll
+      for (int u = 0; u < IB; ++u) {
+        const int i = i0 + u;
+        if (i < m - 1) {
+          if (pw[u] == 0) {
+            AT(x, i) = carry;
+            carry = xn[u] - f[u] * carry;
+          } else {
+            AT(x, i) = xn[u];
+            carry = carry - f[u] * xn[u];
+          }
+        }
       }
     }
     // back substitution with U (bandwidth 2); x1, x2 carried
@@ -186,12 +240,24 @@ __global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigB
     double x2 = 0.0;
     double amax = fabs(x1);
     AT(x, m - 1) = x1;
-    for (int i = m - 2; i >= 0; --i) {
-      const double xi = (AT(x, i) - AT(du, i) * x1 - AT(du2, i) * x2) / AT(dU, i);
-      AT(x, i) = xi;
-      x2 = x1;
-      x1 = xi;
-      amax = fmax(amax, fabs(xi));
+    for (int i0 = m - 2; i0 >= 0; i0 -= IB) {
+      double xv[IB], a0[IB], a1[IB], a2[IB];
+#pragma unroll
+      for (int u = 0; u < IB; ++u) {
+        const int i = i0 - u;
+        if (i >= 0) { xv[u] = AT(x, i); a0[u] = AT(dU, i); a1[u] = AT(du, i); a2[u] = AT(du2, i); }
+      }
+#pragma unroll
+      for (int u = 0; u < IB; ++u) {
+        const int i = i0 - u;
+        if (i >= 0) {
+          const double xi = (xv[u] - a1[u] * x1 - a2[u] * x2) / a0[u];
+          AT(x, i) = xi;
+          x2 = x1;
+          x1 = xi;
+          amax = fmax(amax, fabs(xi));
+        }
+      }
     }
     // normalise: scale by 1/max, then by 1/||x||_2 (two streaming passes)
     const double s1 = (amax > 0.0 && isfinite(amax)) ? 1.0 / amax : 1.0;
