@@ -246,6 +246,12 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       p.tiles_n = ceil_div(std::max(p.N, 1), bn);
       if (p.M <= 0 || p.N <= 0) p.tiles_m = p.tiles_n = 0;
       if (!tc || p.M != p.N || bm != bn) p.sym = 0;   // mirrored tiles: tcgen05 square tiles only
+      {
+        auto al = [](const float* q, int ld) {
+          return q == nullptr || ((reinterpret_cast<uintptr_t>(q) & 15) == 0 && (ld & 3) == 0);
+        };
+        p.vec = ((al(p.A, p.lda) && al(p.A2, p.lda2)) ? 1 : 0) | ((al(p.B, p.ldb) && al(p.B2, p.ldb2)) ? 2 : 0);
+      }
       base_tiles += p.sym ? (long)p.tiles_m * (p.tiles_m + 1) / 2 : (long)p.tiles_m * p.tiles_n;
     }
   const long target = tc ? (long)kNumSM : 2L * kNumSM;
@@ -1198,6 +1204,12 @@ bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha
   return run_gemms(&tmp, gs, static_cast<cudaStream_t>(stream), "gemm_user");
 }
 
+#ifdef BKFAC_TC_TIMING
+void bkfac_debug_tc(unsigned long long* host, int reset) {
+  if (reset) { static unsigned long long z[148 * 8]; cudaMemcpyToSymbol(g_tc_dbg, z, sizeof(z)); return; }
+  cudaMemcpyFromSymbol(host, g_tc_dbg, sizeof(unsigned long long) * 148 * 8);
+}
+#endif
 #ifdef BKFAC_SYT_TIMING
 // tuning builds only (not part of the ABI): device address of a factor's eigensolver
 // scratch, where BKFAC_SYT_TIMING kernels leave per-phase cycle sums.

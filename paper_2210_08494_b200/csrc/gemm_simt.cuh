@@ -20,6 +20,7 @@ struct GemmProb {
   const float* beta_dev;   // if non-null, beta = *beta_dev (device scalar)
   int splits, kchunk, tiles_m, tiles_n, tile_start;
   int sym;                 // tcgen05 path: C = C^T known (e.g. M M^T): lower tiles only, mirrored
+  int vec;                 // tcgen05 path: bit 0 A (and A2), bit 1 B (and B2) 16-byte aligned
 };
 
 constexpr int GEMM_MAXP = 100;

@@ -79,7 +79,11 @@ struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 4;          // one half (hi or lo)
   static constexpr int B_BYTES = BN * TC_BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+#ifdef BKFAC_TC_STAGES
+  static constexpr int STAGES = BKFAC_TC_STAGES;
+#else
   static constexpr int STAGES = (BN >= 256) ? 2 : 3;
+#endif
   static constexpr int TMEM_COLS = 4 * BN;                   // 2 K-block buffers + running sum
   static constexpr int LINES = TC_BM + BN;                   // 128-byte lines per stage half
   static constexpr int LPW = LINES / NLW;                    // lines per loader warp
@@ -262,6 +266,9 @@ BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
   return x;
 }
 
+#ifdef BKFAC_TC_TIMING
+__device__ unsigned long long g_tc_dbg[148 * 8];   // tuning builds: per-CTA MMA-warp cycle sums
+#endif
 // ----------------------------------------------------------------------- kernel
 template <bool TA, bool TB, int BN, int NLW, int DEPTH>
 __global__ void __launch_bounds__(TcCfg<BN, NLW, DEPTH>::THREADS, 1)
@@ -306,30 +313,53 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
   if (warp == TC_MMA_WARP) {
     // ------------------------------------------------------------- MMA issuer
     constexpr uint32_t IDESC = umma_idesc_tf32<BN>(!TA, TB);
-    int stage = 0; uint32_t phase = 0;
-    int kb = 0;   // K-block counter over all tiles of this CTA (TMEM buffer = kb & 1)
-    for (int t = blockIdx.x; t < b.total_tiles; t += gridDim.x) {
-      const TcTile x = tc_tile<BN>(b, t);
-      for (int c0 = x.c_beg; c0 < x.c_end; c0 += TC_PROMO, ++kb) {
-        const int buf = kb & 1;
-        mbar_wait(tempty_bar(buf), ((kb >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
-        const int c1 = min(x.c_end, c0 + TC_PROMO);
-        for (int c = c0; c < c1; ++c) {
-          mbar_wait(full_bar(stage), phase);
+    // k-step strides of the start-address field: K-major 32 B, MN-major two 4-row groups
+    constexpr uint32_t STEP_A = TA ? 2u : (2u * (TC_BM / 32 * 512)) >> 4;
+    constexpr uint32_t STEP_B = TB ? (2u * (BN / 32 * 512)) >> 4 : 2u;
+    const uint64_t dAH = tc_op_desc<!TA, TC_BM>(sbase, 0);
+    const uint64_t dAL = tc_op_desc<!TA, TC_BM>(sbase + Cfg::A_BYTES, 0);
+    const uint64_t dBH = tc_op_desc<TB, BN>(sbase + 2 * Cfg::A_BYTES, 0);
+    const uint64_t dBL = tc_op_desc<TB, BN>(sbase + 2 * Cfg::A_BYTES + Cfg::B_BYTES, 0);
+    // one thread runs the whole issue loop: the tensor pipe's instruction queue is shallow,
+    // so every cycle the issuer spends on warp-wide waits or shuffles is pipe idle time
+    if (lane == 0) {
+      int stage = 0; uint32_t phase = 0;
+      int kb = 0;   // K-block counter over all tiles of this CTA (TMEM buffer = kb & 1)
+      for (int t = blockIdx.x; t < b.total_tiles; t += gridDim.x) {
+        const TcTile x = tc_tile<BN>(b, t);
+        for (int c0 = x.c_beg; c0 < x.c_end; c0 += TC_PROMO, ++kb) {
+          const int buf = kb & 1;
+#ifdef BKFAC_TC_TIMING
+          unsigned long long t0 = clock64();
+#endif
+          mbar_wait(tempty_bar(buf), ((kb >> 1) & 1) ^ 1);
+#ifdef BKFAC_TC_TIMING
+          g_tc_dbg[blockIdx.x * 8 + 0] += clock64() - t0;
+#endif
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t sA = sbase + stage * Cfg::STAGE_BYTES;
-            const uint32_t sAlo = sA + Cfg::A_BYTES;
-            const uint32_t sB = sA + 2 * Cfg::A_BYTES;
-            const uint32_t sBlo = sB + Cfg::B_BYTES;
+          const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
+          const int c1 = min(x.c_end, c0 + TC_PROMO);
+          for (int c = c0; c < c1; ++c) {
+#ifdef BKFAC_TC_TIMING
+            unsigned long long t1 = clock64();
+#endif
+#ifndef BKFAC_TC_DEBUG_NOFULLWAIT
+            mbar_wait(full_bar(stage), phase);
+#endif
+#ifdef BKFAC_TC_TIMING
+            unsigned long long t2 = clock64();
+            g_tc_dbg[blockIdx.x * 8 + 1] += t2 - t1;
+#endif
+            tc_fence_after();
+            // descriptors: precomputed stage-0 bases + (stage, k-step) offsets in 16-byte
+            // units (start-address field; smem < 256 KB, so no carry out of the field)
+            const uint64_t so = (uint64_t)((stage * Cfg::STAGE_BYTES) >> 4);
 #pragma unroll
             for (int ks = 0; ks < TC_BK / 8; ++ks) {
-              const uint64_t aH = tc_op_desc<!TA, TC_BM>(sA, ks);
-              const uint64_t aL = tc_op_desc<!TA, TC_BM>(sAlo, ks);
-              const uint64_t bH = tc_op_desc<TB, BN>(sB, ks);
-              const uint64_t bL = tc_op_desc<TB, BN>(sBlo, ks);
+              const uint64_t aH = dAH + so + (uint64_t)(ks * STEP_A);
+              const uint64_t aL = dAL + so + (uint64_t)(ks * STEP_A);
+              const uint64_t bH = dBH + so + (uint64_t)(ks * STEP_B);
+              const uint64_t bL = dBL + so + (uint64_t)(ks * STEP_B);
               const uint32_t first = (c == c0 && ks == 0) ? 0u : 1u;
 #ifndef BKFAC_TC_DEBUG_ONEPASS
               tc_mma_tf32(tmem_d, aL, bH, IDESC, first);   // small terms first
@@ -340,14 +370,17 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 #endif
             }
             tc_commit(empty_bar(stage));
+#ifdef BKFAC_TC_TIMING
+            g_tc_dbg[blockIdx.x * 8 + 2] += clock64() - t2;
+            g_tc_dbg[blockIdx.x * 8 + 3] += 1;
+#endif
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
           }
-          __syncwarp();
-          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+          tc_commit(tfull_bar(buf));
         }
-        if (lane == 0) tc_commit(tfull_bar(buf));
-        __syncwarp();
       }
     }
+    __syncwarp();
   } else if (warp > TC_MMA_WARP) {
     // ------------------------------------------------------------- loaders
     const int lw = warp - TC_MMA_WARP - 1;
@@ -363,7 +396,27 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
       }
       return false;
     };
-    auto load = [&](float (&v)[Cfg::LPW]) {
+    // Lines are handled in quads (4 consecutive lines; quad g = lw + qd * NLW).  A quad
+    // whose operand is 16-byte aligned (base and leading dimension) is loaded with one
+    // LDG.128 per lane (lane: line 4g + lane/8, elements 4*(lane%8) .. +3) and stored with
+    // STS.128; otherwise with four coalesced LDG.32 (lane = element of each of the 4
+    // lines) and scalar stores.  Both keep 4 values per lane per quad.
+    constexpr int NQ = Cfg::LPW / 4;
+    auto line_src = [&](const GemmProb& p, const float* Ap, const float* Bp, long lda, long ldb,
+                        int ks, int klen, int l, int e, bool& ok) -> const float* {
+      if (l < TC_BM) {
+        if (TA) { const int i = x.m0 + l, k = ks + e; ok = i < p.M && k < klen; return Ap + k + (long)i * lda; }
+        const int k = ks + (l & 31), i = x.m0 + ((l >> 5) << 5) + e;
+        ok = i < p.M && k < klen;
+        return Ap + i + (long)k * lda;
+      }
+      const int lb = l - TC_BM;
+      if (!TB) { const int j = x.n0 + lb, k = ks + e; ok = j < p.N && k < klen; return Bp + k + (long)j * ldb; }
+      const int k = ks + (lb & 31), j = x.n0 + ((lb >> 5) << 5) + e;
+      ok = j < p.N && k < klen;
+      return Bp + j + (long)k * ldb;
+    };
+    auto load = [&](float (&v)[Cfg::LPW], int& vmode) {
       const GemmProb& p = b.p[x.pi];
       const int seg = c < x.nc1 ? 0 : 1;
       const int ks = (seg ? c - x.nc1 : c) * TC_BK;
@@ -372,90 +425,92 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
       const float* Bp = seg ? p.B2 : p.B;
       const long lda = seg ? p.lda2 : p.lda;
       const long ldb = seg ? p.ldb2 : p.ldb;
+      vmode = p.vec;
 #pragma unroll
-      for (int q = 0; q < Cfg::LPW; ++q) {
-        const int l = lw + q * TC_LOAD_WARPS;
-        float val = 0.f;
-        if (l < TC_BM) {
-          if (TA) {            // K-major line: row m0+l, k = ks + lane
-            const int i = x.m0 + l, k = ks + lane;
-            if (i < p.M && k < klen) val = TC_LDG(Ap + k + (long)i * lda);
-          } else {             // MN-major line: k = ks + (l & 31), rows m0 + 32*(l>>5) + lane
-            const int k = ks + (l & 31), i = x.m0 + ((l >> 5) << 5) + lane;
-            if (i < p.M && k < klen) val = TC_LDG(Ap + i + (long)k * lda);
+      for (int qd = 0; qd < NQ; ++qd) {
+        const int g = lw + qd * TC_LOAD_WARPS;
+        const bool isA = 4 * g < TC_BM;
+        const bool vec = isA ? (p.vec & 1) : (p.vec & 2);
+        if (vec) {
+          const int l = 4 * g + (lane >> 3), e0 = (lane & 7) * 4;
+          bool ok0, ok3;
+          const float* src = line_src(p, Ap, Bp, lda, ldb, ks, klen, l, e0, ok0);
+          line_src(p, Ap, Bp, lda, ldb, ks, klen, l, e0 + 3, ok3);
+          if (ok0 && ok3) {
+            const float4 w = __ldg(reinterpret_cast<const float4*>(src));
+            v[4 * qd + 0] = w.x; v[4 * qd + 1] = w.y; v[4 * qd + 2] = w.z; v[4 * qd + 3] = w.w;
+          } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              bool ok;
+              const float* s1 = line_src(p, Ap, Bp, lda, ldb, ks, klen, l, e0 + t, ok);
+              v[4 * qd + t] = ok ? __ldg(s1) : 0.f;
+            }
           }
         } else {
-          const int lb = l - TC_BM;
-          if (!TB) {           // K-major line: column n0+lb, k = ks + lane
-            const int j = x.n0 + lb, k = ks + lane;
-            if (j < p.N && k < klen) val = TC_LDG(Bp + k + (long)j * ldb);
-          } else {             // MN-major line: k = ks + (lb & 31), cols n0 + 32*(lb>>5) + lane
-            const int k = ks + (lb & 31), j = x.n0 + ((lb >> 5) << 5) + lane;
-            if (j < p.N && k < klen) val = TC_LDG(Bp + j + (long)k * ldb);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            bool ok;
+            const float* s1 = line_src(p, Ap, Bp, lda, ldb, ks, klen, 4 * g + t, lane, ok);
+            v[4 * qd + t] = ok ? __ldg(s1) : 0.f;
           }
         }
-        v[q] = val;
       }
     };
-    auto store = [&](const float (&v)[Cfg::LPW]) {
+    auto store = [&](const float (&v)[Cfg::LPW], int vmode) {
       mbar_wait(empty_bar(stage), phase ^ 1);
       const uint32_t st = sbase + stage * Cfg::STAGE_BYTES;
+#ifndef BKFAC_TC_DEBUG_NOSTORE
 #pragma unroll
-      for (int q = 0; q < Cfg::LPW; ++q) {
-        const int l = lw + q * TC_LOAD_WARPS;
-        const float hi = tf32_round(v[q]);
-        const float lo = v[q] - hi;
-        uint32_t dh, dl;
-        if (l < TC_BM) {
-          dh = st + tc_line_off<!TA, TC_BM>(l, lane);
-          dl = dh + Cfg::A_BYTES;
+      for (int qd = 0; qd < NQ; ++qd) {
+        const int g = lw + qd * TC_LOAD_WARPS;
+        const bool isA = 4 * g < TC_BM;
+        const bool vec = isA ? (vmode & 1) : (vmode & 2);
+        if (vec) {
+          const int l = 4 * g + (lane >> 3), e0 = (lane & 7) * 4;
+          uint32_t dh, dl;
+          if (isA) { dh = st + tc_line_off<!TA, TC_BM>(l, e0); dl = dh + Cfg::A_BYTES; }
+          else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, e0); dl = dh + Cfg::B_BYTES; }
+          float h[4], lo[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) { h[t] = tf32_round(v[4 * qd + t]); lo[t] = v[4 * qd + t] - h[t]; }
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dh), "f"(h[0]), "f"(h[1]), "f"(h[2]), "f"(h[3]));
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dl), "f"(lo[0]), "f"(lo[1]), "f"(lo[2]), "f"(lo[3]));
         } else {
-          dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, lane);
-          dl = dh + Cfg::B_BYTES;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int l = 4 * g + t;
+            const float hi = tf32_round(v[4 * qd + t]);
+            const float lo = v[4 * qd + t] - hi;
+            uint32_t dh, dl;
+            if (isA) { dh = st + tc_line_off<!TA, TC_BM>(l, lane); dl = dh + Cfg::A_BYTES; }
+            else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, lane); dl = dh + Cfg::B_BYTES; }
+            sts_f32(dh, hi);
+            sts_f32(dl, lo);
+          }
         }
-        sts_f32(dh, hi);
-        sts_f32(dl, lo);
       }
+#endif
+#ifndef BKFAC_TC_DEBUG_NOFENCE
       fence_proxy_async_smem();
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(full_bar(stage));
       if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
     };
-    if constexpr (DEPTH == 1) {
-      float va[Cfg::LPW], vb[Cfg::LPW];
-      bool have = seek();
-      if (have) { load(va); ++c; }
-      while (have) {
-        const bool more = seek();
-        if (more) { load(vb); ++c; }
-        store(va);
-        if (!more) break;
-        const bool more2 = seek();
-        if (more2) { load(va); ++c; }
-        store(vb);
-        have = more2;
-      }
-    } else {
-      // three register buffers, two chunks of loads in flight while one is stored
-      float v0[Cfg::LPW], v1[Cfg::LPW], v2[Cfg::LPW];
-      bool h0 = seek();
-      if (h0) { load(v0); ++c; }
-      bool h1 = h0 && seek();
-      if (h1) { load(v1); ++c; }
-      while (h0) {
-        const bool h2 = h1 && seek();
-        if (h2) { load(v2); ++c; }
-        store(v0);
-        if (!h1) break;
-        const bool h3 = h2 && seek();
-        if (h3) { load(v0); ++c; }
-        store(v1);
-        if (!h2) break;
-        const bool h4 = h3 && seek();
-        if (h4) { load(v1); ++c; }
-        store(v2);
-        h0 = h3; h1 = h4;
-      }
+    float va[Cfg::LPW], vb[Cfg::LPW];
+    int ma = 0, mb = 0;
+    bool have = seek();
+    if (have) { load(va, ma); ++c; }
+    while (have) {
+      const bool more = seek();
+      if (more) { load(vb, mb); ++c; }
+      store(va, ma);
+      if (!more) break;
+      const bool more2 = seek();
+      if (more2) { load(va, ma); ++c; }
+      store(vb, mb);
+      have = more2;
     }
   } else {
     // ------------------------------------------------------------- epilogue
@@ -479,6 +534,9 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 #pragma unroll 1
         for (int g = 0; g < BN / 16; ++g) {
           if (last && x.n0 + g * 16 >= p.N) break;      // warp-uniform
+#ifdef BKFAC_TC_DEBUG_NOEPI
+          if (!last) break;                             // tuning only: skip promotion
+#endif
           float v[16];
           tmem_ld16(src + g * 16, v);
           if (blk > 0) {

@@ -78,3 +78,29 @@ def test_simt_path_same_contract(cuda_lib):
     from paper_2210_08494_b200 import binding
     err = _run(False, True, 300, 260, 333, 1.0, 1.0, binding.BKFAC_GEMM_SIMT, seed=4)
     assert err < 1e-6
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
+def test_tc_gemm_misaligned_base(cuda_lib, ta, tb):
+    """Operands whose base address is 4-byte but not 16-byte aligned (leading dimension
+    a multiple of 4) must take the scalar loader path and still be exact to 3xTF32."""
+    import torch
+    from paper_2210_08494_b200 import binding
+    M, N, K = 256, 192, 300
+    rng = np.random.default_rng(21)
+    A = _mat(rng, M, K) if ta else _mat(rng, K, M)
+    B = _mat(rng, K, N) if tb else _mat(rng, N, K)
+    bufA = torch.empty(A.size + 1, device="cuda"); bufB = torch.empty(B.size + 1, device="cuda")
+    tA = bufA[1:].view(*A.shape); tA.copy_(torch.from_numpy(A))
+    tB = bufB[1:].view(*B.shape); tB.copy_(torch.from_numpy(B))
+    C = torch.zeros((N, M), device="cuda")
+    binding.bkfac_gemm(ta, tb, 1.0, tA, tB, 0.0, C)
+    torch.cuda.synchronize()
+    opA = A.astype(np.float64) if ta else A.T.astype(np.float64)
+    opB = B.T.astype(np.float64).T if tb else B.T.astype(np.float64)
+    opA = A.T.T.astype(np.float64) if ta else A.T.astype(np.float64)
+    opB = B.astype(np.float64) if tb else B.T.astype(np.float64)
+    ref = opA @ opB
+    got = C.cpu().numpy().T
+    err = np.abs(got - ref).max() / (np.abs(opA) @ np.abs(opB)).max()
+    assert err < 1e-6
