@@ -269,6 +269,82 @@ BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
 #ifdef BKFAC_TC_TIMING
 __device__ unsigned long long g_tc_dbg[148 * 8];   // tuning builds: per-CTA MMA-warp cycle sums
 #endif
+// Epilogue warps 0-3 (thread = tile row = TMEM lane): promote each K-block accumulator
+// into the running sum (TMEM), then alpha/beta and coalesced stores of the tile.
+template <int BN>
+BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int lane,
+                           uint32_t tfull0, uint32_t tfull1, uint32_t tempty0, uint32_t tempty1) {
+  auto tfull_bar = [&](int a) { return a ? tfull1 : tfull0; };
+  auto tempty_bar = [&](int a) { return a ? tempty1 : tempty0; };
+    const int row = warp * 32 + lane;                         // TMEM lane = tile row
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t run = tmem_base + lane_off + 2 * BN;       // running-sum columns
+    int kb = 0;
+    for (int t = blockIdx.x; t < b.total_tiles; t += gridDim.x) {
+      const TcTile x = tc_tile<BN>(b, t);
+      const GemmProb& p = b.p[x.pi];
+      const int nblk = (x.c_end - x.c_beg + TC_PROMO - 1) / TC_PROMO;
+      const int i = x.m0 + row;
+      const float beta = p.beta_dev ? *p.beta_dev : p.beta;
+      float* w = p.splits > 1 ? p.ws + (long)x.split * p.M * p.N : nullptr;
+      for (int blk = 0; blk < nblk; ++blk, ++kb) {
+        const int buf = kb & 1;
+        const bool last = blk == nblk - 1;
+        mbar_wait(tfull_bar(buf), (kb >> 1) & 1);
+        tc_fence_after();
+        const uint32_t src = tmem_base + lane_off + (uint32_t)(buf * BN);
+#pragma unroll 1
+        for (int g = 0; g < BN / 16; ++g) {
+          if (last && x.n0 + g * 16 >= p.N) break;      // warp-uniform
+#ifdef BKFAC_TC_DEBUG_NOEPI
+          if (!last) break;                             // tuning only: skip promotion
+#endif
+          float v[16];
+          tmem_ld16(src + g * 16, v);
+          if (blk > 0) {
+            float r[16];
+            tmem_ld16(run + g * 16, r);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] += r[j];
+          }
+          if (!last) {
+            tmem_st16(run + g * 16, v);
+          } else if (i < p.M) {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int j = x.n0 + g * 16 + jj;
+              if (j < p.N) {
+                if (w) {
+                  w[i + (long)j * p.M] = v[jj];
+                } else {
+                  float o = p.alpha * v[jj];
+                  if (beta != 0.f) o += beta * p.C0[i + (long)j * p.ldc0];
+                  p.C[i + (long)j * p.ldc] = o;
+                  if (p.sym && x.m0 != x.n0) p.C[j + (long)i * p.ldc] = o;   // mirror tile
+                }
+              }
+            }
+          }
+        }
+        if (!last) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_bar(buf));
+      }
+      if (nblk == 0 && i < p.M) {     // empty K range (split beyond K or K = 0)
+        for (int j = x.n0; j < min(p.N, x.n0 + BN); ++j) {
+          if (w) {
+            w[i + (long)j * p.M] = 0.f;
+          } else {
+            float o = 0.f;
+            if (beta != 0.f) o += beta * p.C0[i + (long)j * p.ldc0];
+            p.C[i + (long)j * p.ldc] = o;
+          }
+        }
+      }
+    }
+  }
+
 // ----------------------------------------------------------------------- kernel
 template <bool TA, bool TB, int BN, int NLW, int DEPTH>
 __global__ void __launch_bounds__(TcCfg<BN, NLW, DEPTH>::THREADS, 1)
@@ -514,73 +590,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     }
   } else {
     // ------------------------------------------------------------- epilogue
-    const int row = warp * 32 + lane;                         // TMEM lane = tile row
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    const uint32_t run = tmem_base + lane_off + 2 * BN;       // running-sum columns
-    int kb = 0;
-    for (int t = blockIdx.x; t < b.total_tiles; t += gridDim.x) {
-      const TcTile x = tc_tile<BN>(b, t);
-      const GemmProb& p = b.p[x.pi];
-      const int nblk = (x.c_end - x.c_beg + TC_PROMO - 1) / TC_PROMO;
-      const int i = x.m0 + row;
-      const float beta = p.beta_dev ? *p.beta_dev : p.beta;
-      float* w = p.splits > 1 ? p.ws + (long)x.split * p.M * p.N : nullptr;
-      for (int blk = 0; blk < nblk; ++blk, ++kb) {
-        const int buf = kb & 1;
-        const bool last = blk == nblk - 1;
-        mbar_wait_sleep(tfull_bar(buf), (kb >> 1) & 1);
-        tc_fence_after();
-        const uint32_t src = tmem_base + lane_off + (uint32_t)(buf * BN);
-#pragma unroll 1
-        for (int g = 0; g < BN / 16; ++g) {
-          if (last && x.n0 + g * 16 >= p.N) break;      // warp-uniform
-#ifdef BKFAC_TC_DEBUG_NOEPI
-          if (!last) break;                             // tuning only: skip promotion
-#endif
-          float v[16];
-          tmem_ld16(src + g * 16, v);
-          if (blk > 0) {
-            float r[16];
-            tmem_ld16(run + g * 16, r);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] += r[j];
-          }
-          if (!last) {
-            tmem_st16(run + g * 16, v);
-          } else if (i < p.M) {
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-              const int j = x.n0 + g * 16 + jj;
-              if (j < p.N) {
-                if (w) {
-                  w[i + (long)j * p.M] = v[jj];
-                } else {
-                  float o = p.alpha * v[jj];
-                  if (beta != 0.f) o += beta * p.C0[i + (long)j * p.ldc0];
-                  p.C[i + (long)j * p.ldc] = o;
-                  if (p.sym && x.m0 != x.n0) p.C[j + (long)i * p.ldc] = o;   // mirror tile
-                }
-              }
-            }
-          }
-        }
-        if (!last) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty_bar(buf));
-      }
-      if (nblk == 0 && i < p.M) {     // empty K range (split beyond K or K = 0)
-        for (int j = x.n0; j < min(p.N, x.n0 + BN); ++j) {
-          if (w) {
-            w[i + (long)j * p.M] = 0.f;
-          } else {
-            float o = 0.f;
-            if (beta != 0.f) o += beta * p.C0[i + (long)j * p.ldc0];
-            p.C[i + (long)j * p.ldc] = o;
-          }
-        }
-      }
-    }
+    tc_epilogue<BN>(b, tmem_base, warp, lane, tfull_bar(0), tfull_bar(1), tempty_bar(0), tempty_bar(1));
   }
   tc_fence_before();
   __syncthreads();
