@@ -64,6 +64,7 @@ typedef enum {
 
 /* bkfac_brand_args.flags */
 #define BKFAC_BRAND_NO_REORTH 1   /* skip the second (CGS2) projection against U           */
+#define BKFAC_BRAND_NO_REFRESH 2  /* skip the orthonormality refresh of U_out (R8)  */
 
 /* bkfac_precond_args.flags */
 #define BKFAC_PRECOND_CONTINUATION 1    /* lambda <- lambda + min D, D <- D - min D (:711)  */

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libbkfac.so")
 
 BKFAC_FACTOR_DENSE_EA = 1
 BKFAC_BRAND_NO_REORTH = 1
+BKFAC_BRAND_NO_REFRESH = 2
 BKFAC_PRECOND_CONTINUATION = 1
 BKFAC_PRECOND_LAMBDA_RELATIVE = 2
 BKFAC_GEMM_TCGEN05 = 0

@@ -42,7 +42,7 @@ struct Arena {
 };
 
 struct EigWs {  // workspace of one eigen problem of order <= m with <= r outputs
-  size_t K, d, e, tau, lam, Y, scr, piv, V, gt;
+  size_t K, d, e, tau, lam, Y, scr, piv, V, gt, U, Z, S;
   int m, r;
 };
 
@@ -58,6 +58,9 @@ void plan_eig(Arena& a, EigWs& w, int m, int r) {
   w.scr = a.take(sizeof(double) * 4 * (size_t)m * r);
   w.piv = a.take((size_t)m * r);
   w.V = a.take(sizeof(float) * (size_t)m * r);
+  w.U = a.take(sizeof(float) * (size_t)m * std::max(bt_panels(m), 1) * BT_PW);
+  w.Z = a.take(sizeof(float) * (size_t)BT_PW * r);
+  w.S = a.take(sizeof(float) * (size_t)std::max(bt_panels(m), 1) * 2 * BT_PW * BT_PW);
 }
 
 struct FactorPlan {
@@ -69,6 +72,9 @@ struct FactorPlan {
   size_t ws_elems = 0;
   // dense path
   size_t T;
+  // orthonormality refresh of the output basis (both paths): U' before, U'^T U', split-K
+  size_t Urot, Gref, wsr;
+  size_t wsr_elems = 0;
   EigWs eig;
   // RSVD
   bool rsvd = false;
@@ -159,6 +165,7 @@ void prof_end(bkfac_ctx c, cudaStream_t st) {
 
 // ------------------------------------------------------------------ GEMM stage
 struct GemmStage {
+  bool fp32_simt = false;   // this stage on the fp32 CUDA-core kernel (accuracy-critical, small)
   std::vector<GemmProb> probs[4];
   std::vector<long> caps[4];
   void add(bool ta, bool tb, const GemmProb& p, long ws_cap_elems) {
@@ -237,7 +244,7 @@ bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char*
 // tiles, one persistent CTA per SM.  Splits only when a stage has fewer tiles than the
 // machine has SMs (x2 for SIMT); the reduction order is fixed (deterministic).
 bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
-  const bool tc = ctx->use_tc;
+  const bool tc = ctx->use_tc && !s.fp32_simt;
   const int bm = tc ? TC_BM : SG_BM, bn = tc ? TC_BN : SG_BN;
   long base_tiles = 0;
   for (int v = 0; v < 4; ++v)
@@ -297,6 +304,7 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
   if ((r = launch_variant<true, false>(ctx, s.probs[2], st, tc)) != BKFAC_OK) return r;
   if ((r = launch_variant<true, true>(ctx, s.probs[3], st, tc)) != BKFAC_OK) return r;
   for (int v = 0; v < 4; ++v) { s.probs[v].clear(); s.caps[v].clear(); }
+  s.fp32_simt = false;
   return BKFAC_OK;
 }
 
@@ -431,12 +439,70 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     cluster_kernel<<<(unsigned)n, 1024, 0, st>>>(b);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
-    // back-transform: 2 m^2 r flops (m-2 reflectors on r columns); bytes: reflectors + Y + V
-    prof_begin(ctx, "eig_backtr", st, 2.0 * m2r, 2.0 * m2 + 12.0 * mr);
-    backtr_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, 32)), 1024,
-                    sizeof(float) * 33 * (size_t)mmax, st>>>(b);
-    LAUNCH_CHECK(ctx);
-    prof_end(ctx, st);
+    // back-transform V = H Y, blocked (eig.cuh 5'): 2 m^2 r flops in two GEMMs per panel
+    // of BT_PW reflectors, applied last panel first
+    {
+      int pmax = 0;
+      for (size_t i = 0; i < n; ++i) pmax = std::max(pmax, bt_panels(b.p[i].m));
+      prof_begin(ctx, "eig_backtr", st, 0.0, 4.0 * m2 + 12.0 * mr);
+      backtr_prep_kernel<<<dim3((unsigned)n, 64), 256, 0, st>>>(b);
+      LAUNCH_CHECK(ctx);
+      prof_end(ctx, st);
+      GemmStage gs;
+      bkfac_status rs2;
+      if (pmax > 0) {
+        for (size_t i = 0; i < n; ++i) {      // S_j = W_j^T W_j
+          const EigProb& q = b.p[i];
+          for (int j = 0; j < bt_panels(q.m); ++j) {
+            const int r0 = j * BT_PW + 1, np = std::min(BT_PW, q.m - 2 - j * BT_PW);
+            const float* Wj = q.K + r0 + (long)(j * BT_PW) * q.ldk;
+            gs.add(true, false, gp(Wj, q.ldk, Wj, q.ldk, q.Sw + (long)j * 2 * BT_PW * BT_PW, BT_PW, np, np,
+                                   q.m - r0, 1.f), 0);
+          }
+        }
+        // S and U define the compact-WY operator I - W T W^T: their errors become departures
+        // from orthogonality of V, so they run in plain fp32 (small: 2 m PW^2 per panel)
+        gs.fp32_simt = true;
+        if ((rs2 = run_gemms(ctx, gs, st, "gemm_backtr_s")) != BKFAC_OK) return rs2;
+        prof_begin(ctx, "eig_backtr", st, 0.0, 0.0);
+        backtr_t_kernel<<<dim3((unsigned)n, (unsigned)pmax), BT_THREADS, bt_smem_bytes(), st>>>(b);
+        LAUNCH_CHECK(ctx);
+        prof_end(ctx, st);
+        for (size_t i = 0; i < n; ++i) {      // U_j = W_j T_j
+          const EigProb& q = b.p[i];
+          for (int j = 0; j < bt_panels(q.m); ++j) {
+            const int r0 = j * BT_PW + 1, np = std::min(BT_PW, q.m - 2 - j * BT_PW);
+            gs.add(false, false, gp(q.K + r0 + (long)(j * BT_PW) * q.ldk, q.ldk,
+                                    q.Sw + (long)j * 2 * BT_PW * BT_PW + BT_PW * BT_PW, BT_PW,
+                                    q.Uw + (long)(j * BT_PW) * q.m + r0, q.m, q.m - r0, np, np, 1.f), 0);
+          }
+        }
+        gs.fp32_simt = true;
+        if ((rs2 = run_gemms(ctx, gs, st, "gemm_backtr_wt")) != BKFAC_OK) return rs2;
+      }
+      for (int j = pmax - 1; j >= 0; --j) {
+        for (size_t i = 0; i < n; ++i) {
+          const EigProb& q = b.p[i];
+          if (j >= bt_panels(q.m)) continue;
+          const int r0 = j * BT_PW + 1, mr0 = q.m - r0;
+          const int np = std::min(BT_PW, q.m - 2 - j * BT_PW);   // reflectors in this panel
+          // Z = W_j^T V(r0:, :)   (np x r)
+          gs.add(true, false, gp(q.K + r0 + (long)(j * BT_PW) * q.ldk, q.ldk, q.V + r0, q.ldv, q.Zw, BT_PW,
+                                 np, q.r, mr0, 1.f), 0);
+        }
+        if ((rs2 = run_gemms(ctx, gs, st, "gemm_backtr_z")) != BKFAC_OK) return rs2;
+        for (size_t i = 0; i < n; ++i) {
+          const EigProb& q = b.p[i];
+          if (j >= bt_panels(q.m)) continue;
+          const int r0 = j * BT_PW + 1, mr0 = q.m - r0;
+          const int np = std::min(BT_PW, q.m - 2 - j * BT_PW);
+          // V(r0:, :) -= U_j(r0:, 0:np) Z
+          gs.add(false, false, gp(q.Uw + (long)(j * BT_PW) * q.m + r0, q.m, q.Zw, BT_PW, q.V + r0, q.ldv,
+                                  mr0, q.r, np, -1.f, q.V + r0, q.ldv, 1.f), 0);
+        }
+        if ((rs2 = run_gemms(ctx, gs, st, "gemm_backtr_u")) != BKFAC_OK) return rs2;
+      }
+    }
     i0 += n;
   }
   v.clear();
@@ -457,6 +523,9 @@ EigProb eig_prob(bkfac_ctx ctx, const EigWs& w, int m, int r, float* V, int ldv,
   p.Dout = Dout;
   p.status = status;
   p.gtiles = w.gt ? at<float>(ctx, w.gt) : nullptr;
+  p.Uw = at<float>(ctx, w.U);
+  p.Zw = at<float>(ctx, w.Z);
+  p.Sw = at<float>(ctx, w.S);
   return p;
 }
 
@@ -534,6 +603,10 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
       fp.ws = a.take(sizeof(float) * fp.ws_elems);
       plan_eig(a, fp.eig, m, r);
     }
+    fp.Urot = a.take(sizeof(float) * (size_t)n * r);
+    fp.Gref = a.take(sizeof(float) * (size_t)r * r);
+    fp.wsr_elems = (long)kSplitMax * r * (long)r;
+    fp.wsr = a.take(sizeof(float) * fp.wsr_elems);
     if (fp.d.flags & BKFAC_FACTOR_DENSE_EA) {
       fp.rsvd = true;
       const int l = std::min(n, r + kRsvdOversampleMax);
@@ -580,7 +653,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
-  attr_ok &= cudaFuncSetAttribute(backtr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(backtr_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bt_smem_bytes()) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(chol_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT_SMEM_BYTES) == cudaSuccess;
@@ -740,7 +813,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     for (int i : dense) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
-      eg.push_back(eig_prob(ctx, fp.eig, fp.d.n, fp.d.r, a.U_out, fp.d.n, a.D_out,
+      eg.push_back(eig_prob(ctx, fp.eig, fp.d.n, fp.d.r, at<float>(ctx, fp.Urot), fp.d.n, a.D_out,
                             status_ptr(ctx, a.factor)));
     }
   }
@@ -753,6 +826,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
       GemmProb p = gp(a.U_in, n, a.M, n, at<float>(ctx, fp.W), fp.m, r, a.c, n, 1.f);
+      p.status = status_ptr(ctx, a.factor);   // U_in and M enter here
       gemm_ws(p, at<float>(ctx, fp.ws));
       gs.add(true, false, p, fp.ws_elems);
     }
@@ -866,13 +940,43 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const auto& fp = ctx->f[a.factor];
     const int n = fp.d.n, r = fp.d.r, mm = r + a.c;
     const float* V = at<float>(ctx, fp.eig.V);
-    GemmProb p = gp(a.U_in, n, V, mm, a.U_out, n, n, r, mm, 1.f);
+    GemmProb p = gp(a.U_in, n, V, mm, at<float>(ctx, fp.Urot), n, n, r, mm, 1.f);
     p.A2 = at<float>(ctx, fp.R); p.lda2 = n;
     p.B2 = V + r; p.ldb2 = mm;
     p.k1 = r;
     gs.add(false, false, p, 0);
   }
   STAGE(run("gemm_rotate"));
+  // orthonormality refresh (reading R8): U_out = U' (3/2 I - 1/2 U'^T U'), one Newton-Schulz
+  // step.  In exact arithmetic U' is orthonormal and this is the identity map; in fp32 it
+  // removes the per-step departure (~1e-6..1e-5 from the GEMMs) instead of letting it
+  // accumulate along the chain, at 4 n r^2 flops.
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    if (a.flags & BKFAC_BRAND_NO_REFRESH) continue;
+    const auto& fp = ctx->f[a.factor];
+    const int n = fp.d.n, r = fp.d.r;
+    const float* Ur = at<float>(ctx, fp.Urot);
+    GemmProb p = gp(Ur, n, Ur, n, at<float>(ctx, fp.Gref), r, r, r, n, 1.f);
+    gemm_ws(p, at<float>(ctx, fp.wsr));
+    gs.add(true, false, p, fp.wsr_elems);
+  }
+  STAGE(run("gemm_refresh_gram"));
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    const auto& fp = ctx->f[a.factor];
+    const int n = fp.d.n, r = fp.d.r;
+    const float* Ur = at<float>(ctx, fp.Urot);
+    if (a.flags & BKFAC_BRAND_NO_REFRESH) {
+      EwProb e{};
+      e.Y = a.U_out; e.ldy = n; e.X = Ur; e.ldx = n; e.rows = n; e.cols = r; e.op = EW_COPY;
+      ew.push_back(e);
+      continue;
+    }
+    gs.add(false, false, gp(Ur, n, at<float>(ctx, fp.Gref), r, a.U_out, n, n, r, r, -0.5f, Ur, n, 1.5f), 0);
+  }
+  STAGE(run("gemm_refresh"));
+  if (!ew.empty()) STAGE(run_ew(ctx, ew, st, "ew_copy_out"));
 done:
 #undef STAGE
   if (dev_prev != ctx->device) cudaSetDevice(dev_prev);
@@ -893,6 +997,7 @@ bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K, const floa
   const int n = fp.d.n;
   GemmStage gs;
   GemmProb pe = gp(M, n, M, n, K, n, n, n, c, 1.f - rho, K, n, rho);
+  pe.status = status_ptr(ctx, factor);
   pe.sym = 1;   // K and M M^T are symmetric: lower tiles computed, mirrored
   gs.add(false, true, pe, 0);
   return run_gemms(ctx, gs, st, "gemm_ea");
@@ -913,6 +1018,7 @@ bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args,
     if (!(a.rho >= 0.f && a.rho < 1.f)) return BKFAC_ERR_INVALID_ARG;
     const int n = fp.d.n;
     GemmProb pe = gp(a.M, n, a.M, n, a.K_dense, n, n, n, a.c, 1.f - a.rho, a.K_dense, n, a.rho);
+    pe.status = status_ptr(ctx, a.factor);
     pe.sym = 1;   // K and M M^T are symmetric: lower tiles computed, mirrored
     gs.add(false, true, pe, 0);
   }
@@ -971,9 +1077,12 @@ bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* ar
     }
     prof_end(ctx, st);
   }
-  for (int i : rf)
-    gs.add(false, false, gp(args[i].K_dense, L[i].n, L[i].Q, L[i].n, L[i].Y, L[i].n, L[i].n, L[i].l,
-                            L[i].n, 1.f), 0);
+  for (int i : rf) {
+    GemmProb pk = gp(args[i].K_dense, L[i].n, L[i].Q, L[i].n, L[i].Y, L[i].n, L[i].n, L[i].l,
+                     L[i].n, 1.f);
+    pk.status = L[i].status;   // K_dense enters here
+    gs.add(false, false, pk, 0);
+  }
   if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
   // shifted CholeskyQR3 of X (the power-iteration block K Q is ill-conditioned by
   // design): X -> Qout (shifted) -> Q2 -> Qout, for the factors in `act`
@@ -1116,10 +1225,15 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G;
     if (rA > 0) {
       GemmProb p = gp(a.J, dA, a.U_A, dA, at<float>(ctx, lp.Y), dG, dG, rA, dA, 1.f);
+      p.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);   // J and U_A enter here
       gemm_ws(p, at<float>(ctx, lp.ws));
       gs.add(true, false, p, lp.ws_elems);
     }
-    if (rG > 0) gs.add(false, false, gp(a.J, dA, a.U_G, dG, at<float>(ctx, lp.Xt), dA, dA, rG, dG, 1.f), 0);
+    if (rG > 0) {
+      GemmProb p = gp(a.J, dA, a.U_G, dG, at<float>(ctx, lp.Xt), dA, dA, rG, dG, 1.f);
+      p.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);
+      gs.add(false, false, p, 0);
+    }
   }
   if ((rs = run_gemms(ctx, gs, st, "gemm_prec_proj")) != BKFAC_OK) return rs;
   // S3: Z = U_G^T Y (r_G x r_A)

@@ -27,6 +27,9 @@ struct EigProb {
   float* Dout;             // output eigenvalues (r), clamped >= 0
   int* status;
   float* gtiles;           // tridiagonalisation tiles in global memory (large m), else null
+  float* Uw;               // blocked back-transform: m x (npanel*BT_PW) panels U_j = W_j T_j
+  float* Zw;               // blocked back-transform: BT_PW x r scratch
+  float* Sw;               // blocked back-transform: per panel S_j, T_j (BT_PW x BT_PW each)
 };
 constexpr int EIG_MAXP = 100;
 struct EigBatch { int nprob; EigProb p[EIG_MAXP]; };
@@ -364,6 +367,82 @@ __global__ void __launch_bounds__(1024) backtr_kernel(const __grid_constant__ Ei
     for (int i = lane; i < m; i += 32) p.V[i + (long)j * p.ldv] = yc[i];
   bad = __syncthreads_or(bad);
   if (bad && tid == 0 && p.status) atomicOr(p.status, ST_EIG_FAIL);
+}
+
+// ------------------------------------------------------------------ 5'. blocked back-transform
+// V = H_0 H_1 ... H_{m-3} Y applied panel by panel (BT_PW reflectors each, compact WY form
+// H_{k0} ... H_{k0+PW-1} = I - W T W^T, T upper triangular, LAPACK dlarft 'F','C'):
+//   prep   : K's column k becomes the explicit v_k (0 above row k+1, 1 at row k+1; columns
+//            k >= m-2 zero), V = (float) Y;
+//   S, U   : S_j = W_j^T W_j and U_j = W_j T_j on the tensor-core GEMM; in between the
+//            dlarft recurrence T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i), T(i, i) = tau_i
+//            (one small CTA per panel);
+//   apply  : last panel first, Z = W_j^T V and V -= U_j Z on the tensor-core GEMM
+//            (bkfac_api.cu).  2 m^2 r flops become two GEMMs per panel instead of m-2
+//            sequential rank-1 reflections.
+constexpr int BT_PW = 128;
+__host__ __device__ inline int bt_panels(int m) { return m > 2 ? (m - 2 + BT_PW - 1) / BT_PW : 0; }
+
+// grid: (nprob, 64), block 256
+__global__ void backtr_prep_kernel(const __grid_constant__ EigBatch b) {
+  const EigProb& p = b.p[blockIdx.x];
+  const int m = p.m, r = p.r;
+  const long tot = (long)m * m;
+  for (long e = blockIdx.y * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.y * blockDim.x) {
+    const int i = (int)(e % m), k = (int)(e / m);
+    float* a = p.K + i + (long)k * p.ldk;
+    if (k >= m - 2 || i < k + 1) *a = 0.f;
+    else if (i == k + 1) *a = 1.f;
+  }
+  int bad = 0;
+  const long tv = (long)m * r;
+  for (long e = blockIdx.y * (long)blockDim.x + threadIdx.x; e < tv; e += (long)gridDim.y * blockDim.x) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    const float v = (float)p.Y[(long)i * r + j];
+    bad |= !isfinite(v);
+    p.V[i + (long)j * p.ldv] = v;
+  }
+  if (bad && p.status) atomicOr(p.status, ST_EIG_FAIL);
+}
+
+// grid: (nprob, max panels), block 128: the dlarft recurrence of one panel from its Gram
+// matrix S_j = W_j^T W_j (computed by the tensor-core GEMM), T written next to S.
+//   T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i),  T(i, i) = tau_i
+constexpr int BT_THREADS = 128;
+inline size_t bt_smem_bytes() { return sizeof(float) * 2 * BT_PW * (BT_PW + 1); }
+__global__ void __launch_bounds__(BT_THREADS) backtr_t_kernel(const __grid_constant__ EigBatch b) {
+  const EigProb& p = b.p[blockIdx.x];
+  const int m = p.m, j = blockIdx.y;
+  if (j >= bt_panels(m)) return;
+  constexpr int PW = BT_PW, LD = BT_PW + 1;
+  extern __shared__ __align__(16) float btsm[];
+  float* S = btsm;
+  float* T = S + PW * LD;
+  const int tid = threadIdx.x;
+  const int k0 = j * PW, np = min(PW, m - 2 - k0);
+  const float* Sg = p.Sw + (long)j * 2 * PW * PW;         // S_j col-major, ld PW
+  float* Tg = p.Sw + (long)j * 2 * PW * PW + PW * PW;     // T_j col-major, ld PW
+  for (int e = tid; e < PW * PW; e += BT_THREADS) {
+    const int a = e % PW, c = e / PW;
+    S[a * LD + c] = (a < np && c < np) ? Sg[a + (long)c * PW] : 0.f;
+    T[a * LD + c] = 0.f;
+  }
+  __syncthreads();
+  for (int i = 0; i < np; ++i) {
+    const float taui = p.tau[k0 + i];
+    if (tid < i) {
+      float s = 0.f;
+      for (int c = tid; c < i; ++c) s = fmaf(T[tid * LD + c], S[c * LD + i], s);
+      T[tid * LD + i] = -taui * s;
+    } else if (tid == i) {
+      T[i * LD + i] = taui;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < PW * PW; e += BT_THREADS) {
+    const int a = e % PW, c = e / PW;
+    Tg[a + (long)c * PW] = T[a * LD + c];
+  }
 }
 
 }  // namespace bkfac

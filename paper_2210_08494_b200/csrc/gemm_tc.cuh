@@ -8,7 +8,8 @@
 // Why 3xTF32 (SURVEY §8(c) survey probe; BASELINE north_star): every contraction of the
 // Brand update, the RSVD and the preconditioner must meet fp32 tolerances; single-pass
 // TF32 fails them.  Each fp32 operand x is split as x = hi + lo with hi = rna_tf32(x),
-// lo = x - hi (exact in fp32) and the product is accumulated in fp32 TMEM as
+// lo = rna_tf32(x - hi) (the tensor core truncates fp32 inputs to tf32, so both halves are
+// rounded explicitly; |x - hi - lo| <= 2^-22 |x|) and the product is accumulated as
 //     hi_A hi_B + hi_A lo_B + lo_A hi_B       (the lo_A lo_B term is O(2^-22)).
 //
 // Accumulator promotion.  The tensor core's fp32 accumulate is not round-to-nearest: a
@@ -492,6 +493,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
       ok = j < p.N && k < klen;
       return Bp + j + (long)k * ldb;
     };
+    int* st_b = nullptr;   // status pointer of the chunk just loaded
     auto load = [&](float (&v)[Cfg::LPW], int& vmode) {
       const GemmProb& p = b.p[x.pi];
       const int seg = c < x.nc1 ? 0 : 1;
@@ -502,6 +504,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
       const long lda = seg ? p.lda2 : p.lda;
       const long ldb = seg ? p.ldb2 : p.ldb;
       vmode = p.vec;
+      st_b = p.status;
 #pragma unroll
       for (int qd = 0; qd < NQ; ++qd) {
         const int g = lw + qd * TC_LOAD_WARPS;
@@ -533,7 +536,13 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
         }
       }
     };
-    auto store = [&](const float (&v)[Cfg::LPW], int vmode) {
+    auto store = [&](const float (&v)[Cfg::LPW], int vmode, int* status) {
+      if (status) {   // inf/NaN in the operands: report (exponent field all ones)
+        unsigned nf = 0;
+#pragma unroll
+        for (int q = 0; q < Cfg::LPW; ++q) nf |= ((__float_as_uint(v[q]) & 0x7F800000u) == 0x7F800000u);
+        if (__any_sync(0xffffffffu, nf) && lane == 0) atomicOr(status, ST_NONFINITE);
+      }
       mbar_wait(empty_bar(stage), phase ^ 1);
       const uint32_t st = sbase + stage * Cfg::STAGE_BYTES;
 #ifndef BKFAC_TC_DEBUG_NOSTORE
@@ -549,7 +558,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
           else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, e0); dl = dh + Cfg::B_BYTES; }
           float h[4], lo[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) { h[t] = tf32_round(v[4 * qd + t]); lo[t] = v[4 * qd + t] - h[t]; }
+          for (int t = 0; t < 4; ++t) { h[t] = tf32_round(v[4 * qd + t]); lo[t] = tf32_round(v[4 * qd + t] - h[t]); }
           asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dh), "f"(h[0]), "f"(h[1]), "f"(h[2]), "f"(h[3]));
           asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dl), "f"(lo[0]), "f"(lo[1]), "f"(lo[2]), "f"(lo[3]));
         } else {
@@ -557,7 +566,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
           for (int t = 0; t < 4; ++t) {
             const int l = 4 * g + t;
             const float hi = tf32_round(v[4 * qd + t]);
-            const float lo = v[4 * qd + t] - hi;
+            const float lo = tf32_round(v[4 * qd + t] - hi);   // the MMA would truncate it
             uint32_t dh, dl;
             if (isA) { dh = st + tc_line_off<!TA, TC_BM>(l, lane); dl = dh + Cfg::A_BYTES; }
             else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, lane); dl = dh + Cfg::B_BYTES; }
@@ -576,16 +585,18 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     };
     float va[Cfg::LPW], vb[Cfg::LPW];
     int ma = 0, mb = 0;
+    int* sa_ = nullptr;
+    int* sb_ = nullptr;
     bool have = seek();
-    if (have) { load(va, ma); ++c; }
+    if (have) { load(va, ma); sa_ = st_b; ++c; }
     while (have) {
       const bool more = seek();
-      if (more) { load(vb, mb); ++c; }
-      store(va, ma);
+      if (more) { load(vb, mb); sb_ = st_b; ++c; }
+      store(va, ma, sa_);
       if (!more) break;
       const bool more2 = seek();
-      if (more2) { load(va, ma); ++c; }
-      store(vb, mb);
+      if (more2) { load(va, ma); sa_ = st_b; ++c; }
+      store(vb, mb, sb_);
       have = more2;
     }
   } else {
