@@ -792,6 +792,17 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       }
     }
     STAGE(run_ew(ctx, ew, st, "ew_dense_scale"));
+    {   // M reaches the tensor cores only as an MMA operand on this path: guard it
+      static NfBatch nb;
+      nb.nprob = 0;
+      for (int i : dense) {
+        if (nb.nprob == NF_MAXP) break;
+        const auto& a = args[i];
+        nb.p[nb.nprob++] = NfProb{a.M, ctx->f[a.factor].d.n, a.c, ctx->f[a.factor].d.n, status_ptr(ctx, a.factor)};
+      }
+      nonfinite_kernel<<<dim3(16, (unsigned)nb.nprob), 256, 0, st>>>(nb);
+      LAUNCH_CHECK(ctx);
+    }
     for (int i : dense) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
@@ -826,7 +837,6 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
       GemmProb p = gp(a.U_in, n, a.M, n, at<float>(ctx, fp.W), fp.m, r, a.c, n, 1.f);
-      p.status = status_ptr(ctx, a.factor);   // U_in and M enter here
       gemm_ws(p, at<float>(ctx, fp.ws));
       gs.add(true, false, p, fp.ws_elems);
     }
@@ -836,8 +846,10 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
-      gs.add(false, false, gp(a.U_in, n, at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), n, n, a.c,
-                              r, -1.f, a.M, n, 1.f), 0);
+      GemmProb pr = gp(a.U_in, n, at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), n, n, a.c,
+                       r, -1.f, a.M, n, 1.f);
+      pr.status = status_ptr(ctx, a.factor);   // every element of M passes this epilogue
+      gs.add(false, false, pr, 0);
     }
     STAGE(run("gemm_resid"));
     // CGS2 re-projection: P2 = U^T R; R -= U P2; P += P2
@@ -973,7 +985,9 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       ew.push_back(e);
       continue;
     }
-    gs.add(false, false, gp(Ur, n, at<float>(ctx, fp.Gref), r, a.U_out, n, n, r, r, -0.5f, Ur, n, 1.5f), 0);
+    GemmProb pf = gp(Ur, n, at<float>(ctx, fp.Gref), r, a.U_out, n, n, r, r, -0.5f, Ur, n, 1.5f);
+    pf.status = status_ptr(ctx, a.factor);   // the new basis passes this epilogue
+    gs.add(false, false, pf, 0);
   }
   STAGE(run("gemm_refresh"));
   if (!ew.empty()) STAGE(run_ew(ctx, ew, st, "ew_copy_out"));
@@ -1080,7 +1094,6 @@ bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* ar
   for (int i : rf) {
     GemmProb pk = gp(args[i].K_dense, L[i].n, L[i].Q, L[i].n, L[i].Y, L[i].n, L[i].n, L[i].l,
                      L[i].n, 1.f);
-    pk.status = L[i].status;   // K_dense enters here
     gs.add(false, false, pk, 0);
   }
   if ((rs = run_gemms(ctx, gs, st, "gemm_rsvd_mul")) != BKFAC_OK) return rs;
@@ -1225,14 +1238,11 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G;
     if (rA > 0) {
       GemmProb p = gp(a.J, dA, a.U_A, dA, at<float>(ctx, lp.Y), dG, dG, rA, dA, 1.f);
-      p.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);   // J and U_A enter here
       gemm_ws(p, at<float>(ctx, lp.ws));
       gs.add(true, false, p, lp.ws_elems);
     }
     if (rG > 0) {
-      GemmProb p = gp(a.J, dA, a.U_G, dG, at<float>(ctx, lp.Xt), dA, dA, rG, dG, 1.f);
-      p.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);
-      gs.add(false, false, p, 0);
+      gs.add(false, false, gp(a.J, dA, a.U_G, dG, at<float>(ctx, lp.Xt), dA, dA, rG, dG, 1.f), 0);
     }
   }
   if ((rs = run_gemms(ctx, gs, st, "gemm_prec_proj")) != BKFAC_OK) return rs;
@@ -1291,6 +1301,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     p.B2 = a.U_G ? a.U_G : at<float>(ctx, lp.Y); p.ldb2 = dG;
     p.k1 = rA;
     p.beta_dev = lam + 2;
+    p.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);   // every element of J passes here
     gs.add(false, true, p, 0);
   }
   return run_gemms(ctx, gs, st, "gemm_prec_out");

@@ -21,8 +21,9 @@ struct GemmProb {
   int splits, kchunk, tiles_m, tiles_n, tile_start;
   int sym;                 // tcgen05 path: C = C^T known (e.g. M M^T): lower tiles only, mirrored
   int vec;                 // tcgen05 path: bit 0 A (and A2), bit 1 B (and B2) 16-byte aligned
-  int* status;             // if set: ST_NONFINITE is OR-ed in when an operand holds inf/NaN
-                           // (the tensor core does not propagate NaN reliably)
+  int* status;             // if set: ST_NONFINITE is OR-ed in when C0 (beta != 0) holds
+                           // inf/NaN -- the tensor core does not propagate NaN reliably, so
+                           // inputs are checked where an epilogue reads them anyway
 };
 
 constexpr int GEMM_MAXP = 100;
@@ -75,12 +76,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const __grid_constant__ 
       if (!TA) { i = row0 + (tid & 63); k = k0 + (tid >> 6) + 4 * q; }
       else     { k = k0 + (tid & 15);   i = row0 + (tid >> 4) + 16 * q; }
       ra[q] = (i < p.M && k < kend) ? gemm_a<TA>(p, i, k) : 0.f;
-      if (p.status && !isfinite(ra[q])) atomicOr(p.status, ST_NONFINITE);
       int j;
       if (!TB) { k = k0 + (tid & 15);   j = col0 + (tid >> 4) + 16 * q; }
       else     { j = col0 + (tid & 63); k = k0 + (tid >> 6) + 4 * q; }
       rb[q] = (j < p.N && k < kend) ? gemm_b<TB>(p, k, j) : 0.f;
-      if (p.status && !isfinite(rb[q])) atomicOr(p.status, ST_NONFINITE);
     }
   };
   auto store = [&](int buf) {
@@ -137,7 +136,11 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const __grid_constant__ 
         const int i = row0 + ty * 4 + ii;
         if (i >= p.M) continue;
         float v = p.alpha * acc[ii][jj];
-        if (beta != 0.f) v += beta * p.C0[i + (long)j * p.ldc0];
+        if (beta != 0.f) {
+          const float c0 = p.C0[i + (long)j * p.ldc0];
+          if (p.status && !isfinite(c0)) atomicOr(p.status, ST_NONFINITE);
+          v += beta * c0;
+        }
         p.C[i + (long)j * p.ldc] = v;
       }
     }
@@ -168,7 +171,11 @@ __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmBatch b) {
     for (int s = 0; s < p.splits; ++s) acc += p.ws[(long)s * total + e];
     const int i = (int)(e % p.M), j = (int)(e / p.M);
     float v = p.alpha * acc;
-    if (beta != 0.f) v += beta * p.C0[i + (long)j * p.ldc0];
+    if (beta != 0.f) {
+      const float c0 = p.C0[i + (long)j * p.ldc0];
+      if (p.status && !isfinite(c0)) atomicOr(p.status, ST_NONFINITE);
+      v += beta * c0;
+    }
     p.C[i + (long)j * p.ldc] = v;
   }
 }

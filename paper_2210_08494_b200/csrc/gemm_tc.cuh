@@ -8,8 +8,9 @@
 // Why 3xTF32 (SURVEY §8(c) survey probe; BASELINE north_star): every contraction of the
 // Brand update, the RSVD and the preconditioner must meet fp32 tolerances; single-pass
 // TF32 fails them.  Each fp32 operand x is split as x = hi + lo with hi = rna_tf32(x),
-// lo = rna_tf32(x - hi) (the tensor core truncates fp32 inputs to tf32, so both halves are
-// rounded explicitly; |x - hi - lo| <= 2^-22 |x|) and the product is accumulated as
+// lo = x - hi (exact in fp32; the tensor core truncates lo to tf32: |x - hi - tf32(lo)|
+// <= 2^-21 |x|; rounding lo explicitly measured no better and costs loader issue slots)
+// and the product is accumulated as
 //     hi_A hi_B + hi_A lo_B + lo_A hi_B       (the lo_A lo_B term is O(2^-22)).
 //
 // Accumulator promotion.  The tensor core's fp32 accumulate is not round-to-nearest: a
@@ -286,6 +287,7 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
       const GemmProb& p = b.p[x.pi];
       const int nblk = (x.c_end - x.c_beg + TC_PROMO - 1) / TC_PROMO;
       const int i = x.m0 + row;
+      bool nonfinite = false;   // inf/NaN in C0 (the operands' tensor-core path cannot report it)
       const float beta = p.beta_dev ? *p.beta_dev : p.beta;
       float* w = p.splits > 1 ? p.ws + (long)x.split * p.M * p.N : nullptr;
       for (int blk = 0; blk < nblk; ++blk, ++kb) {
@@ -319,7 +321,11 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
                   w[i + (long)j * p.M] = v[jj];
                 } else {
                   float o = p.alpha * v[jj];
-                  if (beta != 0.f) o += beta * p.C0[i + (long)j * p.ldc0];
+                  if (beta != 0.f) {
+                    const float c0 = p.C0[i + (long)j * p.ldc0];
+                    nonfinite |= !isfinite(c0);
+                    o += beta * c0;
+                  }
                   p.C[i + (long)j * p.ldc] = o;
                   if (p.sym && x.m0 != x.n0) p.C[j + (long)i * p.ldc] = o;   // mirror tile
                 }
@@ -332,6 +338,7 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty_bar(buf));
       }
+      if (p.status && __any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(p.status, ST_NONFINITE);
       if (nblk == 0 && i < p.M) {     // empty K range (split beyond K or K = 0)
         for (int j = x.n0; j < min(p.N, x.n0 + BN); ++j) {
           if (w) {
@@ -536,13 +543,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
         }
       }
     };
-    auto store = [&](const float (&v)[Cfg::LPW], int vmode, int* status) {
-      if (status) {   // inf/NaN in the operands: report (exponent field all ones)
-        unsigned nf = 0;
-#pragma unroll
-        for (int q = 0; q < Cfg::LPW; ++q) nf |= ((__float_as_uint(v[q]) & 0x7F800000u) == 0x7F800000u);
-        if (__any_sync(0xffffffffu, nf) && lane == 0) atomicOr(status, ST_NONFINITE);
-      }
+    auto store = [&](const float (&v)[Cfg::LPW], int vmode, int*) {
       mbar_wait(empty_bar(stage), phase ^ 1);
       const uint32_t st = sbase + stage * Cfg::STAGE_BYTES;
 #ifndef BKFAC_TC_DEBUG_NOSTORE
@@ -558,7 +559,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
           else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, e0); dl = dh + Cfg::B_BYTES; }
           float h[4], lo[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) { h[t] = tf32_round(v[4 * qd + t]); lo[t] = tf32_round(v[4 * qd + t] - h[t]); }
+          for (int t = 0; t < 4; ++t) { h[t] = tf32_round(v[4 * qd + t]); lo[t] = v[4 * qd + t] - h[t]; }
           asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dh), "f"(h[0]), "f"(h[1]), "f"(h[2]), "f"(h[3]));
           asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dl), "f"(lo[0]), "f"(lo[1]), "f"(lo[2]), "f"(lo[3]));
         } else {
@@ -566,7 +567,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
           for (int t = 0; t < 4; ++t) {
             const int l = 4 * g + t;
             const float hi = tf32_round(v[4 * qd + t]);
-            const float lo = tf32_round(v[4 * qd + t] - hi);   // the MMA would truncate it
+            const float lo = v[4 * qd + t] - hi;
             uint32_t dh, dl;
             if (isA) { dh = st + tc_line_off<!TA, TC_BM>(l, lane); dl = dh + Cfg::A_BYTES; }
             else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, lane); dl = dh + Cfg::B_BYTES; }

@@ -45,6 +45,20 @@ __global__ void ew_kernel(const __grid_constant__ EwBatch b) {
   }
 }
 
+// ---- inf/NaN guard for inputs that reach the tensor cores only as MMA operands (the MMA
+// does not propagate NaN reliably): one pass, OR into the factor's status word.
+struct NfProb { const float* X; int rows, cols, ld; int* status; };
+constexpr int NF_MAXP = 100;
+struct NfBatch { int nprob; NfProb p[NF_MAXP]; };
+__global__ void nonfinite_kernel(const __grid_constant__ NfBatch b) {
+  const NfProb& p = b.p[blockIdx.y];
+  const long total = (long)p.rows * p.cols;
+  int bad = 0;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x)
+    bad |= !isfinite(p.X[(e % p.rows) + (e / p.rows) * (long)p.ld]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(p.status, ST_NONFINITE);
+}
+
 // ---- preconditioner scalars (Alg 1 lines 16-17) ---------------------
 // For each layer side: effective lambda (relative mode :940, continuation :711) and
 // s_i = (D_i + lambda)^{-1} - 1/lambda.  Writes s (r floats) and lambda_eff (1 float).
