@@ -116,6 +116,15 @@ typedef struct { int factor; float* K_dense; const float* M; int c; float rho; }
 bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args, int count,
                                        void* stream);
 
+/* bkfac_brand_update(args, count) and bkfac_ea_accumulate_batch(ea_args, ea_count) of one
+ * step (Alg 5 lines 5-6 / Alg 1 lines 16-17) in one call.
+ * Same results as the two calls in sequence on `stream`; the EA GEMM runs on an internal
+ * stream, forked when the Brand path reaches its eigensolver and capped to the SMs the
+ * tridiagonalisation leaves idle, and joined before the call's work completes on
+ * `stream`.  No K_dense may alias a U_in / U_out (BKFAC_ERR_ALIAS). */
+bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, int count,
+                                   const bkfac_ea_args* ea_args, int ea_count, void* stream);
+
 /* U_out (n x r), D_out (r) <- RSVD of K_dense with l = r + oversample sketch columns and
  * `power_iters` re-orthonormalised power iterations.  The Gaussian sketch is
  * Philox4x32-10 keyed by `seed`, stream `counter`. */

@@ -28,7 +28,7 @@ STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKF
           7: "BKFAC_ERR_NUMERIC", 8: "BKFAC_ERR_UNSUPPORTED"}
 
 EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac_destroy",
-            "bkfac_brand_update", "bkfac_ea_accumulate", "bkfac_ea_accumulate_batch",
+            "bkfac_brand_update", "bkfac_brand_ea_update", "bkfac_ea_accumulate", "bkfac_ea_accumulate_batch",
             "bkfac_rsvd_overwrite", "bkfac_rsvd_overwrite_batch",
             "bkfac_precondition", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
             "bkfac_profile_enable", "bkfac_profile_read", "bkfac_status_string",
@@ -108,6 +108,8 @@ def load(path: str = None) -> ctypes.CDLL:
     lib.bkfac_destroy.restype = ci
     lib.bkfac_brand_update.argtypes = [vp, ctypes.POINTER(BrandArgs), ci, vp]
     lib.bkfac_brand_update.restype = ci
+    lib.bkfac_brand_ea_update.argtypes = [vp, ctypes.POINTER(BrandArgs), ci, ctypes.POINTER(EaArgs), ci, vp]
+    lib.bkfac_brand_ea_update.restype = ci
     lib.bkfac_ea_accumulate.argtypes = [vp, ci, vp, vp, ci, cf, vp]
     lib.bkfac_ea_accumulate.restype = ci
     lib.bkfac_ea_accumulate_batch.argtypes = [vp, ctypes.POINTER(EaArgs), ci, vp]
@@ -202,6 +204,22 @@ class Context:
                                float(u["alpha"]), float(u["beta"]), int(u.get("flags", 0)))
         _check(self.lib.bkfac_brand_update(self.h, arr, len(updates), _stream_ptr(stream)),
                "bkfac_brand_update")
+
+    def bkfac_brand_ea_update(self, updates: List[dict], ea_items: List[dict], stream=None) -> None:
+        """bkfac_brand_ea_update: bkfac_brand_update(updates) + bkfac_ea_accumulate_batch(ea_items)
+        of one step, the EA GEMM overlapped with the eigensolver inside the library."""
+        arr = (BrandArgs * max(len(updates), 1))()
+        for i, u in enumerate(updates):
+            arr[i] = BrandArgs(u["factor"], _ptr(u["U_in"]), _ptr(u["D_in"]), _ptr(u["M"]),
+                               int(u["M"].shape[0]), _ptr(u["U_out"]), _ptr(u["D_out"]),
+                               float(u["alpha"]), float(u["beta"]), int(u.get("flags", 0)))
+        ea = (EaArgs * max(len(ea_items), 1))()
+        for i, a in enumerate(ea_items):
+            ea[i] = EaArgs(a["factor"], _ptr(a["K"]), _ptr(a["M"]), int(a["M"].shape[0]),
+                           float(a["rho"]))
+        _check(self.lib.bkfac_brand_ea_update(self.h, arr, len(updates), ea, len(ea_items),
+                                              _stream_ptr(stream)),
+               "bkfac_brand_ea_update")
 
     def bkfac_ea_accumulate(self, factor: int, K, M, rho: float, stream=None) -> None:
         _check(self.lib.bkfac_ea_accumulate(self.h, factor, _ptr(K), _ptr(M), int(M.shape[0]),

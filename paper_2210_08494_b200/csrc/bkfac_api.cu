@@ -10,6 +10,7 @@
 #include <new>
 #include <map>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "bkfac.h"
@@ -106,6 +107,12 @@ struct bkfac_ctx_s {
   // side streams for independent launch groups inside one call (fork/join with events)
   cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
+  // bkfac_brand_ea_update: the EA accumulate, launched on ea_stream by the eigensolver
+  // (pending_ea(busy SMs)) so that it runs on the SMs the tridiagonalisation leaves idle
+  cudaStream_t ea_stream = nullptr;
+  cudaEvent_t ev_ea_fork = nullptr, ev_ea_done = nullptr;
+  std::function<bkfac_status(int)> pending_ea;
+  int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs
   // optional per-stage CUDA-event profiling (bkfac_profile_enable)
   bool prof = false;
   struct Rec { std::string tag; cudaEvent_t a, b; double flops, bytes; uint64_t launches; };
@@ -209,7 +216,7 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
     b.total_tiles = tiles;
     if (tiles > 0) {
       if (tc) {
-        const int grid = std::min(tiles, kNumSM);
+        const int grid = std::min(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM);
         tc_launch<TA, TB>(b, grid, st);
       } else {
         gemm_simt_kernel<TA, TB><<<tiles, 256, 0, st>>>(b);
@@ -261,7 +268,8 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       }
       base_tiles += p.sym ? (long)p.tiles_m * (p.tiles_m + 1) / 2 : (long)p.tiles_m * p.tiles_n;
     }
-  const long target = tc ? (long)kNumSM : 2L * kNumSM;
+  const long nsm = ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM;
+  const long target = tc ? nsm : 2L * nsm;
   for (int v = 0; v < 4; ++v)
     for (size_t i = 0; i < s.probs[v].size(); ++i) {
       GemmProb& p = s.probs[v][i];
@@ -366,6 +374,17 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     for (size_t i = 0; i < n; ++i) {
       const double m = b.p[i].m, r = b.p[i].r;
       m3 += m * m * m; m2 += m * m; m2r += m * m * r; mr += m * r;
+    }
+    if (ctx->pending_ea) {   // bkfac_brand_ea_update: EA GEMM beside the tridiagonalisation
+      int busy = 0;
+      for (size_t i = 0; i < n; ++i) {
+        const int C = sytrd_tiled_cluster(b.p[i].m);
+        busy += C == 0 ? 1 : C;
+      }
+      auto f = std::move(ctx->pending_ea);
+      ctx->pending_ea = nullptr;
+      const bkfac_status re = f(busy);
+      if (re != BKFAC_OK) return re;
     }
     // sytrd: 4/3 m^3 flops; algorithmic bytes: read K (lower), write reflectors + T
     prof_begin(ctx, "eig_sytrd", st, 4.0 / 3.0 * m3, 4.0 * m2);
@@ -667,6 +686,12 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
     if (cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) != cudaSuccess) c->ev_join[i] = nullptr;
   }
   if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess) c->ev_fork = nullptr;
+  if (cudaStreamCreateWithFlags(&c->ea_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_ea_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_ea_done, cudaEventDisableTiming) != cudaSuccess) {
+    fprintf(stderr, "bkfac: side stream creation failed\n");
+    return BKFAC_ERR_CUDA;
+  }
   for (int i = 0; i < 4; ++i)
     if (!c->side[i] || !c->ev_join[i]) { if (c->ev_fork) cudaEventDestroy(c->ev_fork); c->ev_fork = nullptr; }
   cudaGetLastError();
@@ -698,6 +723,9 @@ bkfac_status bkfac_destroy(bkfac_ctx c) {
     if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ea_stream) cudaStreamDestroy(c->ea_stream);
+  if (c->ev_ea_fork) cudaEventDestroy(c->ev_ea_fork);
+  if (c->ev_ea_done) cudaEventDestroy(c->ev_ea_done);
   delete c;
   return BKFAC_OK;
 }
@@ -1017,11 +1045,8 @@ bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K, const floa
   return run_gemms(ctx, gs, st, "gemm_ea");
 }
 
-bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args, int count,
-                                       void* stream) {
-  if (!ctx || count < 0 || (count > 0 && !args)) return BKFAC_ERR_INVALID_ARG;
-  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
-  GemmStage gs;
+namespace {
+bkfac_status ea_stage(bkfac_ctx ctx, const bkfac_ea_args* args, int count, GemmStage& gs) {
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
     if (a.factor < 0 || a.factor >= (int)ctx->f.size() || !a.K_dense || !a.M)
@@ -1036,8 +1061,66 @@ bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args,
     pe.sym = 1;   // K and M M^T are symmetric: lower tiles computed, mirrored
     gs.add(false, true, pe, 0);
   }
-  if (count == 0) return BKFAC_OK;
+  return BKFAC_OK;
+}
+}  // namespace
+
+bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args, int count,
+                                       void* stream) {
+  if (!ctx || count < 0 || (count > 0 && !args)) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  GemmStage gs;
+  const bkfac_status r = ea_stage(ctx, args, count, gs);
+  if (r != BKFAC_OK || count == 0) return r;
   return run_gemms(ctx, gs, static_cast<cudaStream_t>(stream), "gemm_ea");
+}
+
+bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, int count,
+                                   const bkfac_ea_args* ea_args, int ea_count, void* stream) {
+  if (!ctx || ea_count < 0 || (ea_count > 0 && !ea_args)) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  for (int i = 0; i < ea_count; ++i)
+    for (int j = 0; j < count && args; ++j)
+      if (ea_args[i].K_dense == args[j].U_out || ea_args[i].K_dense == args[j].U_in)
+        return BKFAC_ERR_ALIAS;
+  GemmStage gs;
+  bkfac_status r = ea_stage(ctx, ea_args, ea_count, gs);
+  if (r != BKFAC_OK) return r;
+  if (ea_count == 0) return bkfac_brand_update(ctx, args, count, stream);
+  static const int ea_mode = [] { const char* e = getenv("BKFAC_EA_MODE"); return e ? atoi(e) : 1; }();
+  if (ea_mode == 1) {   // tuning: EA first, full grid, on the caller's stream
+    r = run_gemms(ctx, gs, static_cast<cudaStream_t>(stream), "gemm_ea");
+    return r != BKFAC_OK ? r : bkfac_brand_update(ctx, args, count, stream);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev_prev = 0;
+  cudaGetDevice(&dev_prev);
+  if (dev_prev != ctx->device) cudaSetDevice(ctx->device);
+  bool launched = false;
+  ctx->pending_ea = [&](int busy) -> bkfac_status {
+    if (!cuda_ok(cudaEventRecord(ctx->ev_ea_fork, st)) ||
+        !cuda_ok(cudaStreamWaitEvent(ctx->ea_stream, ctx->ev_ea_fork, 0)))
+      return BKFAC_ERR_CUDA;
+    ctx->grid_cap = ea_mode == 2 ? 0 : std::max(kNumSM / 8, kNumSM - busy);
+    const bkfac_status re = run_gemms(ctx, gs, ctx->ea_stream, "gemm_ea");
+    ctx->grid_cap = 0;
+    if (re != BKFAC_OK) return re;
+    if (!cuda_ok(cudaEventRecord(ctx->ev_ea_done, ctx->ea_stream))) return BKFAC_ERR_CUDA;
+    launched = true;
+    return BKFAC_OK;
+  };
+  r = bkfac_brand_update(ctx, args, count, stream);
+  ctx->pending_ea = nullptr;
+  ctx->grid_cap = 0;
+  if (r == BKFAC_OK) {
+    if (launched) {
+      if (!cuda_ok(cudaStreamWaitEvent(st, ctx->ev_ea_done, 0))) r = BKFAC_ERR_CUDA;
+    } else {
+      r = run_gemms(ctx, gs, st, "gemm_ea");   // no eigensolver ran (count == 0)
+    }
+  }
+  if (dev_prev != ctx->device) cudaSetDevice(dev_prev);
+  return r;
 }
 
 // ------------------------------------------------------------------------- RSVD

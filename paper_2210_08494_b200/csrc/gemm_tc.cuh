@@ -89,7 +89,10 @@ struct TcCfg {
   static constexpr int TMEM_COLS = 4 * BN;                   // 2 K-block buffers + running sum
   static constexpr int LINES = TC_BM + BN;                   // 128-byte lines per stage half
   static constexpr int LPW = LINES / NLW;                    // lines per loader warp
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // + per-epilogue-warp 16 x 34 staging for the transposed (mirror) stores of symmetric tiles
+  static constexpr int EPI_STAGE_FLOATS = 16 * 34;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                                    TC_EPI_WARPS * EPI_STAGE_FLOATS * 4;
 };
 
 // ----------------------------------------------------------------------- PTX helpers
@@ -275,7 +278,8 @@ __device__ unsigned long long g_tc_dbg[148 * 8];   // tuning builds: per-CTA MMA
 // into the running sum (TMEM), then alpha/beta and coalesced stores of the tile.
 template <int BN>
 BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int lane,
-                           uint32_t tfull0, uint32_t tfull1, uint32_t tempty0, uint32_t tempty1) {
+                           uint32_t tfull0, uint32_t tfull1, uint32_t tempty0, uint32_t tempty1,
+                           float* stage) {
   auto tfull_bar = [&](int a) { return a ? tfull1 : tfull0; };
   auto tempty_bar = [&](int a) { return a ? tempty1 : tempty0; };
     const int row = warp * 32 + lane;                         // TMEM lane = tile row
@@ -312,24 +316,49 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
           }
           if (!last) {
             tmem_st16(run + g * 16, v);
-          } else if (i < p.M) {
+          } else if (w) {
+            if (i < p.M) {
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) {
+                const int j = x.n0 + g * 16 + jj;
+                if (j < p.N) w[i + (long)j * p.M] = v[jj];
+              }
+            }
+          } else {
+            const bool rowok = i < p.M;
+            const int j0 = x.n0 + g * 16;
+            // all 16 C0 loads of the group in flight together (each thread reads only the
+            // elements it writes, so this is safe when C0 aliases C)
+            float c0v[16];
+            if (beta != 0.f) {
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj)
+                c0v[jj] = (rowok && j0 + jj < p.N) ? p.C0[i + (long)(j0 + jj) * p.ldc0] : 0.f;
+            }
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {
-              const int j = x.n0 + g * 16 + jj;
-              if (j < p.N) {
-                if (w) {
-                  w[i + (long)j * p.M] = v[jj];
-                } else {
-                  float o = p.alpha * v[jj];
-                  if (beta != 0.f) {
-                    const float c0 = p.C0[i + (long)j * p.ldc0];
-                    nonfinite |= !isfinite(c0);
-                    o += beta * c0;
-                  }
-                  p.C[i + (long)j * p.ldc] = o;
-                  if (p.sym && x.m0 != x.n0) p.C[j + (long)i * p.ldc] = o;   // mirror tile
-                }
+              float o = p.alpha * v[jj];
+              if (beta != 0.f) {
+                nonfinite |= !isfinite(c0v[jj]);
+                o += beta * c0v[jj];
               }
+              if (rowok && j0 + jj < p.N) p.C[i + (long)(j0 + jj) * p.ldc] = o;
+              v[jj] = o;
+            }
+            if (p.sym && x.m0 != x.n0) {
+              // mirror tile C(j, i) = C(i, j): transposed through a warp-private staging
+              // buffer so that each store instruction writes two 64-byte column runs
+              // instead of 32 scattered words
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) stage[jj * 34 + lane] = v[jj];
+              __syncwarp();
+#pragma unroll 4
+              for (int q = 0; q < 16; ++q) {
+                const int jj = lane & 15, rr = 2 * q + (lane >> 4);
+                const int ir = x.m0 + warp * 32 + rr, jc = j0 + jj;
+                if (ir < p.M && jc < p.N) p.C[jc + (long)ir * p.ldc] = stage[jj * 34 + rr];
+              }
+              __syncwarp();
             }
           }
         }
@@ -602,7 +631,10 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     }
   } else {
     // ------------------------------------------------------------- epilogue
-    tc_epilogue<BN>(b, tmem_base, warp, lane, tfull_bar(0), tfull_bar(1), tempty_bar(0), tempty_bar(1));
+    float* stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256) +
+                   warp * Cfg::EPI_STAGE_FLOATS;
+    tc_epilogue<BN>(b, tmem_base, warp, lane, tfull_bar(0), tfull_bar(1), tempty_bar(0), tempty_bar(1),
+                    stage);
   }
   tc_fence_before();
   __syncthreads();

@@ -8,9 +8,12 @@
 // (0..C-1, C-1..0, ...), which balances the triangular sizes.
 //
 // Step k (reflector H_k = I - tau v v^T zeroing column k below the subdiagonal):
-//   (a) the owner of column k applies the pending rank-2 update of step k-1 to it
-//       (A <- A - v w^T - w v^T), forms v_k, tau_k (dlarfg) and broadcasts v_k into every
-//       CTA (st.shared::cluster);                                     cluster barrier
+//   (a) EVERY CTA reads column k from its owner's shared memory (ld.shared::cluster; the
+//       column is final after step k-1's tiles), applies the pending rank-2 update of step
+//       k-1 (A <- A - v w^T - w v^T) and forms v_k, tau_k (dlarfg) locally.  All CTAs
+//       compute bitwise-identical v_k (same inputs, same reduction order), so no
+//       broadcast and no cluster barrier is needed here; the owner writes d, e, tau and
+//       the reflector (rows >= k+2 of column k of K) to global memory;
 //   (b) every CTA walks its tiles (I >= J) of the trailing matrix with one warp per tile,
 //       lane = row: applies the pending update in registers, writes the tile back, and
 //       accumulates its partial y = A v_k both ways from the lower triangle -- row sums
@@ -18,10 +21,12 @@
 //       CTA's partial y with shared-memory atomics;                  cluster barrier
 //   (c) every CTA sums the C partial y through DSMEM and forms
 //       w_k = tau y - (tau^2/2)(y.v) v locally.
-// Per element of the trailing matrix and step: one LDS, one STS and five FP32 ops (the
-// column-cyclic first version of this kernel needed seven shared-memory accesses).
-// v and y are double-buffered by step parity.  Outputs as sytrd_kernel: d, e, tau and
-// the reflectors (rows >= k+2 of column k) in K's lower triangle for the back-transform.
+// One cluster barrier per step.  Hazards: the partial y are double-buffered by step
+// parity (a CTA rewrites a parity only after the next barrier, which every reader of the
+// previous use has passed); column k is never written after step k-1's tiles.
+// Per element of the trailing matrix and step: one LDS, one STS and five FP32 ops.
+// Outputs as sytrd_kernel: d, e, tau and the reflectors (rows >= k+2 of column k) in K's
+// lower triangle for the back-transform.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -48,7 +53,7 @@ inline long syt_own_floats(int NB, int C, int q) {
     if (syt_owner(J, C) == q) s += 1024L * (NB - J);
   return s;
 }
-inline int syt_vec_floats(int m_pad) { return 7 * m_pad + 64 + 64; }
+inline int syt_vec_floats(int m_pad) { return 7 * m_pad + 64 + 128; }
 // smallest cluster size whose largest per-CTA share fits; 0 = does not fit
 inline int sytrd_tiled_cluster(int m) {
   const int NB = (m + 31) / 32, m_pad = NB * 32;
@@ -73,6 +78,21 @@ inline size_t syt_global_tile_floats(int m) {
   return NB * (NB + 1) / 2 * 1024;
 }
 
+// Block sum with one barrier.  Precondition: every call is separated from the next one
+// by at least one __syncthreads (true at both call sites below), so `red` is not
+// rewritten while a warp still reads it.
+__device__ __forceinline__ float syt_block_sum(float v, float* red) {
+  constexpr int NW = SYT_THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float t = red[lane & (NW - 1)];
+#pragma unroll
+  for (int o = NW / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
 template <bool GT>
 __global__ void __launch_bounds__(SYT_THREADS, 1)
 sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
@@ -84,24 +104,30 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   float* K = p.K;
   const int NB = (m + 31) >> 5, m_pad = NB << 5;
   extern __shared__ __align__(16) float tsm[];
-  float* vbuf = tsm;                 // 2 * m_pad  (v_k by parity, broadcast by the owner)
+  float* vbuf = tsm;                 // 2 * m_pad  (v_k by parity, formed by every CTA)
   float* ybuf = vbuf + 2 * m_pad;    // 2 * m_pad  (partial y by parity, read remotely)
   float* ys = ybuf + 2 * m_pad;      // m_pad      (summed y)
   float* wp = ys + m_pad;            // m_pad      (w_{k-1})
-  float* scal = wp + m_pad;          // 64: [0..1] tau by parity, [2] bad flag, [4..] reduce
-  int* boff = reinterpret_cast<int*>(scal + 64);   // 64: storage offset of block-column J
-  float* tiles = GT ? p.gtiles : scal + 128;   // owned block-columns
+  float* scal = wp + m_pad;          // 64: [2] bad flag, [4..35] reduce, [40..41] alpha, d
+  int* boff = reinterpret_cast<int*>(scal + 64);   // 64: storage offset of block-column J (-1: not owned)
+  int* boffo = boff + 64;                          // 64: offset of block-column J in its owner
+  float* tiles = GT ? p.gtiles : scal + 192;   // owned block-columns
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = SYT_THREADS / 32;
   float* red = scal + 4;
   // address of `ptr` in CTA r of the cluster (plain local pointer for 1-CTA launches)
   auto rptr = [&](float* ptr, int r) -> float* { return C == 1 ? ptr : cluster.map_shared_rank(ptr, r); };
 
-  if (tid == 0) {
+  if (tid < C) {
     int off = 0;
     for (int J = 0; J < NB; ++J) {
-      if (syt_owner(J, C) == q) { boff[J] = off; off += 1024 * (NB - J); }
-      else boff[J] = -1;
+      if (syt_owner(J, C) == tid) {
+        boffo[J] = off;
+        if (tid == q) boff[J] = off;
+        off += 1024 * (NB - J);
+      } else if (tid == q) {
+        boff[J] = -1;
+      }
     }
   }
   for (int i = tid; i < 4 * m_pad; i += SYT_THREADS) vbuf[i] = 0.f;   // vbuf + ybuf
@@ -158,20 +184,24 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     float* y = ybuf + (k & 1) * m_pad;
     const bool have_prev = k > 0;
     const int kb = k >> 5, jk = k & 31;
-    // (a) owner of column k
-    if (boff[kb] >= 0) {
-      const int rows = m_pad - 32 * kb;
-      float* ck = tiles + boff[kb] + jk * rows - 32 * kb;   // ck[i], i >= k
-      if (have_prev) {
-        const float wk = wp[k], vk = vp[k];
-        for (int i = k + tid; i < m; i += SYT_THREADS) ck[i] -= vp[i] * wk + wp[i] * vk;
-      }
-      __syncthreads();
-      const float alpha = ck[k + 1];
+    // (a) every CTA: column k from its owner, pending update, v_k and tau_k
+    float tau;
+    {
+      const int own = syt_owner(kb, C), rows = m_pad - 32 * kb;
+      const float* ck = rptr(tiles + boffo[kb] + jk * rows - 32 * kb, own);   // ck[i], i >= k
+      const float wk = wp[k], vk = vp[k];
       float ss = 0.f;
-      for (int i = k + 2 + tid; i < m; i += SYT_THREADS) ss += ck[i] * ck[i];
-      ss = block_sum(ss, red);
-      float tau, beta, scale;
+      for (int i = k + tid; i < m; i += SYT_THREADS) {
+        float x = ck[i];
+        if (have_prev) x -= vp[i] * wk + wp[i] * vk;
+        if (i >= k + 2) ss = fmaf(x, x, ss);
+        else scal[40 + (i - k)] = x;          // d_k (i = k), alpha (i = k + 1)
+        v[i] = x;
+      }
+      for (int i = tid; i < m_pad; i += SYT_THREADS) y[i] = 0.f;
+      ss = syt_block_sum(ss, red);
+      const float dk = scal[40], alpha = scal[41];
+      float beta, scale;
       if (ss == 0.f) {
         tau = 0.f; beta = alpha; scale = 0.f;
       } else {
@@ -180,25 +210,22 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
         tau = (beta - alpha) / beta;
         scale = 1.f / (alpha - beta);
       }
-      for (int i = tid; i < m_pad; i += SYT_THREADS) {
+      const bool owner = (q == own);
+      float* kcol = K + (long)k * ld;
+      for (int i = k + tid; i < m; i += SYT_THREADS) {
         float vi = 0.f;
         if (i == k + 1) vi = 1.f;
-        else if (i >= k + 2 && i < m) { vi = ck[i] * scale; ck[i] = vi; }
-        for (int r = 0; r < C; ++r) *rptr(v + i, r) = vi;
+        else if (i >= k + 2) { vi = v[i] * scale; if (owner) kcol[i] = vi; }
+        v[i] = vi;
       }
       if (tid == 0) {
-        p.d[k] = ck[k];
-        p.e[k] = beta;
-        p.tau[k] = tau;
-        for (int r = 0; r < C; ++r) *rptr(scal + (k & 1), r) = tau;
+        if (k >= 1) v[k - 1] = 0.f;           // stale 1 of v_{k-2} (same parity buffer)
+        if (owner) { p.d[k] = dk; p.e[k] = beta; p.tau[k] = tau; }
       }
     }
     SYT_T(0);
-    if (C > 1) cluster.sync(); else __syncthreads();             // (1) v_k, tau_k everywhere
-    SYT_T(1);
-    const float tau = scal[k & 1];
-    for (int i = tid; i < m_pad; i += SYT_THREADS) y[i] = 0.f;
     __syncthreads();
+    SYT_T(1);
     // (b) tiles (I >= J) of owned block-columns that have columns j > k, one per warp
     int tcount = 0;
     for (int J = kb; J < NB; ++J) {
@@ -272,7 +299,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       ys[i] = s;
       pv = fmaf(s, v[i], pv);
     }
-    pv = block_sum(pv, red);
+    pv = syt_block_sum(pv, red);
     const float gamma = 0.5f * tau * tau * pv;
     for (int i = tid; i < m_pad; i += SYT_THREADS)
       wp[i] = (i > k && i < m) ? tau * ys[i] - gamma * v[i] : 0.f;
@@ -314,20 +341,6 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     if (boff[b1] >= 0 && tid == 0) {
       const int rows = m_pad - 32 * b1;
       p.d[m - 1] = tiles[boff[b1] + ((m - 1) & 31) * rows - 32 * b1 + m - 1];
-    }
-  }
-  // reflectors back to K's lower triangle (rows >= j) for the back-transform
-  for (int J = 0; J < NB; ++J) {
-    if (boff[J] < 0) continue;
-    const int rows = m_pad - 32 * J;
-    const float* blk = tiles + boff[J];
-    for (int jj = warp; jj < 32; jj += NW) {
-      const int j = 32 * J + jj;
-      if (j >= m) continue;
-      for (int ii = lane; ii < rows; ii += 32) {
-        const int i = 32 * J + ii;
-        if (i >= j && i < m) K[i + (long)j * ld] = blk[jj * rows + ii];
-      }
     }
   }
   if (C > 1) cluster.sync();   // no CTA exits while others may still address its smem

@@ -88,7 +88,6 @@ class BKFACStack:
         self.cur = [0] * len(self.my_factors)
         self.k = 0
         self.n_overwrites = 0
-        self.side = None   # side stream for the dense EA accumulate
         self.S: Dict[int, "torch.Tensor"] = {}
         for li in self.my_layers:
             dG, dA, _, _ = self.layers[li]
@@ -135,29 +134,19 @@ class BKFACStack:
                                       D_out=self.D[i][self.cur[i]]))
                 self.ctx.bkfac_rsvd_batch(items, main)
                 self.n_overwrites += 1
-        ea_done = None
-        if self.rsvd_every:
-            # the dense EA accumulate (a8) needs only M_k and must follow this step's RSVD
-            # read of Mcal_{k-1}: it runs on a side stream, overlapped with the Brand update
-            if self.side is None:
-                self.side = torch.cuda.Stream(device=self.device)
-            ev = torch.cuda.Event()
-            ev.record(main)
-            self.side.wait_event(ev)
-            for g in self.my_factors:
-                M[g].record_stream(self.side)
-            self.ctx.bkfac_ea_batch([dict(factor=i, K=self.K[i], M=M[g],
-                                          rho=self.rho if k > 0 else 0.0)
-                                     for i, g in enumerate(self.my_factors)], self.side)
-            ea_done = torch.cuda.Event()
-            ea_done.record(self.side)
         ups = []
         for i, g in enumerate(self.my_factors):
             c, nx = self.cur[i], 1 - self.cur[i]
             ups.append(dict(factor=i, U_in=self.U[i][c], D_in=self.D[i][c], M=M[g],
                             U_out=self.U[i][nx], D_out=self.D[i][nx], alpha=alpha, beta=beta,
                             flags=self.brand_flags))
-        if ups:
+        if self.rsvd_every:
+            # the dense EA accumulate (a8) needs only M_k and must follow this step's RSVD
+            # read of Mcal_{k-1}; the library overlaps it with the Brand eigensolver
+            ea = [dict(factor=i, K=self.K[i], M=M[g], rho=self.rho if k > 0 else 0.0)
+                  for i, g in enumerate(self.my_factors)]
+            self.ctx.bkfac_brand_ea_update(ups, ea, main)
+        elif ups:
             self.ctx.bkfac_brand_update(ups, main)
         for i in range(len(self.my_factors)):
             self.cur[i] = 1 - self.cur[i]
@@ -173,8 +162,6 @@ class BKFACStack:
                                   flags=self.precond_flags))
             self.ctx.bkfac_precondition(items, main)
             out = {li: self.S[li] for li in self.my_layers}
-        if ea_done is not None:
-            main.wait_event(ea_done)
         self.k += 1
         return out
 

@@ -346,3 +346,52 @@ def test_rsvd_batch_mixed_shapes(cuda_lib):
         Uo, Do = O.rsvd_overwrite(Kg, r, ro, 2, it["seed"], 1)
         assert lowrank_rel_err(Uo, Do, from_dev_cols(U), D.double().cpu().numpy()) < TOL_STEP
     assert ctx.bkfac_check()[0] == 0
+
+
+def test_brand_ea_update_equals_sequential(cuda_lib):
+    """bkfac_brand_ea_update (EA GEMM forked beside the eigensolver, capped grid) gives the
+    same bits as bkfac_ea_accumulate_batch + bkfac_brand_update in sequence, and K matches
+    the oracle's EA recursion (Alg 1 line 16)."""
+    import torch
+    shapes = [(577, 64, 220), (300, 32, 40), (96, 8, 100), (1000, 96, 150)]   # incl. dense path
+    rho = 0.95
+    ctxs = [_ctx([(n, min(r, n), c, 1) for (n, c, r) in shapes]) for _ in range(2)]
+    state = []
+    for fused in (False, True):
+        ctx = ctxs[int(fused)]
+        Ks = [torch.zeros((n, n), device="cuda") for (n, _, _) in shapes]
+        U = [to_dev_cols(synth.phantom_basis(n, min(r, n))) for (n, _, r) in shapes]
+        D = [torch.zeros((min(r, n),), device="cuda") for (n, _, r) in shapes]
+        Kref = [None] * len(shapes)
+        for k in range(3):
+            Ms = [to_dev_cols(synth.random_case(n, c, min(r, n), seed=77 + 10 * i, k=16).batch(k))
+                  for i, (n, c, r) in enumerate(shapes)]
+            Uo = [torch.empty_like(u) for u in U]
+            Do = [torch.empty_like(d) for d in D]
+            a, b = (0.0, 1.0) if k == 0 else (rho, 1 - rho)
+            ups = [dict(factor=i, U_in=U[i], D_in=D[i], M=Ms[i], U_out=Uo[i], D_out=Do[i],
+                        alpha=a, beta=b) for i in range(len(shapes))]
+            ea = [dict(factor=i, K=Ks[i], M=Ms[i], rho=rho if k else 0.0) for i in range(len(shapes))]
+            if fused:
+                ctx.bkfac_brand_ea_update(ups, ea)
+            else:
+                ctx.bkfac_ea_batch(ea)
+                ctx.bkfac_brand_update(ups)
+            U, D = Uo, Do
+            for i in range(len(shapes)):
+                Mi = Ms[i].double().cpu().numpy().T
+                Kref[i] = O.ea_update(Kref[i], Mi, rho)
+        torch.cuda.synchronize()
+        assert ctx.bkfac_check()[0] == 0
+        for i in range(len(shapes)):
+            Kg = Ks[i].double().cpu().numpy()
+            assert np.abs(Kg - Kref[i]).max() / np.abs(Kref[i]).max() < 1e-5
+        state.append(([u.cpu() for u in U], [d.cpu() for d in D], [K.cpu() for K in Ks]))
+    # K: the same GEMM tiles on fewer CTAs -> same bits.  U, D: the tridiagonalisation sums
+    # its partial y with shared-memory float atomics (order not fixed), so two runs agree
+    # to rounding, not bitwise
+    for Ks, Kf in zip(state[0][2], state[1][2]):
+        assert torch.equal(Ks, Kf)
+    for Us, Ds, Uf, Df in zip(state[0][0], state[0][1], state[1][0], state[1][1]):
+        Us, Ds, Uf, Df = (t.double().numpy() for t in (Us, Ds, Uf, Df))
+        assert lowrank_rel_err(Us.T, Ds, Uf.T, Df) < 1e-5

@@ -5,20 +5,22 @@ import numpy as np, torch
 from paper_2210_08494_b200 import binding
 lib = binding.load()
 lib.bkfac_debug_tc.argtypes = [ctypes.c_void_p, ctypes.c_int]
-for (ta, tb, M, N, K) in [(False, False, 8192, 8192, 8192), (False, True, 4097, 16384, 1024)]:
+for (ta, tb, M, N, K, beta) in [(False, False, 8192, 8192, 8192, 0.0), (False, True, 4097, 16384, 1024, 0.0),
+                                (False, True, 4609, 4609, 256, 0.0), (False, True, 4609, 4609, 256, 0.95),
+                                (False, True, 4608, 4608, 256, 0.95)]:
     A = torch.randn((M, K) if ta else (K, M), device="cuda")
     B = torch.randn((K, N) if tb else (N, K), device="cuda")
     C = torch.zeros((N, M), device="cuda")
-    binding.bkfac_gemm(ta, tb, 1.0, A, B, 0.0, C); torch.cuda.synchronize()
+    binding.bkfac_gemm(ta, tb, 1.0, A, B, beta, C); torch.cuda.synchronize()
     lib.bkfac_debug_tc(None, 1); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(); binding.bkfac_gemm(ta, tb, 1.0, A, B, 0.0, C); e1.record(); torch.cuda.synchronize()
+    e0.record(); binding.bkfac_gemm(ta, tb, 1.0, A, B, beta, C); e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     buf = (ctypes.c_ulonglong * (148 * 8))()
     lib.bkfac_debug_tc(ctypes.addressof(buf), 0)
     a = np.array(buf, dtype=np.float64).reshape(148, 8)
     cyc = ms * 1e-3 * 1.9e9
     nch = a[:, 3].mean()
-    print(f"{M}x{N}x{K} ta={ta} tb={tb}: {ms:.3f} ms ~{cyc:.0f} cyc; per CTA chunks {nch:.0f}; per chunk: "
+    print(f"{M}x{N}x{K} ta={ta} tb={tb} beta={beta}: {ms:.3f} ms ~{cyc:.0f} cyc; per CTA chunks {nch:.0f}; per chunk: "
           f"wait tempty {a[:,0].mean()/nch:.0f}  wait full {a[:,1].mean()/nch:.0f}  issue {a[:,2].mean()/nch:.0f}  "
           f"(total cyc/chunk {cyc/nch:.0f})")
