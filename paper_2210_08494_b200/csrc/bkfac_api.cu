@@ -450,7 +450,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
     prof_begin(ctx, "eig_invit", st, 0.0, 8.0 * mr);
-    invit_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, 128)), 128,
+    invit_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, INV_THREADS)), INV_THREADS,
                    sizeof(double) * 2 * (size_t)mmax, st>>>(b);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);

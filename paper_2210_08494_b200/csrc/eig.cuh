@@ -148,11 +148,16 @@ BKFAC_DEV double hash_unit(unsigned a, unsigned b) {
   return ((double)h / 4294967296.0) - 0.5;
 }
 
-// grid: (nprob, ceil(rmax/128)), block 128: thread = eigenvector j.  smem: 2m doubles.
+// grid: (nprob, ceil(rmax/INV_THREADS)), block INV_THREADS: thread = eigenvector j.
+// smem: 2m doubles.  Small blocks spread the latency-bound chains over every SM.
 // Chains (pivot recurrence, forward and back substitution) are carried in registers;
 // the per-vector arrays are written once per pass and read back in the next pass
-// (interleaved a[i*r + j] so a warp's accesses are coalesced).
-__global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigBatch b) {
+// (interleaved a[i*r + j] so a warp's accesses are coalesced).  U's diagonal is stored
+// inverted (one division per LU step, none in the substitutions); each iteration is two
+// streaming passes: the 2-norm is accumulated during back substitution and the
+// normalisation is folded into the next iteration's forward pass (one final scale pass).
+constexpr int INV_THREADS = 32;
+__global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   const int m = p.m, r = p.r;
   extern __shared__ __align__(16) double ism[];
@@ -174,8 +179,8 @@ __global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigB
   const int j = blockIdx.y * blockDim.x + threadIdx.x;
   if (j >= r) return;
   const double tiny = s_tiny;
-  double* dU = p.scr;                  // U diagonal
-  double* du = dU + (long)m * r;       // U first superdiagonal
+  double* dUi = p.scr;                 // 1 / (U diagonal)
+  double* du = dUi + (long)m * r;      // U first superdiagonal
   double* du2 = du + (long)m * r;      // U second superdiagonal
   double* dl = du2 + (long)m * r;      // multipliers
   unsigned char* pv = p.piv;
@@ -193,84 +198,118 @@ __global__ void __launch_bounds__(128) invit_kernel(const __grid_constant__ EigB
     if (fabs(dcur) >= fabs(sub)) {
       double piv = dcur;
       if (fabs(piv) < tiny) piv = (piv >= 0.0) ? tiny : -tiny;
-      const double f = sub / piv;
-      AT(dU, i) = piv; AT(du, i) = dufcur; AT(du2, i) = 0.0; AT(dl, i) = f; AT(pv, i) = 0;
+      const double rp = 1.0 / piv;
+      const double f = sub * rp;
+      AT(dUi, i) = rp; AT(du, i) = dufcur; AT(du2, i) = 0.0; AT(dl, i) = f; AT(pv, i) = 0;
       dcur = dnext - f * dufcur;
       dufcur = dunext;
     } else {
-      const double f = dcur / sub;
-      AT(dU, i) = sub; AT(du, i) = dnext; AT(du2, i) = dunext; AT(dl, i) = f; AT(pv, i) = 1;
+      const double rs = 1.0 / sub;
+      const double f = dcur * rs;
+      AT(dUi, i) = rs; AT(du, i) = dnext; AT(du2, i) = dunext; AT(dl, i) = f; AT(pv, i) = 1;
       dcur = dufcur - f * dnext;
       dufcur = -f * dunext;
     }
   }
   if (fabs(dcur) < tiny) dcur = (dcur >= 0.0) ? tiny : -tiny;
-  AT(dU, m - 1) = dcur;
+  AT(dUi, m - 1) = 1.0 / dcur;
   // start vector (deterministic, distinct per eigenvector)
   for (int i = 0; i < m; ++i) AT(x, i) = hash_unit((unsigned)i, (unsigned)j) + 0.5;
-  // The passes below stream the per-vector arrays; every dependent chain (carry, x1/x2)
-  // is in registers, and the array loads of a batch of IB entries are issued before the
-  // batch's stores (the compiler cannot reorder a load past a store to x it cannot prove
-  // distinct), so one memory latency is exposed per batch instead of per entry.
+  // Streaming passes in batches of IB entries: the batch's loads are issued together,
+  // unguarded (full batches; the ragged end runs entry by entry), and the recurrences are
+  // branch-free selects, so one memory latency is exposed per batch instead of per entry.
   constexpr int IB = 16;
+  const long R = r;
+  double* xj = x + j;
+  const double* dUj = dUi + j;
+  const double* duj = du + j;
+  const double* du2j = du2 + j;
+  const double* dlj = dl + j;
+  const unsigned char* pvj = pv + j;
+  double s = 1.0;   // pending scale of x (applied as x is read in the next pass)
+  double nrm = 0.0, amax = 0.0;
   for (int it = 0; it < 3; ++it) {
     // forward: apply L^{-1} with row interchanges; the running entry is carried
-    double carry = AT(x, 0);
-    for (int i0 = 0; i0 < m - 1; i0 += IB) {
+    double carry = xj[0] * s;
+    int i0 = 0;
+    for (; i0 + IB <= m - 1; i0 += IB) {
       double xn[IB], f[IB];
       unsigned char pw[IB];
 #pragma unroll
       for (int u = 0; u < IB; ++u) {
-        const int i = i0 + u;
-        if (i < m - 1) { xn[u] = AT(x, i + 1); f[u] = AT(dl, i); pw[u] = AT(pv, i); }
+        xn[u] = xj[(i0 + u + 1) * R];
+        f[u] = dlj[(i0 + u) * R];
+        pw[u] = pvj[(i0 + u) * R];
       }
 #pragma unroll
       for (int u = 0; u < IB; ++u) {
-        const int i = i0 + u;
-        if (i < m - 1) {
-          if (pw[u] == 0) {
-            AT(x, i) = carry;
-            carry = xn[u] - f[u] * carry;
-          } else {
-            AT(x, i) = xn[u];
-            carry = carry - f[u] * xn[u];
-          }
-        }
+        const double xs = xn[u] * s;
+        const bool sw = pw[u] != 0;
+        xj[(i0 + u) * R] = sw ? xs : carry;
+        carry = sw ? carry - f[u] * xs : xs - f[u] * carry;
       }
     }
-    // back substitution with U (bandwidth 2); x1, x2 carried
-    double x1 = carry / AT(dU, m - 1);
+    for (; i0 < m - 1; ++i0) {
+      const double xs = xj[(i0 + 1) * R] * s, f = dlj[i0 * R];
+      const bool sw = pvj[i0 * R] != 0;
+      xj[i0 * R] = sw ? xs : carry;
+      carry = sw ? carry - f * xs : xs - f * carry;
+    }
+    // back substitution with U (bandwidth 2); x1, x2 carried; ||x||_2^2 and max|x| on the fly
+    double x1 = carry * dUj[(m - 1) * R];
     double x2 = 0.0;
-    double amax = fabs(x1);
-    AT(x, m - 1) = x1;
-    for (int i0 = m - 2; i0 >= 0; i0 -= IB) {
+    nrm = x1 * x1;
+    amax = fabs(x1);
+    xj[(m - 1) * R] = x1;
+    int i1 = m - 2;
+    for (; i1 - IB + 1 >= 0; i1 -= IB) {
       double xv[IB], a0[IB], a1[IB], a2[IB];
 #pragma unroll
       for (int u = 0; u < IB; ++u) {
-        const int i = i0 - u;
-        if (i >= 0) { xv[u] = AT(x, i); a0[u] = AT(dU, i); a1[u] = AT(du, i); a2[u] = AT(du2, i); }
+        const long o = (i1 - u) * R;
+        xv[u] = xj[o]; a0[u] = dUj[o]; a1[u] = duj[o]; a2[u] = du2j[o];
       }
 #pragma unroll
       for (int u = 0; u < IB; ++u) {
-        const int i = i0 - u;
-        if (i >= 0) {
-          const double xi = (xv[u] - a1[u] * x1 - a2[u] * x2) / a0[u];
-          AT(x, i) = xi;
-          x2 = x1;
-          x1 = xi;
-          amax = fmax(amax, fabs(xi));
-        }
+        const double xi = (xv[u] - a1[u] * x1 - a2[u] * x2) * a0[u];
+        xj[(i1 - u) * R] = xi;
+        x2 = x1;
+        x1 = xi;
+        nrm = fma(xi, xi, nrm);
+        amax = fmax(amax, fabs(xi));
       }
     }
-    // normalise: scale by 1/max, then by 1/||x||_2 (two streaming passes)
-    const double s1 = (amax > 0.0 && isfinite(amax)) ? 1.0 / amax : 1.0;
-    double nrm = 0.0;
-    for (int i = 0; i < m; ++i) {
-      const double t = AT(x, i) * s1;
-      nrm += t * t;
+    for (; i1 >= 0; --i1) {
+      const long o = i1 * R;
+      const double xi = (xj[o] - duj[o] * x1 - du2j[o] * x2) * dUj[o];
+      xj[o] = xi;
+      x2 = x1;
+      x1 = xi;
+      nrm = fma(xi, xi, nrm);
+      amax = fmax(amax, fabs(xi));
     }
-    const double s2 = (nrm > 0.0) ? s1 / sqrt(nrm) : 0.0;
-    for (int i = 0; i < m; ++i) AT(x, i) *= s2;
+    if (nrm > 0.0 && isfinite(nrm)) {
+      s = 1.0 / sqrt(nrm);
+    } else {   // ||x||^2 overflowed (or x = 0): scale by 1/max now, renormalise below
+      s = (amax > 0.0 && isfinite(amax)) ? 1.0 / amax : 1.0;
+      nrm = 0.0;
+    }
+  }
+  if (nrm == 0.0) {   // the last iteration fell back to 1/max: exact 2-norm of s*x
+    double t2 = 0.0;
+    for (int i = 0; i < m; ++i) { const double t = xj[i * R] * s; t2 = fma(t, t, t2); }
+    s = (t2 > 0.0) ? s / sqrt(t2) : 0.0;
+  }
+  {
+    int i = 0;
+    for (; i + IB <= m; i += IB) {
+      double t[IB];
+#pragma unroll
+      for (int u = 0; u < IB; ++u) t[u] = xj[(i + u) * R];
+#pragma unroll
+      for (int u = 0; u < IB; ++u) xj[(i + u) * R] = t[u] * s;
+    }
+    for (; i < m; ++i) xj[i * R] *= s;
   }
 #undef AT
 }
