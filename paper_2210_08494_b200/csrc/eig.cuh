@@ -36,13 +36,23 @@ struct EigBatch { int nprob; EigProb p[EIG_MAXP]; };
 
 // ------------------------------------------------------------------ 2. bisection
 // Number of eigenvalues of T strictly below x (Sturm sequence of the LDL^T pivots).
+// e2 / q as e2 * rcp(q): hardware reciprocal seed + one Newton step (relative error
+// ~1e-14; the count's backward error stays far below the 1e-10 * span stopping width).
+// |q| >= pivmin (a normal number), so the flush-to-zero seed is exact in range.
+BKFAC_DEV double sturm_div(double e2, double q) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  y = fma(y, fma(-q, y, 1.0), y);
+  return e2 * y;
+}
+
 BKFAC_DEV int sturm_count(const double* dd, const double* e2, int m, double x, double pivmin) {
   int cnt = 0;
   double q = dd[0] - x;
   if (fabs(q) < pivmin) q = -pivmin;
   cnt += (q < 0.0);
   for (int i = 1; i < m; ++i) {
-    q = (dd[i] - x) - e2[i - 1] / q;
+    q = (dd[i] - x) - sturm_div(e2[i - 1], q);
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += (q < 0.0);
   }
@@ -106,7 +116,9 @@ __global__ void __launch_bounds__(BIS_WARPS * 32) bisect_kernel(const __grid_con
   const double pivmin = s_pivmin;
   // invariant: count(lo) <= kasc < count(hi).  Phase 1: 32-way multisection with fp32
   // Sturm counts (fast reciprocal) down to ~1e-6 of the spectrum's span; phase 2: the
-  // bracket, widened by the fp32 counts' backward error, refined with fp64 counts.
+  // bracket, widened by the fp32 counts' backward error, refined with fp64 counts to
+  // 1e-10 of the span (fp32 outputs; eigenvalues closer than 1e-7 ||T|| are treated as a
+  // cluster by stage 4, so inverse iteration never has to separate them).
   const double span = fmax(fabs(lo), fabs(hi));
   {
     const float pivf = 1e-30f;
@@ -128,7 +140,7 @@ __global__ void __launch_bounds__(BIS_WARPS * 32) bisect_kernel(const __grid_con
   }
   for (int round = 0; round < 10; ++round) {
     const double w = hi - lo;
-    if (w <= 1e-12 * span + pivmin) break;
+    if (w <= 1e-10 * span + pivmin) break;
     const double x = lo + w * (double)(lane + 1) / 33.0;
     const int cnt = sturm_count(dd, e2, m, x, pivmin);
     const unsigned above = __ballot_sync(0xffffffffu, cnt >= kasc + 1);
@@ -316,8 +328,9 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
 
 // ------------------------------------------------------------------ 4. clusters
 // One CTA (32 warps) per problem; clusters are runs of eigenvalues whose consecutive
-// gaps are <= 1e-9 * ||T|| (beyond that, fp64 inverse iteration is orthogonal to
-// ~1e-7).  Each warp orthonormalises one cluster by modified Gram-Schmidt.
+// gaps are <= 1e-7 * ||T|| (beyond that, three inverse iterations from shifts accurate to
+// 1e-10 * span separate the eigenvectors to ~1e-9).  Each warp orthonormalises one
+// cluster by modified Gram-Schmidt.
 __global__ void __launch_bounds__(1024) cluster_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   const int m = p.m, r = p.r;
@@ -328,7 +341,7 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const __grid_constant__ E
     double tn = 0.0;
     for (int j = 0; j < r; ++j) tn = fmax(tn, fabs(p.lam[j]));
     for (int i = 0; i < m; ++i) tn = fmax(tn, fabs((double)p.d[i]));
-    const double tol = 1e-9 * fmax(tn, 1e-300);
+    const double tol = 1e-7 * fmax(tn, 1e-300);
     int n = 0, st = 0;
     for (int j = 1; j <= r; ++j) {
       if (j == r || p.lam[j - 1] - p.lam[j] > tol) {
