@@ -1294,23 +1294,20 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
   GemmStage gs;
   // S1: scalars
   prof_begin(ctx, "prec_scalars", st, 0.0, 0.0);
-  for (int i0 = 0; i0 < count; i0 += PS_MAXP / 2) {
-    const int n = std::min(count - i0, PS_MAXP / 2);
+  for (int i0 = 0; i0 < count; i0 += PS_MAXP) {
+    const int n = std::min(count - i0, PS_MAXP);
     psb.nprob = 0;
     for (int i = i0; i < i0 + n; ++i) {
       const auto& a = args[i];
       const auto& lp = ctx->l[a.layer];
-      float* lam = at<float>(ctx, lp.lam);
-      psb.p[psb.nprob++] = PrecScalProb{a.D_A, lp.d.r_A, a.lambda_A, a.flags, at<float>(ctx, lp.sA), lam + 0};
-      psb.p[psb.nprob++] = PrecScalProb{a.D_G, lp.d.r_G, a.lambda_G, a.flags, at<float>(ctx, lp.sG), lam + 1};
+      PrecScalProb q{};
+      q.D[0] = a.D_A; q.r[0] = lp.d.r_A; q.lam[0] = a.lambda_A; q.s[0] = at<float>(ctx, lp.sA);
+      q.D[1] = a.D_G; q.r[1] = lp.d.r_G; q.lam[1] = a.lambda_G; q.s[1] = at<float>(ctx, lp.sG);
+      q.flags = a.flags;
+      q.lam_out = at<float>(ctx, lp.lam);   // {lambda_A, lambda_G, 1 / (lambda_G lambda_A)}
+      psb.p[psb.nprob++] = q;
     }
     prec_scalars_kernel<<<psb.nprob, 256, 0, st>>>(psb);
-    LAUNCH_CHECK(ctx);
-  }
-  for (int i0 = 0; i0 < count; ++i0) {
-    const auto& lp = ctx->l[args[i0].layer];
-    float* lam = at<float>(ctx, lp.lam);
-    prec_coef_kernel<<<1, 1, 0, st>>>(lam + 1, lam + 0, lam + 2);
     LAUNCH_CHECK(ctx);
   }
   prof_end(ctx, st);

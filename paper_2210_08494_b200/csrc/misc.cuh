@@ -60,34 +60,45 @@ __global__ void nonfinite_kernel(const __grid_constant__ NfBatch b) {
 }
 
 // ---- preconditioner scalars (Alg 1 lines 16-17) ---------------------
-// For each layer side: effective lambda (relative mode :940, continuation :711) and
-// s_i = (D_i + lambda)^{-1} - 1/lambda.  Writes s (r floats) and lambda_eff (1 float).
+// One CTA per layer.  For each side: effective lambda (relative mode :940, continuation
+// :711) and s_i = (D_i + lambda)^{-1} - 1/lambda; then the coefficient of J in S,
+// 1 / (lambda_G lambda_A).  Writes s_A, s_G and lam_out[0..2] = {lambda_A, lambda_G, coef}.
 struct PrecScalProb {
-  const float* D; int r; float lam; int flags;
-  float* s; float* lam_out;
+  const float* D[2]; int r[2]; float lam[2]; float* s[2];   // [0] = A side, [1] = Gamma side
+  int flags;
+  float* lam_out;
 };
 constexpr int PS_MAXP = 200;
 struct PrecScalBatch { int nprob; PrecScalProb p[PS_MAXP]; };
 
 __global__ void prec_scalars_kernel(const __grid_constant__ PrecScalBatch b) {
   const PrecScalProb& p = b.p[blockIdx.x];
-  __shared__ float s_min, s_max;
-  if (threadIdx.x == 0) {
+  __shared__ float s_min[2], s_max[2];
+  if (threadIdx.x < 2) {
+    const int q = threadIdx.x;
     float mn = 3.4e38f, mx = 0.f;
-    for (int i = 0; i < p.r; ++i) { mn = fminf(mn, p.D[i]); mx = fmaxf(mx, p.D[i]); }
-    if (p.r == 0) mn = 0.f;
-    s_min = mn; s_max = mx;
+    for (int i = 0; i < p.r[q]; ++i) { mn = fminf(mn, p.D[q][i]); mx = fmaxf(mx, p.D[q][i]); }
+    if (p.r[q] == 0) mn = 0.f;
+    s_min[q] = mn; s_max[q] = mx;
   }
   __syncthreads();
-  float lam = p.lam;
-  if (p.flags & 2) lam = lam * s_max;          // relative: lambda = phi * max D
-  float shift = 0.f;
-  if (p.flags & 1) { shift = s_min; lam += shift; }  // continuation
-  for (int i = threadIdx.x; i < p.r; i += blockDim.x) {
-    const float dd = p.D[i] - shift;
-    p.s[i] = 1.f / (dd + lam) - 1.f / lam;
+  float lam[2];
+  for (int q = 0; q < 2; ++q) {
+    float l = p.lam[q];
+    if (p.flags & 2) l = l * s_max[q];          // relative: lambda = phi * max D
+    float shift = 0.f;
+    if (p.flags & 1) { shift = s_min[q]; l += shift; }  // continuation
+    for (int i = threadIdx.x; i < p.r[q]; i += blockDim.x) {
+      const float dd = p.D[q][i] - shift;
+      p.s[q][i] = 1.f / (dd + l) - 1.f / l;
+    }
+    lam[q] = l;
   }
-  if (threadIdx.x == 0) *p.lam_out = lam;
+  if (threadIdx.x == 0) {
+    p.lam_out[0] = lam[0];
+    p.lam_out[1] = lam[1];
+    p.lam_out[2] = 1.f / (lam[1] * lam[0]);
+  }
 }
 
 // Scale rows/cols of small blocks by the preconditioner vectors:
@@ -112,11 +123,6 @@ __global__ void prec_scale_kernel(const __grid_constant__ PrecScaleBatch b) {
     else f *= p.s_row[i];
     p.Y[i + (long)j * p.ld] *= f;
   }
-}
-
-// Final coefficient of J in S: 1 / (lambda_G lambda_A), written to a device scalar.
-__global__ void prec_coef_kernel(const float* lamG, const float* lamA, float* coef) {
-  *coef = 1.f / (*lamG * *lamA);
 }
 
 // ---- Philox4x32-10 Gaussian sketch -------------------------------------

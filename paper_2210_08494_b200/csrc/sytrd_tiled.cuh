@@ -2,31 +2,34 @@
 // PAPER.md:505) with the lower triangle resident in the distributed shared memory of a
 // thread-block cluster, processed in 32 x 32 register tiles.
 //
-// Storage.  K is padded to m_pad = 32*NB rows/cols (zeros).  Block-column J (columns
-// 32J..32J+31, rows 32J..m_pad-1, col-major) lives in the shared memory of CTA
-// owner(J) of the cluster; block-columns are dealt to the C CTAs in boustrophedon order
-// (0..C-1, C-1..0, ...), which balances the triangular sizes.
+// Storage.  K is padded to m_pad = 32*NB rows/cols (zeros).  The lower tiles (I >= J) are
+// enumerated by decreasing block column J (then increasing I): pos(I, J) =
+// T(NB-1-J) + I - J, T(n) = n(n+1)/2, and dealt round-robin to the C CTAs of the cluster
+// (owner = pos % C, slot = pos / C; each tile 32 x 32 col-major in the owner's shared
+// memory).  The tiles still active at step k (J >= k/32) are a prefix of this order, so
+// every CTA holds an equal share (+-1) of the active tiles at EVERY step, and each CTA's
+// active tiles are a prefix of its slots: warp w takes slots w, w + NW, ...
 //
 // Step k (reflector H_k = I - tau v v^T zeroing column k below the subdiagonal):
-//   (a) EVERY CTA reads column k from its owner's shared memory (ld.shared::cluster; the
+//   (a) EVERY CTA reads column k from its owners' shared memory (ld.shared::cluster; the
 //       column is final after step k-1's tiles), applies the pending rank-2 update of step
 //       k-1 (A <- A - v w^T - w v^T) and forms v_k, tau_k (dlarfg) locally.  All CTAs
 //       compute bitwise-identical v_k (same inputs, same reduction order), so no
-//       broadcast and no cluster barrier is needed here; the owner writes d, e, tau and
+//       broadcast and no cluster barrier is needed here; CTA k % C writes d, e, tau and
 //       the reflector (rows >= k+2 of column k of K) to global memory;
-//   (b) every CTA walks its tiles (I >= J) of the trailing matrix with one warp per tile,
-//       lane = row: applies the pending update in registers, writes the tile back, and
-//       accumulates its partial y = A v_k both ways from the lower triangle -- row sums
-//       in a register, column sums by a 31-shuffle transpose-reduce; both go to the
-//       CTA's partial y with shared-memory atomics;                  cluster barrier
+//   (b) every CTA walks its active tiles with one warp per tile, lane = row: applies the
+//       pending update in registers, writes the tile back, and accumulates its partial
+//       y = A v_k both ways from the lower triangle -- row sums in a register, column
+//       sums by a 31-shuffle transpose-reduce; both go to the CTA's partial y with
+//       shared-memory atomics;                                        cluster barrier
 //   (c) every CTA sums the C partial y through DSMEM and forms
 //       w_k = tau y - (tau^2/2)(y.v) v locally.
 // One cluster barrier per step.  Hazards: the partial y are double-buffered by step
 // parity (a CTA rewrites a parity only after the next barrier, which every reader of the
 // previous use has passed); column k is never written after step k-1's tiles.
 // Per element of the trailing matrix and step: one LDS, one STS and five FP32 ops.
-// Outputs as sytrd_kernel: d, e, tau and the reflectors (rows >= k+2 of column k) in K's
-// lower triangle for the back-transform.
+// Outputs: d, e, tau and the reflectors (rows >= k+2 of column k) in K's lower triangle
+// for the back-transform.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -42,40 +45,31 @@ namespace cgt = cooperative_groups;
 constexpr int SYT_THREADS = 512;
 constexpr int SYT_SMEM_FLOATS = 55 * 1024;   // per-CTA budget (220 KB)
 
-__host__ __device__ inline int syt_owner(int J, int C) {
-  const int t = J / C, pos = J % C;
-  return (t & 1) ? C - 1 - pos : pos;
+__host__ __device__ inline int syt_tiles(int NB) { return NB * (NB + 1) / 2; }
+// enumeration position of lower tile (I, J): block columns NB-1, NB-2, ..., 0
+__host__ __device__ inline int syt_pos(int I, int J, int NB) {
+  const int n = NB - 1 - J;
+  return n * (n + 1) / 2 + (I - J);
 }
-// floats of tile storage owned by CTA q
-inline long syt_own_floats(int NB, int C, int q) {
-  long s = 0;
-  for (int J = 0; J < NB; ++J)
-    if (syt_owner(J, C) == q) s += 1024L * (NB - J);
-  return s;
-}
-inline int syt_vec_floats(int m_pad) { return 7 * m_pad + 64 + 128; }
-// smallest cluster size whose largest per-CTA share fits; 0 = does not fit
+inline int syt_vec_floats(int m_pad) { return 7 * m_pad + 64; }
+inline long syt_own_floats(int NB, int C) { return 1024L * ((syt_tiles(NB) + C - 1) / C); }
+// smallest cluster size whose per-CTA share fits; 0 = does not fit
 inline int sytrd_tiled_cluster(int m) {
   const int NB = (m + 31) / 32, m_pad = NB * 32;
-  for (int C = 1; C <= 8; C *= 2) {
-    long mx = 0;
-    for (int q = 0; q < C; ++q) mx = std::max(mx, syt_own_floats(NB, C, q));
-    if (mx + syt_vec_floats(m_pad) <= SYT_SMEM_FLOATS) return C;
-  }
+  for (int C = 1; C <= 8; C *= 2)
+    if (syt_own_floats(NB, C) + syt_vec_floats(m_pad) <= SYT_SMEM_FLOATS) return C;
   return 0;
 }
 inline size_t sytrd_tiled_smem_bytes(int m, int C) {
   const int NB = (m + 31) / 32, m_pad = NB * 32;
-  long mx = 0;
-  for (int q = 0; q < C; ++q) mx = std::max(mx, syt_own_floats(NB, C, q));
-  return sizeof(float) * (size_t)(mx + syt_vec_floats(m_pad));
+  return sizeof(float) * (size_t)(syt_own_floats(NB, C) + syt_vec_floats(m_pad));
 }
 
 // Tile storage of one factor when the tiles do not fit the cluster's shared memory
 // (GT = true: one CTA per factor, tiles in global memory / L2).
 inline size_t syt_global_tile_floats(int m) {
-  const size_t NB = (size_t)(m + 31) / 32;
-  return NB * (NB + 1) / 2 * 1024;
+  const int NB = (m + 31) / 32;
+  return (size_t)syt_tiles(NB) * 1024;
 }
 
 // Block sum with one barrier.  Precondition: every call is separated from the next one
@@ -109,44 +103,37 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   float* ys = ybuf + 2 * m_pad;      // m_pad      (summed y)
   float* wp = ys + m_pad;            // m_pad      (w_{k-1})
   float* scal = wp + m_pad;          // 64: [2] bad flag, [4..35] reduce, [40..41] alpha, d
-  int* boff = reinterpret_cast<int*>(scal + 64);   // 64: storage offset of block-column J (-1: not owned)
-  int* boffo = boff + 64;                          // 64: offset of block-column J in its owner
-  float* tiles = GT ? p.gtiles : scal + 192;   // owned block-columns
+  float* tiles = GT ? p.gtiles : scal + 64;   // owned tiles, slot s at 1024 s
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = SYT_THREADS / 32;
   float* red = scal + 4;
+  const int ntiles = syt_tiles(NB);
+  const int nown = (ntiles - q + C - 1) / C;          // tiles owned by this CTA
   // address of `ptr` in CTA r of the cluster (plain local pointer for 1-CTA launches)
   auto rptr = [&](float* ptr, int r) -> float* { return C == 1 ? ptr : cluster.map_shared_rank(ptr, r); };
+  // (I, J) of the tile at enumeration position pos (inverse of syt_pos)
+  auto tile_ij = [&](int pos, int& I, int& J) {
+    int n = (int)((sqrtf(8.f * pos + 1.f) - 1.f) * 0.5f);   // largest n: n(n+1)/2 <= pos
+    while (n * (n + 1) / 2 > pos) --n;
+    while ((n + 1) * (n + 2) / 2 <= pos) ++n;
+    J = NB - 1 - n;
+    I = J + (pos - n * (n + 1) / 2);
+  };
 
-  if (tid < C) {
-    int off = 0;
-    for (int J = 0; J < NB; ++J) {
-      if (syt_owner(J, C) == tid) {
-        boffo[J] = off;
-        if (tid == q) boff[J] = off;
-        off += 1024 * (NB - J);
-      } else if (tid == q) {
-        boff[J] = -1;
-      }
-    }
-  }
   for (int i = tid; i < 4 * m_pad; i += SYT_THREADS) vbuf[i] = 0.f;   // vbuf + ybuf
   for (int i = tid; i < 2 * m_pad; i += SYT_THREADS) ys[i] = 0.f;     // ys + wp
-  __syncthreads();
-  // load owned block-columns (zero padding) + finiteness check
+  // load owned tiles (zero padding) + finiteness check
   int bad = 0;
-  for (int J = 0; J < NB; ++J) {
-    if (boff[J] < 0) continue;
-    const int rows = m_pad - 32 * J;
-    float* blk = tiles + boff[J];
-    for (int jj = warp; jj < 32; jj += NW) {
+  for (int sl = warp; sl < nown; sl += NW) {
+    int I, J;
+    tile_ij(sl * C + q, I, J);
+    float* t = tiles + 1024L * sl;
+    const int i = 32 * I + lane;
+    for (int jj = 0; jj < 32; ++jj) {
       const int j = 32 * J + jj;
-      for (int ii = lane; ii < rows; ii += 32) {
-        const int i = 32 * J + ii;
-        float a = 0.f;
-        if (i < m && j < m && i >= j) { a = K[i + (long)j * ld]; bad |= !isfinite(a); }
-        blk[jj * rows + ii] = a;
-      }
+      float a = 0.f;
+      if (i < m && j < m && i >= j) { a = K[i + (long)j * ld]; bad |= !isfinite(a); }
+      t[jj * 32 + lane] = a;
     }
   }
   bad = __syncthreads_or(bad);
@@ -179,20 +166,20 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
 #define SYT_T(i) do {} while (0)
 #endif
   for (int k = 0; k < m - 2; ++k) {
-    float* v = vbuf + (k & 1) * m_pad;            // v_k (written by the owner)
+    float* v = vbuf + (k & 1) * m_pad;            // v_k
     const float* vp = vbuf + ((k + 1) & 1) * m_pad;   // v_{k-1} (zero at k = 0)
     float* y = ybuf + (k & 1) * m_pad;
     const bool have_prev = k > 0;
     const int kb = k >> 5, jk = k & 31;
-    // (a) every CTA: column k from its owner, pending update, v_k and tau_k
+    // (a) every CTA: column k from its owners, pending update, v_k and tau_k
     float tau;
     {
-      const int own = syt_owner(kb, C), rows = m_pad - 32 * kb;
-      const float* ck = rptr(tiles + boffo[kb] + jk * rows - 32 * kb, own);   // ck[i], i >= k
+      const int base = syt_pos(kb, kb, NB);
       const float wk = wp[k], vk = vp[k];
       float ss = 0.f;
       for (int i = k + tid; i < m; i += SYT_THREADS) {
-        float x = ck[i];
+        const int pos = base + (i >> 5) - kb;
+        float x = *rptr(tiles + 1024L * (pos / C) + jk * 32 + (i & 31), pos % C);
         if (have_prev) x -= vp[i] * wk + wp[i] * vk;
         if (i >= k + 2) ss = fmaf(x, x, ss);
         else scal[40 + (i - k)] = x;          // d_k (i = k), alpha (i = k + 1)
@@ -210,83 +197,79 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
         tau = (beta - alpha) / beta;
         scale = 1.f / (alpha - beta);
       }
-      const bool owner = (q == own);
+      const bool writer = (q == k % C);
       float* kcol = K + (long)k * ld;
       for (int i = k + tid; i < m; i += SYT_THREADS) {
         float vi = 0.f;
         if (i == k + 1) vi = 1.f;
-        else if (i >= k + 2) { vi = v[i] * scale; if (owner) kcol[i] = vi; }
+        else if (i >= k + 2) { vi = v[i] * scale; if (writer) kcol[i] = vi; }
         v[i] = vi;
       }
       if (tid == 0) {
         if (k >= 1) v[k - 1] = 0.f;           // stale 1 of v_{k-2} (same parity buffer)
-        if (owner) { p.d[k] = dk; p.e[k] = beta; p.tau[k] = tau; }
+        if (writer) { p.d[k] = dk; p.e[k] = beta; p.tau[k] = tau; }
       }
     }
     SYT_T(0);
     __syncthreads();
     SYT_T(1);
-    // (b) tiles (I >= J) of owned block-columns that have columns j > k, one per warp
-    int tcount = 0;
-    for (int J = kb; J < NB; ++J) {
-      if (boff[J] < 0) continue;
-      const int rows = m_pad - 32 * J;
-      float* blkc = tiles + boff[J];
+    // (b) active tiles (J >= kb): this CTA's slots 0 .. nact-1, one per warp
+    const int nact = (syt_tiles(NB - kb) - q + C - 1) / C;
+    for (int sl = warp; sl < nact; sl += NW) {
+      int I, J;
+      tile_ij(sl * C + q, I, J);
+      float* tcol = tiles + 1024L * sl + lane;   // + jj * 32
+      const int i = 32 * I + lane;
       const float cv = v[32 * J + lane], cvp = vp[32 * J + lane], cwp = wp[32 * J + lane];
-      for (int I = J; I < NB; ++I, ++tcount) {
-        if ((tcount % NW) != warp) continue;
-        float* tcol = blkc + 32 * (I - J) + lane;   // + jj * rows
-        const int i = 32 * I + lane;
-        const float vi = v[i], vpi = vp[i], wpi = wp[i];
-        // all 32 loads first: a store to column jj must not order the load of column
-        // jj+1 behind it (the compiler cannot prove they differ)
-        float colv[32];
+      const float vi = v[i], vpi = vp[i], wpi = wp[i];
+      // all 32 loads first: a store to column jj must not order the load of column
+      // jj+1 behind it (the compiler cannot prove they differ)
+      float colv[32];
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) colv[jj] = tcol[jj * rows];
-        float racc[4] = {0.f, 0.f, 0.f, 0.f};
-        if ((32 * J > k) && (I > J)) {
+      for (int jj = 0; jj < 32; ++jj) colv[jj] = tcol[jj * 32];
+      float racc[4] = {0.f, 0.f, 0.f, 0.f};
+      if ((32 * J > k) && (I > J)) {
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            float x = colv[jj];
-            if (have_prev) {
-              x -= vpi * __shfl_sync(0xffffffffu, cwp, jj) + wpi * __shfl_sync(0xffffffffu, cvp, jj);
-              tcol[jj * rows] = x;
-            }
-            racc[jj & 3] = fmaf(x, __shfl_sync(0xffffffffu, cv, jj), racc[jj & 3]);
-            colv[jj] = x * vi;
+        for (int jj = 0; jj < 32; ++jj) {
+          float x = colv[jj];
+          if (have_prev) {
+            x -= vpi * __shfl_sync(0xffffffffu, cwp, jj) + wpi * __shfl_sync(0xffffffffu, cvp, jj);
+            tcol[jj * 32] = x;
           }
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const int j = 32 * J + jj;
-            const bool valid = (j > k) && (i >= j);
-            const float cwpj = __shfl_sync(0xffffffffu, cwp, jj);
-            const float cvpj = __shfl_sync(0xffffffffu, cvp, jj);
-            const float cvj = __shfl_sync(0xffffffffu, cv, jj);
-            float x = colv[jj];
-            if (valid && have_prev) {
-              x -= vpi * cwpj + wpi * cvpj;
-              tcol[jj * rows] = x;
-            }
-            const float xe = valid ? x : 0.f;
-            racc[jj & 3] = fmaf(xe, cvj, racc[jj & 3]);
-            colv[jj] = (i > j) ? xe * vi : 0.f;
-          }
+          racc[jj & 3] = fmaf(x, __shfl_sync(0xffffffffu, cv, jj), racc[jj & 3]);
+          colv[jj] = x * vi;
         }
-        // transpose-reduce: lane l ends with sum over lanes of colv[l]
+      } else {
 #pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) {
-          const bool upper = (lane & s) != 0;
-#pragma unroll
-          for (int t = 0; t < s; ++t) {
-            const float send = upper ? colv[t] : colv[t + s];
-            const float keep = upper ? colv[t + s] : colv[t];
-            colv[t] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        for (int jj = 0; jj < 32; ++jj) {
+          const int j = 32 * J + jj;
+          const bool valid = (j > k) && (i >= j);
+          const float cwpj = __shfl_sync(0xffffffffu, cwp, jj);
+          const float cvpj = __shfl_sync(0xffffffffu, cvp, jj);
+          const float cvj = __shfl_sync(0xffffffffu, cv, jj);
+          float x = colv[jj];
+          if (valid && have_prev) {
+            x -= vpi * cwpj + wpi * cvpj;
+            tcol[jj * 32] = x;
           }
+          const float xe = valid ? x : 0.f;
+          racc[jj & 3] = fmaf(xe, cvj, racc[jj & 3]);
+          colv[jj] = (i > j) ? xe * vi : 0.f;
         }
-        atomicAdd(&y[i], (racc[0] + racc[1]) + (racc[2] + racc[3]));
-        atomicAdd(&y[32 * J + lane], colv[0]);
       }
+      // transpose-reduce: lane l ends with sum over lanes of colv[l]
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) {
+        const bool upper = (lane & s) != 0;
+#pragma unroll
+        for (int t = 0; t < s; ++t) {
+          const float send = upper ? colv[t] : colv[t + s];
+          const float keep = upper ? colv[t + s] : colv[t];
+          colv[t] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+      }
+      atomicAdd(&y[i], (racc[0] + racc[1]) + (racc[2] + racc[3]));
+      atomicAdd(&y[32 * J + lane], colv[0]);
     }
     __syncthreads();
     SYT_T(2);
@@ -312,35 +295,21 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     for (int i = 0; i < 5; ++i) o[i] = tacc[i];
   }
 #endif
-  // trailing 2x2 block: the pending update of step m-3, then d, e
+  // trailing 2x2 block: the pending update of step m-3 (v_{m-3}, w_{m-3}), then d, e;
+  // each element by the CTA that owns it
   {
-    const int k = m - 2;
-    const float* vp = vbuf + ((k + 1) & 1) * m_pad;
-    const int b2 = (m - 2) >> 5, b1 = (m - 1) >> 5;
-    if (boff[b2] >= 0 && tid < 2) {
-      const int rows = m_pad - 32 * b2;
-      float* c2 = tiles + boff[b2] + ((m - 2) & 31) * rows - 32 * b2;
-      const int i = m - 2 + tid;
-      c2[i] -= vp[i] * wp[m - 2] + wp[i] * vp[m - 2];
-    }
-    if (boff[b1] >= 0 && tid == 32) {
-      const int rows = m_pad - 32 * b1;
-      float* c1 = tiles + boff[b1] + ((m - 1) & 31) * rows - 32 * b1;
-      c1[m - 1] -= 2.f * vp[m - 1] * wp[m - 1];
-    }
-    __syncthreads();
-    if (boff[b2] >= 0 && tid == 0) {
-      const int rows = m_pad - 32 * b2;
-      const float* c2 = tiles + boff[b2] + ((m - 2) & 31) * rows - 32 * b2;
-      p.d[m - 2] = c2[m - 2];
-      p.e[m - 2] = c2[m - 1];
-      p.e[m - 1] = 0.f;
-      p.tau[m - 2] = 0.f;
-      p.tau[m - 1] = 0.f;
-    }
-    if (boff[b1] >= 0 && tid == 0) {
-      const int rows = m_pad - 32 * b1;
-      p.d[m - 1] = tiles[boff[b1] + ((m - 1) & 31) * rows - 32 * b1 + m - 1];
+    const float* vq = vbuf + ((m - 1) & 1) * m_pad;   // v_{m-3}
+    if (tid < 3) {
+      const int i = (tid == 0) ? m - 2 : m - 1, j = (tid == 2) ? m - 1 : m - 2;
+      const int pos = syt_pos(i >> 5, j >> 5, NB);
+      if (pos % C == q) {
+        float* a = tiles + 1024L * (pos / C) + (j & 31) * 32 + (i & 31);
+        const float x = *a - (vq[i] * wp[j] + wp[i] * vq[j]);
+        *a = x;
+        if (tid == 0) { p.d[m - 2] = x; p.tau[m - 2] = 0.f; }
+        if (tid == 1) { p.e[m - 2] = x; p.e[m - 1] = 0.f; }
+        if (tid == 2) { p.d[m - 1] = x; p.tau[m - 1] = 0.f; }
+      }
     }
   }
   if (C > 1) cluster.sync();   // no CTA exits while others may still address its smem
