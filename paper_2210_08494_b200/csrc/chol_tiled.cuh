@@ -79,17 +79,26 @@ BKFAC_DEV void tile_stage(float* dst, const float* src, int lane) {
 }
 
 // ---- 32 x 32 diagonal tile on one warp, fully unrolled by templates (compile-time
-// register indices: no local memory).  Factor: lane = row i, a[j] = A(i, j).
-template <int K, int J>
-BKFAC_DEV void ct_upd(float (&a)[32], float lik, int lane) {
-  if constexpr (J < 32) {
-    const float ljk = __shfl_sync(0xffffffffu, lik, J);
-    if (lane >= J) a[J] = fmaf(-lik, ljk, a[J]);
-    ct_upd<K, J + 1>(a, lik, lane);
+// register indices: no local memory).  Factor: lane = row i, a[j] = A(i, j).  Step K
+// publishes column K of L to shared memory (col-major scratch D) and every lane reads it
+// back as broadcast float4 loads (8 loads instead of 31 shuffles per step).
+template <int K, int Q>
+BKFAC_DEV void ct_upd4(float (&a)[32], float lik, const float* D, int lane) {
+  if constexpr (Q < 8) {
+    if constexpr (4 * Q + 3 > K) {
+      const float4 l4 = reinterpret_cast<const float4*>(D + K * 32)[Q];
+      const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = 4 * Q + t;
+        if (j > K && lane >= j) a[j] = fmaf(-lik, lv[t], a[j]);
+      }
+    }
+    ct_upd4<K, Q + 1>(a, lik, D, lane);
   }
 }
 template <int K>
-BKFAC_DEV void ct_factor(float (&a)[32], int lane, int nreal, float tol, int& dropped) {
+BKFAC_DEV void ct_factor(float (&a)[32], float* D, int lane, int nreal, float tol, int& dropped) {
   if constexpr (K < 32) {
     const float akk = __shfl_sync(0xffffffffu, a[K], K);
     const bool drop = (K < nreal) && !(akk > tol);
@@ -98,29 +107,37 @@ BKFAC_DEV void ct_factor(float (&a)[32], int lane, int nreal, float tol, int& dr
     dropped |= drop;
     const float lik = (lane > K) ? a[K] * rs : (lane == K ? lkk : 0.f);
     a[K] = lik;
-    ct_upd<K, K + 1>(a, lik, lane);
-    ct_factor<K + 1>(a, lane, nreal, tol, dropped);
+    if constexpr (K < 31) {
+      D[K * 32 + lane] = lik;
+      __syncwarp();
+      ct_upd4<K, 0>(a, lik, D, lane);
+    }
+    ct_factor<K + 1>(a, D, lane, nreal, tol, dropped);
   }
 }
-// Inverse of the lower-triangular tile held as a (lane = row): lane j computes column j
-// of X = L^{-1}: x[i] = X(i, j).
-template <int I, int Kk>
-BKFAC_DEV void ct_inv_dot(const float (&a)[32], const float (&x)[32], float& s, int lane) {
-  if constexpr (Kk < I) {
-    const float lik = __shfl_sync(0xffffffffu, a[Kk], I);
-    if (Kk >= lane) s = fmaf(lik, x[Kk], s);
-    ct_inv_dot<I, Kk + 1>(a, x, s, lane);
+// Inverse of the lower-triangular tile: R (row-major copy of L in shared memory) is read
+// row by row as broadcast float4 loads; lane j computes column j of X = L^{-1}:
+// x[i] = X(i, j) = (delta_ij - sum_{k<i} L(i,k) x[k]) / L(i,i).
+template <int I, int Q>
+BKFAC_DEV void ct_inv_dot4(const float* R, const float (&x)[32], float& s) {
+  if constexpr (4 * Q < I) {
+    const float4 l4 = reinterpret_cast<const float4*>(R + I * 32)[Q];
+    const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (4 * Q + t < I) s = fmaf(lv[t], x[4 * Q + t], s);
+    ct_inv_dot4<I, Q + 1>(R, x, s);
   }
 }
 template <int I>
-BKFAC_DEV void ct_inverse(const float (&a)[32], float (&x)[32], int lane) {
+BKFAC_DEV void ct_inverse(const float* R, float (&x)[32], int lane) {
   if constexpr (I < 32) {
     float s = 0.f;
-    ct_inv_dot<I, 0>(a, x, s, lane);
-    const float lii = __shfl_sync(0xffffffffu, a[I], I);
+    ct_inv_dot4<I, 0>(R, x, s);          // terms with x[k] = 0 (k < lane) add zero
+    const float lii = R[I * 32 + I];
     const float rinv = (lii > 0.f) ? __frcp_rn(lii) : 0.f;
     x[I] = (I < lane) ? 0.f : (I == lane ? rinv : -s * rinv);
-    ct_inverse<I + 1>(a, x, lane);
+    ct_inverse<I + 1>(R, x, lane);
   }
 }
 
@@ -199,12 +216,20 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
         for (int j = 0; j < 32; ++j) if (j == lane) a[j] += sh;
       }
       int dropped = 0;
-      ct_factor<0>(a, lane, c - 32 * J, tol, dropped);
-      // write L_JJ (lower), zero the upper part
+      ct_factor<0>(a, sA, lane, c - 32 * J, tol, dropped);
+      // write L_JJ (lower), zero the upper part; row-major copy (lane = row) for the
+      // inverse, rows 16-byte aligned: element (i, j) at i*32 + j
 #pragma unroll
       for (int j = 0; j < 32; ++j) T[j * 32 + lane] = (lane >= j) ? a[j] : 0.f;
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(sB + lane * 32)[q] =
+            make_float4(lane >= 4 * q ? a[4 * q] : 0.f, lane >= 4 * q + 1 ? a[4 * q + 1] : 0.f,
+                        lane >= 4 * q + 2 ? a[4 * q + 2] : 0.f, lane >= 4 * q + 3 ? a[4 * q + 3] : 0.f);
+      __syncwarp();
       float x[32];
-      ct_inverse<0>(a, x, lane);
+      ct_inverse<0>(sB, x, lane);
       // X_JJ: row-major into the X tiles, col-major copy into Xd
       float* XJ = Xt + (size_t)ctix(J, J) * 1024;
       float* XJc = Xd + (size_t)J * 1024;
