@@ -349,7 +349,12 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
       const CholProb& q = v[i0 + i];
       b.p[i] = CholTiledProb{q.G, q.ldg, q.L, q.Linv, q.scratch, q.status, q.c, q.shift};
     }
-    chol_tiled_kernel<<<(unsigned)n, CT_THREADS, CT_SMEM_BYTES, st>>>(b);
+    int cmax = 0;
+    for (size_t i = 0; i < n; ++i) cmax = std::max(cmax, b.p[i].c);
+    if (cmax <= 32 * CS_MAXNB)   // every tile resident in shared memory
+      chol_smem_kernel<<<(unsigned)n, CT_THREADS, chol_smem_bytes(cmax), st>>>(b);
+    else
+      chol_tiled_kernel<<<(unsigned)n, CT_THREADS, CT_SMEM_BYTES, st>>>(b);
     LAUNCH_CHECK(ctx);
     i0 += n;
   }
@@ -676,6 +681,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   attr_ok &= cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(chol_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT_SMEM_BYTES) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem_bytes(32 * CS_MAXNB)) == cudaSuccess;
   attr_ok &= tc_init_attributes();
   if (!attr_ok) fprintf(stderr, "bkfac: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
   cudaGetLastError();  // never leave a sticky error behind
@@ -1413,6 +1419,12 @@ bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha
 void bkfac_debug_tc(unsigned long long* host, int reset) {
   if (reset) { static unsigned long long z[148 * 8]; cudaMemcpyToSymbol(g_tc_dbg, z, sizeof(z)); return; }
   cudaMemcpyFromSymbol(host, g_tc_dbg, sizeof(unsigned long long) * 148 * 8);
+}
+#endif
+#ifdef BKFAC_CHOL_TIMING
+void bkfac_debug_chol(unsigned long long* host, int reset) {
+  if (reset) { static unsigned long long z[8]; cudaMemcpyToSymbol(g_chol_dbg, z, sizeof(z)); return; }
+  cudaMemcpyFromSymbol(host, g_chol_dbg, sizeof(unsigned long long) * 8);
 }
 #endif
 #ifdef BKFAC_SYT_TIMING

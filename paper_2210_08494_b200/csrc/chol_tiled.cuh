@@ -158,7 +158,16 @@ inline size_t chol_tiled_scratch_floats(int c) {
   return 2 * NB * (NB + 1) / 2 * 1024 + NB * 1024;
 }
 
+#ifdef BKFAC_CHOL_TIMING
+__device__ unsigned long long g_chol_dbg[8];   // tuning builds: per-phase cycle sums (CTA 0)
+#define CT_T(ph) do { if (threadIdx.x == 0 && blockIdx.x == 0) { const unsigned long long tn = clock64(); g_chol_dbg[ph] += tn - ct_prev; ct_prev = tn; } } while (0)
+#else
+#define CT_T(ph) do {} while (0)
+#endif
 __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_constant__ CholTiledBatch b) {
+#ifdef BKFAC_CHOL_TIMING
+  unsigned long long ct_prev = clock64();
+#endif
   const CholTiledProb& p = b.p[blockIdx.x];
   const int c = p.c, NB = (c + 31) >> 5;
   const int ntile = NB * (NB + 1) / 2;
@@ -180,11 +189,18 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     const int J = t - I * (I + 1) / 2;
     float* T = Lt + (size_t)t * 1024;
+    float gv[32];   // all 32 loads in flight before the stores
+    const int i = 32 * I + lane;
+#pragma unroll
     for (int jj = 0; jj < 32; ++jj) {
-      const int i = 32 * I + lane, j = 32 * J + jj;
-      float g;
-      if (i < c && j < c) g = (i >= j) ? p.G[i + (long)j * p.ldg] : 0.f;
-      else g = (i == j) ? 1.f : 0.f;
+      const int j = 32 * J + jj;
+      gv[jj] = (i < c && j < c && i >= j) ? p.G[i + (long)j * p.ldg] : 0.f;
+    }
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = 32 * J + jj;
+      float g = gv[jj];
+      if (!(i < c && j < c)) g = (i == j) ? 1.f : 0.f;
       T[jj * 32 + lane] = g;
       if (i == j && i < c) { dsum += g; dmax = fmaxf(dmax, g); }
     }
@@ -201,6 +217,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
   const float sh = (p.shift > 0.f) ? p.shift * trace : 0.f;
   const float tol = 4.0f * 1.1920929e-7f * (gmax + sh);
   __syncthreads();
+  CT_T(0);
 
   for (int J = 0; J < NB; ++J) {
     // (1) diagonal tile: one warp factors it (lane = row, register rows, shuffles; fully
@@ -241,6 +258,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
       if (dropped && lane == 0) s_drop = 1;
     }
     __syncthreads();
+    CT_T(1);
     // (2) L_IJ = G_IJ X_JJ^T for I > J (X_JJ^T(k, j) = X_JJ(j, k) -> col-major copy as B)
     for (int I = J + 1 + warp; I < NB; I += NW) {
       float* T = Lt + (size_t)ctix(I, J) * 1024;
@@ -257,6 +275,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
       for (int j = 0; j < 32; ++j) T[j * 32 + lane] = acc[j];
     }
     __syncthreads();
+    CT_T(2);
     // (3) trailing update G_IK -= L_IJ L_KJ^T for I >= K > J
     {
       const int n = NB - J - 1;
@@ -281,6 +300,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
       }
     }
     __syncthreads();
+    CT_T(3);
   }
   // ---- X = L^{-1}, right-looking by block rows K: the off-diagonal X tiles first hold
   // the accumulators A_IJ = -sum_{M<I} L_IM X_MJ (zero-initialised), then
@@ -309,6 +329,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
       for (int j = 0; j < 32; ++j) XK[lane * 32 + j] = acc[j];
     }
     __syncthreads();
+    CT_T(5);
     const int nI = NB - K - 1, nJ = K + 1;
     for (int t = warp; t < nI * nJ; t += NW) {         // (2)
       const int I = K + 1 + t / nJ, J = t % nJ;
@@ -325,22 +346,263 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
       for (int j = 0; j < 32; ++j) XI[lane * 32 + j] -= acc[j];
     }
     __syncthreads();
+    CT_T(6);
   }
   // ---- outputs: L and Linv, c x c col-major, zeros above the diagonal
   for (int t = warp; t < NB * NB; t += NW) {
     const int I = t % NB, J = t / NB;
     const int i = 32 * I + lane;
+    float lv[32], xv[32];   // all loads in flight before the stores
+    if (I >= J) {
+      const float* LT = Lt + (size_t)ctix(I, J) * 1024;
+      const float4* XT = reinterpret_cast<const float4*>(Xt + (size_t)ctix(I, J) * 1024 + lane * 32);
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) lv[jj] = LT[jj * 32 + lane];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 x4 = XT[q];
+        xv[4 * q] = x4.x; xv[4 * q + 1] = x4.y; xv[4 * q + 2] = x4.z; xv[4 * q + 3] = x4.w;
+      }
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) { lv[jj] = 0.f; xv[jj] = 0.f; }
+    }
+    if (i < c) {
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int j = 32 * J + jj;
+        if (j >= c) break;
+        const bool up = (I == J && lane < jj);
+        p.L[i + (long)j * c] = up ? 0.f : lv[jj];
+        p.Linv[i + (long)j * c] = up ? 0.f : xv[jj];
+      }
+    }
+  }
+  if (tid == 0 && s_drop && p.status) atomicOr(p.status, ST_CHOL_DROP);
+  CT_T(7);
+}
+
+// ---- c <= 256: every tile resident in shared memory -------------------------------------
+// Same right-looking factorisation as chol_tiled_kernel with the NB(NB+1)/2 L tiles
+// (col-major) in shared memory and products read straight from it (no staging).  The
+// inverse is formed IN PLACE, right-looking by block rows K:
+//   (1) X_KJ = X_KK A_KJ            for J < K       (A_KJ row-major accumulator at (K, J))
+//   (2a) A_IJ -= L_IK X_KJ          for I > K, J < K
+//   (2b) A_IK  = -L_IK X_KK         for I > K        (position (I, K): L_IK -> accumulator)
+// so a position holds L_IJ (col-major) until step K = J, then the row-major accumulator /
+// X_IJ.  X_KK = L_KK^{-1} comes from the diagonal step (col-major copy in Xd).
+constexpr int CS_MAXNB = 8;
+inline size_t chol_smem_bytes(int c) {
+  const size_t NB = (size_t)(c + 31) / 32;
+  return sizeof(float) * (NB * (NB + 1) / 2 * 1024 + 2 * NB * 1024 + 2 * 1024);
+}
+
+__global__ void __launch_bounds__(CT_THREADS, 1) chol_smem_kernel(const __grid_constant__ CholTiledBatch b) {
+  const CholTiledProb& p = b.p[blockIdx.x];
+  const int c = p.c, NB = (c + 31) >> 5;
+  const int ntile = NB * (NB + 1) / 2;
+  extern __shared__ __align__(16) float cssm[];
+  float* Lt = cssm;                              // ntile tiles
+  float* Xd = Lt + (size_t)ntile * 1024;         // NB col-major X_KK
+  float* Xr = Xd + (size_t)NB * 1024;            // NB row-major X_KK
+  float* sD = Xr + (size_t)NB * 1024;            // warp-0 scratch: columns of L_JJ
+  float* sR = sD + 1024;                         //                 row-major L_JJ
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = CT_THREADS / 32;
+  __shared__ float red[32];
+  __shared__ int s_drop;
+  auto tile = [&](int I, int J) { return Lt + (size_t)ctix(I, J) * 1024; };
+
+  // ---- load G (lower) into tiles, identity padding; trace and max diagonal
+  float dsum = 0.f, dmax = 0.f;
+  for (int t = warp; t < ntile; t += NW) {
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    const int J = t - I * (I + 1) / 2;
+    float* T = Lt + (size_t)t * 1024;
+    float gv[32];
+    const int i = 32 * I + lane;
+#pragma unroll
     for (int jj = 0; jj < 32; ++jj) {
       const int j = 32 * J + jj;
-      if (i >= c || j >= c) continue;
-      float lv = 0.f, xv = 0.f;
-      if (I >= J) {
-        lv = Lt[(size_t)ctix(I, J) * 1024 + jj * 32 + lane];
-        xv = Xt[(size_t)ctix(I, J) * 1024 + lane * 32 + jj];
-        if (I == J && lane < jj) { lv = 0.f; xv = 0.f; }
+      gv[jj] = (i < c && j < c && i >= j) ? p.G[i + (long)j * p.ldg] : 0.f;
+    }
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = 32 * J + jj;
+      float g = gv[jj];
+      if (!(i < c && j < c)) g = (i == j) ? 1.f : 0.f;
+      T[jj * 32 + lane] = g;
+      if (i == j && i < c) { dsum += g; dmax = fmaxf(dmax, g); }
+    }
+  }
+  const float trace = block_sum(dsum, red);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if (lane == 0) red[warp] = dmax;
+  __syncthreads();
+  float gmax = 0.f;
+  for (int w = 0; w < NW; ++w) gmax = fmaxf(gmax, red[w]);
+  if (tid == 0) s_drop = 0;
+  const float sh = (p.shift > 0.f) ? p.shift * trace : 0.f;   // shifted CholeskyQR
+  const float tol = 4.0f * 1.1920929e-7f * (gmax + sh);
+  __syncthreads();
+
+  for (int J = 0; J < NB; ++J) {
+    // (1) diagonal tile on warp 0: factor (lane = row) and invert (lane = column)
+    if (warp == 0) {
+      float* T = tile(J, J);
+      float a[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) a[j] = T[j * 32 + lane];
+      const bool real = 32 * J + lane < c;
+      if (sh > 0.f && real) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) if (j == lane) a[j] += sh;
       }
-      p.L[i + (long)j * c] = lv;
-      p.Linv[i + (long)j * c] = xv;
+      int dropped = 0;
+      ct_factor<0>(a, sD, lane, c - 32 * J, tol, dropped);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) T[j * 32 + lane] = (lane >= j) ? a[j] : 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(sR + lane * 32)[q] =
+            make_float4(lane >= 4 * q ? a[4 * q] : 0.f, lane >= 4 * q + 1 ? a[4 * q + 1] : 0.f,
+                        lane >= 4 * q + 2 ? a[4 * q + 2] : 0.f, lane >= 4 * q + 3 ? a[4 * q + 3] : 0.f);
+      __syncwarp();
+      float x[32];
+      ct_inverse<0>(sR, x, lane);
+      float* XJc = Xd + (size_t)J * 1024;      // col-major: lane = column
+      float* XJr = Xr + (size_t)J * 1024;      // row-major
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(XJc + lane * 32)[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) XJr[i * 32 + lane] = x[i];
+      if (dropped && lane == 0) s_drop = 1;
+    }
+    __syncthreads();
+    // (2) L_IJ = G_IJ X_JJ^T for I > J, in place (B(j, k) = X_JJ(j, k): col-major X_JJ)
+    for (int I = J + 1 + warp; I < NB; I += NW) {
+      float* T = tile(I, J);
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+      tile_abt<false>(acc, T, Xd + (size_t)J * 1024, lane);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) T[j * 32 + lane] = acc[j];
+    }
+    __syncthreads();
+    // (3) trailing update G_IK -= L_IJ L_KJ^T for I >= K > J
+    {
+      const int n = NB - J - 1;
+      const int npairs = n * (n + 1) / 2;
+      for (int t = warp; t < npairs; t += NW) {
+        int a = 0;
+        while ((a + 1) * (a + 2) / 2 <= t) ++a;
+        const int I = J + 1 + a, K = J + 1 + (t - a * (a + 1) / 2);
+        float* T = tile(I, K);
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = T[j * 32 + lane];
+        tile_abt<true>(acc, tile(I, J), tile(K, J), lane);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) T[j * 32 + lane] = acc[j];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- L out (c x c col-major, zeros above the diagonal)
+  for (int t = warp; t < NB * NB; t += NW) {
+    const int I = t % NB, J = t / NB;
+    const int i = 32 * I + lane;
+    if (i >= c) continue;
+    const float* T = I >= J ? tile(I, J) : nullptr;
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = 32 * J + jj;
+      if (j >= c) break;
+      p.L[i + (long)j * c] = (T && !(I == J && lane < jj)) ? T[jj * 32 + lane] : 0.f;
+    }
+  }
+  __syncthreads();
+  // ---- in-place inverse
+  for (int K = 0; K < NB; ++K) {
+    for (int J = warp; J < K; J += NW) {                 // (1) X_KJ = X_KK A_KJ
+      float* T = tile(K, J);
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+      tile_ab(acc, Xd + (size_t)K * 1024, T, lane);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(T + lane * 32)[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+    }
+    __syncthreads();
+    const int nI = NB - K - 1;
+    for (int t = warp; t < nI * K; t += NW) {             // (2a) A_IJ -= L_IK X_KJ, J < K
+      const int I = K + 1 + t / K, J = t % K;
+      float* T = tile(I, J);
+      float acc[32];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 v4 = reinterpret_cast<const float4*>(T + lane * 32)[q];
+        acc[4 * q] = v4.x; acc[4 * q + 1] = v4.y; acc[4 * q + 2] = v4.z; acc[4 * q + 3] = v4.w;
+      }
+      float prod[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) prod[j] = 0.f;
+      tile_ab(prod, tile(I, K), tile(K, J), lane);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(T + lane * 32)[q] =
+            make_float4(acc[4 * q] - prod[4 * q], acc[4 * q + 1] - prod[4 * q + 1],
+                        acc[4 * q + 2] - prod[4 * q + 2], acc[4 * q + 3] - prod[4 * q + 3]);
+    }
+    __syncthreads();
+    for (int I = K + 1 + warp; I < NB; I += NW) {          // (2b) A_IK = -L_IK X_KK
+      float* T = tile(I, K);
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+      tile_ab(acc, T, Xr + (size_t)K * 1024, lane);      // L_IK X_KK (X_KK row-major)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = -acc[j];
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(T + lane * 32)[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+    }
+    __syncthreads();
+  }
+  // ---- Linv out: off-diagonal X tiles row-major in place, diagonal X_KK col-major in Xd
+  for (int t = warp; t < NB * NB; t += NW) {
+    const int I = t % NB, J = t / NB;
+    const int i = 32 * I + lane;
+    float xv[32];
+    if (I > J) {
+      const float4* X4 = reinterpret_cast<const float4*>(tile(I, J) + lane * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 x4 = X4[q];
+        xv[4 * q] = x4.x; xv[4 * q + 1] = x4.y; xv[4 * q + 2] = x4.z; xv[4 * q + 3] = x4.w;
+      }
+    } else if (I == J) {
+      const float* XJc = Xd + (size_t)J * 1024;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) xv[jj] = (lane >= jj) ? XJc[jj * 32 + lane] : 0.f;
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) xv[jj] = 0.f;
+    }
+    if (i < c) {
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int j = 32 * J + jj;
+        if (j >= c) break;
+        p.Linv[i + (long)j * c] = xv[jj];
+      }
     }
   }
   if (tid == 0 && s_drop && p.status) atomicOr(p.status, ST_CHOL_DROP);
