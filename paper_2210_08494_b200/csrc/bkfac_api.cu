@@ -270,6 +270,17 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
     }
   const long nsm = ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM;
   const long target = tc ? nsm : 2L * nsm;
+  // tcgen05: balance the stage's K-chunk work over the persistent CTAs -- every work item
+  // (tile x split) gets at most `quota` chunks, so one long-K problem no longer sets the
+  // critical path of a stage of mixed sizes (e.g. R^T R over n = 577 ... 4609)
+  long chunk_work = 0;
+  if (tc)
+    for (int v = 0; v < 4; ++v)
+      for (auto& p : s.probs[v]) {
+        const long nt = p.sym ? (long)p.tiles_m * (p.tiles_m + 1) / 2 : (long)p.tiles_m * p.tiles_n;
+        chunk_work += nt * (ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK));
+      }
+  const long quota = std::max<long>(2 * TC_PROMO, (chunk_work + nsm - 1) / nsm);
   for (int v = 0; v < 4; ++v)
     for (size_t i = 0; i < s.probs[v].size(); ++i) {
       GemmProb& p = s.probs[v][i];
@@ -278,9 +289,9 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       if (tc) {
         const int nc = ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK);
         int splits = 1;
-        if (nc >= 8 && base_tiles > 0 && base_tiles < target && p.ws != nullptr && !p.sym) {
-          splits = (int)std::min<long>(kSplitMax, (target + base_tiles - 1) / base_tiles);
-          splits = std::min(splits, nc / 4);
+        if (nc >= 2 * TC_PROMO && nc > quota && p.ws != nullptr && !p.sym) {
+          splits = (int)std::min<long>(kSplitMax, (nc + quota - 1) / quota);
+          splits = std::min(splits, nc / TC_PROMO);
           splits = (int)std::min<long>(splits, cap);
           splits = std::max(splits, 1);
         }
