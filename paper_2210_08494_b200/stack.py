@@ -88,10 +88,14 @@ class BKFACStack:
         self.cur = [0] * len(self.my_factors)
         self.k = 0
         self.n_overwrites = 0
-        self.S: Dict[int, "torch.Tensor"] = {}
+        self._graphs = {}
+        # preconditioned gradients, two sets by step parity: step k's S stays valid while
+        # step k+1 runs (a caller can read it back concurrently)
+        self.S2 = [{}, {}]
         for li in self.my_layers:
             dG, dA, _, _ = self.layers[li]
-            self.S[li] = torch.empty((dG, dA), dtype=torch.float32, device=dev)
+            for par in range(2):
+                self.S2[par][li] = torch.empty((dG, dA), dtype=torch.float32, device=dev)
 
     # ---------------------------------------------------------------------------------
     def state(self, g: int):
@@ -111,9 +115,40 @@ class BKFACStack:
         self.D[i][self.cur[i]].zero_()
 
     def step(self, M: Dict[int, "torch.Tensor"], J: Optional[Dict[int, "torch.Tensor"]] = None,
-             stream=None) -> Dict[int, "torch.Tensor"]:
+             stream=None, graph: bool = False) -> Dict[int, "torch.Tensor"]:
         """One step over the owned factors (M keyed by global factor index, each (c, n))
-        and owned layers (J keyed by global layer index, each (d_G, d_A))."""
+        and owned layers (J keyed by global layer index, each (d_G, d_A)).
+
+        graph=True replays a CUDA graph of the step's launches (captured on first use per
+        U/D ping-pong parity and input buffers -- the inputs must be the same tensors on
+        every replay, refilled in place).  The initial step and RSVD-overwrite steps always
+        run eagerly; the library's per-stage profiling must be off while graphs are used."""
+        torch = self.torch
+        if graph and self.k > 0 and not (self.rsvd_every and self.k % self.rsvd_every == 0):
+            key = (self.cur[0] if self.cur else 0,
+                   tuple(M[g].data_ptr() for g in self.my_factors),
+                   tuple(J[li].data_ptr() for li in self.my_layers) if J is not None else None)
+            main = stream if stream is not None else torch.cuda.current_stream(self.device)
+            hit = self._graphs.get(key)
+            if hit is None:
+                g = torch.cuda.CUDAGraph()
+                main.synchronize()
+                with torch.cuda.graph(g):
+                    out = self._step(M, J, torch.cuda.current_stream(self.device))
+                self._graphs[key] = (g, out)
+                with torch.cuda.stream(main):
+                    g.replay()          # capture only recorded the launches: run them
+                return out
+            g, out = hit
+            with torch.cuda.stream(main):
+                g.replay()
+            self.k += 1
+            for i in range(len(self.my_factors)):
+                self.cur[i] = 1 - self.cur[i]
+            return out
+        return self._step(M, J, stream)
+
+    def _step(self, M, J, stream):
         k = self.k
         torch = self.torch
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -158,10 +193,10 @@ class BKFACStack:
                 UG, DG = self.state(g)
                 UA, DA = self.state(a)
                 items.append(dict(layer=lj, U_G=UG, D_G=DG, lambda_G=self.lam, U_A=UA, D_A=DA,
-                                  lambda_A=self.lam, J=J[li], S=self.S[li],
+                                  lambda_A=self.lam, J=J[li], S=self.S2[k & 1][li],
                                   flags=self.precond_flags))
             self.ctx.bkfac_precondition(items, main)
-            out = {li: self.S[li] for li in self.my_layers}
+            out = {li: self.S2[k & 1][li] for li in self.my_layers}
         self.k += 1
         return out
 

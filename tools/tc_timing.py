@@ -7,7 +7,10 @@ lib = binding.load()
 lib.bkfac_debug_tc.argtypes = [ctypes.c_void_p, ctypes.c_int]
 for (ta, tb, M, N, K, beta) in [(False, False, 8192, 8192, 8192, 0.0), (False, True, 4097, 16384, 1024, 0.0),
                                 (False, True, 4609, 4609, 256, 0.0), (False, True, 4609, 4609, 256, 0.95),
-                                (False, True, 4608, 4608, 256, 0.95)]:
+                                (False, True, 4608, 4608, 256, 0.95),
+                                (False, False, 4609, 220, 476, 0.0), (False, False, 4609, 256, 220, 0.0),
+                                (True, False, 256, 256, 4609, 0.0), (False, False, 128, 128, 32, 0.0),
+                                (False, False, 128, 128, 256, 0.0), (False, False, 4096, 128, 32, 0.0)]:
     A = torch.randn((M, K) if ta else (K, M), device="cuda")
     B = torch.randn((K, N) if tb else (N, K), device="cuda")
     C = torch.zeros((N, M), device="cuda")
