@@ -206,8 +206,12 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
     b.nprob = (int)n;
     int tiles = 0;
     bool any_split = false;
+    int max_chunks = 0;   // K chunks of the longest work item (short K: epilogue-bound)
     for (size_t i = 0; i < n; ++i) {
       GemmProb p = v[i0 + i];
+      max_chunks = std::max(max_chunks, p.splits > 1 ? p.kchunk
+                                                     : ceil_div(std::max(p.k1, 0), TC_BK) +
+                                                           ceil_div(std::max(p.K - p.k1, 0), TC_BK));
       p.tile_start = tiles;
       tiles += (p.sym ? p.tiles_m * (p.tiles_m + 1) / 2 : p.tiles_m * p.tiles_n) * p.splits;
       any_split |= p.splits > 1;
@@ -217,7 +221,7 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
     if (tiles > 0) {
       if (tc) {
         const int grid = std::min(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM);
-        tc_launch<TA, TB>(b, grid, st);
+        tc_launch<TA, TB>(b, grid, st, max_chunks <= TC_SHORT_K_CHUNKS);
       } else {
         gemm_simt_kernel<TA, TB><<<tiles, 256, 0, st>>>(b);
       }

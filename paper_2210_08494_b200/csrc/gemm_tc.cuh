@@ -55,7 +55,11 @@ namespace bkfac {
 
 constexpr int TC_BM = 128;            // UMMA M (TMEM lanes)
 constexpr int TC_BK = 32;             // one 128-byte swizzle line of fp32
-constexpr int TC_EPI_WARPS = 4;
+// Epilogue warps EPI: 4 (warps 0-3, all columns of their TMEM lane quarter) or 8 (warps 0-3
+// plus 4 more after the loaders; quarter = warp % 4, each of a quarter's two warps takes half
+// the columns).  8 puts twice the C0/C traffic in flight per SM -- for stages whose K is
+// short (<= 8 chunks), where the epilogue, not the MMA, sets the pace (the EA accumulate,
+// the residual) -- at the price of 72 instead of 80 registers per thread.
 constexpr int TC_MMA_WARP = 4;
 #ifndef BKFAC_TC_PROMO
 #define BKFAC_TC_PROMO 4
@@ -74,10 +78,11 @@ constexpr int TC_MMA_WARP = 4;
 constexpr int TC_PROMO = BKFAC_TC_PROMO;   // K chunks accumulated in TMEM before promotion
 
 // NLW loader warps, each keeping DEPTH chunks of loads in flight ahead of its stores.
-template <int BN, int NLW = 16, int DEPTH = 2>
+template <int BN, int NLW = 16, int DEPTH = 2, int EPI = 4>
 struct TcCfg {
   static constexpr int LOAD_WARPS = NLW;
-  static constexpr int THREADS = (TC_EPI_WARPS + 1 + NLW) * 32;
+  static constexpr int EPI_WARPS = EPI;
+  static constexpr int THREADS = (EPI + 1 + NLW) * 32;
   static constexpr int A_BYTES = TC_BM * TC_BK * 4;          // one half (hi or lo)
   static constexpr int B_BYTES = BN * TC_BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
@@ -92,7 +97,7 @@ struct TcCfg {
   // + per-epilogue-warp 16 x 34 staging for the transposed (mirror) stores of symmetric tiles
   static constexpr int EPI_STAGE_FLOATS = 16 * 34;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
-                                    TC_EPI_WARPS * EPI_STAGE_FLOATS * 4;
+                                    EPI * EPI_STAGE_FLOATS * 4;
 };
 
 // ----------------------------------------------------------------------- PTX helpers
@@ -276,15 +281,19 @@ __device__ unsigned long long g_tc_dbg[148 * 8];   // tuning builds: per-CTA MMA
 #endif
 // Epilogue warps 0-3 (thread = tile row = TMEM lane): promote each K-block accumulator
 // into the running sum (TMEM), then alpha/beta and coalesced stores of the tile.
-template <int BN>
+template <int BN, int EPI>
 BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int lane,
                            uint32_t tfull0, uint32_t tfull1, uint32_t tempty0, uint32_t tempty1,
                            float* stage) {
   auto tfull_bar = [&](int a) { return a ? tfull1 : tfull0; };
   auto tempty_bar = [&](int a) { return a ? tempty1 : tempty0; };
-    const int row = warp * 32 + lane;                         // TMEM lane = tile row
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const int quarter = warp & 3;                             // TMEM lanes this warp may access
+    const int row = quarter * 32 + lane;                      // TMEM lane = tile row
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const uint32_t run = tmem_base + lane_off + 2 * BN;       // running-sum columns
+    // column groups of this warp: all, or one half when two warps share the quarter
+    constexpr int NG = BN / 16, GPW = NG * 4 / EPI;
+    const int g_beg = (warp < 4 ? 0 : 1) * GPW;
     int kb = 0;
     for (int t = blockIdx.x; t < b.total_tiles; t += gridDim.x) {
       const TcTile x = tc_tile<BN>(b, t);
@@ -301,7 +310,7 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
         tc_fence_after();
         const uint32_t src = tmem_base + lane_off + (uint32_t)(buf * BN);
 #pragma unroll 1
-        for (int g = 0; g < BN / 16; ++g) {
+        for (int g = g_beg; g < g_beg + GPW; ++g) {
           if (last && x.n0 + g * 16 >= p.N) break;      // warp-uniform
 #ifdef BKFAC_TC_DEBUG_NOEPI
           if (!last) break;                             // tuning only: skip promotion
@@ -355,7 +364,7 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
 #pragma unroll 4
               for (int q = 0; q < 16; ++q) {
                 const int jj = lane & 15, rr = 2 * q + (lane >> 4);
-                const int ir = x.m0 + warp * 32 + rr, jc = j0 + jj;
+                const int ir = x.m0 + quarter * 32 + rr, jc = j0 + jj;
                 if (ir < p.M && jc < p.N) p.C[jc + (long)ir * p.ldc] = stage[jj * 34 + rr];
               }
               __syncwarp();
@@ -369,7 +378,7 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
       }
       if (p.status && __any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(p.status, ST_NONFINITE);
       if (nblk == 0 && i < p.M) {     // empty K range (split beyond K or K = 0)
-        for (int j = x.n0; j < min(p.N, x.n0 + BN); ++j) {
+        for (int j = x.n0 + 16 * g_beg; j < min(p.N, x.n0 + 16 * (g_beg + GPW)); ++j) {
           if (w) {
             w[i + (long)j * p.M] = 0.f;
           } else {
@@ -383,10 +392,10 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
   }
 
 // ----------------------------------------------------------------------- kernel
-template <bool TA, bool TB, int BN, int NLW, int DEPTH>
-__global__ void __launch_bounds__(TcCfg<BN, NLW, DEPTH>::THREADS, 1)
+template <bool TA, bool TB, int BN, int NLW, int DEPTH, int EPI>
+__global__ void __launch_bounds__(TcCfg<BN, NLW, DEPTH, EPI>::THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
-  using Cfg = TcCfg<BN, NLW, DEPTH>;
+  using Cfg = TcCfg<BN, NLW, DEPTH, EPI>;
   constexpr int TC_LOAD_WARPS = NLW;
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
@@ -409,7 +418,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(tfull_bar(a), 1);
-        mbar_init(tempty_bar(a), TC_EPI_WARPS);
+        mbar_init(tempty_bar(a), EPI);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -494,7 +503,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
       }
     }
     __syncwarp();
-  } else if (warp > TC_MMA_WARP) {
+  } else if (warp > TC_MMA_WARP && warp <= TC_MMA_WARP + NLW) {
     // ------------------------------------------------------------- loaders
     const int lw = warp - TC_MMA_WARP - 1;
     int stage = 0; uint32_t phase = 0;
@@ -631,9 +640,10 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     }
   } else {
     // ------------------------------------------------------------- epilogue
+    const int e = warp < 4 ? warp : 4 + (warp - (TC_MMA_WARP + 1 + NLW));   // epilogue warp index
     float* stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256) +
-                   warp * Cfg::EPI_STAGE_FLOATS;
-    tc_epilogue<BN>(b, tmem_base, warp, lane, tfull_bar(0), tfull_bar(1), tempty_bar(0), tempty_bar(1),
+                   e * Cfg::EPI_STAGE_FLOATS;
+    tc_epilogue<BN, EPI>(b, tmem_base, warp, lane, tfull_bar(0), tfull_bar(1), tempty_bar(0), tempty_bar(1),
                     stage);
   }
   tc_fence_before();
@@ -648,26 +658,36 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 // Launch configuration of the hot-path GEMM (BN = 128 tiles, 16 loader warps, two
 // chunks of loads in flight per loader).
 constexpr int TC_BN = 128, TC_NLW = BKFAC_TC_NLW, TC_DEPTH = BKFAC_TC_DEPTH;
-using TcMain = TcCfg<TC_BN, TC_NLW, TC_DEPTH>;
+using TcMain = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 4>;
+using TcShortK = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 8>;
+constexpr int TC_SHORT_K_CHUNKS = 8;   // stages with every K <= 8 chunks use 8 epilogue warps
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, int EPI>
 inline bool tc_set_attr() {
-  return cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, TcMain::SMEM_BYTES) == cudaSuccess;
+  using Cfg = TcCfg<TC_BN, TC_NLW, TC_DEPTH, EPI>;
+  return cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, EPI>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) == cudaSuccess;
 }
 
 inline bool tc_init_attributes() {
   bool ok = true;
-  ok &= tc_set_attr<false, false>();
-  ok &= tc_set_attr<false, true>();
-  ok &= tc_set_attr<true, false>();
-  ok &= tc_set_attr<true, true>();
+  ok &= tc_set_attr<false, false, 4>();
+  ok &= tc_set_attr<false, true, 4>();
+  ok &= tc_set_attr<true, false, 4>();
+  ok &= tc_set_attr<true, true, 4>();
+  ok &= tc_set_attr<false, false, 8>();
+  ok &= tc_set_attr<false, true, 8>();
+  ok &= tc_set_attr<true, false, 8>();
+  ok &= tc_set_attr<true, true, 8>();
   return ok;
 }
 
 template <bool TA, bool TB>
-inline void tc_launch(const GemmBatch& b, int grid, cudaStream_t st) {
-  gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH><<<grid, TcMain::THREADS, TcMain::SMEM_BYTES, st>>>(b);
+inline void tc_launch(const GemmBatch& b, int grid, cudaStream_t st, bool short_k) {
+  if (short_k)
+    gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 8><<<grid, TcShortK::THREADS, TcShortK::SMEM_BYTES, st>>>(b);
+  else
+    gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 4><<<grid, TcMain::THREADS, TcMain::SMEM_BYTES, st>>>(b);
 }
 
 }  // namespace bkfac
