@@ -49,6 +49,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     ap.add_argument("--pool", type=int, default=2, help="distinct input batches kept on device")
+    ap.add_argument("--full-rank", action="store_true",
+                    help="NEXT-f1: keep all r + c eigenpairs per step and precondition with them")
     ap.add_argument("--no-graphs", action="store_true",
                     help="launch every step eagerly instead of replaying CUDA graphs")
     return ap.parse_args()
@@ -332,7 +334,8 @@ def run_reference(args, rank, world):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * t_total / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "factors": n_f, "layers": n_l,
+            "config": {"workload": cfg.name + ("+f1_full_rank" if args.full_rank else ""),
+                       "factors": n_f, "layers": n_l,
                        "sample": "one layer (2 factor updates + preconditioning) per step"},
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores,
                              "kind": "oracle", "sample": sample},
@@ -353,7 +356,7 @@ def run_ours(args, rank, world, local_rank):
     layers = [(l.d_G, l.d_A, l.g_index, l.a_index) for l in cfg.layers]
     stack = BKFACStack(factors, layers, cfg.rho, cfg.lam, rsvd_every=cfg.rsvd_every,
                        oversample=cfg.oversample, power_iters=cfg.power_iters,
-                       device=local_rank, rank=rank, world=world)
+                       device=local_rank, rank=rank, world=world, full_rank=args.full_rank)
     gather = SlotGather(layers, stack.owned_layers_all, rank, device) if world > 1 and layers else None
     M_pool, J_pool = device_inputs(cfg, stack.my_factors, stack.my_layers, args.pool, device)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device)
@@ -447,7 +450,8 @@ def run_ours(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "weak" if not layers else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "layers_per_s": round(layers_per_s, 3),
-            "config": {"workload": cfg.name, "factors": n_f, "layers": n_l,
+            "config": {"workload": cfg.name + ("+f1_full_rank" if args.full_rank else ""),
+                       "factors": n_f, "layers": n_l,
                        "n_BS": cfg.factors[0].c, "rho": cfg.rho, "lambda": cfg.lam,
                        "rsvd_every": cfg.rsvd_every, "parallelism": f"layer-shard x{world}",
                        "l2": "flushed between timed steps (512 MiB write)",

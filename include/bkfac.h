@@ -61,6 +61,15 @@ typedef enum {
 
 /* bkfac_factor_desc.flags */
 #define BKFAC_FACTOR_DENSE_EA 1   /* the factor may be RSVD-overwritten: reserve RSVD workspace */
+/* Paper-faithful output rank (NEXT-f1, Alg 4 :540-548, :655-656): the
+ * factor's basis has r_out = min(n, r + c_max) columns.  A Brand update with batch c writes
+ * the min(n, r + c) eigenpairs of M~_B = alpha U_r D_r U_r^T + beta M M^T -- its whole
+ * spectrum, i.e. the rank-(r + c) matrix the paper preconditions with -- into U_out
+ * (n x r_out) and D_out (r_out), zero-filling columns / entries beyond that; it reads
+ * U_in / D_in through their first r columns / entries (the truncation to r that precedes
+ * every Brand step, Alg 4 lines 2-4).  Layers preconditioned with such factors declare
+ * r_G / r_A = r_out; the zero columns contribute nothing. */
+#define BKFAC_FACTOR_FULL_RANK 2
 
 /* bkfac_brand_args.flags */
 #define BKFAC_BRAND_NO_REORTH 1   /* skip the second (CGS2) projection against U           */

@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbkfac.so")
 
 BKFAC_FACTOR_DENSE_EA = 1
+BKFAC_FACTOR_FULL_RANK = 2
 BKFAC_BRAND_NO_REORTH = 1
 BKFAC_BRAND_NO_REFRESH = 2
 BKFAC_PRECOND_CONTINUATION = 1

@@ -68,6 +68,7 @@ struct FactorPlan {
   bkfac_factor_desc d;
   bool dense = false;  // r + c_max >= n: form the n x n sum densely (a6')
   int m = 0;           // core order (r + c_max, or n on the dense path)
+  int rout = 0;        // output columns: r, or min(n, r + c_max) with BKFAC_FACTOR_FULL_RANK
   // Brand path
   size_t W, P2, R, Qb, G, L1, L1i, L2, L2i, cscr, ws;
   size_t ws_elems = 0;
@@ -624,10 +625,13 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
     const int n = fp.d.n, r = fp.d.r, cm = fp.d.c_max;
     if (n <= 0 || r <= 0 || r > n || cm <= 0) { delete c; return BKFAC_ERR_DIM; }
     fp.dense = (r + cm >= n);
+    const bool full = (fp.d.flags & BKFAC_FACTOR_FULL_RANK) != 0;
+    fp.rout = full ? std::min(n, r + cm) : r;
+    const int ro = fp.rout;
     if (fp.dense) {
       fp.m = n;
       fp.T = a.take(sizeof(float) * (size_t)n * r);
-      plan_eig(a, fp.eig, n, r);
+      plan_eig(a, fp.eig, n, ro);
     } else {
       const int m = r + cm;
       fp.m = m;
@@ -640,11 +644,11 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
       fp.cscr = a.take(sizeof(float) * chol_tiled_scratch_floats(cm));
       fp.ws_elems = (long)kSplitMax * std::max(r, cm) * (long)cm;
       fp.ws = a.take(sizeof(float) * fp.ws_elems);
-      plan_eig(a, fp.eig, m, r);
+      plan_eig(a, fp.eig, m, ro);
     }
-    fp.Urot = a.take(sizeof(float) * (size_t)n * r);
-    fp.Gref = a.take(sizeof(float) * (size_t)r * r);
-    fp.wsr_elems = (long)kSplitMax * r * (long)r;
+    fp.Urot = a.take(sizeof(float) * (size_t)n * ro);
+    fp.Gref = a.take(sizeof(float) * (size_t)ro * ro);
+    fp.wsr_elems = (long)kSplitMax * ro * (long)ro;
     fp.wsr = a.take(sizeof(float) * fp.wsr_elems);
     if (fp.d.flags & BKFAC_FACTOR_DENSE_EA) {
       fp.rsvd = true;
@@ -826,7 +830,27 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
   for (int i = 0; i < count; ++i) (ctx->f[args[i].factor].dense ? dense : brand).push_back(i);
 
   auto run = [&](const char* tag) -> bkfac_status { return run_gemms(ctx, gs, st, tag); };
+  // output eigenpairs of this call: r, or (BKFAC_FACTOR_FULL_RANK) all min(n, r + c)
+  auto rout_of = [&](const bkfac_brand_args& a) {
+    const auto& fp = ctx->f[a.factor];
+    return (fp.d.flags & BKFAC_FACTOR_FULL_RANK) ? std::min(fp.d.n, fp.d.r + a.c) : fp.d.r;
+  };
 #define STAGE(x) do { if ((rs = (x)) != BKFAC_OK) goto done; } while (0)
+
+  // full-rank factors with c < c_max: zero the output columns / entries beyond r + c
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    const auto& fp = ctx->f[a.factor];
+    const int ro = rout_of(a);
+    if (ro < fp.rout) {
+      if (!cuda_ok(cudaMemsetAsync(a.U_out + (size_t)fp.d.n * ro, 0,
+                                   sizeof(float) * (size_t)fp.d.n * (fp.rout - ro), st)) ||
+          !cuda_ok(cudaMemsetAsync(a.D_out + ro, 0, sizeof(float) * (fp.rout - ro), st))) {
+        rs = BKFAC_ERR_CUDA;
+        goto done;
+      }
+    }
+  }
 
   // ---------------- dense path (r + c >= n): K = alpha U diag(D) U^T + beta M M^T
   if (!dense.empty()) {
@@ -873,7 +897,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     for (int i : dense) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
-      eg.push_back(eig_prob(ctx, fp.eig, fp.d.n, fp.d.r, at<float>(ctx, fp.Urot), fp.d.n, a.D_out,
+      eg.push_back(eig_prob(ctx, fp.eig, fp.d.n, rout_of(a), at<float>(ctx, fp.Urot), fp.d.n, a.D_out,
                             status_ptr(ctx, a.factor)));
     }
   }
@@ -990,7 +1014,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
       const int mm = fp.d.r + a.c;
-      eg.push_back(eig_prob(ctx, fp.eig, mm, fp.d.r, at<float>(ctx, fp.eig.V), mm, a.D_out,
+      eg.push_back(eig_prob(ctx, fp.eig, mm, rout_of(a), at<float>(ctx, fp.eig.V), mm, a.D_out,
                             status_ptr(ctx, a.factor)));
     }
   }
@@ -999,9 +1023,9 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
   for (int i : brand) {
     const auto& a = args[i];
     const auto& fp = ctx->f[a.factor];
-    const int n = fp.d.n, r = fp.d.r, mm = r + a.c;
+    const int n = fp.d.n, r = fp.d.r, mm = r + a.c, ro = rout_of(a);
     const float* V = at<float>(ctx, fp.eig.V);
-    GemmProb p = gp(a.U_in, n, V, mm, at<float>(ctx, fp.Urot), n, n, r, mm, 1.f);
+    GemmProb p = gp(a.U_in, n, V, mm, at<float>(ctx, fp.Urot), n, n, ro, mm, 1.f);
     p.A2 = at<float>(ctx, fp.R); p.lda2 = n;
     p.B2 = V + r; p.ldb2 = mm;
     p.k1 = r;
@@ -1016,7 +1040,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const auto& a = args[i];
     if (a.flags & BKFAC_BRAND_NO_REFRESH) continue;
     const auto& fp = ctx->f[a.factor];
-    const int n = fp.d.n, r = fp.d.r;
+    const int n = fp.d.n, r = rout_of(a);
     const float* Ur = at<float>(ctx, fp.Urot);
     GemmProb p = gp(Ur, n, Ur, n, at<float>(ctx, fp.Gref), r, r, r, n, 1.f);
     gemm_ws(p, at<float>(ctx, fp.wsr));
@@ -1026,7 +1050,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
     const auto& fp = ctx->f[a.factor];
-    const int n = fp.d.n, r = fp.d.r;
+    const int n = fp.d.n, r = rout_of(a);
     const float* Ur = at<float>(ctx, fp.Urot);
     if (a.flags & BKFAC_BRAND_NO_REFRESH) {
       EwProb e{};

@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
 // gaps are <= 1e-7 * ||T|| (beyond that, three inverse iterations from shifts accurate to
 // 1e-10 * span separate the eigenvectors to ~1e-9).  Each warp orthonormalises one
 // cluster by modified Gram-Schmidt.
+constexpr int CL_BIG = 32;   // clusters longer than this are orthonormalised by the whole CTA
 __global__ void __launch_bounds__(1024) cluster_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   const int m = p.m, r = p.r;
@@ -354,8 +355,10 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const __grid_constant__ E
   }
   __syncthreads();
   double* Y = p.Y;
+  // small clusters: one warp each, modified Gram-Schmidt in place
   for (int cl = warp; cl < s_n; cl += 32) {
     const int st = s_start[cl], len = s_len[cl];
+    if (len > CL_BIG) continue;
     for (int t = st; t < st + len; ++t) {
       for (int s = st; s < t; ++s) {
         double dot = 0.0;
@@ -371,6 +374,52 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const __grid_constant__ E
     }
   }
   __syncthreads();
+  // large clusters (near-null spaces of rank-deficient updates: hundreds of equal
+  // eigenvalues): the whole CTA, one cluster at a time, classical Gram-Schmidt applied twice
+  // per vector (CGS2; the projections onto all previous vectors of the cluster are
+  // parallel), on a transposed copy in the free inverse-iteration scratch (vector t
+  // contiguous: coalesced)
+  __shared__ double s_dot[1024];
+  double* Yt = p.scr;
+  for (int cl = 0; cl < s_n; ++cl) {
+    const int st = s_start[cl], len = s_len[cl];
+    if (len <= CL_BIG) continue;
+    for (int e = tid; e < len * m; e += blockDim.x) {
+      const int t = e / m, i = e % m;
+      Yt[e] = Y[(long)i * r + st + t];
+    }
+    __syncthreads();
+    for (int t = 0; t < len; ++t) {
+      double* yt = Yt + (long)t * m;
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int s2 = warp; s2 < t; s2 += 32) {
+          const double* ys = Yt + (long)s2 * m;
+          double dot = 0.0;
+          for (int i = lane; i < m; i += 32) dot = fma(ys[i], yt[i], dot);
+          dot = warp_sum_d(dot);
+          if (lane == 0) s_dot[s2] = dot;
+        }
+        __syncthreads();
+        for (int i = tid; i < m; i += blockDim.x) {
+          double acc = 0.0;
+          for (int s2 = 0; s2 < t; ++s2) acc = fma(s_dot[s2], Yt[(long)s2 * m + i], acc);
+          yt[i] -= acc;
+        }
+        __syncthreads();
+      }
+      double nrm = 0.0;
+      for (int i = tid; i < m; i += blockDim.x) nrm = fma(yt[i], yt[i], nrm);
+      nrm = block_sum_d(nrm, s_dot);
+      const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+      for (int i = tid; i < m; i += blockDim.x) yt[i] *= inv;
+      __syncthreads();
+    }
+    for (int e = tid; e < len * m; e += blockDim.x) {
+      const int t = e / m, i = e % m;
+      Y[(long)i * r + st + t] = Yt[e];
+    }
+    __syncthreads();
+  }
   // eigenvalues out (clamped at 0: the core is PSD) + finiteness check
   for (int j = tid; j < r; j += blockDim.x) {
     const double l = p.lam[j];

@@ -44,8 +44,13 @@ class BKFACStack:
                  layers: Sequence[Tuple[int, int, int, int]],
                  rho: float, lam: float, rsvd_every: int = 0, oversample: int = 10,
                  power_iters: int = 2, precond_flags: int = 0, brand_flags: int = 0,
-                 device: int = 0, rank: int = 0, world: int = 1, rsvd_seed: int = 20221015):
-        """factors: (n, r, c_max) per global factor; layers: (d_G, d_A, g_index, a_index)."""
+                 device: int = 0, rank: int = 0, world: int = 1, rsvd_seed: int = 20221015,
+                 full_rank: bool = False):
+        """factors: (n, r, c_max) per global factor; layers: (d_G, d_A, g_index, a_index).
+
+        full_rank=True is the paper's own preconditioner (NEXT-f1, PAPER.md:533-534,
+        :655-656): every Brand step keeps all min(n, r + c) eigenpairs of M~_B and the layers
+        are preconditioned with them; the next step truncates to r."""
         import torch
         self.torch = torch
         self.rho, self.lam = float(rho), float(lam)
@@ -68,13 +73,15 @@ class BKFACStack:
             owned_f.update(fo)
         self.my_factors = sorted(owned_f)
         self.local = {g: i for i, g in enumerate(self.my_factors)}
-        dense_flag = binding.BKFAC_FACTOR_DENSE_EA if rsvd_every > 0 else 0
-        fdesc = [(self.factors[g][0], self.factors[g][1], self.factors[g][2], dense_flag)
+        self.full_rank = full_rank
+        flags = (binding.BKFAC_FACTOR_DENSE_EA if rsvd_every > 0 else 0) | \
+                (binding.BKFAC_FACTOR_FULL_RANK if full_rank else 0)
+        fdesc = [(self.factors[g][0], self.factors[g][1], self.factors[g][2], flags)
                  for g in self.my_factors]
         ldesc = []
         for li in self.my_layers:
             dG, dA, g, a = self.layers[li]
-            ldesc.append((dG, dA, self.factors[g][1], self.factors[a][1]))
+            ldesc.append((dG, dA, self.rank_out(g), self.rank_out(a)))
         self.ctx = binding.Context(fdesc, ldesc, device=device)
         dev = f"cuda:{device}"
         self.U = []
@@ -82,8 +89,9 @@ class BKFACStack:
         self.K = []
         for g in self.my_factors:
             n, r, _ = self.factors[g]
-            self.U.append([torch.zeros((r, n), dtype=torch.float32, device=dev) for _ in range(2)])
-            self.D.append([torch.zeros((r,), dtype=torch.float32, device=dev) for _ in range(2)])
+            ro = self.rank_out(g)
+            self.U.append([torch.zeros((ro, n), dtype=torch.float32, device=dev) for _ in range(2)])
+            self.D.append([torch.zeros((ro,), dtype=torch.float32, device=dev) for _ in range(2)])
             self.K.append(torch.zeros((n, n), dtype=torch.float32, device=dev) if rsvd_every > 0 else None)
         self.cur = [0] * len(self.my_factors)
         self.k = 0
@@ -98,6 +106,10 @@ class BKFACStack:
                 self.S2[par][li] = torch.empty((dG, dA), dtype=torch.float32, device=dev)
 
     # ---------------------------------------------------------------------------------
+    def rank_out(self, g: int) -> int:
+        n, r, c = self.factors[g]
+        return min(n, r + c) if self.full_rank else r
+
     def state(self, g: int):
         i = self.local[g]
         return self.U[i][self.cur[i]], self.D[i][self.cur[i]]
@@ -110,7 +122,7 @@ class BKFACStack:
     def _phantom(self, i: int):
         U = self.U[i][self.cur[i]]
         U.zero_()
-        r = U.shape[0]
+        r = self.factors[self.my_factors[i]][1]
         U[self.torch.arange(r), self.torch.arange(r)] = 1.0
         self.D[i][self.cur[i]].zero_()
 

@@ -395,3 +395,83 @@ def test_brand_ea_update_equals_sequential(cuda_lib):
     for Us, Ds, Uf, Df in zip(state[0][0], state[0][1], state[1][0], state[1][1]):
         Us, Ds, Uf, Df = (t.double().numpy() for t in (Us, Ds, Uf, Df))
         assert lowrank_rel_err(Us.T, Ds, Uf.T, Df) < 1e-5
+
+
+# ------------------------------------------------------------------ NEXT-f1: full-rank output
+
+@pytest.mark.parametrize("shape", [(700, 64, 100, 64), (700, 64, 100, 40), (577, 256, 220, 256),
+                                   (200, 64, 150, 64), (96, 32, 40, 20)])
+def test_full_rank_step(cuda_lib, shape):
+    """BKFAC_FACTOR_FULL_RANK (paper-faithful): the step keeps all
+    min(n, r + c) eigenpairs of M~_B = alpha U_r D_r U_r^T + beta M M^T; columns beyond
+    r + c (c < c_max) are zero; U_in is read through its first r columns."""
+    import torch
+    from paper_2210_08494_b200 import binding
+    n, cmax, r, c = shape
+    ro_max = min(n, r + cmax)
+    ro = min(n, r + c)
+    f = synth.random_case(n, c, r, seed=4242 + n + c, k=min(n, 2 * c), decay=0.9)
+    ctx = _ctx([(n, r, cmax, binding.BKFAC_FACTOR_FULL_RANK)])
+    # the input state carries ro_max columns; only the leading r may influence the result
+    rng = np.random.default_rng(5)
+    Ufull, _ = np.linalg.qr(rng.standard_normal((n, ro_max)))
+    Dfull = np.sort(rng.random(ro_max) * 2 + 0.1)[::-1]
+    U32 = Ufull.astype(np.float32).astype(np.float64)
+    D32 = Dfull.astype(np.float32).astype(np.float64)
+    M = f.batch(1).astype(np.float64)
+    tU, tD, tM = to_dev_cols(U32), to_dev(D32), to_dev_cols(M)
+    Uo_t = torch.full((ro_max, n), 7.0, device="cuda")
+    Do_t = torch.full((ro_max,), 7.0, device="cuda")
+    ctx.bkfac_brand_update([dict(factor=0, U_in=tU, D_in=tD, M=tM, U_out=Uo_t, D_out=Do_t,
+                                 alpha=0.95, beta=0.05)])
+    torch.cuda.synchronize()
+    Ug, Dg = from_dev_cols(Uo_t), Do_t.double().cpu().numpy()
+    Uo, Do = O.brand_update(U32[:, :r], D32[:r], M, 0.95, 0.05, ro)
+    assert lowrank_rel_err(Uo, Do, Ug[:, :ro], Dg[:ro]) < TOL_STEP
+    assert eig_rel_err(Do, Dg[:ro]) < TOL_EIG
+    assert np.all(Ug[:, ro:] == 0) and np.all(Dg[ro:] == 0)
+    assert ctx.bkfac_check()[0] == 0
+
+
+def test_full_rank_stack_chain_and_precondition(cuda_lib):
+    """Stack with full_rank=True over one layer (Gamma on the dense path, A on the Brand
+    path): 4 steps, then S = Gamma~^{-1} J A~^{-1} with the
+    rank-(r + c) factors, against the oracle's chain of (truncate to r, Brand keeping
+    r + c) steps (Alg 4 :540-548 with the M~_B preconditioner :655-656)."""
+    import torch
+    from paper_2210_08494_b200 import BKFACStack
+    dG, dA, rG, rA, c = 64, 300, 40, 64, 32     # G: dense path (40 + 32 >= 64); A: Brand path
+    factors = [(dG, rG, c), (dA, rA, c)]
+    layers = [(dG, dA, 0, 1)]
+    rho, lam = 0.95, 0.1
+    st = BKFACStack(factors, layers, rho, lam, full_rank=True)
+    fg = synth.random_case(dG, c, rG, seed=11, k=24, decay=0.9)
+    fa = synth.random_case(dA, c, rA, seed=12, k=24, decay=0.9)
+    states = {0: None, 1: None}
+    J = np.random.default_rng(13).standard_normal((dG, dA))
+    S = None
+    for k in range(4):
+        Ms = {0: fg.batch(k), 1: fa.batch(k)}
+        S = st.step({g: to_dev_cols(Ms[g]) for g in (0, 1)}, {0: to_dev(J)})
+        for g, (n, r, _) in enumerate(factors):
+            Mk = Ms[g].astype(np.float32).astype(np.float64)
+            ro = min(n, r + c)
+            if states[g] is None:
+                U0 = synth.phantom_basis(n, r)
+                states[g] = O.brand_update(U0, np.zeros(r), Mk, 0.0, 1.0, ro)
+            else:
+                U, D = states[g]
+                states[g] = O.brand_update(U[:, :r], D[:r], Mk, rho, 1 - rho, ro)
+    torch.cuda.synchronize()
+    for g, (n, r, _) in enumerate(factors):
+        Ug, Dg = st.state(g)
+        Uo, Do = states[g]
+        ro = min(n, r + c)
+        assert lowrank_rel_err(Uo, Do, from_dev_cols(Ug)[:, :ro], Dg.double().cpu().numpy()[:ro]) < TOL_CHAIN
+    UG, DG = states[0]
+    UA, DA = states[1]
+    Jf = J.astype(np.float32).astype(np.float64)
+    So = O.precondition(Jf, UG, DG, lam, UA, DA, lam)
+    Sg = S[0].double().cpu().numpy()
+    assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC
+    assert st.check()[0] == 0
