@@ -102,7 +102,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   float* ybuf = vbuf + 2 * m_pad;    // 2 * m_pad  (partial y by parity, read remotely)
   float* ys = ybuf + 2 * m_pad;      // m_pad      (summed y)
   float* wp = ys + m_pad;            // m_pad      (w_{k-1})
-  float* scal = wp + m_pad;          // 64: [2] bad flag, [4..35] reduce, [40..41] alpha, d
+  float* scal = wp + m_pad;          // 64: [2] bad, [4..35] reduce, [40..41] alpha, d, [44..59] reduce 2, [60] y_k[k+1]
   float* tiles = GT ? p.gtiles : scal + 64;   // owned tiles, slot s at 1024 s
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = SYT_THREADS / 32;
@@ -165,53 +165,57 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
 #else
 #define SYT_T(i) do {} while (0)
 #endif
+  float* red2 = scal + 44;    // second reduction buffer: two block sums in one phase
+  // v_k, tau_k from column k (already carrying the pending update in x = v[]): scale,
+  // the reflector to K, d / e / tau (CTA k % C); returns tau_k
+  auto finish = [&](int kk, float ss, float* vv) -> float {
+    const float dk = scal[40], alpha = scal[41];
+    float tk, beta, scale;
+    if (ss == 0.f) {
+      tk = 0.f; beta = alpha; scale = 0.f;
+    } else {
+      const float nrm = sqrtf(alpha * alpha + ss);
+      beta = alpha >= 0.f ? -nrm : nrm;
+      tk = (beta - alpha) / beta;
+      scale = 1.f / (alpha - beta);
+    }
+    const bool writer = (q == kk % C);
+    float* kcol = K + (long)kk * ld;
+    for (int i = kk + 1 + tid; i < m; i += SYT_THREADS) {
+      float vi = 1.f;
+      if (i >= kk + 2) { vi = vv[i] * scale; if (writer) kcol[i] = vi; }
+      vv[i] = vi;
+    }
+    if (tid == 0) {
+      vv[kk] = 0.f;
+      if (kk >= 1) vv[kk - 1] = 0.f;           // stale 1 of v_{kk-2} (same parity buffer)
+      if (writer) { p.d[kk] = dk; p.e[kk] = beta; p.tau[kk] = tk; }
+    }
+    return tk;
+  };
+  // (a) for step 0: column 0 (no pending update) -> v_0, tau_0
+  float tau;
+  {
+    float ss = 0.f;
+    for (int i = tid; i < m; i += SYT_THREADS) {
+      const int pos = syt_pos(i >> 5, 0, NB);
+      const float x = *rptr(tiles + 1024L * (pos / C) + (i & 31), pos % C);
+      if (i >= 2) ss = fmaf(x, x, ss);
+      else scal[40 + i] = x;
+      vbuf[i] = x;
+    }
+    ss = syt_block_sum(ss, red);
+    tau = finish(0, ss, vbuf);
+  }
+  SYT_T(0);
+  constexpr int IPT = 4;   // rows per thread in the merged phase (m <= 2048)
   for (int k = 0; k < m - 2; ++k) {
     float* v = vbuf + (k & 1) * m_pad;            // v_k
     const float* vp = vbuf + ((k + 1) & 1) * m_pad;   // v_{k-1} (zero at k = 0)
     float* y = ybuf + (k & 1) * m_pad;
     const bool have_prev = k > 0;
-    const int kb = k >> 5, jk = k & 31;
-    // (a) every CTA: column k from its owners, pending update, v_k and tau_k
-    float tau;
-    {
-      const int base = syt_pos(kb, kb, NB);
-      const float wk = wp[k], vk = vp[k];
-      float ss = 0.f;
-      for (int i = k + tid; i < m; i += SYT_THREADS) {
-        const int pos = base + (i >> 5) - kb;
-        float x = *rptr(tiles + 1024L * (pos / C) + jk * 32 + (i & 31), pos % C);
-        if (have_prev) x -= vp[i] * wk + wp[i] * vk;
-        if (i >= k + 2) ss = fmaf(x, x, ss);
-        else scal[40 + (i - k)] = x;          // d_k (i = k), alpha (i = k + 1)
-        v[i] = x;
-      }
-      for (int i = tid; i < m_pad; i += SYT_THREADS) y[i] = 0.f;
-      ss = syt_block_sum(ss, red);
-      const float dk = scal[40], alpha = scal[41];
-      float beta, scale;
-      if (ss == 0.f) {
-        tau = 0.f; beta = alpha; scale = 0.f;
-      } else {
-        const float nrm = sqrtf(alpha * alpha + ss);
-        beta = alpha >= 0.f ? -nrm : nrm;
-        tau = (beta - alpha) / beta;
-        scale = 1.f / (alpha - beta);
-      }
-      const bool writer = (q == k % C);
-      float* kcol = K + (long)k * ld;
-      for (int i = k + tid; i < m; i += SYT_THREADS) {
-        float vi = 0.f;
-        if (i == k + 1) vi = 1.f;
-        else if (i >= k + 2) { vi = v[i] * scale; if (writer) kcol[i] = vi; }
-        v[i] = vi;
-      }
-      if (tid == 0) {
-        if (k >= 1) v[k - 1] = 0.f;           // stale 1 of v_{k-2} (same parity buffer)
-        if (writer) { p.d[k] = dk; p.e[k] = beta; p.tau[k] = tau; }
-      }
-    }
-    SYT_T(0);
-    __syncthreads();
+    const int kb = k >> 5;
+    __syncthreads();                              // v_k, w_{k-1}, zeroed y visible
     SYT_T(1);
     // (b) active tiles (J >= kb): this CTA's slots 0 .. nact-1, one per warp
     const int nact = (syt_tiles(NB - kb) - q + C - 1) / C;
@@ -273,22 +277,65 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     }
     __syncthreads();
     SYT_T(2);
-    if (C > 1) cluster.sync();                                   // (2) partial y ready
+    if (C > 1) cluster.sync();                    // partial y (and column k+1) ready
     SYT_T(3);
-    float pv = 0.f;
-    for (int i = k + 1 + tid; i < m; i += SYT_THREADS) {
-      float s = 0.f;
-      for (int r = 0; r < C; ++r) s += *rptr(y + i, r);
-      ys[i] = s;
-      pv = fmaf(s, v[i], pv);
+    // (c)+(a) merged: y_k summed through DSMEM -> w_k; in the same pass column k+1 is read
+    // from its owners, gets the pending update (v_k, w_k) and yields v_{k+1}, tau_{k+1}
+    {
+      const int k1 = k + 1;
+      const bool next = k1 <= m - 3;
+      const int kb1 = k1 >> 5, jk1 = k1 & 31, base1 = syt_pos(kb1, kb1, NB);
+      float si[IPT], xi[IPT];
+      float pv = 0.f;
+#pragma unroll
+      for (int u = 0; u < IPT; ++u) {
+        const int i = k1 + tid + u * SYT_THREADS;
+        si[u] = 0.f;
+        xi[u] = 0.f;
+        if (i < m) {
+          float sacc = 0.f;
+          for (int r = 0; r < C; ++r) sacc += *rptr(y + i, r);
+          si[u] = sacc;
+          pv = fmaf(sacc, v[i], pv);
+          if (next) {
+            const int pos = base1 + (i >> 5) - kb1;
+            xi[u] = *rptr(tiles + 1024L * (pos / C) + jk1 * 32 + (i & 31), pos % C);
+          }
+        }
+      }
+      if (tid == 0) scal[60] = si[0];             // y_k at row k+1, shared after the sum's barrier
+      pv = syt_block_sum(pv, red);
+      const float s1 = scal[60];
+      const float gamma = 0.5f * tau * tau * pv;
+      const float vk1 = v[k1];
+      const float wk1 = tau * s1 - gamma * vk1;
+      float* vn = vbuf + (k1 & 1) * m_pad;         // v_{k+1} (v_{k-1} is no longer needed)
+      float ss = 0.f;
+#pragma unroll
+      for (int u = 0; u < IPT; ++u) {
+        const int i = k1 + tid + u * SYT_THREADS;
+        if (i < m) {
+          const float w = tau * si[u] - gamma * v[i];
+          wp[i] = w;
+          if (next) {
+            const float x = xi[u] - (v[i] * wk1 + w * vk1);
+            if (i >= k1 + 2) ss = fmaf(x, x, ss);
+            else scal[40 + (i - k1)] = x;         // d_{k+1} (i = k+1), alpha (i = k+2)
+            vn[i] = x;
+          }
+        }
+      }
+      if (tid == 0) wp[k] = 0.f;                  // w_k vanishes at rows <= k
+      if (next) {
+        float* yn = ybuf + (k1 & 1) * m_pad;       // step k-1's partials: every reader is done
+        for (int i = tid; i < m_pad; i += SYT_THREADS) yn[i] = 0.f;
+        ss = syt_block_sum(ss, red2);
+        tau = finish(k1, ss, vn);
+      }
     }
-    pv = syt_block_sum(pv, red);
-    const float gamma = 0.5f * tau * tau * pv;
-    for (int i = tid; i < m_pad; i += SYT_THREADS)
-      wp[i] = (i > k && i < m) ? tau * ys[i] - gamma * v[i] : 0.f;
-    __syncthreads();
     SYT_T(4);
   }
+  __syncthreads();
 #ifdef BKFAC_SYT_TIMING
   if (tid == 0 && p.status) {   // tuning builds: per-phase cycle sums of CTA q
     unsigned long long* o = reinterpret_cast<unsigned long long*>(p.Y) + 8 * q;
