@@ -347,6 +347,28 @@ def precondition(J: np.ndarray, U_G: np.ndarray, D_G: np.ndarray, lam_G: float,
     return apply_inverse_left(Mk, U_G, DG, lG)
 
 
+def precondition_factored(G: np.ndarray, A: np.ndarray, U_G: np.ndarray, D_G: np.ndarray,
+                          lam_G: float, U_A: np.ndarray, D_A: np.ndarray, lam_A: float,
+                          continuation: bool = False, lam_relative: bool = False) -> np.ndarray:
+    """Algorithm 8 (Eq.(20)-(21)), linear in d: the gradient arrives
+    factored, Mat(g) = G A^T with G (d_Gamma x n_M), A (d_A x n_M), and
+      A^T_bold = A^T V_A [(D_A + lam I)^{-1} - lam^{-1} I] V_A^T + lam^{-1} A^T
+      G_bold   = V_G [(D_G + lam I)^{-1} - lam^{-1} I] V_G^T G + lam^{-1} G
+      S        = G_bold A^T_bold.
+    Effective (D, lambda) as in ``precondition`` (reg_params)."""
+    G = np.asarray(G, dtype=f64)
+    A = np.asarray(A, dtype=f64)
+    DA, lA = reg_params(D_A, lam_A, continuation, lam_relative)
+    DG, lG = reg_params(D_G, lam_G, continuation, lam_relative)
+    UA = np.asarray(U_A, dtype=f64)
+    UG = np.asarray(U_G, dtype=f64)
+    sA = 1.0 / (DA + lA) - 1.0 / lA
+    sG = 1.0 / (DG + lG) - 1.0 / lG
+    At_bold = ((A.T @ UA) * sA[None, :]) @ UA.T + A.T / lA
+    G_bold = UG @ ((UG.T @ G) * sG[:, None]) + G / lG
+    return G_bold @ At_bold
+
+
 # --------------------------------------------------------------------------
 # Stack driver (SURVEY §8(c) c7): init, Brand each step, optional RSVD overwrite
 # of the dense EA factor every T steps (Alg 5), preconditioning each step.

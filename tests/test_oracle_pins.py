@@ -371,6 +371,28 @@ def test_precondition_kronecker_identity():
         assert np.abs(Gam @ S @ Acal - J).max() < 1e-12 * np.abs(J).max()
 
 
+def test_precondition_factored_alg8_kronecker():
+    """Algorithm 8: with Mat(g) = G A^T given factored, the linear-time
+    application equals the Kronecker solve (A~ (x) Gamma~)^{-1} vec(G A^T) (:359), with and
+    without continuation / relative lambda."""
+    rng = np.random.default_rng(202)
+    dG, dA, rG, rA, nM = 7, 10, 3, 4, 5
+    UG, _ = np.linalg.qr(rng.standard_normal((dG, rG)))
+    UA, _ = np.linalg.qr(rng.standard_normal((dA, rA)))
+    DG, DA = np.array([2.0, 0.7, 0.3]), np.array([3.0, 1.0, 0.4, 0.05])
+    lG, lA = 0.25, 0.15
+    G = rng.standard_normal((dG, nM))
+    A = rng.standard_normal((dA, nM))
+    for cont, rel in ((False, False), (True, False), (False, True)):
+        S = O.precondition_factored(G, A, UG, DG, lG, UA, DA, lA, continuation=cont, lam_relative=rel)
+        DGe, lGe = O.reg_params(DG, lG, cont, rel)
+        DAe, lAe = O.reg_params(DA, lA, cont, rel)
+        Gam = O.densify(UG, DGe) + lGe * np.eye(dG)
+        Acal = O.densify(UA, DAe) + lAe * np.eye(dA)
+        vecS = np.linalg.solve(np.kron(Acal, Gam), (G @ A.T).reshape(-1, order="F"))
+        assert np.abs(S - vecS.reshape(dG, dA, order="F")).max() < 1e-12 * np.abs(S).max()
+
+
 def test_precondition_worked_examples():
     sp = _spec()
     e = sp["apply_inverse_e1"]
