@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--pool", type=int, default=2, help="distinct input batches kept on device")
     ap.add_argument("--full-rank", action="store_true",
                     help="NEXT-f1: keep all r + c eigenpairs per step and precondition with them")
+    ap.add_argument("--factored", action="store_true",
+                    help="NEXT-f2: precondition from the factored gradient G A^T (Algorithm 8)")
     ap.add_argument("--no-graphs", action="store_true",
                     help="launch every step eagerly instead of replaying CUDA graphs")
     return ap.parse_args()
@@ -334,7 +336,8 @@ def run_reference(args, rank, world):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * t_total / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name + ("+f1_full_rank" if args.full_rank else ""),
+            "config": {"workload": cfg.name + ("+f1_full_rank" if args.full_rank else "")
+                                   + ("+f2_factored" if args.factored else ""),
                        "factors": n_f, "layers": n_l,
                        "sample": "one layer (2 factor updates + preconditioning) per step"},
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores,
@@ -365,7 +368,8 @@ def run_ours(args, rank, world, local_rank):
     use_graphs = not args.no_graphs
 
     def one_step(i, graph):
-        S = stack.step(M_pool[i % args.pool], J_pool[i % args.pool], graph=graph)
+        S = stack.step(M_pool[i % args.pool], None if args.factored else J_pool[i % args.pool],
+                       graph=graph, factored=args.factored)
         if gather is not None:
             gather.gather(S)
 
@@ -450,7 +454,8 @@ def run_ours(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "weak" if not layers else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "layers_per_s": round(layers_per_s, 3),
-            "config": {"workload": cfg.name + ("+f1_full_rank" if args.full_rank else ""),
+            "config": {"workload": cfg.name + ("+f1_full_rank" if args.full_rank else "")
+                                   + ("+f2_factored" if args.factored else ""),
                        "factors": n_f, "layers": n_l,
                        "n_BS": cfg.factors[0].c, "rho": cfg.rho, "lambda": cfg.lam,
                        "rsvd_every": cfg.rsvd_every, "parallelism": f"layer-shard x{world}",
@@ -495,7 +500,8 @@ def run_e2e(args, stack, gather, cfg, device, stream, world):
               for g in stack.my_factors} for _ in range(2)]
     dev_J = [{li: torch.empty((cfg.layers[li].d_G, cfg.layers[li].d_A), dtype=torch.float32,
                               device=device) for li in stack.my_layers} for _ in range(2)]
-    h2d = sum(4 * t.numel() for t in dev_M[0].values()) + sum(4 * t.numel() for t in dev_J[0].values())
+    h2d = sum(4 * t.numel() for t in dev_M[0].values()) + \
+        (0 if args.factored else sum(4 * t.numel() for t in dev_J[0].values()))
     d2h = sum(4 * cfg.layers[li].d_G * cfg.layers[li].d_A for li in stack.my_layers)
     use_graphs = not args.no_graphs
     up, down = torch.cuda.Stream(device=device), torch.cuda.Stream(device=device)
@@ -512,9 +518,10 @@ def run_e2e(args, stack, gather, cfg, device, stream, world):
             for g, t in dev_M[b].items():
                 f = cfg.factors[g]
                 t.copy_(host_M[(f.c, f.n)], non_blocking=True)
-            for li, t in dev_J[b].items():
-                l = cfg.layers[li]
-                t.copy_(host_J[(l.d_G, l.d_A)], non_blocking=True)
+            if not args.factored:
+                for li, t in dev_J[b].items():
+                    l = cfg.layers[li]
+                    t.copy_(host_J[(l.d_G, l.d_A)], non_blocking=True)
             ev_up[b].record(up)
 
     def run(n):
@@ -523,7 +530,8 @@ def run_e2e(args, stack, gather, cfg, device, stream, world):
             b = (j + par0) & 1
             stream.wait_event(ev_up[b])
             stream.wait_event(ev_down[b])         # S set b was read back (step j-2)
-            S = stack.step(dev_M[b], dev_J[b], graph=use_graphs)
+            S = stack.step(dev_M[b], None if args.factored else dev_J[b], graph=use_graphs,
+                           factored=args.factored)
             if gather is not None:
                 gather.gather(S)
             ev_done[b].record(stream)

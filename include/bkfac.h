@@ -82,8 +82,9 @@ typedef enum {
 /* One K-factor: dimension n, target rank r (1 <= r <= n), largest batch c_max.       */
 typedef struct { int n; int r; int c_max; int flags; } bkfac_factor_desc;
 
-/* One preconditioned layer: gradient J is d_G x d_A (row-major); ranks of its factors. */
-typedef struct { int d_G; int d_A; int r_G; int r_A; } bkfac_layer_desc;
+/* One preconditioned layer: gradient J is d_G x d_A (row-major); ranks of its factors;
+ * n_max > 0 reserves workspace for bkfac_precondition_factored with up to n_max samples. */
+typedef struct { int d_G; int d_A; int r_G; int r_A; int n_max; } bkfac_layer_desc;
 
 /* Creates a context on CUDA device `device` for `nfactors` factors and `nlayers`
  * layers.  Descriptors are copied.  Returns BKFAC_ERR_DIM on invalid shapes. */
@@ -168,6 +169,26 @@ typedef struct {
 } bkfac_precond_args;
 bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, int count,
                                 void* stream);
+
+/* NEXT-f2, Algorithm 8 (Eq.(20)-(21)): the same S = Gamma~^{-1} Mat(g)
+ * A~^{-1} when the gradient arrives factored, Mat(g) = G A^T, without ever forming it:
+ *   A_b = A~^{-1} A = U_A diag(s_A) U_A^T A + A / lambda_A     (d_A x n)
+ *   G_b = Gamma~^{-1} G = U_G diag(s_G) U_G^T G + G / lambda_G (d_G x n)
+ *   S   = G_b A_b^T                                             (d_G x d_A row-major)
+ * O(r (d_G + d_A) n) for the inverse applications.  G (d_G x n) and A (d_A x n) are
+ * col-major (the per-sample matrices whose Gram products are the K-factor statistics:
+ * the M of the layer's two factors); n <= the layer's n_max (BKFAC_ERR_DIM otherwise).
+ * Flags as bkfac_precondition.  S must not alias G or A. */
+typedef struct {
+  int layer;
+  const float* U_G; const float* D_G; float lambda_G;
+  const float* U_A; const float* D_A; float lambda_A;
+  const float* G; const float* A; int n;
+  float* S;
+  int flags;
+} bkfac_precond_factored_args;
+bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_factored_args* args,
+                                         int count, void* stream);
 
 /* The fp32-accurate GEMM every contraction above runs on, exposed for testing and for
  * callers that need the same arithmetic:  C = alpha op(A) op(B) + beta C  (BLAS col-major;

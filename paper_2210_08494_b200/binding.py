@@ -31,7 +31,7 @@ STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKF
 EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac_destroy",
             "bkfac_brand_update", "bkfac_brand_ea_update", "bkfac_ea_accumulate", "bkfac_ea_accumulate_batch",
             "bkfac_rsvd_overwrite", "bkfac_rsvd_overwrite_batch",
-            "bkfac_precondition", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
+            "bkfac_precondition", "bkfac_precondition_factored", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
             "bkfac_profile_enable", "bkfac_profile_read", "bkfac_status_string",
             "bkfac_build_info", "bkfac_gemm"]
 
@@ -49,7 +49,7 @@ class FactorDesc(ctypes.Structure):
 
 class LayerDesc(ctypes.Structure):
     _fields_ = [("d_G", ctypes.c_int), ("d_A", ctypes.c_int), ("r_G", ctypes.c_int),
-                ("r_A", ctypes.c_int)]
+                ("r_A", ctypes.c_int), ("n_max", ctypes.c_int)]
 
 
 class BrandArgs(ctypes.Structure):
@@ -74,6 +74,13 @@ class StageStat(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("calls", ctypes.c_longlong),
                 ("launches", ctypes.c_longlong), ("ms", ctypes.c_double),
                 ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+class PrecondFactoredArgs(ctypes.Structure):
+    _fields_ = [("layer", ctypes.c_int), ("U_G", ctypes.c_void_p), ("D_G", ctypes.c_void_p),
+                ("lambda_G", ctypes.c_float), ("U_A", ctypes.c_void_p), ("D_A", ctypes.c_void_p),
+                ("lambda_A", ctypes.c_float), ("G", ctypes.c_void_p), ("A", ctypes.c_void_p),
+                ("n", ctypes.c_int), ("S", ctypes.c_void_p), ("flags", ctypes.c_int)]
 
 
 class PrecondArgs(ctypes.Structure):
@@ -123,6 +130,8 @@ def load(path: str = None) -> ctypes.CDLL:
     lib.bkfac_gaussian_sketch.restype = ci
     lib.bkfac_precondition.argtypes = [vp, ctypes.POINTER(PrecondArgs), ci, vp]
     lib.bkfac_precondition.restype = ci
+    lib.bkfac_precondition_factored.argtypes = [vp, ctypes.POINTER(PrecondFactoredArgs), ci, vp]
+    lib.bkfac_precondition_factored.restype = ci
     lib.bkfac_check.argtypes = [vp, vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
     lib.bkfac_check.restype = ci
     lib.bkfac_launch_count.argtypes = [vp]
@@ -172,7 +181,9 @@ class Context:
         self.lib = load()
         self.device = device
         fd = (FactorDesc * max(1, len(factors)))(*[FactorDesc(*f) for f in factors])
-        ld = (LayerDesc * max(1, len(layers)))(*[LayerDesc(*l) for l in layers])
+        # (d_G, d_A, r_G, r_A[, n_max]); n_max > 0 enables bkfac_precondition_factored
+        ld = (LayerDesc * max(1, len(layers)))(*[LayerDesc(*(tuple(l) + (0,) * (5 - len(l))))
+                                                 for l in layers])
         h = ctypes.c_void_p()
         _check(self.lib.bkfac_init(ctypes.byref(h), fd, len(factors), ld, len(layers), device),
                "bkfac_init")
@@ -261,6 +272,18 @@ class Context:
                                  _ptr(a["J"]), _ptr(a["S"]), int(a.get("flags", 0)))
         _check(self.lib.bkfac_precondition(self.h, arr, len(items), _stream_ptr(stream)),
                "bkfac_precondition")
+
+    def bkfac_precondition_factored(self, items: List[dict], stream=None) -> None:
+        """Algorithm 8: dict(layer, U_G, D_G, lambda_G, U_A, D_A, lambda_A, G, A, S, flags);
+        G, A are (n, d) tensors (= col-major d x n), n = G.shape[0]."""
+        arr = (PrecondFactoredArgs * len(items))()
+        for i, a in enumerate(items):
+            arr[i] = PrecondFactoredArgs(a["layer"], _ptr(a["U_G"]), _ptr(a["D_G"]), float(a["lambda_G"]),
+                                         _ptr(a["U_A"]), _ptr(a["D_A"]), float(a["lambda_A"]),
+                                         _ptr(a["G"]), _ptr(a["A"]), int(a["G"].shape[0]),
+                                         _ptr(a["S"]), int(a.get("flags", 0)))
+        _check(self.lib.bkfac_precondition_factored(self.h, arr, len(items), _stream_ptr(stream)),
+               "bkfac_precondition_factored")
 
     def bkfac_check(self, stream=None):
         bad = ctypes.c_int(-1)

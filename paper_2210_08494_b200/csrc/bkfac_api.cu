@@ -88,8 +88,11 @@ struct FactorPlan {
 
 struct LayerPlan {
   bkfac_layer_desc d;
-  size_t Y, Xt, Z, sA, sG, lam, ws;  // lam: [lamA, lamG, coef]
+  size_t Y, Xt, Z, sA, sG, lam, ws;  // lam: [lamA, lamG, coef, 1/lamA, 1/lamG]
   size_t ws_elems = 0;
+  // Algorithm 8 (n_max > 0): P_G = G^T U_G, P_A = A^T U_A (n x r), G_b, A_b (d x n)
+  size_t fPG = 0, fPA = 0, fGb = 0, fAb = 0, fws = 0, fws2 = 0;
+  size_t fws_elems = 0;
 };
 
 }  // namespace
@@ -670,7 +673,8 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
     LayerPlan lp;
     lp.d = layers[i];
     const auto& d = lp.d;
-    if (d.d_G <= 0 || d.d_A <= 0 || d.r_G < 0 || d.r_A < 0 || d.r_G > d.d_G || d.r_A > d.d_A) {
+    if (d.d_G <= 0 || d.d_A <= 0 || d.r_G < 0 || d.r_A < 0 || d.r_G > d.d_G || d.r_A > d.d_A ||
+        d.n_max < 0) {
       delete c;
       return BKFAC_ERR_DIM;
     }
@@ -679,7 +683,17 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
     lp.Z = a.take(sizeof(float) * (size_t)std::max(d.r_G, 1) * std::max(d.r_A, 1));
     lp.sA = a.take(sizeof(float) * std::max(d.r_A, 1));
     lp.sG = a.take(sizeof(float) * std::max(d.r_G, 1));
-    lp.lam = a.take(sizeof(float) * 4);
+    lp.lam = a.take(sizeof(float) * 8);
+    if (d.n_max > 0) {
+      const size_t nm = (size_t)d.n_max;
+      lp.fPG = a.take(sizeof(float) * nm * std::max(d.r_G, 1));
+      lp.fPA = a.take(sizeof(float) * nm * std::max(d.r_A, 1));
+      lp.fGb = a.take(sizeof(float) * nm * d.d_G);
+      lp.fAb = a.take(sizeof(float) * nm * d.d_A);
+      lp.fws_elems = (long)kSplitMax * (long)nm * std::max(std::max(d.r_G, d.r_A), 1);
+      lp.fws = a.take(sizeof(float) * lp.fws_elems);
+      lp.fws2 = a.take(sizeof(float) * lp.fws_elems);
+    }
     lp.ws_elems = (long)kSplitMax * std::max((long)d.d_G * d.r_A, (long)d.d_A * d.r_G);
     lp.ws = a.take(sizeof(float) * std::max<long>(lp.ws_elems, 1));
     c->l.push_back(lp);
@@ -1430,6 +1444,112 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     gs.add(false, true, p, 0);
   }
   return run_gemms(ctx, gs, st, "gemm_prec_out");
+}
+
+bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_factored_args* args,
+                                         int count, void* stream) {
+  if (!ctx || (count > 0 && !args) || count < 0) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    if (a.layer < 0 || a.layer >= (int)ctx->l.size()) return BKFAC_ERR_INVALID_ARG;
+    const auto& d = ctx->l[a.layer].d;
+    if (!a.G || !a.A || !a.S) return BKFAC_ERR_INVALID_ARG;
+    if ((d.r_A > 0 && (!a.U_A || !a.D_A)) || (d.r_G > 0 && (!a.U_G || !a.D_G)))
+      return BKFAC_ERR_INVALID_ARG;
+    if (!(a.lambda_A > 0.f) || !(a.lambda_G > 0.f)) return BKFAC_ERR_INVALID_ARG;
+    if (a.n <= 0 || a.n > d.n_max) return BKFAC_ERR_DIM;
+    if (a.S == a.G || a.S == a.A) return BKFAC_ERR_ALIAS;
+    for (int j = 0; j < i; ++j)
+      if (args[j].layer == a.layer) return BKFAC_ERR_INVALID_ARG;
+  }
+  if (count == 0) return BKFAC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static PrecScalBatch psb;
+  static PrecScaleBatch pcb;
+  bkfac_status rs;
+  GemmStage gs;
+  // scalars (s_A, s_G, lambdas, 1/lambdas) as bkfac_precondition
+  prof_begin(ctx, "prec_scalars", st, 0.0, 0.0);
+  for (int i0 = 0; i0 < count; i0 += PS_MAXP) {
+    const int n = std::min(count - i0, PS_MAXP);
+    psb.nprob = 0;
+    for (int i = i0; i < i0 + n; ++i) {
+      const auto& a = args[i];
+      const auto& lp = ctx->l[a.layer];
+      PrecScalProb q{};
+      q.D[0] = a.D_A; q.r[0] = lp.d.r_A; q.lam[0] = a.lambda_A; q.s[0] = at<float>(ctx, lp.sA);
+      q.D[1] = a.D_G; q.r[1] = lp.d.r_G; q.lam[1] = a.lambda_G; q.s[1] = at<float>(ctx, lp.sG);
+      q.flags = a.flags;
+      q.lam_out = at<float>(ctx, lp.lam);
+      psb.p[psb.nprob++] = q;
+    }
+    prec_scalars_kernel<<<psb.nprob, 256, 0, st>>>(psb);
+    LAUNCH_CHECK(ctx);
+  }
+  prof_end(ctx, st);
+  // P_G = G^T U_G (n x r_G), P_A = A^T U_A (n x r_A): long K (d), small output -> split-K
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    const auto& lp = ctx->l[a.layer];
+    const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G, n = a.n;
+    if (rG > 0) {
+      GemmProb p = gp(a.G, dG, a.U_G, dG, at<float>(ctx, lp.fPG), n, n, rG, dG, 1.f);
+      gemm_ws(p, at<float>(ctx, lp.fws));
+      gs.add(true, false, p, lp.fws_elems);
+    }
+    if (rA > 0) {
+      GemmProb p = gp(a.A, dA, a.U_A, dA, at<float>(ctx, lp.fPA), n, n, rA, dA, 1.f);
+      gemm_ws(p, at<float>(ctx, lp.fws2));
+      gs.add(true, false, p, lp.fws_elems);
+    }
+  }
+  if ((rs = run_gemms(ctx, gs, st, "gemm_f2_proj")) != BKFAC_OK) return rs;
+  // P_G(:, j) *= s_G[j], P_A(:, j) *= s_A[j]
+  prof_begin(ctx, "prec_scale", st, 0.0, 0.0);
+  for (int i0 = 0; i0 < count; i0 += PS_MAXP / 2) {
+    const int n = std::min(count - i0, PS_MAXP / 2);
+    pcb.nprob = 0;
+    for (int i = i0; i < i0 + n; ++i) {
+      const auto& a = args[i];
+      const auto& lp = ctx->l[a.layer];
+      if (lp.d.r_G > 0)
+        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.fPG), a.n, a.n, lp.d.r_G, at<float>(ctx, lp.sG), nullptr, nullptr, 0};
+      if (lp.d.r_A > 0)
+        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.fPA), a.n, a.n, lp.d.r_A, at<float>(ctx, lp.sA), nullptr, nullptr, 0};
+    }
+    if (pcb.nprob) {
+      prec_scale_kernel<<<dim3(64, pcb.nprob), 256, 0, st>>>(pcb);
+      LAUNCH_CHECK(ctx);
+    }
+  }
+  prof_end(ctx, st);
+  // G_b = U_G P_G^T + G / lambda_G, A_b = U_A P_A^T + A / lambda_A (device-scalar beta)
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    const auto& lp = ctx->l[a.layer];
+    const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G, n = a.n;
+    float* lam = at<float>(ctx, lp.lam);
+    GemmProb pg = gp(rG > 0 ? a.U_G : a.G, dG, at<float>(ctx, lp.fPG), n, at<float>(ctx, lp.fGb), dG,
+                     dG, n, rG, 1.f, a.G, dG, 1.f);
+    pg.beta_dev = lam + 4;
+    pg.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);   // every element of G passes here
+    gs.add(false, true, pg, 0);
+    GemmProb pa = gp(rA > 0 ? a.U_A : a.A, dA, at<float>(ctx, lp.fPA), n, at<float>(ctx, lp.fAb), dA,
+                     dA, n, rA, 1.f, a.A, dA, 1.f);
+    pa.beta_dev = lam + 3;
+    pa.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);
+    gs.add(false, true, pa, 0);
+  }
+  if ((rs = run_gemms(ctx, gs, st, "gemm_f2_apply")) != BKFAC_OK) return rs;
+  // S^T (d_A x d_G) = A_b G_b^T
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    const auto& lp = ctx->l[a.layer];
+    const int dG = lp.d.d_G, dA = lp.d.d_A, n = a.n;
+    gs.add(false, true, gp(at<float>(ctx, lp.fAb), dA, at<float>(ctx, lp.fGb), dG, a.S, dA, dA, dG, n, 1.f), 0);
+  }
+  return run_gemms(ctx, gs, st, "gemm_f2_out");
 }
 
 // ------------------------------------------------------------------------- GEMM primitive

@@ -62,7 +62,8 @@ __global__ void nonfinite_kernel(const __grid_constant__ NfBatch b) {
 // ---- preconditioner scalars (Alg 1 lines 16-17) ---------------------
 // One CTA per layer.  For each side: effective lambda (relative mode :940, continuation
 // :711) and s_i = (D_i + lambda)^{-1} - 1/lambda; then the coefficient of J in S,
-// 1 / (lambda_G lambda_A).  Writes s_A, s_G and lam_out[0..2] = {lambda_A, lambda_G, coef}.
+// 1 / (lambda_G lambda_A).  Writes s_A, s_G and lam_out[0..4] = {lambda_A, lambda_G, coef,
+// 1 / lambda_A, 1 / lambda_G}.
 struct PrecScalProb {
   const float* D[2]; int r[2]; float lam[2]; float* s[2];   // [0] = A side, [1] = Gamma side
   int flags;
@@ -98,6 +99,8 @@ __global__ void prec_scalars_kernel(const __grid_constant__ PrecScalBatch b) {
     p.lam_out[0] = lam[0];
     p.lam_out[1] = lam[1];
     p.lam_out[2] = 1.f / (lam[1] * lam[0]);
+    p.lam_out[3] = 1.f / lam[0];
+    p.lam_out[4] = 1.f / lam[1];
   }
 }
 

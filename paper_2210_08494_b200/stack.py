@@ -81,7 +81,9 @@ class BKFACStack:
         ldesc = []
         for li in self.my_layers:
             dG, dA, g, a = self.layers[li]
-            ldesc.append((dG, dA, self.rank_out(g), self.rank_out(a)))
+            # n_max: Algorithm 8 (factored gradients G = M_Gamma, A = M_A) needs both batches
+            ldesc.append((dG, dA, self.rank_out(g), self.rank_out(a),
+                          min(self.factors[g][2], self.factors[a][2])))
         self.ctx = binding.Context(fdesc, ldesc, device=device)
         dev = f"cuda:{device}"
         self.U = []
@@ -127,26 +129,31 @@ class BKFACStack:
         self.D[i][self.cur[i]].zero_()
 
     def step(self, M: Dict[int, "torch.Tensor"], J: Optional[Dict[int, "torch.Tensor"]] = None,
-             stream=None, graph: bool = False) -> Dict[int, "torch.Tensor"]:
+             stream=None, graph: bool = False, factored: bool = False) -> Dict[int, "torch.Tensor"]:
         """One step over the owned factors (M keyed by global factor index, each (c, n))
         and owned layers (J keyed by global layer index, each (d_G, d_A)).
 
         graph=True replays a CUDA graph of the step's launches (captured on first use per
         U/D ping-pong parity and input buffers -- the inputs must be the same tensors on
         every replay, refilled in place).  The initial step and RSVD-overwrite steps always
-        run eagerly; the library's per-stage profiling must be off while graphs are used."""
+        run eagerly; the library's per-stage profiling must be off while graphs are used.
+
+        factored=True preconditions every owned layer by Algorithm 8 (NEXT-f2,
+        PAPER.md:882-930) from the factored gradient Mat(g) = G A^T with G = M[Gamma factor],
+        A = M[A factor] (the same per-sample matrices as the statistics); J is not used."""
         torch = self.torch
         if graph and self.k > 0 and not (self.rsvd_every and self.k % self.rsvd_every == 0):
             key = (self.cur[0] if self.cur else 0,
                    tuple(M[g].data_ptr() for g in self.my_factors),
-                   tuple(J[li].data_ptr() for li in self.my_layers) if J is not None else None)
+                   tuple(J[li].data_ptr() for li in self.my_layers) if J is not None else None,
+                   factored)
             main = stream if stream is not None else torch.cuda.current_stream(self.device)
             hit = self._graphs.get(key)
             if hit is None:
                 g = torch.cuda.CUDAGraph()
                 main.synchronize()
                 with torch.cuda.graph(g):
-                    out = self._step(M, J, torch.cuda.current_stream(self.device))
+                    out = self._step(M, J, torch.cuda.current_stream(self.device), factored)
                 self._graphs[key] = (g, out)
                 with torch.cuda.stream(main):
                     g.replay()          # capture only recorded the launches: run them
@@ -158,9 +165,9 @@ class BKFACStack:
             for i in range(len(self.my_factors)):
                 self.cur[i] = 1 - self.cur[i]
             return out
-        return self._step(M, J, stream)
+        return self._step(M, J, stream, factored)
 
-    def _step(self, M, J, stream):
+    def _step(self, M, J, stream, factored=False):
         k = self.k
         torch = self.torch
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -198,7 +205,18 @@ class BKFACStack:
         for i in range(len(self.my_factors)):
             self.cur[i] = 1 - self.cur[i]
         out = {}
-        if J is not None and self.my_layers:
+        if factored and self.my_layers:
+            items = []
+            for lj, li in enumerate(self.my_layers):
+                dG, dA, g, a = self.layers[li]
+                UG, DG = self.state(g)
+                UA, DA = self.state(a)
+                items.append(dict(layer=lj, U_G=UG, D_G=DG, lambda_G=self.lam, U_A=UA, D_A=DA,
+                                  lambda_A=self.lam, G=M[g], A=M[a], S=self.S2[k & 1][li],
+                                  flags=self.precond_flags))
+            self.ctx.bkfac_precondition_factored(items, main)
+            out = {li: self.S2[k & 1][li] for li in self.my_layers}
+        elif J is not None and self.my_layers:
             items = []
             for lj, li in enumerate(self.my_layers):
                 dG, dA, g, a = self.layers[li]

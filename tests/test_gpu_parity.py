@@ -475,3 +475,63 @@ def test_full_rank_stack_chain_and_precondition(cuda_lib):
     Sg = S[0].double().cpu().numpy()
     assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC
     assert st.check()[0] == 0
+
+
+# ------------------------------------------------------------------ NEXT-f2: Algorithm 8
+
+@pytest.mark.parametrize("dims", [(128, 256, 64, 64, 32), (512, 4609, 220, 220, 256),
+                                  (10, 513, 10, 220, 256), (64, 300, 0, 16, 20)])
+@pytest.mark.parametrize("flags", [0, 3])
+def test_precondition_factored_alg8(cuda_lib, dims, flags):
+    """bkfac_precondition_factored vs the oracle's Algorithm 8 on the same
+    fp32 inputs: S = (Gamma~^{-1} G)(A~^{-1} A)^T without forming Mat(g) = G A^T."""
+    import torch
+    dG, dA, rG, rA, n = dims
+    if (flags & 2) and min(rG, rA) == 0:
+        pytest.skip("relative lambda (phi * max D) needs a non-empty spectrum")
+    rng = np.random.default_rng(dG + dA + n + flags)
+    def rep(d, r):
+        if r == 0:
+            return np.zeros((d, 0)), np.zeros(0)
+        U, _ = np.linalg.qr(rng.standard_normal((d, r)))
+        return U, np.sort(rng.random(r) * 3 + 1e-3)[::-1]
+    UG, DG = rep(dG, rG)
+    UA, DA = rep(dA, rA)
+    G = rng.standard_normal((dG, n)) * 0.1
+    A = rng.standard_normal((dA, n))
+    cast = lambda x: x.astype(np.float32).astype(np.float64)
+    UG, DG, UA, DA, G, A = map(cast, (UG, DG, UA, DA, G, A))
+    ctx = _ctx([], [(dG, dA, rG, rA, n)])
+    S = torch.empty((dG, dA), device="cuda")
+    dev = lambda U: to_dev_cols(U) if U.shape[1] else None
+    ctx.bkfac_precondition_factored([dict(layer=0, U_G=dev(UG), D_G=to_dev(DG) if rG else None,
+                                          lambda_G=0.1, U_A=dev(UA), D_A=to_dev(DA) if rA else None,
+                                          lambda_A=0.05, G=to_dev_cols(G), A=to_dev_cols(A), S=S,
+                                          flags=flags)])
+    torch.cuda.synchronize()
+    So = O.precondition_factored(G, A, UG, DG, 0.1, UA, DA, 0.05,
+                                 continuation=bool(flags & 1), lam_relative=bool(flags & 2))
+    Sg = S.double().cpu().numpy()
+    assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC
+    assert ctx.bkfac_check()[0] == 0
+
+
+def test_stack_factored_equals_dense_gradient(cuda_lib):
+    """Stack step with factored=True (G = M_Gamma, A = M_A) equals the regular path on
+    J = G A^T (formed on the host in fp64), on a config-3 layer pair."""
+    import torch
+    from paper_2210_08494_b200 import BKFACStack
+    factors = [(512, 220, 256), (1153, 220, 256)]
+    layers = [(512, 1153, 0, 1)]
+    st_f = BKFACStack(factors, layers, 0.95, 0.1)
+    st_j = BKFACStack(factors, layers, 0.95, 0.1)
+    fs = [synth.random_case(n, c, r, seed=90 + i, k=48, decay=0.93) for i, (n, r, c) in enumerate(factors)]
+    for k in range(3):
+        Ms = {g: to_dev_cols(fs[g].batch(k)) for g in (0, 1)}
+        J = fs[0].batch(k).astype(np.float64) @ fs[1].batch(k).astype(np.float64).T
+        Sf = st_f.step(Ms, None, factored=True)[0]
+        Sj = st_j.step(Ms, {0: to_dev(J)})[0]
+    torch.cuda.synchronize()
+    a, b = Sf.double().cpu().numpy(), Sj.double().cpu().numpy()
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) < TOL_PREC
+    assert st_f.check()[0] == 0
