@@ -300,6 +300,29 @@ def rsvd_overwrite(Mcal: np.ndarray, r: int, oversample: int, power_iters: int,
 
 
 # --------------------------------------------------------------------------
+# Light correction, Algorithm 6 -- B-KFAC-C, Algorithm 7 (:691-701)
+# --------------------------------------------------------------------------
+
+
+def light_correction(U: np.ndarray, D: np.ndarray, Mcal: np.ndarray,
+                     col_idx: Sequence[int]) -> Tuple[np.ndarray, np.ndarray]:
+    """Algorithm 6.  col_idx (n_crc distinct indices < r) is the random
+    choice of line 2, passed in.  Line 4: M_S = U_c^T Mcal U_c with U_c = U[:, col_idx];
+    line 5: U_S D_S U_S^T = EVD(M_S); line 7: the representation is corrected in that
+    subspace -- U[:, col_idx] <- U_c U_S (the EVD's U expressed in the original basis,
+    the reading that keeps U n x r), D[col_idx] <- D_S.  Other columns are unchanged."""
+    U = np.array(U, dtype=f64, copy=True)
+    D = np.array(D, dtype=f64, copy=True)
+    idx = np.asarray(col_idx, dtype=np.int64)
+    Uc = U[:, idx]
+    MS = Uc.T @ np.asarray(Mcal, dtype=f64) @ Uc
+    US, DS = sym_evd(MS)
+    U[:, idx] = Uc @ US
+    D[idx] = DS
+    return U, D
+
+
+# --------------------------------------------------------------------------
 # Regularised low-rank inverse application (Alg 1 lines 16-17 :403-405;
 # identity (A (x) Gamma)^{-1} g = vec(Gamma^{-1} Mat(g) A^{-1}), :359;
 # spectrum continuation :711; relative lambda = lambda_max * phi, :940)

@@ -412,6 +412,36 @@ def test_precondition_worked_examples():
     assert abs(le - 0.5) < 1e-15          # phi=0.1, max D = 5 -> 0.5
 
 
+# ---------------------------------------------------------------- light correction (Alg 6)
+
+def test_light_correction_pins():
+    """Algorithm 6 and its footnote (:683): after correcting the modes
+    col_idx, the error E = Mcal - U D U^T has U_c^T E U_c = 0 on the chosen subspace, so
+    ||E||_F cannot increase; U stays orthonormal; correcting every mode of a factor whose
+    Mcal lives in span(U) recovers Mcal exactly."""
+    rng = np.random.default_rng(303)
+    n, r, ncrc = 40, 10, 4
+    X = rng.standard_normal((n, 25))
+    Mcal = X @ X.T
+    U, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    D = np.sort(rng.random(r))[::-1] * 50
+    idx = rng.choice(r, ncrc, replace=False)
+    Uc0 = U[:, idx]
+    U2, D2 = O.light_correction(U, D, Mcal, idx)
+    E0 = Mcal - O.densify(U, D)
+    E1 = Mcal - O.densify(U2, D2)
+    assert np.abs(Uc0.T @ E1 @ Uc0).max() < 1e-10 * np.abs(Mcal).max()
+    assert np.linalg.norm(E1) <= np.linalg.norm(E0) + 1e-9
+    assert np.abs(U2.T @ U2 - np.eye(r)).max() < 1e-12
+    others = np.setdiff1d(np.arange(r), idx)
+    assert np.array_equal(U2[:, others], U[:, others]) and np.array_equal(D2[others], D[others])
+    # full correction of an Mcal inside span(U): exact
+    W = U @ rng.standard_normal((r, r))
+    M2 = W @ W.T
+    U3, D3 = O.light_correction(U, np.zeros(r), M2, np.arange(r))
+    assert np.abs(O.densify(U3, D3) - M2).max() < 1e-10 * np.abs(M2).max()
+
+
 # ---------------------------------------------------------------- B-R-KFAC chain
 
 def test_brkfac_chain_overwrite_equals_rsvd_then_brand():
