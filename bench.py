@@ -53,6 +53,9 @@ def parse_args():
                     help="NEXT-f1: keep all r + c eigenpairs per step and precondition with them")
     ap.add_argument("--factored", action="store_true",
                     help="NEXT-f2: precondition from the factored gradient G A^T (Algorithm 8)")
+    ap.add_argument("--correct-every", type=int, default=0,
+                    help="NEXT-f3 (B-KFAC-C): light correction (Alg 6) every T steps")
+    ap.add_argument("--phi-crc", type=float, default=0.5, help="n_crc / r of the light correction")
     ap.add_argument("--no-graphs", action="store_true",
                     help="launch every step eagerly instead of replaying CUDA graphs")
     return ap.parse_args()
@@ -337,7 +340,9 @@ def run_reference(args, rank, world):
             "ms_per_step": round(1e3 * t_total / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name + ("+f1_full_rank" if args.full_rank else "")
-                                   + ("+f2_factored" if args.factored else ""),
+                                   + ("+f2_factored" if args.factored else "")
+                                   + (f"+f3_correct{args.correct_every}_phi{args.phi_crc:g}"
+                                      if args.correct_every else ""),
                        "factors": n_f, "layers": n_l,
                        "sample": "one layer (2 factor updates + preconditioning) per step"},
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores,
@@ -359,7 +364,8 @@ def run_ours(args, rank, world, local_rank):
     layers = [(l.d_G, l.d_A, l.g_index, l.a_index) for l in cfg.layers]
     stack = BKFACStack(factors, layers, cfg.rho, cfg.lam, rsvd_every=cfg.rsvd_every,
                        oversample=cfg.oversample, power_iters=cfg.power_iters,
-                       device=local_rank, rank=rank, world=world, full_rank=args.full_rank)
+                       device=local_rank, rank=rank, world=world, full_rank=args.full_rank,
+                       correct_every=args.correct_every, phi_crc=args.phi_crc)
     gather = SlotGather(layers, stack.owned_layers_all, rank, device) if world > 1 and layers else None
     M_pool, J_pool = device_inputs(cfg, stack.my_factors, stack.my_layers, args.pool, device)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device)
@@ -455,7 +461,9 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "layers_per_s": round(layers_per_s, 3),
             "config": {"workload": cfg.name + ("+f1_full_rank" if args.full_rank else "")
-                                   + ("+f2_factored" if args.factored else ""),
+                                   + ("+f2_factored" if args.factored else "")
+                                   + (f"+f3_correct{args.correct_every}_phi{args.phi_crc:g}"
+                                      if args.correct_every else ""),
                        "factors": n_f, "layers": n_l,
                        "n_BS": cfg.factors[0].c, "rho": cfg.rho, "lambda": cfg.lam,
                        "rsvd_every": cfg.rsvd_every, "parallelism": f"layer-shard x{world}",

@@ -150,6 +150,20 @@ typedef struct {
 bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* args, int count,
                                         void* stream);
 
+/* NEXT-f3, Algorithm 6, the light correction of B-KFAC-C (Alg 7,
+ * :691-701): for the n_crc modes col_idx[0..n_crc) (distinct, in [0, r); the random choice
+ * of line 2, drawn by the caller), M_S = U_c^T K_dense U_c with U_c = U[:, col_idx];
+ * U_S D_S U_S^T = EVD(M_S); U[:, col_idx] <- U_c U_S, D[col_idx] <- max(D_S, 0).  U (n x r
+ * col-major; a full-rank factor's leading r columns) and D are updated in place; other
+ * columns are untouched and U stays orthonormal.  col_idx is a device int32 array; an
+ * index outside [0, r) sets the factor's status (BKFAC_ERR_NUMERIC from bkfac_check).
+ * Requires BKFAC_FACTOR_DENSE_EA; 1 <= n_crc <= r. */
+typedef struct {
+  int factor; const float* K_dense; float* U; float* D; const int* col_idx; int n_crc;
+} bkfac_correct_args;
+bkfac_status bkfac_light_correction(bkfac_ctx ctx, const bkfac_correct_args* args, int count,
+                                    void* stream);
+
 /* Omega (n x l col-major) <- the RSVD Gaussian test matrix for (seed, counter): the
  * sketch step of bkfac_rsvd_overwrite exposed on its own (Philox4x32-10, key = seed,
  * counter words (e/4 lo, e/4 hi, counter lo, counter hi) for element e = j*n + i;

@@ -31,7 +31,7 @@ STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKF
 EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac_destroy",
             "bkfac_brand_update", "bkfac_brand_ea_update", "bkfac_ea_accumulate", "bkfac_ea_accumulate_batch",
             "bkfac_rsvd_overwrite", "bkfac_rsvd_overwrite_batch",
-            "bkfac_precondition", "bkfac_precondition_factored", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
+            "bkfac_precondition", "bkfac_precondition_factored", "bkfac_light_correction", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
             "bkfac_profile_enable", "bkfac_profile_read", "bkfac_status_string",
             "bkfac_build_info", "bkfac_gemm"]
 
@@ -74,6 +74,11 @@ class StageStat(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("calls", ctypes.c_longlong),
                 ("launches", ctypes.c_longlong), ("ms", ctypes.c_double),
                 ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+class CorrectArgs(ctypes.Structure):
+    _fields_ = [("factor", ctypes.c_int), ("K_dense", ctypes.c_void_p), ("U", ctypes.c_void_p),
+                ("D", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("n_crc", ctypes.c_int)]
 
 
 class PrecondFactoredArgs(ctypes.Structure):
@@ -132,6 +137,8 @@ def load(path: str = None) -> ctypes.CDLL:
     lib.bkfac_precondition.restype = ci
     lib.bkfac_precondition_factored.argtypes = [vp, ctypes.POINTER(PrecondFactoredArgs), ci, vp]
     lib.bkfac_precondition_factored.restype = ci
+    lib.bkfac_light_correction.argtypes = [vp, ctypes.POINTER(CorrectArgs), ci, vp]
+    lib.bkfac_light_correction.restype = ci
     lib.bkfac_check.argtypes = [vp, vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
     lib.bkfac_check.restype = ci
     lib.bkfac_launch_count.argtypes = [vp]
@@ -163,6 +170,14 @@ def _ptr(t) -> Optional[int]:
         raise TypeError("expected a torch.Tensor")
     if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
         raise ValueError("bkfac expects contiguous float32 CUDA tensors")
+    return t.data_ptr()
+
+
+def _iptr(t) -> Optional[int]:
+    """Device pointer of a contiguous int32 CUDA tensor (index arrays)."""
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError("bkfac expects a contiguous int32 CUDA tensor of indices")
     return t.data_ptr()
 
 
@@ -284,6 +299,15 @@ class Context:
                                          _ptr(a["S"]), int(a.get("flags", 0)))
         _check(self.lib.bkfac_precondition_factored(self.h, arr, len(items), _stream_ptr(stream)),
                "bkfac_precondition_factored")
+
+    def bkfac_light_correction(self, items: List[dict], stream=None) -> None:
+        """Algorithm 6: dict(factor, K, U, D, col_idx (int32 device tensor of n_crc indices))."""
+        arr = (CorrectArgs * len(items))()
+        for i, a in enumerate(items):
+            arr[i] = CorrectArgs(a["factor"], _ptr(a["K"]), _ptr(a["U"]), _ptr(a["D"]),
+                                 _iptr(a["col_idx"]), int(a["col_idx"].numel()))
+        _check(self.lib.bkfac_light_correction(self.h, arr, len(items), _stream_ptr(stream)),
+               "bkfac_light_correction")
 
     def bkfac_check(self, stream=None):
         bad = ctypes.c_int(-1)

@@ -1182,6 +1182,101 @@ bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, 
   return r;
 }
 
+// ------------------------------------------------------------------------- light correction
+// Algorithm 6 on the RSVD scratch of the factor (the two never run in the same call):
+// Yr <- U_c (gather), Qr <- K U_c, eig_r.K <- U_c^T K U_c (split-K), EVD (eig_r, all n_crc pairs,
+// vectors into Br, values into Tr), Q2r <- U_c V, scatter into U and D.
+bkfac_status bkfac_light_correction(bkfac_ctx ctx, const bkfac_correct_args* args, int count,
+                                    void* stream) {
+  if (!ctx || count < 0 || (count > 0 && !args)) return BKFAC_ERR_INVALID_ARG;
+  if (!ctx->ws) return BKFAC_ERR_WORKSPACE;
+  for (int i = 0; i < count; ++i) {
+    const auto& a = args[i];
+    if (a.factor < 0 || a.factor >= (int)ctx->f.size()) return BKFAC_ERR_INVALID_ARG;
+    const auto& fp = ctx->f[a.factor];
+    if (!fp.rsvd) return BKFAC_ERR_INVALID_ARG;
+    if (!a.K_dense || !a.U || !a.D || !a.col_idx) return BKFAC_ERR_INVALID_ARG;
+    if (a.n_crc < 1 || a.n_crc > fp.d.r) return BKFAC_ERR_DIM;
+    for (int j = 0; j < i; ++j)
+      if (args[j].factor == a.factor) return BKFAC_ERR_INVALID_ARG;
+  }
+  if (count == 0) return BKFAC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev_prev = 0;
+  cudaGetDevice(&dev_prev);
+  if (dev_prev != ctx->device) cudaSetDevice(ctx->device);
+  bkfac_status rs = BKFAC_OK;
+  GemmStage gs;
+  std::vector<EigProb> eg;
+  static ColIdxBatch cb;
+  auto colidx = [&](int mode, const char* tag) -> bkfac_status {
+    prof_begin(ctx, tag, st, 0.0, 0.0);
+    for (int i0 = 0; i0 < count; i0 += NF_MAXP) {
+      const int nb = std::min(count - i0, NF_MAXP);
+      cb.nprob = nb;
+      for (int k = 0; k < nb; ++k) {
+        const auto& a = args[i0 + k];
+        const auto& fp = ctx->f[a.factor];
+        const int n = fp.d.n;
+        ColIdxProb q{};
+        q.rows = n; q.idx = a.col_idx; q.n = a.n_crc; q.r = fp.d.r; q.mode = mode;
+        q.status = status_ptr(ctx, a.factor);
+        if (mode == 0) { q.src = a.U; q.lds = n; q.dst = at<float>(ctx, fp.Yr); q.ldd = n; }
+        else {
+          q.src = at<float>(ctx, fp.Q2r); q.lds = n; q.dst = a.U; q.ldd = n;
+          q.dsrc = at<float>(ctx, fp.Tr); q.ddst = a.D;
+        }
+        cb.p[k] = q;
+      }
+      colidx_kernel<<<dim3(64, (unsigned)nb), 256, 0, st>>>(cb);
+      LAUNCH_CHECK(ctx);
+    }
+    prof_end(ctx, st);
+    return BKFAC_OK;
+  };
+#define STAGE(x) do { if ((rs = (x)) != BKFAC_OK) goto done; } while (0)
+  STAGE(colidx(0, "crc_gather"));
+  for (int i = 0; i < count; ++i) {   // Y = K U_c
+    const auto& a = args[i];
+    const auto& fp = ctx->f[a.factor];
+    const int n = fp.d.n;
+    GemmProb p = gp(a.K_dense, n, at<float>(ctx, fp.Yr), n, at<float>(ctx, fp.Qr), n, n, a.n_crc, n, 1.f);
+    p.status = status_ptr(ctx, a.factor);
+    gs.add(false, false, p, 0);
+  }
+  STAGE(run_gemms(ctx, gs, st, "gemm_crc_mul"));
+  for (int i = 0; i < count; ++i) {   // M_S = U_c^T Y
+    const auto& a = args[i];
+    const auto& fp = ctx->f[a.factor];
+    const int n = fp.d.n;
+    GemmProb p = gp(at<float>(ctx, fp.Yr), n, at<float>(ctx, fp.Qr), n, at<float>(ctx, fp.eig_r.K),
+                    a.n_crc, a.n_crc, a.n_crc, n, 1.f);   // straight into the eigensolver's input
+    gemm_ws(p, at<float>(ctx, fp.ws_r));
+    gs.add(true, false, p, fp.ws_r_elems);
+  }
+  STAGE(run_gemms(ctx, gs, st, "gemm_crc_proj"));
+  for (int i = 0; i < count; ++i) {   // EVD(M_S): all n_crc pairs (vectors into Br, values into Tr)
+    const auto& a = args[i];
+    const auto& fp = ctx->f[a.factor];
+    eg.push_back(eig_prob(ctx, fp.eig_r, a.n_crc, a.n_crc, at<float>(ctx, fp.Br), a.n_crc,
+                          at<float>(ctx, fp.Tr), status_ptr(ctx, a.factor)));
+  }
+  STAGE(run_eig(ctx, eg, st));
+  for (int i = 0; i < count; ++i) {   // U_c V
+    const auto& a = args[i];
+    const auto& fp = ctx->f[a.factor];
+    const int n = fp.d.n;
+    gs.add(false, false, gp(at<float>(ctx, fp.Yr), n, at<float>(ctx, fp.Br), a.n_crc,
+                            at<float>(ctx, fp.Q2r), n, n, a.n_crc, a.n_crc, 1.f), 0);
+  }
+  STAGE(run_gemms(ctx, gs, st, "gemm_crc_rot"));
+  STAGE(colidx(1, "crc_scatter"));
+done:
+#undef STAGE
+  if (dev_prev != ctx->device) cudaSetDevice(dev_prev);
+  return rs;
+}
+
 // ------------------------------------------------------------------------- RSVD
 bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* args, int count,
                                         void* stream) {

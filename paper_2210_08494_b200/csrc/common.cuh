@@ -12,6 +12,7 @@ enum : int {
   ST_CHOL_DROP = 1,        // info: a Cholesky pivot was dropped (rank-deficient residual)
   ST_NONFINITE = 1 << 8,   // error: NaN/Inf seen in the eigensolver input
   ST_EIG_FAIL = 1 << 9,    // error: eigensolver did not converge / produced non-finite
+  ST_BAD_INDEX = 1 << 10,  // error: a light-correction column index outside [0, r)
   ST_ERROR_MASK = 0xff00,
 };
 

@@ -59,6 +59,34 @@ __global__ void nonfinite_kernel(const __grid_constant__ NfBatch b) {
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(p.status, ST_NONFINITE);
 }
 
+// ---- column gather / scatter by an index array (light correction, Algorithm 6) ------------
+//   mode 0: dst(:, j) = src(:, idx[j])                      j < n
+//   mode 1: dst(:, idx[j]) = src(:, j), ddst[idx[j]] = dsrc[j]
+// An index outside [0, r) is skipped and reported (ST_BAD_INDEX).
+struct ColIdxProb {
+  const float* src; int lds; float* dst; int ldd; int rows;
+  const int* idx; int n; int r; int mode;
+  const float* dsrc; float* ddst; int* status;
+};
+struct ColIdxBatch { int nprob; ColIdxProb p[NF_MAXP]; };
+__global__ void colidx_kernel(const __grid_constant__ ColIdxBatch b) {
+  const ColIdxProb& p = b.p[blockIdx.y];
+  const long total = (long)p.rows * p.n;
+  int bad = 0;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / p.rows), i = (int)(e % p.rows);
+    const int c = p.idx[j];
+    if (c < 0 || c >= p.r) { bad = 1; continue; }
+    if (p.mode == 0) {
+      p.dst[i + (long)j * p.ldd] = p.src[i + (long)c * p.lds];
+    } else {
+      p.dst[i + (long)c * p.ldd] = p.src[i + (long)j * p.lds];
+      if (i == 0 && p.ddst) p.ddst[c] = p.dsrc[j];
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && p.status) atomicOr(p.status, ST_BAD_INDEX);
+}
+
 // ---- preconditioner scalars (Alg 1 lines 16-17) ---------------------
 // One CTA per layer.  For each side: effective lambda (relative mode :940, continuation
 // :711) and s_i = (D_i + lambda)^{-1} - 1/lambda; then the coefficient of J in S,

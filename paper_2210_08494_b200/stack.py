@@ -45,7 +45,8 @@ class BKFACStack:
                  rho: float, lam: float, rsvd_every: int = 0, oversample: int = 10,
                  power_iters: int = 2, precond_flags: int = 0, brand_flags: int = 0,
                  device: int = 0, rank: int = 0, world: int = 1, rsvd_seed: int = 20221015,
-                 full_rank: bool = False):
+                 full_rank: bool = False, correct_every: int = 0, phi_crc: float = 0.5,
+                 correct_seed: int = 20221016):
         """factors: (n, r, c_max) per global factor; layers: (d_G, d_A, g_index, a_index).
 
         full_rank=True is the paper's own preconditioner (NEXT-f1, PAPER.md:533-534,
@@ -74,6 +75,11 @@ class BKFACStack:
         self.my_factors = sorted(owned_f)
         self.local = {g: i for i, g in enumerate(self.my_factors)}
         self.full_rank = full_rank
+        # B-KFAC-C (NEXT-f3, Alg 7 :691-701): every correct_every steps, Algorithm 6 on
+        # n_crc = max(1, round(phi_crc r)) random modes of every factor against the dense EA
+        self.correct_every, self.phi_crc, self.correct_seed = correct_every, phi_crc, correct_seed
+        if correct_every and not rsvd_every:
+            raise ValueError("the light correction needs the dense EA factor (rsvd_every > 0)")
         flags = (binding.BKFAC_FACTOR_DENSE_EA if rsvd_every > 0 else 0) | \
                 (binding.BKFAC_FACTOR_FULL_RANK if full_rank else 0)
         fdesc = [(self.factors[g][0], self.factors[g][1], self.factors[g][2], flags)
@@ -142,7 +148,9 @@ class BKFACStack:
         PAPER.md:882-930) from the factored gradient Mat(g) = G A^T with G = M[Gamma factor],
         A = M[A factor] (the same per-sample matrices as the statistics); J is not used."""
         torch = self.torch
-        if graph and self.k > 0 and not (self.rsvd_every and self.k % self.rsvd_every == 0):
+        eager = (self.rsvd_every and self.k % self.rsvd_every == 0) or \
+                (self.correct_every and self.k % self.correct_every == 0)
+        if graph and self.k > 0 and not eager:
             key = (self.cur[0] if self.cur else 0,
                    tuple(M[g].data_ptr() for g in self.my_factors),
                    tuple(J[li].data_ptr() for li in self.my_layers) if J is not None else None,
@@ -204,6 +212,21 @@ class BKFACStack:
             self.ctx.bkfac_brand_update(ups, main)
         for i in range(len(self.my_factors)):
             self.cur[i] = 1 - self.cur[i]
+        if self.correct_every and k > 0 and k % self.correct_every == 0:
+            # Alg 7: after this step's Brand update and EA accumulate, correct the
+            # representation against Mcal_k (Algorithm 6); the random modes are drawn here
+            # (seeded per factor and step) and passed to the library
+            gen = torch.Generator(device="cpu")
+            items = []
+            for i, g in enumerate(self.my_factors):
+                r = self.factors[g][1]
+                ncrc = max(1, min(r, int(round(self.phi_crc * r))))
+                gen.manual_seed(self.correct_seed * 1000003 + g * 7919 + k)
+                idx = torch.randperm(r, generator=gen)[:ncrc].to(torch.int32).to(f"cuda:{self.device}")
+                U, D = self.U[i][self.cur[i]], self.D[i][self.cur[i]]
+                items.append(dict(factor=i, K=self.K[i], U=U, D=D, col_idx=idx))
+            self.ctx.bkfac_light_correction(items, main)
+            self._crc_keep = items          # index tensors live until the stream is past them
         out = {}
         if factored and self.my_layers:
             items = []

@@ -535,3 +535,77 @@ def test_stack_factored_equals_dense_gradient(cuda_lib):
     a, b = Sf.double().cpu().numpy(), Sj.double().cpu().numpy()
     assert np.linalg.norm(a - b) / np.linalg.norm(b) < TOL_PREC
     assert st_f.check()[0] == 0
+
+
+# ------------------------------------------------------------------ NEXT-f3: light correction
+
+@pytest.mark.parametrize("shape", [(700, 64, 32, 32), (577, 220, 256, 110), (300, 40, 16, 40)])
+def test_light_correction_alg6(cuda_lib, shape):
+    """bkfac_light_correction (Algorithm 6) vs the oracle with the same
+    random modes: reconstruction of the corrected representation, untouched columns
+    bitwise, orthonormal U, and the footnote's identity U_c^T (Mcal - U D U^T) U_c = 0."""
+    import torch
+    n, r, c, ncrc = shape
+    rng = np.random.default_rng(n + r + ncrc)
+    X = rng.standard_normal((n, 3 * r)) * np.linspace(1, 0.05, 3 * r)[None, :]
+    Mcal = (X @ X.T).astype(np.float32).astype(np.float64)
+    U, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    U = U.astype(np.float32).astype(np.float64)
+    D = (np.sort(rng.random(r))[::-1] * 10).astype(np.float32).astype(np.float64)
+    idx = rng.choice(r, ncrc, replace=False)
+    ctx = _ctx([(n, r, c, 1)])
+    tU, tD, tK = to_dev_cols(U), to_dev(D), to_dev(Mcal)
+    tI = torch.from_numpy(idx.astype(np.int32)).cuda()
+    ctx.bkfac_light_correction([dict(factor=0, K=tK, U=tU, D=tD, col_idx=tI)])
+    torch.cuda.synchronize()
+    Ug, Dg = from_dev_cols(tU), tD.double().cpu().numpy()
+    Uo, Do = O.light_correction(U, D, Mcal, idx)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    others = np.setdiff1d(np.arange(r), idx)
+    assert np.array_equal(Ug[:, others], U[:, others].astype(np.float32).astype(np.float64))
+    assert _orth_check(Ug)
+    Uc = U[:, idx]
+    E = Mcal - O.densify(Ug, Dg)
+    assert np.abs(Uc.T @ E @ Uc).max() < 1e-5 * np.abs(Mcal).max()
+    assert ctx.bkfac_check()[0] == 0
+
+
+def test_light_correction_bad_index_reported(cuda_lib):
+    import torch
+    n, r = 100, 16
+    ctx = _ctx([(n, r, 8, 1)])
+    U = to_dev_cols(synth.phantom_basis(n, r))
+    D = torch.ones(r, device="cuda")
+    K = torch.eye(n, device="cuda")
+    ctx.bkfac_light_correction([dict(factor=0, K=K, U=U, D=D,
+                                     col_idx=torch.tensor([0, 99], dtype=torch.int32, device="cuda"))])
+    code, bad, info = ctx.bkfac_check()
+    assert code != 0 and bad == 0
+
+
+def test_bkfac_c_stack_chain(cuda_lib):
+    """B-KFAC-C (Alg 7): stack with a correction every 2 steps vs the oracle chain (Brand,
+    EA accumulate, Algorithm 6 on the same seeded modes) over 5 steps."""
+    import torch
+    from paper_2210_08494_b200 import BKFACStack
+    n, r, c, rho = 400, 48, 32, 0.95
+    st = BKFACStack([(n, r, c)], [], rho, 0.1, rsvd_every=100, correct_every=2, phi_crc=0.5)
+    f = synth.random_case(n, c, r, seed=515, k=40, decay=0.93)
+    U, D, Mcal = None, None, None
+    for k in range(5):
+        M = f.batch(k).astype(np.float32).astype(np.float64)
+        st.step({0: to_dev_cols(M)})
+        Mcal = O.ea_update(Mcal, M, rho)
+        if k == 0:
+            U, D = O.brand_update(synth.phantom_basis(n, r), np.zeros(r), M, 0.0, 1.0, r)
+        else:
+            U, D = O.brand_update(U, D, M, rho, 1 - rho, r)
+        if k > 0 and k % 2 == 0:
+            gen = torch.Generator(device="cpu")
+            gen.manual_seed(st.correct_seed * 1000003 + 0 * 7919 + k)
+            idx = torch.randperm(r, generator=gen)[: int(round(0.5 * r))].numpy()
+            U, D = O.light_correction(U, D, Mcal, idx)
+    torch.cuda.synchronize()
+    Ug, Dg = st.state(0)
+    assert lowrank_rel_err(U, D, from_dev_cols(Ug), Dg.double().cpu().numpy()) < TOL_CHAIN
+    assert st.check()[0] == 0
