@@ -117,6 +117,7 @@ struct bkfac_ctx_s {
   cudaEvent_t ev_ea_fork = nullptr, ev_ea_done = nullptr;
   std::function<bkfac_status(int)> pending_ea;
   int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs
+  int pair_mode = 1;  // CTA-pair GEMM tiles: 0 never, 1 large long-K stages, 2 always (tests)
   // optional per-stage CUDA-event profiling (bkfac_profile_enable)
   bool prof = false;
   struct Rec { std::string tag; cudaEvent_t a, b; double flops, bytes; uint64_t launches; };
@@ -202,7 +203,8 @@ GemmProb gp(const float* A, int lda, const float* B, int ldb, float* C, int ldc,
 }
 
 template <bool TA, bool TB>
-bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_t st, bool tc) {
+bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_t st, bool tc,
+                            bool pair) {
   size_t i0 = 0;
   while (i0 < v.size()) {
     const size_t n = std::min(v.size() - i0, (size_t)GEMM_MAXP);
@@ -224,8 +226,10 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
     b.total_tiles = tiles;
     if (tiles > 0) {
       if (tc) {
-        const int grid = std::min(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM);
-        tc_launch<TA, TB>(b, grid, st, max_chunks <= TC_SHORT_K_CHUNKS);
+        const int nsm = ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM;
+        const int grid = std::min(tiles, pair ? nsm / 2 : nsm);   // pair: CTA pairs
+        if (!cuda_ok(tc_launch<TA, TB>(b, grid, st, max_chunks <= TC_SHORT_K_CHUNKS, pair)))
+          return BKFAC_ERR_CUDA;
       } else {
         gemm_simt_kernel<TA, TB><<<tiles, 256, 0, st>>>(b);
       }
@@ -260,7 +264,23 @@ bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char*
 // machine has SMs (x2 for SIMT); the reduction order is fixed (deterministic).
 bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
   const bool tc = ctx->use_tc && !s.fp32_simt;
-  const int bm = tc ? TC_BM : SG_BM, bn = tc ? TC_BN : SG_BN;
+  // CTA-pair tiles (256 x 128, tcgen05 cta_group::2) for stages with enough long-K work to
+  // fill the machine with pairs; symmetric (mirrored) and short-K stages keep 128 x 128
+  bool pair = false;
+  if (tc && ctx->pair_mode != 0) {
+    long pair_tiles = 0, max_nc = 0;
+    bool any_sym = false;
+    for (int v = 0; v < 4; ++v)
+      for (auto& p : s.probs[v]) {
+        any_sym |= p.sym != 0;
+        if (p.M <= 0 || p.N <= 0) continue;
+        pair_tiles += (long)ceil_div(p.M, 2 * TC_BM) * ceil_div(p.N, TC_BN);
+        max_nc = std::max<long>(max_nc, ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK));
+      }
+    pair = !any_sym && (ctx->pair_mode == 2 ||
+                        (max_nc > TC_SHORT_K_CHUNKS && pair_tiles >= kNumSM / 2));
+  }
+  const int bm = tc ? (pair ? 2 * TC_BM : TC_BM) : SG_BM, bn = tc ? TC_BN : SG_BN;
   long base_tiles = 0;
   for (int v = 0; v < 4; ++v)
     for (auto& p : s.probs[v]) {
@@ -276,7 +296,7 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       }
       base_tiles += p.sym ? (long)p.tiles_m * (p.tiles_m + 1) / 2 : (long)p.tiles_m * p.tiles_n;
     }
-  const long nsm = ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM;
+  const long nsm = (ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM) / (pair ? 2 : 1);
   const long target = tc ? nsm : 2L * nsm;
   // tcgen05: balance the stage's K-chunk work over the persistent CTAs -- every work item
   // (tile x split) gets at most `quota` chunks, so one long-K problem no longer sets the
@@ -326,10 +346,10 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       p.kchunk = std::max(kchunk, 1);
     }
   bkfac_status r;
-  if ((r = launch_variant<false, false>(ctx, s.probs[0], st, tc)) != BKFAC_OK) return r;
-  if ((r = launch_variant<false, true>(ctx, s.probs[1], st, tc)) != BKFAC_OK) return r;
-  if ((r = launch_variant<true, false>(ctx, s.probs[2], st, tc)) != BKFAC_OK) return r;
-  if ((r = launch_variant<true, true>(ctx, s.probs[3], st, tc)) != BKFAC_OK) return r;
+  if ((r = launch_variant<false, false>(ctx, s.probs[0], st, tc, pair)) != BKFAC_OK) return r;
+  if ((r = launch_variant<false, true>(ctx, s.probs[1], st, tc, pair)) != BKFAC_OK) return r;
+  if ((r = launch_variant<true, false>(ctx, s.probs[2], st, tc, pair)) != BKFAC_OK) return r;
+  if ((r = launch_variant<true, true>(ctx, s.probs[3], st, tc, pair)) != BKFAC_OK) return r;
   for (int v = 0; v < 4; ++v) { s.probs[v].clear(); s.caps[v].clear(); }
   s.fp32_simt = false;
   return BKFAC_OK;
@@ -737,6 +757,8 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   cudaSetDevice(dev_prev);
   const char* env = getenv("BKFAC_GEMM");
   c->use_tc = !(env && strcmp(env, "simt") == 0);
+  const char* penv = getenv("BKFAC_GEMM_PAIR");   // tuning / tests: 0 off, 2 force
+  if (penv) c->pair_mode = atoi(penv);
   *out = c;
   return BKFAC_OK;
 }
@@ -1657,6 +1679,7 @@ bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha
   if (M == 0 || N == 0) return BKFAC_OK;
   bkfac_ctx_s tmp;   // launch bookkeeping only; no workspace
   tmp.use_tc = path == BKFAC_GEMM_TCGEN05;
+  if (const char* penv = getenv("BKFAC_GEMM_PAIR")) tmp.pair_mode = atoi(penv);
   if (tmp.use_tc) {
     static bool attrs = false;
     if (!attrs) { attrs = tc_init_attributes(); cudaGetLastError(); }

@@ -78,21 +78,27 @@ constexpr int TC_MMA_WARP = 4;
 constexpr int TC_PROMO = BKFAC_TC_PROMO;   // K chunks accumulated in TMEM before promotion
 
 // NLW loader warps, each keeping DEPTH chunks of loads in flight ahead of its stores.
-template <int BN, int NLW = 16, int DEPTH = 2, int EPI = 4>
+// PAIR: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes a 256 x BN tile: each CTA
+// stages its own 128 rows of A and BN/2 rows of B, the leader issues M = 256 MMAs that read
+// both CTAs' shared memory, and each CTA's TMEM holds its 128 rows of the accumulator.
+// Per SM per chunk: 1/4 fewer loads and stores, B operand reads halved.
+template <int BN, int NLW = 16, int DEPTH = 2, int EPI = 4, bool PAIR = false>
 struct TcCfg {
   static constexpr int LOAD_WARPS = NLW;
   static constexpr int EPI_WARPS = EPI;
   static constexpr int THREADS = (EPI + 1 + NLW) * 32;
+  static constexpr int BM_T = PAIR ? 2 * TC_BM : TC_BM;     // tile rows (both CTAs)
+  static constexpr int B_ROWS = PAIR ? BN / 2 : BN;          // B rows staged by this CTA
   static constexpr int A_BYTES = TC_BM * TC_BK * 4;          // one half (hi or lo)
-  static constexpr int B_BYTES = BN * TC_BK * 4;
+  static constexpr int B_BYTES = B_ROWS * TC_BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
 #ifdef BKFAC_TC_STAGES
   static constexpr int STAGES = BKFAC_TC_STAGES;
 #else
-  static constexpr int STAGES = (BN >= 256) ? 2 : 3;
+  static constexpr int STAGES = PAIR ? 4 : ((BN >= 256) ? 2 : 3);
 #endif
   static constexpr int TMEM_COLS = 4 * BN;                   // 2 K-block buffers + running sum
-  static constexpr int LINES = TC_BM + BN;                   // 128-byte lines per stage half
+  static constexpr int LINES = TC_BM + B_ROWS;               // 128-byte lines per stage half
   static constexpr int LPW = LINES / NLW;                    // lines per loader warp
   // + per-epilogue-warp 16 x 34 staging for the transposed (mirror) stores of symmetric tiles
   static constexpr int EPI_STAGE_FLOATS = 16 * 34;
@@ -140,6 +146,43 @@ BKFAC_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync
 BKFAC_DEV void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
+}
+BKFAC_DEV void tc_commit2(uint32_t bar) {   // both CTAs of the pair (same smem offset)
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+      ::"r"(bar), "h"((uint16_t)3) : "memory");
+}
+BKFAC_DEV void tc_mma2_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on the mbarrier at the same offset in CTA `rank` of the cluster (release.cluster)
+BKFAC_DEV void mbar_arrive_remote(uint32_t bar, uint32_t rank) {
+  uint32_t rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+}
+BKFAC_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+BKFAC_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+BKFAC_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
 BKFAC_DEV void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                            uint32_t accumulate) {
@@ -229,11 +272,11 @@ BKFAC_DEV uint64_t tc_op_desc(uint32_t saddr, int ks) {
   return umma_desc(saddr + ks * 2u * (R / 32 * 512), 512u, R / 32 * 512, 1u);
 }
 // Instruction descriptor: kind::tf32, fp32 accumulate, M = 128, N = BN.
-template <int BN>
+template <int BN, int BMM = TC_BM>
 BKFAC_DEV constexpr uint32_t umma_idesc_tf32(bool a_mn_major, bool b_mn_major) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn_major ? 1u : 0u) << 15) |
          ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-         ((uint32_t)(TC_BM >> 4) << 24);
+         ((uint32_t)(BMM >> 4) << 24);
 }
 
 // ----------------------------------------------------------------------- tile walk
@@ -250,7 +293,7 @@ BKFAC_DEV int tc_find_prob(const GemmBatch& b, int t) {
   return lo;
 }
 
-template <int BN>
+template <int BN, int BMT = TC_BM>
 BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
   TcTile x;
   x.pi = tc_find_prob(b, t);
@@ -263,10 +306,10 @@ BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
     int tm = (int)((sqrtf(8.f * rem + 1.f) - 1.f) * 0.5f);
     while (tm * (tm + 1) / 2 > rem) --tm;
     while ((tm + 1) * (tm + 2) / 2 <= rem) ++tm;
-    x.m0 = tm * TC_BM;
+    x.m0 = tm * BMT;
     x.n0 = (rem - tm * (tm + 1) / 2) * BN;
   } else {
-    x.m0 = (rem % p.tiles_m) * TC_BM;
+    x.m0 = (rem % p.tiles_m) * BMT;
     x.n0 = (rem / p.tiles_m) * BN;
   }
   x.nc1 = (p.k1 + TC_BK - 1) / TC_BK;
@@ -281,10 +324,14 @@ __device__ unsigned long long g_tc_dbg[148 * 8];   // tuning builds: per-CTA MMA
 #endif
 // Epilogue warps 0-3 (thread = tile row = TMEM lane): promote each K-block accumulator
 // into the running sum (TMEM), then alpha/beta and coalesced stores of the tile.
-template <int BN, int EPI>
+template <int BN, int EPI, bool PAIR>
 BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int lane,
                            uint32_t tfull0, uint32_t tfull1, uint32_t tempty0, uint32_t tempty1,
                            float* stage) {
+  constexpr int BMT = PAIR ? 2 * TC_BM : TC_BM;
+  const uint32_t crank = PAIR ? cluster_rank() : 0u;
+  const int tstride = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const int tfirst = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
   auto tfull_bar = [&](int a) { return a ? tfull1 : tfull0; };
   auto tempty_bar = [&](int a) { return a ? tempty1 : tempty0; };
     const int quarter = warp & 3;                             // TMEM lanes this warp may access
@@ -295,8 +342,9 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
     constexpr int NG = BN / 16, GPW = NG * 4 / EPI;
     const int g_beg = (warp < 4 ? 0 : 1) * GPW;
     int kb = 0;
-    for (int t = blockIdx.x; t < b.total_tiles; t += gridDim.x) {
-      const TcTile x = tc_tile<BN>(b, t);
+    for (int t = tfirst; t < b.total_tiles; t += tstride) {
+      TcTile x = tc_tile<BN, BMT>(b, t);
+      x.m0 += (int)crank * TC_BM;                              // this CTA's 128 rows
       const GemmProb& p = b.p[x.pi];
       const int nblk = (x.c_end - x.c_beg + TC_PROMO - 1) / TC_PROMO;
       const int i = x.m0 + row;
@@ -374,7 +422,10 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
         if (!last) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty_bar(buf));
+        if (lane == 0) {
+          if (PAIR && crank != 0) mbar_arrive_remote(tempty_bar(buf), 0);   // the leader's
+          else mbar_arrive(tempty_bar(buf));
+        }
       }
       if (p.status && __any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(p.status, ST_NONFINITE);
       if (nblk == 0 && i < p.M) {     // empty K range (split beyond K or K = 0)
@@ -392,69 +443,85 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
   }
 
 // ----------------------------------------------------------------------- kernel
-template <bool TA, bool TB, int BN, int NLW, int DEPTH, int EPI>
-__global__ void __launch_bounds__(TcCfg<BN, NLW, DEPTH, EPI>::THREADS, 1)
+template <bool TA, bool TB, int BN, int NLW, int DEPTH, int EPI, bool PAIR>
+__global__ void __launch_bounds__(TcCfg<BN, NLW, DEPTH, EPI, PAIR>::THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
-  using Cfg = TcCfg<BN, NLW, DEPTH, EPI>;
+  using Cfg = TcCfg<BN, NLW, DEPTH, EPI, PAIR>;
+  constexpr int BMT = Cfg::BM_T, B_ROWS = Cfg::B_ROWS;
+  const uint32_t crank = PAIR ? cluster_rank() : 0u;
+  const int tstride = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const int tfirst = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
   constexpr int TC_LOAD_WARPS = NLW;
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
-  // bars: full[S], empty[S], tfull[2], tempty[2]; then the TMEM base address
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4);
+  // bars: full[S], empty[S], tfull[2], tempty[2], pfull[S] (PAIR peer: its loaders' local
+  // barrier, forwarded to the leader by the peer's MMA warp); then the TMEM base address
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * Cfg::STAGES + 4);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (Cfg::STAGES + s); };
   auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + a); };
   auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + 2 + a); };
+  auto pfull_bar = [&](int s) { return bar0 + 8u * (2 * Cfg::STAGES + 4 + s); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == TC_MMA_WARP) {
     if (lane == 0) {
       for (int s = 0; s < Cfg::STAGES; ++s) {
-        mbar_init(full_bar(s), TC_LOAD_WARPS);
+        mbar_init(full_bar(s), PAIR ? TC_LOAD_WARPS + 1 : TC_LOAD_WARPS);   // + the peer's forward
         mbar_init(empty_bar(s), 1);
+        mbar_init(pfull_bar(s), TC_LOAD_WARPS);
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(tfull_bar(a), 1);
-        mbar_init(tempty_bar(a), EPI);
+        mbar_init(tempty_bar(a), PAIR ? 2 * EPI : EPI);                      // + the peer's epilogue
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"((uint32_t)Cfg::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"((uint32_t)Cfg::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"((uint32_t)Cfg::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();   // both CTAs' barriers initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == TC_MMA_WARP) {
     // ------------------------------------------------------------- MMA issuer
-    constexpr uint32_t IDESC = umma_idesc_tf32<BN>(!TA, TB);
+    constexpr uint32_t IDESC = umma_idesc_tf32<BN, BMT>(!TA, TB);
     // k-step strides of the start-address field: K-major 32 B, MN-major two 4-row groups
     constexpr uint32_t STEP_A = TA ? 2u : (2u * (TC_BM / 32 * 512)) >> 4;
-    constexpr uint32_t STEP_B = TB ? (2u * (BN / 32 * 512)) >> 4 : 2u;
+    constexpr uint32_t STEP_B = TB ? (2u * (B_ROWS / 32 * 512)) >> 4 : 2u;
     const uint64_t dAH = tc_op_desc<!TA, TC_BM>(sbase, 0);
     const uint64_t dAL = tc_op_desc<!TA, TC_BM>(sbase + Cfg::A_BYTES, 0);
-    const uint64_t dBH = tc_op_desc<TB, BN>(sbase + 2 * Cfg::A_BYTES, 0);
-    const uint64_t dBL = tc_op_desc<TB, BN>(sbase + 2 * Cfg::A_BYTES + Cfg::B_BYTES, 0);
+    const uint64_t dBH = tc_op_desc<TB, B_ROWS>(sbase + 2 * Cfg::A_BYTES, 0);
+    const uint64_t dBL = tc_op_desc<TB, B_ROWS>(sbase + 2 * Cfg::A_BYTES + Cfg::B_BYTES, 0);
     // one thread runs the whole issue loop: the tensor pipe's instruction queue is shallow,
-    // so every cycle the issuer spends on warp-wide waits or shuffles is pipe idle time
-    if (lane == 0) {
+    // so every cycle the issuer spends on warp-wide waits or shuffles is pipe idle time.
+    // PAIR: the leader issues for both CTAs; the peer's MMA warp only owns its TMEM
+    if (lane == 0 && (!PAIR || crank == 0)) {
       int stage = 0; uint32_t phase = 0;
       int kb = 0;   // K-block counter over all tiles of this CTA (TMEM buffer = kb & 1)
-      for (int t = blockIdx.x; t < b.total_tiles; t += gridDim.x) {
-        const TcTile x = tc_tile<BN>(b, t);
+      for (int t = tfirst; t < b.total_tiles; t += tstride) {
+        const TcTile x = tc_tile<BN, BMT>(b, t);
         for (int c0 = x.c_beg; c0 < x.c_end; c0 += TC_PROMO, ++kb) {
           const int buf = kb & 1;
 #ifdef BKFAC_TC_TIMING
           unsigned long long t0 = clock64();
 #endif
-          mbar_wait(tempty_bar(buf), ((kb >> 1) & 1) ^ 1);
+          if (PAIR) mbar_wait_cluster(tempty_bar(buf), ((kb >> 1) & 1) ^ 1);
+          else mbar_wait(tempty_bar(buf), ((kb >> 1) & 1) ^ 1);
 #ifdef BKFAC_TC_TIMING
           g_tc_dbg[blockIdx.x * 8 + 0] += clock64() - t0;
 #endif
@@ -466,7 +533,8 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
             unsigned long long t1 = clock64();
 #endif
 #ifndef BKFAC_TC_DEBUG_NOFULLWAIT
-            mbar_wait(full_bar(stage), phase);
+            if (PAIR) mbar_wait_cluster(full_bar(stage), phase);
+            else mbar_wait(full_bar(stage), phase);
 #endif
 #ifdef BKFAC_TC_TIMING
             unsigned long long t2 = clock64();
@@ -484,21 +552,40 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
               const uint64_t bL = dBL + so + (uint64_t)(ks * STEP_B);
               const uint32_t first = (c == c0 && ks == 0) ? 0u : 1u;
 #ifndef BKFAC_TC_DEBUG_ONEPASS
-              tc_mma_tf32(tmem_d, aL, bH, IDESC, first);   // small terms first
-              tc_mma_tf32(tmem_d, aH, bL, IDESC, 1u);
-              tc_mma_tf32(tmem_d, aH, bH, IDESC, 1u);
+              if (PAIR) {
+                tc_mma2_tf32(tmem_d, aL, bH, IDESC, first);
+                tc_mma2_tf32(tmem_d, aH, bL, IDESC, 1u);
+                tc_mma2_tf32(tmem_d, aH, bH, IDESC, 1u);
+              } else {
+                tc_mma_tf32(tmem_d, aL, bH, IDESC, first);   // small terms first
+                tc_mma_tf32(tmem_d, aH, bL, IDESC, 1u);
+                tc_mma_tf32(tmem_d, aH, bH, IDESC, 1u);
+              }
 #else                                     // tuning only: 1xTF32 (MMA-rate probe)
               tc_mma_tf32(tmem_d, aH, bH, IDESC, first);
 #endif
             }
-            tc_commit(empty_bar(stage));
+            if (PAIR) tc_commit2(empty_bar(stage)); else tc_commit(empty_bar(stage));
 #ifdef BKFAC_TC_TIMING
             g_tc_dbg[blockIdx.x * 8 + 2] += clock64() - t2;
             g_tc_dbg[blockIdx.x * 8 + 3] += 1;
 #endif
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
           }
-          tc_commit(tfull_bar(buf));
+          if (PAIR) tc_commit2(tfull_bar(buf)); else tc_commit(tfull_bar(buf));
+        }
+      }
+    } else if (PAIR && lane == 0) {
+      // the peer's MMA warp: one cluster-scope arrive per stage on the leader's full barrier
+      // once all of this CTA's loader warps have filled it (one release.cluster instead of
+      // sixteen)
+      int stage = 0; uint32_t phase = 0;
+      for (int t = tfirst; t < b.total_tiles; t += tstride) {
+        const TcTile x = tc_tile<BN, BMT>(b, t);
+        for (int c = x.c_beg; c < x.c_end; ++c) {
+          mbar_wait(pfull_bar(stage), phase);
+          mbar_arrive_remote(full_bar(stage), 0);
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -508,13 +595,18 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     const int lw = warp - TC_MMA_WARP - 1;
     int stage = 0; uint32_t phase = 0;
     // the (tile, chunk) sequence of this CTA, walked one step ahead of the stores
-    int t = blockIdx.x, c = 0;
+    int t = tfirst, c = 0;
     TcTile x;
     auto seek = [&]() {   // advance (t, c) to the next existing chunk; false when done
       while (t < b.total_tiles) {
-        if (c == 0) { x = tc_tile<BN>(b, t); c = x.c_beg; }
+        if (c == 0) {
+          x = tc_tile<BN, BMT>(b, t);
+          x.m0 += (int)crank * TC_BM;      // PAIR: this CTA's 128 rows of A ...
+          x.n0 += (int)crank * B_ROWS;     // ... and its half of B
+          c = x.c_beg;
+        }
         if (c < x.c_end) return true;
-        t += gridDim.x; c = 0;
+        t += tstride; c = 0;
       }
       return false;
     };
@@ -594,7 +686,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
           const int l = 4 * g + (lane >> 3), e0 = (lane & 7) * 4;
           uint32_t dh, dl;
           if (isA) { dh = st + tc_line_off<!TA, TC_BM>(l, e0); dl = dh + Cfg::A_BYTES; }
-          else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, e0); dl = dh + Cfg::B_BYTES; }
+          else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, B_ROWS>(l - TC_BM, e0); dl = dh + Cfg::B_BYTES; }
           float h[4], lo[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) { h[t] = tf32_round(v[4 * qd + t]); lo[t] = v[4 * qd + t] - h[t]; }
@@ -608,7 +700,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
             const float lo = v[4 * qd + t] - hi;
             uint32_t dh, dl;
             if (isA) { dh = st + tc_line_off<!TA, TC_BM>(l, lane); dl = dh + Cfg::A_BYTES; }
-            else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, BN>(l - TC_BM, lane); dl = dh + Cfg::B_BYTES; }
+            else { dh = st + 2 * Cfg::A_BYTES + tc_line_off<TB, B_ROWS>(l - TC_BM, lane); dl = dh + Cfg::B_BYTES; }
             sts_f32(dh, hi);
             sts_f32(dl, lo);
           }
@@ -619,7 +711,10 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
       fence_proxy_async_smem();
 #endif
       __syncwarp();
-      if (lane == 0) mbar_arrive(full_bar(stage));
+      if (lane == 0) {
+        if (PAIR && crank != 0) mbar_arrive(pfull_bar(stage));   // forwarded to the leader
+        else mbar_arrive(full_bar(stage));
+      }
       if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
     };
     float va[Cfg::LPW], vb[Cfg::LPW];
@@ -643,15 +738,20 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     const int e = warp < 4 ? warp : 4 + (warp - (TC_MMA_WARP + 1 + NLW));   // epilogue warp index
     float* stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256) +
                    e * Cfg::EPI_STAGE_FLOATS;
-    tc_epilogue<BN, EPI>(b, tmem_base, warp, lane, tfull_bar(0), tfull_bar(1), tempty_bar(0), tempty_bar(1),
+    tc_epilogue<BN, EPI, PAIR>(b, tmem_base, warp, lane, tfull_bar(0), tfull_bar(1), tempty_bar(0), tempty_bar(1),
                     stage);
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();   // neither CTA frees TMEM / exits while the pair still works
+  else __syncthreads();
   if (warp == TC_MMA_WARP) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"((uint32_t)Cfg::TMEM_COLS));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"((uint32_t)Cfg::TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"((uint32_t)Cfg::TMEM_COLS));
   }
 }
 
@@ -660,34 +760,56 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 constexpr int TC_BN = 128, TC_NLW = BKFAC_TC_NLW, TC_DEPTH = BKFAC_TC_DEPTH;
 using TcMain = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 4>;
 using TcShortK = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 8>;
+using TcPair = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 4, true>;
 constexpr int TC_SHORT_K_CHUNKS = 8;   // stages with every K <= 8 chunks use 8 epilogue warps
 
-template <bool TA, bool TB, int EPI>
+template <bool TA, bool TB, int EPI, bool PAIR>
 inline bool tc_set_attr() {
-  using Cfg = TcCfg<TC_BN, TC_NLW, TC_DEPTH, EPI>;
-  return cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, EPI>,
+  using Cfg = TcCfg<TC_BN, TC_NLW, TC_DEPTH, EPI, PAIR>;
+  return cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, EPI, PAIR>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) == cudaSuccess;
 }
 
 inline bool tc_init_attributes() {
   bool ok = true;
-  ok &= tc_set_attr<false, false, 4>();
-  ok &= tc_set_attr<false, true, 4>();
-  ok &= tc_set_attr<true, false, 4>();
-  ok &= tc_set_attr<true, true, 4>();
-  ok &= tc_set_attr<false, false, 8>();
-  ok &= tc_set_attr<false, true, 8>();
-  ok &= tc_set_attr<true, false, 8>();
-  ok &= tc_set_attr<true, true, 8>();
+  ok &= tc_set_attr<false, false, 4, false>();
+  ok &= tc_set_attr<false, true, 4, false>();
+  ok &= tc_set_attr<true, false, 4, false>();
+  ok &= tc_set_attr<true, true, 4, false>();
+  ok &= tc_set_attr<false, false, 8, false>();
+  ok &= tc_set_attr<false, true, 8, false>();
+  ok &= tc_set_attr<true, false, 8, false>();
+  ok &= tc_set_attr<true, true, 8, false>();
+  ok &= tc_set_attr<false, false, 4, true>();
+  ok &= tc_set_attr<false, true, 4, true>();
+  ok &= tc_set_attr<true, false, 4, true>();
+  ok &= tc_set_attr<true, true, 4, true>();
   return ok;
 }
 
+// grid: persistent CTAs (pair mode: CTA pairs, 2 x grid CTAs in clusters of 2)
 template <bool TA, bool TB>
-inline void tc_launch(const GemmBatch& b, int grid, cudaStream_t st, bool short_k) {
+inline cudaError_t tc_launch(const GemmBatch& b, int grid, cudaStream_t st, bool short_k, bool pair) {
+  if (pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * grid), 1, 1);
+    cfg.blockDim = dim3(TcPair::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = TcPair::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 4, true>, b);
+  }
   if (short_k)
-    gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 8><<<grid, TcShortK::THREADS, TcShortK::SMEM_BYTES, st>>>(b);
+    gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 8, false><<<grid, TcShortK::THREADS, TcShortK::SMEM_BYTES, st>>>(b);
   else
-    gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 4><<<grid, TcMain::THREADS, TcMain::SMEM_BYTES, st>>>(b);
+    gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 4, false><<<grid, TcMain::THREADS, TcMain::SMEM_BYTES, st>>>(b);
+  return cudaGetLastError();
 }
 
 }  // namespace bkfac
