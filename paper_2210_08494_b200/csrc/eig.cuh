@@ -169,6 +169,10 @@ BKFAC_DEV double hash_unit(unsigned a, unsigned b) {
 // streaming passes: the 2-norm is accumulated during back substitution and the
 // normalisation is folded into the next iteration's forward pass (one final scale pass).
 constexpr int INV_THREADS = 32;
+#ifndef BKFAC_INV_ITERS
+#define BKFAC_INV_ITERS 2
+#endif
+constexpr int INV_ITERS = BKFAC_INV_ITERS;   // inverse iterations per eigenvector
 __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   const int m = p.m, r = p.r;
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
   const unsigned char* pvj = pv + j;
   double s = 1.0;   // pending scale of x (applied as x is read in the next pass)
   double nrm = 0.0, amax = 0.0;
-  for (int it = 0; it < 3; ++it) {
+  for (int it = 0; it < INV_ITERS; ++it) {
     // forward: apply L^{-1} with row interchanges; the running entry is carried
     double carry = xj[0] * s;
     int i0 = 0;
