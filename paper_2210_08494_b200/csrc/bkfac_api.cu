@@ -489,7 +489,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     continue;   // tuning builds: keep the sytrd timing sums in Y
 #endif
     prof_begin(ctx, "eig_bisect", st, 0.0, 0.0);
-    bisect_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, BIS_WARPS)), BIS_WARPS * 32,
+    bisect_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, BIS_WARPS * BIS_E)), BIS_WARPS * 32,
                     sizeof(double) * 3 * (size_t)mmax, st>>>(b);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);

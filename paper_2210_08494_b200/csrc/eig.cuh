@@ -3,8 +3,8 @@
 // only the top-r eigenpairs are kept (truncation, Alg 4 :540-543).
 //
 //   1. sytrd_tiled_kernel (sytrd_tiled.cuh) Householder tridiagonalisation T = H^T K H.
-//   2. bisect_kernel    top-r eigenvalues of T by Sturm-count multisection in fp64
-//                       (one warp per eigenvalue, 32 probes per round).
+//   2. bisect_kernel    top-r eigenvalues of T by Sturm-count multisection (fp32, then
+//                       fp64; 4 lanes = 4 probes per eigenvalue, 8 eigenvalues per warp).
 //   3. invit_kernel     eigenvectors of T by inverse iteration in fp64 (one thread per
 //                       eigenvector, tridiagonal LU with partial pivoting).
 //   4. cluster_kernel   modified Gram-Schmidt inside clusters of (near-)equal eigenvalues.
@@ -73,8 +73,13 @@ BKFAC_DEV int sturm_count_f32(const float* dd, const float* e2, int m, float x, 
 }
 
 constexpr int BIS_WARPS = 8;
+#ifndef BKFAC_BIS_G
+#define BKFAC_BIS_G 4
+#endif
+constexpr int BIS_G = BKFAC_BIS_G;    // lanes (probes) per eigenvalue
+constexpr int BIS_E = 32 / BIS_G;     // eigenvalues per warp
 
-// grid: (nprob, ceil(rmax / BIS_WARPS)); smem: 2*m doubles
+// grid: (nprob, ceil(rmax / (BIS_WARPS * BIS_E))); smem: 2*m doubles + 2*m floats
 __global__ void __launch_bounds__(BIS_WARPS * 32) bisect_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   const int m = p.m;
@@ -108,49 +113,62 @@ __global__ void __launch_bounds__(BIS_WARPS * 32) bisect_kernel(const __grid_con
     s_pivmin = 2.3e-308 * fmax(1.0, emax);
   }
   __syncthreads();
+  // BIS_G lanes per eigenvalue (BIS_G probes per round, the bracket cut into BIS_G + 1
+  // parts), BIS_E eigenvalues per warp: far fewer Sturm counts per eigenvalue than one
+  // eigenvalue per warp (the fp64 phase was fp64-pipe bound), at ~2x the rounds
   const int lane = tid & 31, warp = tid >> 5;
-  const int j = blockIdx.y * BIS_WARPS + warp;   // descending index
-  if (j >= p.r) return;
-  const int kasc = m - 1 - j;                     // ascending index
+  const int sub = lane / BIS_G, q = lane % BIS_G;
+  const int j = (blockIdx.y * BIS_WARPS + warp) * BIS_E + sub;   // descending index
+  if ((blockIdx.y * BIS_WARPS + warp) * BIS_E >= p.r) return;    // whole warp idle
+  const bool active = j < p.r;
+  const int kasc = m - 1 - (active ? j : p.r - 1);                // ascending index
+  const unsigned gmask = ((1u << BIS_G) - 1u) << (sub * BIS_G);
   double lo = s_lo, hi = s_hi;
   const double pivmin = s_pivmin;
-  // invariant: count(lo) <= kasc < count(hi).  Phase 1: 32-way multisection with fp32
-  // Sturm counts (fast reciprocal) down to ~1e-6 of the spectrum's span; phase 2: the
-  // bracket, widened by the fp32 counts' backward error, refined with fp64 counts to
-  // 1e-10 of the span (fp32 outputs; eigenvalues closer than 1e-7 ||T|| are treated as a
-  // cluster by stage 4, so inverse iteration never has to separate them).
+  // invariant: count(lo) <= kasc < count(hi).  Phase 1: multisection with fp32 Sturm counts
+  // (fast reciprocal) down to ~1e-6 of the spectrum's span; phase 2: the bracket, widened by
+  // the fp32 counts' backward error, refined with fp64 counts to 1e-10 of the span (fp32
+  // outputs; eigenvalues closer than 1e-7 ||T|| are treated as a cluster by stage 4, so
+  // inverse iteration never has to separate them).
   const double span = fmax(fabs(lo), fabs(hi));
+  constexpr double NP = BIS_G + 1;
   {
     const float pivf = 1e-30f;
-    for (int round = 0; round < 8; ++round) {
+    for (int round = 0; round < 24; ++round) {
       const double w = hi - lo;
-      if (w <= 1e-6 * span) break;
-      const float xf = (float)(lo + w * (double)(lane + 1) / 33.0);
+      const bool go = w > 1e-6 * span;
+      if (!__any_sync(0xffffffffu, go)) break;
+      const float xf = (float)(lo + w * (double)(q + 1) / NP);
       const int cnt = sturm_count_f32(ddf, e2f, m, xf, pivf);
-      const unsigned above = __ballot_sync(0xffffffffu, cnt >= kasc + 1);
-      const int first = above ? __ffs(above) - 1 : 32;
-      const double nlo = (first == 0) ? lo : lo + w * (double)first / 33.0;
-      const double nhi = (first == 32) ? hi : lo + w * (double)(first + 1) / 33.0;
-      lo = nlo;
-      hi = nhi;
+      const unsigned above = (__ballot_sync(0xffffffffu, cnt >= kasc + 1) & gmask) >> (sub * BIS_G);
+      const int first = above ? __ffs(above) - 1 : BIS_G;
+      if (go) {
+        const double nlo = (first == 0) ? lo : lo + w * (double)first / NP;
+        const double nhi = (first == BIS_G) ? hi : lo + w * (double)(first + 1) / NP;
+        lo = nlo;
+        hi = nhi;
+      }
     }
     const double widen = 4e-7 * span * (1.0 + 0.01 * m);
     lo = fmax(lo - widen, s_lo);
     hi = fmin(hi + widen, s_hi);
   }
-  for (int round = 0; round < 10; ++round) {
+  for (int round = 0; round < 24; ++round) {
     const double w = hi - lo;
-    if (w <= 1e-10 * span + pivmin) break;
-    const double x = lo + w * (double)(lane + 1) / 33.0;
+    const bool go = w > 1e-10 * span + pivmin;
+    if (!__any_sync(0xffffffffu, go)) break;
+    const double x = lo + w * (double)(q + 1) / NP;
     const int cnt = sturm_count(dd, e2, m, x, pivmin);
-    const unsigned above = __ballot_sync(0xffffffffu, cnt >= kasc + 1);
-    const int first = above ? __ffs(above) - 1 : 32;
-    const double nlo = (first == 0) ? lo : lo + w * (double)first / 33.0;
-    const double nhi = (first == 32) ? hi : lo + w * (double)(first + 1) / 33.0;
-    lo = nlo;
-    hi = nhi;
+    const unsigned above = (__ballot_sync(0xffffffffu, cnt >= kasc + 1) & gmask) >> (sub * BIS_G);
+    const int first = above ? __ffs(above) - 1 : BIS_G;
+    if (go) {
+      const double nlo = (first == 0) ? lo : lo + w * (double)first / NP;
+      const double nhi = (first == BIS_G) ? hi : lo + w * (double)(first + 1) / NP;
+      lo = nlo;
+      hi = nhi;
+    }
   }
-  if (lane == 0) p.lam[j] = 0.5 * (lo + hi);
+  if (active && q == 0) p.lam[j] = 0.5 * (lo + hi);
 }
 
 // ------------------------------------------------------------------ 3. inverse iteration
@@ -332,8 +350,8 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
 
 // ------------------------------------------------------------------ 4. clusters
 // One CTA (32 warps) per problem; clusters are runs of eigenvalues whose consecutive
-// gaps are <= 1e-7 * ||T|| (beyond that, three inverse iterations from shifts accurate to
-// 1e-10 * span separate the eigenvectors to ~1e-9).  Each warp orthonormalises one
+// gaps are <= 1e-7 * ||T|| (beyond that, two inverse iterations from shifts accurate to
+// 1e-10 * span separate the eigenvectors to ~1e-6).  Each warp orthonormalises one
 // cluster by modified Gram-Schmidt.
 constexpr int CL_BIG = 32;   // clusters longer than this are orthonormalised by the whole CTA
 __global__ void __launch_bounds__(1024) cluster_kernel(const __grid_constant__ EigBatch b) {
