@@ -72,6 +72,26 @@ inline size_t syt_global_tile_floats(int m) {
   return (size_t)syt_tiles(NB) * 1024;
 }
 
+// Load of float `p` (an address in this CTA's shared memory) from CTA r of the cluster:
+// explicit ld.shared::cluster on a mapa'd 32-bit address (no generic-address resolution).
+__device__ __forceinline__ float4 syt_dsmem_ld4(const float* p, int r) {   // p 16-byte aligned
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  uint32_t ra;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
+  return v;
+}
+__device__ __forceinline__ float syt_dsmem_ld(const float* p, int r) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  uint32_t ra;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+  return v;
+}
+
 // Block sum with one barrier.  Precondition: every call is separated from the next one
 // by at least one __syncthreads (true at both call sites below), so `red` is not
 // rewritten while a warp still reads it.
@@ -160,7 +180,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   }
 
 #ifdef BKFAC_SYT_TIMING
-  unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0}, tprev = clock64();
+  unsigned long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tprev = clock64();
 #define SYT_T(i) do { if (tid == 0) { unsigned long long tn = clock64(); tacc[i] += tn - tprev; tprev = tn; } } while (0)
 #else
 #define SYT_T(i) do {} while (0)
@@ -208,7 +228,6 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     tau = finish(0, ss, vbuf);
   }
   SYT_T(0);
-  constexpr int IPT = 4;   // rows per thread in the merged phase (m <= 2048)
   for (int k = 0; k < m - 2; ++k) {
     float* v = vbuf + (k & 1) * m_pad;            // v_k
     const float* vp = vbuf + ((k + 1) & 1) * m_pad;   // v_{k-1} (zero at k = 0)
@@ -285,40 +304,54 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       const int k1 = k + 1;
       const bool next = k1 <= m - 3;
       const int kb1 = k1 >> 5, jk1 = k1 & 31, base1 = syt_pos(kb1, kb1, NB);
-      float si[IPT], xi[IPT];
+      // thread t owns the 4 rows i0 .. i0+3, i0 = (k+1 rounded down to 4) + 4t: 16-byte
+      // DSMEM loads of the C partial y and of column k+1 (4 rows never straddle a tile)
+      const int i0 = (k1 & ~3) + 4 * tid;
+      const bool own = i0 < m;
+      float si[4] = {0.f, 0.f, 0.f, 0.f}, xi[4] = {0.f, 0.f, 0.f, 0.f}, vi4[4] = {0.f, 0.f, 0.f, 0.f};
       float pv = 0.f;
+      if (own) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = 0; r < C; ++r) {
+          const float4 t4 = (C == 1) ? *reinterpret_cast<const float4*>(y + i0) : syt_dsmem_ld4(y + i0, r);
+          acc.x += t4.x; acc.y += t4.y; acc.z += t4.z; acc.w += t4.w;
+        }
+        si[0] = acc.x; si[1] = acc.y; si[2] = acc.z; si[3] = acc.w;
+        if (next) {
+          const int pos = base1 + (i0 >> 5) - kb1;
+          const float* src = tiles + 1024L * (pos / C) + jk1 * 32 + (i0 & 31);
+          const float4 c4 = (C == 1) ? *reinterpret_cast<const float4*>(src) : syt_dsmem_ld4(src, pos % C);
+          xi[0] = c4.x; xi[1] = c4.y; xi[2] = c4.z; xi[3] = c4.w;
+        }
+        const float4 v4 = *reinterpret_cast<const float4*>(v + i0);
+        vi4[0] = v4.x; vi4[1] = v4.y; vi4[2] = v4.z; vi4[3] = v4.w;
 #pragma unroll
-      for (int u = 0; u < IPT; ++u) {
-        const int i = k1 + tid + u * SYT_THREADS;
-        si[u] = 0.f;
-        xi[u] = 0.f;
-        if (i < m) {
-          float sacc = 0.f;
-          for (int r = 0; r < C; ++r) sacc += *rptr(y + i, r);
-          si[u] = sacc;
-          pv = fmaf(sacc, v[i], pv);
-          if (next) {
-            const int pos = base1 + (i >> 5) - kb1;
-            xi[u] = *rptr(tiles + 1024L * (pos / C) + jk1 * 32 + (i & 31), pos % C);
-          }
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u >= k1 && i0 + u < m) pv = fmaf(si[u], vi4[u], pv);
+          else si[u] = 0.f;
+        if (i0 <= k1 && k1 < i0 + 4) {                          // y_k at row k+1
+          const int o = k1 - i0;
+          scal[60] = o == 0 ? si[0] : o == 1 ? si[1] : o == 2 ? si[2] : si[3];
         }
       }
-      if (tid == 0) scal[60] = si[0];             // y_k at row k+1, shared after the sum's barrier
+      SYT_T(5);
       pv = syt_block_sum(pv, red);
+      SYT_T(6);
       const float s1 = scal[60];
       const float gamma = 0.5f * tau * tau * pv;
       const float vk1 = v[k1];
       const float wk1 = tau * s1 - gamma * vk1;
       float* vn = vbuf + (k1 & 1) * m_pad;         // v_{k+1} (v_{k-1} is no longer needed)
       float ss = 0.f;
+      if (own) {
 #pragma unroll
-      for (int u = 0; u < IPT; ++u) {
-        const int i = k1 + tid + u * SYT_THREADS;
-        if (i < m) {
-          const float w = tau * si[u] - gamma * v[i];
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u;
+          if (i < k1 || i >= m) continue;
+          const float w = tau * si[u] - gamma * vi4[u];
           wp[i] = w;
           if (next) {
-            const float x = xi[u] - (v[i] * wk1 + w * vk1);
+            const float x = xi[u] - (vi4[u] * wk1 + w * vk1);
             if (i >= k1 + 2) ss = fmaf(x, x, ss);
             else scal[40 + (i - k1)] = x;         // d_{k+1} (i = k+1), alpha (i = k+2)
             vn[i] = x;
@@ -329,7 +362,9 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       if (next) {
         float* yn = ybuf + (k1 & 1) * m_pad;       // step k-1's partials: every reader is done
         for (int i = tid; i < m_pad; i += SYT_THREADS) yn[i] = 0.f;
+        SYT_T(7);
         ss = syt_block_sum(ss, red2);
+        SYT_T(8);
         tau = finish(k1, ss, vn);
       }
     }
@@ -338,8 +373,8 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   __syncthreads();
 #ifdef BKFAC_SYT_TIMING
   if (tid == 0 && p.status) {   // tuning builds: per-phase cycle sums of CTA q
-    unsigned long long* o = reinterpret_cast<unsigned long long*>(p.Y) + 8 * q;
-    for (int i = 0; i < 5; ++i) o[i] = tacc[i];
+    unsigned long long* o = reinterpret_cast<unsigned long long*>(p.Y) + 16 * q;
+    for (int i = 0; i < 9; ++i) o[i] = tacc[i];
   }
 #endif
   // trailing 2x2 block: the pending update of step m-3 (v_{m-3}, w_{m-3}), then d, e;
