@@ -524,8 +524,11 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
           }
         }
         // S and U define the compact-WY operator I - W T W^T: their errors become departures
-        // from orthogonality of V, so they run in plain fp32 (small: 2 m PW^2 per panel)
-        gs.fp32_simt = true;
+        // from orthogonality of V.  On the 3xTF32 tensor-core path (~1e-6) those departures
+        // are removed by the per-step Newton-Schulz refresh of U_out (R8; the 50-step config-2
+        // chain is unchanged: 5.2e-6 vs 5.0e-6 with fp32 SIMT).  BKFAC_BT_SIMT selects the
+        // fp32 SIMT kernel for them instead.
+        gs.fp32_simt = getenv("BKFAC_BT_SIMT") != nullptr;
         if ((rs2 = run_gemms(ctx, gs, st, "gemm_backtr_s")) != BKFAC_OK) return rs2;
         prof_begin(ctx, "eig_backtr", st, 0.0, 0.0);
         backtr_t_kernel<<<dim3((unsigned)n, (unsigned)pmax), BT_THREADS, bt_smem_bytes(), st>>>(b);
@@ -540,7 +543,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
                                     q.Uw + (long)(j * BT_PW) * q.m + r0, q.m, q.m - r0, np, np, 1.f), 0);
           }
         }
-        gs.fp32_simt = true;
+        gs.fp32_simt = getenv("BKFAC_BT_SIMT") != nullptr;
         if ((rs2 = run_gemms(ctx, gs, st, "gemm_backtr_wt")) != BKFAC_OK) return rs2;
       }
       for (int j = pmax - 1; j >= 0; --j) {
