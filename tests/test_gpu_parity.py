@@ -295,6 +295,40 @@ def test_errors_and_status(cuda_lib):
     assert code == 7 and bad == 0
 
 
+def test_errors_next_rows(cuda_lib):
+    """Argument validation of the NEXT-row entry points (synchronous, before any launch)."""
+    import torch
+    from paper_2210_08494_b200 import binding
+    n, c, r, dG = 100, 8, 10, 40
+    ctx = _ctx([(n, r, c, 0), (dG, 5, c, 0)], [(dG, n, 5, r, c)])
+    U = to_dev_cols(synth.phantom_basis(n, r)); D = torch.ones(r, device="cuda")
+    UG = to_dev_cols(synth.phantom_basis(dG, 5)); DG = torch.ones(5, device="cuda")
+    S = torch.empty((dG, n), device="cuda")
+    G = torch.zeros((c + 1, dG), device="cuda"); A = torch.zeros((c + 1, n), device="cuda")
+    item = dict(layer=0, U_G=UG, D_G=DG, lambda_G=0.1, U_A=U, D_A=D, lambda_A=0.1, G=G, A=A, S=S)
+    with pytest.raises(binding.BkfacError) as e:       # n > n_max
+        ctx.bkfac_precondition_factored([item])
+    assert e.value.code == 2
+    with pytest.raises(binding.BkfacError) as e:       # lambda <= 0
+        ctx.bkfac_precondition_factored([dict(item, G=G[:c], A=A[:c], lambda_A=0.0)])
+    assert e.value.code == 1
+    K = torch.eye(n, device="cuda")
+    idx = torch.arange(4, dtype=torch.int32, device="cuda")
+    with pytest.raises(binding.BkfacError) as e:       # factor without BKFAC_FACTOR_DENSE_EA
+        ctx.bkfac_light_correction([dict(factor=0, K=K, U=U, D=D, col_idx=idx)])
+    assert e.value.code == 1
+    ctx2 = _ctx([(n, r, c, 1)])
+    with pytest.raises(binding.BkfacError) as e:       # n_crc > r
+        ctx2.bkfac_light_correction([dict(factor=0, K=K, U=U, D=D,
+                                          col_idx=torch.arange(r + 1, dtype=torch.int32, device="cuda"))])
+    assert e.value.code == 2
+    M = torch.zeros((c, n), device="cuda")
+    with pytest.raises(binding.BkfacError) as e:       # K_dense aliases U_out
+        ctx2.bkfac_brand_ea_update([dict(factor=0, U_in=U, D_in=D, M=M, U_out=K, D_out=torch.empty_like(D),
+                                         alpha=0.9, beta=0.1)], [dict(factor=0, K=K, M=M, rho=0.9)])
+    assert e.value.code == 4
+
+
 def test_rsvd_ill_conditioned_cfg4_factor(cuda_lib):
     """configs[3] factor shape n = 577, r = 220, l = 230, q = 2 after 25 EA steps: the
     power-iteration block K Q has condition ~1e3, which plain CholeskyQR2 cannot
