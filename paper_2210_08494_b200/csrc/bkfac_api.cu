@@ -460,7 +460,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         if (C == 0) {   // tiles in global memory, one CTA per factor
           const int mp = (msub + 31) / 32 * 32;
           sytrd_tiled_kernel<true><<<(unsigned)sub[g].nprob, SYT_THREADS,
-                                     sizeof(float) * (size_t)syt_vec_floats(mp), sg>>>(sub[g], 1);
+                                     sizeof(float) * (size_t)syt_gt_smem_floats(mp), sg>>>(sub[g], 1);
         } else {
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3((unsigned)(C * sub[g].nprob), 1, 1);

@@ -53,6 +53,8 @@ __host__ __device__ inline int syt_pos(int I, int J, int NB) {
 }
 inline int syt_vec_floats(int m_pad) { return 7 * m_pad + 64; }
 inline long syt_own_floats(int NB, int C) { return 1024L * ((syt_tiles(NB) + C - 1) / C); }
+// global-tile variant: vectors + a two-tile cp.async ring per warp
+inline int syt_gt_smem_floats(int m_pad) { return syt_vec_floats(m_pad) + (SYT_THREADS / 32) * 2048; }
 // smallest cluster size whose per-CTA share fits; 0 = does not fit
 inline int sytrd_tiled_cluster(int m) {
   const int NB = (m + 31) / 32, m_pad = NB * 32;
@@ -238,18 +240,11 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     SYT_T(1);
     // (b) active tiles (J >= kb): this CTA's slots 0 .. nact-1, one per warp
     const int nact = (syt_tiles(NB - kb) - q + C - 1) / C;
-    for (int sl = warp; sl < nact; sl += NW) {
-      int I, J;
-      tile_ij(sl * C + q, I, J);
-      float* tcol = tiles + 1024L * sl + lane;   // + jj * 32
+    // one tile: pending update (v_{k-1}, w_{k-1}) written back to tcol, partial y = A v_k
+    auto tile_work = [&](float (&colv)[32], int I, int J, float* tcol) {
       const int i = 32 * I + lane;
       const float cv = v[32 * J + lane], cvp = vp[32 * J + lane], cwp = wp[32 * J + lane];
       const float vi = v[i], vpi = vp[i], wpi = wp[i];
-      // all 32 loads first: a store to column jj must not order the load of column
-      // jj+1 behind it (the compiler cannot prove they differ)
-      float colv[32];
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) colv[jj] = tcol[jj * 32];
       float racc[4] = {0.f, 0.f, 0.f, 0.f};
       if ((32 * J > k) && (I > J)) {
 #pragma unroll
@@ -293,6 +288,52 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       }
       atomicAdd(&y[i], (racc[0] + racc[1]) + (racc[2] + racc[3]));
       atomicAdd(&y[32 * J + lane], colv[0]);
+    };
+    if constexpr (GT) {
+      // tiles in global memory (L2 / HBM): each warp streams its tiles through a two-deep
+      // shared-memory ring with cp.async, the next tile in flight while this one computes
+      float* stg = scal + 64 + warp * 2048;
+      auto issue = [&](int sl2, int bi) {
+        const float* src = tiles + 1024L * sl2;
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stg + bi * 1024));
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          const int off = (c8 * 32 + lane) * 4;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + off * 4), "l"(src + off) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      if (warp < nact) issue(warp, 0);
+      int idx = 0;
+      for (int sl = warp; sl < nact; sl += NW, ++idx) {
+        if (sl + NW < nact) {
+          issue(sl + NW, (idx + 1) & 1);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+        int I, J;
+        tile_ij(sl * C + q, I, J);
+        const float* sb = stg + (idx & 1) * 1024 + lane;
+        float colv[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) colv[jj] = sb[jj * 32];
+        __syncwarp();   // the ring slot is refilled two tiles later
+        tile_work(colv, I, J, tiles + 1024L * sl + lane);
+      }
+    } else {
+      for (int sl = warp; sl < nact; sl += NW) {
+        int I, J;
+        tile_ij(sl * C + q, I, J);
+        float* tcol = tiles + 1024L * sl + lane;   // + jj * 32
+        // all 32 loads first: a store to column jj must not order the load of column
+        // jj+1 behind it (the compiler cannot prove they differ)
+        float colv[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) colv[jj] = tcol[jj * 32];
+        tile_work(colv, I, J, tcol);
+      }
     }
     __syncthreads();
     SYT_T(2);
