@@ -69,6 +69,8 @@ struct FactorPlan {
   bool dense = false;  // r + c_max >= n: form the n x n sum densely (a6')
   int m = 0;           // core order (r + c_max, or n on the dense path)
   int rout = 0;        // output columns: r, or min(n, r + c_max) with BKFAC_FACTOR_FULL_RANK
+  int nld = 0;         // leading dimension of the internal n-row buffers (R, Qb, Urot): n
+                       // rounded up to 32, so their GEMM loads take the 16-byte vector path
   // Brand path
   size_t W, P2, R, Qb, G, L1, L1i, L2, L2i, cscr, ws;
   size_t ws_elems = 0;
@@ -652,6 +654,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
     if (n <= 0 || r <= 0 || r > n || cm <= 0) { delete c; return BKFAC_ERR_DIM; }
     fp.dense = (r + cm >= n);
     const bool full = (fp.d.flags & BKFAC_FACTOR_FULL_RANK) != 0;
+    fp.nld = (n + 31) / 32 * 32;
     fp.rout = full ? std::min(n, r + cm) : r;
     const int ro = fp.rout;
     if (fp.dense) {
@@ -663,8 +666,8 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
       fp.m = m;
       fp.W = a.take(sizeof(float) * (size_t)m * cm);
       fp.P2 = a.take(sizeof(float) * (size_t)r * cm);
-      fp.R = a.take(sizeof(float) * (size_t)n * cm);
-      fp.Qb = a.take(sizeof(float) * (size_t)n * cm);
+      fp.R = a.take(sizeof(float) * (size_t)fp.nld * cm);
+      fp.Qb = a.take(sizeof(float) * (size_t)fp.nld * cm);
       const size_t cc = sizeof(float) * (size_t)cm * cm;
       fp.G = a.take(cc); fp.L1 = a.take(cc); fp.L1i = a.take(cc); fp.L2 = a.take(cc); fp.L2i = a.take(cc);
       fp.cscr = a.take(sizeof(float) * chol_tiled_scratch_floats(cm));
@@ -672,7 +675,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
       fp.ws = a.take(sizeof(float) * fp.ws_elems);
       plan_eig(a, fp.eig, m, ro);
     }
-    fp.Urot = a.take(sizeof(float) * (size_t)n * ro);
+    fp.Urot = a.take(sizeof(float) * (size_t)fp.nld * ro);
     fp.Gref = a.take(sizeof(float) * (size_t)ro * ro);
     fp.wsr_elems = (long)kSplitMax * ro * (long)ro;
     fp.wsr = a.take(sizeof(float) * fp.wsr_elems);
@@ -936,7 +939,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     for (int i : dense) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
-      eg.push_back(eig_prob(ctx, fp.eig, fp.d.n, rout_of(a), at<float>(ctx, fp.Urot), fp.d.n, a.D_out,
+      eg.push_back(eig_prob(ctx, fp.eig, fp.d.n, rout_of(a), at<float>(ctx, fp.Urot), fp.nld, a.D_out,
                             status_ptr(ctx, a.factor)));
     }
   }
@@ -958,7 +961,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
-      GemmProb pr = gp(a.U_in, n, at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), n, n, a.c,
+      GemmProb pr = gp(a.U_in, n, at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), fp.nld, n, a.c,
                        r, -1.f, a.M, n, 1.f);
       pr.status = status_ptr(ctx, a.factor);   // every element of M passes this epilogue
       gs.add(false, false, pr, 0);
@@ -972,7 +975,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       any_reorth = true;
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
-      GemmProb p = gp(a.U_in, n, at<float>(ctx, fp.R), n, at<float>(ctx, fp.P2), r, r, a.c, n, 1.f);
+      GemmProb p = gp(a.U_in, n, at<float>(ctx, fp.R), fp.nld, at<float>(ctx, fp.P2), r, r, a.c, n, 1.f);
       gemm_ws(p, at<float>(ctx, fp.ws));
       gs.add(true, false, p, fp.ws_elems);
     }
@@ -984,7 +987,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         const auto& fp = ctx->f[a.factor];
         const int n = fp.d.n, r = fp.d.r;
         float* R = at<float>(ctx, fp.R);
-        gs.add(false, false, gp(a.U_in, n, at<float>(ctx, fp.P2), r, R, n, n, a.c, r, -1.f, R, n, 1.f), 0);
+        gs.add(false, false, gp(a.U_in, n, at<float>(ctx, fp.P2), r, R, fp.nld, n, a.c, r, -1.f, R, fp.nld, 1.f), 0);
         EwProb e{};
         e.Y = at<float>(ctx, fp.W); e.ldy = fp.m; e.X = at<float>(ctx, fp.P2); e.ldx = r;
         e.rows = r; e.cols = a.c; e.a = 1.f; e.op = EW_ADD;
@@ -1000,7 +1003,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         const auto& fp = ctx->f[a.factor];
         const int n = fp.d.n, c = a.c;
         const float* X = at<float>(ctx, pass == 0 ? fp.R : fp.Qb);
-        GemmProb p = gp(X, n, X, n, at<float>(ctx, fp.G), c, c, c, n, 1.f);
+        GemmProb p = gp(X, fp.nld, X, fp.nld, at<float>(ctx, fp.G), c, c, c, n, 1.f);
         gemm_ws(p, at<float>(ctx, fp.ws));
         gs.add(true, false, p, fp.ws_elems);
       }
@@ -1021,7 +1024,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         const float* X = at<float>(ctx, pass == 0 ? fp.R : fp.Qb);
         float* Y = at<float>(ctx, pass == 0 ? fp.Qb : fp.R);
         const float* Li = at<float>(ctx, pass == 0 ? fp.L1i : fp.L2i);
-        gs.add(false, true, gp(X, n, Li, c, Y, n, n, c, c, 1.f), 0);
+        gs.add(false, true, gp(X, fp.nld, Li, c, Y, fp.nld, n, c, c, 1.f), 0);
       }
       STAGE(run("gemm_qmul"));
     }
@@ -1064,8 +1067,8 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const auto& fp = ctx->f[a.factor];
     const int n = fp.d.n, r = fp.d.r, mm = r + a.c, ro = rout_of(a);
     const float* V = at<float>(ctx, fp.eig.V);
-    GemmProb p = gp(a.U_in, n, V, mm, at<float>(ctx, fp.Urot), n, n, ro, mm, 1.f);
-    p.A2 = at<float>(ctx, fp.R); p.lda2 = n;
+    GemmProb p = gp(a.U_in, n, V, mm, at<float>(ctx, fp.Urot), fp.nld, n, ro, mm, 1.f);
+    p.A2 = at<float>(ctx, fp.R); p.lda2 = fp.nld;
     p.B2 = V + r; p.ldb2 = mm;
     p.k1 = r;
     gs.add(false, false, p, 0);
@@ -1081,7 +1084,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const auto& fp = ctx->f[a.factor];
     const int n = fp.d.n, r = rout_of(a);
     const float* Ur = at<float>(ctx, fp.Urot);
-    GemmProb p = gp(Ur, n, Ur, n, at<float>(ctx, fp.Gref), r, r, r, n, 1.f);
+    GemmProb p = gp(Ur, fp.nld, Ur, fp.nld, at<float>(ctx, fp.Gref), r, r, r, n, 1.f);
     gemm_ws(p, at<float>(ctx, fp.wsr));
     gs.add(true, false, p, fp.wsr_elems);
   }
@@ -1093,11 +1096,11 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const float* Ur = at<float>(ctx, fp.Urot);
     if (a.flags & BKFAC_BRAND_NO_REFRESH) {
       EwProb e{};
-      e.Y = a.U_out; e.ldy = n; e.X = Ur; e.ldx = n; e.rows = n; e.cols = r; e.op = EW_COPY;
+      e.Y = a.U_out; e.ldy = n; e.X = Ur; e.ldx = fp.nld; e.rows = n; e.cols = r; e.op = EW_COPY;
       ew.push_back(e);
       continue;
     }
-    GemmProb pf = gp(Ur, n, at<float>(ctx, fp.Gref), r, a.U_out, n, n, r, r, -0.5f, Ur, n, 1.5f);
+    GemmProb pf = gp(Ur, fp.nld, at<float>(ctx, fp.Gref), r, a.U_out, n, n, r, r, -0.5f, Ur, fp.nld, 1.5f);
     pf.status = status_ptr(ctx, a.factor);   // the new basis passes this epilogue
     gs.add(false, false, pf, 0);
   }
