@@ -73,6 +73,7 @@ struct FactorPlan {
                        // rounded up to 32, so their GEMM loads take the 16-byte vector path
   // Brand path
   size_t W, P2, R, Qb, G, L1, L1i, L2, L2i, cscr, ws;
+  size_t Ms = 0, Us = 0;   // aligned copies (ld nld) of the caller's M and U_in (odd n only)
   size_t ws_elems = 0;
   // dense path
   size_t T;
@@ -668,6 +669,10 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
       fp.P2 = a.take(sizeof(float) * (size_t)r * cm);
       fp.R = a.take(sizeof(float) * (size_t)fp.nld * cm);
       fp.Qb = a.take(sizeof(float) * (size_t)fp.nld * cm);
+      if (n % 4 != 0) {   // caller buffers with a leading dimension the vector loads cannot use
+        fp.Ms = a.take(sizeof(float) * (size_t)fp.nld * cm);
+        fp.Us = a.take(sizeof(float) * (size_t)fp.nld * r);
+      }
       const size_t cc = sizeof(float) * (size_t)cm * cm;
       fp.G = a.take(cc); fp.L1 = a.take(cc); fp.L1i = a.take(cc); fp.L2 = a.take(cc); fp.L2i = a.take(cc);
       fp.cscr = a.take(sizeof(float) * chol_tiled_scratch_floats(cm));
@@ -946,12 +951,42 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
 
   // ---------------- Brand path
   if (!brand.empty()) {
+    // M and U_in of factors with n % 4 != 0 are first copied to ld = nld (one streaming
+    // pass, ~2 (c + r) n floats), so every GEMM that reads them takes the 16-byte loads
+    for (int i : brand) {
+      const auto& a = args[i];
+      const auto& fp = ctx->f[a.factor];
+      if (!fp.Ms) continue;
+      const int n = fp.d.n;
+      EwProb e{};
+      e.Y = at<float>(ctx, fp.Ms); e.ldy = fp.nld; e.X = a.M; e.ldx = n; e.rows = n; e.cols = a.c;
+      e.op = EW_COPY;
+      ew.push_back(e);
+      EwProb u{};
+      u.Y = at<float>(ctx, fp.Us); u.ldy = fp.nld; u.X = a.U_in; u.ldx = n; u.rows = n; u.cols = fp.d.r;
+      u.op = EW_COPY;
+      ew.push_back(u);
+    }
+    if (!ew.empty()) STAGE(run_ew(ctx, ew, st, "ew_align"));
+    // operand views: the aligned copies where they exist
+    auto Uin = [&](const bkfac_brand_args& a) -> const float* {
+      const auto& fp = ctx->f[a.factor];
+      return fp.Us ? at<float>(ctx, fp.Us) : a.U_in;
+    };
+    auto Min = [&](const bkfac_brand_args& a) -> const float* {
+      const auto& fp = ctx->f[a.factor];
+      return fp.Ms ? at<float>(ctx, fp.Ms) : a.M;
+    };
+    auto ldin = [&](const bkfac_brand_args& a) -> int {
+      const auto& fp = ctx->f[a.factor];
+      return fp.Ms ? fp.nld : fp.d.n;
+    };
     // A: P = U^T M  -> W rows [0, r)
     for (int i : brand) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
-      GemmProb p = gp(a.U_in, n, a.M, n, at<float>(ctx, fp.W), fp.m, r, a.c, n, 1.f);
+      GemmProb p = gp(Uin(a), ldin(a), Min(a), ldin(a), at<float>(ctx, fp.W), fp.m, r, a.c, n, 1.f);
       gemm_ws(p, at<float>(ctx, fp.ws));
       gs.add(true, false, p, fp.ws_elems);
     }
@@ -961,8 +996,8 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
-      GemmProb pr = gp(a.U_in, n, at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), fp.nld, n, a.c,
-                       r, -1.f, a.M, n, 1.f);
+      GemmProb pr = gp(Uin(a), ldin(a), at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), fp.nld, n, a.c,
+                       r, -1.f, Min(a), ldin(a), 1.f);
       pr.status = status_ptr(ctx, a.factor);   // every element of M passes this epilogue
       gs.add(false, false, pr, 0);
     }
@@ -975,7 +1010,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       any_reorth = true;
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
-      GemmProb p = gp(a.U_in, n, at<float>(ctx, fp.R), fp.nld, at<float>(ctx, fp.P2), r, r, a.c, n, 1.f);
+      GemmProb p = gp(Uin(a), ldin(a), at<float>(ctx, fp.R), fp.nld, at<float>(ctx, fp.P2), r, r, a.c, n, 1.f);
       gemm_ws(p, at<float>(ctx, fp.ws));
       gs.add(true, false, p, fp.ws_elems);
     }
@@ -987,7 +1022,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         const auto& fp = ctx->f[a.factor];
         const int n = fp.d.n, r = fp.d.r;
         float* R = at<float>(ctx, fp.R);
-        gs.add(false, false, gp(a.U_in, n, at<float>(ctx, fp.P2), r, R, fp.nld, n, a.c, r, -1.f, R, fp.nld, 1.f), 0);
+        gs.add(false, false, gp(Uin(a), ldin(a), at<float>(ctx, fp.P2), r, R, fp.nld, n, a.c, r, -1.f, R, fp.nld, 1.f), 0);
         EwProb e{};
         e.Y = at<float>(ctx, fp.W); e.ldy = fp.m; e.X = at<float>(ctx, fp.P2); e.ldx = r;
         e.rows = r; e.cols = a.c; e.a = 1.f; e.op = EW_ADD;
@@ -1067,7 +1102,8 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const auto& fp = ctx->f[a.factor];
     const int n = fp.d.n, r = fp.d.r, mm = r + a.c, ro = rout_of(a);
     const float* V = at<float>(ctx, fp.eig.V);
-    GemmProb p = gp(a.U_in, n, V, mm, at<float>(ctx, fp.Urot), fp.nld, n, ro, mm, 1.f);
+    const float* U0 = fp.Us ? at<float>(ctx, fp.Us) : a.U_in;
+    GemmProb p = gp(U0, fp.Us ? fp.nld : n, V, mm, at<float>(ctx, fp.Urot), fp.nld, n, ro, mm, 1.f);
     p.A2 = at<float>(ctx, fp.R); p.lda2 = fp.nld;
     p.B2 = V + r; p.ldb2 = mm;
     p.k1 = r;

@@ -30,17 +30,19 @@ __global__ void ew_kernel(const __grid_constant__ EwBatch b) {
       p.Y[i + (long)i * p.ldy] += p.a * p.vec[i];
     return;
   }
-  const long total = (long)p.rows * p.cols;
-  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
-       e += (long)gridDim.x * blockDim.x) {
-    const int i = (int)(e % p.rows), j = (int)(e / p.rows);
-    float* y = p.Y + i + (long)j * p.ldy;
-    const float x = p.X[i + (long)j * p.ldx];
-    switch (p.op) {
-      case EW_ADD: *y += p.a * x; break;
-      case EW_SCALE_COLS: *y = x * p.vec[j]; break;
-      case EW_COPY: *y = x; break;
-      default: break;
+  // columns over blocks, rows over threads (coalesced, no index division)
+  for (int j = blockIdx.x; j < p.cols; j += gridDim.x) {
+    float* yc = p.Y + (long)j * p.ldy;
+    const float* xc = p.X + (long)j * p.ldx;
+    const float sj = (p.op == EW_SCALE_COLS) ? p.vec[j] : 1.f;
+    for (int i = threadIdx.x; i < p.rows; i += blockDim.x) {
+      const float x = xc[i];
+      switch (p.op) {
+        case EW_ADD: yc[i] += p.a * x; break;
+        case EW_SCALE_COLS: yc[i] = x * sj; break;
+        case EW_COPY: yc[i] = x; break;
+        default: break;
+      }
     }
   }
 }
