@@ -393,6 +393,42 @@ def precondition_factored(G: np.ndarray, A: np.ndarray, U_G: np.ndarray, D_G: np
 
 
 # --------------------------------------------------------------------------
+# §4.2 error protocol metrics -- NEXT-f4
+# --------------------------------------------------------------------------
+
+
+def reg_inverse_dense(U: np.ndarray, D: np.ndarray, lam: float, continuation: bool = False,
+                      lam_relative: bool = False) -> np.ndarray:
+    """The regularised inverse of a low-rank representation as a dense matrix
+    (Alg 1 lines 16-17, :403-405): U diag((D + lam)^{-1} - lam^{-1}) U^T + I / lam, with the
+    effective (D, lam) of reg_params."""
+    U = np.asarray(U, dtype=f64)
+    De, le = reg_params(D, lam, continuation, lam_relative)
+    s = 1.0 / (De + le) - 1.0 / le
+    return (U * s[None, :]) @ U.T + np.eye(U.shape[0]) / le
+
+
+def error_metrics(approx_A, approx_G, ref_A, ref_G, J: np.ndarray) -> Tuple[float, float, float, float]:
+    """§4.2 metrics: (1) ||A~^{-1} - A^{-1}_ref||_F / ||A^{-1}_ref||_F,
+    (2) the same for Gamma, (3) ||s~ - s_ref||_F / ||s_ref||_F, (4) 1 - cos(angle(s~, s_ref)),
+    with s = Gamma^{-1} J A^{-1} (the step of Alg 1 lines 14-17).  Each argument approx_* /
+    ref_* is (U, D, lam, continuation); the inverses are formed densely."""
+    Ai, Gi = reg_inverse_dense(*approx_A), reg_inverse_dense(*approx_G)
+    Ar, Gr = reg_inverse_dense(*ref_A), reg_inverse_dense(*ref_G)
+    J = np.asarray(J, dtype=f64)
+    s_t = Gi @ J @ Ai
+    s_r = Gr @ J @ Ar
+    m1 = float(np.linalg.norm(Ai - Ar) / np.linalg.norm(Ar))
+    m2 = float(np.linalg.norm(Gi - Gr) / np.linalg.norm(Gr))
+    nr = float(np.linalg.norm(s_r))
+    if nr == 0.0:
+        raise ValueError("ZeroReference: the reference step is zero (SPEC.md:342)")
+    m3 = float(np.linalg.norm(s_t - s_r) / nr)
+    m4 = float(1.0 - np.sum(s_t * s_r) / (np.linalg.norm(s_t) * nr))
+    return m1, m2, m3, m4
+
+
+# --------------------------------------------------------------------------
 # Stack driver (SURVEY §8(c) c7): init, Brand each step, optional RSVD overwrite
 # of the dense EA factor every T steps (Alg 5), preconditioning each step.
 # --------------------------------------------------------------------------

@@ -442,6 +442,35 @@ def test_light_correction_pins():
     assert np.abs(O.densify(U3, D3) - M2).max() < 1e-10 * np.abs(M2).max()
 
 
+# ---------------------------------------------------------------- §4.2 error metrics
+
+def test_error_metrics_pins():
+    """SPEC.md:343-346 examples: approx == ref -> all zero; approx = 2 x ref as an operator
+    -> m3 = 1, m4 = 0; m4 is invariant under positive rescaling; the dense inverse form
+    equals a direct inverse of U D U^T + lam I (independent of reg_inverse_dense's formula)."""
+    rng = np.random.default_rng(404)
+    dA, dG, rA, rG = 12, 9, 4, 3
+    UA, _ = np.linalg.qr(rng.standard_normal((dA, rA)))
+    UG, _ = np.linalg.qr(rng.standard_normal((dG, rG)))
+    DA, DG = np.array([5.0, 2.0, 1.0, 0.5]), np.array([3.0, 1.0, 0.2])
+    J = rng.standard_normal((dG, dA))
+    a, g = (UA, DA, 0.1, False), (UG, DG, 0.2, False)
+    assert max(abs(x) for x in O.error_metrics(a, g, a, g, J)) < 1e-14
+    Xi = O.reg_inverse_dense(UA, DA, 0.1)
+    assert np.abs(Xi - np.linalg.inv(UA @ np.diag(DA) @ UA.T + 0.1 * np.eye(dA))).max() < 1e-12
+    # "2 x ref as an operator": the approximate Gamma inverse is twice the reference one.
+    # lam/2 with D/2 gives (U D/2 U^T + lam/2 I)^{-1} = 2 (U D U^T + lam I)^{-1}
+    g2 = (UG, DG / 2, 0.1, False)
+    m1, m2, m3, m4 = O.error_metrics(a, g2, a, g, J)
+    assert abs(m2 - 1.0) < 1e-12 and abs(m3 - 1.0) < 1e-12 and abs(m4) < 1e-12 and m1 == 0.0
+    # m4 scale invariance: scale the approximate A inverse by 7 (D/7, lam/7)
+    b = (UA, DA * 1.3, 0.1, True)
+    b7 = (UA, DA * 1.3 / 7, 0.1 / 7, True)
+    m4a = O.error_metrics(b, g, a, g, J)[3]
+    m4b = O.error_metrics(b7, g, a, g, J)[3]
+    assert abs(m4a - m4b) < 1e-12
+
+
 # ---------------------------------------------------------------- B-R-KFAC chain
 
 def test_brkfac_chain_overwrite_equals_rsvd_then_brand():
