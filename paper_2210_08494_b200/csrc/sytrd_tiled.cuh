@@ -51,7 +51,8 @@ __host__ __device__ inline int syt_pos(int I, int J, int NB) {
   const int n = NB - 1 - J;
   return n * (n + 1) / 2 + (I - J);
 }
-inline int syt_vec_floats(int m_pad) { return 7 * m_pad + 64; }
+// vectors (6 m_pad + 64 scalars) + one m_pad of slack + a 96-float broadcast stage per warp
+inline int syt_vec_floats(int m_pad) { return 7 * m_pad + 64 + (SYT_THREADS / 32) * 96; }
 inline long syt_own_floats(int NB, int C) { return 1024L * ((syt_tiles(NB) + C - 1) / C); }
 // global-tile variant: vectors + a two-tile cp.async ring per warp
 inline int syt_gt_smem_floats(int m_pad) { return syt_vec_floats(m_pad) + (SYT_THREADS / 32) * 2048; }
@@ -125,7 +126,8 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   float* ys = ybuf + 2 * m_pad;      // m_pad      (summed y)
   float* wp = ys + m_pad;            // m_pad      (w_{k-1})
   float* scal = wp + m_pad;          // 64: [2] bad, [4..35] reduce, [40..41] alpha, d, [44..59] reduce 2, [60] y_k[k+1]
-  float* tiles = GT ? p.gtiles : scal + 64;   // owned tiles, slot s at 1024 s
+  float* bst = scal + 64 + (threadIdx.x >> 5) * 96;   // this warp's broadcast stage
+  float* tiles = GT ? p.gtiles : scal + 64 + (SYT_THREADS / 32) * 96;   // owned tiles, slot s at 1024 s
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = SYT_THREADS / 32;
   float* red = scal + 4;
@@ -187,36 +189,15 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
 #else
 #define SYT_T(i) do {} while (0)
 #endif
-  float* red2 = scal + 44;    // second reduction buffer: two block sums in one phase
-  // v_k, tau_k from column k (already carrying the pending update in x = v[]): scale,
-  // the reflector to K, d / e / tau (CTA k % C); returns tau_k
-  auto finish = [&](int kk, float ss, float* vv) -> float {
-    const float dk = scal[40], alpha = scal[41];
-    float tk, beta, scale;
-    if (ss == 0.f) {
-      tk = 0.f; beta = alpha; scale = 0.f;
-    } else {
-      const float nrm = sqrtf(alpha * alpha + ss);
-      beta = alpha >= 0.f ? -nrm : nrm;
-      tk = (beta - alpha) / beta;
-      scale = 1.f / (alpha - beta);
-    }
-    const bool writer = (q == kk % C);
-    float* kcol = K + (long)kk * ld;
-    for (int i = kk + 1 + tid; i < m; i += SYT_THREADS) {
-      float vi = 1.f;
-      if (i >= kk + 2) { vi = vv[i] * scale; if (writer) kcol[i] = vi; }
-      vv[i] = vi;
-    }
-    if (tid == 0) {
-      vv[kk] = 0.f;
-      if (kk >= 1) vv[kk - 1] = 0.f;           // stale 1 of v_{kk-2} (same parity buffer)
-      if (writer) { p.d[kk] = dk; p.e[kk] = beta; p.tau[kk] = tk; }
-    }
-    return tk;
+  float* red2 = scal + 44;    // per-warp partial sums of ||x||^2 of the next reflector
+  // The reflector v_k is kept UNSCALED in vbuf (x = column k with the pending updates);
+  // dlarfg's scaling is applied on read: v_k[i] = 0 (i <= k), 1 (i = k+1), x_i s_k (i >= k+2).
+  // Its norm is reduced through the barrier that opens step k, so forming v_k costs no
+  // barrier and no pass of its own.
+  auto vget = [](const float* buf, int kk, float s, int i) -> float {
+    return i >= kk + 2 ? buf[i] * s : (i == kk + 1 ? 1.f : 0.f);
   };
-  // (a) for step 0: column 0 (no pending update) -> v_0, tau_0
-  float tau;
+  // (a) for step 0: column 0 (no pending update)
   {
     float ss = 0.f;
     for (int i = tid; i < m; i += SYT_THREADS) {
@@ -226,9 +207,10 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       else scal[40 + i] = x;
       vbuf[i] = x;
     }
-    ss = syt_block_sum(ss, red);
-    tau = finish(0, ss, vbuf);
+    ss = warp_sum(ss);
+    if (lane == 0) red2[warp] = ss;
   }
+  float tau = 0.f, sc = 0.f, sc_prev = 0.f;   // tau_k, scale of v_k, scale of v_{k-1}
   SYT_T(0);
   for (int k = 0; k < m - 2; ++k) {
     float* v = vbuf + (k & 1) * m_pad;            // v_k
@@ -236,27 +218,68 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     float* y = ybuf + (k & 1) * m_pad;
     const bool have_prev = k > 0;
     const int kb = k >> 5;
-    __syncthreads();                              // v_k, w_{k-1}, zeroed y visible
+    __syncthreads();              // raw v_k + its norm partials, w_{k-1}, zeroed y visible
+    {
+      // dlarfg for v_k, redundantly in every thread (same inputs and order: identical)
+      float t = red2[lane & (NW - 1)];
+#pragma unroll
+      for (int o = NW / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      const float dk = scal[40], alpha = scal[41];
+      float tk, beta, scale;
+      if (t == 0.f) {
+        tk = 0.f; beta = alpha; scale = 0.f;
+      } else {
+        const float nrm = sqrtf(alpha * alpha + t);
+        beta = alpha >= 0.f ? -nrm : nrm;
+        tk = (beta - alpha) / beta;
+        scale = 1.f / (alpha - beta);
+      }
+      sc_prev = sc; sc = scale; tau = tk;
+      if (q == k % C) {             // the reflector (rows >= k+2) and d, e, tau to global
+        float* kcol = K + (long)k * ld;
+        for (int i = k + 2 + tid; i < m; i += SYT_THREADS) kcol[i] = v[i] * scale;
+        if (tid == 0) { p.d[k] = dk; p.e[k] = beta; p.tau[k] = tk; }
+      }
+    }
     SYT_T(1);
     // (b) active tiles (J >= kb): this CTA's slots 0 .. nact-1, one per warp
     const int nact = (syt_tiles(NB - kb) - q + C - 1) / C;
     // one tile: pending update (v_{k-1}, w_{k-1}) written back to tcol, partial y = A v_k
     auto tile_work = [&](float (&colv)[32], int I, int J, float* tcol) {
       const int i = 32 * I + lane;
-      const float cv = v[32 * J + lane], cvp = vp[32 * J + lane], cwp = wp[32 * J + lane];
-      const float vi = v[i], vpi = vp[i], wpi = wp[i];
+      const float cv = vget(v, k, sc, 32 * J + lane), cvp = vget(vp, k - 1, sc_prev, 32 * J + lane);
+      const float cwp = wp[32 * J + lane];
+      const float vi = vget(v, k, sc, i), vpi = vget(vp, k - 1, sc_prev, i), wpi = wp[i];
       float racc[4] = {0.f, 0.f, 0.f, 0.f};
       if ((32 * J > k) && (I > J)) {
+        // interior tile: the column-indexed values go through the warp's shared stage as
+        // (cwp, cwp, cvp, cvp) float4 and (cv, cv) float2 pairs read by broadcast, and the
+        // arithmetic runs on column pairs (FFMA2): no shuffles in the element loop
+        bst[(lane >> 1) * 4 + (lane & 1)] = cwp;
+        bst[(lane >> 1) * 4 + 2 + (lane & 1)] = cvp;
+        bst[64 + lane] = cv;
+        __syncwarp();
+        const float4* q4 = reinterpret_cast<const float4*>(bst);
+        const float2* v2 = reinterpret_cast<const float2*>(bst + 64);
+        const float2 nvp2 = make_float2(-vpi, -vpi), nwp2 = make_float2(-wpi, -wpi), vi2 = make_float2(vi, vi);
+        float2 r2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          float x = colv[jj];
+        for (int pp = 0; pp < 16; ++pp) {
+          float2 x2 = make_float2(colv[2 * pp], colv[2 * pp + 1]);
           if (have_prev) {
-            x -= vpi * __shfl_sync(0xffffffffu, cwp, jj) + wpi * __shfl_sync(0xffffffffu, cvp, jj);
-            tcol[jj * 32] = x;
+            const float4 q = q4[pp];
+            x2 = __ffma2_rn(nvp2, make_float2(q.x, q.y), x2);
+            x2 = __ffma2_rn(nwp2, make_float2(q.z, q.w), x2);
+            tcol[(2 * pp) * 32] = x2.x;
+            tcol[(2 * pp + 1) * 32] = x2.y;
           }
-          racc[jj & 3] = fmaf(x, __shfl_sync(0xffffffffu, cv, jj), racc[jj & 3]);
-          colv[jj] = x * vi;
+          r2[pp & 1] = __ffma2_rn(x2, v2[pp], r2[pp & 1]);
+          const float2 c2 = __fmul2_rn(x2, vi2);
+          colv[2 * pp] = c2.x;
+          colv[2 * pp + 1] = c2.y;
         }
+        __syncwarp();                               // the stage is rewritten by the next tile
+        racc[0] = r2[0].x; racc[1] = r2[0].y; racc[2] = r2[1].x; racc[3] = r2[1].y;
       } else {
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
@@ -292,7 +315,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     if constexpr (GT) {
       // tiles in global memory (L2 / HBM): each warp streams its tiles through a two-deep
       // shared-memory ring with cp.async, the next tile in flight while this one computes
-      float* stg = scal + 64 + warp * 2048;
+      float* stg = scal + 64 + NW * 96 + warp * 2048;
       auto issue = [&](int sl2, int bi) {
         const float* src = tiles + 1024L * sl2;
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stg + bi * 1024));
@@ -335,9 +358,8 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
         tile_work(colv, I, J, tcol);
       }
     }
-    __syncthreads();
     SYT_T(2);
-    if (C > 1) cluster.sync();                    // partial y (and column k+1) ready
+    if (C > 1) cluster.sync(); else __syncthreads();   // partial y (and column k+1) ready
     SYT_T(3);
     // (c)+(a) merged: y_k summed through DSMEM -> w_k; in the same pass column k+1 is read
     // from its owners, gets the pending update (v_k, w_k) and yields v_{k+1}, tau_{k+1}
@@ -352,20 +374,25 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       float si[4] = {0.f, 0.f, 0.f, 0.f}, xi[4] = {0.f, 0.f, 0.f, 0.f}, vi4[4] = {0.f, 0.f, 0.f, 0.f};
       float pv = 0.f;
       if (own) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int r = 0; r < C; ++r) {
-          const float4 t4 = (C == 1) ? *reinterpret_cast<const float4*>(y + i0) : syt_dsmem_ld4(y + i0, r);
-          acc.x += t4.x; acc.y += t4.y; acc.z += t4.z; acc.w += t4.w;
-        }
-        si[0] = acc.x; si[1] = acc.y; si[2] = acc.z; si[3] = acc.w;
+        // all C + 1 remote loads in flight together, then the sums
+        float4 t4[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (r < C) t4[r] = (C == 1) ? *reinterpret_cast<const float4*>(y + i0) : syt_dsmem_ld4(y + i0, r);
+        float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (next) {
           const int pos = base1 + (i0 >> 5) - kb1;
           const float* src = tiles + 1024L * (pos / C) + jk1 * 32 + (i0 & 31);
-          const float4 c4 = (C == 1) ? *reinterpret_cast<const float4*>(src) : syt_dsmem_ld4(src, pos % C);
-          xi[0] = c4.x; xi[1] = c4.y; xi[2] = c4.z; xi[3] = c4.w;
+          c4 = (C == 1) ? *reinterpret_cast<const float4*>(src) : syt_dsmem_ld4(src, pos % C);
         }
-        const float4 v4 = *reinterpret_cast<const float4*>(v + i0);
-        vi4[0] = v4.x; vi4[1] = v4.y; vi4[2] = v4.z; vi4[3] = v4.w;
+        float4 acc = t4[0];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+          if (r < C) { acc.x += t4[r].x; acc.y += t4[r].y; acc.z += t4[r].z; acc.w += t4[r].w; }
+        si[0] = acc.x; si[1] = acc.y; si[2] = acc.z; si[3] = acc.w;
+        xi[0] = c4.x; xi[1] = c4.y; xi[2] = c4.z; xi[3] = c4.w;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) vi4[u] = vget(v, k, sc, i0 + u);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if (i0 + u >= k1 && i0 + u < m) pv = fmaf(si[u], vi4[u], pv);
@@ -380,7 +407,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       SYT_T(6);
       const float s1 = scal[60];
       const float gamma = 0.5f * tau * tau * pv;
-      const float vk1 = v[k1];
+      const float vk1 = 1.f;                       // v_k[k+1]
       const float wk1 = tau * s1 - gamma * vk1;
       float* vn = vbuf + (k1 & 1) * m_pad;         // v_{k+1} (v_{k-1} is no longer needed)
       float ss = 0.f;
@@ -395,7 +422,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
             const float x = xi[u] - (vi4[u] * wk1 + w * vk1);
             if (i >= k1 + 2) ss = fmaf(x, x, ss);
             else scal[40 + (i - k1)] = x;         // d_{k+1} (i = k+1), alpha (i = k+2)
-            vn[i] = x;
+            vn[i] = x;                              // raw; scaled on read
           }
         }
       }
@@ -404,9 +431,9 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
         float* yn = ybuf + (k1 & 1) * m_pad;       // step k-1's partials: every reader is done
         for (int i = tid; i < m_pad; i += SYT_THREADS) yn[i] = 0.f;
         SYT_T(7);
-        ss = syt_block_sum(ss, red2);
+        ss = warp_sum(ss);                          // reduced after the next step's barrier
+        if (lane == 0) red2[warp] = ss;
         SYT_T(8);
-        tau = finish(k1, ss, vn);
       }
     }
     SYT_T(4);
@@ -427,7 +454,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       const int pos = syt_pos(i >> 5, j >> 5, NB);
       if (pos % C == q) {
         float* a = tiles + 1024L * (pos / C) + (j & 31) * 32 + (i & 31);
-        const float x = *a - (vq[i] * wp[j] + wp[i] * vq[j]);
+        const float x = *a - (vget(vq, m - 3, sc, i) * wp[j] + wp[i] * vget(vq, m - 3, sc, j));
         *a = x;
         if (tid == 0) { p.d[m - 2] = x; p.tau[m - 2] = 0.f; }
         if (tid == 1) { p.e[m - 2] = x; p.e[m - 1] = 0.f; }
