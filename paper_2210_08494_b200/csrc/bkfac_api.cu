@@ -452,7 +452,10 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
             msub = std::max(msub, b.p[i].m);
           }
         if (sb.nprob == 0) continue;
-        gC[ngroups] = Cs[ci]; gm[ngroups] = msub; ++ngroups;
+        int Cg = Cs[ci];
+        static const int c_force = [] { const char* e = getenv("BKFAC_SYT_C"); return e ? atoi(e) : 0; }();
+        if (c_force > Cg && Cg >= 2) Cg = std::min(c_force, 8);   // tuning: wider clusters
+        gC[ngroups] = Cg; gm[ngroups] = msub; ++ngroups;
       }
       const bool fork = ngroups > 1 && ctx->ev_fork != nullptr;
       if (fork && !cuda_ok(cudaEventRecord(ctx->ev_fork, st))) return BKFAC_ERR_CUDA;

@@ -134,7 +134,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   const int ntiles = syt_tiles(NB);
   const int nown = (ntiles - q + C - 1) / C;          // tiles owned by this CTA
   // address of `ptr` in CTA r of the cluster (plain local pointer for 1-CTA launches)
-  auto rptr = [&](float* ptr, int r) -> float* { return C == 1 ? ptr : cluster.map_shared_rank(ptr, r); };
+  auto rptr = [&](float* ptr, int r) -> float* { return (GT || C == 1) ? ptr : cluster.map_shared_rank(ptr, r); };
   // (I, J) of the tile at enumeration position pos (inverse of syt_pos)
   auto tile_ij = [&](int pos, int& I, int& J) {
     int n = (int)((sqrtf(8.f * pos + 1.f) - 1.f) * 0.5f);   // largest n: n(n+1)/2 <= pos
@@ -162,10 +162,10 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   }
   bad = __syncthreads_or(bad);
   if (tid == 0) scal[2] = bad ? 1.f : 0.f;
-  if (C > 1) cluster.sync(); else __syncthreads();
+  if (!GT && C > 1) cluster.sync(); else __syncthreads();
   float anybad = 0.f;
   for (int r = 0; r < C; ++r) anybad += *rptr(scal + 2, r);
-  if (C > 1) cluster.sync(); else __syncthreads();
+  if (!GT && C > 1) cluster.sync(); else __syncthreads();
   if (anybad != 0.f) {
     if (q == 0) {
       if (tid == 0 && p.status) atomicOr(p.status, ST_NONFINITE);
@@ -359,7 +359,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       }
     }
     SYT_T(2);
-    if (C > 1) cluster.sync(); else __syncthreads();   // partial y (and column k+1) ready
+    if (!GT && C > 1) cluster.sync(); else __syncthreads();   // partial y (and column k+1) ready
     SYT_T(3);
     // (c)+(a) merged: y_k summed through DSMEM -> w_k; in the same pass column k+1 is read
     // from its owners, gets the pending update (v_k, w_k) and yields v_{k+1}, tau_{k+1}
@@ -374,21 +374,28 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       float si[4] = {0.f, 0.f, 0.f, 0.f}, xi[4] = {0.f, 0.f, 0.f, 0.f}, vi4[4] = {0.f, 0.f, 0.f, 0.f};
       float pv = 0.f;
       if (own) {
-        // all C + 1 remote loads in flight together, then the sums
-        float4 t4[8];
+        float4 acc, c4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (GT || C == 1) {                         // one CTA (global tiles: always): local
+          acc = *reinterpret_cast<const float4*>(y + i0);
+          if (next) {
+            const int pos = base1 + (i0 >> 5) - kb1;
+            c4 = *reinterpret_cast<const float4*>(tiles + 1024L * pos + jk1 * 32 + (i0 & 31));
+          }
+        } else {
+          // all C + 1 remote loads in flight together, then the sums
+          float4 t4[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
-          if (r < C) t4[r] = (C == 1) ? *reinterpret_cast<const float4*>(y + i0) : syt_dsmem_ld4(y + i0, r);
-        float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (next) {
-          const int pos = base1 + (i0 >> 5) - kb1;
-          const float* src = tiles + 1024L * (pos / C) + jk1 * 32 + (i0 & 31);
-          c4 = (C == 1) ? *reinterpret_cast<const float4*>(src) : syt_dsmem_ld4(src, pos % C);
+          for (int r = 0; r < 8; ++r)
+            if (r < C) t4[r] = syt_dsmem_ld4(y + i0, r);
+          if (next) {
+            const int pos = base1 + (i0 >> 5) - kb1;
+            c4 = syt_dsmem_ld4(tiles + 1024L * (pos / C) + jk1 * 32 + (i0 & 31), pos % C);
+          }
+          acc = t4[0];
+#pragma unroll
+          for (int r = 1; r < 8; ++r)
+            if (r < C) { acc.x += t4[r].x; acc.y += t4[r].y; acc.z += t4[r].z; acc.w += t4[r].w; }
         }
-        float4 acc = t4[0];
-#pragma unroll
-        for (int r = 1; r < 8; ++r)
-          if (r < C) { acc.x += t4[r].x; acc.y += t4[r].y; acc.z += t4[r].z; acc.w += t4[r].w; }
         si[0] = acc.x; si[1] = acc.y; si[2] = acc.z; si[3] = acc.w;
         xi[0] = c4.x; xi[1] = c4.y; xi[2] = c4.z; xi[3] = c4.w;
 #pragma unroll
@@ -462,7 +469,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       }
     }
   }
-  if (C > 1) cluster.sync();   // no CTA exits while others may still address its smem
+  if (!GT && C > 1) cluster.sync();   // no CTA exits while others may still address its smem
 }
 
 }  // namespace bkfac
