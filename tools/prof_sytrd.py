@@ -23,5 +23,5 @@ if len(sys.argv) > 5 and sys.argv[5] == "time":
         ctx.bkfac_brand_update(ups)
     torch.cuda.synchronize()
     for s in ctx.bkfac_profile_read():
-        if s["name"].startswith("eig"):
+        if s["name"].startswith(("eig", "chol")):
             print(f"{s['name']:14s} {s['ms'] / max(s['calls'], 1):8.4f} ms/call")

@@ -71,7 +71,9 @@ def main():
                 t[0] += n
                 t[1] += by
     # the EA accumulate: the symmetric gemm_tc variant with 8 epilogue warps
-    ea = [v for k, v in agg.items() if k.startswith("gemm_tc_kernel<0, 1") and k.rstrip(">").endswith("8")]
+    # template args <TA, TB, BN, NLW, DEPTH, EPI, PAIR>: TB = 1 with EPI = 8
+    ea = [v for k, v in agg.items() if k.startswith("gemm_tc_kernel<0, 1,")
+          and k.split("<")[1].rstrip(">").split(",")[5].strip() == "8"]
     if ea:
         traffic["gemm_ea"] = [sum(v[0] for v in ea), sum(v[2] for v in ea)]
     out.append("# not the library's (outside the timed region): " + ", ".join(
