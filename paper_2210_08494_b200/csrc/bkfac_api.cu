@@ -422,16 +422,16 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
       const double m = b.p[i].m, r = b.p[i].r;
       m3 += m * m * m; m2 += m * m; m2r += m * m * r; mr += m * r;
     }
-    if (ctx->pending_ea) {   // bkfac_brand_ea_update: EA GEMM beside the tridiagonalisation
-      int busy = 0;
+    // bkfac_brand_ea_update: the EA GEMM runs beside the tridiagonalisation on the SMs its
+    // clusters leave idle.  It depends only on the work before this point (fork event here)
+    // but is SUBMITTED after the tridiagonalisation, so the clusters are placed first.
+    int ea_busy = 0;
+    if (ctx->pending_ea) {
       for (size_t i = 0; i < n; ++i) {
         const int C = sytrd_tiled_cluster(b.p[i].m);
-        busy += C == 0 ? 1 : C;
+        ea_busy += C == 0 ? 1 : C;
       }
-      auto f = std::move(ctx->pending_ea);
-      ctx->pending_ea = nullptr;
-      const bkfac_status re = f(busy);
-      if (re != BKFAC_OK) return re;
+      if (!cuda_ok(cudaEventRecord(ctx->ev_ea_fork, st))) return BKFAC_ERR_CUDA;
     }
     // sytrd: 4/3 m^3 flops; algorithmic bytes: read K (lower), write reflectors + T
     prof_begin(ctx, "eig_sytrd", st, 4.0 / 3.0 * m3, 4.0 * m2);
@@ -490,6 +490,12 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
           if (!cuda_ok(cudaStreamWaitEvent(st, ctx->ev_join[g - 1], 0))) return BKFAC_ERR_CUDA;
     }
     prof_end(ctx, st);
+    if (ctx->pending_ea) {
+      auto f = std::move(ctx->pending_ea);
+      ctx->pending_ea = nullptr;
+      const bkfac_status re = f(ea_busy);
+      if (re != BKFAC_OK) return re;
+    }
 #ifdef BKFAC_SYT_TIMING
     i0 += n;
     continue;   // tuning builds: keep the sytrd timing sums in Y
@@ -1213,8 +1219,10 @@ bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, 
   bkfac_status r = ea_stage(ctx, ea_args, ea_count, gs);
   if (r != BKFAC_OK) return r;
   if (ea_count == 0) return bkfac_brand_update(ctx, args, count, stream);
-  static const int ea_mode = [] { const char* e = getenv("BKFAC_EA_MODE"); return e ? atoi(e) : 1; }();
-  if (ea_mode == 1) {   // tuning: EA first, full grid, on the caller's stream
+  // 0 (default): EA GEMM on a side stream beside the tridiagonalisation, grid capped at the
+  // SMs its clusters leave idle; 2: the same, uncapped; 1: EA first, serially, full grid
+  static const int ea_mode = [] { const char* e = getenv("BKFAC_EA_MODE"); return e ? atoi(e) : 0; }();
+  if (ea_mode == 1) {
     r = run_gemms(ctx, gs, static_cast<cudaStream_t>(stream), "gemm_ea");
     return r != BKFAC_OK ? r : bkfac_brand_update(ctx, args, count, stream);
   }
@@ -1224,10 +1232,10 @@ bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, 
   if (dev_prev != ctx->device) cudaSetDevice(ctx->device);
   bool launched = false;
   ctx->pending_ea = [&](int busy) -> bkfac_status {
-    if (!cuda_ok(cudaEventRecord(ctx->ev_ea_fork, st)) ||
-        !cuda_ok(cudaStreamWaitEvent(ctx->ea_stream, ctx->ev_ea_fork, 0)))
+    if (!cuda_ok(cudaStreamWaitEvent(ctx->ea_stream, ctx->ev_ea_fork, 0)))   // recorded by run_eig
       return BKFAC_ERR_CUDA;
-    ctx->grid_cap = ea_mode == 2 ? 0 : std::max(kNumSM / 8, kNumSM - busy);
+    static const int ea_cap = [] { const char* e = getenv("BKFAC_EA_CAP"); return e ? atoi(e) : 0; }();
+    ctx->grid_cap = ea_mode == 2 ? 0 : (ea_cap > 0 ? ea_cap : std::max(kNumSM / 8, kNumSM - busy));
     const bkfac_status re = run_gemms(ctx, gs, ctx->ea_stream, "gemm_ea");
     ctx->grid_cap = 0;
     if (re != BKFAC_OK) return re;
