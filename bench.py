@@ -205,13 +205,17 @@ def roofline_from_stages(stages, peaks, clocks):
     return roof, table
 
 
-def traffic_lookup(kernel_stage: str):
+def traffic_lookup(kernel_stage: str, workload: str):
+    """DRAM bytes per launch of the stage's kernel from the committed ncu launch list, when
+    that list was taken on this workload (else None)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(path):
         return None
     try:
         with open(path) as f:
             d = json.load(f)
+        if d.get("workload") != workload:
+            return None
         return d.get(kernel_stage)
     except (OSError, ValueError):
         return None
@@ -452,7 +456,8 @@ def run_ours(args, rank, world, local_rank):
         s["path"] = "tc" if os.environ.get("BKFAC_GEMM", "tc") != "simt" and stack_uses_tc(stack) else "simt"
     roof, table = roofline_from_stages(stages, peaks, clocks)
     if roof is not None:
-        roof["traffic"] = traffic_lookup(roof["kernel"])
+        variant = ((args.full_rank or args.factored or args.correct_every) and "+variant") or ""
+        roof["traffic"] = traffic_lookup(roof["kernel"], cfg.name + variant)
         roof["launches_per_step"] = round(next(s["launches"] for s in stages
                                                if s["name"] == roof["kernel"]) / args.steps, 2)
     cpu = None
