@@ -351,6 +351,21 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
       bool nonfinite = false;   // inf/NaN in C0 (the operands' tensor-core path cannot report it)
       const float beta = p.beta_dev ? *p.beta_dev : p.beta;
       float* w = p.splits > 1 ? p.ws + (long)x.split * p.M * p.N : nullptr;
+      // C0 of this warp's rows x columns into L2 while the tile's K loop runs: the final
+      // epilogue then waits for L2, not HBM, on each of its column groups
+      if (!w && beta != 0.f && nblk > 0) {
+        const int r0 = x.m0 + quarter * 32;
+        if (r0 < p.M) {
+          const int r1 = min(r0 + 31, p.M - 1);
+          for (int c = lane; c < 16 * GPW; c += 32) {
+            const int j = x.n0 + g_beg * 16 + c;
+            if (j >= p.N) break;
+            const float* col = p.C0 + (long)j * p.ldc0;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(col + r0));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(col + r1));
+          }
+        }
+      }
       for (int blk = 0; blk < nblk; ++blk, ++kb) {
         const int buf = kb & 1;
         const bool last = blk == nblk - 1;

@@ -643,3 +643,108 @@ def test_bkfac_c_stack_chain(cuda_lib):
     Ug, Dg = st.state(0)
     assert lowrank_rel_err(U, D, from_dev_cols(Ug), Dg.double().cpu().numpy()) < TOL_CHAIN
     assert st.check()[0] == 0
+
+
+# ------------------------------------------------------------------ full size, bench launch configuration
+
+def test_cfg4_stack_bench_launch_config_sampled(cuda_lib):
+    """configs[3] at full size in the launch configuration bench.py times: the whole
+    32-factor / 16-layer stack, dense EA on the side stream beside the eigensolver, steps
+    after the first replayed from a CUDA graph with the inputs refilled in place.  Sampled
+    outputs against the oracle's chain on the same fp32 inputs: four factors (dense path
+    n = 28, Brand paths n = 577 / 4609 / 512, fc2's n = 10), their EA factors, and the
+    preconditioned gradients of fc0 and conv12 (Alg 4 :540-548, Eq. 8 :565,
+    Alg 1 lines 16-17 :403-405)."""
+    import torch
+    from paper_2210_08494_b200 import BKFACStack
+    cfg = synth.cfg4_vgg_sharded()
+    factors = [(f.n, f.r, f.c) for f in cfg.factors]
+    layers = [(L.d_G, L.d_A, L.g_index, L.a_index) for L in cfg.layers]
+    st = BKFACStack(factors, layers, cfg.rho, cfg.lam, rsvd_every=cfg.rsvd_every,
+                    oversample=cfg.oversample, power_iters=cfg.power_iters)
+    Mbuf = {g: torch.empty((f.c, f.n), device="cuda") for g, f in enumerate(cfg.factors)}
+    Jbuf = {li: torch.empty((L.d_G, L.d_A), device="cuda") for li, L in enumerate(cfg.layers)}
+    names = [f.name for f in cfg.factors]
+    sample = [names.index(x) for x in ("conv0.A", "conv1.A", "conv12.A", "conv12.G", "fc2.G")]
+    lnames = [L.name for L in cfg.layers]
+    lsample = [lnames.index("fc0"), lnames.index("conv12")]
+    for li in lsample:
+        for g in (cfg.layers[li].g_index, cfg.layers[li].a_index):
+            if g not in sample:
+                sample.append(g)
+    states = {g: None for g in sample}
+    Kor = {g: None for g in sample}
+    steps = 4
+    for k in range(steps):
+        for g, f in enumerate(cfg.factors):
+            Mbuf[g].copy_(torch.from_numpy(np.ascontiguousarray(f.batch(k).T)))
+        for li, L in enumerate(cfg.layers):
+            Jbuf[li].copy_(torch.from_numpy(L.grad(k)))
+        S = st.step(Mbuf, Jbuf, graph=True)
+        for g in sample:
+            n, r, c = factors[g]
+            Mk = cfg.factors[g].batch(k).astype(np.float64)
+            if states[g] is None:
+                states[g] = O.brand_update(synth.phantom_basis(n, r), np.zeros(r), Mk, 0.0, 1.0, r)
+            else:
+                U, D = states[g]
+                states[g] = O.brand_update(U, D, Mk, cfg.rho, 1 - cfg.rho, r)
+            Kor[g] = O.ea_update(Kor[g], Mk, cfg.rho)
+    torch.cuda.synchronize()
+    assert st.check()[0] == 0
+    for g in sample:
+        Ug, Dg = st.state(g)
+        Uo, Do = states[g]
+        assert lowrank_rel_err(Uo, Do, from_dev_cols(Ug), Dg.double().cpu().numpy()) < TOL_CHAIN, names[g]
+        Kg = st.K[st.local[g]].double().cpu().numpy()
+        assert np.linalg.norm(Kg - Kor[g]) / np.linalg.norm(Kor[g]) < 1e-5, names[g]
+    for li in lsample:
+        L = cfg.layers[li]
+        UG, DG = states[L.g_index]
+        UA, DA = states[L.a_index]
+        J = L.grad(steps - 1).astype(np.float64)
+        So = O.precondition(J, UG, DG, cfg.lam, UA, DA, cfg.lam)
+        Sg = S[li].double().cpu().numpy()
+        assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC, lnames[li]
+
+
+def test_cfg5_block_stack_bench_launch_config_sampled(cuda_lib):
+    """configs[4]'s factor and layer shapes (one transformer block: 4097 -> 16384 and
+    16385 -> 4096; n_BS = 1024, r = 512; global-tile tridiagonalisation of the 1536 cores)
+    through the stack in bench.py's launch configuration (graph replay after the first
+    step), 3 steps; every factor and both preconditioned gradients against the oracle."""
+    import torch
+    from paper_2210_08494_b200 import BKFACStack
+    cfg = synth.cfg5_transformer(blocks=1, steps=3)
+    factors = [(f.n, f.r, f.c) for f in cfg.factors]
+    layers = [(L.d_G, L.d_A, L.g_index, L.a_index) for L in cfg.layers]
+    st = BKFACStack(factors, layers, cfg.rho, cfg.lam)
+    Mbuf = {g: torch.empty((f.c, f.n), device="cuda") for g, f in enumerate(cfg.factors)}
+    Jbuf = {li: torch.empty((L.d_G, L.d_A), device="cuda") for li, L in enumerate(cfg.layers)}
+    states = [None] * len(factors)
+    steps = 3
+    for k in range(steps):
+        for g, f in enumerate(cfg.factors):
+            Mbuf[g].copy_(torch.from_numpy(np.ascontiguousarray(f.batch(k).T)))
+        for li, L in enumerate(cfg.layers):
+            Jbuf[li].copy_(torch.from_numpy(L.grad(k)))
+        S = st.step(Mbuf, Jbuf, graph=True)
+        for g, (n, r, c) in enumerate(factors):
+            Mk = cfg.factors[g].batch(k).astype(np.float64)
+            if states[g] is None:
+                states[g] = O.brand_update(synth.phantom_basis(n, r), np.zeros(r), Mk, 0.0, 1.0, r)
+            else:
+                U, D = states[g]
+                states[g] = O.brand_update(U, D, Mk, cfg.rho, 1 - cfg.rho, r)
+    torch.cuda.synchronize()
+    assert st.check()[0] == 0
+    for g in range(len(factors)):
+        Ug, Dg = st.state(g)
+        Uo, Do = states[g]
+        assert lowrank_rel_err(Uo, Do, from_dev_cols(Ug), Dg.double().cpu().numpy()) < TOL_CHAIN, g
+    for li, L in enumerate(cfg.layers):
+        UG, DG = states[L.g_index]
+        UA, DA = states[L.a_index]
+        So = O.precondition(L.grad(steps - 1).astype(np.float64), UG, DG, cfg.lam, UA, DA, cfg.lam)
+        Sg = S[li].double().cpu().numpy()
+        assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC, li
