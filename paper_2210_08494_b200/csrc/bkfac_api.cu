@@ -119,7 +119,8 @@ struct bkfac_ctx_s {
   cudaStream_t ea_stream = nullptr;
   cudaEvent_t ev_ea_fork = nullptr, ev_ea_done = nullptr;
   std::function<bkfac_status(int)> pending_ea;
-  int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs
+  int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs; < 0: one CTA per tile
+  bool ea_join_early = false;   // join the side-stream EA right after the tridiagonalisation
   int pair_mode = 1;  // CTA-pair GEMM tiles: 0 never, 1 large long-K stages, 2 always (tests)
   // optional per-stage CUDA-event profiling (bkfac_profile_enable)
   bool prof = false;
@@ -230,7 +231,8 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
     if (tiles > 0) {
       if (tc) {
         const int nsm = ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM;
-        const int grid = std::min(tiles, pair ? nsm / 2 : nsm);   // pair: CTA pairs
+        // grid_cap < 0: one CTA per tile (a background job whose CTAs retire quickly)
+        const int grid = ctx->grid_cap < 0 ? tiles : std::min(tiles, pair ? nsm / 2 : nsm);
         if (!cuda_ok(tc_launch<TA, TB>(b, grid, st, max_chunks <= TC_SHORT_K_CHUNKS, pair)))
           return BKFAC_ERR_CUDA;
       } else {
@@ -473,13 +475,18 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
           cfg.blockDim = dim3(SYT_THREADS, 1, 1);
           cfg.dynamicSmemBytes = sytrd_tiled_smem_bytes(msub, C);
           cfg.stream = sg;
-          cudaLaunchAttribute attr[1];
+          cudaLaunchAttribute attr[2];
           attr[0].id = cudaLaunchAttributeClusterDimension;
           attr[0].val.clusterDim.x = (unsigned)C;
           attr[0].val.clusterDim.y = 1;
           attr[0].val.clusterDim.z = 1;
+          // highest scheduling priority: when the EA GEMM runs beside (bkfac_brand_ea_update),
+          // pending clusters are placed before its pending CTAs
+          static const int prio = [] { int lo = 0, hi = 0; cudaDeviceGetStreamPriorityRange(&lo, &hi); return hi; }();
+          attr[1].id = cudaLaunchAttributePriority;
+          attr[1].val.priority = prio;
           cfg.attrs = attr;
-          cfg.numAttrs = 1;
+          cfg.numAttrs = 2;
           if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_tiled_kernel<false>, sub[g], C))) return BKFAC_ERR_CUDA;
         }
         LAUNCH_CHECK(ctx);
@@ -495,6 +502,9 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
       ctx->pending_ea = nullptr;
       const bkfac_status re = f(ea_busy);
       if (re != BKFAC_OK) return re;
+      // mode 4: the rest of the eigensolver waits for the EA (which then only shares the GPU
+      // with the tridiagonalisation)
+      if (ctx->ea_join_early && !cuda_ok(cudaStreamWaitEvent(st, ctx->ev_ea_done, 0))) return BKFAC_ERR_CUDA;
     }
 #ifdef BKFAC_SYT_TIMING
     i0 += n;
@@ -1235,7 +1245,9 @@ bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, 
     if (!cuda_ok(cudaStreamWaitEvent(ctx->ea_stream, ctx->ev_ea_fork, 0)))   // recorded by run_eig
       return BKFAC_ERR_CUDA;
     static const int ea_cap = [] { const char* e = getenv("BKFAC_EA_CAP"); return e ? atoi(e) : 0; }();
-    ctx->grid_cap = ea_mode == 2 ? 0 : (ea_cap > 0 ? ea_cap : std::max(kNumSM / 8, kNumSM - busy));
+    ctx->grid_cap = ea_mode == 2 ? 0 : (ea_mode == 3 || ea_mode == 4) ? -1
+                  : (ea_cap > 0 ? ea_cap : std::max(kNumSM / 8, kNumSM - busy));
+    ctx->ea_join_early = ea_mode == 4;
     const bkfac_status re = run_gemms(ctx, gs, ctx->ea_stream, "gemm_ea");
     ctx->grid_cap = 0;
     if (re != BKFAC_OK) return re;
@@ -1246,6 +1258,7 @@ bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, 
   r = bkfac_brand_update(ctx, args, count, stream);
   ctx->pending_ea = nullptr;
   ctx->grid_cap = 0;
+  ctx->ea_join_early = false;
   if (r == BKFAC_OK) {
     if (launched) {
       if (!cuda_ok(cudaStreamWaitEvent(st, ctx->ev_ea_done, 0))) r = BKFAC_ERR_CUDA;

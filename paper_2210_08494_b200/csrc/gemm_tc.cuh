@@ -369,7 +369,7 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
       for (int blk = 0; blk < nblk; ++blk, ++kb) {
         const int buf = kb & 1;
         const bool last = blk == nblk - 1;
-        mbar_wait(tfull_bar(buf), (kb >> 1) & 1);
+        mbar_wait_sleep(tfull_bar(buf), (kb >> 1) & 1);
         tc_fence_after();
         const uint32_t src = tmem_base + lane_off + (uint32_t)(buf * BN);
 #pragma unroll 1
@@ -689,7 +689,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
       }
     };
     auto store = [&](const float (&v)[Cfg::LPW], int vmode, int*) {
-      mbar_wait(empty_bar(stage), phase ^ 1);
+      mbar_wait_sleep(empty_bar(stage), phase ^ 1);
       const uint32_t st = sbase + stage * Cfg::STAGE_BYTES;
 #ifndef BKFAC_TC_DEBUG_NOSTORE
 #pragma unroll
