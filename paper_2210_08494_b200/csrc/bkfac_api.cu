@@ -465,10 +465,29 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         cudaStream_t sg = (fork && g > 0) ? ctx->side[g - 1] : st;
         if (sg != st && !cuda_ok(cudaStreamWaitEvent(sg, ctx->ev_fork, 0))) return BKFAC_ERR_CUDA;
         const int C = gC[g], msub = gm[g];
-        if (C == 0) {   // tiles in global memory, one CTA per factor
+        // tiles in global memory: one CTA per factor when the factors fill the GPU, else a
+        // cluster of up to 8 CTAs per factor sharing its tiles through L2 (an 8-GPU rank's
+        // share of configs[4]: 12 factors of m = 1536)
+        const int cgt = std::max(1, std::min(8, kNumSM / std::max(1, sub[g].nprob)));
+        if (C == 0 && cgt == 1) {
           const int mp = (msub + 31) / 32 * 32;
-          sytrd_tiled_kernel<true><<<(unsigned)sub[g].nprob, SYT_THREADS,
-                                     sizeof(float) * (size_t)syt_gt_smem_floats(mp), sg>>>(sub[g], 1);
+          sytrd_tiled_kernel<1><<<(unsigned)sub[g].nprob, SYT_THREADS,
+                                  sizeof(float) * (size_t)syt_gt_smem_floats(mp), sg>>>(sub[g], 1);
+        } else if (C == 0) {
+          const int mp = (msub + 31) / 32 * 32;
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3((unsigned)(cgt * sub[g].nprob), 1, 1);
+          cfg.blockDim = dim3(SYT_THREADS, 1, 1);
+          cfg.dynamicSmemBytes = sizeof(float) * (size_t)syt_gt_smem_floats(mp);
+          cfg.stream = sg;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeClusterDimension;
+          attr[0].val.clusterDim.x = (unsigned)cgt;
+          attr[0].val.clusterDim.y = 1;
+          attr[0].val.clusterDim.z = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_tiled_kernel<2>, sub[g], cgt))) return BKFAC_ERR_CUDA;
         } else {
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3((unsigned)(C * sub[g].nprob), 1, 1);
@@ -487,7 +506,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
           attr[1].val.priority = prio;
           cfg.attrs = attr;
           cfg.numAttrs = 2;
-          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_tiled_kernel<false>, sub[g], C))) return BKFAC_ERR_CUDA;
+          if (!cuda_ok(cudaLaunchKernelEx(&cfg, sytrd_tiled_kernel<0>, sub[g], C))) return BKFAC_ERR_CUDA;
         }
         LAUNCH_CHECK(ctx);
         if (sg != st && !cuda_ok(cudaEventRecord(ctx->ev_join[g - 1], sg))) return BKFAC_ERR_CUDA;
@@ -757,9 +776,10 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   cudaSetDevice(device);
   const int big = 220 * 1024;  // below the 227 KB opt-in limit minus static smem
   bool attr_ok = true;
-  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
-  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
-  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sytrd_tiled_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SYT_SMEM_FLOATS * 4) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(backtr_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bt_smem_bytes()) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;

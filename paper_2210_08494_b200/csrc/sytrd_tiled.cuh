@@ -110,9 +110,14 @@ __device__ __forceinline__ float syt_block_sum(float v, float* red) {
   return t;
 }
 
-template <bool GT>
+// MODE 0: tiles in the cluster's shared memory; 1: tiles in global memory, one CTA per
+// factor; 2: tiles in global memory (L2) shared by a cluster of C CTAs -- for few, large
+// factors (an 8-GPU rank's share of configs[4]), where one CTA per factor leaves most SMs idle
+template <int MODE>
 __global__ void __launch_bounds__(SYT_THREADS, 1)
 sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
+  constexpr bool GT = MODE >= 1;    // tiles in global memory
+  constexpr bool CL = MODE != 1;    // cluster code compiled (C may exceed 1)
   cgt::cluster_group cluster = cgt::this_cluster();
   const int q = (int)cluster.block_rank();
   const EigProb& p = b.p[blockIdx.x / C];
@@ -134,7 +139,10 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   const int ntiles = syt_tiles(NB);
   const int nown = (ntiles - q + C - 1) / C;          // tiles owned by this CTA
   // address of `ptr` in CTA r of the cluster (plain local pointer for 1-CTA launches)
-  auto rptr = [&](float* ptr, int r) -> float* { return (GT || C == 1) ? ptr : cluster.map_shared_rank(ptr, r); };
+  auto rptr = [&](float* ptr, int r) -> float* { return (!CL || C == 1) ? ptr : cluster.map_shared_rank(ptr, r); };
+  // this CTA's tile slot sl: shared memory (slot order) or global memory (position order,
+  // pos = sl * C + q, so any CTA of the cluster can address any tile)
+  auto slot_ptr = [&](int sl) -> float* { return GT ? tiles + 1024L * ((long)sl * C + q) : tiles + 1024L * sl; };
   // (I, J) of the tile at enumeration position pos (inverse of syt_pos)
   auto tile_ij = [&](int pos, int& I, int& J) {
     int n = (int)((sqrtf(8.f * pos + 1.f) - 1.f) * 0.5f);   // largest n: n(n+1)/2 <= pos
@@ -151,7 +159,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   for (int sl = warp; sl < nown; sl += NW) {
     int I, J;
     tile_ij(sl * C + q, I, J);
-    float* t = tiles + 1024L * sl;
+    float* t = slot_ptr(sl);
     const int i = 32 * I + lane;
     for (int jj = 0; jj < 32; ++jj) {
       const int j = 32 * J + jj;
@@ -162,10 +170,10 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
   }
   bad = __syncthreads_or(bad);
   if (tid == 0) scal[2] = bad ? 1.f : 0.f;
-  if (!GT && C > 1) cluster.sync(); else __syncthreads();
+  if (CL && C > 1) cluster.sync(); else __syncthreads();
   float anybad = 0.f;
   for (int r = 0; r < C; ++r) anybad += *rptr(scal + 2, r);
-  if (!GT && C > 1) cluster.sync(); else __syncthreads();
+  if (CL && C > 1) cluster.sync(); else __syncthreads();
   if (anybad != 0.f) {
     if (q == 0) {
       if (tid == 0 && p.status) atomicOr(p.status, ST_NONFINITE);
@@ -202,7 +210,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
     float ss = 0.f;
     for (int i = tid; i < m; i += SYT_THREADS) {
       const int pos = syt_pos(i >> 5, 0, NB);
-      const float x = *rptr(tiles + 1024L * (pos / C) + (i & 31), pos % C);
+      const float x = GT ? tiles[1024L * pos + (i & 31)] : *rptr(tiles + 1024L * (pos / C) + (i & 31), pos % C);
       if (i >= 2) ss = fmaf(x, x, ss);
       else scal[40 + i] = x;
       vbuf[i] = x;
@@ -317,7 +325,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       // shared-memory ring with cp.async, the next tile in flight while this one computes
       float* stg = scal + 64 + NW * 96 + warp * 2048;
       auto issue = [&](int sl2, int bi) {
-        const float* src = tiles + 1024L * sl2;
+        const float* src = slot_ptr(sl2);
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stg + bi * 1024));
 #pragma unroll
         for (int c8 = 0; c8 < 8; ++c8) {
@@ -343,7 +351,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) colv[jj] = sb[jj * 32];
         __syncwarp();   // the ring slot is refilled two tiles later
-        tile_work(colv, I, J, tiles + 1024L * sl + lane);
+        tile_work(colv, I, J, slot_ptr(sl) + lane);
       }
     } else {
       for (int sl = warp; sl < nact; sl += NW) {
@@ -359,7 +367,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       }
     }
     SYT_T(2);
-    if (!GT && C > 1) cluster.sync(); else __syncthreads();   // partial y (and column k+1) ready
+    if (CL && C > 1) cluster.sync(); else __syncthreads();   // partial y (and column k+1) ready
     SYT_T(3);
     // (c)+(a) merged: y_k summed through DSMEM -> w_k; in the same pass column k+1 is read
     // from its owners, gets the pending update (v_k, w_k) and yields v_{k+1}, tau_{k+1}
@@ -375,26 +383,24 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       float pv = 0.f;
       if (own) {
         float4 acc, c4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (GT || C == 1) {                         // one CTA (global tiles: always): local
+        const int pos1 = base1 + (i0 >> 5) - kb1;   // tile of rows i0.. in column k+1
+        if (!CL || C == 1) {                        // one CTA: local partial y
           acc = *reinterpret_cast<const float4*>(y + i0);
-          if (next) {
-            const int pos = base1 + (i0 >> 5) - kb1;
-            c4 = *reinterpret_cast<const float4*>(tiles + 1024L * pos + jk1 * 32 + (i0 & 31));
-          }
         } else {
-          // all C + 1 remote loads in flight together, then the sums
+          // all C remote loads in flight together, then the sums
           float4 t4[8];
 #pragma unroll
           for (int r = 0; r < 8; ++r)
             if (r < C) t4[r] = syt_dsmem_ld4(y + i0, r);
-          if (next) {
-            const int pos = base1 + (i0 >> 5) - kb1;
-            c4 = syt_dsmem_ld4(tiles + 1024L * (pos / C) + jk1 * 32 + (i0 & 31), pos % C);
-          }
           acc = t4[0];
 #pragma unroll
           for (int r = 1; r < 8; ++r)
             if (r < C) { acc.x += t4[r].x; acc.y += t4[r].y; acc.z += t4[r].z; acc.w += t4[r].w; }
+        }
+        if (next) {
+          if (GT) c4 = *reinterpret_cast<const float4*>(tiles + 1024L * pos1 + jk1 * 32 + (i0 & 31));
+          else if (C == 1) c4 = *reinterpret_cast<const float4*>(tiles + 1024L * pos1 + jk1 * 32 + (i0 & 31));
+          else c4 = syt_dsmem_ld4(tiles + 1024L * (pos1 / C) + jk1 * 32 + (i0 & 31), pos1 % C);
         }
         si[0] = acc.x; si[1] = acc.y; si[2] = acc.z; si[3] = acc.w;
         xi[0] = c4.x; xi[1] = c4.y; xi[2] = c4.z; xi[3] = c4.w;
@@ -460,7 +466,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       const int i = (tid == 0) ? m - 2 : m - 1, j = (tid == 2) ? m - 1 : m - 2;
       const int pos = syt_pos(i >> 5, j >> 5, NB);
       if (pos % C == q) {
-        float* a = tiles + 1024L * (pos / C) + (j & 31) * 32 + (i & 31);
+        float* a = (GT ? tiles + 1024L * pos : tiles + 1024L * (pos / C)) + (j & 31) * 32 + (i & 31);
         const float x = *a - (vget(vq, m - 3, sc, i) * wp[j] + wp[i] * vget(vq, m - 3, sc, j));
         *a = x;
         if (tid == 0) { p.d[m - 2] = x; p.tau[m - 2] = 0.f; }
@@ -469,7 +475,7 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       }
     }
   }
-  if (!GT && C > 1) cluster.sync();   // no CTA exits while others may still address its smem
+  if (CL && C > 1) cluster.sync();   // no CTA exits while others may still address its smem
 }
 
 }  // namespace bkfac

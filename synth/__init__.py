@@ -173,12 +173,21 @@ def cfg5_transformer(blocks: int = 24, steps: int = 50) -> StackConfig:
                   sigma=0.02, rho=0.97, lam=0.01, steps=steps, grad_std=0.1)
 
 
+def cfg5_rank_of_8() -> StackConfig:
+    """One rank's share of configs[4] at 8 GPUs (layer sharding gives every rank 3 of the
+    24 identical blocks): 12 factors, 6 layers -- the per-GPU work of the 8-GPU run, timed
+    on one GPU to project strong scaling (the all-gather excluded)."""
+    c = cfg5_transformer(blocks=3)
+    return dataclasses.replace(c, name="cfg5_transformer_rank_of_8")
+
+
 CONFIGS = {
     "cfg1": cfg1_toy,
     "cfg2": cfg2_conv,
     "cfg3": cfg3_vgg,
     "cfg4": cfg4_vgg_sharded,
     "cfg5": cfg5_transformer,
+    "cfg5r8": cfg5_rank_of_8,
 }
 
 
