@@ -397,8 +397,28 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
     for (size_t i = 0; i < n; ++i) cmax = std::max(cmax, b.p[i].c);
     if (cmax <= 32 * CS_MAXNB)   // every tile resident in shared memory
       chol_smem_kernel<<<(unsigned)n, CT_THREADS, chol_smem_bytes(cmax), st>>>(b);
-    else
-      chol_tiled_kernel<<<(unsigned)n, CT_THREADS, CT_SMEM_BYTES, st>>>(b);
+    else {
+      // tiles in global memory; clusters of up to 8 CTAs per factor when the factors alone
+      // would leave most SMs idle
+      const int cc = std::max(1, std::min(8, kNumSM / std::max(1, (int)n)));
+      if (cc == 1) {
+        chol_tiled_kernel<<<(unsigned)n, CT_THREADS, CT_SMEM_BYTES, st>>>(b, 1);
+      } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(cc * n), 1, 1);
+        cfg.blockDim = dim3(CT_THREADS, 1, 1);
+        cfg.dynamicSmemBytes = CT_SMEM_BYTES;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)cc;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (!cuda_ok(cudaLaunchKernelEx(&cfg, chol_tiled_kernel, b, cc))) return BKFAC_ERR_CUDA;
+      }
+    }
     LAUNCH_CHECK(ctx);
     i0 += n;
   }

@@ -18,6 +18,7 @@
 // row of X are zero and ST_CHOL_DROP is reported (informational, as before).
 // Outputs: L and Linv = L^{-1} (c x c col-major, zeros above the diagonal).
 #pragma once
+#include <cooperative_groups.h>
 #include "chol.cuh"
 #include "common.cuh"
 
@@ -164,11 +165,17 @@ __device__ unsigned long long g_chol_dbg[8];   // tuning builds: per-phase cycle
 #else
 #define CT_T(ph) do {} while (0)
 #endif
-__global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_constant__ CholTiledBatch b) {
+// C > 1: a cluster of C CTAs per factor (tiles in global memory / L2 are shared; every
+// tile loop is dealt over the cluster's C * 16 warps, the phase barriers are cluster
+// barriers, the diagonal tiles are factored by CTA 0) -- for few factors per GPU (an 8-GPU
+// rank's share of configs[4]), where one CTA per factor leaves most SMs idle.
+__global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_constant__ CholTiledBatch b, int C) {
 #ifdef BKFAC_CHOL_TIMING
   unsigned long long ct_prev = clock64();
 #endif
-  const CholTiledProb& p = b.p[blockIdx.x];
+  cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
+  const int q = C > 1 ? (int)cluster.block_rank() : 0;
+  const CholTiledProb& p = b.p[blockIdx.x / C];
   const int c = p.c, NB = (c + 31) >> 5;
   const int ntile = NB * (NB + 1) / 2;
   float* Lt = p.tiles;                       // L tiles (col-major)
@@ -176,7 +183,10 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
   float* Xd = Xt + (size_t)ntile * 1024;     // col-major copies of the diagonal X_JJ
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = CT_THREADS / 32;
+  const int gw = q * NW + warp, NWC = NW * C;   // warp index / count over the cluster
+  auto csync = [&]() { if (C > 1) cluster.sync(); else __syncthreads(); };
   __shared__ float red[32];
+  __shared__ float s_part[2];
   __shared__ int s_drop;
   extern __shared__ __align__(16) float ctsm[];
   float* sA = ctsm + warp * 2048;     // per-warp staging: A tile, B tile
@@ -184,7 +194,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
 
   // ---- load G (lower) into tiles, identity padding; trace and max diagonal
   float dsum = 0.f, dmax = 0.f;
-  for (int t = warp; t < ntile; t += NW) {
+  for (int t = gw; t < ntile; t += NWC) {
     int I = 0;
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     const int J = t - I * (I + 1) / 2;
@@ -205,7 +215,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
       if (i == j && i < c) { dsum += g; dmax = fmaxf(dmax, g); }
     }
   }
-  const float trace = block_sum(dsum, red);
+  float trace = block_sum(dsum, red);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if (lane == 0) red[warp] = dmax;
@@ -213,6 +223,19 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
   float gmax = 0.f;
   for (int w = 0; w < NW; ++w) gmax = fmaxf(gmax, red[w]);
   if (tid == 0) s_drop = 0;
+  if (C > 1) {                       // the cluster's trace and max diagonal, in rank order
+    if (tid == 0) { s_part[0] = trace; s_part[1] = gmax; }
+    cluster.sync();                  // also: every CTA's tiles of G are loaded
+    float tr = 0.f, gm = 0.f;
+    for (int r = 0; r < C; ++r) {
+      const float* rp = cluster.map_shared_rank(s_part, r);
+      tr += rp[0];
+      gm = fmaxf(gm, rp[1]);
+    }
+    trace = tr;
+    gmax = gm;
+    cluster.sync();                  // no CTA reuses / leaves s_part while it is read
+  }
   // shifted first pass (sCQR, Fukaya et al. 2020): G_ii += shift * tr(G)
   const float sh = (p.shift > 0.f) ? p.shift * trace : 0.f;
   const float tol = 4.0f * 1.1920929e-7f * (gmax + sh);
@@ -222,7 +245,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
   for (int J = 0; J < NB; ++J) {
     // (1) diagonal tile: one warp factors it (lane = row, register rows, shuffles; fully
     //     unrolled by templates) and inverts it (lane = column).
-    if (warp == 0) {
+    if (q == 0 && warp == 0) {
       float* T = Lt + (size_t)ctix(J, J) * 1024;
       float a[32];
 #pragma unroll
@@ -257,10 +280,10 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
       }
       if (dropped && lane == 0) s_drop = 1;
     }
-    __syncthreads();
+    csync();
     CT_T(1);
     // (2) L_IJ = G_IJ X_JJ^T for I > J (X_JJ^T(k, j) = X_JJ(j, k) -> col-major copy as B)
-    for (int I = J + 1 + warp; I < NB; I += NW) {
+    for (int I = J + 1 + gw; I < NB; I += NWC) {
       float* T = Lt + (size_t)ctix(I, J) * 1024;
       float acc[32];
 #pragma unroll
@@ -274,13 +297,13 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
 #pragma unroll
       for (int j = 0; j < 32; ++j) T[j * 32 + lane] = acc[j];
     }
-    __syncthreads();
+    csync();
     CT_T(2);
     // (3) trailing update G_IK -= L_IJ L_KJ^T for I >= K > J
     {
       const int n = NB - J - 1;
       const int npairs = n * (n + 1) / 2;
-      for (int t = warp; t < npairs; t += NW) {
+      for (int t = gw; t < npairs; t += NWC) {
         int a = 0;
         while ((a + 1) * (a + 2) / 2 <= t) ++a;
         const int I = J + 1 + a, K = J + 1 + (t - a * (a + 1) / 2);
@@ -299,13 +322,13 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
         for (int j = 0; j < 32; ++j) T[j * 32 + lane] = acc[j];
       }
     }
-    __syncthreads();
+    csync();
     CT_T(3);
   }
   // ---- X = L^{-1}, right-looking by block rows K: the off-diagonal X tiles first hold
   // the accumulators A_IJ = -sum_{M<I} L_IM X_MJ (zero-initialised), then
   //   (1) X_KJ = X_KK A_KJ for J < K;     (2) A_IJ -= L_IK X_KJ for I > K, J <= K.
-  for (int t = warp; t < ntile; t += NW) {
+  for (int t = gw; t < ntile; t += NWC) {
     int I = 0;
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     if (t - I * (I + 1) / 2 == I) continue;            // diagonal X_II already set
@@ -313,9 +336,9 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
 #pragma unroll
     for (int q = 0; q < 8; ++q) T4[q * 32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  __syncthreads();
+  csync();
   for (int K = 0; K < NB; ++K) {
-    for (int J = warp; J < K; J += NW) {               // (1)
+    for (int J = gw; J < K; J += NWC) {                // (1)
       float* XK = Xt + (size_t)ctix(K, J) * 1024;
       float acc[32];
 #pragma unroll
@@ -328,10 +351,10 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
 #pragma unroll
       for (int j = 0; j < 32; ++j) XK[lane * 32 + j] = acc[j];
     }
-    __syncthreads();
+    csync();
     CT_T(5);
     const int nI = NB - K - 1, nJ = K + 1;
-    for (int t = warp; t < nI * nJ; t += NW) {         // (2)
+    for (int t = gw; t < nI * nJ; t += NWC) {          // (2)
       const int I = K + 1 + t / nJ, J = t % nJ;
       float* XI = Xt + (size_t)ctix(I, J) * 1024;
       float acc[32];
@@ -345,11 +368,11 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_tiled_kernel(const __grid_
 #pragma unroll
       for (int j = 0; j < 32; ++j) XI[lane * 32 + j] -= acc[j];
     }
-    __syncthreads();
+    csync();
     CT_T(6);
   }
   // ---- outputs: L and Linv, c x c col-major, zeros above the diagonal
-  for (int t = warp; t < NB * NB; t += NW) {
+  for (int t = gw; t < NB * NB; t += NWC) {
     const int I = t % NB, J = t / NB;
     const int i = 32 * I + lane;
     float lv[32], xv[32];   // all loads in flight before the stores
