@@ -7,6 +7,7 @@ tail -2 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_cfg4.json 2> gpurun_out/bench_cfg4.err; echo "cfg4 exit $?"
 timeout 900 python bench.py --config cfg5 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg5.json 2> gpurun_out/bench_cfg5.err; echo "cfg5 exit $?"
+timeout 900 python bench.py --config cfg5r8 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg5r8.json 2> gpurun_out/bench_cfg5r8.err; echo "cfg5r8 exit $?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref exit $?"
 if [ "$SKIP_NCU" != 1 ]; then
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
