@@ -11,7 +11,9 @@ WANT = ["gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak
         "sm__warps_active.avg.per_cycle_active", "launch__grid_size", "launch__block_size",
         "launch__cluster_dim_x", "launch__registers_per_thread",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__t_bytes.sum", "lts__t_bytes.sum.per_second", "dram__bytes.sum.per_second",
+        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"]
 
 out, title, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
 lines = [f"# {title}"]
