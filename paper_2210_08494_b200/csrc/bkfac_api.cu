@@ -1228,7 +1228,11 @@ bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K, const floa
 }
 
 namespace {
-bkfac_status ea_stage(bkfac_ctx ctx, const bkfac_ea_args* args, int count, GemmStage& gs) {
+// brand / nbrand: the same call's Brand updates (bkfac_brand_ea_update, EA beside the
+// eigensolver): an EA item whose M is a Brand item's M reads the 16-byte-aligned copy the
+// Brand update has already made of it (odd n), so the loaders take the vector path
+bkfac_status ea_stage(bkfac_ctx ctx, const bkfac_ea_args* args, int count, GemmStage& gs,
+                      const bkfac_brand_args* brand = nullptr, int nbrand = 0) {
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
     if (a.factor < 0 || a.factor >= (int)ctx->f.size() || !a.K_dense || !a.M)
@@ -1238,7 +1242,15 @@ bkfac_status ea_stage(bkfac_ctx ctx, const bkfac_ea_args* args, int count, GemmS
     if (a.c <= 0 || a.c > fp.d.c_max) return BKFAC_ERR_DIM;
     if (!(a.rho >= 0.f && a.rho < 1.f)) return BKFAC_ERR_INVALID_ARG;
     const int n = fp.d.n;
-    GemmProb pe = gp(a.M, n, a.M, n, a.K_dense, n, n, n, a.c, 1.f - a.rho, a.K_dense, n, a.rho);
+    const float* Mp = a.M;
+    int ldm = n;
+    for (int j = 0; j < nbrand; ++j)
+      if (brand[j].factor == a.factor && brand[j].M == a.M && brand[j].c == a.c && fp.Ms &&
+          !fp.dense) {
+        Mp = at<float>(ctx, fp.Ms);
+        ldm = fp.nld;
+      }
+    GemmProb pe = gp(Mp, ldm, Mp, ldm, a.K_dense, n, n, n, a.c, 1.f - a.rho, a.K_dense, n, a.rho);
     pe.status = status_ptr(ctx, a.factor);
     pe.sym = 1;   // K and M M^T are symmetric: lower tiles computed, mirrored
     gs.add(false, true, pe, 0);
@@ -1265,13 +1277,15 @@ bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, 
     for (int j = 0; j < count && args; ++j)
       if (ea_args[i].K_dense == args[j].U_out || ea_args[i].K_dense == args[j].U_in)
         return BKFAC_ERR_ALIAS;
-  GemmStage gs;
-  bkfac_status r = ea_stage(ctx, ea_args, ea_count, gs);
-  if (r != BKFAC_OK) return r;
-  if (ea_count == 0) return bkfac_brand_update(ctx, args, count, stream);
   // 0 (default): EA GEMM on a side stream beside the tridiagonalisation, grid capped at the
   // SMs its clusters leave idle; 2: the same, uncapped; 1: EA first, serially, full grid
   static const int ea_mode = [] { const char* e = getenv("BKFAC_EA_MODE"); return e ? atoi(e) : 0; }();
+  GemmStage gs;
+  // beside the eigensolver the Brand update's aligned copies of M already exist
+  bkfac_status r = ea_mode == 1 ? ea_stage(ctx, ea_args, ea_count, gs)
+                                : ea_stage(ctx, ea_args, ea_count, gs, args, args ? count : 0);
+  if (r != BKFAC_OK) return r;
+  if (ea_count == 0) return bkfac_brand_update(ctx, args, count, stream);
   if (ea_mode == 1) {
     r = run_gemms(ctx, gs, static_cast<cudaStream_t>(stream), "gemm_ea");
     return r != BKFAC_OK ? r : bkfac_brand_update(ctx, args, count, stream);
