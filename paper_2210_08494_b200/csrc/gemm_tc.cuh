@@ -100,6 +100,8 @@ struct TcCfg {
   static constexpr int TMEM_COLS = 4 * BN;                   // 2 K-block buffers + running sum
   static constexpr int LINES = TC_BM + B_ROWS;               // 128-byte lines per stage half
   static constexpr int LPW = LINES / NLW;                    // lines per loader warp
+  // quads of A lines and of B lines never mix in one loader-warp quad slot
+  static_assert(TC_BM % (4 * NLW) == 0 && B_ROWS % (4 * NLW) == 0, "loader quad split");
   // + per-epilogue-warp 16 x 34 staging for the transposed (mirror) stores of symmetric tiles
   static constexpr int EPI_STAGE_FLOATS = 16 * 34;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
@@ -632,8 +634,8 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     // lines) and scalar stores.  Both keep 4 values per lane per quad.
     constexpr int NQ = Cfg::LPW / 4;
     auto line_src = [&](const GemmProb& p, const float* Ap, const float* Bp, long lda, long ldb,
-                        int ks, int klen, int l, int e, bool& ok) -> const float* {
-      if (l < TC_BM) {
+                        int ks, int klen, int l, int e, bool& ok, bool isA) -> const float* {
+      if (isA) {                                   // l < TC_BM (compile-time per quad)
         if (TA) { const int i = x.m0 + l, k = ks + e; ok = i < p.M && k < klen; return Ap + k + (long)i * lda; }
         const int k = ks + (l & 31), i = x.m0 + ((l >> 5) << 5) + e;
         ok = i < p.M && k < klen;
@@ -660,13 +662,13 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 #pragma unroll
       for (int qd = 0; qd < NQ; ++qd) {
         const int g = lw + qd * TC_LOAD_WARPS;
-        const bool isA = 4 * g < TC_BM;
+        const bool isA = qd < TC_BM / (4 * TC_LOAD_WARPS);   // compile-time: g = lw + qd * NLW, lw < NLW
         const bool vec = isA ? (p.vec & 1) : (p.vec & 2);
         if (vec) {
           const int l = 4 * g + (lane >> 3), e0 = (lane & 7) * 4;
           bool ok0, ok3;
-          const float* src = line_src(p, Ap, Bp, lda, ldb, ks, klen, l, e0, ok0);
-          line_src(p, Ap, Bp, lda, ldb, ks, klen, l, e0 + 3, ok3);
+          const float* src = line_src(p, Ap, Bp, lda, ldb, ks, klen, l, e0, ok0, isA);
+          line_src(p, Ap, Bp, lda, ldb, ks, klen, l, e0 + 3, ok3, isA);
           if (ok0 && ok3) {
             const float4 w = __ldg(reinterpret_cast<const float4*>(src));
             v[4 * qd + 0] = w.x; v[4 * qd + 1] = w.y; v[4 * qd + 2] = w.z; v[4 * qd + 3] = w.w;
@@ -674,7 +676,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               bool ok;
-              const float* s1 = line_src(p, Ap, Bp, lda, ldb, ks, klen, l, e0 + t, ok);
+              const float* s1 = line_src(p, Ap, Bp, lda, ldb, ks, klen, l, e0 + t, ok, isA);
               v[4 * qd + t] = ok ? __ldg(s1) : 0.f;
             }
           }
@@ -682,7 +684,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             bool ok;
-            const float* s1 = line_src(p, Ap, Bp, lda, ldb, ks, klen, 4 * g + t, lane, ok);
+            const float* s1 = line_src(p, Ap, Bp, lda, ldb, ks, klen, 4 * g + t, lane, ok, isA);
             v[4 * qd + t] = ok ? __ldg(s1) : 0.f;
           }
         }
@@ -695,7 +697,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 #pragma unroll
       for (int qd = 0; qd < NQ; ++qd) {
         const int g = lw + qd * TC_LOAD_WARPS;
-        const bool isA = 4 * g < TC_BM;
+        const bool isA = qd < TC_BM / (4 * TC_LOAD_WARPS);   // compile-time: g = lw + qd * NLW, lw < NLW
         const bool vec = isA ? (vmode & 1) : (vmode & 2);
         if (vec) {
           const int l = 4 * g + (lane >> 3), e0 = (lane & 7) * 4;
