@@ -28,43 +28,37 @@ constexpr int CT_THREADS = 512;
 
 BKFAC_DEV int ctix(int I, int J) { return I * (I + 1) / 2 + J; }
 
-// acc[j] -= (or +=) sum_k A(lane, k) * B(j, k); A, B col-major 32 x 32 tiles
+// acc[j] -= (or +=) sum_k A(lane, k) * B(j, k); A, B col-major 32 x 32 tiles.  The FMAs run
+// on column pairs (FFMA2: half the FP instructions; same per-element rounding as FFMA).
 template <bool SUB>
 BKFAC_DEV void tile_abt(float (&acc)[32], const float* A, const float* B, int lane) {
+  float2* acc2 = reinterpret_cast<float2*>(acc);
 #pragma unroll 2
   for (int k = 0; k < 32; ++k) {
-    const float a = A[k * 32 + lane];
+    const float a = SUB ? -A[k * 32 + lane] : A[k * 32 + lane];
+    const float2 a2 = make_float2(a, a);
     const float4* b4 = reinterpret_cast<const float4*>(B + k * 32);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const float4 bb = b4[q];
-      if (SUB) {
-        acc[4 * q + 0] = fmaf(-a, bb.x, acc[4 * q + 0]);
-        acc[4 * q + 1] = fmaf(-a, bb.y, acc[4 * q + 1]);
-        acc[4 * q + 2] = fmaf(-a, bb.z, acc[4 * q + 2]);
-        acc[4 * q + 3] = fmaf(-a, bb.w, acc[4 * q + 3]);
-      } else {
-        acc[4 * q + 0] = fmaf(a, bb.x, acc[4 * q + 0]);
-        acc[4 * q + 1] = fmaf(a, bb.y, acc[4 * q + 1]);
-        acc[4 * q + 2] = fmaf(a, bb.z, acc[4 * q + 2]);
-        acc[4 * q + 3] = fmaf(a, bb.w, acc[4 * q + 3]);
-      }
+      acc2[2 * q] = __ffma2_rn(a2, make_float2(bb.x, bb.y), acc2[2 * q]);
+      acc2[2 * q + 1] = __ffma2_rn(a2, make_float2(bb.z, bb.w), acc2[2 * q + 1]);
     }
   }
 }
 // acc[j] += sum_k A(lane, k) * B(k, j); A col-major, B row-major 32 x 32 tiles
 BKFAC_DEV void tile_ab(float (&acc)[32], const float* A, const float* Brm, int lane) {
+  float2* acc2 = reinterpret_cast<float2*>(acc);
 #pragma unroll 2
   for (int k = 0; k < 32; ++k) {
     const float a = A[k * 32 + lane];
+    const float2 a2 = make_float2(a, a);
     const float4* b4 = reinterpret_cast<const float4*>(Brm + k * 32);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const float4 bb = b4[q];
-      acc[4 * q + 0] = fmaf(a, bb.x, acc[4 * q + 0]);
-      acc[4 * q + 1] = fmaf(a, bb.y, acc[4 * q + 1]);
-      acc[4 * q + 2] = fmaf(a, bb.z, acc[4 * q + 2]);
-      acc[4 * q + 3] = fmaf(a, bb.w, acc[4 * q + 3]);
+      acc2[2 * q] = __ffma2_rn(a2, make_float2(bb.x, bb.y), acc2[2 * q]);
+      acc2[2 * q + 1] = __ffma2_rn(a2, make_float2(bb.z, bb.w), acc2[2 * q + 1]);
     }
   }
 }
