@@ -1,6 +1,7 @@
 // Blocked Cholesky factorisation and triangular inverse of the c x c Gram matrix
 // G = R^T R of CholeskyQR (Alg 3 line 2 "QR_decomp(A_perp)"; footnote :451
-// allows any orthonormal decomposition) -- one CTA per factor, 32 x 32 register tiles.
+// allows any orthonormal decomposition) -- one CTA per factor (or, with few factors per
+// GPU, a cluster of up to 8 CTAs sharing the global tiles), 32 x 32 register tiles.
 //
 // G is split into NB = ceil(c/32) block rows/columns (padding: identity), tiles packed
 // lower-triangular in a global scratch (L1/L2 resident):

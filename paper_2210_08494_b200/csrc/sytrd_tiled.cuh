@@ -30,6 +30,10 @@
 // Per element of the trailing matrix and step: one LDS, one STS and five FP32 ops.
 // Outputs: d, e, tau and the reflectors (rows >= k+2 of column k) in K's lower triangle
 // for the back-transform.
+// Instantiations (MODE): 0 = the above, tiles in the cluster's shared memory (m <= ~700);
+// 1 = tiles in global memory, one CTA per factor (large m with many factors: HBM-bound);
+// 2 = tiles in global memory shared by a cluster of up to 8 CTAs (large m with few factors
+// per GPU, e.g. one 8-GPU rank's share: tiles L2-resident, partial y through DSMEM).
 #pragma once
 #include <cooperative_groups.h>
 
