@@ -386,7 +386,10 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
             float r[16];
             tmem_ld16(run + g * 16, r);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] += r[j];
+            for (int j = 0; j < 16; j += 2) {   // FADD2: same round-to-nearest per element
+              const float2 t = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(r[j], r[j + 1]));
+              v[j] = t.x; v[j + 1] = t.y;
+            }
           }
           if (!last) {
             tmem_st16(run + g * 16, v);
@@ -409,15 +412,19 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
               for (int jj = 0; jj < 16; ++jj)
                 c0v[jj] = (rowok && j0 + jj < p.N) ? p.C0[i + (long)(j0 + jj) * p.ldc0] : 0.f;
             }
+            // alpha v + beta C0 on pairs (FMUL2 / FFMA2: the same per-element roundings as
+            // the scalar o = alpha v; o += beta c0)
+            const float2 al2 = make_float2(p.alpha, p.alpha), be2 = make_float2(beta, beta);
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-              float o = p.alpha * v[jj];
+            for (int jj = 0; jj < 16; jj += 2) {
+              float2 o = __fmul2_rn(al2, make_float2(v[jj], v[jj + 1]));
               if (beta != 0.f) {
-                nonfinite |= !isfinite(c0v[jj]);
-                o += beta * c0v[jj];
+                nonfinite |= !isfinite(c0v[jj]) | !isfinite(c0v[jj + 1]);
+                o = __ffma2_rn(be2, make_float2(c0v[jj], c0v[jj + 1]), o);
               }
-              if (rowok && j0 + jj < p.N) p.C[i + (long)(j0 + jj) * p.ldc] = o;
-              v[jj] = o;
+              if (rowok && j0 + jj < p.N) p.C[i + (long)(j0 + jj) * p.ldc] = o.x;
+              if (rowok && j0 + jj + 1 < p.N) p.C[i + (long)(j0 + jj + 1) * p.ldc] = o.y;
+              v[jj] = o.x; v[jj + 1] = o.y;
             }
             if (p.sym && x.m0 != x.n0) {
               // mirror tile C(j, i) = C(i, j): transposed through a warp-private staging
