@@ -263,13 +263,17 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
       const float cwp = wp[32 * J + lane];
       const float vi = vget(v, k, sc, i), vpi = vget(vp, k - 1, sc_prev, i), wpi = wp[i];
       float racc[4] = {0.f, 0.f, 0.f, 0.f};
-      if ((32 * J > k) && (I > J)) {
-        // interior tile: the column-indexed values go through the warp's shared stage as
+      if (I > J) {
+        // off-diagonal tile: the column-indexed values go through the warp's shared stage as
         // (cwp, cwp, cvp, cvp) float4 and (cv, cv) float2 pairs read by broadcast, and the
-        // arithmetic runs on column pairs (FFMA2): no shuffles in the element loop
-        bst[(lane >> 1) * 4 + (lane & 1)] = cwp;
-        bst[(lane >> 1) * 4 + 2 + (lane & 1)] = cvp;
-        bst[64 + lane] = cv;
+        // arithmetic runs on column pairs (FFMA2): no shuffles in the element loop.  In the
+        // current block column (32 J <= k) the finished columns j <= k get zero broadcast
+        // values: their elements are written back unchanged and add nothing to y at rows
+        // > k (their transposed contributions land in y rows <= k, which are never read).
+        const bool live = 32 * J + lane > k;
+        bst[(lane >> 1) * 4 + (lane & 1)] = live ? cwp : 0.f;
+        bst[(lane >> 1) * 4 + 2 + (lane & 1)] = live ? cvp : 0.f;
+        bst[64 + lane] = live ? cv : 0.f;
         __syncwarp();
         const float4* q4 = reinterpret_cast<const float4*>(bst);
         const float2* v2 = reinterpret_cast<const float2*>(bst + 64);
