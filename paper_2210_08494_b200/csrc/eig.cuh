@@ -46,6 +46,15 @@ BKFAC_DEV double sturm_div(double e2, double q) {
   return e2 * y;
 }
 
+// 1/q for the LU pivots of inverse iteration: reciprocal seed + two Newton steps (relative
+// error at the fp64 rounding level; |q| >= tiny, a normal number)
+BKFAC_DEV double inv_rcp(double q) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+  y = fma(y, fma(-q, y, 1.0), y);
+  return fma(y, fma(-q, y, 1.0), y);
+}
+
 BKFAC_DEV int sturm_count(const double* dd, const double* e2, int m, double x, double pivmin) {
   int cnt = 0;
   double q = dd[0] - x;
@@ -232,13 +241,13 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
     if (fabs(dcur) >= fabs(sub)) {
       double piv = dcur;
       if (fabs(piv) < tiny) piv = (piv >= 0.0) ? tiny : -tiny;
-      const double rp = 1.0 / piv;
+      const double rp = inv_rcp(piv);
       const double f = sub * rp;
       AT(dUi, i) = rp; AT(du, i) = dufcur; AT(du2, i) = 0.0; AT(dl, i) = f; AT(pv, i) = 0;
       dcur = dnext - f * dufcur;
       dufcur = dunext;
     } else {
-      const double rs = 1.0 / sub;
+      const double rs = inv_rcp(sub);
       const double f = dcur * rs;
       AT(dUi, i) = rs; AT(du, i) = dnext; AT(du2, i) = dunext; AT(dl, i) = f; AT(pv, i) = 1;
       dcur = dufcur - f * dnext;
