@@ -234,25 +234,24 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
   // LU with partial pivoting of T - lam I (LAPACK dgttrf recurrence)
   double dcur = dd[0] - lam;
   double dufcur = ee[0];
+  // branch-free (threads = eigenvectors pivot differently; selects instead of divergence)
   for (int i = 0; i < m - 1; ++i) {
     const double sub = ee[i];
     const double dnext = dd[i + 1] - lam;
     const double dunext = ee[i + 1];
-    if (fabs(dcur) >= fabs(sub)) {
-      double piv = dcur;
-      if (fabs(piv) < tiny) piv = (piv >= 0.0) ? tiny : -tiny;
-      const double rp = inv_rcp(piv);
-      const double f = sub * rp;
-      AT(dUi, i) = rp; AT(du, i) = dufcur; AT(du2, i) = 0.0; AT(dl, i) = f; AT(pv, i) = 0;
-      dcur = dnext - f * dufcur;
-      dufcur = dunext;
-    } else {
-      const double rs = inv_rcp(sub);
-      const double f = dcur * rs;
-      AT(dUi, i) = rs; AT(du, i) = dnext; AT(du2, i) = dunext; AT(dl, i) = f; AT(pv, i) = 1;
-      dcur = dufcur - f * dnext;
-      dufcur = -f * dunext;
-    }
+    const bool sw = fabs(dcur) < fabs(sub);                 // row interchange
+    double piv = sw ? sub : dcur;
+    if (!sw && fabs(piv) < tiny) piv = (piv >= 0.0) ? tiny : -tiny;
+    const double rp = inv_rcp(piv);
+    const double f = (sw ? dcur : sub) * rp;
+    AT(dUi, i) = rp;
+    AT(du, i) = sw ? dnext : dufcur;
+    AT(du2, i) = sw ? dunext : 0.0;
+    AT(dl, i) = f;
+    AT(pv, i) = sw ? 1 : 0;
+    const double ncur = (sw ? dufcur : dnext) - f * (sw ? dnext : dufcur);
+    dufcur = sw ? -f * dunext : dunext;
+    dcur = ncur;
   }
   if (fabs(dcur) < tiny) dcur = (dcur >= 0.0) ? tiny : -tiny;
   AT(dUi, m - 1) = 1.0 / dcur;
