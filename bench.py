@@ -187,6 +187,8 @@ def roofline_from_stages(stages, peaks, clocks):
     if name.startswith("gemm_") and top.get("path") == "tc":
         tf32 = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))) * 0.5
         bound, peak, unit, achieved = "tensor", tf32 / 3.0, "TFLOP/s", top["flops"] / sec / 1e12
+    elif name == "eig_sytrd_gt":   # global-tile tridiagonalisation: streams the trailing matrix
+        bound, peak, unit, achieved = "hbm", float(peaks["hbm_gbs"]), "GB/s", top["bytes"] / sec / 1e9
     elif name.startswith("gemm_") or name.startswith("eig_") or name.startswith("chol"):
         bound, peak, unit, achieved = "alu", fp32_peak, "TFLOP/s", top["flops"] / sec / 1e12
     else:

@@ -455,8 +455,14 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
       }
       if (!cuda_ok(cudaEventRecord(ctx->ev_ea_fork, st))) return BKFAC_ERR_CUDA;
     }
-    // sytrd: 4/3 m^3 flops; algorithmic bytes: read K (lower), write reflectors + T
-    prof_begin(ctx, "eig_sytrd", st, 4.0 / 3.0 * m3, 4.0 * m2);
+    // sytrd: 4/3 m^3 flops; algorithmic bytes: read K (lower), write reflectors + T.  When
+    // every factor's tiles live in global memory ("eig_sytrd_gt"), the one-stage reduction
+    // streams the trailing lower triangle every column (symv + rank-2 update: read + write
+    // of (m-k)^2/2 floats at step k, 4/3 m^3 bytes in all) -- that is its algorithmic traffic
+    bool all_gt = n > 0;
+    for (size_t i = 0; i < n; ++i) all_gt &= sytrd_tiled_cluster(b.p[i].m) == 0;
+    if (all_gt) prof_begin(ctx, "eig_sytrd_gt", st, 4.0 / 3.0 * m3, 4.0 / 3.0 * m3);
+    else prof_begin(ctx, "eig_sytrd", st, 4.0 / 3.0 * m3, 4.0 * m2);
     {
       // one launch per cluster size; the launches are independent problems, so all but
       // the first run on side streams (fork/join) and overlap on the GPU
