@@ -45,7 +45,7 @@ SHAPES = [  # (n, c, r): several tiles and ragged tails, c = 1, r = 1
     (900, 128, 250),    # core m = 378: 2-CTA cluster tridiagonalisation
     (2000, 250, 350),   # core m = 600: 8-CTA cluster tridiagonalisation
     (2000, 300, 450),   # core m = 750: 8-CTA cluster tridiagonalisation
-    (1300, 300, 700)]   # core m = 1000: tiles in global memory
+    (1300, 300, 700)]   # core m = 1000: global tiles shared by an 8-CTA cluster; c = 300: clustered global-tile Cholesky
 
 
 @pytest.mark.parametrize("shape", SHAPES)
