@@ -173,6 +173,13 @@ void prof_end(bkfac_ctx c, cudaStream_t st) {
   c->open_rec = -1;
 }
 
+// largest cluster for the global-tile tridiagonalisation and Cholesky (few factors per GPU);
+// BKFAC_GT_CLUSTER=1 forces one CTA per factor (tests cover both paths at small batch sizes)
+static int gt_cluster_max() {
+  const char* e = getenv("BKFAC_GT_CLUSTER");
+  return e ? std::max(1, std::min(8, atoi(e))) : 8;
+}
+
 #define LAUNCH_CHECK(ctx)                                   \
   do {                                                      \
     (ctx)->launches++;                                      \
@@ -400,7 +407,7 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
     else {
       // tiles in global memory; clusters of up to 8 CTAs per factor when the factors alone
       // would leave most SMs idle
-      const int cc = std::max(1, std::min(8, kNumSM / std::max(1, (int)n)));
+      const int cc = std::max(1, std::min(gt_cluster_max(), kNumSM / std::max(1, (int)n)));
       if (cc == 1) {
         chol_tiled_kernel<<<(unsigned)n, CT_THREADS, CT_SMEM_BYTES, st>>>(b, 1);
       } else {
@@ -494,7 +501,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         // tiles in global memory: one CTA per factor when the factors fill the GPU, else a
         // cluster of up to 8 CTAs per factor sharing its tiles through L2 (an 8-GPU rank's
         // share of configs[4]: 12 factors of m = 1536)
-        const int cgt = std::max(1, std::min(8, kNumSM / std::max(1, sub[g].nprob)));
+        const int cgt = std::max(1, std::min(gt_cluster_max(), kNumSM / std::max(1, sub[g].nprob)));
         if (C == 0 && cgt == 1) {
           const int mp = (msub + 31) / 32 * 32;
           sytrd_tiled_kernel<1><<<(unsigned)sub[g].nprob, SYT_THREADS,

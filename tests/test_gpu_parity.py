@@ -748,3 +748,26 @@ def test_cfg5_block_stack_bench_launch_config_sampled(cuda_lib):
         So = O.precondition(L.grad(steps - 1).astype(np.float64), UG, DG, cfg.lam, UA, DA, cfg.lam)
         Sg = S[li].double().cpu().numpy()
         assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC, li
+
+
+def test_global_tile_single_cta_paths(cuda_lib, monkeypatch):
+    """The one-CTA-per-factor global-tile tridiagonalisation (MODE 1) and Cholesky, which
+    the library picks when many large factors fill the GPU (configs[4]: 96 factors), forced
+    here on one factor with BKFAC_GT_CLUSTER=1: core m = 1000 (ragged tail), c = 300."""
+    monkeypatch.setenv("BKFAC_GT_CLUSTER", "1")
+    n, c, r = 1300, 300, 700
+    f = synth.random_case(n, c, r, seed=4242, k=min(n, 2 * c), decay=0.9)
+    M0, M1 = f.batch(0).astype(np.float64), f.batch(1).astype(np.float64)
+    ctx = _ctx([(n, r, c, 0)])
+    U0 = synth.phantom_basis(n, r)
+    Ug, Dg = gpu_brand(ctx, 0, U0, np.zeros(r), M0, 0.0, 1.0)
+    Uo, Do = O.brand_update(U0, np.zeros(r), M0, 0.0, 1.0, r)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    U32 = Uo.astype(np.float32).astype(np.float64)
+    D32 = Do.astype(np.float32).astype(np.float64)
+    Ug, Dg = gpu_brand(ctx, 0, U32, D32, M1, 0.95, 0.05)
+    Uo, Do = O.brand_update(U32, D32, M1, 0.95, 0.05, r)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    assert eig_rel_err(Do, Dg) < TOL_EIG
+    assert _orth_check(Ug)
+    assert ctx.bkfac_check()[0] == 0
