@@ -314,16 +314,26 @@ sytrd_tiled_kernel(const __grid_constant__ EigBatch b, int C) {
           colv[jj] = (i > j) ? xe * vi : 0.f;
         }
       }
-      // transpose-reduce: lane l ends with sum over lanes of colv[l]
+      // transpose-reduce: lane l ends with sum over lanes of colv[l] (adds on pairs)
 #pragma unroll
-      for (int s = 16; s >= 1; s >>= 1) {
+      for (int s = 16; s >= 2; s >>= 1) {
         const bool upper = (lane & s) != 0;
 #pragma unroll
-        for (int t = 0; t < s; ++t) {
-          const float send = upper ? colv[t] : colv[t + s];
-          const float keep = upper ? colv[t + s] : colv[t];
-          colv[t] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        for (int t = 0; t < s; t += 2) {
+          const float2 send = upper ? make_float2(colv[t], colv[t + 1]) : make_float2(colv[t + s], colv[t + s + 1]);
+          const float2 keep = upper ? make_float2(colv[t + s], colv[t + s + 1]) : make_float2(colv[t], colv[t + 1]);
+          const float2 recv = make_float2(__shfl_xor_sync(0xffffffffu, send.x, s),
+                                          __shfl_xor_sync(0xffffffffu, send.y, s));
+          const float2 sum = __fadd2_rn(keep, recv);
+          colv[t] = sum.x;
+          colv[t + 1] = sum.y;
         }
+      }
+      {
+        const bool upper = (lane & 1) != 0;
+        const float send = upper ? colv[0] : colv[1];
+        const float keep = upper ? colv[1] : colv[0];
+        colv[0] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
       }
       atomicAdd(&y[i], (racc[0] + racc[1]) + (racc[2] + racc[3]));
       atomicAdd(&y[32 * J + lane], colv[0]);
