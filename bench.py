@@ -7,10 +7,12 @@ accumulate and -- every T_RSVD steps -- the RSVD overwrite (a7, a8), the
 preconditioning of every owned layer (a9), and for N > 1 the NCCL all-gather of the
 preconditioned gradients (§8(e)).
 
-Default workload: BASELINE.json configs[3] semantics on the configs[2] VGG16_bn stack
-(32 K-factors, 16 layers, n_BS = 256, r = min(220, n), rho = 0.95, lambda = 0.1, dense
-EA + RSVD overwrite every 25 steps), the same workload at every GPU count.
-``--config cfg1|cfg2|cfg3|cfg4|cfg5`` selects another BASELINE config.
+Default workload: BASELINE.json configs[4], the transformer-MLP stack the metric's
+1/2/4/8-GPU figures are quoted on (24 blocks x (4097->16384, 16385->4096): 96 K-factors,
+48 layers, n_BS = 1024, r = 512, rho = 0.97, lambda = 0.01), the same workload at every
+GPU count (strong scaling).  ``--config cfg1|cfg2|cfg3|cfg4|cfg5r8`` selects another
+BASELINE config; with an RSVD schedule (cfg2, cfg4) the timed window starts on an
+overwrite step, so it always holds ceil(steps / T_RSVD) overwrites.
 
 value = Brand factor-updates/s over the whole job (all ranks); the line also carries
 preconditioned layers/s.  ``--impl reference`` times the fp64 oracle (the reference arm
@@ -43,7 +45,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=25)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--config", default="cfg5")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -187,8 +189,6 @@ def roofline_from_stages(stages, peaks, clocks):
     if name.startswith("gemm_") and top.get("path") == "tc":
         tf32 = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))) * 0.5
         bound, peak, unit, achieved = "tensor", tf32 / 3.0, "TFLOP/s", top["flops"] / sec / 1e12
-    elif name == "eig_sytrd_gt":   # global-tile tridiagonalisation: streams the trailing matrix
-        bound, peak, unit, achieved = "hbm", float(peaks["hbm_gbs"]), "GB/s", top["bytes"] / sec / 1e9
     elif name.startswith("gemm_") or name.startswith("eig_") or name.startswith("chol"):
         bound, peak, unit, achieved = "alu", fp32_peak, "TFLOP/s", top["flops"] / sec / 1e12
     else:
@@ -295,6 +295,26 @@ def oracle_sample(cfg, budget_s: float):
     return nupd, sum(counts.values()), total, step_s, desc
 
 
+def oracle_thread_ratio(cfg):
+    """Wall time of one oracle Brand update of the workload's smallest Brand-path factor at 1
+    BLAS thread over the same at all threads: scales the all-cores baseline to one core."""
+    import numpy as np
+    import oracle as O
+    from threadpoolctl import threadpool_limits
+    f = min(cfg.factors, key=lambda x: (x.r + x.c >= x.n, x.n))
+    rng = np.random.default_rng(7)
+    U, _ = np.linalg.qr(rng.standard_normal((f.n, f.r)))
+    D = np.sort(rng.random(f.r))[::-1]
+    M = f.batch(1).astype(np.float64)
+    t = {}
+    for nt in (None, 1):
+        with threadpool_limits(limits=nt, user_api="blas"):
+            t0 = time.perf_counter()
+            O.brand_update(U, D, M, cfg.rho, 1 - cfg.rho, f.r)
+            t[nt] = time.perf_counter() - t0
+    return t[None] / t[1], f"one Brand update of n={f.n}: {t[None]:.2f} s at all threads, {t[1]:.2f} s at 1 thread"
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -385,51 +405,78 @@ def run_ours(args, rank, world, local_rank):
 
     use_graphs = not args.no_graphs
 
-    def one_step(i, graph):
+    def one_step(i, graph, profile=False):
         S = stack.step(M_pool[i % args.pool], None if args.factored else J_pool[i % args.pool],
-                       graph=graph, factored=args.factored)
+                       graph=graph, factored=args.factored, profile=profile)
         if gather is not None:
             gather.gather(S)
 
     # warm-up (>= 3 steps also captures the two CUDA graphs of a non-RSVD step: the U/D
-    # ping-pong parity and the input pool alternate together)
-    for i in range(args.warmup):
+    # ping-pong parity and the input pool alternate together).  With an RSVD schedule the
+    # warm-up is extended so that the timed window starts on an overwrite step: the window
+    # then holds ceil(K / T_RSVD) overwrites (never none).
+    warm = args.warmup
+    T = cfg.rsvd_every
+    if T and warm % T != 0:
+        warm += T - warm % T
+    for i in range(warm):
         one_step(i, use_graphs)
     torch.cuda.synchronize()
     code, bad, info = stack.check()
     if code != 0:
         raise SystemExit(f"device status error after warm-up (factor {bad})")
 
-    def timed(first, nsteps, graph):
+    def timed(first, nsteps, graph, profile=False):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(nsteps)]
+        stage_acc = {}
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         for i in range(nsteps):
             flush.zero_()                       # L2 flush between timed steps (not timed)
+            r0 = stack.ctx.bkfac_profile_count() if profile else 0
+            stack.last_profile_range = None
             ev[i][0].record(stream)
-            one_step(first + i, graph)
+            one_step(first + i, graph, profile)
             ev[i][1].record(stream)
+            if profile:
+                # the stage events of this step: a profiled graph's record range (re-recorded
+                # by every replay), or the records an eager (RSVD) step appended
+                rng = stack.last_profile_range or (r0, stack.ctx.bkfac_profile_count())
+                torch.cuda.synchronize()
+                for st_ in stack.ctx.bkfac_profile_read(rng):
+                    acc = stage_acc.setdefault(st_["name"], dict(st_, ms=0.0, flops=0.0, bytes=0.0,
+                                                                 launches=0, calls=0))
+                    for key_ in ("ms", "flops", "bytes", "launches", "calls"):
+                        acc[key_] += st_[key_]
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        return sum(a.elapsed_time(b) for a, b in ev)
+        return sum(a.elapsed_time(b) for a, b in ev), list(stage_acc.values())
 
     # headline: K steps (RSVD steps included at their schedule), profiling off
     sampler = ClockSampler(local_rank)
     sampler.start()
-    ms = timed(args.warmup, args.steps, use_graphs)
+    ms, _ = timed(warm, args.steps, use_graphs)
     clocks = sampler.stop()
-    # stage table + roofline: the next K steps again, eagerly, with the library's per-stage
-    # CUDA events on the launching streams (these events add ~3 % to a step, so this pass
-    # is not the headline); the launch count per step comes from the same pass
+    n_rsvd = sum(1 for k in range(warm, warm + args.steps) if T and k % T == 0)
+    # stage table + roofline: the next K steps again with the library's per-stage CUDA events
+    # on the launching streams.  With graphs these events are nodes of separately captured
+    # "profiled" graphs (the same kernels; the event nodes add little), so the stage times
+    # are graph-replay times like the headline's; launch counts come from an eager step.
     stack.ctx.bkfac_profile_enable(True)
-    l0 = stack.launches()
-    ms_prof = timed(args.warmup + args.steps, args.steps, False)
-    launches = stack.launches() - l0
-    stages = stack.ctx.bkfac_profile_read()
+    first_prof = warm + args.steps
+    if T:   # same RSVD phase as the headline window
+        first_prof += (T - first_prof % T) % T
+        for i in range(warm + args.steps, first_prof):
+            one_step(i, use_graphs)
+    ms_prof, stages = timed(first_prof, args.steps, use_graphs, profile=True)
     stack.ctx.bkfac_profile_enable(False)
+    l0 = stack.launches()
+    one_step(first_prof + args.steps, False)      # one eager step: launches per step
+    torch.cuda.synchronize()
+    launches = (stack.launches() - l0) * args.steps
     t = torch.tensor([ms, float(launches)], dtype=torch.float64, device=device)
     if world > 1:
         tmax = t.clone()
@@ -449,7 +496,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e through the public API with host buffers (pinned), copies timed
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, stack, gather, cfg, device, stream, world)
+        e2e = run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool)
 
     if rank != 0:
         return
@@ -467,7 +514,15 @@ def run_ours(args, rank, world, local_rank):
         upd, lay, ssec, step_s, desc = oracle_sample(cfg, args.cpu_budget_s)
         cpu = {"value": round(n_f / step_s, 4), "unit": UNIT, "cores": blas_threads(),
                "kind": "oracle", "sample": desc + f"; sample took {ssec:.1f}s",
-               "measured_updates_per_s_on_sample": round(upd / ssec, 4)}
+               "measured_updates_per_s_on_sample": round(upd / ssec, 4),
+               "host_cpu_count": os.cpu_count()}
+        try:
+            ratio, rdesc = oracle_thread_ratio(cfg)
+            cpu["value_1_thread"] = round(n_f / step_s * ratio, 4)
+            cpu["value_1_thread_how"] = "all-threads value x (t_all / t_1) measured on " + rdesc
+        except Exception as exc:   # threadpoolctl missing: report the all-cores figure only
+            cpu["value_1_thread"] = None
+            cpu["value_1_thread_how"] = f"unavailable: {exc}"
     line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "weak" if not layers else "strong",
@@ -479,13 +534,16 @@ def run_ours(args, rank, world, local_rank):
                                       if args.correct_every else ""),
                        "factors": n_f, "layers": n_l,
                        "n_BS": cfg.factors[0].c, "rho": cfg.rho, "lambda": cfg.lam,
-                       "rsvd_every": cfg.rsvd_every, "parallelism": f"layer-shard x{world}",
+                       "rsvd_every": cfg.rsvd_every, "rsvd_steps_in_window": n_rsvd,
+                       "parallelism": f"layer-shard x{world}",
                        "l2": "flushed between timed steps (512 MiB write)",
                        "inputs": "device-resident pool of %d synthetic batches" % args.pool},
             "roofline": roof, "stages": table, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
             "launch_mode": "cuda-graph replay (non-RSVD steps)" if use_graphs else "eager",
-            "profiled_pass_ms_per_step": round(ms_prof / args.steps, 4)}
+            "profiled_pass_ms_per_step": round(ms_prof / args.steps, 4),
+            "profiled_pass": ("graph replays with the library's stage events as graph nodes"
+                              if use_graphs else "eager launches with stage events")}
     print(json.dumps(line), flush=True)
 
 
@@ -496,24 +554,22 @@ def stack_uses_tc(stack) -> bool:
         return False
 
 
-def run_e2e(args, stack, gather, cfg, device, stream, world):
+def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
     """Same metric through the public API with HOST inputs: per step, pinned host -> device
     copies of the step's M and J, the step, and a device -> host read of S."""
     import torch
     import torch.distributed as dist
     steps = max(1, min(args.e2e_steps, args.steps))
-    host_M = {}
-    for g in stack.my_factors:
-        f = cfg.factors[g]
-        key = (f.c, f.n)
-        if key not in host_M:
-            host_M[key] = torch.randn(key, dtype=torch.float32).pin_memory()
+    # host inputs: the headline's own synthetic batches (synth recipe, device pool batch 0)
+    # copied to pinned host memory -- every factor's M (so the eigensolver sees the same
+    # spectra as the headline) and one gradient per layer shape (J ~ N(0, var) throughout)
+    host_M = {g: M_pool[0][g].cpu().pin_memory() for g in stack.my_factors}
     host_J, host_S = {}, {}
     for li in stack.my_layers:
         l = cfg.layers[li]
         key = (l.d_G, l.d_A)
         if key not in host_J:
-            host_J[key] = (l.grad_std * torch.randn(key, dtype=torch.float32)).pin_memory()
+            host_J[key] = J_pool[0][li].cpu().pin_memory()
             host_S[key] = torch.empty(key, dtype=torch.float32).pin_memory()
     # two device input sets: step i+1's host->device copies run (copy stream) while step i
     # computes; step i's S is read back (second copy stream) while step i+1 computes
@@ -537,8 +593,7 @@ def run_e2e(args, stack, gather, cfg, device, stream, world):
         with torch.cuda.stream(up):
             up.wait_event(ev_done[b])             # step j-2 (same buffers) has finished
             for g, t in dev_M[b].items():
-                f = cfg.factors[g]
-                t.copy_(host_M[(f.c, f.n)], non_blocking=True)
+                t.copy_(host_M[g], non_blocking=True)
             if not args.factored:
                 for li, t in dev_J[b].items():
                     l = cfg.layers[li]

@@ -241,6 +241,14 @@ bkfac_status bkfac_profile_enable(bkfac_ctx ctx, int enable);   /* also clears r
 /* Synchronises the recorded events, aggregates per stage name into out[0..max_out),
  * clears the records and returns the number of distinct stages (-1 on error). */
 int bkfac_profile_read(bkfac_ctx ctx, bkfac_stage_stat* out, int max_out);
+/* Number of stage records so far (-1 on error). */
+int bkfac_profile_count(bkfac_ctx ctx);
+/* As bkfac_profile_read over records [begin, end) only, and without clearing them.  Events
+ * recorded while profiling was on during a CUDA-graph capture are graph nodes: every replay
+ * re-records them, so reading a graph's record range after each (synchronised) replay gives
+ * that replay's per-stage times.  Returns the number of distinct stages (-1 on error). */
+int bkfac_profile_read_range(bkfac_ctx ctx, int begin, int end, bkfac_stage_stat* out,
+                             int max_out);
 
 const char* bkfac_status_string(bkfac_status s);
 

@@ -32,7 +32,7 @@ EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac
             "bkfac_brand_update", "bkfac_brand_ea_update", "bkfac_ea_accumulate", "bkfac_ea_accumulate_batch",
             "bkfac_rsvd_overwrite", "bkfac_rsvd_overwrite_batch",
             "bkfac_precondition", "bkfac_precondition_factored", "bkfac_light_correction", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
-            "bkfac_profile_enable", "bkfac_profile_read", "bkfac_status_string",
+            "bkfac_profile_enable", "bkfac_profile_read", "bkfac_profile_count", "bkfac_profile_read_range", "bkfac_status_string",
             "bkfac_build_info", "bkfac_gemm"]
 
 
@@ -147,6 +147,10 @@ def load(path: str = None) -> ctypes.CDLL:
     lib.bkfac_profile_enable.restype = ci
     lib.bkfac_profile_read.argtypes = [vp, ctypes.POINTER(StageStat), ci]
     lib.bkfac_profile_read.restype = ci
+    lib.bkfac_profile_count.argtypes = [vp]
+    lib.bkfac_profile_count.restype = ci
+    lib.bkfac_profile_read_range.argtypes = [vp, ci, ci, ctypes.POINTER(StageStat), ci]
+    lib.bkfac_profile_read_range.restype = ci
     lib.bkfac_status_string.argtypes = [ci]
     lib.bkfac_status_string.restype = ctypes.c_char_p
     lib.bkfac_build_info.argtypes = []
@@ -322,9 +326,18 @@ class Context:
     def bkfac_profile_enable(self, on: bool = True) -> None:
         _check(self.lib.bkfac_profile_enable(self.h, 1 if on else 0), "bkfac_profile_enable")
 
-    def bkfac_profile_read(self) -> List[dict]:
+    def bkfac_profile_count(self) -> int:
+        return int(self.lib.bkfac_profile_count(self.h))
+
+    def bkfac_profile_read(self, rng=None) -> List[dict]:
+        """Per-stage event times.  rng=(begin, end): only those records, kept in place
+        (bkfac_profile_read_range; events captured into a CUDA graph are re-recorded by every
+        replay); else all records, cleared (bkfac_profile_read)."""
         arr = (StageStat * 128)()
-        n = self.lib.bkfac_profile_read(self.h, arr, 128)
+        if rng is None:
+            n = self.lib.bkfac_profile_read(self.h, arr, 128)
+        else:
+            n = self.lib.bkfac_profile_read_range(self.h, int(rng[0]), int(rng[1]), arr, 128)
         if n < 0:
             raise BkfacError(6, "bkfac_profile_read")
         return [dict(name=arr[i].name.decode(), calls=arr[i].calls, launches=arr[i].launches,

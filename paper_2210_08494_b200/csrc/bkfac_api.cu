@@ -885,11 +885,15 @@ bkfac_status bkfac_profile_enable(bkfac_ctx c, int enable) {
   return BKFAC_OK;
 }
 
-int bkfac_profile_read(bkfac_ctx c, bkfac_stage_stat* out, int max_out) {
+namespace {
+int profile_aggregate(bkfac_ctx c, bkfac_stage_stat* out, int max_out, bool clear, size_t begin,
+                      size_t end) {
   if (!c) return -1;
   std::map<std::string, bkfac_stage_stat> agg;
   std::vector<std::string> order;
-  for (auto& r : c->recs) {
+  end = std::min(end, c->recs.size());
+  for (size_t ri = begin; ri < end; ++ri) {
+    const auto& r = c->recs[ri];
     if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
@@ -912,9 +916,23 @@ int bkfac_profile_read(bkfac_ctx c, bkfac_stage_stat* out, int max_out) {
     if (out && n < max_out) out[n] = agg[t];
     ++n;
   }
-  c->recs.clear();
-  c->pool_used = 0;
+  if (clear) {
+    c->recs.clear();
+    c->pool_used = 0;
+  }
   return n;
+}
+}  // namespace
+
+int bkfac_profile_read(bkfac_ctx c, bkfac_stage_stat* out, int max_out) {
+  return profile_aggregate(c, out, max_out, true, 0, ~size_t(0));
+}
+
+int bkfac_profile_count(bkfac_ctx c) { return c ? (int)c->recs.size() : -1; }
+
+int bkfac_profile_read_range(bkfac_ctx c, int begin, int end, bkfac_stage_stat* out, int max_out) {
+  if (!c || begin < 0 || end < begin) return -1;
+  return profile_aggregate(c, out, max_out, false, (size_t)begin, (size_t)end);
 }
 
 // ------------------------------------------------------------------------- Brand

@@ -13,7 +13,8 @@ rank n and sketch width l = n, R7); no truncation, no continuation.
 
 Algorithms (:782), each fed the same M_A, M_Gamma stream:
   b-kfac          Brand update every update (T_Brand = T_updt, Alg 4)
-  b-r-kfac        Brand update, RSVD overwrite every 5 updates (Alg 5)
+  b-r-kfac        Brand update every update; every 5 updates it is preceded by the RSVD
+                  overwrite of the previous EA factor Mcal_{k-1} (Alg 5, :641-646)
   b-kfac-c        Brand update, light correction every 5 updates, phi = 0.5 (Alg 6-7)
   r-kfac-T50      RSVD of the EA factor every 5 updates (Alg 2)
   r-kfac-T10      RSVD every update
@@ -142,6 +143,14 @@ def run(fA, fG, layer, r: int, rho: float, lam: float, burn_in: int = 30, window
     for k in range(burn_in + window):
         MA, MG, J = gen(k)
         Ms = (MA, MG)
+        # B-R-KFAC (Alg 5, :641-646): the overwrite is RSVD(Mcal_{k-1}), taken before M_k is
+        # accumulated; the B-update with M_k follows below as on every update
+        for a in algos:
+            if a.brand and a.rsvd and k > 0 and k % a.rsvd == 0:
+                for i in range(2):
+                    U, D = rep[a.name][i]
+                    low.bkfac_rsvd_overwrite(i, K[i], min(oversample, dims[i] - rr[i]), power_iters,
+                                             seed, 2 * k + i, U, D)
         for i in range(2):
             full.bkfac_ea_accumulate(i, K[i], Ms[i], rho if k else 0.0)
             full.bkfac_rsvd_overwrite(i, K[i], 0, 0, seed, k, ex[i][0], ex[i][1])
@@ -152,7 +161,7 @@ def run(fA, fG, layer, r: int, rho: float, lam: float, burn_in: int = 30, window
                     if k % a.evd == 0:
                         U.copy_(ex[i][0]); D.copy_(ex[i][1])
                     continue
-                if a.rsvd and k % a.rsvd == 0:
+                if a.rsvd and not a.brand and k % a.rsvd == 0:   # R-KFAC: RSVD(Mcal_k)
                     low.bkfac_rsvd_overwrite(i, K[i], min(oversample, dims[i] - rr[i]), power_iters,
                                              seed, 2 * k + i, U, D)
                     continue

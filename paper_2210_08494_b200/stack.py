@@ -105,6 +105,7 @@ class BKFACStack:
         self.k = 0
         self.n_overwrites = 0
         self._graphs = {}
+        self.last_profile_range = None
         # preconditioned gradients, two sets by step parity: step k's S stays valid while
         # step k+1 runs (a caller can read it back concurrently)
         self.S2 = [{}, {}]
@@ -135,7 +136,8 @@ class BKFACStack:
         self.D[i][self.cur[i]].zero_()
 
     def step(self, M: Dict[int, "torch.Tensor"], J: Optional[Dict[int, "torch.Tensor"]] = None,
-             stream=None, graph: bool = False, factored: bool = False) -> Dict[int, "torch.Tensor"]:
+             stream=None, graph: bool = False, factored: bool = False,
+             profile: bool = False) -> Dict[int, "torch.Tensor"]:
         """One step over the owned factors (M keyed by global factor index, each (c, n))
         and owned layers (J keyed by global layer index, each (d_G, d_A)).
 
@@ -146,7 +148,12 @@ class BKFACStack:
 
         factored=True preconditions every owned layer by Algorithm 8 (NEXT-f2,
         PAPER.md:882-930) from the factored gradient Mat(g) = G A^T with G = M[Gamma factor],
-        A = M[A factor] (the same per-sample matrices as the statistics); J is not used."""
+        A = M[A factor] (the same per-sample matrices as the statistics); J is not used.
+
+        profile=True (with graph=True) replays a separate graph captured with the library's
+        per-stage events on (the caller enables them with ctx.bkfac_profile_enable first):
+        its event nodes are re-recorded by every replay, and ``last_profile_range`` names the
+        stage records of the graph just replayed (ctx.bkfac_profile_read(rng=...))."""
         torch = self.torch
         eager = (self.rsvd_every and self.k % self.rsvd_every == 0) or \
                 (self.correct_every and self.k % self.correct_every == 0)
@@ -154,19 +161,23 @@ class BKFACStack:
             key = (self.cur[0] if self.cur else 0,
                    tuple(M[g].data_ptr() for g in self.my_factors),
                    tuple(J[li].data_ptr() for li in self.my_layers) if J is not None else None,
-                   factored)
+                   factored, profile)
             main = stream if stream is not None else torch.cuda.current_stream(self.device)
             hit = self._graphs.get(key)
             if hit is None:
                 g = torch.cuda.CUDAGraph()
                 main.synchronize()
+                r0 = self.ctx.bkfac_profile_count() if profile else 0
                 with torch.cuda.graph(g):
                     out = self._step(M, J, torch.cuda.current_stream(self.device), factored)
-                self._graphs[key] = (g, out)
+                rng = (r0, self.ctx.bkfac_profile_count()) if profile else None
+                self._graphs[key] = (g, out, rng)
+                self.last_profile_range = rng
                 with torch.cuda.stream(main):
                     g.replay()          # capture only recorded the launches: run them
                 return out
-            g, out = hit
+            g, out, rng = hit
+            self.last_profile_range = rng
             with torch.cuda.stream(main):
                 g.replay()
             self.k += 1

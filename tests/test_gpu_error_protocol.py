@@ -26,6 +26,12 @@ def _oracle_protocol(fA, fG, layer, r, rho, lam, burn_in, window, algos, oversam
     for k in range(burn_in + window):
         Ms = (fA.batch(k).astype(np.float64), fG.batch(k).astype(np.float64))
         J = layer.grad(k).astype(np.float64)
+        # B-R-KFAC (Alg 5): RSVD(Mcal_{k-1}), then the B-update with M_k
+        for a in algos:
+            if a.brand and a.rsvd and k > 0 and k % a.rsvd == 0:
+                for i in range(2):
+                    rep[a.name][i] = O.rsvd_overwrite(K[i], rr[i], min(oversample, dims[i] - rr[i]),
+                                                      power_iters, seed, 2 * k + i)
         ex = []
         for i in range(2):
             K[i] = O.ea_update(K[i], Ms[i], rho)
@@ -37,7 +43,7 @@ def _oracle_protocol(fA, fG, layer, r, rho, lam, burn_in, window, algos, oversam
                     if k % a.evd == 0:
                         rep[a.name][i] = ex[i]
                     continue
-                if a.rsvd and k % a.rsvd == 0:
+                if a.rsvd and not a.brand and k % a.rsvd == 0:   # R-KFAC: RSVD(Mcal_k)
                     rep[a.name][i] = O.rsvd_overwrite(K[i], rr[i], min(oversample, dims[i] - rr[i]),
                                                       power_iters, seed, 2 * k + i)
                     continue
@@ -82,9 +88,10 @@ def test_error_protocol_matches_oracle(cuda_lib):
         assert np.all(np.isfinite(g))
         bad = np.abs(g - o) > REL * np.abs(o) + ABS
         assert not bad.any(), (a.name, g[bad], o[bad])
-    # the window starts on every algorithm's heaviest update (:784): all RSVD-refreshed
-    # representations are the same RSVD of the same EA factor there
-    first = [np.asarray(got[n][0]) for n in ("b-r-kfac", "r-kfac-T2", "r-kfac-T1", "r-kfac-T6")]
+    # the window starts on every algorithm's heaviest update (:784): all R-KFAC
+    # representations are the same RSVD of the same EA factor there (B-R-KFAC's overwrite
+    # reads Mcal_{k-1} and is followed by a B-update, Alg 5)
+    first = [np.asarray(got[n][0]) for n in ("r-kfac-T2", "r-kfac-T1", "r-kfac-T6")]
     for f in first[1:]:
         assert np.allclose(f, first[0], rtol=1e-4, atol=1e-6)
 
