@@ -208,11 +208,14 @@ bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_fact
  * callers that need the same arithmetic:  C = alpha op(A) op(B) + beta C  (BLAS col-major;
  * op(X) = X^T when trans* != 0; C is M x N with leading dimension ldc >= M).
  * path BKFAC_GEMM_TCGEN05: 3xTF32 on tcgen05 tensor cores (the hot-path kernel);
- * path BKFAC_GEMM_SIMT: fp32 FFMA on CUDA cores (comparison baseline).
+ * path BKFAC_GEMM_SIMT: fp32 FFMA on CUDA cores (comparison baseline);
+ * path BKFAC_GEMM_TCGEN05_PAIR: the tcgen05 kernel forced onto CTA-pair 256 x 256 tiles
+ * (cta_group::2), which the library otherwise picks only for large long-K stages (tests).
  * ws (device, optional, ws_bytes) enables deterministic split-K when K is long and the
  * output small; without it the product runs unsplit.  Asynchronous on `stream`. */
 #define BKFAC_GEMM_TCGEN05 0
 #define BKFAC_GEMM_SIMT 1
+#define BKFAC_GEMM_TCGEN05_PAIR 2
 bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha, const float* A,
                         int lda, const float* B, int ldb, float beta, float* C, int ldc, float* ws,
                         size_t ws_bytes, int path, void* stream);

@@ -23,6 +23,7 @@ BKFAC_PRECOND_CONTINUATION = 1
 BKFAC_PRECOND_LAMBDA_RELATIVE = 2
 BKFAC_GEMM_TCGEN05 = 0
 BKFAC_GEMM_SIMT = 1
+BKFAC_GEMM_TCGEN05_PAIR = 2
 
 STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKFAC_ERR_RANK",
           4: "BKFAC_ERR_ALIAS", 5: "BKFAC_ERR_WORKSPACE", 6: "BKFAC_ERR_CUDA",

@@ -155,20 +155,31 @@ cudaEvent_t prof_event(bkfac_ctx c) {
   return c->pool[c->pool_used++];
 }
 
+// Records a profiling event on `st`.  Under stream capture a plain cudaEventRecord only
+// becomes a dependency edge; cudaEventRecordExternal makes it an event-record node, which
+// every replay of the graph re-records (so per-stage times can be read after a replay).
+void prof_record(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, st);
+}
+
 // Brackets one stage (one or more kernel launches on `st`) with CUDA events.
 void prof_begin(bkfac_ctx c, const char* tag, cudaStream_t st, double flops, double bytes) {
   if (!c->prof) return;
   bkfac_ctx_s::Rec r;
   r.tag = tag; r.flops = flops; r.bytes = bytes; r.launches = c->launches;
   r.a = prof_event(c); r.b = prof_event(c);
-  cudaEventRecord(r.a, st);
+  prof_record(r.a, st);
   c->recs.push_back(r);
   c->open_rec = (int)c->recs.size() - 1;
 }
 void prof_end(bkfac_ctx c, cudaStream_t st) {
   if (!c->prof || c->open_rec < 0) return;
   auto& r = c->recs[c->open_rec];
-  cudaEventRecord(r.b, st);
+  prof_record(r.b, st);
   r.launches = c->launches - r.launches;
   c->open_rec = -1;
 }
@@ -286,13 +297,13 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       for (auto& p : s.probs[v]) {
         any_sym |= p.sym != 0;
         if (p.M <= 0 || p.N <= 0) continue;
-        pair_tiles += (long)ceil_div(p.M, 2 * TC_BM) * ceil_div(p.N, TC_BN);
+        pair_tiles += (long)ceil_div(p.M, 2 * TC_BM) * ceil_div(p.N, TC_BN_PAIR);
         max_nc = std::max<long>(max_nc, ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK));
       }
     pair = !any_sym && (ctx->pair_mode == 2 ||
                         (max_nc > TC_SHORT_K_CHUNKS && pair_tiles >= kNumSM / 2));
   }
-  const int bm = tc ? (pair ? 2 * TC_BM : TC_BM) : SG_BM, bn = tc ? TC_BN : SG_BN;
+  const int bm = tc ? (pair ? 2 * TC_BM : TC_BM) : SG_BM, bn = tc ? (pair ? TC_BN_PAIR : TC_BN) : SG_BN;
   long base_tiles = 0;
   for (int v = 0; v < 4; ++v)
     for (auto& p : s.probs[v]) {
@@ -894,9 +905,9 @@ int profile_aggregate(bkfac_ctx c, bkfac_stage_stat* out, int max_out, bool clea
   end = std::min(end, c->recs.size());
   for (size_t ri = begin; ri < end; ++ri) {
     const auto& r = c->recs[ri];
-    if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
+    if (!cuda_ok(cudaEventSynchronize(r.b))) return -1;
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, r.a, r.b);
+    if (!cuda_ok(cudaEventElapsedTime(&ms, r.a, r.b))) return -1;
     auto it = agg.find(r.tag);
     if (it == agg.end()) {
       bkfac_stage_stat z;
@@ -1825,12 +1836,13 @@ bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha
                         int lda, const float* B, int ldb, float beta, float* C, int ldc, float* ws,
                         size_t ws_bytes, int path, void* stream) {
   if (M < 0 || N < 0 || K < 0 || !C || (K > 0 && (!A || !B))) return BKFAC_ERR_INVALID_ARG;
-  if (path != BKFAC_GEMM_TCGEN05 && path != BKFAC_GEMM_SIMT) return BKFAC_ERR_INVALID_ARG;
+  if (path != BKFAC_GEMM_TCGEN05 && path != BKFAC_GEMM_SIMT && path != BKFAC_GEMM_TCGEN05_PAIR)
+    return BKFAC_ERR_INVALID_ARG;
   if (ldc < std::max(M, 1) || lda < 1 || ldb < 1) return BKFAC_ERR_DIM;
   if (M == 0 || N == 0) return BKFAC_OK;
   bkfac_ctx_s tmp;   // launch bookkeeping only; no workspace
-  tmp.use_tc = path == BKFAC_GEMM_TCGEN05;
-  if (const char* penv = getenv("BKFAC_GEMM_PAIR")) tmp.pair_mode = atoi(penv);
+  tmp.use_tc = path != BKFAC_GEMM_SIMT;
+  if (path == BKFAC_GEMM_TCGEN05_PAIR) tmp.pair_mode = 2;
   if (tmp.use_tc) {
     static bool attrs = false;
     if (!attrs) { attrs = tc_init_attributes(); cudaGetLastError(); }

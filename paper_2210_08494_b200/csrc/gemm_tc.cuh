@@ -95,9 +95,14 @@ struct TcCfg {
 #ifdef BKFAC_TC_STAGES
   static constexpr int STAGES = BKFAC_TC_STAGES;
 #else
-  static constexpr int STAGES = PAIR ? 4 : ((BN >= 256) ? 2 : 3);
+  static constexpr int STAGES = PAIR ? ((BN >= 256) ? 3 : 4) : ((BN >= 256) ? 2 : 3);
 #endif
-  static constexpr int TMEM_COLS = 4 * BN;                   // 2 K-block buffers + running sum
+  // TMEM: BN <= 128: two K-block buffers + a running-sum region (4 BN columns, a power of
+  // two).  BN = 256 ("swap" protocol, see tc_epilogue): two BN-column buffers whose roles
+  // alternate per tile -- the running sum of tile t lives in buffer t & 1, its K-blocks after
+  // the first accumulate in the other one -- so a 256-wide tile fits the 512 TMEM columns.
+  static constexpr bool SWAP = BN >= 256;
+  static constexpr int TMEM_COLS = SWAP ? 2 * BN : 4 * BN;
   static constexpr int LINES = TC_BM + B_ROWS;               // 128-byte lines per stage half
   static constexpr int LPW = LINES / NLW;                    // lines per loader warp
   // quads of A lines and of B lines never mix in one loader-warp quad slot
@@ -324,7 +329,63 @@ BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
 #ifdef BKFAC_TC_TIMING
 __device__ unsigned long long g_tc_dbg[148 * 8];   // tuning builds: per-CTA MMA-warp cycle sums
 #endif
-// Epilogue warps 0-3 (thread = tile row = TMEM lane): promote each K-block accumulator
+// Output of one 16-column group of a finished tile (thread = row i): split-K partials
+// into w, or C = alpha v + beta C0 (coalesced along M), plus the mirrored tile of a symmetric
+// problem through the warp's staging buffer.
+BKFAC_DEV void tc_store_group(const GemmProb& p, const TcTile& x, int g, float (&v)[16], int i,
+                              int quarter, int lane, float beta, float* w, float* stage,
+                              bool& nonfinite) {
+  if (w) {
+    if (i < p.M) {
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int j = x.n0 + g * 16 + jj;
+        if (j < p.N) w[i + (long)j * p.M] = v[jj];
+      }
+    }
+    return;
+  }
+  const bool rowok = i < p.M;
+  const int j0 = x.n0 + g * 16;
+  // all 16 C0 loads of the group in flight together (each thread reads only the elements
+  // it writes, so this is safe when C0 aliases C)
+  float c0v[16];
+  if (beta != 0.f) {
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj)
+      c0v[jj] = (rowok && j0 + jj < p.N) ? p.C0[i + (long)(j0 + jj) * p.ldc0] : 0.f;
+  }
+  // alpha v + beta C0 on pairs (FMUL2 / FFMA2: the same per-element roundings as the scalar
+  // o = alpha v; o += beta c0)
+  const float2 al2 = make_float2(p.alpha, p.alpha), be2 = make_float2(beta, beta);
+#pragma unroll
+  for (int jj = 0; jj < 16; jj += 2) {
+    float2 o = __fmul2_rn(al2, make_float2(v[jj], v[jj + 1]));
+    if (beta != 0.f) {
+      nonfinite |= !isfinite(c0v[jj]) | !isfinite(c0v[jj + 1]);
+      o = __ffma2_rn(be2, make_float2(c0v[jj], c0v[jj + 1]), o);
+    }
+    if (rowok && j0 + jj < p.N) p.C[i + (long)(j0 + jj) * p.ldc] = o.x;
+    if (rowok && j0 + jj + 1 < p.N) p.C[i + (long)(j0 + jj + 1) * p.ldc] = o.y;
+    v[jj] = o.x; v[jj + 1] = o.y;
+  }
+  if (p.sym && x.m0 != x.n0) {
+    // mirror tile C(j, i) = C(i, j): transposed through a warp-private staging buffer so
+    // that each store instruction writes two 64-byte column runs instead of 32 scattered words
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) stage[jj * 34 + lane] = v[jj];
+    __syncwarp();
+#pragma unroll 4
+    for (int q = 0; q < 16; ++q) {
+      const int jj = lane & 15, rr = 2 * q + (lane >> 4);
+      const int ir = x.m0 + quarter * 32 + rr, jc = j0 + jj;
+      if (ir < p.M && jc < p.N) p.C[jc + (long)ir * p.ldc] = stage[jj * 34 + rr];
+    }
+    __syncwarp();
+  }
+}
+
+// Epilogue, BN <= 128 protocol -- warps 0-3 (thread = tile row = TMEM lane): promote each K-block accumulator
 // into the running sum (TMEM), then alpha/beta and coalesced stores of the tile.
 template <int BN, int EPI, bool PAIR>
 BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int lane,
@@ -344,6 +405,7 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
     constexpr int NG = BN / 16, GPW = NG * 4 / EPI;
     const int g_beg = (warp < 4 ? 0 : 1) * GPW;
     int kb = 0;
+    int tl = 0, jf0 = 0, jf1 = 0;   // swap protocol: local tile count, full waits per buffer
     for (int t = tfirst; t < b.total_tiles; t += tstride) {
       TcTile x = tc_tile<BN, BMT>(b, t);
       x.m0 += (int)crank * TC_BM;                              // this CTA's 128 rows
@@ -368,6 +430,59 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
           }
         }
       }
+      if constexpr (BN >= 256) {
+        // "swap" protocol: the tile's running sum lives in buffer sb = (local tile) & 1 --
+        // its first K-block is accumulated there directly -- and every later K-block in
+        // buffer ab = sb ^ 1, which is released as soon as it has been read (S += A), so the
+        // MMA stalls only for that TMEM pass.  The next tile's sum buffer is this tile's ab;
+        // this tile's sb is released after the tile's output, one K-block of slack later.
+        const int sb = tl & 1, ab = sb ^ 1;
+        ++tl;
+        if (nblk > 0) {
+          auto waitfull = [&](int bf) {
+            int& j = bf ? jf1 : jf0;
+            mbar_wait_sleep(tfull_bar(bf), j & 1);
+            ++j;
+            tc_fence_after();
+          };
+          auto release = [&](int bf) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (PAIR && crank != 0) mbar_arrive_remote(tempty_bar(bf), 0);   // the leader's
+              else mbar_arrive(tempty_bar(bf));
+            }
+          };
+          const uint32_t Ssum = tmem_base + lane_off + (uint32_t)(sb * BN);
+          const uint32_t Aacc = tmem_base + lane_off + (uint32_t)(ab * BN);
+          waitfull(sb);
+          for (int blk = 1; blk < nblk; ++blk) {
+            waitfull(ab);
+#pragma unroll 1
+            for (int g = g_beg; g < g_beg + GPW; ++g) {
+              float v[16], r[16];
+              tmem_ld16(Aacc + g * 16, v);
+              tmem_ld16(Ssum + g * 16, r);
+#pragma unroll
+              for (int j = 0; j < 16; j += 2) {   // FADD2: same round-to-nearest per element
+                const float2 t2 = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(r[j], r[j + 1]));
+                v[j] = t2.x; v[j + 1] = t2.y;
+              }
+              tmem_st16(Ssum + g * 16, v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            release(ab);
+          }
+#pragma unroll 1
+          for (int g = g_beg; g < g_beg + GPW; ++g) {
+            if (x.n0 + g * 16 >= p.N) break;      // warp-uniform
+            float v[16];
+            tmem_ld16(Ssum + g * 16, v);
+            tc_store_group(p, x, g, v, i, quarter, lane, beta, w, stage, nonfinite);
+          }
+          release(sb);
+        }
+      } else
       for (int blk = 0; blk < nblk; ++blk, ++kb) {
         const int buf = kb & 1;
         const bool last = blk == nblk - 1;
@@ -391,57 +506,8 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
               v[j] = t.x; v[j + 1] = t.y;
             }
           }
-          if (!last) {
-            tmem_st16(run + g * 16, v);
-          } else if (w) {
-            if (i < p.M) {
-#pragma unroll
-              for (int jj = 0; jj < 16; ++jj) {
-                const int j = x.n0 + g * 16 + jj;
-                if (j < p.N) w[i + (long)j * p.M] = v[jj];
-              }
-            }
-          } else {
-            const bool rowok = i < p.M;
-            const int j0 = x.n0 + g * 16;
-            // all 16 C0 loads of the group in flight together (each thread reads only the
-            // elements it writes, so this is safe when C0 aliases C)
-            float c0v[16];
-            if (beta != 0.f) {
-#pragma unroll
-              for (int jj = 0; jj < 16; ++jj)
-                c0v[jj] = (rowok && j0 + jj < p.N) ? p.C0[i + (long)(j0 + jj) * p.ldc0] : 0.f;
-            }
-            // alpha v + beta C0 on pairs (FMUL2 / FFMA2: the same per-element roundings as
-            // the scalar o = alpha v; o += beta c0)
-            const float2 al2 = make_float2(p.alpha, p.alpha), be2 = make_float2(beta, beta);
-#pragma unroll
-            for (int jj = 0; jj < 16; jj += 2) {
-              float2 o = __fmul2_rn(al2, make_float2(v[jj], v[jj + 1]));
-              if (beta != 0.f) {
-                nonfinite |= !isfinite(c0v[jj]) | !isfinite(c0v[jj + 1]);
-                o = __ffma2_rn(be2, make_float2(c0v[jj], c0v[jj + 1]), o);
-              }
-              if (rowok && j0 + jj < p.N) p.C[i + (long)(j0 + jj) * p.ldc] = o.x;
-              if (rowok && j0 + jj + 1 < p.N) p.C[i + (long)(j0 + jj + 1) * p.ldc] = o.y;
-              v[jj] = o.x; v[jj + 1] = o.y;
-            }
-            if (p.sym && x.m0 != x.n0) {
-              // mirror tile C(j, i) = C(i, j): transposed through a warp-private staging
-              // buffer so that each store instruction writes two 64-byte column runs
-              // instead of 32 scattered words
-#pragma unroll
-              for (int jj = 0; jj < 16; ++jj) stage[jj * 34 + lane] = v[jj];
-              __syncwarp();
-#pragma unroll 4
-              for (int q = 0; q < 16; ++q) {
-                const int jj = lane & 15, rr = 2 * q + (lane >> 4);
-                const int ir = x.m0 + quarter * 32 + rr, jc = j0 + jj;
-                if (ir < p.M && jc < p.N) p.C[jc + (long)ir * p.ldc] = stage[jj * 34 + rr];
-              }
-              __syncwarp();
-            }
-          }
+          if (!last) tmem_st16(run + g * 16, v);
+          else tc_store_group(p, x, g, v, i, quarter, lane, beta, w, stage, nonfinite);
         }
         if (!last) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
@@ -537,15 +603,20 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     if (lane == 0 && (!PAIR || crank == 0)) {
       int stage = 0; uint32_t phase = 0;
       int kb = 0;   // K-block counter over all tiles of this CTA (TMEM buffer = kb & 1)
-      for (int t = tfirst; t < b.total_tiles; t += tstride) {
+      int tl = 0, u0 = 0, u1 = 0;   // swap protocol (BN = 256): local tile, fills per buffer
+      for (int t = tfirst; t < b.total_tiles; t += tstride, ++tl) {
         const TcTile x = tc_tile<BN, BMT>(b, t);
         for (int c0 = x.c_beg; c0 < x.c_end; c0 += TC_PROMO, ++kb) {
-          const int buf = kb & 1;
+          // swap: first K-block of the tile into its sum buffer (tl & 1), the others into
+          // the other buffer (see tc_epilogue)
+          const int buf = Cfg::SWAP ? ((c0 == x.c_beg) ? (tl & 1) : ((tl & 1) ^ 1)) : (kb & 1);
+          int use = (kb >> 1);
+          if (Cfg::SWAP) { int& u = buf ? u1 : u0; use = u; ++u; }
 #ifdef BKFAC_TC_TIMING
           unsigned long long t0 = clock64();
 #endif
-          if (PAIR) mbar_wait_cluster(tempty_bar(buf), ((kb >> 1) & 1) ^ 1);
-          else mbar_wait(tempty_bar(buf), ((kb >> 1) & 1) ^ 1);
+          if (PAIR) mbar_wait_cluster(tempty_bar(buf), (use & 1) ^ 1);
+          else mbar_wait(tempty_bar(buf), (use & 1) ^ 1);
 #ifdef BKFAC_TC_TIMING
           g_tc_dbg[blockIdx.x * 8 + 0] += clock64() - t0;
 #endif
@@ -781,16 +852,25 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 
 // Launch configuration of the hot-path GEMM (BN = 128 tiles, 16 loader warps, two
 // chunks of loads in flight per loader).
-constexpr int TC_BN = 128, TC_NLW = BKFAC_TC_NLW, TC_DEPTH = BKFAC_TC_DEPTH;
+#ifndef BKFAC_TC_BN_PAIR
+#define BKFAC_TC_BN_PAIR 256
+#endif
+// CTA pairs compute 256 x TC_BN_PAIR tiles: with N = 256 every MMA (M = 256, N = 256, K = 8,
+// 128 cycles) reads 4 KB of A and 4 KB of B from each CTA's shared memory (64 B/cycle), and
+// the loaders store 64 KB (hi/lo of 128 A rows + 128 B rows) per 32-deep chunk of 12 MMAs
+// (42 B/cycle): both fit the ~128 B/cycle of shared memory together.  With N = 128 the same
+// chunk needed 96 + 64 B/cycle, which capped the pipe near 80 % of its rate.
+constexpr int TC_BN = 128, TC_BN_PAIR = BKFAC_TC_BN_PAIR, TC_NLW = BKFAC_TC_NLW, TC_DEPTH = BKFAC_TC_DEPTH;
 using TcMain = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 4>;
 using TcShortK = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 8>;
-using TcPair = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 4, true>;
+using TcPair = TcCfg<TC_BN_PAIR, TC_NLW, TC_DEPTH, 4, true>;
 constexpr int TC_SHORT_K_CHUNKS = 8;   // stages with every K <= 8 chunks use 8 epilogue warps
 
 template <bool TA, bool TB, int EPI, bool PAIR>
 inline bool tc_set_attr() {
-  using Cfg = TcCfg<TC_BN, TC_NLW, TC_DEPTH, EPI, PAIR>;
-  return cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, EPI, PAIR>,
+  constexpr int BN = PAIR ? TC_BN_PAIR : TC_BN;
+  using Cfg = TcCfg<BN, TC_NLW, TC_DEPTH, EPI, PAIR>;
+  return cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, BN, TC_NLW, TC_DEPTH, EPI, PAIR>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) == cudaSuccess;
 }
 
@@ -827,7 +907,7 @@ inline cudaError_t tc_launch(const GemmBatch& b, int grid, cudaStream_t st, bool
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 4, true>, b);
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TA, TB, TC_BN_PAIR, TC_NLW, TC_DEPTH, 4, true>, b);
   }
   if (short_k)
     gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 8, false><<<grid, TcShortK::THREADS, TcShortK::SMEM_BYTES, st>>>(b);

@@ -50,6 +50,22 @@ def test_tc_gemm_matches_fp64(cuda_lib, ta, tb, shape):
     assert err < 1e-6, f"3xTF32 error {err:.3e} (normalised)"
 
 
+PAIR_CASES = [  # CTA-pair 256 x 256 tiles: several tiles per pair (> 74 tiles), K-blocks
+    (2560, 2304, 1100), (300, 700, 64), (4097, 512, 1024), (257, 300, 300)]
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("shape", PAIR_CASES)
+def test_tc_gemm_pair_tiles(cuda_lib, ta, tb, shape):
+    """The cta_group::2 path (256 x 256 tiles, TMEM sum / accumulation buffers swapping roles
+    per tile) forced on: ragged tails, one to 5 K-blocks per tile, CTA pairs that walk
+    several tiles (the per-tile buffer alternation and its barrier phases)."""
+    from paper_2210_08494_b200 import binding
+    M, N, K = shape
+    err = _run(ta, tb, M, N, K, 0.75, -0.5, binding.BKFAC_GEMM_TCGEN05_PAIR, seed=M + 5 * N + 11 * K)
+    assert err < 1e-6, f"3xTF32 pair-tile error {err:.3e} (normalised)"
+
+
 def test_tc_gemm_no_workspace_and_beta_zero(cuda_lib):
     from paper_2210_08494_b200 import binding
     err = _run(True, False, 220, 256, 4609, 1.0, 0.0, binding.BKFAC_GEMM_TCGEN05, seed=3,
