@@ -178,7 +178,7 @@ def roofline_from_stages(stages, peaks, clocks):
         return None, []
     # the EA accumulate runs on a side stream beside the tridiagonalisation (library default,
     # BKFAC_EA_MODE != 1): it is off the step's critical path, so it is not the dominant stage
-    side = {"gemm_ea"} if os.environ.get("BKFAC_EA_MODE", "0") != "1" else set()
+    side = {"gemm_ea"}
     total = sum(s["ms"] for s in stages if s["name"] not in side)
     stages = sorted(stages, key=lambda s: -s["ms"])
     top = [s for s in stages if s["name"] not in side][0]
@@ -502,7 +502,7 @@ def run_ours(args, rank, world, local_rank):
         return
     peaks = load_peaks()
     for s in stages:
-        s["path"] = "tc" if os.environ.get("BKFAC_GEMM", "tc") != "simt" and stack_uses_tc(stack) else "simt"
+        s["path"] = "tc" if stack_uses_tc(stack) else "simt"
     roof, table = roofline_from_stages(stages, peaks, clocks)
     if roof is not None:
         variant = ((args.full_rank or args.factored or args.correct_every) and "+variant") or ""
@@ -549,7 +549,7 @@ def run_ours(args, rank, world, local_rank):
 
 def stack_uses_tc(stack) -> bool:
     try:
-        return b"tcgen05" in stack.ctx.lib.bkfac_build_info() and os.environ.get("BKFAC_GEMM") != "simt"
+        return b"tcgen05" in stack.ctx.lib.bkfac_build_info()
     except Exception:
         return False
 

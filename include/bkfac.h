@@ -93,6 +93,33 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
 
 /* Bytes of device workspace needed so that every factor and layer can be processed
  * in a single batched call (all of them concurrently). */
+/* Run-time options of a context (defaults: the tuned configuration).  Synchronous host-side
+ * state; affects calls issued afterwards.  BKFAC_ERR_INVALID_ARG for an unknown option or an
+ * out-of-range value.
+ *   BKFAC_OPT_TWO_STAGE   eigensolver reduction: 0 auto (two-stage dense->band->tridiagonal,
+ *                         sbr.cuh, for orders whose one-stage tiles do not fit a cluster's
+ *                         shared memory, 864 < m <= 1696), 1 one-stage only, 2 two-stage for
+ *                         every order it supports (34 <= m <= 1696)
+ *   BKFAC_OPT_GT_CLUSTER  1..8: largest cluster of the global-tile one-stage tridiagonalisation
+ *                         and of the global-tile Cholesky (default 8)
+ *   BKFAC_OPT_GEMM_PAIR   0 never / 1 auto (default) / 2 always: CTA-pair 256 x 256 GEMM tiles
+ *   BKFAC_OPT_GEMM_SIMT   != 0: every contraction on the fp32 CUDA-core GEMM (comparison)
+ *   BKFAC_OPT_EA_MODE     bkfac_brand_ea_update's EA placement: 0 beside the eigensolver on the
+ *                         SMs it leaves idle (default), 1 serially first, 2 beside uncapped,
+ *                         3 one CTA per tile, 4 as 3 with the join right after the reduction
+ *   BKFAC_OPT_EA_CAP      > 0: the EA grid cap in CTAs instead of the idle-SM count
+ *   BKFAC_OPT_SYT_CLUSTER > 0: wider clusters for the shared-memory tridiagonalisation (tuning)
+ *   BKFAC_OPT_BT_SIMT     != 0: back-transform Gram/T products on the fp32 SIMT GEMM */
+#define BKFAC_OPT_TWO_STAGE 1
+#define BKFAC_OPT_GT_CLUSTER 2
+#define BKFAC_OPT_GEMM_PAIR 3
+#define BKFAC_OPT_GEMM_SIMT 4
+#define BKFAC_OPT_EA_MODE 5
+#define BKFAC_OPT_EA_CAP 6
+#define BKFAC_OPT_SYT_CLUSTER 7
+#define BKFAC_OPT_BT_SIMT 8
+bkfac_status bkfac_set_option(bkfac_ctx ctx, int option, int value);
+
 size_t bkfac_workspace_bytes(bkfac_ctx ctx);
 
 /* Registers caller-owned device memory (>= bkfac_workspace_bytes, 256-B aligned).

@@ -24,12 +24,20 @@ BKFAC_PRECOND_LAMBDA_RELATIVE = 2
 BKFAC_GEMM_TCGEN05 = 0
 BKFAC_GEMM_SIMT = 1
 BKFAC_GEMM_TCGEN05_PAIR = 2
+BKFAC_OPT_TWO_STAGE = 1
+BKFAC_OPT_GT_CLUSTER = 2
+BKFAC_OPT_GEMM_PAIR = 3
+BKFAC_OPT_GEMM_SIMT = 4
+BKFAC_OPT_EA_MODE = 5
+BKFAC_OPT_EA_CAP = 6
+BKFAC_OPT_SYT_CLUSTER = 7
+BKFAC_OPT_BT_SIMT = 8
 
 STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKFAC_ERR_RANK",
           4: "BKFAC_ERR_ALIAS", 5: "BKFAC_ERR_WORKSPACE", 6: "BKFAC_ERR_CUDA",
           7: "BKFAC_ERR_NUMERIC", 8: "BKFAC_ERR_UNSUPPORTED"}
 
-EXPORTED = ["bkfac_init", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac_destroy",
+EXPORTED = ["bkfac_init", "bkfac_set_option", "bkfac_workspace_bytes", "bkfac_set_workspace", "bkfac_destroy",
             "bkfac_brand_update", "bkfac_brand_ea_update", "bkfac_ea_accumulate", "bkfac_ea_accumulate_batch",
             "bkfac_rsvd_overwrite", "bkfac_rsvd_overwrite_batch",
             "bkfac_precondition", "bkfac_precondition_factored", "bkfac_light_correction", "bkfac_gaussian_sketch", "bkfac_check", "bkfac_launch_count",
@@ -142,6 +150,8 @@ def load(path: str = None) -> ctypes.CDLL:
     lib.bkfac_light_correction.restype = ci
     lib.bkfac_check.argtypes = [vp, vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
     lib.bkfac_check.restype = ci
+    lib.bkfac_set_option.argtypes = [vp, ci, ci]
+    lib.bkfac_set_option.restype = ci
     lib.bkfac_launch_count.argtypes = [vp]
     lib.bkfac_launch_count.restype = u64
     lib.bkfac_profile_enable.argtypes = [vp, ci]
@@ -320,6 +330,9 @@ class Context:
         code = self.lib.bkfac_check(self.h, _stream_ptr(stream), ctypes.byref(bad),
                                     ctypes.byref(info))
         return code, bad.value, info.value
+
+    def bkfac_set_option(self, option: int, value: int) -> None:
+        _check(self.lib.bkfac_set_option(self.h, int(option), int(value)), "bkfac_set_option")
 
     def bkfac_launch_count(self) -> int:
         return int(self.lib.bkfac_launch_count(self.h))

@@ -21,6 +21,7 @@
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "misc.cuh"
+#include "sbr.cuh"
 #include "sytrd_tiled.cuh"
 
 using namespace bkfac;
@@ -44,6 +45,8 @@ struct Arena {
 
 struct EigWs {  // workspace of one eigen problem of order <= m with <= r outputs
   size_t K, d, e, tau, lam, Y, scr, piv, V, gt, U, Z, S;
+  size_t Vp = 0, Xp = 0, Wp = 0, Tp = 0, AB = 0, Vq = 0, tq = 0;   // two-stage (sbr.cuh)
+  bool sbr = false;   // two-stage workspace planned (sbr_supported(m))
   int m, r;
 };
 
@@ -51,6 +54,15 @@ void plan_eig(Arena& a, EigWs& w, int m, int r) {
   w.m = m; w.r = r;
   w.K = a.take(sizeof(float) * (size_t)m * m);
   w.gt = sytrd_tiled_cluster(m) == 0 ? a.take(sizeof(float) * syt_global_tile_floats(m)) : 0;
+  w.sbr = sbr_supported(m);
+  if (w.sbr) {
+    const size_t mb = sizeof(float) * (size_t)m * SBR_B;
+    w.Vp = a.take(mb); w.Xp = a.take(mb); w.Wp = a.take(mb);
+    w.Tp = a.take(sizeof(float) * SBR_B * SBR_B);
+    w.AB = a.take(sizeof(float) * (size_t)m * SBR_LDB);
+    w.Vq = a.take(sizeof(float) * (size_t)m * sbr_tasks(m) * SBR_B);
+    w.tq = a.take(sizeof(float) * (size_t)m * sbr_tasks(m));
+  }
   w.d = a.take(sizeof(float) * m);
   w.e = a.take(sizeof(float) * m);
   w.tau = a.take(sizeof(float) * m);
@@ -122,6 +134,16 @@ struct bkfac_ctx_s {
   int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs; < 0: one CTA per tile
   bool ea_join_early = false;   // join the side-stream EA right after the tridiagonalisation
   int pair_mode = 1;  // CTA-pair GEMM tiles: 0 never, 1 large long-K stages, 2 always (tests)
+  // run-time options (bkfac_set_option; defaults are the tuned configuration)
+  int two_stage = 0;    // eigensolver reduction: 0 auto (two-stage when the one-stage tiles do
+                        // not fit a cluster's shared memory), 1 one-stage only, 2 two-stage
+                        // wherever supported
+  int gt_cluster = 8;   // largest cluster of the global-tile tridiagonalisation / Cholesky
+  int syt_cluster = 0;  // > 0: wider clusters for the shared-memory tridiagonalisation (tuning)
+  int bt_simt = 0;      // back-transform Gram / T products on the fp32 SIMT GEMM
+  int ea_mode = 0;      // EA accumulate: 0 beside the eigensolver (capped grid), 1 serial
+                        // first, 2 beside uncapped, 3/4 one CTA per tile (4: early join)
+  int ea_cap = 0;       // > 0: EA grid cap (CTAs) instead of the idle-SM count
   // optional per-stage CUDA-event profiling (bkfac_profile_enable)
   bool prof = false;
   struct Rec { std::string tag; cudaEvent_t a, b; double flops, bytes; uint64_t launches; };
@@ -185,10 +207,13 @@ void prof_end(bkfac_ctx c, cudaStream_t st) {
 }
 
 // largest cluster for the global-tile tridiagonalisation and Cholesky (few factors per GPU);
-// BKFAC_GT_CLUSTER=1 forces one CTA per factor (tests cover both paths at small batch sizes)
-static int gt_cluster_max() {
-  const char* e = getenv("BKFAC_GT_CLUSTER");
-  return e ? std::max(1, std::min(8, atoi(e))) : 8;
+// option BKFAC_OPT_GT_CLUSTER = 1 forces one CTA per factor (tests cover the cluster sizes)
+int gt_cluster_max(bkfac_ctx c) { return std::max(1, std::min(8, c->gt_cluster)); }
+
+// two-stage reduction (sbr.cuh) for an eigenproblem of order m?
+bool use_sbr(bkfac_ctx c, const EigWs& w, int m) {
+  if (!w.sbr || !sbr_supported(m) || c->two_stage == 1) return false;
+  return c->two_stage == 2 || sytrd_tiled_cluster(m) == 0;
 }
 
 #define LAUNCH_CHECK(ctx)                                   \
@@ -418,7 +443,7 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
     else {
       // tiles in global memory; clusters of up to 8 CTAs per factor when the factors alone
       // would leave most SMs idle
-      const int cc = std::max(1, std::min(gt_cluster_max(), kNumSM / std::max(1, (int)n)));
+      const int cc = std::max(1, std::min(gt_cluster_max(ctx), kNumSM / std::max(1, (int)n)));
       if (cc == 1) {
         chol_tiled_kernel<<<(unsigned)n, CT_THREADS, CT_SMEM_BYTES, st>>>(b, 1);
       } else {
@@ -441,6 +466,60 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
     i0 += n;
   }
   v.clear();
+  prof_end(ctx, st);
+  return BKFAC_OK;
+}
+
+// Two-stage reduction (sbr.cuh) of the batch's problems with p.sbr set: stage 1 panel by
+// panel (panel QR, X = A22 V, W, A22 -= V W^T + W V^T), then the bulge chase to d, e.
+bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
+  const int n = b.nprob;
+  int pmax = 0, mmax = 0;
+  for (int i = 0; i < n; ++i)
+    if (b.p[i].sbr) { pmax = std::max(pmax, sbr_panels(b.p[i].m)); mmax = std::max(mmax, b.p[i].m); }
+  constexpr int B = SBR_B;
+  GemmStage gs;
+  bkfac_status rs;
+  for (int j = 0; j < pmax; ++j) {
+    double pf = 0.0;
+    for (int i = 0; i < n; ++i)
+      if (b.p[i].sbr && j < sbr_panels(b.p[i].m)) pf += 4.0 * (double)(b.p[i].m - (j + 1) * B) * B * B;
+    prof_begin(ctx, "eig_sbr_panel", st, pf, 0.0);
+    sbr_panel_kernel<<<(unsigned)n, SBR_PANEL_THREADS, sbr_panel_smem_bytes(mmax), st>>>(b, j);
+    LAUNCH_CHECK(ctx);
+    prof_end(ctx, st);
+    for (int i = 0; i < n; ++i) {     // X = A22 V
+      const EigProb& q = b.p[i];
+      if (!q.sbr || j >= sbr_panels(q.m)) continue;
+      const int r0 = (j + 1) * B, L = q.m - r0;
+      float* A22 = q.K + r0 + (long)r0 * q.ldk;
+      gs.add(false, false, gp(A22, q.ldk, q.Vp + r0, q.m, q.Xp + r0, q.m, L, B, L, 1.f), 0);
+    }
+    if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_x")) != BKFAC_OK) return rs;
+    prof_begin(ctx, "eig_sbr_w", st, pf, 0.0);
+    sbr_w_kernel<<<(unsigned)n, SBR_W_WARPS * 32, sbr_w_smem_bytes(), st>>>(b, j);
+    LAUNCH_CHECK(ctx);
+    prof_end(ctx, st);
+    for (int i = 0; i < n; ++i) {     // A22 -= V W^T + W V^T  (symmetric: lower tiles, mirrored)
+      const EigProb& q = b.p[i];
+      if (!q.sbr || j >= sbr_panels(q.m)) continue;
+      const int r0 = (j + 1) * B, L = q.m - r0;
+      float* A22 = q.K + r0 + (long)r0 * q.ldk;
+      GemmProb pu = gp(q.Vp + r0, q.m, q.Wp + r0, q.m, A22, q.ldk, L, L, 2 * B, -1.f, A22, q.ldk, 1.f);
+      pu.A2 = q.Wp + r0; pu.lda2 = q.m;
+      pu.B2 = q.Vp + r0; pu.ldb2 = q.m;
+      pu.k1 = B;
+      pu.sym = 1;
+      gs.add(false, true, pu, 0);
+    }
+    if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_update")) != BKFAC_OK) return rs;
+  }
+  double cf = 0.0;
+  for (int i = 0; i < n; ++i)
+    if (b.p[i].sbr) cf += 6.0 * (double)b.p[i].m * b.p[i].m * B;
+  prof_begin(ctx, "eig_sbr_chase", st, cf, 0.0);
+  sbr_chase_kernel<<<(unsigned)n, SBR_CHASE_WARPS * 32, sbr_chase_smem_bytes(), st>>>(b);
+  LAUNCH_CHECK(ctx);
   prof_end(ctx, st);
   return BKFAC_OK;
 }
@@ -469,7 +548,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     if (ctx->pending_ea) {
       for (size_t i = 0; i < n; ++i) {
         const int C = sytrd_tiled_cluster(b.p[i].m);
-        ea_busy += C == 0 ? 1 : C;
+        ea_busy += (b.p[i].sbr || C == 0) ? 1 : C;
       }
       if (!cuda_ok(cudaEventRecord(ctx->ev_ea_fork, st))) return BKFAC_ERR_CUDA;
     }
@@ -477,8 +556,17 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     // every factor's tiles live in global memory ("eig_sytrd_gt"), the one-stage reduction
     // streams the trailing lower triangle every column (symv + rank-2 update: read + write
     // of (m-k)^2/2 floats at step k, 4/3 m^3 bytes in all) -- that is its algorithmic traffic
+    bool any_sbr = false, all_sbr = n > 0;
+    for (size_t i = 0; i < n; ++i) { any_sbr |= b.p[i].sbr != 0; all_sbr &= b.p[i].sbr != 0; }
+    if (any_sbr) {
+      const bkfac_status rs0 = run_sbr(ctx, b, st);
+      if (rs0 != BKFAC_OK) return rs0;
+    }
     bool all_gt = n > 0;
-    for (size_t i = 0; i < n; ++i) all_gt &= sytrd_tiled_cluster(b.p[i].m) == 0;
+    for (size_t i = 0; i < n; ++i) all_gt &= b.p[i].sbr || sytrd_tiled_cluster(b.p[i].m) == 0;
+    if (all_sbr) {
+      // every problem was reduced in two stages above
+    } else {
     if (all_gt) prof_begin(ctx, "eig_sytrd_gt", st, 4.0 / 3.0 * m3, 4.0 / 3.0 * m3);
     else prof_begin(ctx, "eig_sytrd", st, 4.0 / 3.0 * m3, 4.0 * m2);
     {
@@ -493,14 +581,13 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         sb.nprob = 0;
         int msub = 0;
         for (size_t i = 0; i < n; ++i)
-          if (sytrd_tiled_cluster(b.p[i].m) == Cs[ci]) {
+          if (!b.p[i].sbr && sytrd_tiled_cluster(b.p[i].m) == Cs[ci]) {
             sb.p[sb.nprob++] = b.p[i];
             msub = std::max(msub, b.p[i].m);
           }
         if (sb.nprob == 0) continue;
         int Cg = Cs[ci];
-        static const int c_force = [] { const char* e = getenv("BKFAC_SYT_C"); return e ? atoi(e) : 0; }();
-        if (c_force > Cg && Cg >= 2) Cg = std::min(c_force, 8);   // tuning: wider clusters
+        if (ctx->syt_cluster > Cg && Cg >= 2) Cg = std::min(ctx->syt_cluster, 8);   // tuning: wider clusters
         gC[ngroups] = Cg; gm[ngroups] = msub; ++ngroups;
       }
       const bool fork = ngroups > 1 && ctx->ev_fork != nullptr;
@@ -512,7 +599,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         // tiles in global memory: one CTA per factor when the factors fill the GPU, else a
         // cluster of up to 8 CTAs per factor sharing its tiles through L2 (an 8-GPU rank's
         // share of configs[4]: 12 factors of m = 1536)
-        const int cgt = std::max(1, std::min(gt_cluster_max(), kNumSM / std::max(1, sub[g].nprob)));
+        const int cgt = std::max(1, std::min(gt_cluster_max(ctx), kNumSM / std::max(1, sub[g].nprob)));
         if (C == 0 && cgt == 1) {
           const int mp = (msub + 31) / 32 * 32;
           sytrd_tiled_kernel<1><<<(unsigned)sub[g].nprob, SYT_THREADS,
@@ -560,6 +647,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
           if (!cuda_ok(cudaStreamWaitEvent(st, ctx->ev_join[g - 1], 0))) return BKFAC_ERR_CUDA;
     }
     prof_end(ctx, st);
+    }   // one-stage problems
     if (ctx->pending_ea) {
       auto f = std::move(ctx->pending_ea);
       ctx->pending_ea = nullptr;
@@ -590,8 +678,17 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     // back-transform V = H Y, blocked (eig.cuh 5'): 2 m^2 r flops in two GEMMs per panel
     // of BT_PW reflectors, applied last panel first
     {
+      if (any_sbr) {   // Q2 (chase reflectors) first: Zr = Q2 Y
+        double q2f = 0.0;
+        for (size_t i = 0; i < n; ++i)
+          if (b.p[i].sbr) q2f += 2.0 * (double)b.p[i].m * b.p[i].m * b.p[i].r;
+        prof_begin(ctx, "eig_sbr_q2", st, q2f, 0.0);
+        sbr_q2_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, SBR_Q2_WARPS * 32)), SBR_Q2_WARPS * 32, 0, st>>>(b);
+        LAUNCH_CHECK(ctx);
+        prof_end(ctx, st);
+      }
       int pmax = 0;
-      for (size_t i = 0; i < n; ++i) pmax = std::max(pmax, bt_panels(b.p[i].m));
+      for (size_t i = 0; i < n; ++i) pmax = std::max(pmax, bt_panels(b.p[i].m, b.p[i].off));
       prof_begin(ctx, "eig_backtr", st, 0.0, 4.0 * m2 + 12.0 * mr);
       backtr_prep_kernel<<<dim3((unsigned)n, 64), 256, 0, st>>>(b);
       LAUNCH_CHECK(ctx);
@@ -601,8 +698,8 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
       if (pmax > 0) {
         for (size_t i = 0; i < n; ++i) {      // S_j = W_j^T W_j
           const EigProb& q = b.p[i];
-          for (int j = 0; j < bt_panels(q.m); ++j) {
-            const int r0 = j * BT_PW + 1, np = std::min(BT_PW, q.m - 2 - j * BT_PW);
+          for (int j = 0; j < bt_panels(q.m, q.off); ++j) {
+            const int r0 = j * BT_PW + q.off, np = std::min(BT_PW, q.m - q.off - 1 - j * BT_PW);
             const float* Wj = q.K + r0 + (long)(j * BT_PW) * q.ldk;
             gs.add(true, false, gp(Wj, q.ldk, Wj, q.ldk, q.Sw + (long)j * 2 * BT_PW * BT_PW, BT_PW, np, np,
                                    q.m - r0, 1.f), 0);
@@ -613,7 +710,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         // are removed by the per-step Newton-Schulz refresh of U_out (R8; the 50-step config-2
         // chain is unchanged: 5.2e-6 vs 5.0e-6 with fp32 SIMT).  BKFAC_BT_SIMT selects the
         // fp32 SIMT kernel for them instead.
-        gs.fp32_simt = getenv("BKFAC_BT_SIMT") != nullptr;
+        gs.fp32_simt = ctx->bt_simt != 0;
         if ((rs2 = run_gemms(ctx, gs, st, "gemm_backtr_s")) != BKFAC_OK) return rs2;
         prof_begin(ctx, "eig_backtr", st, 0.0, 0.0);
         backtr_t_kernel<<<dim3((unsigned)n, (unsigned)pmax), BT_THREADS, bt_smem_bytes(), st>>>(b);
@@ -621,22 +718,22 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         prof_end(ctx, st);
         for (size_t i = 0; i < n; ++i) {      // U_j = W_j T_j
           const EigProb& q = b.p[i];
-          for (int j = 0; j < bt_panels(q.m); ++j) {
-            const int r0 = j * BT_PW + 1, np = std::min(BT_PW, q.m - 2 - j * BT_PW);
+          for (int j = 0; j < bt_panels(q.m, q.off); ++j) {
+            const int r0 = j * BT_PW + q.off, np = std::min(BT_PW, q.m - q.off - 1 - j * BT_PW);
             gs.add(false, false, gp(q.K + r0 + (long)(j * BT_PW) * q.ldk, q.ldk,
                                     q.Sw + (long)j * 2 * BT_PW * BT_PW + BT_PW * BT_PW, BT_PW,
                                     q.Uw + (long)(j * BT_PW) * q.m + r0, q.m, q.m - r0, np, np, 1.f), 0);
           }
         }
-        gs.fp32_simt = getenv("BKFAC_BT_SIMT") != nullptr;
+        gs.fp32_simt = ctx->bt_simt != 0;
         if ((rs2 = run_gemms(ctx, gs, st, "gemm_backtr_wt")) != BKFAC_OK) return rs2;
       }
       for (int j = pmax - 1; j >= 0; --j) {
         for (size_t i = 0; i < n; ++i) {
           const EigProb& q = b.p[i];
-          if (j >= bt_panels(q.m)) continue;
-          const int r0 = j * BT_PW + 1, mr0 = q.m - r0;
-          const int np = std::min(BT_PW, q.m - 2 - j * BT_PW);   // reflectors in this panel
+          if (j >= bt_panels(q.m, q.off)) continue;
+          const int r0 = j * BT_PW + q.off, mr0 = q.m - r0;
+          const int np = std::min(BT_PW, q.m - q.off - 1 - j * BT_PW);   // reflectors in this panel
           // Z = W_j^T V(r0:, :)   (np x r)
           gs.add(true, false, gp(q.K + r0 + (long)(j * BT_PW) * q.ldk, q.ldk, q.V + r0, q.ldv, q.Zw, BT_PW,
                                  np, q.r, mr0, 1.f), 0);
@@ -644,9 +741,9 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         if ((rs2 = run_gemms(ctx, gs, st, "gemm_backtr_z")) != BKFAC_OK) return rs2;
         for (size_t i = 0; i < n; ++i) {
           const EigProb& q = b.p[i];
-          if (j >= bt_panels(q.m)) continue;
-          const int r0 = j * BT_PW + 1, mr0 = q.m - r0;
-          const int np = std::min(BT_PW, q.m - 2 - j * BT_PW);
+          if (j >= bt_panels(q.m, q.off)) continue;
+          const int r0 = j * BT_PW + q.off, mr0 = q.m - r0;
+          const int np = std::min(BT_PW, q.m - q.off - 1 - j * BT_PW);
           // V(r0:, :) -= U_j(r0:, 0:np) Z
           gs.add(false, false, gp(q.Uw + (long)(j * BT_PW) * q.m + r0, q.m, q.Zw, BT_PW, q.V + r0, q.ldv,
                                   mr0, q.r, np, -1.f, q.V + r0, q.ldv, 1.f), 0);
@@ -677,6 +774,16 @@ EigProb eig_prob(bkfac_ctx ctx, const EigWs& w, int m, int r, float* V, int ldv,
   p.Uw = at<float>(ctx, w.U);
   p.Zw = at<float>(ctx, w.Z);
   p.Sw = at<float>(ctx, w.S);
+  p.sbr = use_sbr(ctx, w, m) ? 1 : 0;
+  p.off = p.sbr ? SBR_B : 1;
+  p.Vp = w.sbr ? at<float>(ctx, w.Vp) : nullptr;
+  p.Xp = w.sbr ? at<float>(ctx, w.Xp) : nullptr;
+  p.Wp = w.sbr ? at<float>(ctx, w.Wp) : nullptr;
+  p.Tp = w.sbr ? at<float>(ctx, w.Tp) : nullptr;
+  p.AB = w.sbr ? at<float>(ctx, w.AB) : nullptr;
+  p.Vq = w.sbr ? at<float>(ctx, w.Vq) : nullptr;
+  p.tq = w.sbr ? at<float>(ctx, w.tq) : nullptr;
+  p.Zr = reinterpret_cast<float*>(p.scr);   // free once inverse iteration has finished
   return p;
 }
 
@@ -829,6 +936,9 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   attr_ok &= cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(chol_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT_SMEM_BYTES) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem_bytes(32 * CS_MAXNB)) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sbr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_panel_smem_bytes(SBR_MAX_L + SBR_B)) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sbr_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_w_smem_bytes()) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sbr_chase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_chase_smem_bytes()) == cudaSuccess;
   attr_ok &= tc_init_attributes();
   if (!attr_ok) fprintf(stderr, "bkfac: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
   cudaGetLastError();  // never leave a sticky error behind
@@ -849,11 +959,23 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
     if (!c->side[i] || !c->ev_join[i]) { if (c->ev_fork) cudaEventDestroy(c->ev_fork); c->ev_fork = nullptr; }
   cudaGetLastError();
   cudaSetDevice(dev_prev);
-  const char* env = getenv("BKFAC_GEMM");
-  c->use_tc = !(env && strcmp(env, "simt") == 0);
-  const char* penv = getenv("BKFAC_GEMM_PAIR");   // tuning / tests: 0 off, 2 force
-  if (penv) c->pair_mode = atoi(penv);
   *out = c;
+  return BKFAC_OK;
+}
+
+bkfac_status bkfac_set_option(bkfac_ctx c, int option, int value) {
+  if (!c) return BKFAC_ERR_INVALID_ARG;
+  switch (option) {
+    case BKFAC_OPT_TWO_STAGE: if (value < 0 || value > 2) return BKFAC_ERR_INVALID_ARG; c->two_stage = value; break;
+    case BKFAC_OPT_GT_CLUSTER: if (value < 1 || value > 8) return BKFAC_ERR_INVALID_ARG; c->gt_cluster = value; break;
+    case BKFAC_OPT_GEMM_PAIR: if (value < 0 || value > 2) return BKFAC_ERR_INVALID_ARG; c->pair_mode = value; break;
+    case BKFAC_OPT_GEMM_SIMT: c->use_tc = value == 0; break;
+    case BKFAC_OPT_EA_MODE: if (value < 0 || value > 4) return BKFAC_ERR_INVALID_ARG; c->ea_mode = value; break;
+    case BKFAC_OPT_EA_CAP: if (value < 0) return BKFAC_ERR_INVALID_ARG; c->ea_cap = value; break;
+    case BKFAC_OPT_SYT_CLUSTER: if (value < 0 || value > 8) return BKFAC_ERR_INVALID_ARG; c->syt_cluster = value; break;
+    case BKFAC_OPT_BT_SIMT: c->bt_simt = value != 0; break;
+    default: return BKFAC_ERR_INVALID_ARG;
+  }
   return BKFAC_OK;
 }
 
@@ -1321,7 +1443,7 @@ bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, 
         return BKFAC_ERR_ALIAS;
   // 0 (default): EA GEMM on a side stream beside the tridiagonalisation, grid capped at the
   // SMs its clusters leave idle; 2: the same, uncapped; 1: EA first, serially, full grid
-  static const int ea_mode = [] { const char* e = getenv("BKFAC_EA_MODE"); return e ? atoi(e) : 0; }();
+  const int ea_mode = ctx->ea_mode;
   GemmStage gs;
   // beside the eigensolver the Brand update's aligned copies of M already exist
   bkfac_status r = ea_mode == 1 ? ea_stage(ctx, ea_args, ea_count, gs)
@@ -1340,7 +1462,7 @@ bkfac_status bkfac_brand_ea_update(bkfac_ctx ctx, const bkfac_brand_args* args, 
   ctx->pending_ea = [&](int busy) -> bkfac_status {
     if (!cuda_ok(cudaStreamWaitEvent(ctx->ea_stream, ctx->ev_ea_fork, 0)))   // recorded by run_eig
       return BKFAC_ERR_CUDA;
-    static const int ea_cap = [] { const char* e = getenv("BKFAC_EA_CAP"); return e ? atoi(e) : 0; }();
+    const int ea_cap = ctx->ea_cap;
     ctx->grid_cap = ea_mode == 2 ? 0 : (ea_mode == 3 || ea_mode == 4) ? -1
                   : (ea_cap > 0 ? ea_cap : std::max(kNumSM / 8, kNumSM - busy));
     ctx->ea_join_early = ea_mode == 4;

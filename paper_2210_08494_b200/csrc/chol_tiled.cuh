@@ -139,11 +139,14 @@ BKFAC_DEV void ct_inverse(const float* R, float (&x)[32], int lane) {
 
 struct CholTiledProb {
   const float* G; int ldg;
-  float* L; float* Linv;   // c x c col-major, ld = c
+  float* L; float* Linv;   // c x c col-major, ld = ldl (0: c)
   float* tiles;            // chol_tiled_scratch_floats(c) floats of scratch
   int* status;
   int c;
   float shift;
+  int ldl;                 // leading dimension of L / Linv (0: c); chol_smem_kernel only
+  const float* gref;       // optional device scalar: pivot-drop tolerance reference (the whole
+                           // matrix's max diagonal when this problem is a diagonal block of it)
 };
 constexpr int CT_MAXP = 100;
 struct CholTiledBatch { int nprob; CholTiledProb p[CT_MAXP]; };
@@ -461,9 +464,11 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_smem_kernel(const __grid_c
   __syncthreads();
   float gmax = 0.f;
   for (int w = 0; w < NW; ++w) gmax = fmaxf(gmax, red[w]);
+  if (p.gref) gmax = fmaxf(gmax, *p.gref);
   if (tid == 0) s_drop = 0;
   const float sh = (p.shift > 0.f) ? p.shift * trace : 0.f;   // shifted CholeskyQR
   const float tol = 4.0f * 1.1920929e-7f * (gmax + sh);
+  const long ldl = p.ldl ? p.ldl : c;
   __syncthreads();
 
   for (int J = 0; J < NB; ++J) {
@@ -540,7 +545,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_smem_kernel(const __grid_c
     for (int jj = 0; jj < 32; ++jj) {
       const int j = 32 * J + jj;
       if (j >= c) break;
-      p.L[i + (long)j * c] = (T && !(I == J && lane < jj)) ? T[jj * 32 + lane] : 0.f;
+      p.L[i + (long)j * ldl] = (T && !(I == J && lane < jj)) ? T[jj * 32 + lane] : 0.f;
     }
   }
   __syncthreads();
@@ -619,11 +624,46 @@ __global__ void __launch_bounds__(CT_THREADS, 1) chol_smem_kernel(const __grid_c
       for (int jj = 0; jj < 32; ++jj) {
         const int j = 32 * J + jj;
         if (j >= c) break;
-        p.Linv[i + (long)j * c] = xv[jj];
+        p.Linv[i + (long)j * ldl] = xv[jj];
       }
     }
   }
   if (tid == 0 && s_drop && p.status) atomicOr(p.status, ST_CHOL_DROP);
+}
+
+// Blocked Cholesky for c > 256 (host side: run_chol_blocked in bkfac_api.cu): 256 x 256
+// diagonal blocks on chol_smem_kernel, the panel solve L21 = A21 L11^{-T} and the trailing
+// update A22 -= L21 L21^T (SYRK), and the off-diagonal blocks of L^{-1}, on the tcgen05 GEMM.
+// This kernel starts it: A = lower(G) + shift * trace(G) I into L (upper zero), L^{-1} = 0,
+// and the tolerance reference max_i G_ii + shift trace(G) into *gref.
+// grid (nprob, 32), block 256.
+__global__ void __launch_bounds__(256) chol_blocked_prep_kernel(const __grid_constant__ CholTiledBatch b) {
+  const CholTiledProb& p = b.p[blockIdx.x];
+  const int c = p.c;
+  __shared__ float red[32];
+  float ds = 0.f, dm = 0.f;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) {
+    const float g = p.G[i + (long)i * p.ldg];
+    ds += g;
+    dm = fmaxf(dm, g);
+  }
+  const float trace = block_sum(ds, red);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dm = fmaxf(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dm;
+  __syncthreads();
+  float gmax = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) gmax = fmaxf(gmax, red[w]);
+  const float sh = (p.shift > 0.f) ? p.shift * trace : 0.f;
+  if (blockIdx.y == 0 && threadIdx.x == 0) *const_cast<float*>(p.gref) = gmax + sh;
+  const long tot = (long)c * c;
+  for (long e = blockIdx.y * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.y * blockDim.x) {
+    const int i = (int)(e % c), j = (int)(e / c);
+    float v = 0.f;
+    if (i >= j) v = p.G[i + (long)j * p.ldg] + (i == j ? sh : 0.f);
+    p.L[e] = v;
+    p.Linv[e] = 0.f;
+  }
 }
 
 }  // namespace bkfac

@@ -30,6 +30,13 @@ struct EigProb {
   float* Uw;               // blocked back-transform: m x (npanel*BT_PW) panels U_j = W_j T_j
   float* Zw;               // blocked back-transform: BT_PW x r scratch
   float* Sw;               // blocked back-transform: per panel S_j, T_j (BT_PW x BT_PW each)
+  int off;                 // reflector offset: reflector of column k has its unit at row k + off
+                           // (1: one-stage sytrd; SBR_B: two-stage, sbr.cuh)
+  int sbr;                 // two-stage tridiagonalisation (sbr.cuh) for this problem
+  float* Vp; float* Xp; float* Wp; float* Tp;   // sbr stage 1: m x B panel V, X, W; B x B T
+  float* AB;               // sbr stage 2: band with bulge space, m x SBR_LDB
+  float* Vq; float* tq;    // sbr chase reflectors (m x KT x B, m x KT)
+  float* Zr;               // sbr: Q2 Y, fp32 row-major m x r (in the inverse-iteration scratch)
 };
 constexpr int EIG_MAXP = 100;
 struct EigBatch { int nprob; EigProb p[EIG_MAXP]; };
@@ -512,7 +519,10 @@ __global__ void __launch_bounds__(1024) backtr_kernel(const __grid_constant__ Ei
 //            (bkfac_api.cu).  2 m^2 r flops become two GEMMs per panel instead of m-2
 //            sequential rank-1 reflections.
 constexpr int BT_PW = 128;
-__host__ __device__ inline int bt_panels(int m) { return m > 2 ? (m - 2 + BT_PW - 1) / BT_PW : 0; }
+// panels of BT_PW reflectors; reflectors exist for columns k < m - off - 1
+__host__ __device__ inline int bt_panels(int m, int off = 1) {
+  return m > off + 1 ? (m - off - 1 + BT_PW - 1) / BT_PW : 0;
+}
 
 // grid: (nprob, 64), block 256
 __global__ void backtr_prep_kernel(const __grid_constant__ EigBatch b) {
@@ -522,14 +532,14 @@ __global__ void backtr_prep_kernel(const __grid_constant__ EigBatch b) {
   for (long e = blockIdx.y * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.y * blockDim.x) {
     const int i = (int)(e % m), k = (int)(e / m);
     float* a = p.K + i + (long)k * p.ldk;
-    if (k >= m - 2 || i < k + 1) *a = 0.f;
-    else if (i == k + 1) *a = 1.f;
+    if (k >= m - p.off - 1 || i < k + p.off) *a = 0.f;
+    else if (i == k + p.off) *a = 1.f;
   }
   int bad = 0;
   const long tv = (long)m * r;
   for (long e = blockIdx.y * (long)blockDim.x + threadIdx.x; e < tv; e += (long)gridDim.y * blockDim.x) {
     const int i = (int)(e % m), j = (int)(e / m);
-    const float v = (float)p.Y[(long)i * r + j];
+    const float v = p.sbr ? p.Zr[(long)i * r + j] : (float)p.Y[(long)i * r + j];
     bad |= !isfinite(v);
     p.V[i + (long)j * p.ldv] = v;
   }
@@ -544,13 +554,13 @@ inline size_t bt_smem_bytes() { return sizeof(float) * 2 * BT_PW * (BT_PW + 1); 
 __global__ void __launch_bounds__(BT_THREADS) backtr_t_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   const int m = p.m, j = blockIdx.y;
-  if (j >= bt_panels(m)) return;
+  if (j >= bt_panels(m, p.off)) return;
   constexpr int PW = BT_PW, LD = BT_PW + 1;
   extern __shared__ __align__(16) float btsm[];
   float* S = btsm;
   float* T = S + PW * LD;
   const int tid = threadIdx.x;
-  const int k0 = j * PW, np = min(PW, m - 2 - k0);
+  const int k0 = j * PW, np = min(PW, m - p.off - 1 - k0);
   const float* Sg = p.Sw + (long)j * 2 * PW * PW;         // S_j col-major, ld PW
   float* Tg = p.Sw + (long)j * 2 * PW * PW + PW * PW;     // T_j col-major, ld PW
   for (int e = tid; e < PW * PW; e += BT_THREADS) {

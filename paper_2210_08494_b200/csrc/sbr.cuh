@@ -1,0 +1,475 @@
+// Two-stage Householder tridiagonalisation for the large eigenproblems of the path (the
+// Brand cores of order m = r + c = 1536 at configs[4]): "EVD(M_S)" of Alg 3 line 4
+// (PAPER.md:505).  The one-stage reduction (sytrd_tiled.cuh) streams the whole trailing
+// matrix once per column -- 4/3 m^3 bytes per factor, HBM-bound when 96 such factors run
+// at once.  Here the reduction is split:
+//
+// Stage 1, dense -> band (bandwidth SBR_B = 32), panel by panel j (columns c0 = 32 j ..
+// c0 + 31, rows below the band r0 = c0 + 32 .. m - 1, L = m - r0):
+//   sbr_panel_kernel  Householder QR of P = K[r0:, c0:c0+32] in shared memory: R stays in
+//                     K (it is the band part of those columns), the reflectors' tails go
+//                     below it (geqrf layout: reflector of column k has its unit at row
+//                     k + 32), the explicit unit-lower V into Vp and the compact-WY factor T
+//                     (Q = I - V T V^T, dlarft recurrence) into Tp.
+//   GEMM  X = A22 V                 (A22 = K[r0:, r0:], full symmetric storage; tcgen05)
+//   sbr_w_kernel      Y = X T,  W = Y - 1/2 V (T^T (V^T Y))
+//   GEMM  A22 -= V W^T + W V^T      (symmetric: lower tiles computed and mirrored; tcgen05)
+// which is the two-sided block update Q^T A22 Q = A22 - V W^T - W V^T.  All O(m^3) work of
+// the reduction is in the two GEMMs per panel: m / 32 synchronisation points instead of m.
+//
+// Stage 2, band -> tridiagonal (sbr_chase_kernel, one CTA per problem): bulge chasing.
+// Sweep j annihilates column j below the subdiagonal (task 0: reflector on rows j+1 ..
+// j+32, applied two-sidedly to that diagonal block); task k >= 1 right-applies the
+// previous reflector to the block below (rows R_k = [j+1+32k, +32), columns R_{k-1}),
+// which fills it, computes a reflector from its first column, applies it from the left and
+// two-sidedly to the diagonal block R_k.  The fill beyond the band (at most 2b - 1 below the
+// diagonal) is removed by the following sweeps.  One warp per sweep (lane = row of the
+// 32-row block), sweeps pipelined over the CTA's warps: task (j, k) starts once sweep j - 1
+// has finished task k + 1 (the last task whose rows meet those of (j, k)).  The band with
+// its bulge space (2b diagonals) lives in global memory (L2-resident; ld/st.cg).
+//
+// Back-transform V = Q1 Q2 Y of the tridiagonal's eigenvectors Y (eig.cuh 2-4):
+//   sbr_q2_kernel  applies the chase reflectors: in reverse order, grouped into "diamonds"
+//                  (the reflectors of 32 consecutive sweeps at the same task index touch a
+//                  63-row window, applied in one pass with the window in registers, lane =
+//                  eigenvector column; diamonds run group by group, last group first, task
+//                  index ascending inside a group -- the order the overlaps require).
+//   then the blocked compact-WY back-transform of eig.cuh with reflector offset 32 (Q1).
+#pragma once
+#include "common.cuh"
+#include "eig.cuh"
+
+namespace bkfac {
+
+constexpr int SBR_B = 32;                 // band width (= warp size: lane = row of a block)
+constexpr int SBR_LDB = 2 * SBR_B;        // band storage: diagonals 0 .. 2b-1 (bulge included)
+constexpr int SBR_PANEL_THREADS = 512;
+constexpr int SBR_W_WARPS = 8;
+constexpr int SBR_CHASE_WARPS = 16;
+constexpr int SBR_Q2_WARPS = 8;           // 256 eigenvector columns per CTA
+constexpr int SBR_G = 32;                 // sweeps per diamond
+constexpr int SBR_MAX_L = 1664;           // panel rows held in shared memory (m <= 1696)
+
+__host__ __device__ inline int sbr_panels(int m) { return m - 2 >= SBR_B ? (m - 2) / SBR_B : 0; }
+__host__ __device__ inline int sbr_tasks(int m) { return (m + SBR_B - 1) / SBR_B + 1; }   // KT
+inline bool sbr_supported(int m) { return m - SBR_B <= SBR_MAX_L && sbr_panels(m) > 0; }
+inline size_t sbr_panel_smem_bytes(int m) {
+  return sizeof(float) * ((size_t)(m - SBR_B) * SBR_B + 2 * SBR_B * (SBR_B + 1) + 64 + SBR_B);
+}
+inline size_t sbr_w_smem_bytes() {
+  return sizeof(float) * (3 * SBR_B * (SBR_B + 1) + SBR_W_WARPS * 3 * SBR_B * (SBR_B + 1));
+}
+inline size_t sbr_chase_smem_bytes() {
+  return sizeof(float) * SBR_CHASE_WARPS * (2 * SBR_B * (SBR_B + 1) + 3 * SBR_B) + 64 * sizeof(int);
+}
+
+// ---------------------------------------------------------------------- stage 1: panel QR
+// grid (nprob), block SBR_PANEL_THREADS; panel j of every problem that has one.
+__global__ void __launch_bounds__(SBR_PANEL_THREADS, 1)
+sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
+  const EigProb& p = b.p[blockIdx.x];
+  const int m = p.m, ld = p.ldk;
+  if (p.sbr == 0 || j >= sbr_panels(m)) return;
+  constexpr int B = SBR_B, NT = SBR_PANEL_THREADS, NW = NT / 32, LDT = B + 1;
+  const int c0 = j * B, r0 = c0 + B, L = m - r0;
+  extern __shared__ __align__(16) float ps[];
+  float* P = ps;                     // L x B, col-major (ld L)
+  float* G = P + (size_t)L * B;      // B x B, G[a*LDT + c] = (V^T V)(a, c), c >= a
+  float* T = G + B * LDT;            // B x B upper triangular, T[a*LDT + c]
+  float* red = T + B * LDT;          // 64
+  float* taus = red + 64;            // B
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* K = p.K;
+  for (int e = tid; e < L * B; e += NT) {
+    const int l = e % L, i = e / L;
+    P[e] = K[(r0 + l) + (long)(c0 + i) * ld];
+  }
+  __syncthreads();
+  for (int i = 0; i < B; ++i) {
+    float taui = 0.f;
+    if (i < L) {
+      float s = 0.f;
+      for (int l = i + 1 + tid; l < L; l += NT) s = fmaf(P[l + i * L], P[l + i * L], s);
+      s = block_sum(s, red);
+      const float alpha = P[i + i * L];
+      if (L - i > 1 && s > 0.f) {
+        const float beta = -copysignf(sqrtf(fmaf(alpha, alpha, s)), alpha);
+        taui = (beta - alpha) / beta;
+        const float sc = 1.f / (alpha - beta);
+        for (int l = i + 1 + tid; l < L; l += NT) P[l + i * L] *= sc;
+        __syncthreads();
+        if (tid == 0) P[i + i * L] = beta;
+        // H_i applied to the panel's later columns (one warp per column)
+        for (int c = i + 1 + warp; c < B; c += NW) {
+          float d = 0.f;
+          for (int l = i + 1 + lane; l < L; l += 32) d = fmaf(P[l + i * L], P[l + c * L], d);
+          d = warp_sum(d) + P[i + c * L];
+          const float tw = taui * d;
+          for (int l = i + 1 + lane; l < L; l += 32) P[l + c * L] = fmaf(-tw, P[l + i * L], P[l + c * L]);
+          if (lane == 0) P[i + c * L] -= tw;
+        }
+      }
+    }
+    if (tid == 0) taus[i] = taui;
+    __syncthreads();
+  }
+  // G = V^T V (upper part c >= a), V unit lower trapezoidal (V(l, a) = P[l + a L], l > a)
+  for (int e = tid; e < B * B; e += NT) {
+    const int a = e / B, c = e % B;
+    if (c < a || c >= L) continue;
+    float s = (c == a) ? 1.f : P[c + a * L];       // row l = c: V(c, c) = 1
+    for (int l = c + 1; l < L; ++l) s = fmaf(P[l + a * L], P[l + c * L], s);
+    G[a * LDT + c] = s;
+  }
+  for (int e = tid; e < B * LDT; e += NT) T[e] = 0.f;
+  __syncthreads();
+  // T(0:i, i) = -tau_i T(0:i, 0:i) G(0:i, i), T(i, i) = tau_i
+  for (int i = 0; i < B; ++i) {
+    const float ti = taus[i];
+    if (tid < i && i < L) {
+      float s = 0.f;
+      for (int c = tid; c < i; ++c) s = fmaf(T[tid * LDT + c], G[c * LDT + i], s);
+      T[tid * LDT + i] = -ti * s;
+    } else if (tid == i) {
+      T[i * LDT + i] = ti;
+    }
+    __syncthreads();
+  }
+  // write back: K panel (R above / on the diagonal, reflector tails below), explicit V, T, tau
+  for (int e = tid; e < L * B; e += NT) {
+    const int l = e % L, i = e / L;
+    const float x = P[e];
+    K[(r0 + l) + (long)(c0 + i) * ld] = x;
+    p.Vp[(r0 + l) + (long)i * m] = (l < i) ? 0.f : (l == i ? 1.f : x);
+  }
+  for (int e = tid; e < B * B; e += NT) {
+    const int a = e % B, c = e / B;
+    p.Tp[a + c * B] = T[a * LDT + c];
+  }
+  if (tid < B) p.tau[c0 + tid] = taus[tid];
+}
+
+// ---------------------------------------------------------------------- stage 1: W
+// grid (nprob), block SBR_W_WARPS*32:  Y = X T;  Z = V^T Y;  M2 = T^T Z;  W = Y - 1/2 V M2
+// (rows r0 .. m-1 of the m x B buffers Xp, Vp, Wp, col-major ld m).  Each warp walks 32-row
+// blocks staged through shared memory (coalesced loads, lane = column in the arithmetic).
+__global__ void __launch_bounds__(SBR_W_WARPS * 32)
+sbr_w_kernel(const __grid_constant__ EigBatch b, int j) {
+  const EigProb& p = b.p[blockIdx.x];
+  const int m = p.m;
+  if (p.sbr == 0 || j >= sbr_panels(m)) return;
+  constexpr int B = SBR_B, LDT = B + 1, NW = SBR_W_WARPS;
+  const int r0 = (j + 1) * B, L = m - r0;
+  extern __shared__ __align__(16) float wsm[];
+  float* T = wsm;                    // T[a*LDT + c]
+  float* Zs = T + B * LDT;           // Z, then M2 (in place after a sync)
+  float* M2 = Zs + B * LDT;
+  float* tiles = M2 + B * LDT;       // per warp: xs, vs, ys (B x LDT each); also the Z reduction
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* xs = tiles + warp * 3 * B * LDT;
+  float* vs = xs + B * LDT;
+  float* ys = vs + B * LDT;
+  for (int e = tid; e < B * B; e += NW * 32) {
+    const int a = e % B, c = e / B;
+    T[a * LDT + c] = p.Tp[a + c * B];
+  }
+  __syncthreads();
+  const float* X = p.Xp;
+  const float* V = p.Vp;
+  float* W = p.Wp;
+  float zacc[B];
+#pragma unroll
+  for (int a = 0; a < B; ++a) zacc[a] = 0.f;
+  const int nblk = (L + B - 1) / B;
+  for (int blk = warp; blk < nblk; blk += NW) {
+    const int rb = r0 + blk * B;
+    const bool ok = rb + lane < m;
+#pragma unroll 4
+    for (int a = 0; a < B; ++a) {
+      xs[lane * LDT + a] = ok ? X[(rb + lane) + (long)a * m] : 0.f;
+      vs[lane * LDT + a] = ok ? V[(rb + lane) + (long)a * m] : 0.f;
+    }
+    __syncwarp();
+    for (int i = 0; i < B; ++i) {
+      float y = 0.f;
+#pragma unroll
+      for (int a = 0; a < B; ++a) y = fmaf(xs[i * LDT + a], T[a * LDT + lane], y);
+      ys[i * LDT + lane] = y;
+#pragma unroll
+      for (int a = 0; a < B; ++a) zacc[a] = fmaf(vs[i * LDT + a], y, zacc[a]);
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int a = 0; a < B; ++a)
+      if (ok) W[(rb + lane) + (long)a * m] = ys[lane * LDT + a];   // Y, finished below
+    __syncwarp();
+  }
+  __syncthreads();
+  // Z = sum over warps (reduction space: the tiles)
+  float* zr = tiles;                 // [NW][B][LDT]
+#pragma unroll
+  for (int a = 0; a < B; ++a) zr[(warp * B + a) * LDT + lane] = zacc[a];
+  __syncthreads();
+  for (int e = tid; e < B * B; e += NW * 32) {
+    const int a = e / B, c = e % B;
+    float s = 0.f;
+    for (int w = 0; w < NW; ++w) s += zr[(w * B + a) * LDT + c];
+    Zs[a * LDT + c] = s;
+  }
+  __syncthreads();
+  for (int e = tid; e < B * B; e += NW * 32) {    // M2 = T^T Z  (T upper: e <= a)
+    const int a = e / B, c = e % B;
+    float s = 0.f;
+    for (int q = 0; q <= a; ++q) s = fmaf(T[q * LDT + a], Zs[q * LDT + c], s);
+    M2[a * LDT + c] = 0.5f * s;
+  }
+  __syncthreads();
+  for (int blk = warp; blk < nblk; blk += NW) {
+    const int rb = r0 + blk * B;
+    const bool ok = rb + lane < m;
+#pragma unroll 4
+    for (int a = 0; a < B; ++a) {
+      ys[lane * LDT + a] = ok ? W[(rb + lane) + (long)a * m] : 0.f;
+      vs[lane * LDT + a] = ok ? V[(rb + lane) + (long)a * m] : 0.f;
+    }
+    __syncwarp();
+    for (int i = 0; i < B; ++i) {
+      float w = ys[i * LDT + lane];
+#pragma unroll
+      for (int a = 0; a < B; ++a) w = fmaf(-vs[i * LDT + a], M2[a * LDT + lane], w);
+      xs[i * LDT + lane] = w;
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int a = 0; a < B; ++a)
+      if (ok) W[(rb + lane) + (long)a * m] = xs[lane * LDT + a];
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------- stage 2: chase
+BKFAC_DEV float sbr_ldcg(const float* a) { return __ldcg(a); }
+BKFAC_DEV void sbr_stcg(float* a, float v) { __stcg(a, v); }
+
+// grid (nprob), block SBR_CHASE_WARPS*32.  Band element (r, c), 0 <= r - c < SBR_LDB, at
+// AB[c * SBR_LDB + (r - c)].  Outputs d, e (fp32 tridiagonal) and the chase reflectors:
+// task (j, k) -> Vq[((j * KT) + k) * B + i], tq[j * KT + k].
+__global__ void __launch_bounds__(SBR_CHASE_WARPS * 32, 1)
+sbr_chase_kernel(const __grid_constant__ EigBatch b) {
+  const EigProb& p = b.p[blockIdx.x];
+  if (p.sbr == 0) return;
+  const int m = p.m, ld = p.ldk;
+  constexpr int B = SBR_B, LDB = SBR_LDB, NW = SBR_CHASE_WARPS, LDT = B + 1;
+  const int KT = sbr_tasks(m);
+  extern __shared__ __align__(16) float csm[];
+  volatile int* prog = reinterpret_cast<volatile int*>(csm);      // 64 ints
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* Dt = csm + 64 + warp * (2 * B * LDT + 3 * B);
+  float* Et = Dt + B * LDT;
+  float* vs = Et + B * LDT;
+  float* ws = vs + B;
+  float* us = ws + B;
+  float* AB = p.AB;
+  const float* K = p.K;
+  // band of the stage-1 result (lower, bandwidth B) + zeroed bulge space
+  for (long e = tid; e < (long)m * LDB; e += NW * 32) {
+    const int c = (int)(e / LDB), d = (int)(e % LDB);
+    AB[e] = (d <= B && c + d < m) ? K[(c + d) + (long)c * ld] : 0.f;
+  }
+  if (tid < 64) prog[tid] = -1;
+  __syncthreads();
+  auto at = [&](int r, int c) -> float* { return AB + (long)c * LDB + (r - c); };
+  for (int j = warp; j < m - 2; j += NW) {
+    float tau_u = 0.f;
+    for (int k = 0;; ++k) {
+      const int s = j + 1 + k * B;
+      if (s >= m) break;
+      const int nk = min(B, m - s);
+      if (j > 0) {
+        const int need = ((j - 1) << 8) + (k + 2);
+        while (prog[(j - 1) % NW] < need) __nanosleep(32);
+      }
+      __syncwarp();
+      float x;
+      float er[B];
+      if (k == 0) {
+        x = lane < nk ? sbr_ldcg(at(s + lane, j)) : 0.f;
+      } else {
+#pragma unroll
+        for (int l = 0; l < B; ++l) er[l] = lane < nk ? sbr_ldcg(at(s + lane, s - B + l)) : 0.f;
+        // E <- E H_{k-1}
+        float t = 0.f;
+#pragma unroll
+        for (int l = 0; l < B; ++l) t = fmaf(er[l], us[l], t);
+        t *= tau_u;
+#pragma unroll
+        for (int l = 0; l < B; ++l) er[l] = fmaf(-t, us[l], er[l]);
+        x = er[0];
+      }
+      // reflector from x (length nk): annihilates x[1:nk]
+      const float alpha = __shfl_sync(0xffffffffu, x, 0);
+      const float xn2 = warp_sum((lane >= 1 && lane < nk) ? x * x : 0.f);
+      float tau = 0.f, beta = alpha, v = lane == 0 ? 1.f : 0.f;
+      if (nk > 1 && xn2 > 0.f) {
+        beta = -copysignf(sqrtf(fmaf(alpha, alpha, xn2)), alpha);
+        tau = (beta - alpha) / beta;
+        v = lane == 0 ? 1.f : (lane < nk ? x / (alpha - beta) : 0.f);
+      }
+      vs[lane] = v;
+      __syncwarp();
+      if (k == 0) {
+        if (lane < nk) sbr_stcg(at(s + lane, j), lane == 0 ? beta : 0.f);
+      } else {
+        // E <- H_k E: s_l = sum_i v_i E(i, l)
+#pragma unroll
+        for (int l = 0; l < B; ++l) Et[lane * LDT + l] = er[l];
+        __syncwarp();
+        float sl = 0.f;
+#pragma unroll
+        for (int i = 0; i < B; ++i) sl = fmaf(vs[i], Et[i * LDT + lane], sl);
+        ws[lane] = tau * sl;
+        __syncwarp();
+#pragma unroll
+        for (int l = 0; l < B; ++l) er[l] = fmaf(-v, ws[l], er[l]);
+        er[0] = lane == 0 ? beta : 0.f;
+        if (lane < nk) {
+#pragma unroll
+          for (int l = 0; l < B; ++l) sbr_stcg(at(s + lane, s - B + l), er[l]);
+        }
+        __syncwarp();
+      }
+      if (tau != 0.f) {
+        // D = A[R_k, R_k] <- H D H:  p = tau D v, w = p - tau/2 (p.v) v, D -= v w^T + w v^T
+#pragma unroll 4
+        for (int l = 0; l < B; ++l) {
+          if (l <= lane && lane < nk) {
+            const float dv = sbr_ldcg(at(s + lane, s + l));
+            Dt[lane * LDT + l] = dv;
+            Dt[l * LDT + lane] = dv;
+          }
+        }
+        __syncwarp();
+        float pi = 0.f;
+        if (lane < nk)
+          for (int l = 0; l < nk; ++l) pi = fmaf(Dt[lane * LDT + l], vs[l], pi);
+        pi *= tau;
+        const float dot = warp_sum(pi * v);
+        const float wi = fmaf(-0.5f * tau * dot, v, pi);
+        ws[lane] = wi;
+        __syncwarp();
+        if (lane < nk)
+          for (int l = 0; l <= lane; ++l)
+            sbr_stcg(at(s + lane, s + l), Dt[lane * LDT + l] - v * ws[l] - wi * vs[l]);
+      }
+      p.Vq[((long)j * KT + k) * B + lane] = v;
+      if (lane == 0) p.tq[(long)j * KT + k] = tau;
+      us[lane] = v;
+      tau_u = tau;
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) prog[warp] = (j << 8) + (k + 1);
+    }
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) prog[warp] = (j << 8) + 255;
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += NW * 32) {
+    p.d[i] = sbr_ldcg(AB + (long)i * LDB);
+    if (i < m - 1) p.e[i] = sbr_ldcg(AB + (long)i * LDB + 1);
+  }
+}
+
+// ---------------------------------------------------------------------- Q2 back-transform
+// grid (nprob, ceil(r / (SBR_Q2_WARPS*32))), block SBR_Q2_WARPS*32, thread = eigenvector
+// column c.  Reads the inverse-iteration output Y (fp64, Y[i*r + c]) and leaves Q2 Y in
+// Zr (fp32, row-major m x r), which backtr_prep_kernel turns into the column-major V.
+__global__ void __launch_bounds__(SBR_Q2_WARPS * 32, 1)
+sbr_q2_kernel(const __grid_constant__ EigBatch b) {
+  const EigProb& p = b.p[blockIdx.x];
+  if (p.sbr == 0) return;
+  const int m = p.m, r = p.r;
+  constexpr int B = SBR_B, G = SBR_G, NT = SBR_Q2_WARPS * 32, WIN = B + G - 1;
+  const int KT = sbr_tasks(m);
+  const int c = blockIdx.y * NT + threadIdx.x;
+  if (blockIdx.y * NT >= r) return;
+  const bool cok = c < r;
+  __shared__ __align__(16) float vsm[G * B];
+  __shared__ float tsm[G];
+  float* Z = p.Zr;
+  if (cok)
+    for (int i = 0; i < m; ++i) Z[(long)i * r + c] = (float)p.Y[(long)i * r + c];
+  const int nsw = m - 2;
+  const int ngroups = (nsw + G - 1) / G;
+  for (int g = ngroups - 1; g >= 0; --g) {
+    const int j0 = g * G, jn = min(G, nsw - j0);
+    for (int k = 0;; ++k) {
+      const int rbase = j0 + 1 + k * B;
+      if (rbase >= m) break;
+      __syncthreads();
+      for (int e = threadIdx.x; e < G * B; e += NT) {
+        const int a = e / B, i = e % B;
+        const bool ex = a < jn && j0 + a + 1 + k * B < m;
+        vsm[e] = ex ? p.Vq[((long)(j0 + a) * KT + k) * B + i] : 0.f;
+      }
+      for (int a = threadIdx.x; a < G; a += NT) {
+        const bool ex = a < jn && j0 + a + 1 + k * B < m;
+        tsm[a] = ex ? p.tq[(long)(j0 + a) * KT + k] : 0.f;
+      }
+      __syncthreads();
+      // window rows rbase .. rbase + WIN - 1 (a running pointer: no per-row address kept live)
+      const int nrow = cok ? min(WIN, m - rbase) : 0;
+      float w[WIN];
+      {
+        // laundered base and stride: the compiler cannot precompute (and keep live across the
+        // whole diamond) the 63 row addresses of the load and store loops
+        const float* zp;
+        int rl;
+        asm volatile("mov.b64 %0, %1;" : "=l"(zp) : "l"(Z + (long)rbase * r + c));
+        asm volatile("mov.b32 %0, %1;" : "=r"(rl) : "r"(r));
+#pragma unroll
+        for (int t = 0; t < WIN; ++t) {
+          w[t] = t < nrow ? *zp : 0.f;
+          zp += rl;
+        }
+      }
+      // the diamond's block reflector H_{j0} H_{j0+1} ... H_{j0+G-1}: applied last first
+#pragma unroll
+      for (int a = G - 1; a >= 0; --a) {
+        // the memory clobber keeps the compiler from hoisting every reflector's loads
+        // (1024 values) ahead of the chain: one reflector's 32 values live at a time
+        asm volatile("" ::: "memory");
+        float v[B];
+#pragma unroll
+        for (int i = 0; i < B; i += 4) {
+          const float4 q = *reinterpret_cast<const float4*>(&vsm[a * B + i]);
+          v[i] = q.x; v[i + 1] = q.y; v[i + 2] = q.z; v[i + 3] = q.w;
+        }
+        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;   // four chains: 8 dependent FMAs each
+#pragma unroll
+        for (int i = 0; i < B; i += 4) {
+          d0 = fmaf(v[i], w[a + i], d0);
+          d1 = fmaf(v[i + 1], w[a + i + 1], d1);
+          d2 = fmaf(v[i + 2], w[a + i + 2], d2);
+          d3 = fmaf(v[i + 3], w[a + i + 3], d3);
+        }
+        const float d = ((d0 + d1) + (d2 + d3)) * tsm[a];
+#pragma unroll
+        for (int i = 0; i < B; ++i) w[a + i] = fmaf(-d, v[i], w[a + i]);
+      }
+      {
+        float* zp;
+        int rl;
+        asm volatile("mov.b64 %0, %1;" : "=l"(zp) : "l"(Z + (long)rbase * r + c));
+        asm volatile("mov.b32 %0, %1;" : "=r"(rl) : "r"(r));
+#pragma unroll
+        for (int t = 0; t < WIN; ++t) {
+          if (t < nrow) *zp = w[t];
+          zp += rl;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace bkfac

@@ -802,15 +802,19 @@ def test_cfg5_block_stack_bench_launch_config_sampled(cuda_lib):
         assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC, li
 
 
-def test_global_tile_single_cta_paths(cuda_lib, monkeypatch):
-    """The one-CTA-per-factor global-tile tridiagonalisation (MODE 1) and Cholesky, which
-    the library picks when many large factors fill the GPU (configs[4]: 96 factors), forced
-    here on one factor with BKFAC_GT_CLUSTER=1: core m = 1000 (ragged tail), c = 300."""
-    monkeypatch.setenv("BKFAC_GT_CLUSTER", "1")
+@pytest.mark.parametrize("cluster", [1, 3, 6, 8])
+def test_global_tile_one_stage_paths(cuda_lib, cluster):
+    """The one-stage global-tile tridiagonalisation (MODE 1 at one CTA per factor, MODE 2 at
+    cluster sizes 3 / 6 / 8 -- what 2-, 4- and 8-GPU ranks of configs[4] pick) and the
+    global-tile Cholesky at the same cluster sizes, forced on one factor through the context
+    options (two-stage off): core m = 1000 (ragged tail), c = 300."""
+    from paper_2210_08494_b200 import binding
     n, c, r = 1300, 300, 700
     f = synth.random_case(n, c, r, seed=4242, k=min(n, 2 * c), decay=0.9)
     M0, M1 = f.batch(0).astype(np.float64), f.batch(1).astype(np.float64)
     ctx = _ctx([(n, r, c, 0)])
+    ctx.bkfac_set_option(binding.BKFAC_OPT_TWO_STAGE, 1)
+    ctx.bkfac_set_option(binding.BKFAC_OPT_GT_CLUSTER, cluster)
     U0 = synth.phantom_basis(n, r)
     Ug, Dg = gpu_brand(ctx, 0, U0, np.zeros(r), M0, 0.0, 1.0)
     Uo, Do = O.brand_update(U0, np.zeros(r), M0, 0.0, 1.0, r)
@@ -822,4 +826,63 @@ def test_global_tile_single_cta_paths(cuda_lib, monkeypatch):
     assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
     assert eig_rel_err(Do, Dg) < TOL_EIG
     assert _orth_check(Ug)
+    assert ctx.bkfac_check()[0] == 0
+
+
+TWO_STAGE_SHAPES = [  # (n, c, r): cores m = r + c from 40 to 1536, ragged and whole bands
+    (200, 8, 32), (300, 32, 64), (700, 64, 100), (1000, 96, 150), (577, 256, 220),
+    (2000, 250, 350), (1300, 300, 700), (1700, 1024, 512)]
+
+
+@pytest.mark.parametrize("shape", TWO_STAGE_SHAPES)
+def test_two_stage_eigensolver_brand(cuda_lib, shape):
+    """The two-stage reduction (dense -> band 32 by panel QR + tcgen05 two-sided updates,
+    band -> tridiagonal by bulge chasing, back-transform through both reflector sets; sbr.cuh)
+    forced for every core order: init + one Brand step against the oracle (reconstruction
+    and eigenvalues at 1e-4, orthonormal basis)."""
+    from paper_2210_08494_b200 import binding
+    n, c, r = shape
+    f = synth.random_case(n, c, r, seed=7000 + n + c + r, k=min(n, 2 * c), decay=0.9)
+    M0, M1 = f.batch(0).astype(np.float64), f.batch(1).astype(np.float64)
+    ctx = _ctx([(n, r, c, 0)])
+    ctx.bkfac_set_option(binding.BKFAC_OPT_TWO_STAGE, 2)
+    U0 = synth.phantom_basis(n, r)
+    Ug, Dg = gpu_brand(ctx, 0, U0, np.zeros(r), M0, 0.0, 1.0)
+    Uo, Do = O.brand_update(U0, np.zeros(r), M0, 0.0, 1.0, r)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    assert eig_rel_err(Do, Dg) < TOL_EIG
+    U32 = Uo.astype(np.float32).astype(np.float64)
+    D32 = Do.astype(np.float32).astype(np.float64)
+    Ug, Dg = gpu_brand(ctx, 0, U32, D32, M1, 0.95, 0.05)
+    Uo, Do = O.brand_update(U32, D32, M1, 0.95, 0.05, r)
+    e, ee = lowrank_rel_err(Uo, Do, Ug, Dg), eig_rel_err(Do, Dg)
+    assert e < TOL_STEP, f"{shape}: reconstruction {e:.2e}"
+    assert ee < TOL_EIG, f"{shape}: eigenvalues {ee:.2e}"
+    assert np.all(np.diff(Dg) <= 0) and np.all(Dg >= 0)
+    assert _orth_check(Ug), f"max |U^T U - I| = {_orth_dev(Ug):.2e}"
+    assert ctx.bkfac_check()[0] == 0
+
+
+def test_two_stage_batch_mixed_orders(cuda_lib):
+    """A batch of factors with different core orders (one-stage cluster, two-stage) in one
+    call: every factor against the oracle."""
+    from paper_2210_08494_b200 import binding
+    shapes = [(700, 64, 100), (1300, 300, 700), (577, 256, 220), (2000, 250, 350)]
+    ctx = _ctx([(n, r, c, 0) for (n, c, r) in shapes])
+    ctx.bkfac_set_option(binding.BKFAC_OPT_TWO_STAGE, 0)
+    import torch
+    items, refs = [], []
+    for i, (n, c, r) in enumerate(shapes):
+        f = synth.random_case(n, c, r, seed=900 + i, k=min(n, 2 * c), decay=0.9)
+        M = f.batch(0).astype(np.float64)
+        tU, tD, tM = to_dev_cols(synth.phantom_basis(n, r)), torch.zeros(r, device="cuda"), to_dev_cols(M)
+        Uo_, Do_ = torch.empty_like(tU), torch.empty_like(tD)
+        items.append(dict(factor=i, U_in=tU, D_in=tD, M=tM, U_out=Uo_, D_out=Do_, alpha=0.0, beta=1.0))
+        refs.append(O.brand_update(synth.phantom_basis(n, r), np.zeros(r), M, 0.0, 1.0, r))
+    ctx.bkfac_brand_update(items)
+    torch.cuda.synchronize()
+    for it, (Uo, Do) in zip(items, refs):
+        Ug, Dg = from_dev_cols(it["U_out"]), it["D_out"].double().cpu().numpy()
+        assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+        assert eig_rel_err(Do, Dg) < TOL_EIG
     assert ctx.bkfac_check()[0] == 0
