@@ -109,7 +109,10 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
  *                         3 one CTA per tile, 4 as 3 with the join right after the reduction
  *   BKFAC_OPT_EA_CAP      > 0: the EA grid cap in CTAs instead of the idle-SM count
  *   BKFAC_OPT_SYT_CLUSTER > 0: wider clusters for the shared-memory tridiagonalisation (tuning)
- *   BKFAC_OPT_BT_SIMT     != 0: back-transform Gram/T products on the fp32 SIMT GEMM */
+ *   BKFAC_OPT_BT_SIMT     != 0: back-transform Gram/T products on the fp32 SIMT GEMM
+ *   BKFAC_OPT_CHOL_BLOCKED Cholesky of orders > 256: 1 (default) blocked with the panel solve,
+ *                         trailing SYRK and inverse on the tcgen05 GEMM, 0 one tiled CTA or
+ *                         cluster per factor on CUDA cores */
 #define BKFAC_OPT_TWO_STAGE 1
 #define BKFAC_OPT_GT_CLUSTER 2
 #define BKFAC_OPT_GEMM_PAIR 3
@@ -118,6 +121,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
 #define BKFAC_OPT_EA_CAP 6
 #define BKFAC_OPT_SYT_CLUSTER 7
 #define BKFAC_OPT_BT_SIMT 8
+#define BKFAC_OPT_CHOL_BLOCKED 9
 bkfac_status bkfac_set_option(bkfac_ctx ctx, int option, int value);
 
 size_t bkfac_workspace_bytes(bkfac_ctx ctx);

@@ -144,6 +144,8 @@ struct bkfac_ctx_s {
   int ea_mode = 0;      // EA accumulate: 0 beside the eigensolver (capped grid), 1 serial
                         // first, 2 beside uncapped, 3/4 one CTA per tile (4: early join)
   int ea_cap = 0;       // > 0: EA grid cap (CTAs) instead of the idle-SM count
+  int chol_blocked = 1; // Cholesky of orders > 256 blocked on the tcgen05 GEMM (0: one tiled
+                        // CTA / cluster per factor, chol_tiled_kernel)
   // optional per-stage CUDA-event profiling (bkfac_profile_enable)
   bool prof = false;
   struct Rec { std::string tag; cudaEvent_t a, b; double flops, bytes; uint64_t launches; };
@@ -423,9 +425,136 @@ bkfac_status run_ew(bkfac_ctx ctx, std::vector<EwProb>& v, cudaStream_t st, cons
   return BKFAC_OK;
 }
 
+bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char* tag);
+bkfac_status run_ew(bkfac_ctx ctx, std::vector<EwProb>& v, cudaStream_t st, const char* tag);
+
+// Blocked Cholesky + triangular inverse for orders c > 256 (chol_tiled.cuh,
+// chol_blocked_prep_kernel): 256 x 256 diagonal blocks on chol_smem_kernel (L_kk and
+// L_kk^{-1}), the panel L21 = A21 L11^{-T} and the trailing SYRK A22 -= L21 L21^T on the
+// tcgen05 GEMM; then X = L^{-1} by block rows, X(i, 0:i) = -X_ii (L(i, 0:i) X(0:i, 0:i)),
+// two GEMMs per block row.  Scratch per problem: the tolerance reference (first float) and a
+// c x 256 panel (from float 64 on).
+bkfac_status run_chol_blocked(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) {
+  constexpr int BS = 32 * CS_MAXNB;
+  const int n = (int)v.size();
+  static thread_local CholTiledBatch pb;   // host staging (the kernels copy their parameters)
+  bkfac_status rs;
+  for (int i0 = 0; i0 < n; i0 += CT_MAXP) {
+    pb.nprob = std::min(n - i0, CT_MAXP);
+    for (int i = 0; i < pb.nprob; ++i) {
+      const CholProb& q = v[i0 + i];
+      pb.p[i] = CholTiledProb{q.G, q.ldg, q.L, q.Linv, q.scratch, q.status, q.c, q.shift, 0, q.scratch};
+    }
+    prof_begin(ctx, "chol_diag", st, 0.0, 0.0);
+    chol_blocked_prep_kernel<<<dim3((unsigned)pb.nprob, 32), 256, 0, st>>>(pb);
+    LAUNCH_CHECK(ctx);
+    prof_end(ctx, st);
+  }
+  int nbmax = 0;
+  for (auto& q : v) nbmax = std::max(nbmax, ceil_div(q.c, BS));
+  GemmStage gs;
+  std::vector<EwProb> ew;
+  for (int kb = 0; kb < nbmax; ++kb) {
+    int nd = 0;
+    for (int i = 0; i < n; ++i) {
+      const CholProb& q = v[i];
+      const int o = kb * BS;
+      if (o >= q.c) continue;
+      const int w = std::min(BS, q.c - o);
+      float* Lk = q.L + o + (long)o * q.c;
+      pb.p[nd++] = CholTiledProb{Lk, q.c, Lk, q.Linv + o + (long)o * q.c, nullptr, q.status, w, 0.f, q.c, q.scratch};
+      if (nd == CT_MAXP) {
+        pb.nprob = nd;
+        prof_begin(ctx, "chol_diag", st, 2.0 / 3.0 * BS * BS * (double)BS * nd, 0.0);
+        chol_smem_kernel<<<(unsigned)nd, CT_THREADS, chol_smem_bytes(BS), st>>>(pb);
+        LAUNCH_CHECK(ctx);
+        prof_end(ctx, st);
+        nd = 0;
+      }
+    }
+    if (nd) {
+      pb.nprob = nd;
+      prof_begin(ctx, "chol_diag", st, 2.0 / 3.0 * BS * BS * (double)BS * nd, 0.0);
+      chol_smem_kernel<<<(unsigned)nd, CT_THREADS, chol_smem_bytes(BS), st>>>(pb);
+      LAUNCH_CHECK(ctx);
+      prof_end(ctx, st);
+    }
+    bool more = false;
+    for (auto& q : v) {
+      const int o = kb * BS, w = std::min(BS, q.c - o), o2 = o + w, rem = q.c - o2;
+      if (o >= q.c || rem <= 0) continue;
+      more = true;
+      float* T21 = q.scratch + 64;
+      // T21 = A21 L11^{-T}
+      gs.add(false, true, gp(q.L + o2 + (long)o * q.c, q.c, q.Linv + o + (long)o * q.c, q.c, T21, q.c,
+                             rem, w, w, 1.f), 0);
+    }
+    if (!more) continue;
+    if ((rs = run_gemms(ctx, gs, st, "chol_panel")) != BKFAC_OK) return rs;
+    for (auto& q : v) {
+      const int o = kb * BS, w = std::min(BS, q.c - o), o2 = o + w, rem = q.c - o2;
+      if (o >= q.c || rem <= 0) continue;
+      float* T21 = q.scratch + 64;
+      EwProb e{};
+      e.Y = q.L + o2 + (long)o * q.c; e.ldy = q.c; e.X = T21; e.ldx = q.c; e.rows = rem; e.cols = w;
+      e.op = EW_COPY;
+      ew.push_back(e);
+      float* A22 = q.L + o2 + (long)o2 * q.c;
+      GemmProb pu = gp(T21, q.c, T21, q.c, A22, q.c, rem, rem, w, -1.f, A22, q.c, 1.f);
+      pu.sym = 2;   // lower tiles only: the upper triangle of L stays zero
+      gs.add(false, true, pu, 0);
+    }
+    if ((rs = run_ew(ctx, ew, st, "chol_copy")) != BKFAC_OK) return rs;
+    if ((rs = run_gemms(ctx, gs, st, "chol_syrk")) != BKFAC_OK) return rs;
+  }
+  if (!ctx->use_tc) {   // the SIMT GEMM computes whole squares: clear what the SYRK left above
+    for (auto& q : v) {
+      EwProb e{};
+      e.Y = q.L; e.ldy = q.c; e.rows = q.c; e.cols = q.c; e.op = EW_ZERO_UPPER;
+      ew.push_back(e);
+    }
+    if ((rs = run_ew(ctx, ew, st, "chol_copy")) != BKFAC_OK) return rs;
+  }
+  // X = L^{-1}: block row i (offset oi, width wi): T = L(i, 0:i) X(0:i, 0:i); X(i, 0:i) = -X_ii T
+  for (int i = 1; i < nbmax; ++i) {
+    bool any = false;
+    for (auto& q : v) {
+      const int oi = i * BS;
+      if (oi >= q.c) continue;
+      any = true;
+      const int wi = std::min(BS, q.c - oi);
+      gs.add(false, false, gp(q.L + oi, q.c, q.Linv, q.c, q.scratch + 64, wi, wi, oi, oi, 1.f), 0);
+    }
+    if (!any) break;
+    if ((rs = run_gemms(ctx, gs, st, "chol_inv_t")) != BKFAC_OK) return rs;
+    for (auto& q : v) {
+      const int oi = i * BS;
+      if (oi >= q.c) continue;
+      const int wi = std::min(BS, q.c - oi);
+      gs.add(false, false, gp(q.Linv + oi + (long)oi * q.c, q.c, q.scratch + 64, wi, q.Linv + oi, q.c,
+                              wi, oi, wi, -1.f), 0);
+    }
+    if ((rs = run_gemms(ctx, gs, st, "chol_inv_x")) != BKFAC_OK) return rs;
+  }
+  return BKFAC_OK;
+}
+
 bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) {
   double flops = 0.0, bytes = 0.0;
   for (auto& p : v) { flops += 2.0 * p.c * (double)p.c * p.c / 3.0; bytes += 12.0 * p.c * (double)p.c; }
+  // orders above the shared-memory kernel's 256: blocked on the tensor-core GEMM
+  if (ctx->chol_blocked) {
+    std::vector<CholProb> big, small;
+    for (auto& p : v) (p.c > 32 * CS_MAXNB ? big : small).push_back(p);
+    if (!big.empty()) {
+      const bkfac_status rb = run_chol_blocked(ctx, big, st);
+      if (rb != BKFAC_OK) return rb;
+      v.swap(small);
+      if (v.empty()) return BKFAC_OK;
+      flops = bytes = 0.0;
+      for (auto& p : v) { flops += 2.0 * p.c * (double)p.c * p.c / 3.0; bytes += 12.0 * p.c * (double)p.c; }
+    }
+  }
   prof_begin(ctx, "chol_inv", st, flops, bytes);
   static CholTiledBatch b;
   size_t i0 = 0;
@@ -434,7 +563,7 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
     b.nprob = (int)n;
     for (size_t i = 0; i < n; ++i) {
       const CholProb& q = v[i0 + i];
-      b.p[i] = CholTiledProb{q.G, q.ldg, q.L, q.Linv, q.scratch, q.status, q.c, q.shift};
+      b.p[i] = CholTiledProb{q.G, q.ldg, q.L, q.Linv, q.scratch, q.status, q.c, q.shift, 0, nullptr};
     }
     int cmax = 0;
     for (size_t i = 0; i < n; ++i) cmax = std::max(cmax, b.p[i].c);
@@ -683,7 +812,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         for (size_t i = 0; i < n; ++i)
           if (b.p[i].sbr) q2f += 2.0 * (double)b.p[i].m * b.p[i].m * b.p[i].r;
         prof_begin(ctx, "eig_sbr_q2", st, q2f, 0.0);
-        sbr_q2_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, SBR_Q2_WARPS * 32)), SBR_Q2_WARPS * 32, 0, st>>>(b);
+        sbr_q2_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, SBR_Q2_THREADS)), SBR_Q2_THREADS, 0, st>>>(b);
         LAUNCH_CHECK(ctx);
         prof_end(ctx, st);
       }
@@ -974,6 +1103,7 @@ bkfac_status bkfac_set_option(bkfac_ctx c, int option, int value) {
     case BKFAC_OPT_EA_CAP: if (value < 0) return BKFAC_ERR_INVALID_ARG; c->ea_cap = value; break;
     case BKFAC_OPT_SYT_CLUSTER: if (value < 0 || value > 8) return BKFAC_ERR_INVALID_ARG; c->syt_cluster = value; break;
     case BKFAC_OPT_BT_SIMT: c->bt_simt = value != 0; break;
+    case BKFAC_OPT_CHOL_BLOCKED: c->chol_blocked = value != 0; break;
     default: return BKFAC_ERR_INVALID_ARG;
   }
   return BKFAC_OK;

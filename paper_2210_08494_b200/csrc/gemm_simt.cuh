@@ -19,7 +19,8 @@ struct GemmProb {
   float alpha, beta;
   const float* beta_dev;   // if non-null, beta = *beta_dev (device scalar)
   int splits, kchunk, tiles_m, tiles_n, tile_start;
-  int sym;                 // tcgen05 path: C = C^T known (e.g. M M^T): lower tiles only, mirrored
+  int sym;                 // tcgen05 path: 1: C = C^T known (e.g. M M^T): lower tiles only, mirrored;
+                           // 2: lower tiles only, the upper triangle beyond them left untouched
   int vec;                 // tcgen05 path: bit 0 A (and A2), bit 1 B (and B2) 16-byte aligned
   int* status;             // if set: ST_NONFINITE is OR-ed in when C0 (beta != 0) holds
                            // inf/NaN -- the tensor core does not propagate NaN reliably, so

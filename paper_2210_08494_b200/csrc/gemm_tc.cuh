@@ -369,7 +369,7 @@ BKFAC_DEV void tc_store_group(const GemmProb& p, const TcTile& x, int g, float (
     if (rowok && j0 + jj + 1 < p.N) p.C[i + (long)(j0 + jj + 1) * p.ldc] = o.y;
     v[jj] = o.x; v[jj + 1] = o.y;
   }
-  if (p.sym && x.m0 != x.n0) {
+  if (p.sym == 1 && x.m0 != x.n0) {
     // mirror tile C(j, i) = C(i, j): transposed through a warp-private staging buffer so
     // that each store instruction writes two 64-byte column runs instead of 32 scattered words
 #pragma unroll

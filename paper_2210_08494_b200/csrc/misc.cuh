@@ -19,6 +19,7 @@ enum : int {
   EW_ADD_DIAG = 2,   // Y(i,i) += a * vec[i], i < rows
   EW_COPY = 3,       // Y = X
   EW_SCALE_ROWSCOLS = 4, // Y(i,j) = X(i,j) * a * vec[i]... (unused)
+  EW_ZERO_UPPER = 5, // Y(i,j) = 0 for i < j (X unused)
 };
 constexpr int EW_MAXP = 100;
 struct EwBatch { int nprob; EwProb p[EW_MAXP]; };
@@ -31,6 +32,11 @@ __global__ void ew_kernel(const __grid_constant__ EwBatch b) {
     return;
   }
   // columns over blocks, rows over threads (coalesced, no index division)
+  if (p.op == EW_ZERO_UPPER) {
+    for (int j = blockIdx.x; j < p.cols; j += gridDim.x)
+      for (int i = threadIdx.x; i < min(j, p.rows); i += blockDim.x) p.Y[i + (long)j * p.ldy] = 0.f;
+    return;
+  }
   for (int j = blockIdx.x; j < p.cols; j += gridDim.x) {
     float* yc = p.Y + (long)j * p.ldy;
     const float* xc = p.X + (long)j * p.ldx;

@@ -46,7 +46,6 @@ constexpr int SBR_LDB = 2 * SBR_B;        // band storage: diagonals 0 .. 2b-1 (
 constexpr int SBR_PANEL_THREADS = 512;
 constexpr int SBR_W_WARPS = 8;
 constexpr int SBR_CHASE_WARPS = 16;
-constexpr int SBR_Q2_WARPS = 8;           // 256 eigenvector columns per CTA
 constexpr int SBR_G = 32;                 // sweeps per diamond
 constexpr int SBR_MAX_L = 1664;           // panel rows held in shared memory (m <= 1696)
 
@@ -285,81 +284,94 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
       const int s = j + 1 + k * B;
       if (s >= m) break;
       const int nk = min(B, m - s);
+      const bool row = lane < nk;              // lane = row s + lane of the task's blocks
       if (j > 0) {
         const int need = ((j - 1) << 8) + (k + 2);
-        while (prog[(j - 1) % NW] < need) __nanosleep(32);
+        while (prog[(j - 1) % NW] < need) __nanosleep(20);
       }
       __syncwarp();
+      // every load of the task in flight at once: the E row (k >= 1; k = 0: column j) and the
+      // lower D row (D(lane, l), l <= lane) -- one L2 round trip
+      float er[B], dr[B];
+#pragma unroll
+      for (int l = 0; l < B; ++l) {
+        // k >= 1: E(lane, l) = A(s + lane, s - B + l) at AB[(s - B + l) LDB + (B + lane - l)];
+        // k = 0: er[0] = A(s + lane, j), the column the sweep annihilates
+        if (k == 0) er[l] = (row && l == 0) ? sbr_ldcg(at(s + lane, j)) : 0.f;
+        else er[l] = row ? sbr_ldcg(AB + (long)(s - B + l) * LDB + (B + lane - l)) : 0.f;
+        dr[l] = (row && l <= lane) ? sbr_ldcg(AB + (long)(s + l) * LDB + (lane - l)) : 0.f;
+      }
       float x;
-      float er[B];
       if (k == 0) {
-        x = lane < nk ? sbr_ldcg(at(s + lane, j)) : 0.f;
+        x = er[0];
       } else {
-#pragma unroll
-        for (int l = 0; l < B; ++l) er[l] = lane < nk ? sbr_ldcg(at(s + lane, s - B + l)) : 0.f;
         // E <- E H_{k-1}
-        float t = 0.f;
+        float t0 = 0.f, t1 = 0.f;
 #pragma unroll
-        for (int l = 0; l < B; ++l) t = fmaf(er[l], us[l], t);
-        t *= tau_u;
+        for (int l = 0; l < B; l += 2) { t0 = fmaf(er[l], us[l], t0); t1 = fmaf(er[l + 1], us[l + 1], t1); }
+        const float t = (t0 + t1) * tau_u;
 #pragma unroll
         for (int l = 0; l < B; ++l) er[l] = fmaf(-t, us[l], er[l]);
         x = er[0];
       }
       // reflector from x (length nk): annihilates x[1:nk]
       const float alpha = __shfl_sync(0xffffffffu, x, 0);
-      const float xn2 = warp_sum((lane >= 1 && lane < nk) ? x * x : 0.f);
+      const float xn2 = warp_sum((lane >= 1 && row) ? x * x : 0.f);
       float tau = 0.f, beta = alpha, v = lane == 0 ? 1.f : 0.f;
       if (nk > 1 && xn2 > 0.f) {
         beta = -copysignf(sqrtf(fmaf(alpha, alpha, xn2)), alpha);
         tau = (beta - alpha) / beta;
-        v = lane == 0 ? 1.f : (lane < nk ? x / (alpha - beta) : 0.f);
+        v = lane == 0 ? 1.f : (row ? x / (alpha - beta) : 0.f);
       }
       vs[lane] = v;
-      __syncwarp();
       if (k == 0) {
-        if (lane < nk) sbr_stcg(at(s + lane, j), lane == 0 ? beta : 0.f);
+        if (row) sbr_stcg(at(s + lane, j), lane == 0 ? beta : 0.f);
       } else {
-        // E <- H_k E: s_l = sum_i v_i E(i, l)
+        // E <- H_k E: s_l = sum_i v_i E(i, l) through a shared-memory transpose
 #pragma unroll
         for (int l = 0; l < B; ++l) Et[lane * LDT + l] = er[l];
         __syncwarp();
-        float sl = 0.f;
+        float sl0 = 0.f, sl1 = 0.f;
 #pragma unroll
-        for (int i = 0; i < B; ++i) sl = fmaf(vs[i], Et[i * LDT + lane], sl);
-        ws[lane] = tau * sl;
-        __syncwarp();
-#pragma unroll
-        for (int l = 0; l < B; ++l) er[l] = fmaf(-v, ws[l], er[l]);
-        er[0] = lane == 0 ? beta : 0.f;
-        if (lane < nk) {
-#pragma unroll
-          for (int l = 0; l < B; ++l) sbr_stcg(at(s + lane, s - B + l), er[l]);
+        for (int i = 0; i < B; i += 2) {
+          sl0 = fmaf(vs[i], Et[i * LDT + lane], sl0);
+          sl1 = fmaf(vs[i + 1], Et[(i + 1) * LDT + lane], sl1);
         }
+        ws[lane] = tau * (sl0 + sl1);
         __syncwarp();
+#pragma unroll
+        for (int l = 1; l < B; ++l) er[l] = fmaf(-v, ws[l], er[l]);
+        er[0] = lane == 0 ? beta : 0.f;
+        if (row) {
+#pragma unroll
+          for (int l = 0; l < B; ++l) sbr_stcg(AB + (long)(s - B + l) * LDB + (B + lane - l), er[l]);
+        }
       }
+      __syncwarp();
       if (tau != 0.f) {
         // D = A[R_k, R_k] <- H D H:  p = tau D v, w = p - tau/2 (p.v) v, D -= v w^T + w v^T
-#pragma unroll 4
+#pragma unroll
         for (int l = 0; l < B; ++l) {
-          if (l <= lane && lane < nk) {
-            const float dv = sbr_ldcg(at(s + lane, s + l));
-            Dt[lane * LDT + l] = dv;
-            Dt[l * LDT + lane] = dv;
-          }
+          Dt[lane * LDT + l] = dr[l];                 // lower (zeros above)
+          if (l < lane) Dt[l * LDT + lane] = dr[l];   // mirrored
         }
         __syncwarp();
-        float pi = 0.f;
-        if (lane < nk)
-          for (int l = 0; l < nk; ++l) pi = fmaf(Dt[lane * LDT + l], vs[l], pi);
-        pi *= tau;
+        float p0 = 0.f, p1 = 0.f;
+#pragma unroll
+        for (int l = 0; l < B; l += 2) {
+          p0 = fmaf(Dt[lane * LDT + l], vs[l], p0);
+          p1 = fmaf(Dt[lane * LDT + l + 1], vs[l + 1], p1);
+        }
+        const float pi = tau * (p0 + p1);
         const float dot = warp_sum(pi * v);
         const float wi = fmaf(-0.5f * tau * dot, v, pi);
         ws[lane] = wi;
         __syncwarp();
-        if (lane < nk)
-          for (int l = 0; l <= lane; ++l)
-            sbr_stcg(at(s + lane, s + l), Dt[lane * LDT + l] - v * ws[l] - wi * vs[l]);
+        if (row) {
+#pragma unroll
+          for (int l = 0; l < B; ++l)
+            if (l <= lane) sbr_stcg(AB + (long)(s + l) * LDB + (lane - l), dr[l] - v * ws[l] - wi * vs[l]);
+        }
       }
       p.Vq[((long)j * KT + k) * B + lane] = v;
       if (lane == 0) p.tq[(long)j * KT + k] = tau;
@@ -381,71 +393,76 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
 }
 
 // ---------------------------------------------------------------------- Q2 back-transform
-// grid (nprob, ceil(r / (SBR_Q2_WARPS*32))), block SBR_Q2_WARPS*32, thread = eigenvector
-// column c.  Reads the inverse-iteration output Y (fp64, Y[i*r + c]) and leaves Q2 Y in
-// Zr (fp32, row-major m x r), which backtr_prep_kernel turns into the column-major V.
-__global__ void __launch_bounds__(SBR_Q2_WARPS * 32, 1)
+// grid (nprob, ceil(r / SBR_Q2_THREADS)), block SBR_Q2_THREADS, thread = eigenvector column c
+// (its column of Z is private to it).  Reads the inverse-iteration output Y (fp64,
+// Y[i*r + c]) and leaves Q2 Y in Zr (fp32, row-major m x r), which backtr_prep_kernel turns
+// into the column-major V.  Per group of SBR_G sweeps the 63-row diamond window slides down
+// the column in steps of 32 rows: rows leaving the window are stored, the next 32 rows are
+// loaded before the current diamond is applied (they are not touched by it), so each group
+// streams the column through registers once.
+constexpr int SBR_Q2_THREADS = 128;
+__global__ void __launch_bounds__(SBR_Q2_THREADS, 3)
 sbr_q2_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   if (p.sbr == 0) return;
   const int m = p.m, r = p.r;
-  constexpr int B = SBR_B, G = SBR_G, NT = SBR_Q2_WARPS * 32, WIN = B + G - 1;
+  constexpr int B = SBR_B, G = SBR_G, NT = SBR_Q2_THREADS, WIN = B + G - 1;
+  static_assert(G == B, "the window slides by one task (B rows) and holds G - 1 = B - 1 carried rows");
   const int KT = sbr_tasks(m);
   const int c = blockIdx.y * NT + threadIdx.x;
   if (blockIdx.y * NT >= r) return;
   const bool cok = c < r;
-  __shared__ __align__(16) float vsm[G * B];
-  __shared__ float tsm[G];
-  float* Z = p.Zr;
+  __shared__ __align__(16) float vsm[2][G * B];
+  __shared__ float tsm[2][G];
+  float* Z = p.Zr + c;
   if (cok)
-    for (int i = 0; i < m; ++i) Z[(long)i * r + c] = (float)p.Y[(long)i * r + c];
+    for (int i = 0; i < m; ++i) Z[(long)i * r] = (float)p.Y[(long)i * r + c];
   const int nsw = m - 2;
   const int ngroups = (nsw + G - 1) / G;
+  // reflectors of diamond (g, k) into buffer q (every thread of the CTA takes a share)
+  auto stage = [&](int q, int j0, int jn, int k) {
+    for (int e = threadIdx.x; e < G * B; e += NT) {
+      const int a = e / B, i = e % B;
+      const bool ex = a < jn && j0 + a + 1 + k * B < m;
+      vsm[q][e] = ex ? p.Vq[((long)(j0 + a) * KT + k) * B + i] : 0.f;
+    }
+    for (int a = threadIdx.x; a < G; a += NT) {
+      const bool ex = a < jn && j0 + a + 1 + k * B < m;
+      tsm[q][a] = ex ? p.tq[(long)(j0 + a) * KT + k] : 0.f;
+    }
+  };
+  int q = 0;
   for (int g = ngroups - 1; g >= 0; --g) {
     const int j0 = g * G, jn = min(G, nsw - j0);
-    for (int k = 0;; ++k) {
-      const int rbase = j0 + 1 + k * B;
-      if (rbase >= m) break;
-      __syncthreads();
-      for (int e = threadIdx.x; e < G * B; e += NT) {
-        const int a = e / B, i = e % B;
-        const bool ex = a < jn && j0 + a + 1 + k * B < m;
-        vsm[e] = ex ? p.Vq[((long)(j0 + a) * KT + k) * B + i] : 0.f;
-      }
-      for (int a = threadIdx.x; a < G; a += NT) {
-        const bool ex = a < jn && j0 + a + 1 + k * B < m;
-        tsm[a] = ex ? p.tq[(long)(j0 + a) * KT + k] : 0.f;
-      }
-      __syncthreads();
-      // window rows rbase .. rbase + WIN - 1 (a running pointer: no per-row address kept live)
-      const int nrow = cok ? min(WIN, m - rbase) : 0;
-      float w[WIN];
-      {
-        // laundered base and stride: the compiler cannot precompute (and keep live across the
-        // whole diamond) the 63 row addresses of the load and store loops
-        const float* zp;
-        int rl;
-        asm volatile("mov.b64 %0, %1;" : "=l"(zp) : "l"(Z + (long)rbase * r + c));
-        asm volatile("mov.b32 %0, %1;" : "=r"(rl) : "r"(r));
+    __syncthreads();
+    stage(q, j0, jn, 0);
+    // window of diamond k: rows j0 + 1 + k B .. + WIN - 1; w[t] <-> row rb + t
+    int rb = j0 + 1;
+    float w[WIN];
 #pragma unroll
-        for (int t = 0; t < WIN; ++t) {
-          w[t] = t < nrow ? *zp : 0.f;
-          zp += rl;
-        }
+    for (int t = 0; t < WIN; ++t) w[t] = (cok && rb + t < m) ? Z[(long)(rb + t) * r] : 0.f;
+    for (int k = 0; rb < m; ++k, rb += B) {
+      __syncthreads();   // buffer q staged; buffer q ^ 1 free
+      if (rb + B < m) stage(q ^ 1, j0, jn, k + 1);
+      // next diamond's new rows (rb + WIN .. rb + WIN + B - 1): untouched by this diamond
+      float nx[B];
+#pragma unroll
+      for (int t = 0; t < B; ++t) {
+        const int row = rb + WIN + t;
+        nx[t] = (cok && row < m) ? Z[(long)row * r] : 0.f;
       }
       // the diamond's block reflector H_{j0} H_{j0+1} ... H_{j0+G-1}: applied last first
+      const float* vq = vsm[q];
 #pragma unroll
       for (int a = G - 1; a >= 0; --a) {
-        // the memory clobber keeps the compiler from hoisting every reflector's loads
-        // (1024 values) ahead of the chain: one reflector's 32 values live at a time
         asm volatile("" ::: "memory");
         float v[B];
 #pragma unroll
         for (int i = 0; i < B; i += 4) {
-          const float4 q = *reinterpret_cast<const float4*>(&vsm[a * B + i]);
-          v[i] = q.x; v[i + 1] = q.y; v[i + 2] = q.z; v[i + 3] = q.w;
+          const float4 f4 = *reinterpret_cast<const float4*>(&vq[a * B + i]);
+          v[i] = f4.x; v[i + 1] = f4.y; v[i + 2] = f4.z; v[i + 3] = f4.w;
         }
-        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;   // four chains: 8 dependent FMAs each
+        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
 #pragma unroll
         for (int i = 0; i < B; i += 4) {
           d0 = fmaf(v[i], w[a + i], d0);
@@ -453,21 +470,19 @@ sbr_q2_kernel(const __grid_constant__ EigBatch b) {
           d2 = fmaf(v[i + 2], w[a + i + 2], d2);
           d3 = fmaf(v[i + 3], w[a + i + 3], d3);
         }
-        const float d = ((d0 + d1) + (d2 + d3)) * tsm[a];
+        const float d = ((d0 + d1) + (d2 + d3)) * tsm[q][a];
 #pragma unroll
         for (int i = 0; i < B; ++i) w[a + i] = fmaf(-d, v[i], w[a + i]);
       }
-      {
-        float* zp;
-        int rl;
-        asm volatile("mov.b64 %0, %1;" : "=l"(zp) : "l"(Z + (long)rbase * r + c));
-        asm volatile("mov.b32 %0, %1;" : "=r"(rl) : "r"(r));
+      // rows rb .. rb + B - 1 leave the window; slide by B
 #pragma unroll
-        for (int t = 0; t < WIN; ++t) {
-          if (t < nrow) *zp = w[t];
-          zp += rl;
-        }
-      }
+      for (int t = 0; t < B; ++t)
+        if (cok && rb + t < m) Z[(long)(rb + t) * r] = w[t];
+#pragma unroll
+      for (int t = 0; t < WIN - B; ++t) w[t] = w[t + B];
+#pragma unroll
+      for (int t = 0; t < B; ++t) w[WIN - B + t] = nx[t];
+      q ^= 1;
     }
   }
 }

@@ -886,3 +886,31 @@ def test_two_stage_batch_mixed_orders(cuda_lib):
         assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
         assert eig_rel_err(Do, Dg) < TOL_EIG
     assert ctx.bkfac_check()[0] == 0
+
+
+@pytest.mark.parametrize("blocked", [1, 0])
+@pytest.mark.parametrize("shape", [(2000, 777, 100), (1500, 300, 64), (2600, 1024, 512)])
+def test_cholesky_large_orders(cuda_lib, shape, blocked):
+    """CholeskyQR2 of residuals with c > 256: the blocked Cholesky (256-blocks in shared
+    memory, panel solve / trailing SYRK / inverse blocks on the tcgen05 GEMM; default) and
+    the one-CTA tiled kernel, both against the oracle through a Brand step (ragged blocks:
+    c = 777 = 3 x 256 + 9, 300; c = 1024 as at configs[4])."""
+    from paper_2210_08494_b200 import binding
+    n, c, r = shape
+    f = synth.random_case(n, c, r, seed=8100 + c + blocked, k=min(n, 2 * c), decay=0.9)
+    M0, M1 = f.batch(0).astype(np.float64), f.batch(1).astype(np.float64)
+    ctx = _ctx([(n, r, c, 0)])
+    ctx.bkfac_set_option(binding.BKFAC_OPT_CHOL_BLOCKED, blocked)
+    U0 = synth.phantom_basis(n, r)
+    Ug, Dg = gpu_brand(ctx, 0, U0, np.zeros(r), M0, 0.0, 1.0)
+    Uo, Do = O.brand_update(U0, np.zeros(r), M0, 0.0, 1.0, r)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    U32 = Uo.astype(np.float32).astype(np.float64)
+    D32 = Do.astype(np.float32).astype(np.float64)
+    Ug, Dg = gpu_brand(ctx, 0, U32, D32, M1, 0.95, 0.05)
+    Uo, Do = O.brand_update(U32, D32, M1, 0.95, 0.05, r)
+    assert lowrank_rel_err(Uo, Do, Ug, Dg) < TOL_STEP
+    assert eig_rel_err(Do, Dg) < TOL_EIG
+    assert _orth_check(Ug)
+    code, bad, info = ctx.bkfac_check()
+    assert code == 0
