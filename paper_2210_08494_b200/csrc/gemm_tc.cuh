@@ -863,7 +863,11 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 constexpr int TC_BN = 128, TC_BN_PAIR = BKFAC_TC_BN_PAIR, TC_NLW = BKFAC_TC_NLW, TC_DEPTH = BKFAC_TC_DEPTH;
 using TcMain = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 4>;
 using TcShortK = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 8>;
-using TcPair = TcCfg<TC_BN_PAIR, TC_NLW, TC_DEPTH, 4, true>;
+#ifndef BKFAC_TC_PAIR_EPI
+#define BKFAC_TC_PAIR_EPI 4
+#endif
+constexpr int TC_PAIR_EPI = BKFAC_TC_PAIR_EPI;   // epilogue warps of the pair kernel (4 or 8)
+using TcPair = TcCfg<TC_BN_PAIR, TC_NLW, TC_DEPTH, TC_PAIR_EPI, true>;
 constexpr int TC_SHORT_K_CHUNKS = 8;   // stages with every K <= 8 chunks use 8 epilogue warps
 
 template <bool TA, bool TB, int EPI, bool PAIR>
@@ -884,10 +888,10 @@ inline bool tc_init_attributes() {
   ok &= tc_set_attr<false, true, 8, false>();
   ok &= tc_set_attr<true, false, 8, false>();
   ok &= tc_set_attr<true, true, 8, false>();
-  ok &= tc_set_attr<false, false, 4, true>();
-  ok &= tc_set_attr<false, true, 4, true>();
-  ok &= tc_set_attr<true, false, 4, true>();
-  ok &= tc_set_attr<true, true, 4, true>();
+  ok &= tc_set_attr<false, false, TC_PAIR_EPI, true>();
+  ok &= tc_set_attr<false, true, TC_PAIR_EPI, true>();
+  ok &= tc_set_attr<true, false, TC_PAIR_EPI, true>();
+  ok &= tc_set_attr<true, true, TC_PAIR_EPI, true>();
   return ok;
 }
 
@@ -907,7 +911,7 @@ inline cudaError_t tc_launch(const GemmBatch& b, int grid, cudaStream_t st, bool
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TA, TB, TC_BN_PAIR, TC_NLW, TC_DEPTH, 4, true>, b);
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TA, TB, TC_BN_PAIR, TC_NLW, TC_DEPTH, TC_PAIR_EPI, true>, b);
   }
   if (short_k)
     gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 8, false><<<grid, TcShortK::THREADS, TcShortK::SMEM_BYTES, st>>>(b);

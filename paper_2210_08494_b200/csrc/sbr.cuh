@@ -44,16 +44,17 @@ namespace bkfac {
 constexpr int SBR_B = 32;                 // band width (= warp size: lane = row of a block)
 constexpr int SBR_LDB = 2 * SBR_B;        // band storage: diagonals 0 .. 2b-1 (bulge included)
 constexpr int SBR_PANEL_THREADS = 512;
-constexpr int SBR_W_WARPS = 8;
+constexpr int SBR_W_WARPS = 16;
 constexpr int SBR_CHASE_WARPS = 16;
 constexpr int SBR_G = 32;                 // sweeps per diamond
-constexpr int SBR_MAX_L = 1664;           // panel rows held in shared memory (m <= 1696)
+constexpr int SBR_MAX_L = 1600;           // panel rows held in shared memory (m <= 1632)
 
 __host__ __device__ inline int sbr_panels(int m) { return m - 2 >= SBR_B ? (m - 2) / SBR_B : 0; }
 __host__ __device__ inline int sbr_tasks(int m) { return (m + SBR_B - 1) / SBR_B + 1; }   // KT
 inline bool sbr_supported(int m) { return m - SBR_B <= SBR_MAX_L && sbr_panels(m) > 0; }
 inline size_t sbr_panel_smem_bytes(int m) {
-  return sizeof(float) * ((size_t)(m - SBR_B) * SBR_B + 2 * SBR_B * (SBR_B + 1) + 64 + SBR_B);
+  return sizeof(float) * ((size_t)(m - SBR_B) * (SBR_B + 1) + SBR_B * (SBR_B + 1) +
+                          2 * (SBR_PANEL_THREADS / 32) * SBR_B + 3 * SBR_B);
 }
 inline size_t sbr_w_smem_bytes() {
   return sizeof(float) * (3 * SBR_B * (SBR_B + 1) + SBR_W_WARPS * 3 * SBR_B * (SBR_B + 1));
@@ -64,80 +65,128 @@ inline size_t sbr_chase_smem_bytes() {
 
 // ---------------------------------------------------------------------- stage 1: panel QR
 // grid (nprob), block SBR_PANEL_THREADS; panel j of every problem that has one.
+// The panel lives row-major in shared memory (row l at P[l * 33], conflict-free for a thread
+// walking its own row); thread t owns rows t, t + 512, ...  Column step i needs one block
+// barrier: every thread forms, over its rows below i, the 32 partial sums
+//   value[i] = sum x_l^2,  value[c] = sum x_l P(l, c) (c > i),  value[a] = sum x_l V(l, a) (a < i)
+// (x = column i), reduced across the warp by a 31-shuffle transpose-reduce (lane c ends with
+// value[c]) and across warps through shared memory (double-buffered by step parity); then
+// every thread has beta, tau, the update coefficients w_c = tau (P(i, c) + s_c / (alpha -
+// beta)) and applies the reflector to its own rows, warp 0 extends T (dlarft:
+// T(0:i, i) = -tau T(0:i, 0:i) g, g_a = V(i, a) + u_a / (alpha - beta)), and the owner of
+// row i + 1 publishes that row for the next step.
+BKFAC_DEV float sbr_transpose_reduce(float (&v)[32], int lane) {
+  // after the 5 rounds lane c holds sum over the warp of v[c]
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool upper = (lane & h) != 0;
+#pragma unroll
+    for (int q = 0; q < h; ++q) {
+      // keep half of the 2h values: lanes with bit h set keep the upper half
+      const float send = upper ? v[q] : v[q + h];
+      const float keep = upper ? v[q + h] : v[q];
+      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return v[0];
+}
+
 __global__ void __launch_bounds__(SBR_PANEL_THREADS, 1)
 sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
   const EigProb& p = b.p[blockIdx.x];
   const int m = p.m, ld = p.ldk;
   if (p.sbr == 0 || j >= sbr_panels(m)) return;
-  constexpr int B = SBR_B, NT = SBR_PANEL_THREADS, NW = NT / 32, LDT = B + 1;
+  constexpr int B = SBR_B, NT = SBR_PANEL_THREADS, NW = NT / 32, LDP = B + 1, LDT = B + 1;
   const int c0 = j * B, r0 = c0 + B, L = m - r0;
   extern __shared__ __align__(16) float ps[];
-  float* P = ps;                     // L x B, col-major (ld L)
-  float* G = P + (size_t)L * B;      // B x B, G[a*LDT + c] = (V^T V)(a, c), c >= a
-  float* T = G + B * LDT;            // B x B upper triangular, T[a*LDT + c]
-  float* red = T + B * LDT;          // 64
-  float* taus = red + 64;            // B
+  float* P = ps;                          // L x B row-major, ld 33
+  float* T = P + (size_t)L * LDP;         // B x B upper triangular, T[a*LDT + c]
+  float* red = T + B * LDT;               // [2][NW][B] partial sums by step parity
+  float* rowb = red + 2 * NW * B;         // [2][B] row i of the panel by step parity
+  float* taus = rowb + 2 * B;             // B
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* K = p.K;
   for (int e = tid; e < L * B; e += NT) {
     const int l = e % L, i = e / L;
-    P[e] = K[(r0 + l) + (long)(c0 + i) * ld];
-  }
-  __syncthreads();
-  for (int i = 0; i < B; ++i) {
-    float taui = 0.f;
-    if (i < L) {
-      float s = 0.f;
-      for (int l = i + 1 + tid; l < L; l += NT) s = fmaf(P[l + i * L], P[l + i * L], s);
-      s = block_sum(s, red);
-      const float alpha = P[i + i * L];
-      if (L - i > 1 && s > 0.f) {
-        const float beta = -copysignf(sqrtf(fmaf(alpha, alpha, s)), alpha);
-        taui = (beta - alpha) / beta;
-        const float sc = 1.f / (alpha - beta);
-        for (int l = i + 1 + tid; l < L; l += NT) P[l + i * L] *= sc;
-        __syncthreads();
-        if (tid == 0) P[i + i * L] = beta;
-        // H_i applied to the panel's later columns (one warp per column)
-        for (int c = i + 1 + warp; c < B; c += NW) {
-          float d = 0.f;
-          for (int l = i + 1 + lane; l < L; l += 32) d = fmaf(P[l + i * L], P[l + c * L], d);
-          d = warp_sum(d) + P[i + c * L];
-          const float tw = taui * d;
-          for (int l = i + 1 + lane; l < L; l += 32) P[l + c * L] = fmaf(-tw, P[l + i * L], P[l + c * L]);
-          if (lane == 0) P[i + c * L] -= tw;
-        }
-      }
-    }
-    if (tid == 0) taus[i] = taui;
-    __syncthreads();
-  }
-  // G = V^T V (upper part c >= a), V unit lower trapezoidal (V(l, a) = P[l + a L], l > a)
-  for (int e = tid; e < B * B; e += NT) {
-    const int a = e / B, c = e % B;
-    if (c < a || c >= L) continue;
-    float s = (c == a) ? 1.f : P[c + a * L];       // row l = c: V(c, c) = 1
-    for (int l = c + 1; l < L; ++l) s = fmaf(P[l + a * L], P[l + c * L], s);
-    G[a * LDT + c] = s;
+    P[l * LDP + i] = K[(r0 + l) + (long)(c0 + i) * ld];
   }
   for (int e = tid; e < B * LDT; e += NT) T[e] = 0.f;
   __syncthreads();
-  // T(0:i, i) = -tau_i T(0:i, 0:i) G(0:i, i), T(i, i) = tau_i
+  if (tid < B) rowb[tid] = P[tid];        // row 0 for step 0
+  __syncthreads();
   for (int i = 0; i < B; ++i) {
-    const float ti = taus[i];
-    if (tid < i && i < L) {
-      float s = 0.f;
-      for (int c = tid; c < i; ++c) s = fmaf(T[tid * LDT + c], G[c * LDT + i], s);
-      T[tid * LDT + i] = -ti * s;
-    } else if (tid == i) {
-      T[i * LDT + i] = ti;
+    const int par = i & 1;
+    // ---- partial sums over this thread's rows l > i
+    float v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = 0.f;
+    for (int l = tid; l < L; l += NT) {
+      if (l <= i) continue;
+      const float* pr = P + l * LDP;
+      const float x = pr[i];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = fmaf(x, c == i ? x : pr[c], v[c]);
     }
+    const float mine = sbr_transpose_reduce(v, lane);   // lane c: warp total of value[c]
+    red[(par * NW + warp) * B + lane] = mine;
     __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) tot += red[(par * NW + w) * B + lane];
+    // lane c of every warp: value[c] (c == i: ||x||^2 below row i; c > i: s_c; c < i: u_c)
+    const float xn2 = __shfl_sync(0xffffffffu, tot, i);
+    const float* ri = rowb + par * B;     // row i (published by its owner before the barrier)
+    const float alpha = ri[i];
+    float tau = 0.f, beta = alpha, sc = 0.f;
+    if (L - i > 1 && xn2 > 0.f && i < L) {
+      beta = -copysignf(sqrtf(fmaf(alpha, alpha, xn2)), alpha);
+      tau = (beta - alpha) / beta;
+      sc = 1.f / (alpha - beta);
+    }
+    // w_c = tau (P(i, c) + s_c sc) for c > i (lane c)
+    const float wc = (lane > i) ? tau * fmaf(tot, sc, ri[lane]) : 0.f;
+    // T column i (warp 0): g_a = V(i, a) + u_a sc, a < i
+    if (warp == 0) {
+      const float g = (lane < i) ? fmaf(tot, sc, ri[lane]) : 0.f;
+      float tcol = 0.f;
+      for (int e = 0; e < i; ++e) {
+        const float ge = __shfl_sync(0xffffffffu, g, e);
+        if (lane <= e) tcol = fmaf(T[lane * LDT + e], ge, tcol);
+      }
+      if (lane < i) T[lane * LDT + i] = -tau * tcol;
+      if (lane == i) { T[i * LDT + i] = tau; taus[i] = tau; }
+    }
+    // ---- apply H_i to this thread's rows (scale x into v, update the later columns)
+    float wl[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) wl[c] = __shfl_sync(0xffffffffu, wc, c);
+    for (int l = tid; l < L; l += NT) {
+      if (l < i) continue;
+      float* pr = P + l * LDP;
+      if (l == i) {
+        if (tau != 0.f) {
+          pr[i] = beta;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) if (c > i) pr[c] -= wl[c];
+        }
+      } else if (tau != 0.f) {
+        const float vx = pr[i] * sc;
+        pr[i] = vx;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) if (c > i) pr[c] = fmaf(-wl[c], vx, pr[c]);
+      }
+      // publish row i + 1 (after this step's update) for the next step
+      if (l == i + 1) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) rowb[(par ^ 1) * B + c] = pr[c];
+      }
+    }
   }
+  __syncthreads();
   // write back: K panel (R above / on the diagonal, reflector tails below), explicit V, T, tau
   for (int e = tid; e < L * B; e += NT) {
     const int l = e % L, i = e / L;
-    const float x = P[e];
+    const float x = P[l * LDP + i];
     K[(r0 + l) + (long)(c0 + i) * ld] = x;
     p.Vp[(r0 + l) + (long)i * m] = (l < i) ? 0.f : (l == i ? 1.f : x);
   }
@@ -287,7 +336,11 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
       const bool row = lane < nk;              // lane = row s + lane of the task's blocks
       if (j > 0) {
         const int need = ((j - 1) << 8) + (k + 2);
-        while (prog[(j - 1) % NW] < need) __nanosleep(20);
+        while (prog[(j - 1) % NW] < need) {
+#ifndef BKFAC_CHASE_SPIN
+          __nanosleep(20);
+#endif
+        }
       }
       __syncwarp();
       // every load of the task in flight at once: the E row (k >= 1; k = 0: column j) and the
@@ -352,8 +405,10 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
         // D = A[R_k, R_k] <- H D H:  p = tau D v, w = p - tau/2 (p.v) v, D -= v w^T + w v^T
 #pragma unroll
         for (int l = 0; l < B; ++l) {
-          Dt[lane * LDT + l] = dr[l];                 // lower (zeros above)
-          if (l < lane) Dt[l * LDT + lane] = dr[l];   // mirrored
+          if (l <= lane) {                            // lane writes row lane's lower part and
+            Dt[lane * LDT + l] = dr[l];               // its mirror; padding rows are zero
+            Dt[l * LDT + lane] = dr[l];
+          }
         }
         __syncwarp();
         float p0 = 0.f, p1 = 0.f;
