@@ -399,17 +399,28 @@ def run_ours(args, rank, world, local_rank):
                        device=local_rank, rank=rank, world=world, full_rank=args.full_rank,
                        correct_every=args.correct_every, phi_crc=args.phi_crc)
     gather = SlotGather(layers, stack.owned_layers_all, rank, device) if world > 1 and layers else None
+    if gather is not None:
+        # precondition straight into the send slots; step k's all-gather (buffer set k & 1)
+        # overlaps step k + 1's compute
+        stack.bind_outputs([gather.send_views(0), gather.send_views(1)])
     M_pool, J_pool = device_inputs(cfg, stack.my_factors, stack.my_layers, args.pool, device)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device)
+    in_bytes = sum(4 * t.numel() for t in M_pool[0].values()) + sum(4 * t.numel() for t in J_pool[0].values())
+    # inputs larger than L2 (configs[4]: 17 GB per step on one GPU, 2 GB per rank at 8): no
+    # flush needed between steps; smaller workloads flush L2 (512 MiB write) between steps
+    use_flush = in_bytes < 2 * (126 << 20)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device) if use_flush else None
     stream = torch.cuda.current_stream()
 
     use_graphs = not args.no_graphs
 
     def one_step(i, graph, profile=False):
+        b = stack.k & 1
+        if gather is not None:
+            gather.finish(b)          # step k - 2's gather on this buffer set has completed
         S = stack.step(M_pool[i % args.pool], None if args.factored else J_pool[i % args.pool],
                        graph=graph, factored=args.factored, profile=profile)
         if gather is not None:
-            gather.gather(S)
+            gather.start(b)
 
     # warm-up (>= 3 steps also captures the two CUDA graphs of a non-RSVD step: the U/D
     # ping-pong parity and the input pool alternate together).  With an RSVD schedule the
@@ -434,7 +445,10 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
         for i in range(nsteps):
-            flush.zero_()                       # L2 flush between timed steps (not timed)
+            if use_flush:
+                if gather is not None:          # no collective overlaps the (untimed) flush
+                    gather.finish(0); gather.finish(1)
+                flush.zero_()                   # L2 flush between timed steps (not timed)
             r0 = stack.ctx.bkfac_profile_count() if profile else 0
             stack.last_profile_range = None
             ev[i][0].record(stream)
@@ -450,10 +464,17 @@ def run_ours(args, rank, world, local_rank):
                                                                  launches=0, calls=0))
                     for key_ in ("ms", "flops", "bytes", "launches", "calls"):
                         acc[key_] += st_[key_]
+        # the last steps' all-gathers still in flight belong to the timed work
+        tail = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        tail[0].record(stream)
+        if gather is not None:
+            gather.finish(0); gather.finish(1)
+        tail[1].record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        return sum(a.elapsed_time(b) for a, b in ev), list(stage_acc.values())
+        return (sum(a.elapsed_time(b) for a, b in ev) + tail[0].elapsed_time(tail[1]),
+                list(stage_acc.values()))
 
     # headline: K steps (RSVD steps included at their schedule), profiling off
     sampler = ClockSampler(local_rank)
@@ -536,7 +557,10 @@ def run_ours(args, rank, world, local_rank):
                        "n_BS": cfg.factors[0].c, "rho": cfg.rho, "lambda": cfg.lam,
                        "rsvd_every": cfg.rsvd_every, "rsvd_steps_in_window": n_rsvd,
                        "parallelism": f"layer-shard x{world}",
-                       "l2": "flushed between timed steps (512 MiB write)",
+                       "l2": ("flushed between timed steps (512 MiB write)" if use_flush else
+                              f"inputs larger than L2 ({in_bytes / 2**30:.1f} GiB per step per rank), no flush"),
+                       "allgather": ("per-slot NCCL all-gather of step k overlapped with step k+1 "
+                                     "(preconditioned straight into the send slots)") if gather else None,
                        "inputs": "device-resident pool of %d synthetic batches" % args.pool},
             "roofline": roof, "stages": table, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
@@ -606,10 +630,13 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
             b = (j + par0) & 1
             stream.wait_event(ev_up[b])
             stream.wait_event(ev_down[b])         # S set b was read back (step j-2)
+            if gather is not None:
+                gather.finish(stack.k & 1)
+            sb = stack.k & 1
             S = stack.step(dev_M[b], None if args.factored else dev_J[b], graph=use_graphs,
                            factored=args.factored)
             if gather is not None:
-                gather.gather(S)
+                gather.start(sb)
             ev_done[b].record(stream)
             if j + 1 < n:
                 upload(j + 1)
@@ -619,6 +646,8 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
                     l = cfg.layers[li]
                     host_S[(l.d_G, l.d_A)].copy_(s_, non_blocking=True)
                 ev_down[b].record(down)
+        if gather is not None:
+            gather.finish(0); gather.finish(1)
         torch.cuda.synchronize()
 
     run(2)                  # untimed: captures this input set's graphs

@@ -309,76 +309,88 @@ bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char*
   return rr;
 }
 
-// Split-K planning.  SIMT: K units, 64x64 tiles.  tcgen05: 32-wide K chunks, 128 x 128
-// tiles, one persistent CTA per SM.  Splits only when a stage has fewer tiles than the
-// machine has SMs (x2 for SIMT); the reduction order is fixed (deterministic).
+// Tile-shape and split-K planning.  SIMT: K units, 64 x 64 tiles, splits while the stage
+// has fewer tiles than twice the SM count.  tcgen05 (the hot path): every decision depends on
+// the problem alone, never on the rest of the batch, so a factor's arithmetic (and its bits)
+// is the same whichever rank computes it and whatever else shares the launch:
+//   * CTA-pair 256 x 256 tiles for non-symmetric problems with long K (> 8 chunks) and
+//     M >= 512, N >= 256; 128 x 128 tiles otherwise (a stage launches each group separately);
+//   * split-K (deterministic fixed-order reduction) into work items of at most
+//     TC_SPLIT_CHUNKS chunks of 32 when the caller supplied a workspace.
+constexpr int TC_SPLIT_CHUNKS = 128;
+bool tc_pair_tiles(const bkfac_ctx ctx, const GemmProb& p) {
+  if (p.sym || ctx->pair_mode == 0) return false;
+  if (ctx->pair_mode == 2) return true;
+  const int nc = ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK);
+  return nc > TC_SHORT_K_CHUNKS && p.M >= 512 && p.N >= 256;
+}
+
 bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
   const bool tc = ctx->use_tc && !s.fp32_simt;
-  // CTA-pair tiles (256 x 128, tcgen05 cta_group::2) for stages with enough long-K work to
-  // fill the machine with pairs; symmetric (mirrored) and short-K stages keep 128 x 128
-  bool pair = false;
-  if (tc && ctx->pair_mode != 0) {
-    long pair_tiles = 0, max_nc = 0;
-    bool any_sym = false;
-    for (int v = 0; v < 4; ++v)
-      for (auto& p : s.probs[v]) {
-        any_sym |= p.sym != 0;
-        if (p.M <= 0 || p.N <= 0) continue;
-        pair_tiles += (long)ceil_div(p.M, 2 * TC_BM) * ceil_div(p.N, TC_BN_PAIR);
-        max_nc = std::max<long>(max_nc, ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK));
+  if (tc) {
+    GemmStage ps;   // the pair-tile problems of the stage
+    for (int v = 0; v < 4; ++v) {
+      std::vector<GemmProb> keep;
+      std::vector<long> keepc;
+      for (size_t i = 0; i < s.probs[v].size(); ++i) {
+        GemmProb p = s.probs[v][i];
+        const bool pair = tc_pair_tiles(ctx, p);
+        const int bm = pair ? 2 * TC_BM : TC_BM, bn = pair ? TC_BN_PAIR : TC_BN;
+        p.tiles_m = ceil_div(std::max(p.M, 1), bm);
+        p.tiles_n = ceil_div(std::max(p.N, 1), bn);
+        if (p.M <= 0 || p.N <= 0) p.tiles_m = p.tiles_n = 0;
+        if (p.M != p.N || bm != bn || pair) p.sym = 0;   // mirrored tiles: square 128 x 128 only
+        auto al = [](const float* q, int ld) {
+          return q == nullptr || ((reinterpret_cast<uintptr_t>(q) & 15) == 0 && (ld & 3) == 0);
+        };
+        p.vec = ((al(p.A, p.lda) && al(p.A2, p.lda2)) ? 1 : 0) | ((al(p.B, p.ldb) && al(p.B2, p.ldb2)) ? 2 : 0);
+        const long mn = (long)p.M * p.N;
+        const long cap = (p.ws != nullptr && mn > 0) ? s.caps[v][i] / mn : 1;
+        const int nc = ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK);
+        int splits = 1;
+        if (nc > TC_SPLIT_CHUNKS && p.ws != nullptr && !p.sym) {
+          splits = std::min(kSplitMax, ceil_div(nc, TC_SPLIT_CHUNKS));
+          splits = (int)std::min<long>(splits, cap);
+          splits = std::max(splits, 1);
+        }
+        const int cps = std::max(ceil_div(nc, splits), 1);
+        p.splits = std::max(ceil_div(nc, cps), 1);
+        p.kchunk = cps;
+        if (pair) { ps.probs[v].push_back(p); ps.caps[v].push_back(s.caps[v][i]); }
+        else { keep.push_back(p); keepc.push_back(s.caps[v][i]); }
       }
-    pair = !any_sym && (ctx->pair_mode == 2 ||
-                        (max_nc > TC_SHORT_K_CHUNKS && pair_tiles >= kNumSM / 2));
+      s.probs[v].swap(keep);
+      s.caps[v].swap(keepc);
+    }
+    bkfac_status r;
+    for (int pass = 0; pass < 2; ++pass) {
+      GemmStage& g = pass == 0 ? ps : s;
+      const bool pair = pass == 0;
+      if ((r = launch_variant<false, false>(ctx, g.probs[0], st, true, pair)) != BKFAC_OK) return r;
+      if ((r = launch_variant<false, true>(ctx, g.probs[1], st, true, pair)) != BKFAC_OK) return r;
+      if ((r = launch_variant<true, false>(ctx, g.probs[2], st, true, pair)) != BKFAC_OK) return r;
+      if ((r = launch_variant<true, true>(ctx, g.probs[3], st, true, pair)) != BKFAC_OK) return r;
+    }
+    for (int v = 0; v < 4; ++v) { s.probs[v].clear(); s.caps[v].clear(); }
+    s.fp32_simt = false;
+    return BKFAC_OK;
   }
-  const int bm = tc ? (pair ? 2 * TC_BM : TC_BM) : SG_BM, bn = tc ? (pair ? TC_BN_PAIR : TC_BN) : SG_BN;
+  const int bm = SG_BM, bn = SG_BN;
   long base_tiles = 0;
   for (int v = 0; v < 4; ++v)
     for (auto& p : s.probs[v]) {
       p.tiles_m = ceil_div(std::max(p.M, 1), bm);
       p.tiles_n = ceil_div(std::max(p.N, 1), bn);
       if (p.M <= 0 || p.N <= 0) p.tiles_m = p.tiles_n = 0;
-      if (!tc || p.M != p.N || bm != bn) p.sym = 0;   // mirrored tiles: tcgen05 square tiles only
-      {
-        auto al = [](const float* q, int ld) {
-          return q == nullptr || ((reinterpret_cast<uintptr_t>(q) & 15) == 0 && (ld & 3) == 0);
-        };
-        p.vec = ((al(p.A, p.lda) && al(p.A2, p.lda2)) ? 1 : 0) | ((al(p.B, p.ldb) && al(p.B2, p.ldb2)) ? 2 : 0);
-      }
-      base_tiles += p.sym ? (long)p.tiles_m * (p.tiles_m + 1) / 2 : (long)p.tiles_m * p.tiles_n;
+      p.sym = 0;
+      base_tiles += (long)p.tiles_m * p.tiles_n;
     }
-  const long nsm = (ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM) / (pair ? 2 : 1);
-  const long target = tc ? nsm : 2L * nsm;
-  // tcgen05: balance the stage's K-chunk work over the persistent CTAs -- every work item
-  // (tile x split) gets at most `quota` chunks, so one long-K problem no longer sets the
-  // critical path of a stage of mixed sizes (e.g. R^T R over n = 577 ... 4609)
-  long chunk_work = 0;
-  if (tc)
-    for (int v = 0; v < 4; ++v)
-      for (auto& p : s.probs[v]) {
-        const long nt = p.sym ? (long)p.tiles_m * (p.tiles_m + 1) / 2 : (long)p.tiles_m * p.tiles_n;
-        chunk_work += nt * (ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK));
-      }
-  const long quota = std::max<long>(2 * TC_PROMO, (chunk_work + nsm - 1) / nsm);
+  const long target = 2L * kNumSM;
   for (int v = 0; v < 4; ++v)
     for (size_t i = 0; i < s.probs[v].size(); ++i) {
       GemmProb& p = s.probs[v][i];
       const long mn = (long)p.M * p.N;
       const long cap = (p.ws != nullptr && mn > 0) ? s.caps[v][i] / mn : 1;
-      if (tc) {
-        const int nc = ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK);
-        int splits = 1;
-        if (nc >= 2 * TC_PROMO && nc > quota && p.ws != nullptr && !p.sym) {
-          splits = (int)std::min<long>(kSplitMax, (nc + quota - 1) / quota);
-          splits = std::min(splits, nc / TC_PROMO);
-          splits = (int)std::min<long>(splits, cap);
-          splits = std::max(splits, 1);
-        }
-        int cps = std::max(ceil_div(nc, splits), 1);
-        splits = std::max(ceil_div(nc, cps), 1);
-        p.splits = splits;
-        p.kchunk = cps;
-        continue;
-      }
       int splits = 1;
       if (p.K >= 1024 && base_tiles > 0 && base_tiles < target && p.ws != nullptr) {
         splits = (int)std::min<long>(kSplitMax, (target + base_tiles - 1) / base_tiles);
@@ -396,10 +408,10 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
       p.kchunk = std::max(kchunk, 1);
     }
   bkfac_status r;
-  if ((r = launch_variant<false, false>(ctx, s.probs[0], st, tc, pair)) != BKFAC_OK) return r;
-  if ((r = launch_variant<false, true>(ctx, s.probs[1], st, tc, pair)) != BKFAC_OK) return r;
-  if ((r = launch_variant<true, false>(ctx, s.probs[2], st, tc, pair)) != BKFAC_OK) return r;
-  if ((r = launch_variant<true, true>(ctx, s.probs[3], st, tc, pair)) != BKFAC_OK) return r;
+  if ((r = launch_variant<false, false>(ctx, s.probs[0], st, false, false)) != BKFAC_OK) return r;
+  if ((r = launch_variant<false, true>(ctx, s.probs[1], st, false, false)) != BKFAC_OK) return r;
+  if ((r = launch_variant<true, false>(ctx, s.probs[2], st, false, false)) != BKFAC_OK) return r;
+  if ((r = launch_variant<true, true>(ctx, s.probs[3], st, false, false)) != BKFAC_OK) return r;
   for (int v = 0; v < 4; ++v) { s.probs[v].clear(); s.caps[v].clear(); }
   s.fp32_simt = false;
   return BKFAC_OK;

@@ -114,6 +114,19 @@ class BKFACStack:
             for par in range(2):
                 self.S2[par][li] = torch.empty((dG, dA), dtype=torch.float32, device=dev)
 
+    def bind_outputs(self, by_parity: Sequence[Dict[int, "torch.Tensor"]]) -> None:
+        """Precondition straight into caller buffers (e.g. SlotGather.send_views(b)): the
+        S of step k goes to by_parity[k & 1][layer].  Call before any graph is captured."""
+        if self._graphs:
+            raise RuntimeError("bind_outputs after a CUDA graph was captured")
+        for par in range(2):
+            for li in self.my_layers:
+                t = by_parity[par][li]
+                dG, dA, _, _ = self.layers[li]
+                if tuple(t.shape) != (dG, dA) or not t.is_contiguous():
+                    raise ValueError(f"output buffer of layer {li} must be a contiguous ({dG}, {dA}) tensor")
+                self.S2[par][li] = t
+
     # ---------------------------------------------------------------------------------
     def rank_out(self, g: int) -> int:
         n, r, c = self.factors[g]
@@ -274,10 +287,17 @@ class BKFACStack:
 class SlotGather:
     """All-gather of the preconditioned gradients: slot s holds each
     rank's s-th owned layer, packed fp32 and padded to the slot maximum; one
-    ``all_gather_into_tensor`` per slot (NCCL over NVLink on the GPU box, gloo in tests)."""
+    ``all_gather_into_tensor`` per slot (NCCL over NVLink on the GPU box, gloo in tests).
+
+    Double-buffered by step parity so that step k's gather overlaps step k+1's compute:
+    the stack preconditions straight into the send slots (``send_views`` bound with
+    ``BKFACStack.bind_outputs``), ``start(b)`` issues the slot collectives asynchronously
+    (NCCL orders them after the work already on the current stream, then runs them on its
+    own stream beside the next step), and ``finish(b)`` makes the current stream wait for
+    them and returns every layer's S -- called before buffer set b is written again."""
 
     def __init__(self, layers: Sequence[Tuple[int, int, int, int]], owned: List[List[int]],
-                 rank: int, device):
+                 rank: int, device, nbuf: int = 2):
         import torch
         self.torch = torch
         self.layers = layers
@@ -289,26 +309,57 @@ class SlotGather:
         for s in range(self.nslots):
             sizes = [layers[o[s]][0] * layers[o[s]][1] if s < len(o) else 0 for o in owned]
             self.slot_numel.append(max(sizes))
-        self.send = [torch.zeros(n, dtype=torch.float32, device=device) for n in self.slot_numel]
-        self.recv = [torch.zeros(n * self.world, dtype=torch.float32, device=device)
-                     for n in self.slot_numel]
+        self.nbuf = nbuf
+        self.send = [[torch.zeros(n, dtype=torch.float32, device=device) for n in self.slot_numel]
+                     for _ in range(nbuf)]
+        self.recv = [[torch.zeros(n * self.world, dtype=torch.float32, device=device)
+                      for n in self.slot_numel] for _ in range(nbuf)]
+        self.pending = [None] * nbuf
 
     def bytes_per_step(self) -> int:
         return sum(4 * n * (self.world - 1) for n in self.slot_numel)
 
-    def gather(self, S_local: Dict[int, "torch.Tensor"], group=None) -> Dict[int, "torch.Tensor"]:
+    def send_views(self, b: int = 0) -> Dict[int, "torch.Tensor"]:
+        """This rank's layers as (d_G, d_A) views of buffer set b's send slots."""
+        out = {}
+        for s, li in enumerate(self.owned[self.rank]):
+            dG, dA = self.layers[li][0], self.layers[li][1]
+            out[li] = self.send[b][s][: dG * dA].view(dG, dA)
+        return out
+
+    def start(self, b: int, S_local: Optional[Dict[int, "torch.Tensor"]] = None, group=None) -> None:
+        """Issue buffer set b's slot all-gathers (async).  S_local: copied into the send slots
+        first unless it already lives there (send_views)."""
         import torch.distributed as dist
-        out: Dict[int, "torch.Tensor"] = {}
+        if self.pending[b] is not None:
+            raise RuntimeError("SlotGather.start: buffer set still in flight (call finish first)")
         mine = self.owned[self.rank]
+        if S_local is not None:
+            for s, li in enumerate(mine):
+                t = S_local[li].reshape(-1)
+                dst = self.send[b][s]
+                if t.data_ptr() != dst.data_ptr():
+                    dst[: t.numel()].copy_(t)
+        self.pending[b] = [dist.all_gather_into_tensor(self.recv[b][s], self.send[b][s], group=group,
+                                                       async_op=True) for s in range(self.nslots)]
+
+    def finish(self, b: int) -> Dict[int, "torch.Tensor"]:
+        """Wait (stream-ordered) for buffer set b's gathers; every layer's S as views."""
+        if self.pending[b] is not None:
+            for w in self.pending[b]:
+                w.wait()
+            self.pending[b] = None
+        out: Dict[int, "torch.Tensor"] = {}
         for s in range(self.nslots):
-            if s < len(mine):
-                t = S_local[mine[s]].reshape(-1)
-                self.send[s][: t.numel()].copy_(t)
-            dist.all_gather_into_tensor(self.recv[s], self.send[s], group=group)
             for q in range(self.world):
                 if s < len(self.owned[q]):
                     li = self.owned[q][s]
                     dG, dA = self.layers[li][0], self.layers[li][1]
                     base = q * self.slot_numel[s]
-                    out[li] = self.recv[s][base: base + dG * dA].view(dG, dA)
+                    out[li] = self.recv[b][s][base: base + dG * dA].view(dG, dA)
         return out
+
+    def gather(self, S_local: Dict[int, "torch.Tensor"], group=None, b: int = 0) -> Dict[int, "torch.Tensor"]:
+        """Synchronous form: start + finish on buffer set b."""
+        self.start(b, S_local, group)
+        return self.finish(b)

@@ -89,3 +89,53 @@ def test_sharding_covers_every_layer_once_and_is_deterministic():
         owned = shard_layers(costs, world)
         assert owned == shard_layers(costs, world)
         assert sorted(sum(owned, [])) == list(range(len(LAYERS)))
+
+
+def _worker_overlap(rank, world, port, out_q):
+    """The overlapped form bench.py uses: outputs bound to the double-buffered send slots,
+    step k's gather started asynchronously and finished only before buffer set k & 1 is
+    written again (two steps later) or at the end."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        layers = [(dG, dA, 2 * i, 2 * i + 1) for i, (dG, dA, _, _) in enumerate(LAYERS)]
+        costs = [layer_cost(dA, dG) for (dG, dA, _, _) in LAYERS]
+        owned = shard_layers(costs, world)
+        gather = SlotGather(layers, owned, rank, "cpu")
+        views = [gather.send_views(0), gather.send_views(1)]
+        base = {li: torch.from_numpy(_layer_result(li)) for li in owned[rank]}
+        results = []
+        for k in range(4):
+            b = k & 1
+            if k >= 2:
+                results.append({li: v.numpy().copy() for li, v in gather.finish(b).items()})
+            for li in owned[rank]:           # "precondition straight into the send slot"
+                views[b][li].copy_(base[li] * float(k + 1))
+            gather.start(b)
+        for b in (0, 1):
+            results.append({li: v.numpy().copy() for li, v in gather.finish(b).items()})
+        out_q.put((rank, results))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slot_allgather_overlapped_double_buffer():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_overlap, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = {li: _layer_result(li) for li in range(len(LAYERS))}
+    for rank, steps in results:
+        assert len(steps) == 4
+        for k, full in enumerate(steps):          # finished in step order 0, 1, 2, 3
+            assert sorted(full) == list(range(len(LAYERS)))
+            for li, S in full.items():
+                assert np.array_equal(S, ref[li] * np.float32(k + 1)), (rank, k, li)
