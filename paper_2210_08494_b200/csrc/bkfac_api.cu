@@ -278,7 +278,7 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
         const int nsm = ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM;
         // grid_cap < 0: one CTA per tile (a background job whose CTAs retire quickly)
         const int grid = ctx->grid_cap < 0 ? tiles : std::min(tiles, pair ? nsm / 2 : nsm);
-        if (!cuda_ok(tc_launch<TA, TB>(b, grid, st, max_chunks <= TC_SHORT_K_CHUNKS, pair)))
+        if (!cuda_ok(tc_launch<TA, TB>(b, grid, st, max_chunks, pair)))
           return BKFAC_ERR_CUDA;
       } else {
         gemm_simt_kernel<TA, TB><<<tiles, 256, 0, st>>>(b);
@@ -316,7 +316,8 @@ bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char*
 //   * CTA-pair 256 x 256 tiles for non-symmetric problems with long K (> 8 chunks) and
 //     M >= 512, N >= 256; 128 x 128 tiles otherwise (a stage launches each group separately);
 //   * split-K (deterministic fixed-order reduction) into work items of at most
-//     TC_SPLIT_CHUNKS chunks of 32 when the caller supplied a workspace.
+//     TC_SPLIT_CHUNKS chunks of 32, for problems with fewer tiles than SMs, when the caller
+//     supplied a workspace.
 constexpr int TC_SPLIT_CHUNKS = 128;
 bool tc_pair_tiles(const bkfac_ctx ctx, const GemmProb& p) {
   if (p.sym || ctx->pair_mode == 0) return false;
@@ -348,7 +349,8 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
         const long cap = (p.ws != nullptr && mn > 0) ? s.caps[v][i] / mn : 1;
         const int nc = ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK);
         int splits = 1;
-        if (nc > TC_SPLIT_CHUNKS && p.ws != nullptr && !p.sym) {
+        const long own_tiles = (long)p.tiles_m * p.tiles_n;   // the problem alone fills the GPU?
+        if (nc > TC_SPLIT_CHUNKS && own_tiles < kNumSM && p.ws != nullptr && !p.sym) {
           splits = std::min(kSplitMax, ceil_div(nc, TC_SPLIT_CHUNKS));
           splits = (int)std::min<long>(splits, cap);
           splits = std::max(splits, 1);
@@ -2123,6 +2125,12 @@ bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha
 void bkfac_debug_tc(unsigned long long* host, int reset) {
   if (reset) { static unsigned long long z[148 * 8]; cudaMemcpyToSymbol(g_tc_dbg, z, sizeof(z)); return; }
   cudaMemcpyFromSymbol(host, g_tc_dbg, sizeof(unsigned long long) * 148 * 8);
+}
+#endif
+#ifdef BKFAC_CHASE_TIMING
+void bkfac_debug_chase(unsigned long long* host, int reset) {
+  if (reset) { static unsigned long long z[8]; cudaMemcpyToSymbol(g_chase_dbg, z, sizeof(z)); return; }
+  cudaMemcpyFromSymbol(host, g_chase_dbg, sizeof(unsigned long long) * 8);
 }
 #endif
 #ifdef BKFAC_CHOL_TIMING

@@ -606,6 +606,14 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
       int tl = 0, u0 = 0, u1 = 0;   // swap protocol (BN = 256): local tile, fills per buffer
       for (int t = tfirst; t < b.total_tiles; t += tstride, ++tl) {
         const TcTile x = tc_tile<BN, BMT>(b, t);
+        // single-CTA tiles: the instruction's N shrinks to the tile's valid columns (rounded to
+        // 16) -- a narrow problem (N = 32: the band reduction's X = A22 V) costs N / BN of
+        // the MMA time.  Pair tiles keep N = BN (each CTA stages half of B's rows).
+        uint32_t idesc = IDESC;
+        if (!PAIR) {
+          const int nv = min(BN, ((b.p[x.pi].N - x.n0 + 15) >> 4) << 4);
+          idesc = (IDESC & ~(0x3Fu << 17)) | ((uint32_t)(nv >> 3) << 17);
+        }
         for (int c0 = x.c_beg; c0 < x.c_end; c0 += TC_PROMO, ++kb) {
           // swap: first K-block of the tile into its sum buffer (tl & 1), the others into
           // the other buffer (see tc_epilogue)
@@ -652,12 +660,12 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
                 tc_mma2_tf32(tmem_d, aH, bL, IDESC, 1u);
                 tc_mma2_tf32(tmem_d, aH, bH, IDESC, 1u);
               } else {
-                tc_mma_tf32(tmem_d, aL, bH, IDESC, first);   // small terms first
-                tc_mma_tf32(tmem_d, aH, bL, IDESC, 1u);
-                tc_mma_tf32(tmem_d, aH, bH, IDESC, 1u);
+                tc_mma_tf32(tmem_d, aL, bH, idesc, first);   // small terms first
+                tc_mma_tf32(tmem_d, aH, bL, idesc, 1u);
+                tc_mma_tf32(tmem_d, aH, bH, idesc, 1u);
               }
 #else                                     // tuning only: 1xTF32 (MMA-rate probe)
-              tc_mma_tf32(tmem_d, aH, bH, IDESC, first);
+              tc_mma_tf32(tmem_d, aH, bH, idesc, first);
 #endif
             }
             if (PAIR) tc_commit2(empty_bar(stage)); else tc_commit(empty_bar(stage));
@@ -863,11 +871,13 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 constexpr int TC_BN = 128, TC_BN_PAIR = BKFAC_TC_BN_PAIR, TC_NLW = BKFAC_TC_NLW, TC_DEPTH = BKFAC_TC_DEPTH;
 using TcMain = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 4>;
 using TcShortK = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 8>;
-#ifndef BKFAC_TC_PAIR_EPI
-#define BKFAC_TC_PAIR_EPI 4
-#endif
-constexpr int TC_PAIR_EPI = BKFAC_TC_PAIR_EPI;   // epilogue warps of the pair kernel (4 or 8)
-using TcPair = TcCfg<TC_BN_PAIR, TC_NLW, TC_DEPTH, TC_PAIR_EPI, true>;
+// Pair kernels come with 4 epilogue warps (long K: the mainloop sets the pace, registers go
+// to the loaders) and with 8 (K <= TC_PAIR_EPI8_CHUNKS chunks: a 256 x 256 tile's output --
+// C0 read + C write, 512 KB per pair -- must drain within about one K-block of the next
+// tile's MMAs; measured at configs[4]: prec_out 57.8 -> 46.3 ms, resid 10.8 -> 7.6 ms)
+constexpr int TC_PAIR_EPI8_CHUNKS = 48;
+using TcPair = TcCfg<TC_BN_PAIR, TC_NLW, TC_DEPTH, 4, true>;
+using TcPair8 = TcCfg<TC_BN_PAIR, TC_NLW, TC_DEPTH, 8, true>;
 constexpr int TC_SHORT_K_CHUNKS = 8;   // stages with every K <= 8 chunks use 8 epilogue warps
 
 template <bool TA, bool TB, int EPI, bool PAIR>
@@ -888,21 +898,27 @@ inline bool tc_init_attributes() {
   ok &= tc_set_attr<false, true, 8, false>();
   ok &= tc_set_attr<true, false, 8, false>();
   ok &= tc_set_attr<true, true, 8, false>();
-  ok &= tc_set_attr<false, false, TC_PAIR_EPI, true>();
-  ok &= tc_set_attr<false, true, TC_PAIR_EPI, true>();
-  ok &= tc_set_attr<true, false, TC_PAIR_EPI, true>();
-  ok &= tc_set_attr<true, true, TC_PAIR_EPI, true>();
+  ok &= tc_set_attr<false, false, 4, true>();
+  ok &= tc_set_attr<false, true, 4, true>();
+  ok &= tc_set_attr<true, false, 4, true>();
+  ok &= tc_set_attr<true, true, 4, true>();
+  ok &= tc_set_attr<false, false, 8, true>();
+  ok &= tc_set_attr<false, true, 8, true>();
+  ok &= tc_set_attr<true, false, 8, true>();
+  ok &= tc_set_attr<true, true, 8, true>();
   return ok;
 }
 
 // grid: persistent CTAs (pair mode: CTA pairs, 2 x grid CTAs in clusters of 2)
 template <bool TA, bool TB>
-inline cudaError_t tc_launch(const GemmBatch& b, int grid, cudaStream_t st, bool short_k, bool pair) {
+inline cudaError_t tc_launch(const GemmBatch& b, int grid, cudaStream_t st, int max_chunks, bool pair) {
+  const bool short_k = max_chunks <= TC_SHORT_K_CHUNKS;
   if (pair) {
+    const bool e8 = max_chunks <= TC_PAIR_EPI8_CHUNKS;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * grid), 1, 1);
-    cfg.blockDim = dim3(TcPair::THREADS, 1, 1);
-    cfg.dynamicSmemBytes = TcPair::SMEM_BYTES;
+    cfg.blockDim = dim3(e8 ? TcPair8::THREADS : TcPair::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = e8 ? TcPair8::SMEM_BYTES : TcPair::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -911,7 +927,8 @@ inline cudaError_t tc_launch(const GemmBatch& b, int grid, cudaStream_t st, bool
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TA, TB, TC_BN_PAIR, TC_NLW, TC_DEPTH, TC_PAIR_EPI, true>, b);
+    if (e8) return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TA, TB, TC_BN_PAIR, TC_NLW, TC_DEPTH, 8, true>, b);
+    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TA, TB, TC_BN_PAIR, TC_NLW, TC_DEPTH, 4, true>, b);
   }
   if (short_k)
     gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 8, false><<<grid, TcShortK::THREADS, TcShortK::SMEM_BYTES, st>>>(b);

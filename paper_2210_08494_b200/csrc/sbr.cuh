@@ -296,6 +296,14 @@ sbr_w_kernel(const __grid_constant__ EigBatch b, int j) {
 }
 
 // ---------------------------------------------------------------------- stage 2: chase
+#ifdef BKFAC_CHASE_TIMING
+__device__ unsigned long long g_chase_dbg[8];   // tuning builds: phase cycle sums (all warps)
+#define CH_T(v) const unsigned long long v = clock64()
+#define CH_ACC(i, a, b) atomicAdd(&g_chase_dbg[i], (b) - (a))
+#else
+#define CH_T(v)
+#define CH_ACC(i, a, b)
+#endif
 BKFAC_DEV float sbr_ldcg(const float* a) { return __ldcg(a); }
 BKFAC_DEV void sbr_stcg(float* a, float v) { __stcg(a, v); }
 
@@ -326,6 +334,9 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
   }
   if (tid < 64) prog[tid] = -1;
   __syncthreads();
+#ifdef BKFAC_CHASE_TIMING
+  const unsigned long long t_kernel0 = clock64();
+#endif
   auto at = [&](int r, int c) -> float* { return AB + (long)c * LDB + (r - c); };
   for (int j = warp; j < m - 2; j += NW) {
     float tau_u = 0.f;
@@ -334,6 +345,7 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
       if (s >= m) break;
       const int nk = min(B, m - s);
       const bool row = lane < nk;              // lane = row s + lane of the task's blocks
+      CH_T(t0);
       if (j > 0) {
         const int need = ((j - 1) << 8) + (k + 2);
         while (prog[(j - 1) % NW] < need) {
@@ -343,6 +355,7 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
         }
       }
       __syncwarp();
+      CH_T(t1);
       // every load of the task in flight at once: the E row (k >= 1; k = 0: column j) and the
       // lower D row (D(lane, l), l <= lane) -- one L2 round trip
       float er[B], dr[B];
@@ -355,6 +368,7 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
         dr[l] = (row && l <= lane) ? sbr_ldcg(AB + (long)(s + l) * LDB + (lane - l)) : 0.f;
       }
       float x;
+      CH_T(t2);
       if (k == 0) {
         x = er[0];
       } else {
@@ -401,6 +415,7 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
         }
       }
       __syncwarp();
+      CH_T(t3);
       if (tau != 0.f) {
         // D = A[R_k, R_k] <- H D H:  p = tau D v, w = p - tau/2 (p.v) v, D -= v w^T + w v^T
 #pragma unroll
@@ -428,6 +443,7 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
             if (l <= lane) sbr_stcg(AB + (long)(s + l) * LDB + (lane - l), dr[l] - v * ws[l] - wi * vs[l]);
         }
       }
+      CH_T(t4);
       p.Vq[((long)j * KT + k) * B + lane] = v;
       if (lane == 0) p.tq[(long)j * KT + k] = tau;
       us[lane] = v;
@@ -435,12 +451,22 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
       __syncwarp();
       __threadfence_block();
       if (lane == 0) prog[warp] = (j << 8) + (k + 1);
+      CH_T(t5);
+#ifdef BKFAC_CHASE_TIMING
+      if (lane == 0 && blockIdx.x == 0) {
+        CH_ACC(0, t0, t1); CH_ACC(1, t1, t2); CH_ACC(2, t2, t3); CH_ACC(3, t3, t4); CH_ACC(4, t4, t5);
+        atomicAdd(&g_chase_dbg[5], 1ull);
+      }
+#endif
     }
     __syncwarp();
     __threadfence_block();
     if (lane == 0) prog[warp] = (j << 8) + 255;
   }
   __syncthreads();
+#ifdef BKFAC_CHASE_TIMING
+  if (tid == 0 && blockIdx.x == 0) atomicAdd(&g_chase_dbg[6], clock64() - t_kernel0);
+#endif
   for (int i = tid; i < m; i += NW * 32) {
     p.d[i] = sbr_ldcg(AB + (long)i * LDB);
     if (i < m - 1) p.e[i] = sbr_ldcg(AB + (long)i * LDB + 1);
@@ -474,30 +500,40 @@ sbr_q2_kernel(const __grid_constant__ EigBatch b) {
     for (int i = 0; i < m; ++i) Z[(long)i * r] = (float)p.Y[(long)i * r + c];
   const int nsw = m - 2;
   const int ngroups = (nsw + G - 1) / G;
-  // reflectors of diamond (g, k) into buffer q (every thread of the CTA takes a share)
+  // reflectors of diamond (g, k) into buffer q (every thread of the CTA takes a share) by
+  // cp.async (zero-filled where a task does not exist): the copies complete while the
+  // current diamond is applied, and are waited for before the next diamond's barrier
+  auto cp4 = [](float* dst, const float* src, bool ok) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
+  };
   auto stage = [&](int q, int j0, int jn, int k) {
     for (int e = threadIdx.x; e < G * B; e += NT) {
       const int a = e / B, i = e % B;
       const bool ex = a < jn && j0 + a + 1 + k * B < m;
-      vsm[q][e] = ex ? p.Vq[((long)(j0 + a) * KT + k) * B + i] : 0.f;
+      cp4(&vsm[q][e], ex ? p.Vq + ((long)(j0 + a) * KT + k) * B + i : p.Vq, ex);
     }
     for (int a = threadIdx.x; a < G; a += NT) {
       const bool ex = a < jn && j0 + a + 1 + k * B < m;
-      tsm[q][a] = ex ? p.tq[(long)(j0 + a) * KT + k] : 0.f;
+      cp4(&tsm[q][a], ex ? p.tq + (long)(j0 + a) * KT + k : p.tq, ex);
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  auto stage_wait = [] { asm volatile("cp.async.wait_all;" ::: "memory"); };
   int q = 0;
   for (int g = ngroups - 1; g >= 0; --g) {
     const int j0 = g * G, jn = min(G, nsw - j0);
     __syncthreads();
     stage(q, j0, jn, 0);
+    stage_wait();
     // window of diamond k: rows j0 + 1 + k B .. + WIN - 1; w[t] <-> row rb + t
     int rb = j0 + 1;
     float w[WIN];
 #pragma unroll
     for (int t = 0; t < WIN; ++t) w[t] = (cok && rb + t < m) ? Z[(long)(rb + t) * r] : 0.f;
     for (int k = 0; rb < m; ++k, rb += B) {
-      __syncthreads();   // buffer q staged; buffer q ^ 1 free
+      stage_wait();      // this thread's copies into buffer q have landed
+      __syncthreads();   // buffer q staged by every thread; buffer q ^ 1 free
       if (rb + B < m) stage(q ^ 1, j0, jn, k + 1);
       // next diamond's new rows (rb + WIN .. rb + WIN + B - 1): untouched by this diamond
       float nx[B];
