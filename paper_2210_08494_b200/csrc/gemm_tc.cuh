@@ -387,7 +387,7 @@ BKFAC_DEV void tc_store_group(const GemmProb& p, const TcTile& x, int g, float (
 
 // Epilogue, BN <= 128 protocol -- warps 0-3 (thread = tile row = TMEM lane): promote each K-block accumulator
 // into the running sum (TMEM), then alpha/beta and coalesced stores of the tile.
-template <int BN, int EPI, bool PAIR>
+template <int BN, int EPI, bool PAIR, int NLW_EPI>
 BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int lane,
                            uint32_t tfull0, uint32_t tfull1, uint32_t tempty0, uint32_t tempty1,
                            float* stage) {
@@ -402,8 +402,12 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const uint32_t run = tmem_base + lane_off + 2 * BN;       // running-sum columns
     // column groups of this warp: all, or one half when two warps share the quarter
+    // EPI = 4, 8 or 16 warps: warps 0-3 and, after the loaders, groups of 4 consecutive warps
+    // (one per TMEM lane quarter); slice = which of the EPI / 4 column slices this warp takes
     constexpr int NG = BN / 16, GPW = NG * 4 / EPI;
-    const int g_beg = (warp < 4 ? 0 : 1) * GPW;
+    static_assert(EPI == 4 || EPI == 8 || EPI == 16, "epilogue warps");
+    const int eidx = warp < 4 ? warp : 4 + (warp - (TC_MMA_WARP + 1 + NLW_EPI));
+    const int g_beg = (eidx >> 2) * GPW;
     int kb = 0;
     int tl = 0, jf0 = 0, jf1 = 0;   // swap protocol: local tile count, full waits per buffer
     for (int t = tfirst; t < b.total_tiles; t += tstride) {
@@ -841,7 +845,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     const int e = warp < 4 ? warp : 4 + (warp - (TC_MMA_WARP + 1 + NLW));   // epilogue warp index
     float* stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256) +
                    e * Cfg::EPI_STAGE_FLOATS;
-    tc_epilogue<BN, EPI, PAIR>(b, tmem_base, warp, lane, tfull_bar(0), tfull_bar(1), tempty_bar(0), tempty_bar(1),
+    tc_epilogue<BN, EPI, PAIR, NLW>(b, tmem_base, warp, lane, tfull_bar(0), tfull_bar(1), tempty_bar(0), tempty_bar(1),
                     stage);
   }
   tc_fence_before();
@@ -870,7 +874,16 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 // chunk needed 96 + 64 B/cycle, which capped the pipe near 80 % of its rate.
 constexpr int TC_BN = 128, TC_BN_PAIR = BKFAC_TC_BN_PAIR, TC_NLW = BKFAC_TC_NLW, TC_DEPTH = BKFAC_TC_DEPTH;
 using TcMain = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 4>;
-using TcShortK = TcCfg<TC_BN, TC_NLW, TC_DEPTH, 8>;
+// short-K stages (every K <= 8 chunks): the epilogue, not the MMA, sets the pace (C0 read
+// + C write of whole output tiles): more epilogue warps, fewer loaders
+#ifndef BKFAC_TC_SHORT_EPI
+#define BKFAC_TC_SHORT_EPI 8
+#endif
+#ifndef BKFAC_TC_SHORT_NLW
+#define BKFAC_TC_SHORT_NLW TC_NLW
+#endif
+constexpr int TC_SHORT_EPI = BKFAC_TC_SHORT_EPI, TC_SHORT_NLW = BKFAC_TC_SHORT_NLW;
+using TcShortK = TcCfg<TC_BN, TC_SHORT_NLW, TC_DEPTH, TC_SHORT_EPI>;
 // Pair kernels come with 4 epilogue warps (long K: the mainloop sets the pace, registers go
 // to the loaders) and with 8 (K <= TC_PAIR_EPI8_CHUNKS chunks: a 256 x 256 tile's output --
 // C0 read + C write, 512 KB per pair -- must drain within about one K-block of the next
@@ -894,10 +907,14 @@ inline bool tc_init_attributes() {
   ok &= tc_set_attr<false, true, 4, false>();
   ok &= tc_set_attr<true, false, 4, false>();
   ok &= tc_set_attr<true, true, 4, false>();
-  ok &= tc_set_attr<false, false, 8, false>();
-  ok &= tc_set_attr<false, true, 8, false>();
-  ok &= tc_set_attr<true, false, 8, false>();
-  ok &= tc_set_attr<true, true, 8, false>();
+  ok &= cudaFuncSetAttribute(gemm_tc_kernel<false, false, TC_BN, TC_SHORT_NLW, TC_DEPTH, TC_SHORT_EPI, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, TcShortK::SMEM_BYTES) == cudaSuccess;
+  ok &= cudaFuncSetAttribute(gemm_tc_kernel<false, true, TC_BN, TC_SHORT_NLW, TC_DEPTH, TC_SHORT_EPI, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, TcShortK::SMEM_BYTES) == cudaSuccess;
+  ok &= cudaFuncSetAttribute(gemm_tc_kernel<true, false, TC_BN, TC_SHORT_NLW, TC_DEPTH, TC_SHORT_EPI, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, TcShortK::SMEM_BYTES) == cudaSuccess;
+  ok &= cudaFuncSetAttribute(gemm_tc_kernel<true, true, TC_BN, TC_SHORT_NLW, TC_DEPTH, TC_SHORT_EPI, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, TcShortK::SMEM_BYTES) == cudaSuccess;
   ok &= tc_set_attr<false, false, 4, true>();
   ok &= tc_set_attr<false, true, 4, true>();
   ok &= tc_set_attr<true, false, 4, true>();
@@ -931,7 +948,7 @@ inline cudaError_t tc_launch(const GemmBatch& b, int grid, cudaStream_t st, int 
     return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TA, TB, TC_BN_PAIR, TC_NLW, TC_DEPTH, 4, true>, b);
   }
   if (short_k)
-    gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 8, false><<<grid, TcShortK::THREADS, TcShortK::SMEM_BYTES, st>>>(b);
+    gemm_tc_kernel<TA, TB, TC_BN, TC_SHORT_NLW, TC_DEPTH, TC_SHORT_EPI, false><<<grid, TcShortK::THREADS, TcShortK::SMEM_BYTES, st>>>(b);
   else
     gemm_tc_kernel<TA, TB, TC_BN, TC_NLW, TC_DEPTH, 4, false><<<grid, TcMain::THREADS, TcMain::SMEM_BYTES, st>>>(b);
   return cudaGetLastError();
