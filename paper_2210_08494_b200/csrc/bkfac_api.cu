@@ -257,7 +257,7 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
   size_t i0 = 0;
   while (i0 < v.size()) {
     const size_t n = std::min(v.size() - i0, (size_t)GEMM_MAXP);
-    static GemmBatch b;  // host staging (large); kernel params are copied at launch
+    static thread_local GemmBatch b;  // host staging (large); kernel params are copied at launch
     b.nprob = (int)n;
     int tiles = 0;
     bool any_split = false;
@@ -427,7 +427,7 @@ bkfac_status run_ew(bkfac_ctx ctx, std::vector<EwProb>& v, cudaStream_t st, cons
   size_t i0 = 0;
   while (i0 < v.size()) {
     const size_t n = std::min(v.size() - i0, (size_t)EW_MAXP);
-    static EwBatch b;
+    static thread_local EwBatch b;
     b.nprob = (int)n;
     for (size_t i = 0; i < n; ++i) b.p[i] = v[i0 + i];
     ew_kernel<<<dim3(128, (unsigned)n), 256, 0, st>>>(b);
@@ -570,7 +570,7 @@ bkfac_status run_chol(bkfac_ctx ctx, std::vector<CholProb>& v, cudaStream_t st) 
     }
   }
   prof_begin(ctx, "chol_inv", st, flops, bytes);
-  static CholTiledBatch b;
+  static thread_local CholTiledBatch b;
   size_t i0 = 0;
   while (i0 < v.size()) {
     const size_t n = std::min(v.size() - i0, (size_t)CT_MAXP);
@@ -669,7 +669,7 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
 
 bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
   size_t i0 = 0;
-  static EigBatch b;
+  static thread_local EigBatch b;
   while (i0 < v.size()) {
     const size_t n = std::min(v.size() - i0, (size_t)EIG_MAXP);
     b.nprob = (int)n;
@@ -689,9 +689,12 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     // but is SUBMITTED after the tridiagonalisation, so the clusters are placed first.
     int ea_busy = 0;
     if (ctx->pending_ea) {
+      int ngt = 0;
+      for (size_t i = 0; i < n; ++i) ngt += !b.p[i].sbr && sytrd_tiled_cluster(b.p[i].m) == 0;
+      const int cgt = std::max(1, std::min(gt_cluster_max(ctx), kNumSM / std::max(1, ngt)));
       for (size_t i = 0; i < n; ++i) {
         const int C = sytrd_tiled_cluster(b.p[i].m);
-        ea_busy += (b.p[i].sbr || C == 0) ? 1 : C;
+        ea_busy += b.p[i].sbr ? 1 : (C == 0 ? cgt : C);   // CTAs its reduction occupies
       }
       if (!cuda_ok(cudaEventRecord(ctx->ev_ea_fork, st))) return BKFAC_ERR_CUDA;
     }
@@ -715,7 +718,7 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
     {
       // one launch per cluster size; the launches are independent problems, so all but
       // the first run on side streams (fork/join) and overlap on the GPU
-      static EigBatch sub[5];
+      static thread_local EigBatch sub[5];
       int ngroups = 0;
       const int Cs[5] = {0, 1, 2, 4, 8};
       int gC[5], gm[5];
@@ -1061,6 +1064,16 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
     lp.ws = a.take(sizeof(float) * std::max<long>(lp.ws_elems, 1));
     c->l.push_back(lp);
   }
+  // every eigenproblem order must fit one of the tridiagonalisation paths: shared-memory
+  // cluster tiles (m <= 864), two-stage (m <= 1632), or global tiles whose per-CTA vectors and
+  // staging fit the shared-memory opt-in (m up to ~3100)
+  auto eig_ok = [](int m) {
+    const int m_pad = (m + 31) / 32 * 32;
+    return sytrd_tiled_cluster(m) != 0 || sbr_supported(m) || syt_gt_smem_floats(m_pad) <= SYT_SMEM_FLOATS;
+  };
+  for (const auto& fp : c->f) {
+    if (!eig_ok(fp.m) || (fp.rsvd && !eig_ok(fp.lmax))) { delete c; return BKFAC_ERR_UNSUPPORTED; }
+  }
   c->ws_bytes = a.cur;
   cudaError_t e = cudaMallocHost(&c->host_status, sizeof(int) * (size_t)(nfactors + nlayers + 1));
   if (e != cudaSuccess) { delete c; return BKFAC_ERR_CUDA; }
@@ -1279,16 +1292,18 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       }
     }
     STAGE(run_ew(ctx, ew, st, "ew_dense_scale"));
-    {   // M reaches the tensor cores only as an MMA operand on this path: guard it
-      static NfBatch nb;
-      nb.nprob = 0;
-      for (int i : dense) {
-        if (nb.nprob == NF_MAXP) break;
-        const auto& a = args[i];
-        nb.p[nb.nprob++] = NfProb{a.M, ctx->f[a.factor].d.n, a.c, ctx->f[a.factor].d.n, status_ptr(ctx, a.factor)};
+    {   // M reaches the tensor cores only as an MMA operand on this path: guard it (every
+        // dense factor, in launches of up to NF_MAXP)
+      static thread_local NfBatch nb;
+      for (size_t i0 = 0; i0 < dense.size(); i0 += NF_MAXP) {
+        nb.nprob = 0;
+        for (size_t q = i0; q < std::min(dense.size(), i0 + NF_MAXP); ++q) {
+          const auto& a = args[dense[q]];
+          nb.p[nb.nprob++] = NfProb{a.M, ctx->f[a.factor].d.n, a.c, ctx->f[a.factor].d.n, status_ptr(ctx, a.factor)};
+        }
+        nonfinite_kernel<<<dim3(16, (unsigned)nb.nprob), 256, 0, st>>>(nb);
+        LAUNCH_CHECK(ctx);
       }
-      nonfinite_kernel<<<dim3(16, (unsigned)nb.nprob), 256, 0, st>>>(nb);
-      LAUNCH_CHECK(ctx);
     }
     for (int i : dense) {
       const auto& a = args[i];
@@ -1444,16 +1459,13 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& fp = ctx->f[a.factor];
       const int mm = fp.d.r + a.c;
       const float* W = at<float>(ctx, fp.W);
-      gs.add(false, true, gp(W, fp.m, W, fp.m, at<float>(ctx, fp.eig.K), mm, mm, mm, a.c, a.beta), 0);
-      if (a.alpha != 0.f) {
-        EwProb e{};
-        e.Y = at<float>(ctx, fp.eig.K); e.ldy = mm; e.X = nullptr; e.vec = a.D_in;
-        e.rows = fp.d.r; e.cols = 1; e.a = a.alpha; e.op = EW_ADD_DIAG;
-        ew.push_back(e);
+      GemmProb pc = gp(W, fp.m, W, fp.m, at<float>(ctx, fp.eig.K), mm, mm, mm, a.c, a.beta);
+      if (a.alpha != 0.f) {   // + diag(alpha D, 0) in the epilogue (Eq.(7) with rho D)
+        pc.diag_vec = a.D_in; pc.diag_a = a.alpha; pc.diag_n = fp.d.r;
       }
+      gs.add(false, true, pc, 0);
     }
     STAGE(run("gemm_core"));
-    STAGE(run_ew(ctx, ew, st, "ew_core_diag"));
     for (int i : brand) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
@@ -1658,7 +1670,7 @@ bkfac_status bkfac_light_correction(bkfac_ctx ctx, const bkfac_correct_args* arg
   bkfac_status rs = BKFAC_OK;
   GemmStage gs;
   std::vector<EigProb> eg;
-  static ColIdxBatch cb;
+  static thread_local ColIdxBatch cb;
   auto colidx = [&](int mode, const char* tag) -> bkfac_status {
     prof_begin(ctx, tag, st, 0.0, 0.0);
     for (int i0 = 0; i0 < count; i0 += NF_MAXP) {
@@ -1892,8 +1904,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
   }
   if (count == 0) return BKFAC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static PrecScalBatch psb;
-  static PrecScaleBatch pcb;
+  static thread_local PrecScalBatch psb;
   bkfac_status rs;
   GemmStage gs;
   // S1: scalars
@@ -1920,47 +1931,32 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     const auto& a = args[i];
     const auto& lp = ctx->l[a.layer];
     const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G;
-    if (rA > 0) {
+    float* lam = at<float>(ctx, lp.lam);   // {lamA, lamG, 1/(lamG lamA), 1/lamA, 1/lamG}
+    if (rA > 0) {   // Y' = (J U_A) diag(sA) / lamG  (scaling in the epilogue)
       GemmProb p = gp(a.J, dA, a.U_A, dA, at<float>(ctx, lp.Y), dG, dG, rA, dA, 1.f);
+      p.col_scale = at<float>(ctx, lp.sA); p.alpha_dev = lam + 4;
       gemm_ws(p, at<float>(ctx, lp.ws));
       gs.add(true, false, p, lp.ws_elems);
     }
-    if (rG > 0) {
-      gs.add(false, false, gp(a.J, dA, a.U_G, dG, at<float>(ctx, lp.Xt), dA, dA, rG, dG, 1.f), 0);
+    if (rG > 0) {   // Xt' = (J^T U_G) diag(sG) / lamA
+      GemmProb p = gp(a.J, dA, a.U_G, dG, at<float>(ctx, lp.Xt), dA, dA, rG, dG, 1.f);
+      p.col_scale = at<float>(ctx, lp.sG); p.alpha_dev = lam + 3;
+      gs.add(false, false, p, 0);
     }
   }
   if ((rs = run_gemms(ctx, gs, st, "gemm_prec_proj")) != BKFAC_OK) return rs;
-  // S3: Z = U_G^T Y (r_G x r_A)
+  // S3: Z' = diag(sG) U_G^T (Y diag(sA)) = lamG diag(sG) (U_G^T Y')  (r_G x r_A)
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
     const auto& lp = ctx->l[a.layer];
     const int dG = lp.d.d_G, rA = lp.d.r_A, rG = lp.d.r_G;
-    if (rA > 0 && rG > 0)
-      gs.add(true, false, gp(a.U_G, dG, at<float>(ctx, lp.Y), dG, at<float>(ctx, lp.Z), rG, rG, rA, dG, 1.f), 0);
+    if (rA > 0 && rG > 0) {
+      GemmProb p = gp(a.U_G, dG, at<float>(ctx, lp.Y), dG, at<float>(ctx, lp.Z), rG, rG, rA, dG, 1.f);
+      p.row_scale = at<float>(ctx, lp.sG); p.alpha_dev = at<float>(ctx, lp.lam) + 1;
+      gs.add(true, false, p, 0);
+    }
   }
   if ((rs = run_gemms(ctx, gs, st, "gemm_prec_z")) != BKFAC_OK) return rs;
-  // S4: Y' = Y diag(sA)/lamG ; Z' = diag(sG) Z diag(sA) ; Xt' = Xt diag(sG)/lamA
-  prof_begin(ctx, "prec_scale", st, 0.0, 0.0);
-  for (int i0 = 0; i0 < count; i0 += PS_MAXP / 3) {
-    const int n = std::min(count - i0, PS_MAXP / 3);
-    pcb.nprob = 0;
-    for (int i = i0; i < i0 + n; ++i) {
-      const auto& lp = ctx->l[args[i].layer];
-      const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G;
-      float* lam = at<float>(ctx, lp.lam);
-      if (rA > 0)
-        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.Y), dG, dG, rA, at<float>(ctx, lp.sA), nullptr, lam + 1, 0};
-      if (rA > 0 && rG > 0)
-        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.Z), rG, rG, rA, at<float>(ctx, lp.sA), at<float>(ctx, lp.sG), nullptr, 1};
-      if (rG > 0)
-        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.Xt), dA, dA, rG, at<float>(ctx, lp.sG), nullptr, lam + 0, 0};
-    }
-    if (pcb.nprob) {
-      prec_scale_kernel<<<dim3(64, pcb.nprob), 256, 0, st>>>(pcb);
-      LAUNCH_CHECK(ctx);
-    }
-  }
-  prof_end(ctx, st);
   // S5: Y' += U_G Z'
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
@@ -2010,8 +2006,7 @@ bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_fact
   }
   if (count == 0) return BKFAC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static PrecScalBatch psb;
-  static PrecScaleBatch pcb;
+  static thread_local PrecScalBatch psb;
   bkfac_status rs;
   GemmStage gs;
   // scalars (s_A, s_G, lambdas, 1/lambdas) as bkfac_precondition
@@ -2038,37 +2033,20 @@ bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_fact
     const auto& a = args[i];
     const auto& lp = ctx->l[a.layer];
     const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G, n = a.n;
-    if (rG > 0) {
+    if (rG > 0) {   // P_G diag(s_G), the scaling in the epilogue
       GemmProb p = gp(a.G, dG, a.U_G, dG, at<float>(ctx, lp.fPG), n, n, rG, dG, 1.f);
+      p.col_scale = at<float>(ctx, lp.sG);
       gemm_ws(p, at<float>(ctx, lp.fws));
       gs.add(true, false, p, lp.fws_elems);
     }
     if (rA > 0) {
       GemmProb p = gp(a.A, dA, a.U_A, dA, at<float>(ctx, lp.fPA), n, n, rA, dA, 1.f);
+      p.col_scale = at<float>(ctx, lp.sA);
       gemm_ws(p, at<float>(ctx, lp.fws2));
       gs.add(true, false, p, lp.fws_elems);
     }
   }
   if ((rs = run_gemms(ctx, gs, st, "gemm_f2_proj")) != BKFAC_OK) return rs;
-  // P_G(:, j) *= s_G[j], P_A(:, j) *= s_A[j]
-  prof_begin(ctx, "prec_scale", st, 0.0, 0.0);
-  for (int i0 = 0; i0 < count; i0 += PS_MAXP / 2) {
-    const int n = std::min(count - i0, PS_MAXP / 2);
-    pcb.nprob = 0;
-    for (int i = i0; i < i0 + n; ++i) {
-      const auto& a = args[i];
-      const auto& lp = ctx->l[a.layer];
-      if (lp.d.r_G > 0)
-        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.fPG), a.n, a.n, lp.d.r_G, at<float>(ctx, lp.sG), nullptr, nullptr, 0};
-      if (lp.d.r_A > 0)
-        pcb.p[pcb.nprob++] = PrecScaleProb{at<float>(ctx, lp.fPA), a.n, a.n, lp.d.r_A, at<float>(ctx, lp.sA), nullptr, nullptr, 0};
-    }
-    if (pcb.nprob) {
-      prec_scale_kernel<<<dim3(64, pcb.nprob), 256, 0, st>>>(pcb);
-      LAUNCH_CHECK(ctx);
-    }
-  }
-  prof_end(ctx, st);
   // G_b = U_G P_G^T + G / lambda_G, A_b = U_A P_A^T + A / lambda_A (device-scalar beta)
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
@@ -2109,9 +2087,9 @@ bkfac_status bkfac_gemm(int transA, int transB, int M, int N, int K, float alpha
   bkfac_ctx_s tmp;   // launch bookkeeping only; no workspace
   tmp.use_tc = path != BKFAC_GEMM_SIMT;
   if (path == BKFAC_GEMM_TCGEN05_PAIR) tmp.pair_mode = 2;
-  if (tmp.use_tc) {
-    static bool attrs = false;
-    if (!attrs) { attrs = tc_init_attributes(); cudaGetLastError(); }
+  if (tmp.use_tc) {   // once per process (thread-safe static initialisation)
+    static const bool attrs = [] { const bool ok = tc_init_attributes(); cudaGetLastError(); return ok; }();
+    (void)attrs;
   }
   GemmStage gs;
   GemmProb p = gp(A, lda, B, ldb, C, ldc, M, N, K, alpha, C, ldc, beta);

@@ -25,7 +25,33 @@ struct GemmProb {
   int* status;             // if set: ST_NONFINITE is OR-ed in when C0 (beta != 0) holds
                            // inf/NaN -- the tensor core does not propagate NaN reliably, so
                            // inputs are checked where an epilogue reads them anyway
+  // fused epilogue scalings (all optional):
+  //   C(i, j) = alpha * (*alpha_dev) * row_scale[i] * col_scale[j] * (AB)(i, j)
+  //             + beta * C0(i, j) + [i == j < diag_n] diag_a * diag_vec[i]
+  const float* alpha_dev;
+  const float* row_scale;
+  const float* col_scale;
+  const float* diag_vec; float diag_a; int diag_n;
 };
+
+// output multiplier of row i (alpha, device alpha, row scale); the column scale is applied per
+// element by the epilogues
+BKFAC_DEV float gemm_row_alpha(const GemmProb& p, int i) {
+  float a = p.alpha;
+  if (p.alpha_dev) a *= *p.alpha_dev;
+  if (p.row_scale && i < p.M) a *= p.row_scale[i];
+  return a;
+}
+BKFAC_DEV float gemm_out(const GemmProb& p, int i, int j, float ra, float acc, float beta) {
+  float v = (p.col_scale ? ra * p.col_scale[j] : ra) * acc;
+  if (beta != 0.f) {
+    const float c0 = p.C0[i + (long)j * p.ldc0];
+    if (p.status && !isfinite(c0)) atomicOr(p.status, ST_NONFINITE);
+    v += beta * c0;
+  }
+  if (p.diag_vec && i == j && i < p.diag_n) v += p.diag_a * p.diag_vec[i];
+  return v;
+}
 
 constexpr int GEMM_MAXP = 100;
 struct GemmBatch {
@@ -136,13 +162,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const __grid_constant__ 
       for (int ii = 0; ii < 4; ++ii) {
         const int i = row0 + ty * 4 + ii;
         if (i >= p.M) continue;
-        float v = p.alpha * acc[ii][jj];
-        if (beta != 0.f) {
-          const float c0 = p.C0[i + (long)j * p.ldc0];
-          if (p.status && !isfinite(c0)) atomicOr(p.status, ST_NONFINITE);
-          v += beta * c0;
-        }
-        p.C[i + (long)j * p.ldc] = v;
+        p.C[i + (long)j * p.ldc] = gemm_out(p, i, j, gemm_row_alpha(p, i), acc[ii][jj], beta);
       }
     }
   } else {
@@ -171,13 +191,7 @@ __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmBatch b) {
     float acc = 0.f;
     for (int s = 0; s < p.splits; ++s) acc += p.ws[(long)s * total + e];
     const int i = (int)(e % p.M), j = (int)(e / p.M);
-    float v = p.alpha * acc;
-    if (beta != 0.f) {
-      const float c0 = p.C0[i + (long)j * p.ldc0];
-      if (p.status && !isfinite(c0)) atomicOr(p.status, ST_NONFINITE);
-      v += beta * c0;
-    }
-    p.C[i + (long)j * p.ldc] = v;
+    p.C[i + (long)j * p.ldc] = gemm_out(p, i, j, gemm_row_alpha(p, i), acc, beta);
   }
 }
 

@@ -356,14 +356,24 @@ BKFAC_DEV void tc_store_group(const GemmProb& p, const TcTile& x, int g, float (
       c0v[jj] = (rowok && j0 + jj < p.N) ? p.C0[i + (long)(j0 + jj) * p.ldc0] : 0.f;
   }
   // alpha v + beta C0 on pairs (FMUL2 / FFMA2: the same per-element roundings as the scalar
-  // o = alpha v; o += beta c0)
-  const float2 al2 = make_float2(p.alpha, p.alpha), be2 = make_float2(beta, beta);
+  // o = alpha v; o += beta c0); fused scalings (device alpha, row / column scale, diagonal)
+  const float ra = gemm_row_alpha(p, i);
+  const float2 be2 = make_float2(beta, beta);
 #pragma unroll
   for (int jj = 0; jj < 16; jj += 2) {
+    float2 al2 = make_float2(ra, ra);
+    if (p.col_scale) {
+      al2.x *= (j0 + jj < p.N) ? p.col_scale[j0 + jj] : 0.f;
+      al2.y *= (j0 + jj + 1 < p.N) ? p.col_scale[j0 + jj + 1] : 0.f;
+    }
     float2 o = __fmul2_rn(al2, make_float2(v[jj], v[jj + 1]));
     if (beta != 0.f) {
       nonfinite |= !isfinite(c0v[jj]) | !isfinite(c0v[jj + 1]);
       o = __ffma2_rn(be2, make_float2(c0v[jj], c0v[jj + 1]), o);
+    }
+    if (p.diag_vec && i < p.diag_n) {
+      if (i == j0 + jj) o.x += p.diag_a * p.diag_vec[i];
+      if (i == j0 + jj + 1) o.y += p.diag_a * p.diag_vec[i];
     }
     if (rowok && j0 + jj < p.N) p.C[i + (long)(j0 + jj) * p.ldc] = o.x;
     if (rowok && j0 + jj + 1 < p.N) p.C[i + (long)(j0 + jj + 1) * p.ldc] = o.y;
@@ -527,9 +537,7 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
           if (w) {
             w[i + (long)j * p.M] = 0.f;
           } else {
-            float o = 0.f;
-            if (beta != 0.f) o += beta * p.C0[i + (long)j * p.ldc0];
-            p.C[i + (long)j * p.ldc] = o;
+            p.C[i + (long)j * p.ldc] = gemm_out(p, i, j, 0.f, 0.f, beta);
           }
         }
       }

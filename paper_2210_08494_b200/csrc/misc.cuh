@@ -140,30 +140,6 @@ __global__ void prec_scalars_kernel(const __grid_constant__ PrecScalBatch b) {
   }
 }
 
-// Scale rows/cols of small blocks by the preconditioner vectors:
-//   mode 0: Y(:, j) *= s[j] * c            (c = 1/lambda_other read from device)
-//   mode 1: Z(i, j) *= sG[i] * sA[j]
-struct PrecScaleProb {
-  float* Y; int ld; int rows, cols;
-  const float* s_col; const float* s_row; const float* lam_div;
-  int mode;
-};
-struct PrecScaleBatch { int nprob; PrecScaleProb p[PS_MAXP]; };
-
-__global__ void prec_scale_kernel(const __grid_constant__ PrecScaleBatch b) {
-  const PrecScaleProb& p = b.p[blockIdx.y];
-  const long total = (long)p.rows * p.cols;
-  const float inv = p.lam_div ? 1.f / *p.lam_div : 1.f;
-  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
-       e += (long)gridDim.x * blockDim.x) {
-    const int i = (int)(e % p.rows), j = (int)(e / p.rows);
-    float f = p.s_col[j];
-    if (p.mode == 0) f *= inv;
-    else f *= p.s_row[i];
-    p.Y[i + (long)j * p.ld] *= f;
-  }
-}
-
 // ---- Philox4x32-10 Gaussian sketch -------------------------------------
 // Omega (n x l col-major), element e = j*n + i; counter block e/4, word pair by e%4;
 // uniforms (x + 0.5) 2^-32; Box-Muller in fp64; rounded to fp32.
