@@ -59,7 +59,9 @@ inline size_t sbr_panel_smem_bytes(int m) {
 inline size_t sbr_w_smem_bytes() {
   return sizeof(float) * (3 * SBR_B * (SBR_B + 1) + SBR_W_WARPS * 3 * SBR_B * (SBR_B + 1));
 }
-inline size_t sbr_chase_smem_bytes() { return 64 * sizeof(int); }
+inline size_t sbr_chase_smem_bytes() {
+  return sizeof(float) * SBR_CHASE_WARPS * (2 * SBR_B * (SBR_B + 1) + 3 * SBR_B) + 64 * sizeof(int);
+}
 
 // ---------------------------------------------------------------------- stage 1: panel QR
 // grid (nprob), block SBR_PANEL_THREADS; panel j of every problem that has one.
@@ -318,6 +320,11 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
   extern __shared__ __align__(16) float csm[];
   volatile int* prog = reinterpret_cast<volatile int*>(csm);      // 64 ints
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* Dt = csm + 64 + warp * (2 * B * LDT + 3 * B);
+  float* Et = Dt + B * LDT;
+  float* vs = Et + B * LDT;
+  float* ws = vs + B;
+  float* us = ws + B;
   float* AB = p.AB;
   const float* K = p.K;
   // band of the stage-1 result (lower, bandwidth B) + zeroed bulge space
@@ -332,7 +339,7 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
 #endif
   auto at = [&](int r, int c) -> float* { return AB + (long)c * LDB + (r - c); };
   for (int j = warp; j < m - 2; j += NW) {
-    float tau_u = 0.f, ureg = 0.f;   // the sweep's previous reflector (lane: component)
+    float tau_u = 0.f;
     for (int k = 0;; ++k) {
       const int s = j + 1 + k * B;
       if (s >= m) break;
@@ -362,24 +369,16 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
       }
       float x;
       CH_T(t2);
-      // Lane = row of the task's blocks; broadcasts by shuffles, column sums by the 31-shuffle
-      // transpose-reduce: no shared-memory round trips on the task's critical path.
-      float bc[B];   // a broadcast vector: u, then v (D part)
       if (k == 0) {
         x = er[0];
       } else {
-        // E <- E H_{k-1}: t_i = tau_u sum_l E(i, l) u_l
+        // E <- E H_{k-1}
+        float t0 = 0.f, t1 = 0.f;
 #pragma unroll
-        for (int l = 0; l < B; ++l) bc[l] = __shfl_sync(0xffffffffu, ureg, l);
-        float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+        for (int l = 0; l < B; l += 2) { t0 = fmaf(er[l], us[l], t0); t1 = fmaf(er[l + 1], us[l + 1], t1); }
+        const float t = (t0 + t1) * tau_u;
 #pragma unroll
-        for (int l = 0; l < B; l += 4) {
-          t0 = fmaf(er[l], bc[l], t0); t1 = fmaf(er[l + 1], bc[l + 1], t1);
-          t2 = fmaf(er[l + 2], bc[l + 2], t2); t3 = fmaf(er[l + 3], bc[l + 3], t3);
-        }
-        const float t = ((t0 + t1) + (t2 + t3)) * tau_u;
-#pragma unroll
-        for (int l = 0; l < B; ++l) er[l] = fmaf(-t, bc[l], er[l]);
+        for (int l = 0; l < B; ++l) er[l] = fmaf(-t, us[l], er[l]);
         x = er[0];
       }
       // reflector from x (length nk): annihilates x[1:nk]
@@ -391,57 +390,63 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
         tau = (beta - alpha) / beta;
         v = lane == 0 ? 1.f : (row ? x / (alpha - beta) : 0.f);
       }
+      vs[lane] = v;
       if (k == 0) {
         if (row) sbr_stcg(at(s + lane, j), lane == 0 ? beta : 0.f);
       } else {
-        // E <- H_k E: s_l = sum_i v_i E(i, l) (transpose-reduce: lane l ends with s_l)
-        float tr[B];
+        // E <- H_k E: s_l = sum_i v_i E(i, l) through a shared-memory transpose
 #pragma unroll
-        for (int l = 0; l < B; ++l) tr[l] = v * er[l];
-        const float sl = tau * sbr_transpose_reduce(tr, lane);
+        for (int l = 0; l < B; ++l) Et[lane * LDT + l] = er[l];
+        __syncwarp();
+        float sl0 = 0.f, sl1 = 0.f;
 #pragma unroll
-        for (int l = 1; l < B; ++l) er[l] = fmaf(-v, __shfl_sync(0xffffffffu, sl, l), er[l]);
+        for (int i = 0; i < B; i += 2) {
+          sl0 = fmaf(vs[i], Et[i * LDT + lane], sl0);
+          sl1 = fmaf(vs[i + 1], Et[(i + 1) * LDT + lane], sl1);
+        }
+        ws[lane] = tau * (sl0 + sl1);
+        __syncwarp();
+#pragma unroll
+        for (int l = 1; l < B; ++l) er[l] = fmaf(-v, ws[l], er[l]);
         er[0] = lane == 0 ? beta : 0.f;
         if (row) {
 #pragma unroll
           for (int l = 0; l < B; ++l) sbr_stcg(AB + (long)(s - B + l) * LDB + (B + lane - l), er[l]);
         }
       }
+      __syncwarp();
       CH_T(t3);
       if (tau != 0.f) {
-        // D = A[R_k, R_k] <- H D H:  p = tau D v, w = p - tau/2 (p.v) v, D -= v w^T + w v^T.
-        // (D v)_i = sum_{l <= i} D(i, l) v_l (this lane's lower row) + sum_{l > i} D(l, i) v_l
-        // (column i below the diagonal: lane l's dr[i], gathered by a transpose-reduce)
+        // D = A[R_k, R_k] <- H D H:  p = tau D v, w = p - tau/2 (p.v) v, D -= v w^T + w v^T
 #pragma unroll
-        for (int l = 0; l < B; ++l) bc[l] = __shfl_sync(0xffffffffu, v, l);
-        float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
-#pragma unroll
-        for (int l = 0; l < B; l += 4) {
-          p0 = fmaf(dr[l], bc[l], p0); p1 = fmaf(dr[l + 1], bc[l + 1], p1);
-          p2 = fmaf(dr[l + 2], bc[l + 2], p2); p3 = fmaf(dr[l + 3], bc[l + 3], p3);
+        for (int l = 0; l < B; ++l) {
+          if (l <= lane) {                            // lane writes row lane's lower part and
+            Dt[lane * LDT + l] = dr[l];               // its mirror; padding rows are zero
+            Dt[l * LDT + lane] = dr[l];
+          }
         }
-        float tr[B];
+        __syncwarp();
+        float p0 = 0.f, p1 = 0.f;
 #pragma unroll
-        for (int l = 0; l < B; ++l) tr[l] = (l < lane) ? dr[l] * v : 0.f;
-        const float col = sbr_transpose_reduce(tr, lane);
-        const float pi = tau * (((p0 + p1) + (p2 + p3)) + col);
+        for (int l = 0; l < B; l += 2) {
+          p0 = fmaf(Dt[lane * LDT + l], vs[l], p0);
+          p1 = fmaf(Dt[lane * LDT + l + 1], vs[l + 1], p1);
+        }
+        const float pi = tau * (p0 + p1);
         const float dot = warp_sum(pi * v);
         const float wi = fmaf(-0.5f * tau * dot, v, pi);
+        ws[lane] = wi;
+        __syncwarp();
         if (row) {
 #pragma unroll
-          for (int l = 0; l < B; ++l) {
-            const float wl = __shfl_sync(0xffffffffu, wi, l);
-            if (l <= lane) sbr_stcg(AB + (long)(s + l) * LDB + (lane - l), dr[l] - v * wl - wi * bc[l]);
-          }
-        } else {
-#pragma unroll
-          for (int l = 0; l < B; ++l) (void)__shfl_sync(0xffffffffu, wi, l);
+          for (int l = 0; l < B; ++l)
+            if (l <= lane) sbr_stcg(AB + (long)(s + l) * LDB + (lane - l), dr[l] - v * ws[l] - wi * vs[l]);
         }
       }
       CH_T(t4);
       p.Vq[((long)j * KT + k) * B + lane] = v;
       if (lane == 0) p.tq[(long)j * KT + k] = tau;
-      ureg = v;
+      us[lane] = v;
       tau_u = tau;
       __syncwarp();
       __threadfence_block();
