@@ -177,7 +177,7 @@ def roofline_from_stages(stages, peaks, clocks):
     if not stages:
         return None, []
     # the EA accumulate runs on a side stream beside the tridiagonalisation (library default,
-    # BKFAC_EA_MODE != 1): it is off the step's critical path, so it is not the dominant stage
+    # option BKFAC_OPT_EA_MODE != 1): off the critical path, so it is not the dominant stage
     side = {"gemm_ea"}
     total = sum(s["ms"] for s in stages if s["name"] not in side)
     stages = sorted(stages, key=lambda s: -s["ms"])
@@ -216,10 +216,8 @@ def traffic_lookup(kernel_stage: str, workload: str):
     try:
         with open(path) as f:
             d = json.load(f)
-        if d.get("workload") != workload:
-            return None
-        return d.get(kernel_stage)
-    except (OSError, ValueError):
+        return d.get(workload, {}).get(kernel_stage)
+    except (OSError, ValueError, AttributeError):
         return None
 
 
