@@ -60,6 +60,8 @@ def parse_args():
     ap.add_argument("--phi-crc", type=float, default=0.5, help="n_crc / r of the light correction")
     ap.add_argument("--no-graphs", action="store_true",
                     help="launch every step eagerly instead of replaying CUDA graphs")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="library option NAME=VALUE (bkfac_set_option, e.g. TWO_STAGE=2); tuning runs")
     return ap.parse_args()
 
 
@@ -396,6 +398,10 @@ def run_ours(args, rank, world, local_rank):
                        oversample=cfg.oversample, power_iters=cfg.power_iters,
                        device=local_rank, rank=rank, world=world, full_rank=args.full_rank,
                        correct_every=args.correct_every, phi_crc=args.phi_crc)
+    from paper_2210_08494_b200 import binding as _bd
+    for o in args.opt:
+        name, val = o.split("=")
+        stack.ctx.bkfac_set_option(getattr(_bd, "BKFAC_OPT_" + name.upper()), int(val))
     gather = SlotGather(layers, stack.owned_layers_all, rank, device) if world > 1 and layers else None
     if gather is not None:
         # precondition straight into the send slots; step k's all-gather (buffer set k & 1)
@@ -566,6 +572,8 @@ def run_ours(args, rank, world, local_rank):
             "profiled_pass_ms_per_step": round(ms_prof / args.steps, 4),
             "profiled_pass": ("graph replays with the library's stage events as graph nodes"
                               if use_graphs else "eager launches with stage events")}
+    if args.opt:
+        line["library_options"] = args.opt
     print(json.dumps(line), flush=True)
 
 

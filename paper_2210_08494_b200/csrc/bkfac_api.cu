@@ -631,25 +631,12 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
     sbr_panel_kernel<<<(unsigned)n, SBR_PANEL_THREADS, sbr_panel_smem_bytes(mmax), st>>>(b, j);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
-    // X = A22 V from A22's lower triangle L: X = tril(L) V, then X += tril(L, -1)^T V
-    for (int i = 0; i < n; ++i) {
+    for (int i = 0; i < n; ++i) {     // X = A22 V
       const EigProb& q = b.p[i];
       if (!q.sbr || j >= sbr_panels(q.m)) continue;
       const int r0 = (j + 1) * B, L = q.m - r0;
       float* A22 = q.K + r0 + (long)r0 * q.ldk;
-      GemmProb px = gp(A22, q.ldk, q.Vp + r0, q.m, q.Xp + r0, q.m, L, B, L, 1.f);
-      px.tri = 1;
-      gs.add(false, false, px, 0);
-    }
-    if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_x")) != BKFAC_OK) return rs;
-    for (int i = 0; i < n; ++i) {
-      const EigProb& q = b.p[i];
-      if (!q.sbr || j >= sbr_panels(q.m)) continue;
-      const int r0 = (j + 1) * B, L = q.m - r0;
-      float* A22 = q.K + r0 + (long)r0 * q.ldk;
-      GemmProb px = gp(A22, q.ldk, q.Vp + r0, q.m, q.Xp + r0, q.m, L, B, L, 1.f, q.Xp + r0, q.m, 1.f);
-      px.tri = 2;
-      gs.add(true, false, px, 0);
+      gs.add(false, false, gp(A22, q.ldk, q.Vp + r0, q.m, q.Xp + r0, q.m, L, B, L, 1.f), 0);
     }
     if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_x")) != BKFAC_OK) return rs;
     prof_begin(ctx, "eig_sbr_w", st, pf, 0.0);
@@ -665,7 +652,7 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
       pu.A2 = q.Wp + r0; pu.lda2 = q.m;
       pu.B2 = q.Vp + r0; pu.ldb2 = q.m;
       pu.k1 = B;
-      pu.sym = 2;   // lower tiles only: every consumer reads A22's lower triangle
+      pu.sym = 1;
       gs.add(false, true, pu, 0);
     }
     if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_update")) != BKFAC_OK) return rs;

@@ -32,15 +32,7 @@ struct GemmProb {
   const float* row_scale;
   const float* col_scale;
   const float* diag_vec; float diag_a; int diag_n;
-  // triangular op(A) (one K segment, no split): 1 keeps op(A)(i, k) with k <= i, 2 keeps
-  // k > i (the other entries read as zero; K chunks outside the band of a tile are skipped).
-  // A symmetric matrix stored in its lower triangle L: A V = tril(L) V (tri 1, A = L) +
-  // tril(L, -1)^T V (tri 2, TA, A = L).
-  int tri;
 };
-BKFAC_DEV bool gemm_tri_keep(const GemmProb& p, int i, int k) {
-  return p.tri == 0 || (p.tri == 1 ? k <= i : k > i);
-}
 
 // output multiplier of row i (alpha, device alpha, row scale); the column scale is applied per
 // element by the epilogues
@@ -110,7 +102,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const __grid_constant__ 
       int i, k;
       if (!TA) { i = row0 + (tid & 63); k = k0 + (tid >> 6) + 4 * q; }
       else     { k = k0 + (tid & 15);   i = row0 + (tid >> 4) + 16 * q; }
-      ra[q] = (i < p.M && k < kend && gemm_tri_keep(p, i, k)) ? gemm_a<TA>(p, i, k) : 0.f;
+      ra[q] = (i < p.M && k < kend) ? gemm_a<TA>(p, i, k) : 0.f;
       int j;
       if (!TB) { k = k0 + (tid & 15);   j = col0 + (tid >> 4) + 16 * q; }
       else     { j = col0 + (tid & 63); k = k0 + (tid >> 6) + 4 * q; }

@@ -323,8 +323,6 @@ BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
   const int nc = x.nc1 + (p.K - p.k1 + TC_BK - 1) / TC_BK;
   x.c_beg = min(nc, x.split * p.kchunk);     // kchunk = chunks per split on this path
   x.c_end = min(nc, x.c_beg + p.kchunk);
-  if (p.tri == 1) x.c_end = min(x.c_end, (x.m0 + BMT + TC_BK - 1) / TC_BK);   // k <= i
-  else if (p.tri == 2) x.c_beg = min(x.c_end, max(x.c_beg, x.m0 / TC_BK));    // k > i
   return x;
 }
 
@@ -736,13 +734,9 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
     auto line_src = [&](const GemmProb& p, const float* Ap, const float* Bp, long lda, long ldb,
                         int ks, int klen, int l, int e, bool& ok, bool isA) -> const float* {
       if (isA) {                                   // l < TC_BM (compile-time per quad)
-        if (TA) {
-          const int i = x.m0 + l, k = ks + e;
-          ok = i < p.M && k < klen && gemm_tri_keep(p, i, k);
-          return Ap + k + (long)i * lda;
-        }
+        if (TA) { const int i = x.m0 + l, k = ks + e; ok = i < p.M && k < klen; return Ap + k + (long)i * lda; }
         const int k = ks + (l & 31), i = x.m0 + ((l >> 5) << 5) + e;
-        ok = i < p.M && k < klen && gemm_tri_keep(p, i, k);
+        ok = i < p.M && k < klen;
         return Ap + i + (long)k * lda;
       }
       const int lb = l - TC_BM;

@@ -11,10 +11,9 @@
 //                     below it (geqrf layout: reflector of column k has its unit at row
 //                     k + 32), the explicit unit-lower V into Vp and the compact-WY factor T
 //                     (Q = I - V T V^T, dlarft recurrence) into Tp.
-//   GEMM  X = A22 V                 (A22 = K[r0:, r0:] held as its lower triangle L:
-//                                    X = tril(L) V + tril(L, -1)^T V, two triangular GEMMs)
+//   GEMM  X = A22 V                 (A22 = K[r0:, r0:], full symmetric storage; tcgen05)
 //   sbr_w_kernel      Y = X T,  W = Y - 1/2 V (T^T (V^T Y))
-//   GEMM  A22 -= V W^T + W V^T      (lower tiles only; tcgen05)
+//   GEMM  A22 -= V W^T + W V^T      (symmetric: lower tiles computed and mirrored; tcgen05)
 // which is the two-sided block update Q^T A22 Q = A22 - V W^T - W V^T.  All O(m^3) work of
 // the reduction is in the two GEMMs per panel: m / 32 synchronisation points instead of m.
 //

@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--runs", type=int, default=5)
     ap.add_argument("--burn-in", type=int, default=60)
     ap.add_argument("--window", type=int, default=30)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_f4_error_protocol.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_f4_error_protocol.json"))
     args = ap.parse_args()
     import torch
     import synth
