@@ -829,7 +829,12 @@ bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
         for (size_t i = 0; i < n; ++i)
           if (b.p[i].sbr) q2f += 2.0 * (double)b.p[i].m * b.p[i].m * b.p[i].r;
         prof_begin(ctx, "eig_sbr_q2", st, q2f, 0.0);
-        sbr_q2_kernel<<<dim3((unsigned)n, (unsigned)ceil_div(rmax, SBR_Q2_THREADS)), SBR_Q2_THREADS, 0, st>>>(b);
+        int nsbr = 0;
+        for (size_t i = 0; i < n; ++i) nsbr += b.p[i].sbr != 0;
+        if ((long)nsbr * ceil_div(rmax, SBR_Q2_THREADS) >= kNumSM)
+          sbr_q2_kernel<SBR_Q2_THREADS><<<dim3((unsigned)n, (unsigned)ceil_div(rmax, SBR_Q2_THREADS)), SBR_Q2_THREADS, 0, st>>>(b);
+        else
+          sbr_q2_kernel<32><<<dim3((unsigned)n, (unsigned)ceil_div(rmax, 32)), 32, 0, st>>>(b);
         LAUNCH_CHECK(ctx);
         prof_end(ctx, st);
       }

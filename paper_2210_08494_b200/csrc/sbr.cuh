@@ -481,13 +481,16 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
 // the column in steps of 32 rows: rows leaving the window are stored, the next 32 rows are
 // loaded before the current diamond is applied (they are not touched by it), so each group
 // streams the column through registers once.
+// NT = 128 columns per CTA; with few factors per launch (an 8-GPU rank's 12) 32-column CTAs
+// spread the same per-column work over more SMs (the arithmetic of a column is unchanged)
 constexpr int SBR_Q2_THREADS = 128;
-__global__ void __launch_bounds__(SBR_Q2_THREADS, 3)
+template <int NT>
+__global__ void __launch_bounds__(NT, 384 / NT)
 sbr_q2_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   if (p.sbr == 0) return;
   const int m = p.m, r = p.r;
-  constexpr int B = SBR_B, G = SBR_G, NT = SBR_Q2_THREADS, WIN = B + G - 1;
+  constexpr int B = SBR_B, G = SBR_G, WIN = B + G - 1;
   static_assert(G == B, "the window slides by one task (B rows) and holds G - 1 = B - 1 carried rows");
   const int KT = sbr_tasks(m);
   const int c = blockIdx.y * NT + threadIdx.x;
