@@ -296,10 +296,13 @@ sbr_w_kernel(const __grid_constant__ EigBatch b, int j) {
 }
 
 // ---------------------------------------------------------------------- stage 2: chase
-#ifdef BKFAC_CHASE_TIMING
-__device__ unsigned long long g_chase_dbg[8];   // tuning builds: phase cycle sums (all warps)
+#if defined(BKFAC_CHASE_TIMING) || defined(BKFAC_Q2_TIMING)
+__device__ unsigned long long g_chase_dbg[8];   // tuning builds: phase cycle sums
 #define CH_T(v) const unsigned long long v = clock64()
 #define CH_ACC(i, a, b) atomicAdd(&g_chase_dbg[i], (b) - (a))
+#elif defined(BKFAC_Q2_TIMING)
+#define CH_T(v) const unsigned long long v = clock64()
+#define CH_ACC(i, a, b)
 #else
 #define CH_T(v)
 #define CH_ACC(i, a, b)
@@ -510,11 +513,15 @@ sbr_q2_kernel(const __grid_constant__ EigBatch b) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
   };
+  auto cp16 = [](float* dst, const float* src, bool ok) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+  };
   auto stage = [&](int q, int j0, int jn, int k) {
-    for (int e = threadIdx.x; e < G * B; e += NT) {
-      const int a = e / B, i = e % B;
+    for (int e = threadIdx.x; e < G * B / 4; e += NT) {   // 16-byte pieces of the reflectors
+      const int a = e / (B / 4), i = (e % (B / 4)) * 4;
       const bool ex = a < jn && j0 + a + 1 + k * B < m;
-      cp4(&vsm[q][e], ex ? p.Vq + ((long)(j0 + a) * KT + k) * B + i : p.Vq, ex);
+      cp16(&vsm[q][a * B + i], ex ? p.Vq + ((long)(j0 + a) * KT + k) * B + i : p.Vq, ex);
     }
     for (int a = threadIdx.x; a < G; a += NT) {
       const bool ex = a < jn && j0 + a + 1 + k * B < m;
@@ -535,43 +542,83 @@ sbr_q2_kernel(const __grid_constant__ EigBatch b) {
 #pragma unroll
     for (int t = 0; t < WIN; ++t) w[t] = (cok && rb + t < m) ? Z[(long)(rb + t) * r] : 0.f;
     for (int k = 0; rb < m; ++k, rb += B) {
+      CH_T(q0);
       stage_wait();      // this thread's copies into buffer q have landed
       __syncthreads();   // buffer q staged by every thread; buffer q ^ 1 free
+      CH_T(q1);
       if (rb + B < m) stage(q ^ 1, j0, jn, k + 1);
       // next diamond's new rows (rb + WIN .. rb + WIN + B - 1): untouched by this diamond
+      // (running pointer laundered through asm: no 64-bit multiply per row)
       float nx[B];
+      {
+        const float* zp;
+        int rl;
+        asm volatile("mov.b64 %0, %1;" : "=l"(zp) : "l"(Z + (long)(rb + WIN) * r));
+        asm volatile("mov.b32 %0, %1;" : "=r"(rl) : "r"(r));
+        const int nn = cok ? m - (rb + WIN) : 0;
 #pragma unroll
-      for (int t = 0; t < B; ++t) {
-        const int row = rb + WIN + t;
-        nx[t] = (cok && row < m) ? Z[(long)row * r] : 0.f;
+        for (int t = 0; t < B; ++t) {
+          nx[t] = t < nn ? *zp : 0.f;
+          zp += rl;
+        }
       }
+      CH_T(q2);
       // the diamond's block reflector H_{j0} H_{j0+1} ... H_{j0+G-1}: applied last first
       const float* vq = vsm[q];
+      // reflector a's vector is loaded while reflector a + 1 is applied (two register sets;
+      // the compiler barrier keeps it from hoisting every reflector's loads)
+      float vc[B], vn[B];
+      float tc = tsm[q][G - 1], tn = 0.f;
+#pragma unroll
+      for (int i = 0; i < B; i += 4) {
+        const float4 f4 = *reinterpret_cast<const float4*>(&vq[(G - 1) * B + i]);
+        vc[i] = f4.x; vc[i + 1] = f4.y; vc[i + 2] = f4.z; vc[i + 3] = f4.w;
+      }
 #pragma unroll
       for (int a = G - 1; a >= 0; --a) {
         asm volatile("" ::: "memory");
-        float v[B];
+        if (a > 0) {
 #pragma unroll
-        for (int i = 0; i < B; i += 4) {
-          const float4 f4 = *reinterpret_cast<const float4*>(&vq[a * B + i]);
-          v[i] = f4.x; v[i + 1] = f4.y; v[i + 2] = f4.z; v[i + 3] = f4.w;
+          for (int i = 0; i < B; i += 4) {
+            const float4 f4 = *reinterpret_cast<const float4*>(&vq[(a - 1) * B + i]);
+            vn[i] = f4.x; vn[i + 1] = f4.y; vn[i + 2] = f4.z; vn[i + 3] = f4.w;
+          }
+          tn = tsm[q][a - 1];
         }
-        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+        float dd[8];
 #pragma unroll
-        for (int i = 0; i < B; i += 4) {
-          d0 = fmaf(v[i], w[a + i], d0);
-          d1 = fmaf(v[i + 1], w[a + i + 1], d1);
-          d2 = fmaf(v[i + 2], w[a + i + 2], d2);
-          d3 = fmaf(v[i + 3], w[a + i + 3], d3);
-        }
-        const float d = ((d0 + d1) + (d2 + d3)) * tsm[q][a];
+        for (int u = 0; u < 8; ++u) dd[u] = 0.f;
 #pragma unroll
-        for (int i = 0; i < B; ++i) w[a + i] = fmaf(-d, v[i], w[a + i]);
+        for (int i = 0; i < B; ++i) dd[i & 7] = fmaf(vc[i], w[a + i], dd[i & 7]);
+        const float d = (((dd[0] + dd[1]) + (dd[2] + dd[3])) + ((dd[4] + dd[5]) + (dd[6] + dd[7]))) * tc;
+#pragma unroll
+        for (int i = 0; i < B; ++i) w[a + i] = fmaf(-d, vc[i], w[a + i]);
+#pragma unroll
+        for (int i = 0; i < B; ++i) vc[i] = vn[i];
+        tc = tn;
       }
+      CH_T(q3);
       // rows rb .. rb + B - 1 leave the window; slide by B
+      {
+        float* zp;
+        int rl;
+        asm volatile("mov.b64 %0, %1;" : "=l"(zp) : "l"(Z + (long)rb * r));
+        asm volatile("mov.b32 %0, %1;" : "=r"(rl) : "r"(r));
+        const int nn = cok ? m - rb : 0;
 #pragma unroll
-      for (int t = 0; t < B; ++t)
-        if (cok && rb + t < m) Z[(long)(rb + t) * r] = w[t];
+        for (int t = 0; t < B; ++t) {
+          if (t < nn) *zp = w[t];
+          zp += rl;
+        }
+      }
+#ifdef BKFAC_Q2_TIMING
+      if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+        const unsigned long long q4 = clock64();
+        atomicAdd(&g_chase_dbg[0], q1 - q0); atomicAdd(&g_chase_dbg[1], q2 - q1);
+        atomicAdd(&g_chase_dbg[2], q3 - q2); atomicAdd(&g_chase_dbg[3], q4 - q3);
+        atomicAdd(&g_chase_dbg[5], 1ull);
+      }
+#endif
 #pragma unroll
       for (int t = 0; t < WIN - B; ++t) w[t] = w[t + B];
 #pragma unroll

@@ -181,6 +181,12 @@ def cfg5_rank_of_8() -> StackConfig:
     return dataclasses.replace(c, name="cfg5_transformer_rank_of_8")
 
 
+def cfg5_rank_of(world: int) -> StackConfig:
+    """One rank's share of configs[4] at `world` GPUs (24 / world of the identical blocks)."""
+    c = cfg5_transformer(blocks=24 // world)
+    return dataclasses.replace(c, name=f"cfg5_transformer_rank_of_{world}")
+
+
 CONFIGS = {
     "cfg1": cfg1_toy,
     "cfg2": cfg2_conv,
@@ -188,6 +194,8 @@ CONFIGS = {
     "cfg4": cfg4_vgg_sharded,
     "cfg5": cfg5_transformer,
     "cfg5r8": cfg5_rank_of_8,
+    "cfg5r4": lambda: cfg5_rank_of(4),
+    "cfg5r2": lambda: cfg5_rank_of(2),
 }
 
 

@@ -20,5 +20,5 @@ lib.bkfac_debug_chase(buf, 1)
 ctx.bkfac_brand_update(items); torch.cuda.synchronize()
 lib.bkfac_debug_chase(buf, 0)
 v = list(buf); nt = max(v[5], 1)
-names = ["wait", "loads", "E part", "D part", "publish"]
+names = ["wait", "loads", "E part", "D part", "publish"] if len(sys.argv) < 2 else ["wait+sync", "stage+nx issue", "compute", "store+shift"]
 print("tasks", nt, "kernel cycles", v[6], "per task:", {nm: round(v[i] / nt) for i, nm in enumerate(names)})
