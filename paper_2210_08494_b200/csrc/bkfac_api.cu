@@ -667,7 +667,21 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
   return BKFAC_OK;
 }
 
+// Auto mode (BKFAC_OPT_TWO_STAGE = 0): the two-stage reduction pays off when many large
+// cores share the launch (its chase and back-transform are per-factor latency chains, the
+// one-stage global-tile kernel is HBM-bound with one CTA per factor); with few (an 8-GPU
+// rank's share) the one-stage kernel on clusters of up to 8 CTAs per factor is faster.
+// Measured on one B200, ms per step of one rank's share of configs[4] (two-stage / one-stage):
+// 96 factors 264 / >300, 48: 147 / 171, 24: 91.4 / 91.3, 12: 66.3 / 46.5.
+constexpr int SBR_AUTO_MIN_FACTORS = 25;
+
 bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
+  if (ctx->two_stage == 0) {
+    int nbig = 0;
+    for (auto& q : v) nbig += q.sbr != 0;
+    if (nbig > 0 && nbig < SBR_AUTO_MIN_FACTORS)
+      for (auto& q : v) { q.sbr = 0; q.off = 1; }
+  }
   size_t i0 = 0;
   static thread_local EigBatch b;
   while (i0 < v.size()) {
