@@ -264,17 +264,21 @@ def test_cfg2_chain_50_steps(cuda_lib):
           f"max |U^T U - I| {drift:.2e}")
 
 
+@pytest.mark.parametrize("two_stage", [0, 2])
 @pytest.mark.parametrize("n", [4097, 16385, 4096])
-def test_cfg5_factor_chain_20_steps(cuda_lib, n):
+def test_cfg5_factor_chain_20_steps(cuda_lib, n, two_stage):
     """BASELINE configs[4] factor shapes (c = 1024, r = 512, rho = 0.97, core m = 1536,
     global-tile tridiagonalisation): 20 chained B-process steps (Eq.(10))
     on the GPU against the oracle's own chain (SURVEY §8(c) c3's sampling of config 5):
-    reconstruction <= 1e-3 and eigenvalues <= 1e-4 normwise at every step."""
+    reconstruction <= 1e-3 and eigenvalues <= 1e-4 normwise at every step.  two_stage = 0:
+    the auto choice for one factor (one-stage kernel on a CTA cluster); 2: the two-stage
+    reduction that bench.py's 96-factor launches take."""
     import torch
-    from paper_2210_08494_b200 import BKFACStack
+    from paper_2210_08494_b200 import BKFACStack, binding
     cfg = synth.cfg5_transformer(blocks=1)
     f = next(x for x in cfg.factors if x.n == n)
     st = BKFACStack([(f.n, f.r, f.c)], [], cfg.rho, cfg.lam)
+    st.ctx.bkfac_set_option(binding.BKFAC_OPT_TWO_STAGE, two_stage)
     chain = O.FactorChain(f.n, f.r, cfg.rho)
     worst, worst_eig = 0.0, 0.0
     Mdev = torch.empty((f.c, f.n), device="cuda")
@@ -761,15 +765,17 @@ def test_cfg4_stack_bench_launch_config_sampled(cuda_lib):
 
 def test_cfg5_block_stack_bench_launch_config_sampled(cuda_lib):
     """configs[4]'s factor and layer shapes (one transformer block: 4097 -> 16384 and
-    16385 -> 4096; n_BS = 1024, r = 512; global-tile tridiagonalisation of the 1536 cores)
-    through the stack in bench.py's launch configuration (graph replay after the first
-    step), 3 steps; every factor and both preconditioned gradients against the oracle."""
+    16385 -> 4096; n_BS = 1024, r = 512; the two-stage reduction of the 1536 cores that the
+    96-factor bench launches take) through the stack in bench.py's launch configuration (graph
+    replay after the first step), 3 steps; every factor and both preconditioned gradients
+    against the oracle."""
     import torch
-    from paper_2210_08494_b200 import BKFACStack
+    from paper_2210_08494_b200 import BKFACStack, binding
     cfg = synth.cfg5_transformer(blocks=1, steps=3)
     factors = [(f.n, f.r, f.c) for f in cfg.factors]
     layers = [(L.d_G, L.d_A, L.g_index, L.a_index) for L in cfg.layers]
     st = BKFACStack(factors, layers, cfg.rho, cfg.lam)
+    st.ctx.bkfac_set_option(binding.BKFAC_OPT_TWO_STAGE, 2)
     Mbuf = {g: torch.empty((f.c, f.n), device="cuda") for g, f in enumerate(cfg.factors)}
     Jbuf = {li: torch.empty((L.d_G, L.d_A), device="cuda") for li, L in enumerate(cfg.layers)}
     states = [None] * len(factors)
