@@ -375,13 +375,19 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
       if (k == 0) {
         x = er[0];
       } else {
-        // E <- E H_{k-1}
-        float t0 = 0.f, t1 = 0.f;
+        // E <- E H_{k-1} (u broadcast as float4 loads)
+        float ub[B];
 #pragma unroll
-        for (int l = 0; l < B; l += 2) { t0 = fmaf(er[l], us[l], t0); t1 = fmaf(er[l + 1], us[l + 1], t1); }
-        const float t = (t0 + t1) * tau_u;
+        for (int l = 0; l < B; l += 4) {
+          const float4 f4 = *reinterpret_cast<const float4*>(&us[l]);
+          ub[l] = f4.x; ub[l + 1] = f4.y; ub[l + 2] = f4.z; ub[l + 3] = f4.w;
+        }
+        float tt[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int l = 0; l < B; ++l) er[l] = fmaf(-t, us[l], er[l]);
+        for (int l = 0; l < B; ++l) tt[l & 3] = fmaf(er[l], ub[l], tt[l & 3]);
+        const float t = ((tt[0] + tt[1]) + (tt[2] + tt[3])) * tau_u;
+#pragma unroll
+        for (int l = 0; l < B; ++l) er[l] = fmaf(-t, ub[l], er[l]);
         x = er[0];
       }
       // reflector from x (length nk): annihilates x[1:nk]
@@ -401,16 +407,25 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
 #pragma unroll
         for (int l = 0; l < B; ++l) Et[lane * LDT + l] = er[l];
         __syncwarp();
-        float sl0 = 0.f, sl1 = 0.f;
+        float sl[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int i = 0; i < B; i += 2) {
-          sl0 = fmaf(vs[i], Et[i * LDT + lane], sl0);
-          sl1 = fmaf(vs[i + 1], Et[(i + 1) * LDT + lane], sl1);
+        for (int i = 0; i < B; i += 4) {
+          const float4 v4 = *reinterpret_cast<const float4*>(&vs[i]);
+          sl[0] = fmaf(v4.x, Et[i * LDT + lane], sl[0]);
+          sl[1] = fmaf(v4.y, Et[(i + 1) * LDT + lane], sl[1]);
+          sl[2] = fmaf(v4.z, Et[(i + 2) * LDT + lane], sl[2]);
+          sl[3] = fmaf(v4.w, Et[(i + 3) * LDT + lane], sl[3]);
         }
-        ws[lane] = tau * (sl0 + sl1);
+        ws[lane] = tau * ((sl[0] + sl[1]) + (sl[2] + sl[3]));
         __syncwarp();
 #pragma unroll
-        for (int l = 1; l < B; ++l) er[l] = fmaf(-v, ws[l], er[l]);
+        for (int l = 0; l < B; l += 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(&ws[l]);
+          if (l > 0) er[l] = fmaf(-v, w4.x, er[l]);
+          er[l + 1] = fmaf(-v, w4.y, er[l + 1]);
+          er[l + 2] = fmaf(-v, w4.z, er[l + 2]);
+          er[l + 3] = fmaf(-v, w4.w, er[l + 3]);
+        }
         er[0] = lane == 0 ? beta : 0.f;
         if (row) {
 #pragma unroll
@@ -421,29 +436,38 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
       CH_T(t3);
       if (tau != 0.f) {
         // D = A[R_k, R_k] <- H D H:  p = tau D v, w = p - tau/2 (p.v) v, D -= v w^T + w v^T
+        // (D v)_i = sum_{l <= i} D(i, l) v_l (this lane's lower row, registers) + sum_{l > i}
+        // D(l, i) v_l (column i below the diagonal: lane l's row, through shared memory)
 #pragma unroll
-        for (int l = 0; l < B; ++l) {
-          if (l <= lane) {                            // lane writes row lane's lower part and
-            Dt[lane * LDT + l] = dr[l];               // its mirror; padding rows are zero
-            Dt[l * LDT + lane] = dr[l];
-          }
+        for (int l = 0; l < B; ++l) Dt[lane * LDT + l] = dr[l];   // row lane (zeros above the diagonal)
+        float vb[B];
+#pragma unroll
+        for (int l = 0; l < B; l += 4) {
+          const float4 f4 = *reinterpret_cast<const float4*>(&vs[l]);
+          vb[l] = f4.x; vb[l + 1] = f4.y; vb[l + 2] = f4.z; vb[l + 3] = f4.w;
         }
         __syncwarp();
-        float p0 = 0.f, p1 = 0.f;
+        float pp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int l = 0; l < B; l += 2) {
-          p0 = fmaf(Dt[lane * LDT + l], vs[l], p0);
-          p1 = fmaf(Dt[lane * LDT + l + 1], vs[l + 1], p1);
+        for (int l = 0; l < B; ++l) {
+          const float col = (l > lane) ? Dt[l * LDT + lane] : dr[l];
+          pp[l & 3] = fmaf(col, vb[l], pp[l & 3]);
         }
-        const float pi = tau * (p0 + p1);
+        const float pi = tau * ((pp[0] + pp[1]) + (pp[2] + pp[3]));
         const float dot = warp_sum(pi * v);
         const float wi = fmaf(-0.5f * tau * dot, v, pi);
         ws[lane] = wi;
         __syncwarp();
         if (row) {
 #pragma unroll
-          for (int l = 0; l < B; ++l)
-            if (l <= lane) sbr_stcg(AB + (long)(s + l) * LDB + (lane - l), dr[l] - v * ws[l] - wi * vs[l]);
+          for (int l = 0; l < B; l += 4) {
+            const float4 w4 = *reinterpret_cast<const float4*>(&ws[l]);
+            const float wl[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (l + u <= lane)
+                sbr_stcg(AB + (long)(s + l + u) * LDB + (lane - l - u), dr[l + u] - v * wl[u] - wi * vb[l + u]);
+          }
         }
       }
       CH_T(t4);
