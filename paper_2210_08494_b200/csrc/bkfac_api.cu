@@ -84,7 +84,7 @@ struct FactorPlan {
   int nld = 0;         // leading dimension of the internal n-row buffers (R, Qb, Urot): n
                        // rounded up to 32, so their GEMM loads take the 16-byte vector path
   // Brand path
-  size_t W, P2, R, Qb, G, L1, L1i, L2, L2i, cscr, ws;
+  size_t W, P2, R, Qb, G, L1, L1i, L2, L2i, cscr, ws, Vf = 0;
   size_t Ms = 0, Us = 0;   // aligned copies (ld nld) of the caller's M and U_in (odd n only)
   size_t ws_elems = 0;
   // dense path
@@ -299,7 +299,8 @@ bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char*
   double flops = 0.0, bytes = 0.0;
   for (int v = 0; v < 4; ++v)
     for (auto& p : s.probs[v]) {
-      flops += 2.0 * p.M * (double)p.N * p.K;
+      // a symmetric product's algorithmic work is its lower triangle
+      flops += (p.sym && p.M == p.N ? (double)p.M * (p.N + 1) : 2.0 * p.M * (double)p.N) * p.K;
       bytes += 4.0 * ((double)p.M * p.K + (double)p.K * p.N + (double)p.M * p.N *
                       ((p.beta != 0.f || p.beta_dev) ? 2.0 : 1.0));
     }
@@ -320,9 +321,17 @@ bkfac_status run_gemms(bkfac_ctx ctx, GemmStage& s, cudaStream_t st, const char*
 //     supplied a workspace.
 constexpr int TC_SPLIT_CHUNKS = 128;
 bool tc_pair_tiles(const bkfac_ctx ctx, const GemmProb& p) {
-  if (p.sym || ctx->pair_mode == 0) return false;
-  if (ctx->pair_mode == 2) return true;
+  if (p.sym == 2 || ctx->pair_mode == 0) return false;
   const int nc = ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK);
+  // a symmetric problem takes pair tiles only where it will be split (the split-K reduce
+  // writes its mirrored upper tiles; the pair epilogue has no mirrored store)
+  if (p.sym) {
+    const long t2 = (long)ceil_div(p.M, 2 * TC_BM) * ceil_div(p.N, TC_BN_PAIR);
+    if (p.M != p.N || TC_BN_PAIR != 2 * TC_BM || p.ws == nullptr || nc <= TC_SPLIT_CHUNKS ||
+        t2 >= kNumSM)
+      return false;
+  }
+  if (ctx->pair_mode == 2) return true;
   return nc > TC_SHORT_K_CHUNKS && p.M >= 512 && p.N >= 256;
 }
 
@@ -340,7 +349,11 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
         p.tiles_m = ceil_div(std::max(p.M, 1), bm);
         p.tiles_n = ceil_div(std::max(p.N, 1), bn);
         if (p.M <= 0 || p.N <= 0) p.tiles_m = p.tiles_n = 0;
-        if (p.M != p.N || bm != bn || pair) p.sym = 0;   // mirrored tiles: square 128 x 128 only
+        if (p.M != p.N || bm != bn) p.sym = 0;   // lower tiles of square tiles only
+        p.tbm = bm;
+        // walk the tiles along the smaller operand: A (M x K) re-read per column block when
+        // M is walked first, B (K x N) per row block otherwise
+        p.nfast = (!p.sym && p.M > p.N) ? 1 : 0;
         auto al = [](const float* q, int ld) {
           return q == nullptr || ((reinterpret_cast<uintptr_t>(q) & 15) == 0 && (ld & 3) == 0);
         };
@@ -350,7 +363,7 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
         const int nc = ceil_div(std::max(p.k1, 0), TC_BK) + ceil_div(std::max(p.K - p.k1, 0), TC_BK);
         int splits = 1;
         const long own_tiles = (long)p.tiles_m * p.tiles_n;   // the problem alone fills the GPU?
-        if (nc > TC_SPLIT_CHUNKS && own_tiles < kNumSM && p.ws != nullptr && !p.sym) {
+        if (nc > TC_SPLIT_CHUNKS && own_tiles < kNumSM && p.ws != nullptr) {
           splits = std::min(kSplitMax, ceil_div(nc, TC_SPLIT_CHUNKS));
           splits = (int)std::min<long>(splits, cap);
           splits = std::max(splits, 1);
@@ -358,6 +371,9 @@ bkfac_status run_gemms_impl(bkfac_ctx ctx, GemmStage& s, cudaStream_t st) {
         const int cps = std::max(ceil_div(nc, splits), 1);
         p.splits = std::max(ceil_div(nc, cps), 1);
         p.kchunk = cps;
+        // symmetric problems: the split-K reduce mirrors (or skips) the upper tiles; without
+        // split-K only the 128 x 128 epilogue has the mirrored store
+        if (pair && p.splits == 1) p.sym = 0;
         if (pair) { ps.probs[v].push_back(p); ps.caps[v].push_back(s.caps[v][i]); }
         else { keep.push_back(p); keepc.push_back(s.caps[v][i]); }
       }
@@ -1030,6 +1046,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
       const size_t cc = sizeof(float) * (size_t)cm * cm;
       fp.G = a.take(cc); fp.L1 = a.take(cc); fp.L1i = a.take(cc); fp.L2 = a.take(cc); fp.L2i = a.take(cc);
       fp.cscr = a.take(sizeof(float) * chol_tiled_scratch_floats(cm));
+      fp.Vf = a.take(sizeof(float) * (size_t)cm * ro);
       fp.ws_elems = (long)kSplitMax * std::max(r, cm) * (long)cm;
       fp.ws = a.take(sizeof(float) * fp.ws_elems);
       plan_eig(a, fp.eig, m, ro);
@@ -1440,6 +1457,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         const int n = fp.d.n, c = a.c;
         const float* X = at<float>(ctx, pass == 0 ? fp.R : fp.Qb);
         GemmProb p = gp(X, fp.nld, X, fp.nld, at<float>(ctx, fp.G), c, c, c, n, 1.f);
+        p.sym = 1;   // Gram: lower tiles computed, the upper mirrored
         gemm_ws(p, at<float>(ctx, fp.ws));
         gs.add(true, false, p, fp.ws_elems);
       }
@@ -1453,6 +1471,10 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
                                pass == 0 ? (float)a.c * 1.1920929e-7f : 0.f));
       }
       STAGE(run_chol(ctx, ch, st));
+      // pass 1's product Q = Q1 L2^{-T} is never formed: the rotation takes Q1 with the
+      // eigenvector rows folded by L2^{-T} (gemm_qfold below), one c x c x r_out product
+      // instead of n x c x c
+      if (pass == 1) break;
       for (int i : brand) {
         const auto& a = args[i];
         const auto& fp = ctx->f[a.factor];
@@ -1494,7 +1516,16 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     }
   }
   STAGE(run_eig(ctx, eg, st));
-  // rotation: U_out = [U Q] V
+  // fold: V_Q = L2^{-T} V[r:r+c, :]  (so that Q V[r:, :] = Q1 V_Q with Q = Q1 L2^{-T})
+  for (int i : brand) {
+    const auto& a = args[i];
+    const auto& fp = ctx->f[a.factor];
+    const int r = fp.d.r, c = a.c, mm = r + c, ro = rout_of(a);
+    gs.add(true, false, gp(at<float>(ctx, fp.L2i), c, at<float>(ctx, fp.eig.V) + r, mm,
+                           at<float>(ctx, fp.Vf), c, c, ro, c, 1.f), 0);
+  }
+  if (!brand.empty()) STAGE(run("gemm_qfold"));
+  // rotation: U_out = [U Q] V = U V[0:r, :] + Q1 V_Q
   for (int i : brand) {
     const auto& a = args[i];
     const auto& fp = ctx->f[a.factor];
@@ -1502,8 +1533,8 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const float* V = at<float>(ctx, fp.eig.V);
     const float* U0 = fp.Us ? at<float>(ctx, fp.Us) : a.U_in;
     GemmProb p = gp(U0, fp.Us ? fp.nld : n, V, mm, at<float>(ctx, fp.Urot), fp.nld, n, ro, mm, 1.f);
-    p.A2 = at<float>(ctx, fp.R); p.lda2 = fp.nld;
-    p.B2 = V + r; p.ldb2 = mm;
+    p.A2 = at<float>(ctx, fp.Qb); p.lda2 = fp.nld;
+    p.B2 = at<float>(ctx, fp.Vf); p.ldb2 = a.c;
     p.k1 = r;
     gs.add(false, false, p, 0);
   }
@@ -1519,6 +1550,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const int n = fp.d.n, r = rout_of(a);
     const float* Ur = at<float>(ctx, fp.Urot);
     GemmProb p = gp(Ur, fp.nld, Ur, fp.nld, at<float>(ctx, fp.Gref), r, r, r, n, 1.f);
+    p.sym = 1;
     gemm_ws(p, at<float>(ctx, fp.wsr));
     gs.add(true, false, p, fp.wsr_elems);
   }
@@ -2000,6 +2032,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     p.B2 = a.U_G ? a.U_G : at<float>(ctx, lp.Y); p.ldb2 = dG;
     p.k1 = rA;
     p.beta_dev = lam + 2;
+    p.stream_c = 1;   // J read and S written once: evict-first, the operands stay in L2
     p.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);   // every element of J passes here
     gs.add(false, true, p, 0);
   }

@@ -21,6 +21,10 @@ struct GemmProb {
   int splits, kchunk, tiles_m, tiles_n, tile_start;
   int sym;                 // tcgen05 path: 1: C = C^T known (e.g. M M^T): lower tiles only, mirrored;
                            // 2: lower tiles only, the upper triangle beyond them left untouched
+  int tbm;                 // tcgen05 path: square tile edge of a symmetric problem (split-K reduce)
+  int nfast;               // tcgen05 path: consecutive tiles walk N first (A row blocks read
+                           // once, B re-read from L2) instead of M first
+  int stream_c;            // C0 read / C written once (evict-first: keeps the operands in L2)
   int vec;                 // tcgen05 path: bit 0 A (and A2), bit 1 B (and B2) 16-byte aligned
   int* status;             // if set: ST_NONFINITE is OR-ed in when C0 (beta != 0) holds
                            // inf/NaN -- the tensor core does not propagate NaN reliably, so
@@ -188,9 +192,14 @@ __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmBatch b) {
   const float beta = p.beta_dev ? *p.beta_dev : p.beta;
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
        e += (long)gridDim.x * blockDim.x) {
-    float acc = 0.f;
-    for (int s = 0; s < p.splits; ++s) acc += p.ws[(long)s * total + e];
     const int i = (int)(e % p.M), j = (int)(e / p.M);
+    long src = e;
+    if (p.sym && i / p.tbm < j / p.tbm) {   // upper tile: not computed
+      if (p.sym == 2) continue;               // left untouched
+      src = j + (long)i * p.M;                // mirrored: C(i, j) = C(j, i), a lower tile
+    }
+    float acc = 0.f;
+    for (int s = 0; s < p.splits; ++s) acc += p.ws[(long)s * total + src];
     p.C[i + (long)j * p.ldc] = gemm_out(p, i, j, gemm_row_alpha(p, i), acc, beta);
   }
 }

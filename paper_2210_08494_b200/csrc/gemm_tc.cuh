@@ -315,6 +315,9 @@ BKFAC_DEV TcTile tc_tile(const GemmBatch& b, int t) {
     while ((tm + 1) * (tm + 2) / 2 <= rem) ++tm;
     x.m0 = tm * BMT;
     x.n0 = (rem - tm * (tm + 1) / 2) * BN;
+  } else if (p.nfast) {
+    x.n0 = (rem % p.tiles_n) * BN;
+    x.m0 = (rem / p.tiles_n) * BMT;
   } else {
     x.m0 = (rem % p.tiles_m) * BMT;
     x.n0 = (rem / p.tiles_m) * BN;
@@ -352,8 +355,10 @@ BKFAC_DEV void tc_store_group(const GemmProb& p, const TcTile& x, int g, float (
   float c0v[16];
   if (beta != 0.f) {
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj)
-      c0v[jj] = (rowok && j0 + jj < p.N) ? p.C0[i + (long)(j0 + jj) * p.ldc0] : 0.f;
+    for (int jj = 0; jj < 16; ++jj) {
+      const float* q = p.C0 + i + (long)(j0 + jj) * p.ldc0;
+      c0v[jj] = (rowok && j0 + jj < p.N) ? (p.stream_c ? __ldcs(q) : *q) : 0.f;
+    }
   }
   // alpha v + beta C0 on pairs (FMUL2 / FFMA2: the same per-element roundings as the scalar
   // o = alpha v; o += beta c0); fused scalings (device alpha, row / column scale, diagonal)
@@ -375,8 +380,14 @@ BKFAC_DEV void tc_store_group(const GemmProb& p, const TcTile& x, int g, float (
       if (i == j0 + jj) o.x += p.diag_a * p.diag_vec[i];
       if (i == j0 + jj + 1) o.y += p.diag_a * p.diag_vec[i];
     }
-    if (rowok && j0 + jj < p.N) p.C[i + (long)(j0 + jj) * p.ldc] = o.x;
-    if (rowok && j0 + jj + 1 < p.N) p.C[i + (long)(j0 + jj + 1) * p.ldc] = o.y;
+    float* q = p.C + i + (long)(j0 + jj) * p.ldc;
+    if (p.stream_c) {
+      if (rowok && j0 + jj < p.N) __stcs(q, o.x);
+      if (rowok && j0 + jj + 1 < p.N) __stcs(q + p.ldc, o.y);
+    } else {
+      if (rowok && j0 + jj < p.N) *q = o.x;
+      if (rowok && j0 + jj + 1 < p.N) q[p.ldc] = o.y;
+    }
     v[jj] = o.x; v[jj + 1] = o.y;
   }
   if (p.sym == 1 && x.m0 != x.n0) {
