@@ -145,8 +145,10 @@ def make_workload(name: str):
 
 def device_inputs(cfg, my_factors, my_layers, pool: int, device):
     """Per-step inputs generated ON DEVICE outside the timed region, same recipe as
-    synth.FactorSpec.batch (L diag(s) W + sigma N) but drawn with torch's CUDA RNG."""
+    synth.FactorSpec.batch (L diag(s) W + sigma N) but drawn with torch's CUDA RNG.  M and J
+    live in buffers whose leading dimension is padded to 32 floats (stack.padded)."""
     import torch
+    from paper_2210_08494_b200.stack import padded
     M_pool = [dict() for _ in range(pool)]
     J_pool = [dict() for _ in range(pool)]
     for g in my_factors:
@@ -161,15 +163,16 @@ def device_inputs(cfg, my_factors, my_layers, pool: int, device):
             W = torch.randn((f.k, f.c), generator=gen, device=device)
             N = torch.randn((f.n, f.c), generator=gen, device=device)
             M = (L * s[None, :]) @ W + f.sigma * N            # n x c
-            M_pool[p][g] = M.t().contiguous()                   # (c, n) == col-major n x c
+            M_pool[p][g] = padded(f.c, f.n, device, zero=False)   # (c, n) == col-major n x c
+            M_pool[p][g].copy_(M.t())
         del G, L, R
     for li in my_layers:
         l = cfg.layers[li]
         gen = torch.Generator(device=device)
         gen.manual_seed(l.seed)
         for p in range(pool):
-            J_pool[p][li] = (l.grad_std * torch.randn((l.d_G, l.d_A), generator=gen,
-                                                      device=device)).contiguous()
+            J_pool[p][li] = padded(l.d_G, l.d_A, device, zero=False)
+            J_pool[p][li].copy_(l.grad_std * torch.randn((l.d_G, l.d_A), generator=gen, device=device))
     torch.cuda.synchronize()
     return M_pool, J_pool
 
@@ -589,27 +592,30 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
     copies of the step's M and J, the step, and a device -> host read of S."""
     import torch
     import torch.distributed as dist
+    from paper_2210_08494_b200.stack import padded, full_rows
     steps = max(1, min(args.e2e_steps, args.steps))
     # host inputs: the headline's own synthetic batches (synth recipe, device pool batch 0)
     # copied to pinned host memory -- every factor's M (so the eigensolver sees the same
     # spectra as the headline) and one gradient per layer shape (J ~ N(0, var) throughout)
-    host_M = {g: M_pool[0][g].cpu().pin_memory() for g in stack.my_factors}
+    # host buffers have the device buffers' padded layout (leading dimension a multiple of
+    # 32), so every copy is one contiguous DMA of the whole buffer
+    host_M = {g: full_rows(M_pool[0][g]).cpu().pin_memory() for g in stack.my_factors}
     host_J, host_S = {}, {}
     for li in stack.my_layers:
         l = cfg.layers[li]
         key = (l.d_G, l.d_A)
         if key not in host_J:
-            host_J[key] = J_pool[0][li].cpu().pin_memory()
-            host_S[key] = torch.empty(key, dtype=torch.float32).pin_memory()
+            host_J[key] = full_rows(J_pool[0][li]).cpu().pin_memory()
+            host_S[key] = torch.empty(tuple(host_J[key].shape), dtype=torch.float32).pin_memory()
     # two device input sets: step i+1's host->device copies run (copy stream) while step i
     # computes; step i's S is read back (second copy stream) while step i+1 computes
-    dev_M = [{g: torch.empty((cfg.factors[g].c, cfg.factors[g].n), dtype=torch.float32, device=device)
+    dev_M = [{g: padded(cfg.factors[g].c, cfg.factors[g].n, device, zero=False)
               for g in stack.my_factors} for _ in range(2)]
-    dev_J = [{li: torch.empty((cfg.layers[li].d_G, cfg.layers[li].d_A), dtype=torch.float32,
-                              device=device) for li in stack.my_layers} for _ in range(2)]
-    h2d = sum(4 * t.numel() for t in dev_M[0].values()) + \
-        (0 if args.factored else sum(4 * t.numel() for t in dev_J[0].values()))
-    d2h = sum(4 * cfg.layers[li].d_G * cfg.layers[li].d_A for li in stack.my_layers)
+    dev_J = [{li: padded(cfg.layers[li].d_G, cfg.layers[li].d_A, device, zero=False)
+              for li in stack.my_layers} for _ in range(2)]
+    h2d = sum(4 * full_rows(t).numel() for t in dev_M[0].values()) + \
+        (0 if args.factored else sum(4 * full_rows(t).numel() for t in dev_J[0].values()))
+    d2h = sum(4 * host_S[(cfg.layers[li].d_G, cfg.layers[li].d_A)].numel() for li in stack.my_layers)
     use_graphs = not args.no_graphs
     up, down = torch.cuda.Stream(device=device), torch.cuda.Stream(device=device)
     ev_up = [torch.cuda.Event() for _ in range(2)]
@@ -623,11 +629,11 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
         with torch.cuda.stream(up):
             up.wait_event(ev_done[b])             # step j-2 (same buffers) has finished
             for g, t in dev_M[b].items():
-                t.copy_(host_M[g], non_blocking=True)
+                full_rows(t).copy_(host_M[g], non_blocking=True)
             if not args.factored:
                 for li, t in dev_J[b].items():
                     l = cfg.layers[li]
-                    t.copy_(host_J[(l.d_G, l.d_A)], non_blocking=True)
+                    full_rows(t).copy_(host_J[(l.d_G, l.d_A)], non_blocking=True)
             ev_up[b].record(up)
 
     def run(n):
@@ -650,7 +656,11 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
                 down.wait_event(ev_done[b])
                 for li, s_ in S.items():
                     l = cfg.layers[li]
-                    host_S[(l.d_G, l.d_A)].copy_(s_, non_blocking=True)
+                    hs = host_S[(l.d_G, l.d_A)]
+                    if s_.stride(0) == hs.shape[1]:
+                        hs.copy_(full_rows(s_), non_blocking=True)
+                    else:   # S bound to packed send slots (N > 1)
+                        hs[:, :l.d_A].copy_(s_, non_blocking=True)
                 ev_down[b].record(down)
         if gather is not None:
             gather.finish(0); gather.finish(1)

@@ -24,6 +24,14 @@
  *   - "col-major a x b" = each length-a column is contiguous (a PyTorch tensor of
  *     shape (b, a)).  U (n x r), M (n x c), K_dense (n x n, symmetric) are col-major.
  *     J and S are row-major d_G x d_A (PyTorch weight.grad layout).
+ *   - Leading dimensions.  The ld_* fields of the argument structs give the distance in
+ *     floats between consecutive columns of a col-major operand (rows of J / S); 0 means
+ *     packed (the row count; d_A for J / S), otherwise ld >= that (BKFAC_ERR_DIM).  With a
+ *     16-byte-aligned base and ld a multiple of 4 the contractions read the operand with
+ *     16-byte loads; odd packed layouts (n = 4097, d_A = 16385, ...) cost an internal
+ *     aligned copy (Brand operands) or the 4-byte load path (preconditioner operands), so
+ *     callers should allocate with ld rounded up to a multiple of 32.  Padding entries are
+ *     never read and never written (except U_out's columns beyond r_out, zero-filled).
  *   - D arrays have length r, are non-increasing and >= 0 on output.
  *   - The library never allocates device memory: the caller allocates the workspace
  *     (bkfac_workspace_bytes) and registers it (bkfac_set_workspace).  The context
@@ -148,6 +156,8 @@ typedef struct {
   float* U_out; float* D_out;
   float alpha; float beta;
   int flags;
+  int ld_U;   /* leading dimension of U_in and U_out (0: n) */
+  int ld_M;   /* leading dimension of M (0: n) */
 } bkfac_brand_args;
 bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int count,
                                 void* stream);
@@ -157,7 +167,10 @@ bkfac_status bkfac_ea_accumulate(bkfac_ctx ctx, int factor, float* K_dense, cons
                                  int c, float rho, void* stream);
 
 /* Batched form of bkfac_ea_accumulate: `count` distinct factors in one grouped launch. */
-typedef struct { int factor; float* K_dense; const float* M; int c; float rho; } bkfac_ea_args;
+typedef struct {
+  int factor; float* K_dense; const float* M; int c; float rho;
+  int ld_M;   /* leading dimension of M (0: n); K_dense is packed */
+} bkfac_ea_args;
 bkfac_status bkfac_ea_accumulate_batch(bkfac_ctx ctx, const bkfac_ea_args* args, int count,
                                        void* stream);
 
@@ -181,6 +194,7 @@ bkfac_status bkfac_rsvd_overwrite(bkfac_ctx ctx, int factor, const float* K_dens
 typedef struct {
   int factor; const float* K_dense; int oversample; int power_iters;
   uint64_t seed; uint64_t counter; float* U_out; float* D_out;
+  int ld_U;   /* leading dimension of U_out (0: n); K_dense is packed */
 } bkfac_rsvd_args;
 bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* args, int count,
                                         void* stream);
@@ -195,6 +209,7 @@ bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* ar
  * Requires BKFAC_FACTOR_DENSE_EA; 1 <= n_crc <= r. */
 typedef struct {
   int factor; const float* K_dense; float* U; float* D; const int* col_idx; int n_crc;
+  int ld_U;   /* leading dimension of U (0: n); K_dense is packed */
 } bkfac_correct_args;
 bkfac_status bkfac_light_correction(bkfac_ctx ctx, const bkfac_correct_args* args, int count,
                                     void* stream);
@@ -215,6 +230,8 @@ typedef struct {
   const float* U_A; const float* D_A; float lambda_A;
   const float* J; float* S;
   int flags;
+  int ld_UG; int ld_UA;   /* leading dimensions of U_G (0: d_G) and U_A (0: d_A) */
+  int ld_J; int ld_S;     /* row strides of J and S (0: d_A) */
 } bkfac_precond_args;
 bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, int count,
                                 void* stream);
@@ -235,6 +252,9 @@ typedef struct {
   const float* G; const float* A; int n;
   float* S;
   int flags;
+  int ld_UG; int ld_UA;   /* leading dimensions of U_G (0: d_G) and U_A (0: d_A) */
+  int ld_G; int ld_A;     /* leading dimensions of G (0: d_G) and A (0: d_A) */
+  int ld_S;               /* row stride of S (0: d_A) */
 } bkfac_precond_factored_args;
 bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_factored_args* args,
                                          int count, void* stream);

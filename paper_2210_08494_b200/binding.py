@@ -1,10 +1,14 @@
 """ctypes binding of the bkfac C ABI (include/bkfac.h).  Argument marshalling only:
 every step of the hot path runs in the CUDA kernels of ``libbkfac.so``.
 
-Tensor conventions (PyTorch, all fp32, CUDA, contiguous):
+Tensor conventions (PyTorch, all fp32, CUDA):
   U: shape (r, n)   == col-major n x r          M: shape (c, n) == col-major n x c
   D: shape (r,)                                  K_dense: shape (n, n) (symmetric)
   J, S: shape (d_G, d_A)  == row-major d_G x d_A (weight.grad layout)
+U, M, J, S (and G, A of Algorithm 8) need unit stride along their last dimension only: a
+view t[:, :n] of a padded (b, ld) buffer is passed with its row stride as the operand's
+leading dimension (bkfac.h "Leading dimensions"; ld a multiple of 32 takes the 16-byte
+load path).  D, K_dense and index arrays must be contiguous.
 """
 from __future__ import annotations
 
@@ -66,18 +70,18 @@ class BrandArgs(ctypes.Structure):
     _fields_ = [("factor", ctypes.c_int), ("U_in", ctypes.c_void_p), ("D_in", ctypes.c_void_p),
                 ("M", ctypes.c_void_p), ("c", ctypes.c_int), ("U_out", ctypes.c_void_p),
                 ("D_out", ctypes.c_void_p), ("alpha", ctypes.c_float), ("beta", ctypes.c_float),
-                ("flags", ctypes.c_int)]
+                ("flags", ctypes.c_int), ("ld_U", ctypes.c_int), ("ld_M", ctypes.c_int)]
 
 
 class EaArgs(ctypes.Structure):
     _fields_ = [("factor", ctypes.c_int), ("K_dense", ctypes.c_void_p), ("M", ctypes.c_void_p),
-                ("c", ctypes.c_int), ("rho", ctypes.c_float)]
+                ("c", ctypes.c_int), ("rho", ctypes.c_float), ("ld_M", ctypes.c_int)]
 
 
 class RsvdArgs(ctypes.Structure):
     _fields_ = [("factor", ctypes.c_int), ("K_dense", ctypes.c_void_p), ("oversample", ctypes.c_int),
                 ("power_iters", ctypes.c_int), ("seed", ctypes.c_uint64), ("counter", ctypes.c_uint64),
-                ("U_out", ctypes.c_void_p), ("D_out", ctypes.c_void_p)]
+                ("U_out", ctypes.c_void_p), ("D_out", ctypes.c_void_p), ("ld_U", ctypes.c_int)]
 
 
 class StageStat(ctypes.Structure):
@@ -88,21 +92,25 @@ class StageStat(ctypes.Structure):
 
 class CorrectArgs(ctypes.Structure):
     _fields_ = [("factor", ctypes.c_int), ("K_dense", ctypes.c_void_p), ("U", ctypes.c_void_p),
-                ("D", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("n_crc", ctypes.c_int)]
+                ("D", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("n_crc", ctypes.c_int),
+                ("ld_U", ctypes.c_int)]
 
 
 class PrecondFactoredArgs(ctypes.Structure):
     _fields_ = [("layer", ctypes.c_int), ("U_G", ctypes.c_void_p), ("D_G", ctypes.c_void_p),
                 ("lambda_G", ctypes.c_float), ("U_A", ctypes.c_void_p), ("D_A", ctypes.c_void_p),
                 ("lambda_A", ctypes.c_float), ("G", ctypes.c_void_p), ("A", ctypes.c_void_p),
-                ("n", ctypes.c_int), ("S", ctypes.c_void_p), ("flags", ctypes.c_int)]
+                ("n", ctypes.c_int), ("S", ctypes.c_void_p), ("flags", ctypes.c_int),
+                ("ld_UG", ctypes.c_int), ("ld_UA", ctypes.c_int), ("ld_G", ctypes.c_int),
+                ("ld_A", ctypes.c_int), ("ld_S", ctypes.c_int)]
 
 
 class PrecondArgs(ctypes.Structure):
     _fields_ = [("layer", ctypes.c_int), ("U_G", ctypes.c_void_p), ("D_G", ctypes.c_void_p),
                 ("lambda_G", ctypes.c_float), ("U_A", ctypes.c_void_p), ("D_A", ctypes.c_void_p),
                 ("lambda_A", ctypes.c_float), ("J", ctypes.c_void_p), ("S", ctypes.c_void_p),
-                ("flags", ctypes.c_int)]
+                ("flags", ctypes.c_int), ("ld_UG", ctypes.c_int), ("ld_UA", ctypes.c_int),
+                ("ld_J", ctypes.c_int), ("ld_S", ctypes.c_int)]
 
 
 _lib = None
@@ -189,6 +197,27 @@ def _ptr(t) -> Optional[int]:
     return t.data_ptr()
 
 
+def _mat(t):
+    """(device pointer, leading dimension) of a 2-D float32 CUDA tensor whose rows are the
+    col-major columns of the operand: unit stride along dim 1, any row stride >= the row
+    length (a view t[:, :n] of a padded (b, ld) buffer passes ld; bkfac.h "Leading
+    dimensions")."""
+    import torch
+    if t is None:
+        return None, 0
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch.Tensor")
+    if t.dtype != torch.float32 or not t.is_cuda or t.dim() != 2:
+        raise ValueError("bkfac expects 2-D float32 CUDA tensors")
+    rows, cols = t.shape
+    if cols > 1 and t.stride(1) != 1:
+        raise ValueError("bkfac expects unit stride along the last dimension")
+    ld = t.stride(0) if rows > 1 else max(t.stride(0), cols)
+    if rows > 1 and ld < cols:
+        raise ValueError("bkfac expects row stride >= row length")
+    return t.data_ptr(), int(ld)
+
+
 def _iptr(t) -> Optional[int]:
     """Device pointer of a contiguous int32 CUDA tensor (index arrays)."""
     import torch
@@ -202,6 +231,15 @@ def _stream_ptr(stream) -> int:
     if stream is None:
         stream = torch.cuda.current_stream()
     return stream.cuda_stream
+
+
+def _brand_args(u) -> BrandArgs:
+    (ui, ldu), (uo, ldo), (m, ldm) = _mat(u["U_in"]), _mat(u["U_out"]), _mat(u["M"])
+    if ldu != ldo:
+        raise ValueError("U_in and U_out must share one leading dimension")
+    return BrandArgs(u["factor"], ui, _ptr(u["D_in"]), m, int(u["M"].shape[0]), uo,
+                     _ptr(u["D_out"]), float(u["alpha"]), float(u["beta"]),
+                     int(u.get("flags", 0)), ldu, ldm)
 
 
 class Context:
@@ -242,9 +280,7 @@ class Context:
     def bkfac_brand_update(self, updates: List[dict], stream=None) -> None:
         arr = (BrandArgs * len(updates))()
         for i, u in enumerate(updates):
-            arr[i] = BrandArgs(u["factor"], _ptr(u["U_in"]), _ptr(u["D_in"]), _ptr(u["M"]),
-                               int(u["M"].shape[0]), _ptr(u["U_out"]), _ptr(u["D_out"]),
-                               float(u["alpha"]), float(u["beta"]), int(u.get("flags", 0)))
+            arr[i] = _brand_args(u)
         _check(self.lib.bkfac_brand_update(self.h, arr, len(updates), _stream_ptr(stream)),
                "bkfac_brand_update")
 
@@ -253,13 +289,11 @@ class Context:
         of one step, the EA GEMM overlapped with the eigensolver inside the library."""
         arr = (BrandArgs * max(len(updates), 1))()
         for i, u in enumerate(updates):
-            arr[i] = BrandArgs(u["factor"], _ptr(u["U_in"]), _ptr(u["D_in"]), _ptr(u["M"]),
-                               int(u["M"].shape[0]), _ptr(u["U_out"]), _ptr(u["D_out"]),
-                               float(u["alpha"]), float(u["beta"]), int(u.get("flags", 0)))
+            arr[i] = _brand_args(u)
         ea = (EaArgs * max(len(ea_items), 1))()
         for i, a in enumerate(ea_items):
-            ea[i] = EaArgs(a["factor"], _ptr(a["K"]), _ptr(a["M"]), int(a["M"].shape[0]),
-                           float(a["rho"]))
+            m, ldm = _mat(a["M"])
+            ea[i] = EaArgs(a["factor"], _ptr(a["K"]), m, int(a["M"].shape[0]), float(a["rho"]), ldm)
         _check(self.lib.bkfac_brand_ea_update(self.h, arr, len(updates), ea, len(ea_items),
                                               _stream_ptr(stream)),
                "bkfac_brand_ea_update")
@@ -273,8 +307,8 @@ class Context:
         """bkfac_ea_accumulate_batch: items of dict(factor, K, M, rho)."""
         arr = (EaArgs * len(items))()
         for i, a in enumerate(items):
-            arr[i] = EaArgs(a["factor"], _ptr(a["K"]), _ptr(a["M"]), int(a["M"].shape[0]),
-                            float(a["rho"]))
+            m, ldm = _mat(a["M"])
+            arr[i] = EaArgs(a["factor"], _ptr(a["K"]), m, int(a["M"].shape[0]), float(a["rho"]), ldm)
         _check(self.lib.bkfac_ea_accumulate_batch(self.h, arr, len(items), _stream_ptr(stream)),
                "bkfac_ea_accumulate_batch")
 
@@ -290,17 +324,20 @@ class Context:
         U_out, D_out)."""
         arr = (RsvdArgs * len(items))()
         for i, a in enumerate(items):
+            uo, ldu = _mat(a["U_out"])
             arr[i] = RsvdArgs(a["factor"], _ptr(a["K"]), int(a["oversample"]), int(a["power_iters"]),
-                              int(a["seed"]), int(a["counter"]), _ptr(a["U_out"]), _ptr(a["D_out"]))
+                              int(a["seed"]), int(a["counter"]), uo, _ptr(a["D_out"]), ldu)
         _check(self.lib.bkfac_rsvd_overwrite_batch(self.h, arr, len(items), _stream_ptr(stream)),
                "bkfac_rsvd_overwrite_batch")
 
     def bkfac_precondition(self, items: List[dict], stream=None) -> None:
         arr = (PrecondArgs * len(items))()
         for i, a in enumerate(items):
-            arr[i] = PrecondArgs(a["layer"], _ptr(a["U_G"]), _ptr(a["D_G"]), float(a["lambda_G"]),
-                                 _ptr(a["U_A"]), _ptr(a["D_A"]), float(a["lambda_A"]),
-                                 _ptr(a["J"]), _ptr(a["S"]), int(a.get("flags", 0)))
+            (ug, ldg), (ua, lda) = _mat(a["U_G"]), _mat(a["U_A"])
+            (j, ldj), (sp, lds) = _mat(a["J"]), _mat(a["S"])
+            arr[i] = PrecondArgs(a["layer"], ug, _ptr(a["D_G"]), float(a["lambda_G"]),
+                                 ua, _ptr(a["D_A"]), float(a["lambda_A"]),
+                                 j, sp, int(a.get("flags", 0)), ldg, lda, ldj, lds)
         _check(self.lib.bkfac_precondition(self.h, arr, len(items), _stream_ptr(stream)),
                "bkfac_precondition")
 
@@ -309,10 +346,12 @@ class Context:
         G, A are (n, d) tensors (= col-major d x n), n = G.shape[0]."""
         arr = (PrecondFactoredArgs * len(items))()
         for i, a in enumerate(items):
-            arr[i] = PrecondFactoredArgs(a["layer"], _ptr(a["U_G"]), _ptr(a["D_G"]), float(a["lambda_G"]),
-                                         _ptr(a["U_A"]), _ptr(a["D_A"]), float(a["lambda_A"]),
-                                         _ptr(a["G"]), _ptr(a["A"]), int(a["G"].shape[0]),
-                                         _ptr(a["S"]), int(a.get("flags", 0)))
+            (ug, ldug), (ua, ldua) = _mat(a["U_G"]), _mat(a["U_A"])
+            (g, ldg), (am, lda), (sp, lds) = _mat(a["G"]), _mat(a["A"]), _mat(a["S"])
+            arr[i] = PrecondFactoredArgs(a["layer"], ug, _ptr(a["D_G"]), float(a["lambda_G"]),
+                                         ua, _ptr(a["D_A"]), float(a["lambda_A"]),
+                                         g, am, int(a["G"].shape[0]), sp, int(a.get("flags", 0)),
+                                         ldug, ldua, ldg, lda, lds)
         _check(self.lib.bkfac_precondition_factored(self.h, arr, len(items), _stream_ptr(stream)),
                "bkfac_precondition_factored")
 
@@ -320,8 +359,9 @@ class Context:
         """Algorithm 6: dict(factor, K, U, D, col_idx (int32 device tensor of n_crc indices))."""
         arr = (CorrectArgs * len(items))()
         for i, a in enumerate(items):
-            arr[i] = CorrectArgs(a["factor"], _ptr(a["K"]), _ptr(a["U"]), _ptr(a["D"]),
-                                 _iptr(a["col_idx"]), int(a["col_idx"].numel()))
+            u, ldu = _mat(a["U"])
+            arr[i] = CorrectArgs(a["factor"], _ptr(a["K"]), u, _ptr(a["D"]),
+                                 _iptr(a["col_idx"]), int(a["col_idx"].numel()), ldu)
         _check(self.lib.bkfac_light_correction(self.h, arr, len(items), _stream_ptr(stream)),
                "bkfac_light_correction")
 

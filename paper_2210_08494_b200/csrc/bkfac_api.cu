@@ -34,6 +34,15 @@ constexpr int kRsvdOversampleMax = 32;
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// caller leading dimensions (bkfac.h "Leading dimensions"): 0 = packed
+inline int ldx(int ld, int rows) { return ld > 0 ? ld : rows; }
+inline bool ld_ok(int ld, int rows) { return ld == 0 || ld >= rows; }
+// the GEMM loaders' 16-byte path: aligned base, leading dimension a multiple of 4
+inline bool al16(const void* q, int ld) {
+  return (reinterpret_cast<uintptr_t>(q) & 15) == 0 && (ld & 3) == 0;
+}
+inline int pad32(int x) { return (x + 31) / 32 * 32; }
+
 struct Arena {
   size_t cur = 0;
   size_t take(size_t bytes) {
@@ -104,6 +113,7 @@ struct FactorPlan {
 struct LayerPlan {
   bkfac_layer_desc d;
   size_t Y, Xt, Z, sA, sG, lam, ws;  // lam: [lamA, lamG, coef, 1/lamA, 1/lamG]
+  int ldY = 0, ldXt = 0;             // Y (d_G x r_A), Xt (d_A x r_G): padded to 32
   size_t ws_elems = 0;
   // Algorithm 8 (n_max > 0): P_G = G^T U_G, P_A = A^T U_A (n x r), G_b, A_b (d x n)
   size_t fPG = 0, fPA = 0, fGb = 0, fAb = 0, fws = 0, fws2 = 0;
@@ -1080,8 +1090,10 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
       delete c;
       return BKFAC_ERR_DIM;
     }
-    lp.Y = a.take(sizeof(float) * (size_t)d.d_G * std::max(d.r_A, 1));
-    lp.Xt = a.take(sizeof(float) * (size_t)d.d_A * std::max(d.r_G, 1));
+    lp.ldY = pad32(d.d_G);
+    lp.ldXt = pad32(d.d_A);
+    lp.Y = a.take(sizeof(float) * (size_t)lp.ldY * std::max(d.r_A, 1));
+    lp.Xt = a.take(sizeof(float) * (size_t)lp.ldXt * std::max(d.r_G, 1));
     lp.Z = a.take(sizeof(float) * (size_t)std::max(d.r_G, 1) * std::max(d.r_A, 1));
     lp.sA = a.take(sizeof(float) * std::max(d.r_A, 1));
     lp.sG = a.take(sizeof(float) * std::max(d.r_G, 1));
@@ -1275,6 +1287,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     if (!(a.alpha >= 0.f) || !(a.beta > 0.f) || !std::isfinite(a.alpha) || !std::isfinite(a.beta))
       return BKFAC_ERR_INVALID_ARG;
     if (a.c <= 0 || a.c > fp.d.c_max) return BKFAC_ERR_DIM;
+    if (!ld_ok(a.ld_U, fp.d.n) || !ld_ok(a.ld_M, fp.d.n)) return BKFAC_ERR_DIM;
     if (a.U_out == a.U_in || a.D_out == a.D_in) return BKFAC_ERR_ALIAS;
     for (int j = 0; j < i; ++j)
       if (args[j].factor == a.factor) return BKFAC_ERR_INVALID_ARG;  // one update per factor per batch
@@ -1298,6 +1311,12 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const auto& fp = ctx->f[a.factor];
     return (fp.d.flags & BKFAC_FACTOR_FULL_RANK) ? std::min(fp.d.n, fp.d.r + a.c) : fp.d.r;
   };
+  auto ldU = [&](const bkfac_brand_args& a) { return ldx(a.ld_U, ctx->f[a.factor].d.n); };
+  auto ldM = [&](const bkfac_brand_args& a) { return ldx(a.ld_M, ctx->f[a.factor].d.n); };
+  // internal 16-byte-aligned copies (ld nld) of M / U_in: odd n and a caller layout the
+  // vector loads cannot use
+  auto useMs = [&](const bkfac_brand_args& a) { return ctx->f[a.factor].Ms && !al16(a.M, ldM(a)); };
+  auto useUs = [&](const bkfac_brand_args& a) { return ctx->f[a.factor].Us && !al16(a.U_in, ldU(a)); };
 #define STAGE(x) do { if ((rs = (x)) != BKFAC_OK) goto done; } while (0)
 
   // full-rank factors with c < c_max: zero the output columns / entries beyond r + c
@@ -1306,8 +1325,8 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const auto& fp = ctx->f[a.factor];
     const int ro = rout_of(a);
     if (ro < fp.rout) {
-      if (!cuda_ok(cudaMemsetAsync(a.U_out + (size_t)fp.d.n * ro, 0,
-                                   sizeof(float) * (size_t)fp.d.n * (fp.rout - ro), st)) ||
+      if (!cuda_ok(cudaMemsetAsync(a.U_out + (size_t)ldU(a) * ro, 0,
+                                   sizeof(float) * ((size_t)ldU(a) * (fp.rout - ro - 1) + fp.d.n), st)) ||
           !cuda_ok(cudaMemsetAsync(a.D_out + ro, 0, sizeof(float) * (fp.rout - ro), st))) {
         rs = BKFAC_ERR_CUDA;
         goto done;
@@ -1322,7 +1341,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& fp = ctx->f[a.factor];
       if (a.alpha != 0.f) {
         EwProb e{};
-        e.Y = at<float>(ctx, fp.T); e.ldy = fp.d.n; e.X = a.U_in; e.ldx = fp.d.n;
+        e.Y = at<float>(ctx, fp.T); e.ldy = fp.d.n; e.X = a.U_in; e.ldx = ldU(a);
         e.vec = a.D_in; e.rows = fp.d.n; e.cols = fp.d.r; e.op = EW_SCALE_COLS;
         ew.push_back(e);
       }
@@ -1335,7 +1354,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         nb.nprob = 0;
         for (size_t q = i0; q < std::min(dense.size(), i0 + NF_MAXP); ++q) {
           const auto& a = args[dense[q]];
-          nb.p[nb.nprob++] = NfProb{a.M, ctx->f[a.factor].d.n, a.c, ctx->f[a.factor].d.n, status_ptr(ctx, a.factor)};
+          nb.p[nb.nprob++] = NfProb{a.M, ctx->f[a.factor].d.n, a.c, ldM(a), status_ptr(ctx, a.factor)};
         }
         nonfinite_kernel<<<dim3(16, (unsigned)nb.nprob), 256, 0, st>>>(nb);
         LAUNCH_CHECK(ctx);
@@ -1346,7 +1365,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& fp = ctx->f[a.factor];
       if (a.alpha != 0.f) {
         const int n = fp.d.n;
-        gs.add(false, true, gp(at<float>(ctx, fp.T), n, a.U_in, n, at<float>(ctx, fp.eig.K), n, n, n,
+        gs.add(false, true, gp(at<float>(ctx, fp.T), n, a.U_in, ldU(a), at<float>(ctx, fp.eig.K), n, n, n,
                                fp.d.r, a.alpha), 0);
       }
     }
@@ -1356,7 +1375,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n;
       float* K = at<float>(ctx, fp.eig.K);
-      gs.add(false, true, gp(a.M, n, a.M, n, K, n, n, n, a.c, a.beta, K, n, a.alpha != 0.f ? 1.f : 0.f), 0);
+      gs.add(false, true, gp(a.M, ldM(a), a.M, ldM(a), K, n, n, n, a.c, a.beta, K, n, a.alpha != 0.f ? 1.f : 0.f), 0);
     }
     STAGE(run("gemm_dense_core"));
     for (int i : dense) {
@@ -1374,37 +1393,40 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     for (int i : brand) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
-      if (!fp.Ms) continue;
       const int n = fp.d.n;
-      EwProb e{};
-      e.Y = at<float>(ctx, fp.Ms); e.ldy = fp.nld; e.X = a.M; e.ldx = n; e.rows = n; e.cols = a.c;
-      e.op = EW_COPY;
-      ew.push_back(e);
-      EwProb u{};
-      u.Y = at<float>(ctx, fp.Us); u.ldy = fp.nld; u.X = a.U_in; u.ldx = n; u.rows = n; u.cols = fp.d.r;
-      u.op = EW_COPY;
-      ew.push_back(u);
+      if (useMs(a)) {
+        EwProb e{};
+        e.Y = at<float>(ctx, fp.Ms); e.ldy = fp.nld; e.X = a.M; e.ldx = ldM(a); e.rows = n; e.cols = a.c;
+        e.op = EW_COPY;
+        ew.push_back(e);
+      }
+      if (useUs(a)) {
+        EwProb u{};
+        u.Y = at<float>(ctx, fp.Us); u.ldy = fp.nld; u.X = a.U_in; u.ldx = ldU(a); u.rows = n; u.cols = fp.d.r;
+        u.op = EW_COPY;
+        ew.push_back(u);
+      }
     }
     if (!ew.empty()) STAGE(run_ew(ctx, ew, st, "ew_align"));
     // operand views: the aligned copies where they exist
     auto Uin = [&](const bkfac_brand_args& a) -> const float* {
-      const auto& fp = ctx->f[a.factor];
-      return fp.Us ? at<float>(ctx, fp.Us) : a.U_in;
+      return useUs(a) ? at<float>(ctx, ctx->f[a.factor].Us) : a.U_in;
     };
     auto Min = [&](const bkfac_brand_args& a) -> const float* {
-      const auto& fp = ctx->f[a.factor];
-      return fp.Ms ? at<float>(ctx, fp.Ms) : a.M;
+      return useMs(a) ? at<float>(ctx, ctx->f[a.factor].Ms) : a.M;
     };
-    auto ldin = [&](const bkfac_brand_args& a) -> int {
-      const auto& fp = ctx->f[a.factor];
-      return fp.Ms ? fp.nld : fp.d.n;
+    auto ldUin = [&](const bkfac_brand_args& a) -> int {
+      return useUs(a) ? ctx->f[a.factor].nld : ldU(a);
+    };
+    auto ldMin = [&](const bkfac_brand_args& a) -> int {
+      return useMs(a) ? ctx->f[a.factor].nld : ldM(a);
     };
     // A: P = U^T M  -> W rows [0, r)
     for (int i : brand) {
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
-      GemmProb p = gp(Uin(a), ldin(a), Min(a), ldin(a), at<float>(ctx, fp.W), fp.m, r, a.c, n, 1.f);
+      GemmProb p = gp(Uin(a), ldUin(a), Min(a), ldMin(a), at<float>(ctx, fp.W), fp.m, r, a.c, n, 1.f);
       gemm_ws(p, at<float>(ctx, fp.ws));
       gs.add(true, false, p, fp.ws_elems);
     }
@@ -1414,8 +1436,8 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       const auto& a = args[i];
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
-      GemmProb pr = gp(Uin(a), ldin(a), at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), fp.nld, n, a.c,
-                       r, -1.f, Min(a), ldin(a), 1.f);
+      GemmProb pr = gp(Uin(a), ldUin(a), at<float>(ctx, fp.W), fp.m, at<float>(ctx, fp.R), fp.nld, n, a.c,
+                       r, -1.f, Min(a), ldMin(a), 1.f);
       pr.status = status_ptr(ctx, a.factor);   // every element of M passes this epilogue
       gs.add(false, false, pr, 0);
     }
@@ -1428,7 +1450,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
       any_reorth = true;
       const auto& fp = ctx->f[a.factor];
       const int n = fp.d.n, r = fp.d.r;
-      GemmProb p = gp(Uin(a), ldin(a), at<float>(ctx, fp.R), fp.nld, at<float>(ctx, fp.P2), r, r, a.c, n, 1.f);
+      GemmProb p = gp(Uin(a), ldUin(a), at<float>(ctx, fp.R), fp.nld, at<float>(ctx, fp.P2), r, r, a.c, n, 1.f);
       gemm_ws(p, at<float>(ctx, fp.ws));
       gs.add(true, false, p, fp.ws_elems);
     }
@@ -1440,7 +1462,7 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
         const auto& fp = ctx->f[a.factor];
         const int n = fp.d.n, r = fp.d.r;
         float* R = at<float>(ctx, fp.R);
-        gs.add(false, false, gp(Uin(a), ldin(a), at<float>(ctx, fp.P2), r, R, fp.nld, n, a.c, r, -1.f, R, fp.nld, 1.f), 0);
+        gs.add(false, false, gp(Uin(a), ldUin(a), at<float>(ctx, fp.P2), r, R, fp.nld, n, a.c, r, -1.f, R, fp.nld, 1.f), 0);
         EwProb e{};
         e.Y = at<float>(ctx, fp.W); e.ldy = fp.m; e.X = at<float>(ctx, fp.P2); e.ldx = r;
         e.rows = r; e.cols = a.c; e.a = 1.f; e.op = EW_ADD;
@@ -1531,8 +1553,9 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const auto& fp = ctx->f[a.factor];
     const int n = fp.d.n, r = fp.d.r, mm = r + a.c, ro = rout_of(a);
     const float* V = at<float>(ctx, fp.eig.V);
-    const float* U0 = fp.Us ? at<float>(ctx, fp.Us) : a.U_in;
-    GemmProb p = gp(U0, fp.Us ? fp.nld : n, V, mm, at<float>(ctx, fp.Urot), fp.nld, n, ro, mm, 1.f);
+    const bool us = useUs(a);
+    const float* U0 = us ? at<float>(ctx, fp.Us) : a.U_in;
+    GemmProb p = gp(U0, us ? fp.nld : ldU(a), V, mm, at<float>(ctx, fp.Urot), fp.nld, n, ro, mm, 1.f);
     p.A2 = at<float>(ctx, fp.Qb); p.lda2 = fp.nld;
     p.B2 = at<float>(ctx, fp.Vf); p.ldb2 = a.c;
     p.k1 = r;
@@ -1562,11 +1585,11 @@ bkfac_status bkfac_brand_update(bkfac_ctx ctx, const bkfac_brand_args* args, int
     const float* Ur = at<float>(ctx, fp.Urot);
     if (a.flags & BKFAC_BRAND_NO_REFRESH) {
       EwProb e{};
-      e.Y = a.U_out; e.ldy = n; e.X = Ur; e.ldx = fp.nld; e.rows = n; e.cols = r; e.op = EW_COPY;
+      e.Y = a.U_out; e.ldy = ldU(a); e.X = Ur; e.ldx = fp.nld; e.rows = n; e.cols = r; e.op = EW_COPY;
       ew.push_back(e);
       continue;
     }
-    GemmProb pf = gp(Ur, fp.nld, at<float>(ctx, fp.Gref), r, a.U_out, n, n, r, r, -0.5f, Ur, fp.nld, 1.5f);
+    GemmProb pf = gp(Ur, fp.nld, at<float>(ctx, fp.Gref), r, a.U_out, ldU(a), n, r, r, -0.5f, Ur, fp.nld, 1.5f);
     pf.status = status_ptr(ctx, a.factor);   // the new basis passes this epilogue
     gs.add(false, false, pf, 0);
   }
@@ -1613,11 +1636,12 @@ bkfac_status ea_stage(bkfac_ctx ctx, const bkfac_ea_args* args, int count, GemmS
     if (a.c <= 0 || a.c > fp.d.c_max) return BKFAC_ERR_DIM;
     if (!(a.rho >= 0.f && a.rho < 1.f)) return BKFAC_ERR_INVALID_ARG;
     const int n = fp.d.n;
+    if (!ld_ok(a.ld_M, n)) return BKFAC_ERR_DIM;
     const float* Mp = a.M;
-    int ldm = n;
+    int ldm = ldx(a.ld_M, n);
     for (int j = 0; j < nbrand; ++j)
       if (brand[j].factor == a.factor && brand[j].M == a.M && brand[j].c == a.c && fp.Ms &&
-          !fp.dense) {
+          !fp.dense && ldx(brand[j].ld_M, n) == ldm && !al16(a.M, ldm)) {
         Mp = at<float>(ctx, fp.Ms);
         ldm = fp.nld;
       }
@@ -1710,6 +1734,7 @@ bkfac_status bkfac_light_correction(bkfac_ctx ctx, const bkfac_correct_args* arg
     if (!fp.rsvd) return BKFAC_ERR_INVALID_ARG;
     if (!a.K_dense || !a.U || !a.D || !a.col_idx) return BKFAC_ERR_INVALID_ARG;
     if (a.n_crc < 1 || a.n_crc > fp.d.r) return BKFAC_ERR_DIM;
+    if (!ld_ok(a.ld_U, fp.d.n)) return BKFAC_ERR_DIM;
     for (int j = 0; j < i; ++j)
       if (args[j].factor == a.factor) return BKFAC_ERR_INVALID_ARG;
   }
@@ -1734,9 +1759,9 @@ bkfac_status bkfac_light_correction(bkfac_ctx ctx, const bkfac_correct_args* arg
         ColIdxProb q{};
         q.rows = n; q.idx = a.col_idx; q.n = a.n_crc; q.r = fp.d.r; q.mode = mode;
         q.status = status_ptr(ctx, a.factor);
-        if (mode == 0) { q.src = a.U; q.lds = n; q.dst = at<float>(ctx, fp.Yr); q.ldd = n; }
+        if (mode == 0) { q.src = a.U; q.lds = ldx(a.ld_U, n); q.dst = at<float>(ctx, fp.Yr); q.ldd = n; }
         else {
-          q.src = at<float>(ctx, fp.Q2r); q.lds = n; q.dst = a.U; q.ldd = n;
+          q.src = at<float>(ctx, fp.Q2r); q.lds = n; q.dst = a.U; q.ldd = ldx(a.ld_U, n);
           q.dsrc = at<float>(ctx, fp.Tr); q.ddst = a.D;
         }
         cb.p[k] = q;
@@ -1799,6 +1824,8 @@ bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* ar
   for (int i = 0; i < count; ++i) {
     const auto& a = args[i];
     if (!a.K_dense || !a.U_out || !a.D_out) return BKFAC_ERR_INVALID_ARG;
+    if (a.factor >= 0 && a.factor < (int)ctx->f.size() && !ld_ok(a.ld_U, ctx->f[a.factor].d.n))
+      return BKFAC_ERR_DIM;
     if (a.factor < 0 || a.factor >= (int)ctx->f.size()) return BKFAC_ERR_INVALID_ARG;
     const auto& fp = ctx->f[a.factor];
     if (!fp.rsvd) return BKFAC_ERR_INVALID_ARG;
@@ -1911,12 +1938,12 @@ bkfac_status bkfac_rsvd_overwrite_batch(bkfac_ctx ctx, const bkfac_rsvd_args* ar
     const bool ex = L[i].l == L[i].n;
     eg.push_back(eig_prob(ctx, L[i].fp->eig_r, L[i].l, L[i].r,
                           ex ? args[i].U_out : at<float>(ctx, L[i].fp->eig_r.V),
-                          ex ? L[i].n : L[i].l, args[i].D_out, L[i].status));
+                          ex ? ldx(args[i].ld_U, L[i].n) : L[i].l, args[i].D_out, L[i].status));
   }
   if ((rs = run_eig(ctx, eg, st)) != BKFAC_OK) return rs;
   for (int i : rf)
     gs.add(false, false, gp(L[i].Q, L[i].n, at<float>(ctx, L[i].fp->eig_r.V), L[i].l, args[i].U_out,
-                            L[i].n, L[i].n, L[i].r, L[i].l, 1.f), 0);
+                            ldx(args[i].ld_U, L[i].n), L[i].n, L[i].r, L[i].l, 1.f), 0);
   return run_gemms(ctx, gs, st, "gemm_rsvd_rot");
 }
 
@@ -1950,6 +1977,9 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
       return BKFAC_ERR_INVALID_ARG;
     if (!(a.lambda_A > 0.f) || !(a.lambda_G > 0.f)) return BKFAC_ERR_INVALID_ARG;
     if (a.S == a.J) return BKFAC_ERR_ALIAS;
+    if (!ld_ok(a.ld_UG, d.d_G) || !ld_ok(a.ld_UA, d.d_A) || !ld_ok(a.ld_J, d.d_A) ||
+        !ld_ok(a.ld_S, d.d_A))
+      return BKFAC_ERR_DIM;
     for (int j = 0; j < i; ++j)
       if (args[j].layer == a.layer) return BKFAC_ERR_INVALID_ARG;
   }
@@ -1984,13 +2014,13 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G;
     float* lam = at<float>(ctx, lp.lam);   // {lamA, lamG, 1/(lamG lamA), 1/lamA, 1/lamG}
     if (rA > 0) {   // Y' = (J U_A) diag(sA) / lamG  (scaling in the epilogue)
-      GemmProb p = gp(a.J, dA, a.U_A, dA, at<float>(ctx, lp.Y), dG, dG, rA, dA, 1.f);
+      GemmProb p = gp(a.J, ldx(a.ld_J, dA), a.U_A, ldx(a.ld_UA, dA), at<float>(ctx, lp.Y), lp.ldY, dG, rA, dA, 1.f);
       p.col_scale = at<float>(ctx, lp.sA); p.alpha_dev = lam + 4;
       gemm_ws(p, at<float>(ctx, lp.ws));
       gs.add(true, false, p, lp.ws_elems);
     }
     if (rG > 0) {   // Xt' = (J^T U_G) diag(sG) / lamA
-      GemmProb p = gp(a.J, dA, a.U_G, dG, at<float>(ctx, lp.Xt), dA, dA, rG, dG, 1.f);
+      GemmProb p = gp(a.J, ldx(a.ld_J, dA), a.U_G, ldx(a.ld_UG, dG), at<float>(ctx, lp.Xt), lp.ldXt, dA, rG, dG, 1.f);
       p.col_scale = at<float>(ctx, lp.sG); p.alpha_dev = lam + 3;
       gs.add(false, false, p, 0);
     }
@@ -2002,7 +2032,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     const auto& lp = ctx->l[a.layer];
     const int dG = lp.d.d_G, rA = lp.d.r_A, rG = lp.d.r_G;
     if (rA > 0 && rG > 0) {
-      GemmProb p = gp(a.U_G, dG, at<float>(ctx, lp.Y), dG, at<float>(ctx, lp.Z), rG, rG, rA, dG, 1.f);
+      GemmProb p = gp(a.U_G, ldx(a.ld_UG, dG), at<float>(ctx, lp.Y), lp.ldY, at<float>(ctx, lp.Z), rG, rG, rA, dG, 1.f);
       p.row_scale = at<float>(ctx, lp.sG); p.alpha_dev = at<float>(ctx, lp.lam) + 1;
       gs.add(true, false, p, 0);
     }
@@ -2015,7 +2045,8 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     const int dG = lp.d.d_G, rA = lp.d.r_A, rG = lp.d.r_G;
     if (rA > 0 && rG > 0) {
       float* Y = at<float>(ctx, lp.Y);
-      gs.add(false, false, gp(a.U_G, dG, at<float>(ctx, lp.Z), rG, Y, dG, dG, rA, rG, 1.f, Y, dG, 1.f), 0);
+      gs.add(false, false, gp(a.U_G, ldx(a.ld_UG, dG), at<float>(ctx, lp.Z), rG, Y, lp.ldY, dG, rA, rG, 1.f,
+                              Y, lp.ldY, 1.f), 0);
     }
   }
   if ((rs = run_gemms(ctx, gs, st, "gemm_prec_small")) != BKFAC_OK) return rs;
@@ -2025,11 +2056,12 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     const auto& lp = ctx->l[a.layer];
     const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G;
     float* lam = at<float>(ctx, lp.lam);
-    GemmProb p = gp(rA > 0 ? a.U_A : at<float>(ctx, lp.Xt), dA,
-                    rA > 0 ? at<float>(ctx, lp.Y) : a.U_G, dG, a.S, dA, dA, dG, rA + rG, 1.f,
-                    a.J, dA, 1.f);
-    p.A2 = at<float>(ctx, lp.Xt); p.lda2 = dA;
-    p.B2 = a.U_G ? a.U_G : at<float>(ctx, lp.Y); p.ldb2 = dG;
+    const int ldUA = ldx(a.ld_UA, dA), ldUG = ldx(a.ld_UG, dG);
+    GemmProb p = gp(rA > 0 ? a.U_A : at<float>(ctx, lp.Xt), rA > 0 ? ldUA : lp.ldXt,
+                    rA > 0 ? at<float>(ctx, lp.Y) : a.U_G, rA > 0 ? lp.ldY : ldUG, a.S,
+                    ldx(a.ld_S, dA), dA, dG, rA + rG, 1.f, a.J, ldx(a.ld_J, dA), 1.f);
+    p.A2 = at<float>(ctx, lp.Xt); p.lda2 = lp.ldXt;
+    p.B2 = a.U_G ? a.U_G : at<float>(ctx, lp.Y); p.ldb2 = a.U_G ? ldUG : lp.ldY;
     p.k1 = rA;
     p.beta_dev = lam + 2;
     p.stream_c = 1;   // J read and S written once: evict-first, the operands stay in L2
@@ -2053,6 +2085,9 @@ bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_fact
     if (!(a.lambda_A > 0.f) || !(a.lambda_G > 0.f)) return BKFAC_ERR_INVALID_ARG;
     if (a.n <= 0 || a.n > d.n_max) return BKFAC_ERR_DIM;
     if (a.S == a.G || a.S == a.A) return BKFAC_ERR_ALIAS;
+    if (!ld_ok(a.ld_UG, d.d_G) || !ld_ok(a.ld_UA, d.d_A) || !ld_ok(a.ld_G, d.d_G) ||
+        !ld_ok(a.ld_A, d.d_A) || !ld_ok(a.ld_S, d.d_A))
+      return BKFAC_ERR_DIM;
     for (int j = 0; j < i; ++j)
       if (args[j].layer == a.layer) return BKFAC_ERR_INVALID_ARG;
   }
@@ -2086,13 +2121,13 @@ bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_fact
     const auto& lp = ctx->l[a.layer];
     const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G, n = a.n;
     if (rG > 0) {   // P_G diag(s_G), the scaling in the epilogue
-      GemmProb p = gp(a.G, dG, a.U_G, dG, at<float>(ctx, lp.fPG), n, n, rG, dG, 1.f);
+      GemmProb p = gp(a.G, ldx(a.ld_G, dG), a.U_G, ldx(a.ld_UG, dG), at<float>(ctx, lp.fPG), n, n, rG, dG, 1.f);
       p.col_scale = at<float>(ctx, lp.sG);
       gemm_ws(p, at<float>(ctx, lp.fws));
       gs.add(true, false, p, lp.fws_elems);
     }
     if (rA > 0) {
-      GemmProb p = gp(a.A, dA, a.U_A, dA, at<float>(ctx, lp.fPA), n, n, rA, dA, 1.f);
+      GemmProb p = gp(a.A, ldx(a.ld_A, dA), a.U_A, ldx(a.ld_UA, dA), at<float>(ctx, lp.fPA), n, n, rA, dA, 1.f);
       p.col_scale = at<float>(ctx, lp.sA);
       gemm_ws(p, at<float>(ctx, lp.fws2));
       gs.add(true, false, p, lp.fws_elems);
@@ -2105,13 +2140,13 @@ bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_fact
     const auto& lp = ctx->l[a.layer];
     const int dG = lp.d.d_G, dA = lp.d.d_A, rA = lp.d.r_A, rG = lp.d.r_G, n = a.n;
     float* lam = at<float>(ctx, lp.lam);
-    GemmProb pg = gp(rG > 0 ? a.U_G : a.G, dG, at<float>(ctx, lp.fPG), n, at<float>(ctx, lp.fGb), dG,
-                     dG, n, rG, 1.f, a.G, dG, 1.f);
+    GemmProb pg = gp(rG > 0 ? a.U_G : a.G, rG > 0 ? ldx(a.ld_UG, dG) : ldx(a.ld_G, dG), at<float>(ctx, lp.fPG), n,
+                     at<float>(ctx, lp.fGb), dG, dG, n, rG, 1.f, a.G, ldx(a.ld_G, dG), 1.f);
     pg.beta_dev = lam + 4;
     pg.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);   // every element of G passes here
     gs.add(false, true, pg, 0);
-    GemmProb pa = gp(rA > 0 ? a.U_A : a.A, dA, at<float>(ctx, lp.fPA), n, at<float>(ctx, lp.fAb), dA,
-                     dA, n, rA, 1.f, a.A, dA, 1.f);
+    GemmProb pa = gp(rA > 0 ? a.U_A : a.A, rA > 0 ? ldx(a.ld_UA, dA) : ldx(a.ld_A, dA), at<float>(ctx, lp.fPA), n,
+                     at<float>(ctx, lp.fAb), dA, dA, n, rA, 1.f, a.A, ldx(a.ld_A, dA), 1.f);
     pa.beta_dev = lam + 3;
     pa.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);
     gs.add(false, true, pa, 0);
@@ -2122,7 +2157,8 @@ bkfac_status bkfac_precondition_factored(bkfac_ctx ctx, const bkfac_precond_fact
     const auto& a = args[i];
     const auto& lp = ctx->l[a.layer];
     const int dG = lp.d.d_G, dA = lp.d.d_A, n = a.n;
-    gs.add(false, true, gp(at<float>(ctx, lp.fAb), dA, at<float>(ctx, lp.fGb), dG, a.S, dA, dA, dG, n, 1.f), 0);
+    gs.add(false, true, gp(at<float>(ctx, lp.fAb), dA, at<float>(ctx, lp.fGb), dG, a.S, ldx(a.ld_S, dA), dA, dG,
+                           n, 1.f), 0);
   }
   return run_gemms(ctx, gs, st, "gemm_f2_out");
 }

@@ -36,6 +36,25 @@ def layer_cost(n_A: int, n_G: int) -> float:
     return float(n_A) ** 3 + float(n_G) ** 3
 
 
+LD_ALIGN = 32
+
+
+def padded(rows: int, cols: int, device, zero: bool = True):
+    """A (rows, cols) float32 view of a (rows, cols rounded up to 32) buffer: the row
+    stride is the operand's leading dimension (bkfac.h "Leading dimensions"), a multiple of
+    32 floats, so every contraction reads it with 16-byte loads.  The padding is never read."""
+    import torch
+    ld = (cols + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN
+    make = torch.zeros if zero else torch.empty
+    return make((rows, ld), dtype=torch.float32, device=device)[:, :cols]
+
+
+def full_rows(t):
+    """The whole padded buffer behind a padded() view (rows x leading dimension)."""
+    import torch
+    return torch.as_strided(t, (t.shape[0], t.stride(0)), (t.stride(0), 1))
+
+
 class BKFACStack:
     """Owns the per-factor state (ping-pong U/D buffers, optional dense EA factor) of
     the factors a rank owns and runs whole steps through the bkfac C ABI."""
@@ -98,7 +117,7 @@ class BKFACStack:
         for g in self.my_factors:
             n, r, _ = self.factors[g]
             ro = self.rank_out(g)
-            self.U.append([torch.zeros((ro, n), dtype=torch.float32, device=dev) for _ in range(2)])
+            self.U.append([padded(ro, n, dev) for _ in range(2)])
             self.D.append([torch.zeros((ro,), dtype=torch.float32, device=dev) for _ in range(2)])
             self.K.append(torch.zeros((n, n), dtype=torch.float32, device=dev) if rsvd_every > 0 else None)
         self.cur = [0] * len(self.my_factors)
@@ -112,7 +131,7 @@ class BKFACStack:
         for li in self.my_layers:
             dG, dA, _, _ = self.layers[li]
             for par in range(2):
-                self.S2[par][li] = torch.empty((dG, dA), dtype=torch.float32, device=dev)
+                self.S2[par][li] = padded(dG, dA, dev, zero=False)
 
     def bind_outputs(self, by_parity: Sequence[Dict[int, "torch.Tensor"]]) -> None:
         """Precondition straight into caller buffers (e.g. SlotGather.send_views(b)): the
@@ -123,8 +142,9 @@ class BKFACStack:
             for li in self.my_layers:
                 t = by_parity[par][li]
                 dG, dA, _, _ = self.layers[li]
-                if tuple(t.shape) != (dG, dA) or not t.is_contiguous():
-                    raise ValueError(f"output buffer of layer {li} must be a contiguous ({dG}, {dA}) tensor")
+                if tuple(t.shape) != (dG, dA) or t.stride(1) != 1 or t.stride(0) < dA:
+                    raise ValueError(f"output buffer of layer {li} must be a ({dG}, {dA}) tensor "
+                                     "with unit stride along its rows")
                 self.S2[par][li] = t
 
     # ---------------------------------------------------------------------------------

@@ -954,3 +954,81 @@ def test_rank_share_bitwise_equal_to_full_run(cuda_lib):
             assert torch.equal(a, b), f"factor {g} differs"
     for li in range(6):
         assert torch.equal(res["full"][1][li], res["rank"][1][li]), f"layer {li} differs"
+
+
+# ------------------------------------------------------------------ leading dimensions
+
+def _padded_copy(t, extra):
+    """t (rows, cols) copied into a view of a (rows, cols + extra) buffer (row stride
+    cols + extra); the padding holds NaN so that a read of it would poison the result."""
+    import torch
+    buf = torch.full((t.shape[0], t.shape[1] + extra), float("nan"), dtype=t.dtype, device=t.device)
+    v = buf[:, :t.shape[1]]
+    v.copy_(t)
+    return v
+
+
+@pytest.mark.parametrize("extra", [3, 31])
+def test_leading_dimensions_bitwise(cuda_lib, extra):
+    """bkfac.h "Leading dimensions": the same Brand update, EA accumulate, RSVD overwrite,
+    light correction and both preconditioners on packed odd layouts (n = 577, d_A = 577:
+    internal aligned copies / 4-byte loads) and on padded views (row stride n + extra:
+    extra = 31 makes it a multiple of 32 -> caller buffers read directly with 16-byte loads;
+    extra = 3 keeps it odd) give bitwise equal results, and the padding (NaN) is neither
+    read nor written."""
+    import torch
+    from paper_2210_08494_b200 import binding
+    dev = "cuda:0"
+    n, c, r, dG = 577, 64, 100, 320
+    f = synth.random_case(n, c, r, seed=4242, k=2 * c, decay=0.9)
+    M = torch.from_numpy(f.batch(0).T.astype(np.float32).copy()).to(dev)      # (c, n)
+    U0 = torch.from_numpy(synth.phantom_basis(n, r).T.astype(np.float32).copy()).to(dev)
+    fg = synth.random_case(dG, c, r, seed=4243, k=2 * c, decay=0.9)
+    MG = torch.from_numpy(fg.batch(0).T.astype(np.float32).copy()).to(dev)
+    UG0 = torch.from_numpy(synth.phantom_basis(dG, r).T.astype(np.float32).copy()).to(dev)
+    J = torch.from_numpy(0.1 * np.random.default_rng(7).standard_normal((dG, n)).astype(np.float32)).to(dev)
+    idx = torch.arange(0, r, 3, dtype=torch.int32, device=dev)
+
+    def run(pad):
+        lay = (lambda t: _padded_copy(t, extra)) if pad else (lambda t: t.clone())
+        ctx = binding.Context([(n, r, c, binding.BKFAC_FACTOR_DENSE_EA), (dG, r, c, 0)],
+                              [(dG, n, r, r, c)], device=0)
+        # the two-stage eigensolver is deterministic (the one-stage cluster kernel sums
+        # partial y with shared-memory atomics: run-to-run rounding differences)
+        ctx.bkfac_set_option(binding.BKFAC_OPT_TWO_STAGE, 2)
+        UA = [lay(U0), lay(torch.zeros_like(U0))]
+        UG = [lay(UG0), lay(torch.zeros_like(UG0))]
+        DA = [torch.zeros(r, device=dev) for _ in range(2)]
+        DG = [torch.zeros(r, device=dev) for _ in range(2)]
+        Mv, MGv, Jv = lay(M), lay(MG), lay(J)
+        K = torch.zeros((n, n), device=dev)
+        ctx.bkfac_ea_batch([dict(factor=0, K=K, M=Mv, rho=0.0)])
+        ctx.bkfac_brand_update([dict(factor=0, U_in=UA[0], D_in=DA[0], M=Mv, U_out=UA[1], D_out=DA[1],
+                                     alpha=0.0, beta=1.0),
+                                dict(factor=1, U_in=UG[0], D_in=DG[0], M=MGv, U_out=UG[1], D_out=DG[1],
+                                     alpha=0.0, beta=1.0)])
+        ctx.bkfac_brand_update([dict(factor=0, U_in=UA[1], D_in=DA[1], M=Mv, U_out=UA[0], D_out=DA[0],
+                                     alpha=0.95, beta=0.05)])
+        S = lay(torch.zeros((dG, n), device=dev))
+        ctx.bkfac_precondition([dict(layer=0, U_G=UG[1], D_G=DG[1], lambda_G=0.1, U_A=UA[0], D_A=DA[0],
+                                     lambda_A=0.1, J=Jv, S=S)])
+        Sf = lay(torch.zeros((dG, n), device=dev))
+        ctx.bkfac_precondition_factored([dict(layer=0, U_G=UG[1], D_G=DG[1], lambda_G=0.1, U_A=UA[0],
+                                              D_A=DA[0], lambda_A=0.1, G=MGv, A=Mv, S=Sf)])
+        Ur, Dr = lay(torch.zeros_like(U0)), torch.zeros(r, device=dev)
+        ctx.bkfac_rsvd_batch([dict(factor=0, K=K, oversample=10, power_iters=2, seed=5, counter=0,
+                                   U_out=Ur, D_out=Dr)])
+        ctx.bkfac_light_correction([dict(factor=0, K=K, U=Ur, D=Dr, col_idx=idx)])
+        torch.cuda.synchronize()
+        assert ctx.bkfac_check()[0] == 0
+        outs = [UA[0], DA[0], UG[1], DG[1], S, Sf, Ur, Dr]
+        if pad:   # the padding columns still hold NaN (never written)
+            for t in (UA[0], UG[1], S, Sf, Ur):
+                full = torch.as_strided(t, (t.shape[0], t.stride(0)), (t.stride(0), 1))
+                assert torch.isnan(full[:, t.shape[1]:]).all()
+        return [t.clone() for t in outs]
+
+    a, b = run(False), run(True)
+    for x, y in zip(a, b):
+        assert torch.isfinite(x).all()
+        assert torch.equal(x, y)
