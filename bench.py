@@ -674,17 +674,49 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
     t0 = time.perf_counter()
     run(steps)
     sec = time.perf_counter() - t0
-    t = torch.tensor([sec], dtype=torch.float64, device=device)
+
+    # the link bound of this leg: the same copies (H2D of the inputs and D2H of S on their
+    # two streams, concurrently) with no compute, wall clock per step
+    def copies_only(n):
+        for j in range(n):
+            b = j & 1
+            with torch.cuda.stream(up):
+                for g, t in dev_M[b].items():
+                    full_rows(t).copy_(host_M[g], non_blocking=True)
+                if not args.factored:
+                    for li, t in dev_J[b].items():
+                        l = cfg.layers[li]
+                        full_rows(t).copy_(host_J[(l.d_G, l.d_A)], non_blocking=True)
+            with torch.cuda.stream(down):
+                for li in stack.my_layers:
+                    l = cfg.layers[li]
+                    s_ = stack.S2[b][li]
+                    hs = host_S[(l.d_G, l.d_A)]
+                    if s_.stride(0) == hs.shape[1]:
+                        hs.copy_(full_rows(s_), non_blocking=True)
+                    else:
+                        hs[:, :l.d_A].copy_(s_, non_blocking=True)
+        torch.cuda.synchronize()
+    copies_only(1)
+    t1 = time.perf_counter()
+    copies_only(steps)
+    link_sec = time.perf_counter() - t1
+    t = torch.tensor([sec, link_sec], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sec = float(t[0])
+        sec, link_sec = float(t[0]), float(t[1])
         hd = torch.tensor([h2d, d2h], dtype=torch.float64, device=device)
         dist.all_reduce(hd, op=dist.ReduceOp.SUM)
         h2d, d2h = int(hd[0]), int(hd[1])
     return {"value": round(len(cfg.factors) * steps / sec, 3), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "ms_per_step": round(1e3 * sec / steps, 3),
+            "copies_only_ms_per_step": round(1e3 * link_sec / steps, 3),
+            "link_frac": round(link_sec / sec, 4),
             "timing": "wall clock around every step's pinned-host H2D copies, the step and the D2H read of S "
-                      "(copies of step i+1 / i-1 overlapped with step i on two copy streams), max over ranks"}
+                      "(copies of step i+1 / i-1 overlapped with step i on two copy streams), max over ranks; "
+                      "copies_only_ms_per_step: the same H2D + D2H copies with no compute (the PCIe bound "
+                      "of this leg), link_frac = copies-only time / e2e time"}
 
 
 def main():

@@ -124,7 +124,9 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
  *   BKFAC_OPT_BT_SIMT     != 0: back-transform Gram/T products on the fp32 SIMT GEMM
  *   BKFAC_OPT_CHOL_BLOCKED Cholesky of orders > 256: 1 (default) blocked with the panel solve,
  *                         trailing SYRK and inverse on the tcgen05 GEMM, 0 one tiled CTA or
- *                         cluster per factor on CUDA cores */
+ *                         cluster per factor on CUDA cores
+ *   BKFAC_OPT_NVTX        != 0: every stage of every call inside a host NVTX range named by
+ *                         its stage tag (profiling: ncu --nvtx --nvtx-include "<tag>/") */
 #define BKFAC_OPT_TWO_STAGE 1
 #define BKFAC_OPT_GT_CLUSTER 2
 #define BKFAC_OPT_GEMM_PAIR 3
@@ -134,6 +136,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
 #define BKFAC_OPT_SYT_CLUSTER 7
 #define BKFAC_OPT_BT_SIMT 8
 #define BKFAC_OPT_CHOL_BLOCKED 9
+#define BKFAC_OPT_NVTX 10
 bkfac_status bkfac_set_option(bkfac_ctx ctx, int option, int value);
 
 size_t bkfac_workspace_bytes(bkfac_ctx ctx);

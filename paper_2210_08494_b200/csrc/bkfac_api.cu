@@ -2,6 +2,7 @@
 // the stream-ordered stage sequence of each call.  All arithmetic runs in the kernels
 // of gemm_*.cuh, chol.cuh, eig.cuh and misc.cuh.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -141,6 +142,7 @@ struct bkfac_ctx_s {
   cudaStream_t ea_stream = nullptr;
   cudaEvent_t ev_ea_fork = nullptr, ev_ea_done = nullptr;
   std::function<bkfac_status(int)> pending_ea;
+  int nvtx = 0;       // BKFAC_OPT_NVTX: every stage inside an NVTX range named by its tag
   int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs; < 0: one CTA per tile
   bool ea_join_early = false;   // join the side-stream EA right after the tridiagonalisation
   int pair_mode = 1;  // CTA-pair GEMM tiles: 0 never, 1 large long-K stages, 2 always (tests)
@@ -202,6 +204,7 @@ void prof_record(cudaEvent_t e, cudaStream_t st) {
 
 // Brackets one stage (one or more kernel launches on `st`) with CUDA events.
 void prof_begin(bkfac_ctx c, const char* tag, cudaStream_t st, double flops, double bytes) {
+  if (c->nvtx) nvtxRangePushA(tag);   // host ranges: ncu --nvtx --nvtx-include "<stage>/"
   if (!c->prof) return;
   bkfac_ctx_s::Rec r;
   r.tag = tag; r.flops = flops; r.bytes = bytes; r.launches = c->launches;
@@ -211,6 +214,7 @@ void prof_begin(bkfac_ctx c, const char* tag, cudaStream_t st, double flops, dou
   c->open_rec = (int)c->recs.size() - 1;
 }
 void prof_end(bkfac_ctx c, cudaStream_t st) {
+  if (c->nvtx) nvtxRangePop();
   if (!c->prof || c->open_rec < 0) return;
   auto& r = c->recs[c->open_rec];
   prof_record(r.b, st);
@@ -1171,6 +1175,7 @@ bkfac_status bkfac_set_option(bkfac_ctx c, int option, int value) {
   if (!c) return BKFAC_ERR_INVALID_ARG;
   switch (option) {
     case BKFAC_OPT_TWO_STAGE: if (value < 0 || value > 2) return BKFAC_ERR_INVALID_ARG; c->two_stage = value; break;
+    case BKFAC_OPT_NVTX: c->nvtx = value != 0; break;
     case BKFAC_OPT_GT_CLUSTER: if (value < 1 || value > 8) return BKFAC_ERR_INVALID_ARG; c->gt_cluster = value; break;
     case BKFAC_OPT_GEMM_PAIR: if (value < 0 || value > 2) return BKFAC_ERR_INVALID_ARG; c->pair_mode = value; break;
     case BKFAC_OPT_GEMM_SIMT: c->use_tc = value == 0; break;

@@ -15,6 +15,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--blocks", type=int, default=24)
     ap.add_argument("--warm", type=int, default=2)
+    ap.add_argument("--stage-nvtx", action="store_true",
+                    help="library NVTX ranges per stage (BKFAC_OPT_NVTX) instead of brand/prec")
     args = ap.parse_args()
     import torch
     import synth
@@ -29,6 +31,11 @@ def main():
     for i in range(args.warm):
         st.step(M_pool[i % 2], J_pool[i % 2])
     torch.cuda.synchronize()
+    from paper_2210_08494_b200 import binding
+    if args.stage_nvtx:
+        st.ctx.bkfac_set_option(binding.BKFAC_OPT_NVTX, 1)
+    push = (lambda name: None) if args.stage_nvtx else torch.cuda.nvtx.range_push
+    pop = (lambda: None) if args.stage_nvtx else torch.cuda.nvtx.range_pop
     # one more step, its two library calls in NVTX ranges (same order as BKFACStack._step)
     k = st.k
     ups = []
@@ -36,10 +43,10 @@ def main():
         c, nx = st.cur[i], 1 - st.cur[i]
         ups.append(dict(factor=i, U_in=st.U[i][c], D_in=st.D[i][c], M=M_pool[k % 2][g],
                         U_out=st.U[i][nx], D_out=st.D[i][nx], alpha=st.rho, beta=1 - st.rho))
-    torch.cuda.nvtx.range_push("brand")
+    push("brand")
     st.ctx.bkfac_brand_update(ups)
     torch.cuda.synchronize()
-    torch.cuda.nvtx.range_pop()
+    pop()
     for i in range(len(st.my_factors)):
         st.cur[i] = 1 - st.cur[i]
     items = []
@@ -49,10 +56,10 @@ def main():
         UA, DA = st.state(a)
         items.append(dict(layer=lj, U_G=UG, D_G=DG, lambda_G=st.lam, U_A=UA, D_A=DA, lambda_A=st.lam,
                           J=J_pool[k % 2][li], S=st.S2[0][li]))
-    torch.cuda.nvtx.range_push("prec")
+    push("prec")
     st.ctx.bkfac_precondition(items)
     torch.cuda.synchronize()
-    torch.cuda.nvtx.range_pop()
+    pop()
     assert st.check()[0] == 0
     print("prof_cfg5 ok")
 
