@@ -47,6 +47,8 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg5")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-sets", type=int, default=2,
+                    help="device input sets of the e2e leg, used round robin (uploads run ahead)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
@@ -607,27 +609,29 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
         if key not in host_J:
             host_J[key] = full_rows(J_pool[0][li]).cpu().pin_memory()
             host_S[key] = torch.empty(tuple(host_J[key].shape), dtype=torch.float32).pin_memory()
-    # two device input sets: step i+1's host->device copies run (copy stream) while step i
-    # computes; step i's S is read back (second copy stream) while step i+1 computes
+    # NB device input sets, used round robin: the host->device copies of steps i+1 .. i+NB-1
+    # run back to back on the copy stream while step i computes (with NB = 2 the next upload
+    # could only start when the step two back had finished, which serialises copies and
+    # compute once the copies are the longer of the two); step i's S is read back on a second
+    # copy stream while step i+1 computes (the stack's two S sets, by step parity)
+    NB = max(2, args.e2e_sets)
     dev_M = [{g: padded(cfg.factors[g].c, cfg.factors[g].n, device, zero=False)
-              for g in stack.my_factors} for _ in range(2)]
+              for g in stack.my_factors} for _ in range(NB)]
     dev_J = [{li: padded(cfg.layers[li].d_G, cfg.layers[li].d_A, device, zero=False)
-              for li in stack.my_layers} for _ in range(2)]
+              for li in stack.my_layers} for _ in range(NB)]
     h2d = sum(4 * full_rows(t).numel() for t in dev_M[0].values()) + \
         (0 if args.factored else sum(4 * full_rows(t).numel() for t in dev_J[0].values()))
     d2h = sum(4 * host_S[(cfg.layers[li].d_G, cfg.layers[li].d_A)].numel() for li in stack.my_layers)
     use_graphs = not args.no_graphs
     up, down = torch.cuda.Stream(device=device), torch.cuda.Stream(device=device)
-    ev_up = [torch.cuda.Event() for _ in range(2)]
-    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_up = [torch.cuda.Event() for _ in range(NB)]
+    ev_done = [torch.cuda.Event() for _ in range(NB)]
     ev_down = [torch.cuda.Event() for _ in range(2)]
-    # the input set and the S set a step uses alternate with the step's parity
-    par0 = stack.k & 1
 
     def upload(j):
-        b = (j + par0) & 1
+        b = j % NB
         with torch.cuda.stream(up):
-            up.wait_event(ev_done[b])             # step j-2 (same buffers) has finished
+            up.wait_event(ev_done[b])             # step j-NB (same buffers) has finished
             for g, t in dev_M[b].items():
                 full_rows(t).copy_(host_M[g], non_blocking=True)
             if not args.factored:
@@ -637,21 +641,22 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
             ev_up[b].record(up)
 
     def run(n):
-        upload(0)
+        for j in range(min(NB - 1, n)):
+            upload(j)
         for j in range(n):
-            b = (j + par0) & 1
-            stream.wait_event(ev_up[b])
-            stream.wait_event(ev_down[b])         # S set b was read back (step j-2)
-            if gather is not None:
-                gather.finish(stack.k & 1)
+            b = j % NB
             sb = stack.k & 1
+            stream.wait_event(ev_up[b])
+            stream.wait_event(ev_down[sb])        # S set sb was read back (step j-2)
+            if gather is not None:
+                gather.finish(sb)
             S = stack.step(dev_M[b], None if args.factored else dev_J[b], graph=use_graphs,
                            factored=args.factored)
             if gather is not None:
                 gather.start(sb)
             ev_done[b].record(stream)
-            if j + 1 < n:
-                upload(j + 1)
+            if j + NB - 1 < n:
+                upload(j + NB - 1)
             with torch.cuda.stream(down):
                 down.wait_event(ev_done[b])
                 for li, s_ in S.items():
@@ -661,13 +666,12 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
                         hs.copy_(full_rows(s_), non_blocking=True)
                     else:   # S bound to packed send slots (N > 1)
                         hs[:, :l.d_A].copy_(s_, non_blocking=True)
-                ev_down[b].record(down)
+                ev_down[sb].record(down)
         if gather is not None:
             gather.finish(0); gather.finish(1)
         torch.cuda.synchronize()
 
-    run(2)                  # untimed: captures this input set's graphs
-    par0 = stack.k & 1
+    run(2 * NB)             # untimed: captures the graphs of every (U parity, input set) pair
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -713,8 +717,10 @@ def run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool):
             "ms_per_step": round(1e3 * sec / steps, 3),
             "copies_only_ms_per_step": round(1e3 * link_sec / steps, 3),
             "link_frac": round(link_sec / sec, 4),
+            "input_sets": NB,
             "timing": "wall clock around every step's pinned-host H2D copies, the step and the D2H read of S "
-                      "(copies of step i+1 / i-1 overlapped with step i on two copy streams), max over ranks; "
+                      "(uploads of the next input sets and the read-back of step i-1 overlapped with step i "
+                      "on two copy streams), max over ranks; "
                       "copies_only_ms_per_step: the same H2D + D2H copies with no compute (the PCIe bound "
                       "of this leg), link_frac = copies-only time / e2e time"}
 

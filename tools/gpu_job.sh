@@ -1,10 +1,7 @@
 # Scratch job for one gpurun call (rewritten per call; the outputs land in gpurun_out/).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 300 python tools/prof_cfg5.py --stage-nvtx > gpurun_out/s2h_prof_plain.log 2>&1 && \
-ncu --set full --import-source on --nvtx --nvtx-include "gemm_sbr_update/" -k regex:gemm_tc -c 1 -o gpurun_out/s2h_sbrupd python tools/prof_cfg5.py --stage-nvtx > gpurun_out/s2h_ncu1.log 2>&1
-ncu --set full --import-source on --nvtx --nvtx-include "gemm_resid/" -k regex:gemm_tc -c 1 -o gpurun_out/s2h_resid python tools/prof_cfg5.py --stage-nvtx > gpurun_out/s2h_ncu2.log 2>&1
-ncu --set full --import-source on --nvtx --nvtx-include "gemm_sbr_x/" -k regex:gemm_tc -c 1 -o gpurun_out/s2h_sbrx python tools/prof_cfg5.py --stage-nvtx > gpurun_out/s2h_ncu3.log 2>&1
-timeout 600 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/s2h_bench_small.json 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"gemm_tc|gemm_splitk|sbr_|chol|bisect|invit|cluster|backtr|ew_|prec_|nonfinite|sytrd|philox|colidx" --csv --log-file gpurun_out/s2h_launches_cfg5.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/s2h_ncu_launches.log 2>&1
-echo done
+timeout 900 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_parity.py -x -q -k "gemm or two_stage or leading or cfg5_factor_shape or ea_accumulate" > gpurun_out/s2i_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/s2i_pytest.log
+timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/s2i_bench.json 2> gpurun_out/s2i_bench.err
+echo "bench rc=$?" >> gpurun_out/s2i_bench.err
