@@ -51,6 +51,8 @@ def parse_args():
                     help="device input sets of the e2e leg, used round robin (uploads run ahead)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ignore-status", action="store_true",
+                    help="tuning runs of deliberately broken library variants: report stage times anyway")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     ap.add_argument("--pool", type=int, default=2, help="distinct input batches kept on device")
     ap.add_argument("--full-rank", action="store_true",
@@ -443,7 +445,7 @@ def run_ours(args, rank, world, local_rank):
         one_step(i, use_graphs)
     torch.cuda.synchronize()
     code, bad, info = stack.check()
-    if code != 0:
+    if code != 0 and not args.ignore_status:
         raise SystemExit(f"device status error after warm-up (factor {bad})")
 
     def timed(first, nsteps, graph, profile=False):
@@ -515,7 +517,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
         ms, launches = float(tmax[0]), int(tsum[1])
     code, bad, info = stack.check()
-    if code != 0:
+    if code != 0 and not args.ignore_status:
         raise SystemExit(f"device status error in the timed region (factor {bad})")
 
     n_f, n_l = len(cfg.factors), len(cfg.layers)

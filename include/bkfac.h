@@ -126,7 +126,10 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
  *                         trailing SYRK and inverse on the tcgen05 GEMM, 0 one tiled CTA or
  *                         cluster per factor on CUDA cores
  *   BKFAC_OPT_NVTX        != 0: every stage of every call inside a host NVTX range named by
- *                         its stage tag (profiling: ncu --nvtx --nvtx-include "<tag>/") */
+ *                         its stage tag (profiling: ncu --nvtx --nvtx-include "<tag>/")
+ *   BKFAC_OPT_SBR_X       two-stage band reduction: 1 (default) X = A22 V on the CUDA cores
+ *                         from the lower triangle and lower-only block updates, 0 X and the
+ *                         mirrored update both on the tcgen05 GEMM (full symmetric storage) */
 #define BKFAC_OPT_TWO_STAGE 1
 #define BKFAC_OPT_GT_CLUSTER 2
 #define BKFAC_OPT_GEMM_PAIR 3
@@ -137,6 +140,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
 #define BKFAC_OPT_BT_SIMT 8
 #define BKFAC_OPT_CHOL_BLOCKED 9
 #define BKFAC_OPT_NVTX 10
+#define BKFAC_OPT_SBR_X 11
 bkfac_status bkfac_set_option(bkfac_ctx ctx, int option, int value);
 
 size_t bkfac_workspace_bytes(bkfac_ctx ctx);

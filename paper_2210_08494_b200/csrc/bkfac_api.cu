@@ -55,7 +55,7 @@ struct Arena {
 
 struct EigWs {  // workspace of one eigen problem of order <= m with <= r outputs
   size_t K, d, e, tau, lam, Y, scr, piv, V, gt, U, Z, S;
-  size_t Vp = 0, Xp = 0, Wp = 0, Tp = 0, AB = 0, Vq = 0, tq = 0;   // two-stage (sbr.cuh)
+  size_t Vp = 0, Vt = 0, Xp = 0, Wp = 0, Tp = 0, AB = 0, Vq = 0, tq = 0;   // two-stage (sbr.cuh)
   bool sbr = false;   // two-stage workspace planned (sbr_supported(m))
   int m, r;
 };
@@ -67,7 +67,7 @@ void plan_eig(Arena& a, EigWs& w, int m, int r) {
   w.sbr = sbr_supported(m);
   if (w.sbr) {
     const size_t mb = sizeof(float) * (size_t)m * SBR_B;
-    w.Vp = a.take(mb); w.Xp = a.take(mb); w.Wp = a.take(mb);
+    w.Vp = a.take(mb); w.Vt = a.take(mb); w.Xp = a.take(mb); w.Wp = a.take(mb);
     w.Tp = a.take(sizeof(float) * SBR_B * SBR_B);
     w.AB = a.take(sizeof(float) * (size_t)m * SBR_LDB);
     w.Vq = a.take(sizeof(float) * (size_t)m * sbr_tasks(m) * SBR_B);
@@ -143,6 +143,7 @@ struct bkfac_ctx_s {
   cudaEvent_t ev_ea_fork = nullptr, ev_ea_done = nullptr;
   std::function<bkfac_status(int)> pending_ea;
   int nvtx = 0;       // BKFAC_OPT_NVTX: every stage inside an NVTX range named by its tag
+  int sbr_x = 1;      // BKFAC_OPT_SBR_X: band reduction's X on the CUDA cores, lower-only updates
   int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs; < 0: one CTA per tile
   bool ea_join_early = false;   // join the side-stream EA right after the tridiagonalisation
   int pair_mode = 1;  // CTA-pair GEMM tiles: 0 never, 1 large long-K stages, 2 always (tests)
@@ -661,19 +662,36 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
     sbr_panel_kernel<<<(unsigned)n, SBR_PANEL_THREADS, sbr_panel_smem_bytes(mmax), st>>>(b, j);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
-    for (int i = 0; i < n; ++i) {     // X = A22 V
-      const EigProb& q = b.p[i];
-      if (!q.sbr || j >= sbr_panels(q.m)) continue;
-      const int r0 = (j + 1) * B, L = q.m - r0;
-      float* A22 = q.K + r0 + (long)r0 * q.ldk;
-      gs.add(false, false, gp(A22, q.ldk, q.Vp + r0, q.m, q.Xp + r0, q.m, L, B, L, 1.f), 0);
+    if (ctx->sbr_x) {   // X = A22 V from the lower triangle (CUDA cores, sbr_x_kernel)
+      double xf = 0.0, xb = 0.0;
+      int lmax = 0;
+      for (int i = 0; i < n; ++i) {
+        if (!b.p[i].sbr || j >= sbr_panels(b.p[i].m)) continue;
+        const double L = b.p[i].m - (j + 1) * B;
+        xf += 2.0 * L * L * B;
+        xb += 4.0 * L * L;
+        lmax = std::max(lmax, (int)L);
+      }
+      prof_begin(ctx, "eig_sbr_x", st, xf, xb);
+      sbr_x_kernel<<<dim3((unsigned)ceil_div(lmax, SBR_X_ROWS), (unsigned)n), SBR_X_THREADS, sbr_x_smem_bytes(), st>>>(b, j);
+      LAUNCH_CHECK(ctx);
+      prof_end(ctx, st);
+    } else {
+      for (int i = 0; i < n; ++i) {     // X = A22 V
+        const EigProb& q = b.p[i];
+        if (!q.sbr || j >= sbr_panels(q.m)) continue;
+        const int r0 = (j + 1) * B, L = q.m - r0;
+        float* A22 = q.K + r0 + (long)r0 * q.ldk;
+        gs.add(false, false, gp(A22, q.ldk, q.Vp + r0, q.m, q.Xp + r0, q.m, L, B, L, 1.f), 0);
+      }
+      if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_x")) != BKFAC_OK) return rs;
     }
-    if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_x")) != BKFAC_OK) return rs;
     prof_begin(ctx, "eig_sbr_w", st, pf, 0.0);
     sbr_w_kernel<<<(unsigned)n, SBR_W_WARPS * 32, sbr_w_smem_bytes(), st>>>(b, j);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
-    for (int i = 0; i < n; ++i) {     // A22 -= V W^T + W V^T  (symmetric: lower tiles, mirrored)
+    // A22 -= V W^T + W V^T  (symmetric: lower tiles; mirrored only while X reads full storage)
+    for (int i = 0; i < n; ++i) {
       const EigProb& q = b.p[i];
       if (!q.sbr || j >= sbr_panels(q.m)) continue;
       const int r0 = (j + 1) * B, L = q.m - r0;
@@ -682,7 +700,7 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
       pu.A2 = q.Wp + r0; pu.lda2 = q.m;
       pu.B2 = q.Vp + r0; pu.ldb2 = q.m;
       pu.k1 = B;
-      pu.sym = 1;
+      pu.sym = ctx->sbr_x ? 2 : 1;
       gs.add(false, true, pu, 0);
     }
     if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_update")) != BKFAC_OK) return rs;
@@ -972,6 +990,7 @@ EigProb eig_prob(bkfac_ctx ctx, const EigWs& w, int m, int r, float* V, int ldv,
   p.sbr = use_sbr(ctx, w, m) ? 1 : 0;
   p.off = p.sbr ? SBR_B : 1;
   p.Vp = w.sbr ? at<float>(ctx, w.Vp) : nullptr;
+  p.Vt = w.sbr ? at<float>(ctx, w.Vt) : nullptr;
   p.Xp = w.sbr ? at<float>(ctx, w.Xp) : nullptr;
   p.Wp = w.sbr ? at<float>(ctx, w.Wp) : nullptr;
   p.Tp = w.sbr ? at<float>(ctx, w.Tp) : nullptr;
@@ -1145,6 +1164,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   attr_ok &= cudaFuncSetAttribute(chol_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT_SMEM_BYTES) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem_bytes(32 * CS_MAXNB)) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sbr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_panel_smem_bytes(SBR_MAX_L + SBR_B)) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sbr_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_x_smem_bytes()) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sbr_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_w_smem_bytes()) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sbr_chase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_chase_smem_bytes()) == cudaSuccess;
   attr_ok &= tc_init_attributes();
@@ -1176,6 +1196,7 @@ bkfac_status bkfac_set_option(bkfac_ctx c, int option, int value) {
   switch (option) {
     case BKFAC_OPT_TWO_STAGE: if (value < 0 || value > 2) return BKFAC_ERR_INVALID_ARG; c->two_stage = value; break;
     case BKFAC_OPT_NVTX: c->nvtx = value != 0; break;
+    case BKFAC_OPT_SBR_X: c->sbr_x = value != 0; break;
     case BKFAC_OPT_GT_CLUSTER: if (value < 1 || value > 8) return BKFAC_ERR_INVALID_ARG; c->gt_cluster = value; break;
     case BKFAC_OPT_GEMM_PAIR: if (value < 0 || value > 2) return BKFAC_ERR_INVALID_ARG; c->pair_mode = value; break;
     case BKFAC_OPT_GEMM_SIMT: c->use_tc = value == 0; break;

@@ -190,6 +190,10 @@ sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
     K[(r0 + l) + (long)(c0 + i) * ld] = x;
     p.Vp[(r0 + l) + (long)i * m] = (l < i) ? 0.f : (l == i ? 1.f : x);
   }
+  for (int e = tid; e < L * B; e += NT) {   // row-major copy for the X kernel's tile copies
+    const int l = e / B, i = e % B;
+    p.Vt[(long)(r0 + l) * B + i] = (l < i) ? 0.f : (l == i ? 1.f : P[l * LDP + i]);
+  }
   for (int e = tid; e < B * B; e += NT) {
     const int a = e % B, c = e / B;
     p.Tp[a + c * B] = T[a * LDT + c];
@@ -292,6 +296,168 @@ sbr_w_kernel(const __grid_constant__ EigBatch b, int j) {
     for (int a = 0; a < B; ++a)
       if (ok) W[(rb + lane) + (long)a * m] = xs[lane * LDT + a];
     __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------- stage 1: X = A22 V
+// grid (row blocks of SBR_X_ROWS, nprob), block SBR_X_THREADS.  Only the lower triangle of
+// A22 is kept current (the block update writes lower tiles only), so element (i, k) of the
+// symmetric A22 is read from K(i, k) when i >= k and from K(k, i) otherwise.  The CTA walks
+// the 32-deep k tiles of its 128 rows through a SBR_X_STAGES-deep cp.async ring (three tiles
+// in flight while one is multiplied, no staging registers), each tile k-major in shared
+// memory:
+//   below the diagonal   16-byte copies along i (4 rows of a stored column), linear As[k][i];
+//   above / crossing it  4-byte copies along k (the stored block read transposed) scattered
+//                        to their k rows, with the 4-float row groups XOR-swizzled by k so that
+//                        the scatter and the compute reads are conflict-free; on a crossing
+//                        tile every element comes from the pattern that reads it from the
+//                        lower triangle; zero-filled out of range;
+//   V                    16-byte copies of the row-major V tile (Vt, written by the panel kernel).
+// Exact fp32 FMAs on the CUDA cores: X = A22 V is 16 flop per byte of A22 with N = 32, an
+// HBM-streaming product, not a tensor-core one (the tcgen05 GEMM reached 1.6 TB/s here, its
+// loaders' memory parallelism being the limit).  Measured and rejected: one 1-D bulk copy
+// (cp.async.bulk) per 512- / 128-byte run -- the copy engine's per-copy cost made the loads
+// alone 10.3 ms per configs[4] step instead of 4.6.
+constexpr int SBR_X_ROWS = 128, SBR_X_THREADS = 256, SBR_X_STAGES = 4;
+constexpr int SBR_X_STAGE_FLOATS = SBR_B * SBR_X_ROWS + SBR_B * SBR_B;   // A tile + V tile
+inline size_t sbr_x_smem_bytes() { return sizeof(float) * SBR_X_STAGES * SBR_X_STAGE_FLOATS; }
+BKFAC_DEV int sbr_x_swz(int k) { return ((k ^ (k >> 3)) & 7) << 2; }
+BKFAC_DEV void sbr_cp4(uint32_t dst, const float* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
+BKFAC_DEV void sbr_cp16(uint32_t dst, const float* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+// one 32-deep k tile: acc(4 rows x 4 columns) += A(rows ir.., k) V(k, cg..);  SWZ: As[k][i ^ swz(k)]
+template <bool SWZ>
+BKFAC_DEV void sbr_x_tile(const float* as, const float* vs, int ir, int cg, float2 (&acc)[4][2]) {
+  constexpr int B = SBR_B, R = SBR_X_ROWS;
+#pragma unroll 8
+  for (int k = 0; k < B; ++k) {
+    const int col = SWZ ? (ir ^ sbr_x_swz(k)) : ir;
+    const float4 a = *reinterpret_cast<const float4*>(as + k * R + col);
+    const float4 v = *reinterpret_cast<const float4*>(vs + k * B + cg);
+    const float2 v01 = make_float2(v.x, v.y), v23 = make_float2(v.z, v.w);
+    const float ar[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float2 a2 = make_float2(ar[r], ar[r]);
+      acc[r][0] = __ffma2_rn(a2, v01, acc[r][0]);
+      acc[r][1] = __ffma2_rn(a2, v23, acc[r][1]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(SBR_X_THREADS, 2)
+sbr_x_kernel(const __grid_constant__ EigBatch b, int j) {
+  const EigProb& p = b.p[blockIdx.y];
+  const int m = p.m;
+  if (p.sbr == 0 || j >= sbr_panels(m)) return;
+  constexpr int B = SBR_B, R = SBR_X_ROWS, NT = SBR_X_THREADS, S = SBR_X_STAGES;
+  const int r0 = (j + 1) * B, L = m - r0;
+  const int i0 = blockIdx.x * R;
+  if (i0 >= L) return;
+  const long ld = p.ldk;
+  const float* A = p.K + r0 + (long)r0 * ld;     // stored lower triangle: A22(i, k) = A[i + k ld], i >= k
+  const float* Vt = p.Vt + (long)r0 * B;         // V(k, c) = Vt[k B + c]
+  extern __shared__ __align__(16) float xsm[];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(xsm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool vec = (ld & 3) == 0 && (m & 3) == 0 && (reinterpret_cast<uintptr_t>(p.K) & 15) == 0;
+  const bool vvec = (reinterpret_cast<uintptr_t>(p.Vt) & 15) == 0;
+  const int nkt = (L + B - 1) / B;
+  auto linear = [&](int kt) {   // tile kt entirely below the diagonal, whole 16-byte runs
+    const int k0 = kt * B;
+    return vec && i0 >= k0 + B - 1;
+  };
+  auto issue = [&](int kt) {           // copies of k tile kt into its stage (one commit group)
+#ifndef BKFAC_SBRX_NOLOAD
+    if (kt < nkt) {
+#else
+    if (false) {
+#endif
+      const int k0 = kt * B;
+      const uint32_t as = sbase + 4u * (uint32_t)((kt % S) * SBR_X_STAGE_FLOATS);
+      const uint32_t vs = as + 4u * (uint32_t)(B * R);
+      if (linear(kt)) {   // along i: 4 consecutive rows of column k, 16-byte copies
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = tid + NT * u, k = q >> 5, i = (q & 31) * 4;
+          const int gi = i0 + i, gk = k0 + k;
+          const bool ok = gi < L && gk < L;      // L % 4 == 0 when ld is: whole runs
+          sbr_cp16(as + 4u * (uint32_t)(k * R + i), ok ? A + gi + (long)gk * ld : A, ok);
+        }
+      } else {
+        const int mode = (i0 >= k0 + B - 1) ? 0 : (k0 > i0 + R - 1) ? 1 : 2;   // below / above / crossing
+        if (mode != 1) {   // along i: 4 consecutive rows of column k
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int q = tid + NT * u, k = q >> 5, i = (q & 31) * 4;
+            const int gi = i0 + i, gk = k0 + k;
+            const float* src = A + gi + (long)gk * ld;
+            const uint32_t d = as + 4u * (uint32_t)(k * R + (i ^ sbr_x_swz(k)));
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (mode == 0 || gi + t >= gk) sbr_cp4(d + 4u * t, (gi + t < L && gk < L) ? src + t : A, gi + t < L && gk < L);
+          }
+        }
+        if (mode != 0) {   // along k: A22(i, k) = A[k + i ld], 4 consecutive k of stored column i
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = u * 32 + warp * 4 + (lane >> 3), k = (lane & 7) * 4;
+            const int gi = i0 + i, gk = k0 + k;
+            const float* src = A + gk + (long)gi * ld;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (mode == 1 || gi < gk + t)
+                sbr_cp4(as + 4u * (uint32_t)((k + t) * R + (i ^ sbr_x_swz(k + t))),
+                        (gk + t < L && gi < L) ? src + t : A, gk + t < L && gi < L);
+          }
+        }
+      }
+      {   // V tile: row k of Vt is 32 contiguous floats (zero-filled beyond L)
+        const int k = tid >> 3, c = (tid & 7) * 4;
+        const bool ok = k0 + k < L;
+        const float* src = ok ? Vt + (long)(k0 + k) * B + c : Vt;
+        if (vvec) {
+          sbr_cp16(vs + 4u * (uint32_t)(k * B + c), src, ok);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) sbr_cp4(vs + 4u * (uint32_t)(k * B + c + t), ok ? src + t : Vt, ok);
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");   // (possibly empty) group per tile
+  };
+  // compute mapping: warp w -> tile rows 16w .. 16w+15; lane -> 4 rows (lane / 8) x 4 columns
+  const int ir = warp * 16 + (lane >> 3) * 4, cg = (lane & 7) * 4;
+  float2 acc[4][2];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) { acc[r][0] = make_float2(0.f, 0.f); acc[r][1] = make_float2(0.f, 0.f); }
+#pragma unroll
+  for (int t = 0; t < S - 1; ++t) issue(t);
+  for (int kt = 0; kt < nkt; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");   // tile kt's copies (own)
+    __syncthreads();   // ... everyone's; and every thread is done with tile kt - 1's stage
+    issue(kt + S - 1);
+    const float* as = xsm + (kt % S) * SBR_X_STAGE_FLOATS;
+    const float* vs = as + B * R;
+#ifndef BKFAC_SBRX_NOCOMP
+    if (linear(kt)) sbr_x_tile<false>(as, vs, ir, cg, acc);
+    else sbr_x_tile<true>(as, vs, ir, cg, acc);
+#endif
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  float* X = p.Xp + r0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int gi = i0 + ir + r;
+    if (gi < L) {
+      X[gi + (long)(cg + 0) * m] = acc[r][0].x;
+      X[gi + (long)(cg + 1) * m] = acc[r][0].y;
+      X[gi + (long)(cg + 2) * m] = acc[r][1].x;
+      X[gi + (long)(cg + 3) * m] = acc[r][1].y;
+    }
   }
 }
 

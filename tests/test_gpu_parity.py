@@ -840,18 +840,22 @@ TWO_STAGE_SHAPES = [  # (n, c, r): cores m = r + c from 40 to 1536, ragged and w
     (2000, 250, 350), (1300, 300, 700), (1700, 1024, 512)]
 
 
+@pytest.mark.parametrize("sbr_x", [1, 0])
 @pytest.mark.parametrize("shape", TWO_STAGE_SHAPES)
-def test_two_stage_eigensolver_brand(cuda_lib, shape):
-    """The two-stage reduction (dense -> band 32 by panel QR + tcgen05 two-sided updates,
+def test_two_stage_eigensolver_brand(cuda_lib, shape, sbr_x):
+    """The two-stage reduction (dense -> band 32 by panel QR + two-sided block updates,
     band -> tridiagonal by bulge chasing, back-transform through both reflector sets; sbr.cuh)
     forced for every core order: init + one Brand step against the oracle (reconstruction
-    and eigenvalues at 1e-4, orthonormal basis)."""
+    and eigenvalues at 1e-4, orthonormal basis).  sbr_x = 1: X = A22 V on the CUDA cores from
+    the lower triangle (aligned and unaligned leading dimensions: m = 246 is not a multiple of
+    4), 0: X and the mirrored update on the tcgen05 GEMM."""
     from paper_2210_08494_b200 import binding
     n, c, r = shape
     f = synth.random_case(n, c, r, seed=7000 + n + c + r, k=min(n, 2 * c), decay=0.9)
     M0, M1 = f.batch(0).astype(np.float64), f.batch(1).astype(np.float64)
     ctx = _ctx([(n, r, c, 0)])
     ctx.bkfac_set_option(binding.BKFAC_OPT_TWO_STAGE, 2)
+    ctx.bkfac_set_option(binding.BKFAC_OPT_SBR_X, sbr_x)
     U0 = synth.phantom_basis(n, r)
     Ug, Dg = gpu_brand(ctx, 0, U0, np.zeros(r), M0, 0.0, 1.0)
     Uo, Do = O.brand_update(U0, np.zeros(r), M0, 0.0, 1.0, r)
