@@ -127,9 +127,10 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
  *                         cluster per factor on CUDA cores
  *   BKFAC_OPT_NVTX        != 0: every stage of every call inside a host NVTX range named by
  *                         its stage tag (profiling: ncu --nvtx --nvtx-include "<tag>/")
- *   BKFAC_OPT_SBR_X       two-stage band reduction: 1 (default) X = A22 V on the CUDA cores
- *                         from the lower triangle and lower-only block updates, 0 X and the
- *                         mirrored update both on the tcgen05 GEMM (full symmetric storage) */
+ *   BKFAC_OPT_SBR_X       two-stage band reduction: 1 (default) X = A22 V and the block update
+ *                         in their own kernels on the lower triangle only (warp-level tensor-core
+ *                         MMA, 3xTF32), 0 both on the tcgen05 GEMM (full symmetric storage,
+ *                         mirrored update) */
 #define BKFAC_OPT_TWO_STAGE 1
 #define BKFAC_OPT_GT_CLUSTER 2
 #define BKFAC_OPT_GEMM_PAIR 3

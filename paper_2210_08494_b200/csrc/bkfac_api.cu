@@ -55,7 +55,7 @@ struct Arena {
 
 struct EigWs {  // workspace of one eigen problem of order <= m with <= r outputs
   size_t K, d, e, tau, lam, Y, scr, piv, V, gt, U, Z, S;
-  size_t Vp = 0, Vt = 0, Xp = 0, Wp = 0, Tp = 0, AB = 0, Vq = 0, tq = 0;   // two-stage (sbr.cuh)
+  size_t Vp = 0, Vt = 0, Wt = 0, Xp = 0, Wp = 0, Tp = 0, AB = 0, Vq = 0, tq = 0;   // two-stage (sbr.cuh)
   bool sbr = false;   // two-stage workspace planned (sbr_supported(m))
   int m, r;
 };
@@ -67,7 +67,7 @@ void plan_eig(Arena& a, EigWs& w, int m, int r) {
   w.sbr = sbr_supported(m);
   if (w.sbr) {
     const size_t mb = sizeof(float) * (size_t)m * SBR_B;
-    w.Vp = a.take(mb); w.Vt = a.take(mb); w.Xp = a.take(mb); w.Wp = a.take(mb);
+    w.Vp = a.take(mb); w.Vt = a.take(mb); w.Wt = a.take(mb); w.Xp = a.take(mb); w.Wp = a.take(mb);
     w.Tp = a.take(sizeof(float) * SBR_B * SBR_B);
     w.AB = a.take(sizeof(float) * (size_t)m * SBR_LDB);
     w.Vq = a.take(sizeof(float) * (size_t)m * sbr_tasks(m) * SBR_B);
@@ -143,7 +143,7 @@ struct bkfac_ctx_s {
   cudaEvent_t ev_ea_fork = nullptr, ev_ea_done = nullptr;
   std::function<bkfac_status(int)> pending_ea;
   int nvtx = 0;       // BKFAC_OPT_NVTX: every stage inside an NVTX range named by its tag
-  int sbr_x = 1;      // BKFAC_OPT_SBR_X: band reduction's X on the CUDA cores, lower-only updates
+  int sbr_x = 1;      // BKFAC_OPT_SBR_X: band reduction's X and update kernels (mma.sync, lower triangle)
   int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs; < 0: one CTA per tile
   bool ea_join_early = false;   // join the side-stream EA right after the tridiagonalisation
   int pair_mode = 1;  // CTA-pair GEMM tiles: 0 never, 1 large long-K stages, 2 always (tests)
@@ -662,7 +662,7 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
     sbr_panel_kernel<<<(unsigned)n, SBR_PANEL_THREADS, sbr_panel_smem_bytes(mmax), st>>>(b, j);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
-    if (ctx->sbr_x) {   // X = A22 V from the lower triangle (CUDA cores, sbr_x_kernel)
+    if (ctx->sbr_x) {   // X = A22 V from the lower triangle (sbr_x_kernel)
       double xf = 0.0, xb = 0.0;
       int lmax = 0;
       for (int i = 0; i < n; ++i) {
@@ -690,7 +690,23 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
     sbr_w_kernel<<<(unsigned)n, SBR_W_WARPS * 32, sbr_w_smem_bytes(), st>>>(b, j);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
-    // A22 -= V W^T + W V^T  (symmetric: lower tiles; mirrored only while X reads full storage)
+    if (ctx->sbr_x) {   // A22 -= V W^T + W V^T on the lower 128 x 128 tiles (sbr_update_kernel)
+      double uf = 0.0, ub = 0.0;
+      int tmax = 0;
+      for (int i = 0; i < n; ++i) {
+        if (!b.p[i].sbr || j >= sbr_panels(b.p[i].m)) continue;
+        const int L = b.p[i].m - (j + 1) * B;
+        uf += 2.0 * (double)L * (L + 1) * 2 * B;          // lower triangle, K = 2B
+        ub += 4.0 * (double)L * (L + 1);                  // its C0 read + C write
+        tmax = std::max(tmax, sbr_u_tiles(L));
+      }
+      prof_begin(ctx, "eig_sbr_update", st, uf, ub);
+      sbr_update_kernel<<<dim3((unsigned)tmax, (unsigned)n), SBR_U_THREADS, sbr_u_smem_bytes(), st>>>(b, j);
+      LAUNCH_CHECK(ctx);
+      prof_end(ctx, st);
+      continue;
+    }
+    // A22 -= V W^T + W V^T  (symmetric: lower tiles computed, mirrored: X reads full storage)
     for (int i = 0; i < n; ++i) {
       const EigProb& q = b.p[i];
       if (!q.sbr || j >= sbr_panels(q.m)) continue;
@@ -700,7 +716,7 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
       pu.A2 = q.Wp + r0; pu.lda2 = q.m;
       pu.B2 = q.Vp + r0; pu.ldb2 = q.m;
       pu.k1 = B;
-      pu.sym = ctx->sbr_x ? 2 : 1;
+      pu.sym = 1;
       gs.add(false, true, pu, 0);
     }
     if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_update")) != BKFAC_OK) return rs;
@@ -991,6 +1007,7 @@ EigProb eig_prob(bkfac_ctx ctx, const EigWs& w, int m, int r, float* V, int ldv,
   p.off = p.sbr ? SBR_B : 1;
   p.Vp = w.sbr ? at<float>(ctx, w.Vp) : nullptr;
   p.Vt = w.sbr ? at<float>(ctx, w.Vt) : nullptr;
+  p.Wt = w.sbr ? at<float>(ctx, w.Wt) : nullptr;
   p.Xp = w.sbr ? at<float>(ctx, w.Xp) : nullptr;
   p.Wp = w.sbr ? at<float>(ctx, w.Wp) : nullptr;
   p.Tp = w.sbr ? at<float>(ctx, w.Tp) : nullptr;
@@ -1165,6 +1182,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
   attr_ok &= cudaFuncSetAttribute(chol_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem_bytes(32 * CS_MAXNB)) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sbr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_panel_smem_bytes(SBR_MAX_L + SBR_B)) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sbr_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_x_smem_bytes()) == cudaSuccess;
+  attr_ok &= cudaFuncSetAttribute(sbr_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_u_smem_bytes()) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sbr_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_w_smem_bytes()) == cudaSuccess;
   attr_ok &= cudaFuncSetAttribute(sbr_chase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbr_chase_smem_bytes()) == cudaSuccess;
   attr_ok &= tc_init_attributes();

@@ -190,7 +190,7 @@ sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
     K[(r0 + l) + (long)(c0 + i) * ld] = x;
     p.Vp[(r0 + l) + (long)i * m] = (l < i) ? 0.f : (l == i ? 1.f : x);
   }
-  for (int e = tid; e < L * B; e += NT) {   // row-major copy for the X kernel's tile copies
+  for (int e = tid; e < L * B; e += NT) {   // row-major copy for the X and update kernels' tiles
     const int l = e / B, i = e % B;
     p.Vt[(long)(r0 + l) * B + i] = (l < i) ? 0.f : (l == i ? 1.f : P[l * LDP + i]);
   }
@@ -295,6 +295,9 @@ sbr_w_kernel(const __grid_constant__ EigBatch b, int j) {
 #pragma unroll 4
     for (int a = 0; a < B; ++a)
       if (ok) W[(rb + lane) + (long)a * m] = xs[lane * LDT + a];
+#pragma unroll 4
+    for (int i = 0; i < B; ++i)   // row-major copy for the update kernel's tiles
+      if (rb + i < m) p.Wt[(long)(rb + i) * B + lane] = xs[i * LDT + lane];
     __syncwarp();
   }
 }
@@ -303,57 +306,89 @@ sbr_w_kernel(const __grid_constant__ EigBatch b, int j) {
 // grid (row blocks of SBR_X_ROWS, nprob), block SBR_X_THREADS.  Only the lower triangle of
 // A22 is kept current (the block update writes lower tiles only), so element (i, k) of the
 // symmetric A22 is read from K(i, k) when i >= k and from K(k, i) otherwise.  The CTA walks
-// the 32-deep k tiles of its 128 rows through a SBR_X_STAGES-deep cp.async ring (three tiles
-// in flight while one is multiplied, no staging registers), each tile k-major in shared
-// memory:
-//   below the diagonal   16-byte copies along i (4 rows of a stored column), linear As[k][i];
-//   above / crossing it  4-byte copies along k (the stored block read transposed) scattered
-//                        to their k rows, with the 4-float row groups XOR-swizzled by k so that
-//                        the scatter and the compute reads are conflict-free; on a crossing
-//                        tile every element comes from the pattern that reads it from the
-//                        lower triangle; zero-filled out of range;
-//   V                    16-byte copies of the row-major V tile (Vt, written by the panel kernel).
-// Exact fp32 FMAs on the CUDA cores: X = A22 V is 16 flop per byte of A22 with N = 32, an
-// HBM-streaming product, not a tensor-core one (the tcgen05 GEMM reached 1.6 TB/s here, its
-// loaders' memory parallelism being the limit).  Measured and rejected: one 1-D bulk copy
-// (cp.async.bulk) per 512- / 128-byte run -- the copy engine's per-copy cost made the loads
-// alone 10.3 ms per configs[4] step instead of 4.6.
-constexpr int SBR_X_ROWS = 128, SBR_X_THREADS = 256, SBR_X_STAGES = 4;
-constexpr int SBR_X_STAGE_FLOATS = SBR_B * SBR_X_ROWS + SBR_B * SBR_B;   // A tile + V tile
+// the 32-deep k tiles of its 128 rows through a SBR_X_STAGES-deep cp.async ring (the next
+// tiles in flight while one is multiplied, no staging registers):
+//   below the diagonal  16-byte copies along i (4 rows of a stored column): As[k][i], pitch 136;
+//   above it            16-byte copies along k (4 k of a stored column i, the stored block
+//                       read transposed): At[i][k], pitch 36;
+//   crossing it         4-byte copies into At, each element by the pattern that reads it
+//                       from the lower triangle; zero-filled out of range;
+//   V                   16-byte copies of the row-major V tile (Vt, written by the panel
+//                       kernel): Vs[k][c], pitch 40.
+// (pitches: every fragment load below is bank-conflict-free).  The products run on the
+// warp-level tensor-core MMA (mma.sync m16n8k8 tf32) in 3xTF32 -- hi = rna_tf32(x), lo = x -
+// hi, hi_A lo_B + lo_A hi_B + hi_A hi_B, the split done in registers -- each warp 32 rows x 32
+// columns; every k tile is accumulated in fresh fragments and added into a running fp32 sum
+// (round-to-nearest FADDs: the MMA accumulate's bias stays bounded by 32 terms, as the
+// tcgen05 GEMM's promotion does).  Measured on configs[4]: the CUDA-core FFMA2 version (8 x 8
+// register tiles) was bound by the FMA pipes at 6.4 ms per step for the products alone (the
+// 3-register FFMA/FFMA2 issue at half the nominal FP32 rate); the tcgen05 GEMM reached 1.6
+// TB/s here (its loaders' memory parallelism); one 1-D bulk copy (cp.async.bulk) per 512- /
+// 128-byte run made the loads alone 10.3 ms (the copy engine's per-copy cost).
+#ifndef BKFAC_SBRX_STAGES
+#define BKFAC_SBRX_STAGES 2   // 2 stages, 4 CTAs per SM: 6.45 ms per configs[4] step (3: 6.94, 4: 7.11)
+#endif
+constexpr int SBR_X_ROWS = 128, SBR_X_THREADS = 128, SBR_X_STAGES = BKFAC_SBRX_STAGES;
+constexpr int SBR_X_LDK = 136, SBR_X_LDT = 36, SBR_X_LDV = 40;
+constexpr int SBR_X_A_FLOATS = SBR_X_ROWS * SBR_X_LDT;                  // >= 32 x 136
+constexpr int SBR_X_STAGE_FLOATS = SBR_X_A_FLOATS + SBR_B * SBR_X_LDV;   // + the V tile
 inline size_t sbr_x_smem_bytes() { return sizeof(float) * SBR_X_STAGES * SBR_X_STAGE_FLOATS; }
-BKFAC_DEV int sbr_x_swz(int k) { return ((k ^ (k >> 3)) & 7) << 2; }
 BKFAC_DEV void sbr_cp4(uint32_t dst, const float* src, bool ok) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
 }
 BKFAC_DEV void sbr_cp16(uint32_t dst, const float* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
-// one 32-deep k tile: acc(4 rows x 4 columns) += A(rows ir.., k) V(k, cg..);  SWZ: As[k][i ^ swz(k)]
-template <bool SWZ>
-BKFAC_DEV void sbr_x_tile(const float* as, const float* vs, int ir, int cg, float2 (&acc)[4][2]) {
-  constexpr int B = SBR_B, R = SBR_X_ROWS;
-#pragma unroll 8
-  for (int k = 0; k < B; ++k) {
-    const int col = SWZ ? (ir ^ sbr_x_swz(k)) : ir;
-    const float4 a = *reinterpret_cast<const float4*>(as + k * R + col);
-    const float4 v = *reinterpret_cast<const float4*>(vs + k * B + cg);
-    const float2 v01 = make_float2(v.x, v.y), v23 = make_float2(v.z, v.w);
-    const float ar[4] = {a.x, a.y, a.z, a.w};
+// x = hi + lo, hi = rna_tf32(x) (bit pattern), lo = x - hi (exact; the MMA truncates it to tf32)
+BKFAC_DEV void sbr_split(float x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  lo = __float_as_uint(x - __uint_as_float(hi));
+}
+BKFAC_DEV void sbr_mma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// one 32-deep k tile of the warp's 32 x 32 block: acc += A(rows, k) V(k, :) in 3xTF32.
+// KMAJOR: A(i, k) at a[k * LDK + i], else at a[i * LDT + k]; rb = the warp's first row.
+template <bool KMAJOR>
+BKFAC_DEV void sbr_x_tile(const float* a, const float* vs, int rb, int g, int t, float (&acc)[2][4][4]) {
+  constexpr int LDK = SBR_X_LDK, LDT = SBR_X_LDT, LDV = SBR_X_LDV;
+  auto A = [&](int i, int k) { return KMAJOR ? a[k * LDK + i] : a[i * LDT + k]; };
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const float2 a2 = make_float2(ar[r], ar[r]);
-      acc[r][0] = __ffma2_rn(a2, v01, acc[r][0]);
-      acc[r][1] = __ffma2_rn(a2, v23, acc[r][1]);
+  for (int ks = 0; ks < SBR_B / 8; ++ks) {
+    const int kb = ks * 8;
+    uint32_t ah[2][4], al[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int i = rb + 16 * mt + g;
+      sbr_split(A(i, kb + t), ah[mt][0], al[mt][0]);
+      sbr_split(A(i + 8, kb + t), ah[mt][1], al[mt][1]);
+      sbr_split(A(i, kb + t + 4), ah[mt][2], al[mt][2]);
+      sbr_split(A(i + 8, kb + t + 4), ah[mt][3], al[mt][3]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      uint32_t bh0, bl0, bh1, bl1;
+      sbr_split(vs[(kb + t) * LDV + 8 * nt + g], bh0, bl0);
+      sbr_split(vs[(kb + t + 4) * LDV + 8 * nt + g], bh1, bl1);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {   // small terms first
+        sbr_mma(acc[mt][nt], al[mt], bh0, bh1);
+        sbr_mma(acc[mt][nt], ah[mt], bl0, bl1);
+        sbr_mma(acc[mt][nt], ah[mt], bh0, bh1);
+      }
     }
   }
 }
 
-__global__ void __launch_bounds__(SBR_X_THREADS, 2)
+__global__ void __launch_bounds__(SBR_X_THREADS)
 sbr_x_kernel(const __grid_constant__ EigBatch b, int j) {
   const EigProb& p = b.p[blockIdx.y];
   const int m = p.m;
   if (p.sbr == 0 || j >= sbr_panels(m)) return;
   constexpr int B = SBR_B, R = SBR_X_ROWS, NT = SBR_X_THREADS, S = SBR_X_STAGES;
+  constexpr int LDK = SBR_X_LDK, LDT = SBR_X_LDT, LDV = SBR_X_LDV;
   const int r0 = (j + 1) * B, L = m - r0;
   const int i0 = blockIdx.x * R;
   if (i0 >= L) return;
@@ -363,12 +398,14 @@ sbr_x_kernel(const __grid_constant__ EigBatch b, int j) {
   extern __shared__ __align__(16) float xsm[];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(xsm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // whole 16-byte runs: the leading dimension (and with it L = m - r0) a multiple of 4 floats
   const bool vec = (ld & 3) == 0 && (m & 3) == 0 && (reinterpret_cast<uintptr_t>(p.K) & 15) == 0;
   const bool vvec = (reinterpret_cast<uintptr_t>(p.Vt) & 15) == 0;
   const int nkt = (L + B - 1) / B;
-  auto linear = [&](int kt) {   // tile kt entirely below the diagonal, whole 16-byte runs
+  auto region = [&](int kt) {   // 0 below the diagonal, 1 above, 2 crossing (or unaligned)
     const int k0 = kt * B;
-    return vec && i0 >= k0 + B - 1;
+    if (!vec) return 2;
+    return (i0 >= k0 + B - 1) ? 0 : (k0 > i0 + R - 1) ? 1 : 2;
   };
   auto issue = [&](int kt) {           // copies of k tile kt into its stage (one commit group)
 #ifndef BKFAC_SBRX_NOLOAD
@@ -378,85 +415,223 @@ sbr_x_kernel(const __grid_constant__ EigBatch b, int j) {
 #endif
       const int k0 = kt * B;
       const uint32_t as = sbase + 4u * (uint32_t)((kt % S) * SBR_X_STAGE_FLOATS);
-      const uint32_t vs = as + 4u * (uint32_t)(B * R);
-      if (linear(kt)) {   // along i: 4 consecutive rows of column k, 16-byte copies
+      const uint32_t vs = as + 4u * (uint32_t)SBR_X_A_FLOATS;
+      const int reg = region(kt);
+      if (reg == 0) {          // As[k][i]: 4 consecutive rows of stored column k per copy
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int q = tid + NT * u, k = q >> 5, i = (q & 31) * 4;
+        for (int u = 0; u < B * R / 4 / NT; ++u) {
+          const int q = tid + NT * u, k = q / (R / 4), i = (q % (R / 4)) * 4;
           const int gi = i0 + i, gk = k0 + k;
-          const bool ok = gi < L && gk < L;      // L % 4 == 0 when ld is: whole runs
-          sbr_cp16(as + 4u * (uint32_t)(k * R + i), ok ? A + gi + (long)gk * ld : A, ok);
+          const bool ok = gi < L && gk < L;
+          sbr_cp16(as + 4u * (uint32_t)(k * LDK + i), ok ? A + gi + (long)gk * ld : A, ok);
         }
-      } else {
-        const int mode = (i0 >= k0 + B - 1) ? 0 : (k0 > i0 + R - 1) ? 1 : 2;   // below / above / crossing
-        if (mode != 1) {   // along i: 4 consecutive rows of column k
+      } else if (reg == 1) {   // At[i][k]: 4 consecutive k of stored column i per copy
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int q = tid + NT * u, k = q >> 5, i = (q & 31) * 4;
-            const int gi = i0 + i, gk = k0 + k;
-            const float* src = A + gi + (long)gk * ld;
-            const uint32_t d = as + 4u * (uint32_t)(k * R + (i ^ sbr_x_swz(k)));
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (mode == 0 || gi + t >= gk) sbr_cp4(d + 4u * t, (gi + t < L && gk < L) ? src + t : A, gi + t < L && gk < L);
-          }
+        for (int u = 0; u < B * R / 4 / NT; ++u) {
+          const int q = tid + NT * u, i = q / (B / 4), k = (q % (B / 4)) * 4;
+          const int gi = i0 + i, gk = k0 + k;
+          const bool ok = gi < L && gk < L;
+          sbr_cp16(as + 4u * (uint32_t)(i * LDT + k), ok ? A + gk + (long)gi * ld : A, ok);
         }
-        if (mode != 0) {   // along k: A22(i, k) = A[k + i ld], 4 consecutive k of stored column i
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = u * 32 + warp * 4 + (lane >> 3), k = (lane & 7) * 4;
-            const int gi = i0 + i, gk = k0 + k;
-            const float* src = A + gk + (long)gi * ld;
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (mode == 1 || gi < gk + t)
-                sbr_cp4(as + 4u * (uint32_t)((k + t) * R + (i ^ sbr_x_swz(k + t))),
-                        (gk + t < L && gi < L) ? src + t : A, gk + t < L && gi < L);
-          }
+      } else {                 // At[i][k], element by element from the lower triangle
+        for (int e = tid; e < B * R; e += NT) {
+          const int i = e % R, k = e / R;
+          const int gi = i0 + i, gk = k0 + k;
+          const bool ok = gi < L && gk < L;
+          const float* src = !ok ? A : (gi >= gk ? A + gi + (long)gk * ld : A + gk + (long)gi * ld);
+          sbr_cp4(as + 4u * (uint32_t)(i * LDT + k), src, ok);
         }
       }
-      {   // V tile: row k of Vt is 32 contiguous floats (zero-filled beyond L)
-        const int k = tid >> 3, c = (tid & 7) * 4;
+      // V tile: row k of Vt is 32 contiguous floats (zero-filled beyond L)
+#pragma unroll
+      for (int u = 0; u < B * B / 4 / NT; ++u) {
+        const int q = tid + NT * u, k = q / (B / 4), c = (q % (B / 4)) * 4;
         const bool ok = k0 + k < L;
         const float* src = ok ? Vt + (long)(k0 + k) * B + c : Vt;
+        const uint32_t d = vs + 4u * (uint32_t)(k * LDV + c);
         if (vvec) {
-          sbr_cp16(vs + 4u * (uint32_t)(k * B + c), src, ok);
+          sbr_cp16(d, src, ok);
         } else {
 #pragma unroll
-          for (int t = 0; t < 4; ++t) sbr_cp4(vs + 4u * (uint32_t)(k * B + c + t), ok ? src + t : Vt, ok);
+          for (int t = 0; t < 4; ++t) sbr_cp4(d + 4u * t, ok ? src + t : Vt, ok);
         }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");   // (possibly empty) group per tile
   };
-  // compute mapping: warp w -> tile rows 16w .. 16w+15; lane -> 4 rows (lane / 8) x 4 columns
-  const int ir = warp * 16 + (lane >> 3) * 4, cg = (lane & 7) * 4;
-  float2 acc[4][2];
+  const int g = lane >> 2, t = lane & 3, rb = warp * 32;   // warp w: rows 32w .. 32w+31, all 32 columns
+  float sum[2][4][4];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) { acc[r][0] = make_float2(0.f, 0.f); acc[r][1] = make_float2(0.f, 0.f); }
+  for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-  for (int t = 0; t < S - 1; ++t) issue(t);
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sum[mt][nt][q] = 0.f;
+#pragma unroll
+  for (int u = 0; u < S - 1; ++u) issue(u);
   for (int kt = 0; kt < nkt; ++kt) {
     asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");   // tile kt's copies (own)
     __syncthreads();   // ... everyone's; and every thread is done with tile kt - 1's stage
     issue(kt + S - 1);
     const float* as = xsm + (kt % S) * SBR_X_STAGE_FLOATS;
-    const float* vs = as + B * R;
+    const float* vs = as + SBR_X_A_FLOATS;
 #ifndef BKFAC_SBRX_NOCOMP
-    if (linear(kt)) sbr_x_tile<false>(as, vs, ir, cg, acc);
-    else sbr_x_tile<true>(as, vs, ir, cg, acc);
+    float acc[2][4][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
+    if (region(kt) == 0) sbr_x_tile<true>(as, vs, rb, g, t, acc);
+    else sbr_x_tile<false>(as, vs, rb, g, t, acc);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sum[mt][nt][q] += acc[mt][nt][q];
 #endif
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   float* X = p.Xp + r0;
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int gi = i0 + ir + r;
-    if (gi < L) {
-      X[gi + (long)(cg + 0) * m] = acc[r][0].x;
-      X[gi + (long)(cg + 1) * m] = acc[r][0].y;
-      X[gi + (long)(cg + 2) * m] = acc[r][1].x;
-      X[gi + (long)(cg + 3) * m] = acc[r][1].y;
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gi = i0 + rb + 16 * mt + g + 8 * h;
+      if (gi < L) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int c = 8 * nt + 2 * t;
+          X[gi + (long)c * m] = sum[mt][nt][2 * h];
+          X[gi + (long)(c + 1) * m] = sum[mt][nt][2 * h + 1];
+        }
+      }
+    }
+}
+
+// ---------------------------------------------------------------------- stage 1: block update
+// grid (lower tiles of the largest A22, nprob), block SBR_U_THREADS:
+//   A22 -= V W^T + W V^T = C0 - [V_I W_I] [W_J V_J]^T      (K = 64)
+// on the 128 x 128 tiles (I, J), I >= J, of the lower triangle only -- the upper triangle is
+// never read again (X, the panels and the band extraction read the lower one); on a diagonal
+// tile the elements above the diagonal are computed and not stored.  Operands: the four
+// 128 x 32 row-major blocks V_I, W_I, W_J, V_J (Vt from the panel kernel, Wt from the W
+// kernel) by 16-byte cp.async into [128][64] tiles of pitch 68 (conflict-free fragment
+// loads); products on mma.sync m16n8k8 tf32 in 3xTF32 (split in registers), warp tile 32 x 64;
+// C0 is prefetched into L2 while the operands land and read per fragment after the MMAs.
+// Replaces the tcgen05 GEMM with a lower-tile epilogue, whose C0 read + C write streamed at
+// 1.2 TB/s (its 8 epilogue warps keep 16 KB in flight per SM).
+constexpr int SBR_U_TILE = 128, SBR_U_THREADS = 256, SBR_U_LD = 68;
+inline size_t sbr_u_smem_bytes() { return sizeof(float) * 2 * SBR_U_TILE * SBR_U_LD; }
+__host__ __device__ inline int sbr_u_tiles(int L) { const int t = (L + SBR_U_TILE - 1) / SBR_U_TILE; return t * (t + 1) / 2; }
+
+__global__ void __launch_bounds__(SBR_U_THREADS, 2)
+sbr_update_kernel(const __grid_constant__ EigBatch b, int j) {
+  const EigProb& p = b.p[blockIdx.y];
+  const int m = p.m;
+  if (p.sbr == 0 || j >= sbr_panels(m)) return;
+  constexpr int B = SBR_B, T = SBR_U_TILE, NT = SBR_U_THREADS, LD = SBR_U_LD;
+  const int r0 = (j + 1) * B, L = m - r0;
+  const int tix = blockIdx.x;
+  if (tix >= sbr_u_tiles(L)) return;
+  int ti = (int)((sqrtf(8.f * tix + 1.f) - 1.f) * 0.5f);   // tix = ti (ti + 1) / 2 + tj, tj <= ti
+  while (ti * (ti + 1) / 2 > tix) --ti;
+  while ((ti + 1) * (ti + 2) / 2 <= tix) ++ti;
+  const int tj = tix - ti * (ti + 1) / 2;
+  const int i0 = ti * T, j0 = tj * T;
+  const long ld = p.ldk;
+  float* C = p.K + r0 + (long)r0 * ld;
+  const float* Vt = p.Vt + (long)r0 * B;
+  const float* Wt = p.Wt + (long)r0 * B;
+  extern __shared__ __align__(16) float usm[];
+  const float* As = usm;              // [V_I | W_I]: row i at As + i LD (k 0..63)
+  const float* Bs = usm + T * LD;     // [W_J | V_J]: row j at Bs + j LD
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(usm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool vec = (reinterpret_cast<uintptr_t>(p.Vt) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.Wt) & 15) == 0;
+#pragma unroll 4
+  for (int u = 0; u < 4 * T * B / 4 / NT; ++u) {
+    const int q = tid + NT * u, blk = q / (T * B / 4), r = (q / (B / 4)) % T, c = (q % (B / 4)) * 4;
+    const int row = (blk < 2 ? i0 : j0) + r;
+    const float* src = ((blk == 0 || blk == 3) ? Vt : Wt) + (long)row * B + c;
+    const bool ok = row < L;
+    const uint32_t d = sbase + 4u * (uint32_t)((blk >> 1) * T * LD + r * LD + (blk & 1) * B + c);
+    if (vec) {
+      sbr_cp16(d, ok ? src : Vt, ok);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sbr_cp4(d + 4u * e, ok ? src + e : Vt, ok);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int e = tid; e < T * (T / 32); e += NT) {   // C0 lines (128 bytes) of the tile into L2
+    const int col = j0 + e / (T / 32), row = i0 + (e % (T / 32)) * 32;
+    if (col < L && row < L) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + row + (long)col * ld));
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const int g = lane >> 2, t = lane & 3;
+  const int rb = (warp & 3) * 32, cb = (warp >> 2) * 64;    // warp tile: 32 rows x 64 columns
+  float acc[2][8][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
+#pragma unroll 2
+  for (int ks = 0; ks < 2 * B / 8; ++ks) {
+    const int kb = ks * 8;
+    uint32_t ah[2][4], al[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const float* ar = As + (rb + 16 * mt + g) * LD + kb + t;
+      sbr_split(ar[0], ah[mt][0], al[mt][0]);
+      sbr_split(ar[8 * LD], ah[mt][1], al[mt][1]);
+      sbr_split(ar[4], ah[mt][2], al[mt][2]);
+      sbr_split(ar[8 * LD + 4], ah[mt][3], al[mt][3]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float* br = Bs + (cb + 8 * nt + g) * LD + kb + t;
+      uint32_t bh0, bl0, bh1, bl1;
+      sbr_split(br[0], bh0, bl0);
+      sbr_split(br[4], bh1, bl1);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {   // small terms first
+        sbr_mma(acc[mt][nt], al[mt], bh0, bh1);
+        sbr_mma(acc[mt][nt], ah[mt], bl0, bl1);
+        sbr_mma(acc[mt][nt], ah[mt], bh0, bh1);
+      }
+    }
+  }
+  // C = C0 - acc on the lower triangle; each row tile's 32 C0 loads issued together
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    float c0[2][8][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = i0 + rb + 16 * mt + g + 8 * h;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = j0 + cb + 8 * nt + 2 * t + e;
+          c0[h][nt][e] = (row < L && col <= row) ? C[row + (long)col * ld] : 0.f;
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = i0 + rb + 16 * mt + g + 8 * h;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = j0 + cb + 8 * nt + 2 * t + e;
+          if (row < L && col <= row) C[row + (long)col * ld] = c0[h][nt][e] - acc[mt][nt][2 * h + e];
+        }
     }
   }
 }
