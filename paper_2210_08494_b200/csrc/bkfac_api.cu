@@ -55,7 +55,7 @@ struct Arena {
 
 struct EigWs {  // workspace of one eigen problem of order <= m with <= r outputs
   size_t K, d, e, tau, lam, Y, scr, piv, V, gt, U, Z, S;
-  size_t Vp = 0, Vt = 0, Wt = 0, Xp = 0, Wp = 0, Tp = 0, AB = 0, Vq = 0, tq = 0;   // two-stage (sbr.cuh)
+  size_t Vp = 0, Vt = 0, Wt = 0, Zp = 0, Xp = 0, Wp = 0, Tp = 0, AB = 0, Vq = 0, tq = 0;   // two-stage (sbr.cuh)
   bool sbr = false;   // two-stage workspace planned (sbr_supported(m))
   int m, r;
 };
@@ -68,6 +68,7 @@ void plan_eig(Arena& a, EigWs& w, int m, int r) {
   if (w.sbr) {
     const size_t mb = sizeof(float) * (size_t)m * SBR_B;
     w.Vp = a.take(mb); w.Vt = a.take(mb); w.Wt = a.take(mb); w.Xp = a.take(mb); w.Wp = a.take(mb);
+    w.Zp = a.take(sizeof(float) * (size_t)ceil_div(m, SBR_X_ROWS) * SBR_B * SBR_B);
     w.Tp = a.take(sizeof(float) * SBR_B * SBR_B);
     w.AB = a.take(sizeof(float) * (size_t)m * SBR_LDB);
     w.Vq = a.take(sizeof(float) * (size_t)m * sbr_tasks(m) * SBR_B);
@@ -655,6 +656,9 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
   GemmStage gs;
   bkfac_status rs;
   for (int j = 0; j < pmax; ++j) {
+    int lmax_j = 0;
+    for (int i = 0; i < n; ++i)
+      if (b.p[i].sbr && j < sbr_panels(b.p[i].m)) lmax_j = std::max(lmax_j, b.p[i].m - (j + 1) * B);
     double pf = 0.0;
     for (int i = 0; i < n; ++i)
       if (b.p[i].sbr && j < sbr_panels(b.p[i].m)) pf += 4.0 * (double)(b.p[i].m - (j + 1) * B) * B * B;
@@ -687,7 +691,10 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
       if ((rs = run_gemms(ctx, gs, st, "gemm_sbr_x")) != BKFAC_OK) return rs;
     }
     prof_begin(ctx, "eig_sbr_w", st, pf, 0.0);
-    sbr_w_kernel<<<(unsigned)n, SBR_W_WARPS * 32, sbr_w_smem_bytes(), st>>>(b, j);
+    if (ctx->sbr_x)   // Y = X T and the shares of V^T Y came out of sbr_x_kernel
+      sbr_wfin_kernel<<<dim3((unsigned)ceil_div(lmax_j, SBR_X_ROWS), (unsigned)n), SBR_X_ROWS, 0, st>>>(b, j);
+    else
+      sbr_w_kernel<<<(unsigned)n, SBR_W_WARPS * 32, sbr_w_smem_bytes(), st>>>(b, j);
     LAUNCH_CHECK(ctx);
     prof_end(ctx, st);
     if (ctx->sbr_x) {   // A22 -= V W^T + W V^T on the lower 128 x 128 tiles (sbr_update_kernel)
@@ -1008,6 +1015,7 @@ EigProb eig_prob(bkfac_ctx ctx, const EigWs& w, int m, int r, float* V, int ldv,
   p.Vp = w.sbr ? at<float>(ctx, w.Vp) : nullptr;
   p.Vt = w.sbr ? at<float>(ctx, w.Vt) : nullptr;
   p.Wt = w.sbr ? at<float>(ctx, w.Wt) : nullptr;
+  p.Zp = w.sbr ? at<float>(ctx, w.Zp) : nullptr;
   p.Xp = w.sbr ? at<float>(ctx, w.Xp) : nullptr;
   p.Wp = w.sbr ? at<float>(ctx, w.Wp) : nullptr;
   p.Tp = w.sbr ? at<float>(ctx, w.Tp) : nullptr;

@@ -35,6 +35,7 @@ struct EigProb {
   int sbr;                 // two-stage tridiagonalisation (sbr.cuh) for this problem
   float* Vp; float* Xp; float* Wp; float* Tp;   // sbr stage 1: m x B panel V, X, W; B x B T
   float* Vt; float* Wt;    // sbr stage 1: V and W row-major (m x B, row l at + l B)
+  float* Zp;               // sbr stage 1: row blocks' shares of Z = V^T Y (ceil(m/128) x B x B)
   float* AB;               // sbr stage 2: band with bulge space, m x SBR_LDB
   float* Vq; float* tq;    // sbr chase reflectors (m x KT x B, m x KT)
   float* Zr;               // sbr: Q2 Y, fp32 row-major m x r (in the inverse-iteration scratch)

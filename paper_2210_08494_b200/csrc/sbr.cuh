@@ -333,6 +333,8 @@ constexpr int SBR_X_LDK = 136, SBR_X_LDT = 36, SBR_X_LDV = 40;
 constexpr int SBR_X_A_FLOATS = SBR_X_ROWS * SBR_X_LDT;                  // >= 32 x 136
 constexpr int SBR_X_STAGE_FLOATS = SBR_X_A_FLOATS + SBR_B * SBR_X_LDV;   // + the V tile
 inline size_t sbr_x_smem_bytes() { return sizeof(float) * SBR_X_STAGES * SBR_X_STAGE_FLOATS; }
+// the epilogue's X, T and V tiles reuse the ring
+static_assert(SBR_X_STAGES * SBR_X_STAGE_FLOATS >= SBR_X_ROWS * 36 + SBR_B * 40 + SBR_X_ROWS * 40, "sbr_x epilogue");
 BKFAC_DEV void sbr_cp4(uint32_t dst, const float* src, bool ok) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
 }
@@ -494,21 +496,187 @@ sbr_x_kernel(const __grid_constant__ EigBatch b, int j) {
 #endif
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();   // the ring is free: the epilogue's tiles below reuse it
+  // ---- epilogue: X block -> Y = X T (rows of W before its correction, into Wt) and this row
+  // block's share of Z = V^T Y (into Zp); sbr_wfin_kernel sums the shares and finishes W
+  float* Xs = xsm;                       // X block, [128][36]
+  float* Ts = xsm + R * 36;              // T, [32][40]: Ts[a * 40 + c] = T(a, c)
+  float* Vs2 = Ts + B * 40;              // V rows of the block, [128][40]
+  float* Ys = xsm;                       // Y block, [128][40] (after Xs, Ts are consumed)
+  float* Zr = Vs2;                       // per-warp Z shares, [4][32][32] (after Vs2 is consumed)
   float* X = p.Xp + r0;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int gi = i0 + rb + 16 * mt + g + 8 * h;
-      if (gi < L) {
+      const int li = rb + 16 * mt + g + 8 * h, gi = i0 + li;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          const int c = 8 * nt + 2 * t;
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = 8 * nt + 2 * t;
+        Xs[li * 36 + c] = sum[mt][nt][2 * h];
+        Xs[li * 36 + c + 1] = sum[mt][nt][2 * h + 1];
+        if (gi < L) {
           X[gi + (long)c * m] = sum[mt][nt][2 * h];
           X[gi + (long)(c + 1) * m] = sum[mt][nt][2 * h + 1];
         }
       }
     }
+  for (int e = tid; e < B * B; e += NT) Ts[(e % B) * 40 + e / B] = p.Tp[e];   // Tp[a + c B] = T(a, c)
+  for (int e = tid; e < R * B; e += NT) {
+    const int i = e / B, a = e % B;
+    Vs2[i * 40 + a] = (i0 + i < L) ? Vt[(long)(i0 + i) * B + a] : 0.f;
+  }
+  __syncthreads();
+  float y[2][4][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) y[mt][nt][q] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < B / 8; ++ks) {   // Y = X T
+    const int kb = ks * 8;
+    uint32_t ah[2][4], al[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const float* ar = Xs + (rb + 16 * mt + g) * 36 + kb + t;
+      sbr_split(ar[0], ah[mt][0], al[mt][0]);
+      sbr_split(ar[8 * 36], ah[mt][1], al[mt][1]);
+      sbr_split(ar[4], ah[mt][2], al[mt][2]);
+      sbr_split(ar[8 * 36 + 4], ah[mt][3], al[mt][3]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      uint32_t bh0, bl0, bh1, bl1;
+      sbr_split(Ts[(kb + t) * 40 + 8 * nt + g], bh0, bl0);
+      sbr_split(Ts[(kb + t + 4) * 40 + 8 * nt + g], bh1, bl1);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        sbr_mma(y[mt][nt], al[mt], bh0, bh1);
+        sbr_mma(y[mt][nt], ah[mt], bl0, bl1);
+        sbr_mma(y[mt][nt], ah[mt], bh0, bh1);
+      }
+    }
+  }
+  __syncthreads();   // Xs, Ts consumed
+  float* Yg = p.Wt + (long)r0 * B;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int li = rb + 16 * mt + g + 8 * h, gi = i0 + li;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = 8 * nt + 2 * t;
+        Ys[li * 40 + c] = y[mt][nt][2 * h];
+        Ys[li * 40 + c + 1] = y[mt][nt][2 * h + 1];
+        if (gi < L) *reinterpret_cast<float2*>(Yg + (long)gi * B + c) = make_float2(y[mt][nt][2 * h], y[mt][nt][2 * h + 1]);
+      }
+    }
+  __syncthreads();
+  float z[2][4][4];   // this warp's rows' share: Z(a, c) += sum_i V(i, a) Y(i, c)
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) z[mt][nt][q] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int kb = rb + ks * 8;      // rows of the block = the contraction index
+    uint32_t ah[2][4], al[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {  // A(a, i) = V(i, a)
+      const float* ar = Vs2 + (kb + t) * 40 + 16 * mt + g;
+      sbr_split(ar[0], ah[mt][0], al[mt][0]);
+      sbr_split(ar[8], ah[mt][1], al[mt][1]);
+      sbr_split(ar[4 * 40], ah[mt][2], al[mt][2]);
+      sbr_split(ar[4 * 40 + 8], ah[mt][3], al[mt][3]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      uint32_t bh0, bl0, bh1, bl1;
+      sbr_split(Ys[(kb + t) * 40 + 8 * nt + g], bh0, bl0);
+      sbr_split(Ys[(kb + t + 4) * 40 + 8 * nt + g], bh1, bl1);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        sbr_mma(z[mt][nt], al[mt], bh0, bh1);
+        sbr_mma(z[mt][nt], ah[mt], bl0, bl1);
+        sbr_mma(z[mt][nt], ah[mt], bh0, bh1);
+      }
+    }
+  }
+  __syncthreads();   // Vs2 consumed
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        Zr[warp * B * B + (16 * mt + g + 8 * (q >> 1)) * B + 8 * nt + 2 * t + (q & 1)] = z[mt][nt][q];
+  __syncthreads();
+  float* Zp = p.Zp + (long)blockIdx.x * B * B;
+  for (int e = tid; e < B * B; e += NT) {
+    float a = 0.f;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) a += Zr[w * B * B + e];
+    Zp[e] = a;
+  }
+}
+
+// ---------------------------------------------------------------------- stage 1: W (finish)
+// grid (row blocks of SBR_X_ROWS, nprob), block SBR_X_ROWS threads (thread = row).  With
+// Y = X T in Wt and the row blocks' shares of Z = V^T Y in Zp (sbr_x_kernel's epilogue):
+// Z = sum of the shares (fixed order), M2 = 1/2 T^T Z, W = Y - V M2 for this block's rows.
+__global__ void __launch_bounds__(SBR_X_ROWS)
+sbr_wfin_kernel(const __grid_constant__ EigBatch b, int j) {
+  const EigProb& p = b.p[blockIdx.y];
+  const int m = p.m;
+  if (p.sbr == 0 || j >= sbr_panels(m)) return;
+  constexpr int B = SBR_B, R = SBR_X_ROWS, LDT = B + 1;
+  const int r0 = (j + 1) * B, L = m - r0;
+  const int i0 = blockIdx.x * R, nrb = (L + R - 1) / R;
+  if (i0 >= L) return;
+  __shared__ float Z[B * LDT], T[B * LDT], M2[B * LDT], Ws[R * LDT];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < B * B; e += R) {
+    float a = 0.f;
+    for (int q = 0; q < nrb; ++q) a += p.Zp[(long)q * B * B + e];
+    Z[(e / B) * LDT + e % B] = a;                        // Z(a, c) at Z[a LDT + c]
+    T[(e % B) * LDT + e / B] = p.Tp[e];                  // T(a, c) at T[a LDT + c]
+  }
+  __syncthreads();
+  for (int e = tid; e < B * B; e += R) {                 // M2 = 1/2 T^T Z  (T upper: q <= a)
+    const int a = e / B, c = e % B;
+    float s = 0.f;
+    for (int q = 0; q <= a; ++q) s = fmaf(T[q * LDT + a], Z[q * LDT + c], s);
+    M2[a * LDT + c] = 0.5f * s;
+  }
+  __syncthreads();
+  const int i = i0 + tid;
+  float* Wt = p.Wt + (long)r0 * B;
+  const float* Vt = p.Vt + (long)r0 * B;
+  if (i < L) {
+    float v[B];
+#pragma unroll
+    for (int a4 = 0; a4 < B / 4; ++a4) {
+      const float4 q = *reinterpret_cast<const float4*>(Vt + (long)i * B + 4 * a4);
+      v[4 * a4] = q.x; v[4 * a4 + 1] = q.y; v[4 * a4 + 2] = q.z; v[4 * a4 + 3] = q.w;
+    }
+#pragma unroll 4
+    for (int c = 0; c < B; ++c) {
+      float w = Wt[(long)i * B + c];
+#pragma unroll
+      for (int a = 0; a < B; ++a) w = fmaf(-v[a], M2[a * LDT + c], w);
+      Ws[tid * LDT + c] = w;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < R * B; e += R) {                 // coalesced write-back of the block's W rows
+    const int li = e / B, c = e % B;
+    if (i0 + li < L) Wt[(long)(i0 + li) * B + c] = Ws[li * LDT + c];
+  }
 }
 
 // ---------------------------------------------------------------------- stage 1: block update
