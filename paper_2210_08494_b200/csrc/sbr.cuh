@@ -106,11 +106,17 @@ sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
   float* taus = rowb + 2 * B;             // B
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* K = p.K;
-  for (int e = tid; e < L * B; e += NT) {
-    const int l = e % L, i = e / L;
-    P[l * LDP + i] = K[(r0 + l) + (long)(c0 + i) * ld];
+  {   // the panel into shared memory: every element's copy in flight at once (cp.async)
+    const uint32_t pb = (uint32_t)__cvta_generic_to_shared(P);
+    for (int e = tid; e < L * B; e += NT) {
+      const int l = e % L, i = e / L;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(pb + 4u * (uint32_t)(l * LDP + i)),
+                   "l"(K + (r0 + l) + (long)(c0 + i) * ld) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   for (int e = tid; e < B * LDT; e += NT) T[e] = 0.f;
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (tid < B) rowb[tid] = P[tid];        // row 0 for step 0
   __syncthreads();

@@ -1,6 +1,6 @@
 # Scratch job for one gpurun call (rewritten per call; the outputs land in gpurun_out/).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "two_stage or cfg5_factor_shape or rank_share" > gpurun_out/s4m_pytest.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/s4m_pytest.log
-timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4m_base.json 2> gpurun_out/s4m_base.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "two_stage or cfg5_factor_shape or rank_share" > gpurun_out/s4o_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/s4o_pytest.log
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4o_base.json 2> gpurun_out/s4o_base.err
