@@ -231,18 +231,21 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
   const int j = blockIdx.y * blockDim.x + threadIdx.x;
   if (j >= r) return;
   const double tiny = s_tiny;
-  double* dUi = p.scr;                 // 1 / (U diagonal)
-  double* du = dUi + (long)m * r;      // U first superdiagonal
-  double* du2 = du + (long)m * r;      // U second superdiagonal
-  double* dl = du2 + (long)m * r;      // multipliers
+  double* dUi = p.scr;                 // 1 / (U diagonal), fp64 (tiny pivots: huge reciprocals)
+  float* du = reinterpret_cast<float*>(dUi + (long)m * r);   // U first superdiagonal (fp32)
+  float* du2 = du + (long)m * r;       // U second superdiagonal (fp32)
+  float* dl = du2 + (long)m * r;       // multipliers, |f| <= 1 (fp32)
   unsigned char* pv = p.piv;
   double* x = p.Y;
 #define AT(a, i) (a)[(long)(i) * r + j]
   if (m == 1) { AT(x, 0) = 1.0; return; }
   const double lam = p.lam[j];
-  // LU with partial pivoting of T - lam I (LAPACK dgttrf recurrence)
+  // LU with partial pivoting of T - lam I (LAPACK dgttrf recurrence), fused with the first
+  // iteration's forward pass (L^{-1} with row interchanges on the start vector, which is
+  // generated on the fly: deterministic, distinct per eigenvector)
   double dcur = dd[0] - lam;
   double dufcur = ee[0];
+  double carry = hash_unit(0u, (unsigned)j) + 0.5;
   // branch-free (threads = eigenvectors pivot differently; selects instead of divergence)
   for (int i = 0; i < m - 1; ++i) {
     const double sub = ee[i];
@@ -254,18 +257,21 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
     const double rp = inv_rcp(piv);
     const double f = (sw ? dcur : sub) * rp;
     AT(dUi, i) = rp;
-    AT(du, i) = sw ? dnext : dufcur;
-    AT(du2, i) = sw ? dunext : 0.0;
-    AT(dl, i) = f;
+    AT(du, i) = (float)(sw ? dnext : dufcur);
+    AT(du2, i) = (float)(sw ? dunext : 0.0);
+    AT(dl, i) = (float)f;
     AT(pv, i) = sw ? 1 : 0;
+    {
+      const double xs = hash_unit((unsigned)(i + 1), (unsigned)j) + 0.5;
+      AT(x, i) = sw ? xs : carry;
+      carry = sw ? carry - f * xs : xs - f * carry;
+    }
     const double ncur = (sw ? dufcur : dnext) - f * (sw ? dnext : dufcur);
     dufcur = sw ? -f * dunext : dunext;
     dcur = ncur;
   }
   if (fabs(dcur) < tiny) dcur = (dcur >= 0.0) ? tiny : -tiny;
   AT(dUi, m - 1) = 1.0 / dcur;
-  // start vector (deterministic, distinct per eigenvector)
-  for (int i = 0; i < m; ++i) AT(x, i) = hash_unit((unsigned)i, (unsigned)j) + 0.5;
   // Streaming passes in batches of IB entries: the batch's loads are issued together,
   // unguarded (full batches; the ragged end runs entry by entry), and the recurrences are
   // branch-free selects, so one memory latency is exposed per batch instead of per entry.
@@ -273,16 +279,18 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
   const long R = r;
   double* xj = x + j;
   const double* dUj = dUi + j;
-  const double* duj = du + j;
-  const double* du2j = du2 + j;
-  const double* dlj = dl + j;
+  const float* duj = du + j;
+  const float* du2j = du2 + j;
+  const float* dlj = dl + j;
   const unsigned char* pvj = pv + j;
   double s = 1.0;   // pending scale of x (applied as x is read in the next pass)
   double nrm = 0.0, amax = 0.0;
+  const double carry_lu = carry;
   for (int it = 0; it < INV_ITERS; ++it) {
-    // forward: apply L^{-1} with row interchanges; the running entry is carried
-    double carry = xj[0] * s;
-    int i0 = 0;
+    // forward: apply L^{-1} with row interchanges; the running entry is carried (the first
+    // iteration's forward pass ran inside the LU loop)
+    double carry = it == 0 ? carry_lu : xj[0] * s;
+    int i0 = it == 0 ? m - 1 : 0;
     for (; i0 + IB <= m - 1; i0 += IB) {
       double xn[IB], f[IB];
       unsigned char pw[IB];
@@ -301,7 +309,7 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
       }
     }
     for (; i0 < m - 1; ++i0) {
-      const double xs = xj[(i0 + 1) * R] * s, f = dlj[i0 * R];
+      const double xs = xj[(i0 + 1) * R] * s, f = (double)dlj[i0 * R];
       const bool sw = pvj[i0 * R] != 0;
       xj[i0 * R] = sw ? xs : carry;
       carry = sw ? carry - f * xs : xs - f * carry;
@@ -314,7 +322,8 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
     xj[(m - 1) * R] = x1;
     int i1 = m - 2;
     for (; i1 - IB + 1 >= 0; i1 -= IB) {
-      double xv[IB], a0[IB], a1[IB], a2[IB];
+      double xv[IB], a0[IB];
+      float a1[IB], a2[IB];
 #pragma unroll
       for (int u = 0; u < IB; ++u) {
         const long o = (i1 - u) * R;
