@@ -535,24 +535,47 @@ __host__ __device__ inline int bt_panels(int m, int off = 1) {
   return m > off + 1 ? (m - off - 1 + BT_PW - 1) / BT_PW : 0;
 }
 
-// grid: (nprob, 64), block 256
-__global__ void backtr_prep_kernel(const __grid_constant__ EigBatch b) {
+// grid: (nprob, 64), block 256.  (1) Unit upper-triangular top block of every panel's
+// reflector block W_j (the rows of W_j above and on its diagonal hold R / band entries):
+// zeros above the diagonal, ones on it -- the back-transform's GEMMs read W_j from its top
+// block down, nothing else of K.  (2) V = the eigenvectors of T (Zr, fp32 row-major after
+// Q2, or Y, fp64 row-major) as col-major fp32, through 32 x 32 shared-memory transposes
+// (coalesced on both sides); non-finite entries flag ST_EIG_FAIL.
+__global__ void __launch_bounds__(256) backtr_prep_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
-  const int m = p.m, r = p.r;
-  const long tot = (long)m * m;
-  for (long e = blockIdx.y * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.y * blockDim.x) {
-    const int i = (int)(e % m), k = (int)(e / m);
-    float* a = p.K + i + (long)k * p.ldk;
-    if (k >= m - p.off - 1 || i < k + p.off) *a = 0.f;
-    else if (i == k + p.off) *a = 1.f;
+  const int m = p.m, r = p.r, off = p.off;
+  constexpr int PW = BT_PW;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long nthr = (long)gridDim.y * blockDim.x;
+  const long tot = (long)bt_panels(m, off) * PW * PW;
+  for (long e = blockIdx.y * (long)blockDim.x + tid; e < tot; e += nthr) {
+    const int jp = (int)(e / (PW * PW)), rem = (int)(e % (PW * PW)), c = rem / PW, rr = rem % PW;
+    const int k0 = jp * PW, np = min(PW, m - off - 1 - k0);
+    if (c >= np || rr > c) continue;
+    p.K[(k0 + off + rr) + (long)(k0 + c) * p.ldk] = rr == c ? 1.f : 0.f;
   }
+  __shared__ float tile[8][32 * 33];
+  float* ts = tile[warp];
   int bad = 0;
-  const long tv = (long)m * r;
-  for (long e = blockIdx.y * (long)blockDim.x + threadIdx.x; e < tv; e += (long)gridDim.y * blockDim.x) {
-    const int i = (int)(e % m), j = (int)(e / m);
-    const float v = p.sbr ? p.Zr[(long)i * r + j] : (float)p.Y[(long)i * r + j];
-    bad |= !isfinite(v);
-    p.V[i + (long)j * p.ldv] = v;
+  const int ti = (m + 31) / 32, tj = (r + 31) / 32;
+  for (int t = blockIdx.y * 8 + warp; t < ti * tj; t += gridDim.y * 8) {
+    const int i0 = (t % ti) * 32, j0 = (t / ti) * 32;
+    for (int q = 0; q < 32; ++q) {          // row i0 + q, columns j0 + lane
+      const int i = i0 + q, j = j0 + lane;
+      float v = 0.f;
+      if (i < m && j < r) v = p.sbr ? p.Zr[(long)i * r + j] : (float)p.Y[(long)i * r + j];
+      ts[q * 33 + lane] = v;
+    }
+    __syncwarp();
+    for (int q = 0; q < 32; ++q) {          // column j0 + q, rows i0 + lane
+      const int i = i0 + lane, j = j0 + q;
+      if (i < m && j < r) {
+        const float v = ts[lane * 33 + q];
+        bad |= !isfinite(v);
+        p.V[i + (long)j * p.ldv] = v;
+      }
+    }
+    __syncwarp();
   }
   if (bad && p.status) atomicOr(p.status, ST_EIG_FAIL);
 }
@@ -580,17 +603,35 @@ __global__ void __launch_bounds__(BT_THREADS) backtr_t_kernel(const __grid_const
     T[a * LD + c] = 0.f;
   }
   __syncthreads();
-  for (int i = 0; i < np; ++i) {
-    const float taui = p.tau[k0 + i];
-    if (tid < i) {
-      float s = 0.f;
-      for (int c = tid; c < i; ++c) s = fmaf(T[tid * LD + c], S[c * LD + i], s);
-      T[tid * LD + i] = -taui * s;
-    } else if (tid == i) {
-      T[i * LD + i] = taui;
+  // T^{-1} = diag(1 / tau) + triu(S, 1) (I - W T W^T = H_1 ... H_np): with every tau != 0 each
+  // thread inverts one column by back substitution (no block-wide step per reflector),
+  //   T(c, c) = tau_c,  T(i, c) = -tau_i sum_{k=i+1..c} S(i, k) T(k, c)  (i = c-1 .. 0);
+  // a zero tau (H_i = I) takes the dlarft recurrence instead, one barrier per reflector.
+  const bool allnz = __syncthreads_and(tid >= np || p.tau[k0 + tid] != 0.f);
+  if (allnz) {
+    const int c = tid;
+    if (c < np) {
+      T[c * LD + c] = p.tau[k0 + c];
+      for (int i = c - 1; i >= 0; --i) {
+        float s = 0.f;
+        for (int k = i + 1; k <= c; ++k) s = fmaf(S[i * LD + k], T[k * LD + c], s);
+        T[i * LD + c] = -p.tau[k0 + i] * s;
+      }
     }
-    __syncthreads();
+  } else {
+    for (int i = 0; i < np; ++i) {
+      const float taui = p.tau[k0 + i];
+      if (tid < i) {
+        float s = 0.f;
+        for (int c = tid; c < i; ++c) s = fmaf(T[tid * LD + c], S[c * LD + i], s);
+        T[tid * LD + i] = -taui * s;
+      } else if (tid == i) {
+        T[i * LD + i] = taui;
+      }
+      __syncthreads();
+    }
   }
+  __syncthreads();
   for (int e = tid; e < PW * PW; e += BT_THREADS) {
     const int a = e % PW, c = e / PW;
     Tg[a + (long)c * PW] = T[a * LD + c];
