@@ -106,7 +106,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
  * out-of-range value.
  *   BKFAC_OPT_TWO_STAGE   eigensolver reduction: 0 auto (two-stage dense->band->tridiagonal,
  *                         sbr.cuh, for orders whose one-stage tiles do not fit a cluster's
- *                         shared memory, 864 < m <= 1632, when at least 25 such problems share
+ *                         shared memory, 864 < m <= 1632, when at least 20 such problems share
  *                         the launch; fewer run the one-stage kernel on CTA clusters), 1
  *                         one-stage only, 2 two-stage for every order it supports
  *                         (34 <= m <= 1632).  Pinned (1 or 2), a factor's result does not depend

@@ -742,9 +742,10 @@ bkfac_status run_sbr(bkfac_ctx ctx, const EigBatch& b, cudaStream_t st) {
 // cores share the launch (its chase and back-transform are per-factor latency chains, the
 // one-stage global-tile kernel is HBM-bound with one CTA per factor); with few (an 8-GPU
 // rank's share) the one-stage kernel on clusters of up to 8 CTAs per factor is faster.
-// Measured on one B200, ms per step of one rank's share of configs[4] (two-stage / one-stage):
-// 96 factors 264 / >300, 48: 147 / 171, 24: 91.4 / 91.3, 12: 66.3 / 46.5.
-constexpr int SBR_AUTO_MIN_FACTORS = 25;
+// Measured on one B200, ms per step of one rank's share of configs[4] (two-stage / one-stage),
+// round 2 session 4 (band reduction on mma.sync): 96 factors 217.6 / >300, 48: 121.1 / 155.5,
+// 24: 76.1 / 84.2, 12: 55.7 / 42.7 -- crossover near 20 (session 3: 24: 91.4 / 91.3).
+constexpr int SBR_AUTO_MIN_FACTORS = 20;
 
 bkfac_status run_eig(bkfac_ctx ctx, std::vector<EigProb>& v, cudaStream_t st) {
   if (ctx->two_stage == 0) {

@@ -45,7 +45,10 @@ constexpr int SBR_B = 32;                 // band width (= warp size: lane = row
 constexpr int SBR_LDB = 2 * SBR_B;        // band storage: diagonals 0 .. 2b-1 (bulge included)
 constexpr int SBR_PANEL_THREADS = 512;
 constexpr int SBR_W_WARPS = 16;
-constexpr int SBR_CHASE_WARPS = 16;
+#ifndef BKFAC_CHASE_WARPS
+#define BKFAC_CHASE_WARPS 16
+#endif
+constexpr int SBR_CHASE_WARPS = BKFAC_CHASE_WARPS;
 constexpr int SBR_G = 32;                 // sweeps per diamond
 constexpr int SBR_MAX_L = 1600;           // panel rows held in shared memory (m <= 1632)
 
