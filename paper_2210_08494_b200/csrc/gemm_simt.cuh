@@ -26,6 +26,7 @@ struct GemmProb {
                            // once, B re-read from L2) instead of M first
   int stream_c;            // C0 read / C written once (evict-first: keeps the operands in L2)
   int vec;                 // tcgen05 path: bit 0 A (and A2), bit 1 B (and B2) 16-byte aligned
+  int promo;               // tcgen05 path: K chunks per TMEM accumulation block (0: TC_PROMO)
   int* status;             // if set: ST_NONFINITE is OR-ed in when C0 (beta != 0) holds
                            // inf/NaN -- the tensor core does not propagate NaN reliably, so
                            // inputs are checked where an epilogue reads them anyway

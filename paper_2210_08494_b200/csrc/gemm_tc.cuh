@@ -19,7 +19,9 @@
 // (TC_PROMO * 32 of K) into a TMEM buffer; the epilogue warps add each such block into a
 // running sum (fp32 FADD, round-to-nearest; the running sum itself lives in a third TMEM
 // region, tcgen05.ld/st) while the MMA fills the other buffer.  The bias is then bounded
-// by one block's length instead of K.
+// by one block's length instead of K.  A problem may ask for longer blocks (GemmProb::promo:
+// the preconditioner's projections, whose 1e-3 tolerance leaves room for 512-term blocks,
+// take 16 chunks -- fewer promotion passes on their long K).
 //
 // Kernel anatomy (one CTA per SM, persistent over the tiles of all problems):
 //   warps 0-3  epilogue: thread = tile row = TMEM lane; promotes each K-block into the
@@ -435,7 +437,8 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
       TcTile x = tc_tile<BN, BMT>(b, t);
       x.m0 += (int)crank * TC_BM;                              // this CTA's 128 rows
       const GemmProb& p = b.p[x.pi];
-      const int nblk = (x.c_end - x.c_beg + TC_PROMO - 1) / TC_PROMO;
+      const int pro = p.promo > 0 ? p.promo : TC_PROMO;
+      const int nblk = (x.c_end - x.c_beg + pro - 1) / pro;
       const int i = x.m0 + row;
       bool nonfinite = false;   // inf/NaN in C0 (the operands' tensor-core path cannot report it)
       const float beta = p.beta_dev ? *p.beta_dev : p.beta;
@@ -637,7 +640,8 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
           const int nv = min(BN, ((b.p[x.pi].N - x.n0 + 15) >> 4) << 4);
           idesc = (IDESC & ~(0x3Fu << 17)) | ((uint32_t)(nv >> 3) << 17);
         }
-        for (int c0 = x.c_beg; c0 < x.c_end; c0 += TC_PROMO, ++kb) {
+        const int pro = b.p[x.pi].promo > 0 ? b.p[x.pi].promo : TC_PROMO;
+        for (int c0 = x.c_beg; c0 < x.c_end; c0 += pro, ++kb) {
           // swap: first K-block of the tile into its sum buffer (tl & 1), the others into
           // the other buffer (see tc_epilogue)
           const int buf = Cfg::SWAP ? ((c0 == x.c_beg) ? (tl & 1) : ((tl & 1) ^ 1)) : (kb & 1);
@@ -653,7 +657,7 @@ gemm_tc_kernel(const __grid_constant__ GemmBatch b) {
 #endif
           tc_fence_after();
           const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
-          const int c1 = min(x.c_end, c0 + TC_PROMO);
+          const int c1 = min(x.c_end, c0 + pro);
           for (int c = c0; c < c1; ++c) {
 #ifdef BKFAC_TC_TIMING
             unsigned long long t1 = clock64();
