@@ -43,7 +43,10 @@ namespace bkfac {
 
 constexpr int SBR_B = 32;                 // band width (= warp size: lane = row of a block)
 constexpr int SBR_LDB = 2 * SBR_B;        // band storage: diagonals 0 .. 2b-1 (bulge included)
-constexpr int SBR_PANEL_THREADS = 512;
+#ifndef BKFAC_PANEL_THREADS
+#define BKFAC_PANEL_THREADS 512
+#endif
+constexpr int SBR_PANEL_THREADS = BKFAC_PANEL_THREADS;
 constexpr int SBR_W_WARPS = 16;
 #ifndef BKFAC_CHASE_WARPS
 #define BKFAC_CHASE_WARPS 16
