@@ -1,7 +1,6 @@
 # Scratch job for one gpurun call (rewritten per call; the outputs land in gpurun_out/).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-for v in pt1024 pt256; do
-  lib=paper_2210_08494_b200/libbkfac_$v.so
-  BKFAC_LIB=$lib timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4z_$v.json 2> gpurun_out/s4z_$v.err
-done
+timeout 600 python tools/prof_cfg5.py > gpurun_out/s4aa_plain.log 2>&1 && \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"sbr_panel_kernel|sbr_chase_kernel" -s 96 -c 2 -o gpurun_out/s4aa_lat python tools/prof_cfg5.py > gpurun_out/s4aa_ncu.log 2>&1
+echo "rc=$?" >> gpurun_out/s4aa_ncu.log
