@@ -301,7 +301,11 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
       }
       LAUNCH_CHECK(ctx);
       if (any_split) {
-        gemm_splitk_reduce_kernel<<<dim3(64, (unsigned)n), 256, 0, st>>>(b);
+        long items = 0;   // largest reduce of the batch, in 4-row groups (about 2 per thread)
+        for (size_t i = 0; i < n; ++i)
+          if (b.p[i].splits > 1) items = std::max(items, (long)b.p[i].M * b.p[i].N / 4);
+        const unsigned gx = (unsigned)std::max(64L, std::min(2048L, (items + 511) / 512));
+        gemm_splitk_reduce_kernel<<<dim3(gx, (unsigned)n), 256, 0, st>>>(b);
         LAUNCH_CHECK(ctx);
       }
     }

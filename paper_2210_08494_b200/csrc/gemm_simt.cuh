@@ -191,6 +191,39 @@ __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmBatch b) {
   if (p.splits <= 1) return;
   const long total = (long)p.M * p.N;
   const float beta = p.beta_dev ? *p.beta_dev : p.beta;
+  if ((p.M & 3) == 0) {
+    // 4 consecutive rows of one column per thread (a symmetric problem's tile edge is a
+    // multiple of 4, so a group never straddles a tile): 16-byte partial loads, the splits'
+    // loads in flight together; the same per-element summation order as the scalar path
+    // (0 + w_0 + w_1 + ...), so results are bitwise those of the scalar loop.
+    const int M4 = p.M >> 2;
+    const long items = (long)M4 * p.N;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < items;
+         e += (long)gridDim.x * blockDim.x) {
+      const int i = (int)(e % M4) * 4, j = (int)(e / M4);
+      const bool mir = p.sym && i / p.tbm < j / p.tbm;   // upper tile
+      if (mir && p.sym == 2) continue;                   // left untouched
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      if (!mir) {
+        const float* w = p.ws + i + (long)j * p.M;
+#pragma unroll 8
+        for (int s = 0; s < p.splits; ++s) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(w + (long)s * total));
+          acc[0] += q.x; acc[1] += q.y; acc[2] += q.z; acc[3] += q.w;
+        }
+      } else {                                           // mirrored: C(i, j) = C(j, i)
+        const float* w = p.ws + j + (long)i * p.M;
+#pragma unroll 4
+        for (int s = 0; s < p.splits; ++s)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) acc[t] += __ldg(w + (long)s * total + (long)t * p.M);
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        p.C[i + t + (long)j * p.ldc] = gemm_out(p, i + t, j, gemm_row_alpha(p, i + t), acc[t], beta);
+    }
+    return;
+  }
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
        e += (long)gridDim.x * blockDim.x) {
     const int i = (int)(e % p.M), j = (int)(e / p.M);
