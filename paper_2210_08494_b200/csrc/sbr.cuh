@@ -52,7 +52,10 @@ constexpr int SBR_W_WARPS = 16;
 #define BKFAC_CHASE_WARPS 16
 #endif
 constexpr int SBR_CHASE_WARPS = BKFAC_CHASE_WARPS;
-constexpr int SBR_G = 32;                 // sweeps per diamond
+#ifndef BKFAC_SBR_G
+#define BKFAC_SBR_G 32
+#endif
+constexpr int SBR_G = BKFAC_SBR_G;        // sweeps per diamond
 constexpr int SBR_MAX_L = 1600;           // panel rows held in shared memory (m <= 1632)
 
 __host__ __device__ inline int sbr_panels(int m) { return m - 2 >= SBR_B ? (m - 2) / SBR_B : 0; }
@@ -1033,13 +1036,13 @@ sbr_chase_kernel(const __grid_constant__ EigBatch b) {
 // spread the same per-column work over more SMs (the arithmetic of a column is unchanged)
 constexpr int SBR_Q2_THREADS = 128;
 template <int NT>
-__global__ void __launch_bounds__(NT, 384 / NT)
+__global__ void __launch_bounds__(NT, (SBR_G > 32 ? 256 : 384) / NT)
 sbr_q2_kernel(const __grid_constant__ EigBatch b) {
   const EigProb& p = b.p[blockIdx.x];
   if (p.sbr == 0) return;
   const int m = p.m, r = p.r;
   constexpr int B = SBR_B, G = SBR_G, WIN = B + G - 1;
-  static_assert(G == B, "the window slides by one task (B rows) and holds G - 1 = B - 1 carried rows");
+  static_assert(G % B == 0, "the window slides by one task (B rows) and carries WIN - B = G - 1 rows");
   const int KT = sbr_tasks(m);
   const int c = blockIdx.y * NT + threadIdx.x;
   if (blockIdx.y * NT >= r) return;
