@@ -1,6 +1,5 @@
 # Scratch job for one gpurun call (rewritten per call; the outputs land in gpurun_out/).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-BKFAC_LIB=paper_2210_08494_b200/libbkfac_g64.so timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "two_stage or cfg5_factor_shape or rank_share" > gpurun_out/s4ac_pytest.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/s4ac_pytest.log
-BKFAC_LIB=paper_2210_08494_b200/libbkfac_g64.so timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4ac_g64.json 2> gpurun_out/s4ac_g64.err
+BKFAC_LIB=paper_2210_08494_b200/libbkfac_l2pf.so timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4ad_l2pf.json 2> gpurun_out/s4ad_l2pf.err
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4ad_base.json 2> gpurun_out/s4ad_base.err
