@@ -1,5 +1,6 @@
 # Scratch job for one gpurun call (rewritten per call; the outputs land in gpurun_out/).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-BKFAC_LIB=paper_2210_08494_b200/libbkfac_l2pf.so timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4ad_l2pf.json 2> gpurun_out/s4ad_l2pf.err
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4ad_base.json 2> gpurun_out/s4ad_base.err
+timeout 600 python tools/prof_cfg5.py --stage-nvtx > gpurun_out/s4ae_plain.log 2>&1 && \
+timeout 1500 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "gemm_gram/" -k regex:gemm_tc -c 1 -o gpurun_out/s4ae_gram python tools/prof_cfg5.py --stage-nvtx > gpurun_out/s4ae_ncu.log 2>&1
+echo "rc=$?" >> gpurun_out/s4ae_ncu.log
