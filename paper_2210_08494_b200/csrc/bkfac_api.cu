@@ -2252,7 +2252,7 @@ void bkfac_debug_tc(unsigned long long* host, int reset) {
   cudaMemcpyFromSymbol(host, g_tc_dbg, sizeof(unsigned long long) * 148 * 8);
 }
 #endif
-#if defined(BKFAC_CHASE_TIMING) || defined(BKFAC_Q2_TIMING)
+#if defined(BKFAC_CHASE_TIMING) || defined(BKFAC_Q2_TIMING) || defined(BKFAC_PANEL_TIMING)
 void bkfac_debug_chase(unsigned long long* host, int reset) {
   if (reset) { static unsigned long long z[8]; cudaMemcpyToSymbol(g_chase_dbg, z, sizeof(z)); return; }
   cudaMemcpyFromSymbol(host, g_chase_dbg, sizeof(unsigned long long) * 8);

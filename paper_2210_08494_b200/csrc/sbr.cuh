@@ -100,6 +100,16 @@ BKFAC_DEV float sbr_transpose_reduce(float (&v)[32], int lane) {
   return v[0];
 }
 
+#if defined(BKFAC_CHASE_TIMING) || defined(BKFAC_Q2_TIMING) || defined(BKFAC_PANEL_TIMING)
+__device__ unsigned long long g_chase_dbg[8];   // tuning builds: phase cycle sums
+#endif
+#ifdef BKFAC_PANEL_TIMING
+#define PN_T(x) const unsigned long long x = clock64()
+#define PN_ACC(k, a, b) if (blockIdx.x == 0 && tid == 0) atomicAdd(&g_chase_dbg[k], (b) - (a))
+#else
+#define PN_T(x)
+#define PN_ACC(k, a, b)
+#endif
 __global__ void __launch_bounds__(SBR_PANEL_THREADS, 1)
 sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
   const EigProb& p = b.p[blockIdx.x];
@@ -131,6 +141,7 @@ sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
   __syncthreads();
   for (int i = 0; i < B; ++i) {
     const int par = i & 1;
+    PN_T(pa);
     // ---- partial sums over this thread's rows l > i
     float v[32];
 #pragma unroll
@@ -144,7 +155,9 @@ sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
     }
     const float mine = sbr_transpose_reduce(v, lane);   // lane c: warp total of value[c]
     red[(par * NW + warp) * B + lane] = mine;
+    PN_T(pb);
     __syncthreads();
+    PN_T(pc);
     float tot = 0.f;
 #pragma unroll
     for (int w = 0; w < NW; ++w) tot += red[(par * NW + w) * B + lane];
@@ -171,6 +184,7 @@ sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
       if (lane < i) T[lane * LDT + i] = -tau * tcol;
       if (lane == i) { T[i * LDT + i] = tau; taus[i] = tau; }
     }
+    PN_T(pd);
     // ---- apply H_i to this thread's rows (scale x into v, update the later columns)
     float wl[32];
 #pragma unroll
@@ -190,12 +204,21 @@ sbr_panel_kernel(const __grid_constant__ EigBatch b, int j) {
 #pragma unroll
         for (int c = 0; c < 32; ++c) if (c > i) pr[c] = fmaf(-wl[c], vx, pr[c]);
       }
-      // publish row i + 1 (after this step's update) for the next step
-      if (l == i + 1) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) rowb[(par ^ 1) * B + c] = pr[c];
-      }
     }
+    // publish row i + 1 (after this step's update) for the next step: its owner's warp copies
+    // it lane by lane (one element each) instead of the owner alone, 32 copies in a row
+    if (i + 1 < L && warp == ((i + 1) % NT) >> 5) {
+      __syncwarp();
+      rowb[(par ^ 1) * B + lane] = P[(i + 1) * LDP + lane];
+    }
+    PN_T(pe);
+    PN_ACC(0, pa, pb); PN_ACC(1, pb, pc); PN_ACC(2, pc, pd); PN_ACC(3, pd, pe);
+    if (blockIdx.x == 0 && tid == 0) { PN_ACC(5, 0ull, 1ull); }
+#ifdef BKFAC_PANEL_TIMING
+    if (blockIdx.x == 0 && tid == 256) {   // a warp without the T column
+      atomicAdd(&g_chase_dbg[7], pb - pa); atomicAdd(&g_chase_dbg[6], pc - pb); atomicAdd(&g_chase_dbg[4], pe - pd);
+    }
+#endif
   }
   __syncthreads();
   // write back: K panel (R above / on the diagonal, reflector tails below), explicit V, T, tau
@@ -821,7 +844,6 @@ sbr_update_kernel(const __grid_constant__ EigBatch b, int j) {
 
 // ---------------------------------------------------------------------- stage 2: chase
 #if defined(BKFAC_CHASE_TIMING) || defined(BKFAC_Q2_TIMING)
-__device__ unsigned long long g_chase_dbg[8];   // tuning builds: phase cycle sums
 #define CH_T(v) const unsigned long long v = clock64()
 #define CH_ACC(i, a, b) atomicAdd(&g_chase_dbg[i], (b) - (a))
 #elif defined(BKFAC_Q2_TIMING)
