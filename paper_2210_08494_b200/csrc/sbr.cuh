@@ -679,8 +679,14 @@ sbr_wfin_kernel(const __grid_constant__ EigBatch b, int j) {
   __shared__ float Z[B * LDT], T[B * LDT], M2[B * LDT], Ws[R * LDT];
   const int tid = threadIdx.x;
   for (int e = tid; e < B * B; e += R) {
+    // the shares' loads issued together (at most NQ row blocks), then summed in order
+    constexpr int NQ = (SBR_MAX_L + SBR_B + SBR_X_ROWS - 1) / SBR_X_ROWS;
+    float zq[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) zq[q] = q < nrb ? p.Zp[(long)q * B * B + e] : 0.f;
     float a = 0.f;
-    for (int q = 0; q < nrb; ++q) a += p.Zp[(long)q * B * B + e];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) if (q < nrb) a += zq[q];
     Z[(e / B) * LDT + e % B] = a;                        // Z(a, c) at Z[a LDT + c]
     T[(e % B) * LDT + e / B] = p.Tp[e];                  // T(a, c) at T[a LDT + c]
   }
@@ -696,15 +702,17 @@ sbr_wfin_kernel(const __grid_constant__ EigBatch b, int j) {
   float* Wt = p.Wt + (long)r0 * B;
   const float* Vt = p.Vt + (long)r0 * B;
   if (i < L) {
-    float v[B];
+    float v[B], y[B];   // this row of V and of Y, loaded together
 #pragma unroll
     for (int a4 = 0; a4 < B / 4; ++a4) {
       const float4 q = *reinterpret_cast<const float4*>(Vt + (long)i * B + 4 * a4);
       v[4 * a4] = q.x; v[4 * a4 + 1] = q.y; v[4 * a4 + 2] = q.z; v[4 * a4 + 3] = q.w;
+      const float4 u = *reinterpret_cast<const float4*>(Wt + (long)i * B + 4 * a4);
+      y[4 * a4] = u.x; y[4 * a4 + 1] = u.y; y[4 * a4 + 2] = u.z; y[4 * a4 + 3] = u.w;
     }
-#pragma unroll 4
+#pragma unroll
     for (int c = 0; c < B; ++c) {
-      float w = Wt[(long)i * B + c];
+      float w = y[c];
 #pragma unroll
       for (int a = 0; a < B; ++a) w = fmaf(-v[a], M2[a * LDT + c], w);
       Ws[tid * LDT + c] = w;

@@ -1,10 +1,6 @@
 # Scratch job for one gpurun call (rewritten per call; the outputs land in gpurun_out/).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-for v in ptime ptime2; do
-BKFAC_LIB=paper_2210_08494_b200/libbkfac_$v.so timeout 600 python tools/panel_timing.py 96 > gpurun_out/s4ak_$v.log 2>&1
-done
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "two_stage or cfg5_factor_shape or rank_share" > gpurun_out/s4ak_pytest.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/s4ak_pytest.log
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4ak_base.json 2> gpurun_out/s4ak_base.err
-BKFAC_LIB=paper_2210_08494_b200/libbkfac_postt.so timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4ak_postt.json 2> gpurun_out/s4ak_postt.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "two_stage or cfg5_factor_shape or rank_share" > gpurun_out/s4al_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/s4al_pytest.log
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s4al_base.json 2> gpurun_out/s4al_base.err
