@@ -115,20 +115,36 @@ __global__ void __launch_bounds__(BIS_WARPS * 32) bisect_kernel(const __grid_con
     ddf[i] = p.d[i];
     e2f[i] = (float)(ee * ee);
   }
-  __syncthreads();
-  if (tid == 0) {
+  // Gershgorin bounds and max e^2: every thread over its rows, then a block reduction
+  // (a single thread walking m rows of global e serialised one load latency per row)
+  {
     double lo = 1e300, hi = -1e300, emax = 0.0;
-    for (int i = 0; i < m; ++i) {
+    for (int i = tid; i < m; i += blockDim.x) {
       const double r = (i > 0 ? fabs((double)p.e[i - 1]) : 0.0) + (i < m - 1 ? fabs((double)p.e[i]) : 0.0);
-      lo = fmin(lo, dd[i] - r);
-      hi = fmax(hi, dd[i] + r);
-      emax = fmax(emax, e2[i]);
+      const double di = (double)p.d[i];
+      lo = fmin(lo, di - r);
+      hi = fmax(hi, di + r);
+      if (i < m - 1) emax = fmax(emax, (double)p.e[i] * (double)p.e[i]);
     }
-    const double span = fmax(fabs(lo), fabs(hi));
-    const double pad = 2.2e-16 * span * 4.0 + 1e-300;
-    s_lo = lo - pad;
-    s_hi = hi + pad;
-    s_pivmin = 2.3e-308 * fmax(1.0, emax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    }
+    __shared__ double s_red[3][BIS_WARPS];
+    if ((tid & 31) == 0) { s_red[0][tid >> 5] = lo; s_red[1][tid >> 5] = hi; s_red[2][tid >> 5] = emax; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < BIS_WARPS; ++w) {
+        lo = fmin(lo, s_red[0][w]); hi = fmax(hi, s_red[1][w]); emax = fmax(emax, s_red[2][w]);
+      }
+      const double span = fmax(fabs(lo), fabs(hi));
+      const double pad = 2.2e-16 * span * 4.0 + 1e-300;
+      s_lo = lo - pad;
+      s_hi = hi + pad;
+      s_pivmin = 2.3e-308 * fmax(1.0, emax);
+    }
   }
   __syncthreads();
   // BIS_G lanes per eigenvalue (BIS_G probes per round, the bracket cut into BIS_G + 1
@@ -204,7 +220,7 @@ BKFAC_DEV double hash_unit(unsigned a, unsigned b) {
 // inverted (one division per LU step, none in the substitutions); each iteration is two
 // streaming passes: the 2-norm is accumulated during back substitution and the
 // normalisation is folded into the next iteration's forward pass (one final scale pass).
-constexpr int INV_THREADS = 32;
+constexpr int INV_THREADS = 32;   // one warp per CTA (the norm reduction below assumes it)
 #ifndef BKFAC_INV_ITERS
 #define BKFAC_INV_ITERS 2
 #endif
@@ -221,11 +237,13 @@ __global__ void __launch_bounds__(INV_THREADS) invit_kernel(const __grid_constan
     ee[i] = (i < m - 1) ? (double)p.e[i] : 0.0;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  {   // ||T||_inf over the warp (blockDim = 32) instead of one thread walking m rows
     double tn = 0.0;
-    for (int i = 0; i < m; ++i)
+    for (int i = threadIdx.x; i < m; i += blockDim.x)
       tn = fmax(tn, fabs(dd[i]) + fabs(ee[i]) + (i > 0 ? fabs(ee[i - 1]) : 0.0));
-    s_tiny = fmax(tn, 1e-300) * 2.2e-16;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+    if (threadIdx.x == 0) s_tiny = fmax(tn, 1e-300) * 2.2e-16;
   }
   __syncthreads();
   const int j = blockIdx.y * blockDim.x + threadIdx.x;
