@@ -7,6 +7,7 @@ from paper_2210_08494_b200 import binding
 lib = binding.load()
 n, c, r = 4097, 1024, 512
 ctx = binding.Context([(n, r, c, 0)] * 4, [], device=0)
+ctx.bkfac_set_option(binding.BKFAC_OPT_TWO_STAGE, 2)   # the chase runs on the two-stage path only
 f = synth.random_case(n, c, r, seed=5, k=256, decay=0.98, sigma=0.02)
 items = []
 for i in range(4):
