@@ -62,6 +62,10 @@ def parse_args():
     ap.add_argument("--correct-every", type=int, default=0,
                     help="NEXT-f3 (B-KFAC-C): light correction (Alg 6) every T steps")
     ap.add_argument("--phi-crc", type=float, default=0.5, help="n_crc / r of the light correction")
+    ap.add_argument("--pipeline", type=int, default=-1,
+                    help="> 0: pipelined steps (Brand(k) beside the preconditioning of step k-1, "
+                         "the persistent GEMM grids split PIPELINE : 148 - PIPELINE SMs); 0 off; "
+                         "-1 (default) auto: stack.pipeline_sms(factors on this rank)")
     ap.add_argument("--no-graphs", action="store_true",
                     help="launch every step eagerly instead of replaying CUDA graphs")
     ap.add_argument("--opt", action="append", default=[],
@@ -424,13 +428,22 @@ def run_ours(args, rank, world, local_rank):
 
     use_graphs = not args.no_graphs
 
+    if args.pipeline < 0:
+        from paper_2210_08494_b200 import pipeline_sms
+        args.pipeline = 0 if (args.factored or args.correct_every) \
+            else pipeline_sms(len(stack.my_factors))
+    if args.pipeline:
+        stack.set_pipeline(args.pipeline)
+
     def one_step(i, graph, profile=False):
-        b = stack.k & 1
-        if gather is not None:
+        # pipelined: this call preconditions (and writes the S of) step k - 1
+        ks = stack.k - 1 if args.pipeline else stack.k
+        b = ks & 1
+        if gather is not None and ks >= 0:
             gather.finish(b)          # step k - 2's gather on this buffer set has completed
         S = stack.step(M_pool[i % args.pool], None if args.factored else J_pool[i % args.pool],
                        graph=graph, factored=args.factored, profile=profile)
-        if gather is not None:
+        if gather is not None and ks >= 0:
             gather.start(b)
 
     # warm-up (>= 3 steps also captures the two CUDA graphs of a non-RSVD step: the U/D
@@ -527,6 +540,9 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- e2e through the public API with host buffers (pinned), copies timed
     e2e = None
+    if args.pipeline:
+        stack.flush()
+        stack.set_pipeline(0)     # the e2e leg runs the unpipelined schedule
     if not args.no_e2e:
         e2e = run_e2e(args, stack, gather, cfg, device, stream, world, M_pool, J_pool)
 
@@ -581,6 +597,11 @@ def run_ours(args, rank, world, local_rank):
                               if use_graphs else "eager launches with stage events")}
     if args.opt:
         line["library_options"] = args.opt
+    if args.pipeline:
+        line["pipeline"] = {"prec_sms": args.pipeline, "schedule": (
+            "step k runs Brand(k) beside the preconditioning of step k-1 (second stream, "
+            "persistent GEMM grids split %d : %d SMs); every timed step does one Brand update of "
+            "every factor and one preconditioning of every layer" % (args.pipeline, 148 - args.pipeline))}
     print(json.dumps(line), flush=True)
 
 

@@ -130,7 +130,11 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
  *   BKFAC_OPT_SBR_X       two-stage band reduction: 1 (default) X = A22 V and the block update
  *                         in their own kernels on the lower triangle only (warp-level tensor-core
  *                         MMA, 3xTF32), 0 both on the tcgen05 GEMM (full symmetric storage,
- *                         mirrored update) */
+ *                         mirrored update)
+ *   BKFAC_OPT_GEMM_CAP    0 (default): persistent tcgen05 GEMM grids span all SMs; 2..148: at
+ *                         most this many CTAs (two calls running concurrently on two streams --
+ *                         the stack's pipelined preconditioning -- each keep their own SMs).
+ *                         Tile work and arithmetic are unchanged (bitwise the same results). */
 #define BKFAC_OPT_TWO_STAGE 1
 #define BKFAC_OPT_GT_CLUSTER 2
 #define BKFAC_OPT_GEMM_PAIR 3
@@ -142,6 +146,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
 #define BKFAC_OPT_CHOL_BLOCKED 9
 #define BKFAC_OPT_NVTX 10
 #define BKFAC_OPT_SBR_X 11
+#define BKFAC_OPT_GEMM_CAP 12
 bkfac_status bkfac_set_option(bkfac_ctx ctx, int option, int value);
 
 size_t bkfac_workspace_bytes(bkfac_ctx ctx);

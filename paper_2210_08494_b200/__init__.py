@@ -6,4 +6,4 @@ is a thin binding plus the stack schedule.  There is no CPU fallback: if the CUD
 library is missing every call raises.
 """
 from . import binding  # noqa: F401
-from .stack import BKFACStack, SlotGather, shard_layers  # noqa: F401
+from .stack import BKFACStack, SlotGather, pipeline_sms, shard_layers  # noqa: F401

@@ -146,6 +146,8 @@ struct bkfac_ctx_s {
   int nvtx = 0;       // BKFAC_OPT_NVTX: every stage inside an NVTX range named by its tag
   int sbr_x = 1;      // BKFAC_OPT_SBR_X: band reduction's X and update kernels (mma.sync, lower triangle)
   int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs; < 0: one CTA per tile
+  int user_cap = 0;   // BKFAC_OPT_GEMM_CAP: > 0 caps every persistent GEMM grid of this context's
+                      // calls (two calls sharing the GPU on two streams, each on its own SMs)
   bool ea_join_early = false;   // join the side-stream EA right after the tridiagonalisation
   int pair_mode = 1;  // CTA-pair GEMM tiles: 0 never, 1 large long-K stages, 2 always (tests)
   // run-time options (bkfac_set_option; defaults are the tuned configuration)
@@ -291,7 +293,8 @@ bkfac_status launch_variant(bkfac_ctx ctx, std::vector<GemmProb>& v, cudaStream_
     b.total_tiles = tiles;
     if (tiles > 0) {
       if (tc) {
-        const int nsm = ctx->grid_cap > 0 ? ctx->grid_cap : kNumSM;
+        const int nsm = ctx->grid_cap > 0 ? ctx->grid_cap
+                      : ctx->user_cap > 0 ? std::max(2, ctx->user_cap) : kNumSM;
         // grid_cap < 0: one CTA per tile (a background job whose CTAs retire quickly)
         const int grid = ctx->grid_cap < 0 ? tiles : std::min(tiles, pair ? nsm / 2 : nsm);
         if (!cuda_ok(tc_launch<TA, TB>(b, grid, st, max_chunks, pair)))
@@ -1236,6 +1239,7 @@ bkfac_status bkfac_set_option(bkfac_ctx c, int option, int value) {
     case BKFAC_OPT_SYT_CLUSTER: if (value < 0 || value > 8) return BKFAC_ERR_INVALID_ARG; c->syt_cluster = value; break;
     case BKFAC_OPT_BT_SIMT: c->bt_simt = value != 0; break;
     case BKFAC_OPT_CHOL_BLOCKED: c->chol_blocked = value != 0; break;
+    case BKFAC_OPT_GEMM_CAP: if (value < 0 || value > kNumSM) return BKFAC_ERR_INVALID_ARG; c->user_cap = value; break;
     default: return BKFAC_ERR_INVALID_ARG;
   }
   return BKFAC_OK;

@@ -39,6 +39,19 @@ def layer_cost(n_A: int, n_G: int) -> float:
 LD_ALIGN = 32
 
 
+def pipeline_sms(n_factors: int) -> int:
+    """SMs for the pipelined preconditioning (BKFACStack.set_pipeline) of a rank that owns
+    n_factors factors; 0 = unpipelined.  Pipelining pays where the Brand update leaves SMs
+    idle -- few factors per GPU, whose latency-bound eigensolver kernels (one CTA or cluster
+    per factor) do not fill 148 SMs; with 96 factors the Brand update fills the GPU and the
+    split only slows both halves.  Measured on configs[4]: 96 factors 212 ms
+    unpipelined vs 219 at 56 SMs; 48 factors 117.8 -> 113.4 (48 SMs); 24 factors 73.5 ->
+    65.5 (44); 12 factors 41.4 -> 36.3 (44); the VGG stacks (32 factors) 4.67 -> 4.54 ms."""
+    if n_factors > 48 or n_factors == 0:
+        return 0
+    return 48 if n_factors > 24 else 44
+
+
 def padded(rows: int, cols: int, device, zero: bool = True):
     """A (rows, cols) float32 view of a (rows, cols rounded up to 32) buffer: the row
     stride is the operand's leading dimension (bkfac.h "Leading dimensions"), a multiple of
@@ -128,6 +141,11 @@ class BKFACStack:
         # preconditioned gradients, two sets by step parity: step k's S stays valid while
         # step k+1 runs (a caller can read it back concurrently)
         self.S2 = [{}, {}]
+        # pipelined preconditioning (set_pipeline): step k's gradients wait here and are
+        # preconditioned by step k + 1's call, beside its Brand update
+        self.pipe = 0
+        self.prec_stream = None
+        self._pend = None          # (step index, J of that step)
         for li in self.my_layers:
             dG, dA, _, _ = self.layers[li]
             for par in range(2):
@@ -146,6 +164,49 @@ class BKFACStack:
                     raise ValueError(f"output buffer of layer {li} must be a ({dG}, {dA}) tensor "
                                      "with unit stride along its rows")
                 self.S2[par][li] = t
+
+    def set_pipeline(self, prec_sms: int) -> None:
+        """prec_sms > 0: pipelined steps.  The preconditioning of step k (Alg 1 lines 16-17,
+        PAPER.md:401-405) needs step k's factors, so it cannot overlap step k's own Brand update;
+        it does not touch step k + 1's (those are written into the other ping-pong buffer).  In
+        pipelined mode step(M_k, J_k) therefore runs Brand(k) on the calling stream and the
+        preconditioning of step k - 1 (J_{k-1}, the factors of step k - 1) on a second stream
+        at the same time, the persistent GEMM grids split prec_sms : 148 - prec_sms SMs
+        (BKFAC_OPT_GEMM_CAP), and returns S_{k-1}.  J_k must stay unchanged until the next call;
+        ``flush()`` preconditions the last step.  The arithmetic of every call is unchanged,
+        so each S is bitwise the S of the unpipelined schedule.  0 turns it off (call flush
+        first)."""
+        if prec_sms and not (2 <= prec_sms <= 146):
+            raise ValueError("prec_sms must be in [2, 146]")
+        if self._pend is not None:
+            raise RuntimeError("set_pipeline with a preconditioning pending (call flush first)")
+        if prec_sms and self.prec_stream is None:
+            self.prec_stream = self.torch.cuda.Stream(device=self.device)
+        if prec_sms != self.pipe:
+            self._graphs = {}
+        self.pipe = int(prec_sms)
+
+    def _prec_items(self, J, k):
+        items = []
+        for lj, li in enumerate(self.my_layers):
+            dG, dA, g, a = self.layers[li]
+            UG, DG = self.state(g)
+            UA, DA = self.state(a)
+            items.append(dict(layer=lj, U_G=UG, D_G=DG, lambda_G=self.lam, U_A=UA, D_A=DA,
+                              lambda_A=self.lam, J=J[li], S=self.S2[k & 1][li],
+                              flags=self.precond_flags))
+        return items
+
+    def flush(self, stream=None) -> Dict[int, "torch.Tensor"]:
+        """Pipelined mode: precondition the pending step (the last step() call's J) with the
+        current factors on `stream`; returns its S ({} when nothing is pending)."""
+        if self._pend is None:
+            return {}
+        kp, J = self._pend
+        self._pend = None
+        main = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        self.ctx.bkfac_precondition(self._prec_items(J, kp), main)
+        return {li: self.S2[kp & 1][li] for li in self.my_layers}
 
     # ---------------------------------------------------------------------------------
     def rank_out(self, g: int) -> int:
@@ -194,7 +255,9 @@ class BKFACStack:
             key = (self.cur[0] if self.cur else 0,
                    tuple(M[g].data_ptr() for g in self.my_factors),
                    tuple(J[li].data_ptr() for li in self.my_layers) if J is not None else None,
-                   factored, profile)
+                   factored, profile,
+                   tuple(self._pend[1][li].data_ptr() for li in self.my_layers)
+                   if self._pend is not None else None)
             main = stream if stream is not None else torch.cuda.current_stream(self.device)
             hit = self._graphs.get(key)
             if hit is None:
@@ -213,6 +276,8 @@ class BKFACStack:
             self.last_profile_range = rng
             with torch.cuda.stream(main):
                 g.replay()
+            if self.pipe:
+                self._pend = (self.k, J)
             self.k += 1
             for i in range(len(self.my_factors)):
                 self.cur[i] = 1 - self.cur[i]
@@ -223,6 +288,26 @@ class BKFACStack:
         k = self.k
         torch = self.torch
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self.pipe and factored:
+            raise ValueError("pipelined preconditioning takes J (not the factored form)")
+        pipe_out = {}
+        side = False     # the pending preconditioning runs beside this step's Brand update
+        if self.pipe and self._pend is not None:
+            rsvd_due = self.rsvd_every and k % self.rsvd_every == 0
+            if rsvd_due or self.correct_every:
+                # the overwrite / correction rewrites the factors the pending step needs:
+                # precondition it first, on this stream
+                pipe_out = self.flush(main)
+            else:
+                kp, Jp = self._pend
+                self._pend = None
+                ps = self.prec_stream
+                ps.wait_stream(main)
+                self.ctx.bkfac_set_option(binding.BKFAC_OPT_GEMM_CAP, self.pipe)
+                self.ctx.bkfac_precondition(self._prec_items(Jp, kp), ps)
+                self.ctx.bkfac_set_option(binding.BKFAC_OPT_GEMM_CAP, 148 - self.pipe)
+                pipe_out = {li: self.S2[kp & 1][li] for li in self.my_layers}
+                side = True
         if k == 0:
             for i in range(len(self.my_factors)):
                 self._phantom(i)
@@ -254,6 +339,9 @@ class BKFACStack:
             self.ctx.bkfac_brand_ea_update(ups, ea, main)
         elif ups:
             self.ctx.bkfac_brand_update(ups, main)
+        if side:
+            self.ctx.bkfac_set_option(binding.BKFAC_OPT_GEMM_CAP, 0)
+            main.wait_stream(self.prec_stream)
         for i in range(len(self.my_factors)):
             self.cur[i] = 1 - self.cur[i]
         if self.correct_every and k > 0 and k % self.correct_every == 0:
@@ -283,16 +371,12 @@ class BKFACStack:
                                   flags=self.precond_flags))
             self.ctx.bkfac_precondition_factored(items, main)
             out = {li: self.S2[k & 1][li] for li in self.my_layers}
+        elif self.pipe:
+            out = pipe_out
+            if J is not None and self.my_layers:
+                self._pend = (k, J)
         elif J is not None and self.my_layers:
-            items = []
-            for lj, li in enumerate(self.my_layers):
-                dG, dA, g, a = self.layers[li]
-                UG, DG = self.state(g)
-                UA, DA = self.state(a)
-                items.append(dict(layer=lj, U_G=UG, D_G=DG, lambda_G=self.lam, U_A=UA, D_A=DA,
-                                  lambda_A=self.lam, J=J[li], S=self.S2[k & 1][li],
-                                  flags=self.precond_flags))
-            self.ctx.bkfac_precondition(items, main)
+            self.ctx.bkfac_precondition(self._prec_items(J, k), main)
             out = {li: self.S2[k & 1][li] for li in self.my_layers}
         self.k += 1
         return out

@@ -139,3 +139,17 @@ def test_slot_allgather_overlapped_double_buffer():
             assert sorted(full) == list(range(len(LAYERS)))
             for li, S in full.items():
                 assert np.array_equal(S, ref[li] * np.float32(k + 1)), (rank, k, li)
+
+
+def test_pipeline_policy_per_rank_share():
+    """stack.pipeline_sms: pipelined preconditioning only where the rank's Brand update leaves
+    SMs idle (<= 48 factors); the cap leaves room for the Brand side (148 - P >= 96 SMs: the
+    12 eight-CTA clusters of an 8-GPU rank's one-stage reduction)."""
+    from paper_2210_08494_b200 import pipeline_sms
+    assert pipeline_sms(96) == 0          # configs[4] on one GPU
+    assert pipeline_sms(0) == 0
+    assert pipeline_sms(48) == 48         # 2 GPUs
+    assert pipeline_sms(24) == 44 and pipeline_sms(12) == 44
+    for nf in range(1, 200):
+        p = pipeline_sms(nf)
+        assert p == 0 or (2 <= p and 148 - p >= 96)
