@@ -45,11 +45,12 @@ def pipeline_sms(n_factors: int) -> int:
     idle -- few factors per GPU, whose latency-bound eigensolver kernels (one CTA or cluster
     per factor) do not fill 148 SMs; with 96 factors the Brand update fills the GPU and the
     split only slows both halves.  Measured on configs[4]: 96 factors 212 ms
-    unpipelined vs 219 at 56 SMs; 48 factors 117.8 -> 113.4 (48 SMs); 24 factors 73.5 ->
-    65.5 (44); 12 factors 41.4 -> 36.3 (44); the VGG stacks (32 factors) 4.67 -> 4.54 ms."""
+    unpipelined vs 219 at 56 SMs; 48 factors 117.8 -> 109.2 (52 SMs); 24 factors 73.5 ->
+    65.3 (44-48); 12 factors 41.4 -> 36.1-36.4 (42-46); the VGG stacks (32 factors) 4.67 ->
+    4.54 ms (44)."""
     if n_factors > 48 or n_factors == 0:
         return 0
-    return 48 if n_factors > 24 else 44
+    return 52 if n_factors > 24 else 44
 
 
 def padded(rows: int, cols: int, device, zero: bool = True):

@@ -148,7 +148,7 @@ def test_pipeline_policy_per_rank_share():
     from paper_2210_08494_b200 import pipeline_sms
     assert pipeline_sms(96) == 0          # configs[4] on one GPU
     assert pipeline_sms(0) == 0
-    assert pipeline_sms(48) == 48         # 2 GPUs
+    assert pipeline_sms(48) == 52         # 2 GPUs
     assert pipeline_sms(24) == 44 and pipeline_sms(12) == 44
     for nf in range(1, 200):
         p = pipeline_sms(nf)
