@@ -134,7 +134,11 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
  *   BKFAC_OPT_GEMM_CAP    0 (default): persistent tcgen05 GEMM grids span all SMs; 2..148: at
  *                         most this many CTAs (two calls running concurrently on two streams --
  *                         the stack's pipelined preconditioning -- each keep their own SMs).
- *                         Tile work and arithmetic are unchanged (bitwise the same results). */
+ *                         Tile work and arithmetic are unchanged (bitwise the same results).
+ *   BKFAC_OPT_PREC_BLOCK  0 (default): bkfac_precondition's output GEMM accumulates its whole
+ *                         K = r_A + r_G in one TMEM block; 1..4096: blocks of this many 32-term
+ *                         chunks, each added to a running sum with round-to-nearest (8 = what
+ *                         the Brand update's GEMMs use; tighter, slower) */
 #define BKFAC_OPT_TWO_STAGE 1
 #define BKFAC_OPT_GT_CLUSTER 2
 #define BKFAC_OPT_GEMM_PAIR 3
@@ -147,6 +151,7 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
 #define BKFAC_OPT_NVTX 10
 #define BKFAC_OPT_SBR_X 11
 #define BKFAC_OPT_GEMM_CAP 12
+#define BKFAC_OPT_PREC_BLOCK 13
 bkfac_status bkfac_set_option(bkfac_ctx ctx, int option, int value);
 
 size_t bkfac_workspace_bytes(bkfac_ctx ctx);

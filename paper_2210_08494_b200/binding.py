@@ -40,6 +40,7 @@ BKFAC_OPT_CHOL_BLOCKED = 9
 BKFAC_OPT_NVTX = 10
 BKFAC_OPT_SBR_X = 11
 BKFAC_OPT_GEMM_CAP = 12
+BKFAC_OPT_PREC_BLOCK = 13
 
 STATUS = {0: "BKFAC_OK", 1: "BKFAC_ERR_INVALID_ARG", 2: "BKFAC_ERR_DIM", 3: "BKFAC_ERR_RANK",
           4: "BKFAC_ERR_ALIAS", 5: "BKFAC_ERR_WORKSPACE", 6: "BKFAC_ERR_CUDA",

@@ -146,6 +146,7 @@ struct bkfac_ctx_s {
   int nvtx = 0;       // BKFAC_OPT_NVTX: every stage inside an NVTX range named by its tag
   int sbr_x = 1;      // BKFAC_OPT_SBR_X: band reduction's X and update kernels (mma.sync, lower triangle)
   int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs; < 0: one CTA per tile
+  int prec_block = 0;  // BKFAC_OPT_PREC_BLOCK: K chunks per TMEM accumulation block of gemm_prec_out (0: whole K)
   int user_cap = 0;   // BKFAC_OPT_GEMM_CAP: > 0 caps every persistent GEMM grid of this context's
                       // calls (two calls sharing the GPU on two streams, each on its own SMs)
   bool ea_join_early = false;   // join the side-stream EA right after the tridiagonalisation
@@ -1239,6 +1240,7 @@ bkfac_status bkfac_set_option(bkfac_ctx c, int option, int value) {
     case BKFAC_OPT_SYT_CLUSTER: if (value < 0 || value > 8) return BKFAC_ERR_INVALID_ARG; c->syt_cluster = value; break;
     case BKFAC_OPT_BT_SIMT: c->bt_simt = value != 0; break;
     case BKFAC_OPT_CHOL_BLOCKED: c->chol_blocked = value != 0; break;
+    case BKFAC_OPT_PREC_BLOCK: if (value < 0 || value > 4096) return BKFAC_ERR_INVALID_ARG; c->prec_block = value; break;
     case BKFAC_OPT_GEMM_CAP: if (value < 0 || value > kNumSM) return BKFAC_ERR_INVALID_ARG; c->user_cap = value; break;
     default: return BKFAC_ERR_INVALID_ARG;
   }
@@ -2128,6 +2130,13 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     p.k1 = rA;
     p.beta_dev = lam + 2;
     p.stream_c = 1;   // J read and S written once: evict-first, the operands stay in L2
+    // one TMEM accumulation block over the whole K = r_A + r_G (no promotion passes): the
+    // tile's output then overlaps the next tile's whole mainloop in the other TMEM buffer.
+    // The tensor core's accumulate bias grows with the block length (gemm_tc.cuh), about 7e-6
+    // of the low-rank term at K = 1024, against this call's 1e-3 tolerance; the J / (lam lam)
+    // term is added in fp32 in the epilogue either way.  BKFAC_OPT_PREC_BLOCK > 0: that many
+    // 32-term chunks per block (8 = the Brand-side default).
+    p.promo = ctx->prec_block > 0 ? ctx->prec_block : 1 << 20;
     p.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);   // every element of J passes here
     gs.add(false, true, p, 0);
   }
