@@ -241,6 +241,34 @@ BKFAC_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Two 16-column loads (a K-block accumulator and the running sum) in flight together, one wait.
+#ifndef BKFAC_TC_LD2
+#define BKFAC_TC_LD2 1
+#endif
+BKFAC_DEV void tmem_ld16x2(uint32_t ta, uint32_t tb, float (&v)[16], float (&w)[16]) {
+#if !BKFAC_TC_LD2
+  tmem_ld16(ta, v);
+  tmem_ld16(tb, w);
+  return;
+#endif
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  uint32_t* q = reinterpret_cast<uint32_t*>(w);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%32];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, "
+      "%26, %27, %28, %29, %30, %31}, [%33];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]),
+        "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]),
+        "=r"(q[7]), "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]),
+        "=r"(q[14]), "=r"(q[15])
+      : "r"(ta), "r"(tb)
+      : "memory");
+}
+
 BKFAC_DEV void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
   asm volatile(
@@ -489,8 +517,7 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
 #pragma unroll 1
             for (int g = g_beg; g < g_beg + GPW; ++g) {
               float v[16], r[16];
-              tmem_ld16(Aacc + g * 16, v);
-              tmem_ld16(Ssum + g * 16, r);
+              tmem_ld16x2(Aacc + g * 16, Ssum + g * 16, v, r);
 #pragma unroll
               for (int j = 0; j < 16; j += 2) {   // FADD2: same round-to-nearest per element
                 const float2 t2 = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(r[j], r[j + 1]));
@@ -524,15 +551,16 @@ BKFAC_DEV void tc_epilogue(const GemmBatch& b, uint32_t tmem_base, int warp, int
           if (!last) break;                             // tuning only: skip promotion
 #endif
           float v[16];
-          tmem_ld16(src + g * 16, v);
           if (blk > 0) {
             float r[16];
-            tmem_ld16(run + g * 16, r);
+            tmem_ld16x2(src + g * 16, run + g * 16, v, r);
 #pragma unroll
             for (int j = 0; j < 16; j += 2) {   // FADD2: same round-to-nearest per element
               const float2 t = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(r[j], r[j + 1]));
               v[j] = t.x; v[j + 1] = t.y;
             }
+          } else {
+            tmem_ld16(src + g * 16, v);
           }
           if (!last) tmem_st16(run + g * 16, v);
           else tc_store_group(p, x, g, v, i, quarter, lane, beta, w, stage, nonfinite);
