@@ -141,6 +141,43 @@ def test_cfg1_chain_20_steps(cuda_lib):
 
 # ------------------------------------------------------------------ preconditioning
 
+@pytest.mark.parametrize("block", [0, 8])
+def test_precondition_output_block_length(cuda_lib, block):
+    """BKFAC_OPT_PREC_BLOCK: the output GEMM's K = r_A + r_G = 1024 in one TMEM accumulation
+    block (0, the default) or in 256-term blocks promoted with round-to-nearest (8).  Both must
+    meet the preconditioning tolerance against the oracle, also on the
+    components inside span(U_G) x span(U_A), where the low-rank term cancels most of
+    J / (lambda lambda) and an accumulation bias would show first."""
+    import torch
+    from paper_2210_08494_b200 import binding
+    dG, dA, rG, rA = 700, 1300, 512, 512
+    rng = np.random.default_rng(99)
+    UG, _ = np.linalg.qr(rng.standard_normal((dG, rG)))
+    UA, _ = np.linalg.qr(rng.standard_normal((dA, rA)))
+    DG = np.sort(rng.random(rG) * 5)[::-1]
+    DA = np.sort(rng.random(rA) * 5)[::-1]
+    J = (0.1 * rng.standard_normal((dG, dA))).astype(np.float32)
+    lG = lA = 0.01
+    ctx = _ctx([], [(dG, dA, rG, rA)])
+    ctx.bkfac_set_option(binding.BKFAC_OPT_PREC_BLOCK, block)
+    S = torch.empty((dG, dA), dtype=torch.float32, device="cuda")
+    ctx.bkfac_precondition([dict(layer=0, U_G=to_dev_cols(UG), D_G=to_dev(DG), lambda_G=lG,
+                                 U_A=to_dev_cols(UA), D_A=to_dev(DA), lambda_A=lA, J=to_dev(J),
+                                 S=S, flags=0)])
+    torch.cuda.synchronize()
+    f32 = lambda x: x.astype(np.float32).astype(np.float64)
+    UGf, UAf = f32(UG), f32(UA)
+    So = O.precondition(J.astype(np.float64), UGf, f32(DG), lG, UAf, f32(DA), lA,
+                        continuation=False, lam_relative=False)
+    Sg = S.double().cpu().numpy()
+    assert np.linalg.norm(Sg - So) / np.linalg.norm(So) < TOL_PREC
+    # the part of S inside both subspaces: U_G^T S U_A = (D_G + l)^-1 (U_G^T J U_A) (D_A + l)^-1
+    Pg, Po = UGf.T @ Sg @ UAf, UGf.T @ So @ UAf
+    assert np.linalg.norm(Pg - Po) / np.linalg.norm(Po) < TOL_PREC
+    code, bad, _ = ctx.bkfac_check()
+    assert code == 0
+
+
 @pytest.mark.parametrize("dims", [(128, 256, 64, 64), (512, 4609, 220, 220), (10, 513, 10, 220),
                                   (77, 301, 13, 29)])
 @pytest.mark.parametrize("flags", [0, 1, 2, 3])

@@ -1,10 +1,13 @@
 # Scratch job for one gpurun call (rewritten per call; the outputs land in gpurun_out/).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-B="timeout 400 python bench.py --no-e2e --no-cpu-baseline"
-$B > gpurun_out/s5k_cfg5_ld2.json 2> gpurun_out/s5k_cfg5_ld2.err
-BKFAC_LIB=$PWD/paper_2210_08494_b200/libbkfac_ld0.so $B > gpurun_out/s5k_cfg5_ld0.json 2> gpurun_out/s5k_cfg5_ld0.err
-$B > gpurun_out/s5k_cfg5_ld2_b.json 2> gpurun_out/s5k_cfg5_ld2_b.err
-BKFAC_LIB=$PWD/paper_2210_08494_b200/libbkfac_ld0.so $B > gpurun_out/s5k_cfg5_ld0_b.json 2> gpurun_out/s5k_cfg5_ld0_b.err
-timeout 600 python -m pytest tests/test_gpu_gemm.py -m gpu -q -x > gpurun_out/s5k_gemmtests.log 2>&1
-echo "tests rc=$?" >> gpurun_out/s5k_gemmtests.log
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/s5m_gputests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/s5m_gputests.log
+timeout 600 python bench.py > gpurun_out/s5m_cfg5.json 2> gpurun_out/s5m_cfg5.err
+for C in cfg1 cfg2 cfg3 cfg4; do
+  timeout 300 python bench.py --config $C > gpurun_out/s5m_$C.json 2> gpurun_out/s5m_$C.err
+done
+timeout 300 python bench.py --config cfg4 --full-rank --no-e2e --no-cpu-baseline > gpurun_out/s5m_cfg4_f1.json 2> gpurun_out/s5m_cfg4_f1.err
+timeout 300 python bench.py --config cfg4 --factored --no-e2e --no-cpu-baseline > gpurun_out/s5m_cfg4_f2.json 2> gpurun_out/s5m_cfg4_f2.err
+timeout 300 python bench.py --config cfg4 --correct-every 5 --no-e2e --no-cpu-baseline > gpurun_out/s5m_cfg4_f3.json 2> gpurun_out/s5m_cfg4_f3.err
+timeout 600 python bench.py > gpurun_out/s5m_cfg5_b.json 2> gpurun_out/s5m_cfg5_b.err
