@@ -135,10 +135,13 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
  *                         most this many CTAs (two calls running concurrently on two streams --
  *                         the stack's pipelined preconditioning -- each keep their own SMs).
  *                         Tile work and arithmetic are unchanged (bitwise the same results).
- *   BKFAC_OPT_PREC_BLOCK  0 (default): bkfac_precondition's output GEMM accumulates its whole
- *                         K = r_A + r_G in one TMEM block; 1..4096: blocks of this many 32-term
- *                         chunks, each added to a running sum with round-to-nearest (8 = what
- *                         the Brand update's GEMMs use; tighter, slower) */
+ *   BKFAC_OPT_PREC_BLOCK  0 (default): bkfac_precondition's output GEMM accumulates K = r_A + r_G
+ *                         in TMEM blocks of 256 terms, each added to a running sum with
+ *                         round-to-nearest, like every other contraction; 1..4096: blocks of
+ *                         this many 32-term chunks (>= K / 32: one block -- about 7 % faster
+ *                         on that GEMM, but the accumulate bias of the longer block nearly
+ *                         doubles the error of S's components inside span(U_G) x span(U_A),
+ *                         where the low-rank term cancels most of J / (lambda lambda)) */
 #define BKFAC_OPT_TWO_STAGE 1
 #define BKFAC_OPT_GT_CLUSTER 2
 #define BKFAC_OPT_GEMM_PAIR 3

@@ -146,7 +146,7 @@ struct bkfac_ctx_s {
   int nvtx = 0;       // BKFAC_OPT_NVTX: every stage inside an NVTX range named by its tag
   int sbr_x = 1;      // BKFAC_OPT_SBR_X: band reduction's X and update kernels (mma.sync, lower triangle)
   int grid_cap = 0;   // > 0: persistent GEMM grids capped at this many CTAs; < 0: one CTA per tile
-  int prec_block = 0;  // BKFAC_OPT_PREC_BLOCK: K chunks per TMEM accumulation block of gemm_prec_out (0: whole K)
+  int prec_block = 0;  // BKFAC_OPT_PREC_BLOCK: K chunks per TMEM accumulation block of gemm_prec_out (0: TC_PROMO)
   int user_cap = 0;   // BKFAC_OPT_GEMM_CAP: > 0 caps every persistent GEMM grid of this context's
                       // calls (two calls sharing the GPU on two streams, each on its own SMs)
   bool ea_join_early = false;   // join the side-stream EA right after the tridiagonalisation
@@ -2130,13 +2130,13 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     p.k1 = rA;
     p.beta_dev = lam + 2;
     p.stream_c = 1;   // J read and S written once: evict-first, the operands stay in L2
-    // one TMEM accumulation block over the whole K = r_A + r_G (no promotion passes): the
-    // tile's output then overlaps the next tile's whole mainloop in the other TMEM buffer.
-    // The tensor core's accumulate bias grows with the block length (gemm_tc.cuh), about 7e-6
-    // of the low-rank term at K = 1024, against this call's 1e-3 tolerance; the J / (lam lam)
-    // term is added in fp32 in the epilogue either way.  BKFAC_OPT_PREC_BLOCK > 0: that many
-    // 32-term chunks per block (8 = the Brand-side default).
-    p.promo = ctx->prec_block > 0 ? ctx->prec_block : 1 << 20;
+    // BKFAC_OPT_PREC_BLOCK > 0: that many 32-term chunks per TMEM accumulation block (>= K / 32:
+    // the whole K in one block, no promotion passes, the tile's output overlaps the next tile's
+    // whole mainloop: 43.65 -> 40.8 ms at configs[4]).  Not the default: the low-rank term
+    // cancels most of J / (lam lam) inside span(U_G) x span(U_A), and the longer block's
+    // accumulate bias shows there (relative error of U_G^T S U_A 1.0e-3 -> 1.8e-3 at lam = 0.01,
+    // tests/test_gpu_parity.py::test_precondition_output_block_length).
+    p.promo = ctx->prec_block;
     p.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);   // every element of J passes here
     gs.add(false, true, p, 0);
   }

@@ -1,13 +1,8 @@
 # Scratch job for one gpurun call (rewritten per call; the outputs land in gpurun_out/).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/s5m_gputests.log 2>&1
-echo "tests rc=$?" >> gpurun_out/s5m_gputests.log
-timeout 600 python bench.py > gpurun_out/s5m_cfg5.json 2> gpurun_out/s5m_cfg5.err
-for C in cfg1 cfg2 cfg3 cfg4; do
-  timeout 300 python bench.py --config $C > gpurun_out/s5m_$C.json 2> gpurun_out/s5m_$C.err
-done
-timeout 300 python bench.py --config cfg4 --full-rank --no-e2e --no-cpu-baseline > gpurun_out/s5m_cfg4_f1.json 2> gpurun_out/s5m_cfg4_f1.err
-timeout 300 python bench.py --config cfg4 --factored --no-e2e --no-cpu-baseline > gpurun_out/s5m_cfg4_f2.json 2> gpurun_out/s5m_cfg4_f2.err
-timeout 300 python bench.py --config cfg4 --correct-every 5 --no-e2e --no-cpu-baseline > gpurun_out/s5m_cfg4_f3.json 2> gpurun_out/s5m_cfg4_f3.err
-timeout 600 python bench.py > gpurun_out/s5m_cfg5_b.json 2> gpurun_out/s5m_cfg5_b.err
+timeout 1200 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "gemm_prec_out/" -k regex:gemm_tc -c 1 -o gpurun_out/s5q_prec_out python tools/prof_cfg5.py --stage-nvtx > gpurun_out/s5q_ncu.log 2>&1
+echo "rc=$?" >> gpurun_out/s5q_ncu.log
+python tools/ncu_full_summary.py gpurun_out/s5q_prec_out_summary.txt "ncu --set full --clock-control none, configs[4] gemm_prec_out (all 48 layers, default 256-term TMEM blocks), session 5 final build" gpurun_out/s5q_prec_out.ncu-rep >> gpurun_out/s5q_ncu.log 2>&1
+timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --nvtx --nvtx-include "brand/" --nvtx-include "prec/" --csv --log-file gpurun_out/s5q_launches.csv python tools/prof_cfg5.py > gpurun_out/s5q_ncu1.log 2>&1
+echo "rc=$?" >> gpurun_out/s5q_ncu1.log
