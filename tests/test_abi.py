@@ -32,6 +32,22 @@ def test_exports_every_declared_symbol(lib):
     assert sorted(binding.EXPORTED) == names
 
 
+def test_binding_constants_match_header():
+    """Every #define of include/bkfac.h that the binding mirrors (options, GEMM paths, factor
+    flags) has the same value on both sides, and every BKFAC_OPT_* of the header is mirrored."""
+    from paper_2210_08494_b200 import binding
+    src = open(os.path.join(ROOT, "include", "bkfac.h")).read()
+    defs = {m.group(1): int(m.group(2), 0)
+            for m in re.finditer(r"^#define\s+(BKFAC_[A-Z0-9_]+)\s+(0x[0-9a-fA-F]+|\d+)\s*$", src, flags=re.M)}
+    opts = [n for n in defs if n.startswith("BKFAC_OPT_")]
+    assert len(opts) >= 13 and len(set(defs[n] for n in opts)) == len(opts)
+    for n in opts:
+        assert hasattr(binding, n), f"binding lacks {n}"
+    for n, v in defs.items():
+        if hasattr(binding, n):
+            assert getattr(binding, n) == v, n
+
+
 def test_status_strings(lib):
     from paper_2210_08494_b200 import binding
     assert binding.bkfac_status_string(0) == "ok"
