@@ -2027,6 +2027,15 @@ bkfac_status bkfac_gaussian_sketch(float* Om, int n, int l, uint64_t seed, uint6
 }
 
 // ------------------------------------------------------------------------- precondition
+#ifndef BKFAC_PREC_PROJ_PROMO
+// K chunks per TMEM accumulation block of Y = J U_A, Xt = J^T U_G.  The same 256-term blocks
+// as the output GEMM: the accumulate biases of the projections and of the output product
+// largely cancel inside span(U_G) x span(U_A) when the block lengths match (relative error of
+// U_G^T S U_A at lambda = 0.01: 3.0e-4 with 256 / 256, 1.0e-3 with 512-term projections,
+// 0.85e-3 with 256-term projections and 32-term output blocks; tools/prec_block_error.py).
+// 16 (512-term blocks) is 1.6 ms faster on gemm_prec_proj and nothing on the power-capped step.
+#define BKFAC_PREC_PROJ_PROMO TC_PROMO
+#endif
 bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, int count,
                                 void* stream) {
   if (!ctx || (count > 0 && !args) || count < 0) return BKFAC_ERR_INVALID_ARG;
@@ -2079,14 +2088,14 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     if (rA > 0) {   // Y' = (J U_A) diag(sA) / lamG  (scaling in the epilogue)
       GemmProb p = gp(a.J, ldx(a.ld_J, dA), a.U_A, ldx(a.ld_UA, dA), at<float>(ctx, lp.Y), lp.ldY, dG, rA, dA, 1.f);
       p.col_scale = at<float>(ctx, lp.sA); p.alpha_dev = lam + 4;
-      p.promo = 2 * TC_PROMO;   // 512-term TMEM blocks (tolerance 1e-3): prec_proj 35.8 -> 34.2 ms
+      p.promo = BKFAC_PREC_PROJ_PROMO;
       gemm_ws(p, at<float>(ctx, lp.ws));
       gs.add(true, false, p, lp.ws_elems);
     }
     if (rG > 0) {   // Xt' = (J^T U_G) diag(sG) / lamA
       GemmProb p = gp(a.J, ldx(a.ld_J, dA), a.U_G, ldx(a.ld_UG, dG), at<float>(ctx, lp.Xt), lp.ldXt, dA, rG, dG, 1.f);
       p.col_scale = at<float>(ctx, lp.sG); p.alpha_dev = lam + 3;
-      p.promo = 2 * TC_PROMO;
+      p.promo = BKFAC_PREC_PROJ_PROMO;
       gs.add(false, false, p, 0);
     }
   }
@@ -2134,7 +2143,7 @@ bkfac_status bkfac_precondition(bkfac_ctx ctx, const bkfac_precond_args* args, i
     // the whole K in one block, no promotion passes, the tile's output overlaps the next tile's
     // whole mainloop: 43.65 -> 40.8 ms at configs[4]).  Not the default: the low-rank term
     // cancels most of J / (lam lam) inside span(U_G) x span(U_A), and the longer block's
-    // accumulate bias shows there (relative error of U_G^T S U_A 1.0e-3 -> 1.8e-3 at lam = 0.01,
+    // accumulate bias shows there (relative error of U_G^T S U_A 3.0e-4 -> 1.2e-3 at lam = 0.01,
     // tests/test_gpu_parity.py::test_precondition_output_block_length).
     p.promo = ctx->prec_block;
     p.status = status_ptr(ctx, (int)ctx->f.size() + a.layer);   // every element of J passes here

@@ -19,9 +19,8 @@
 // (TC_PROMO * 32 of K) into a TMEM buffer; the epilogue warps add each such block into a
 // running sum (fp32 FADD, round-to-nearest; the running sum itself lives in a third TMEM
 // region, tcgen05.ld/st) while the MMA fills the other buffer.  The bias is then bounded
-// by one block's length instead of K.  A problem may ask for longer blocks (GemmProb::promo:
-// the preconditioner's projections, whose 1e-3 tolerance leaves room for 512-term blocks,
-// take 16 chunks -- fewer promotion passes on their long K).
+// by one block's length instead of K.  A problem may ask for other block lengths
+// (GemmProb::promo; BKFAC_OPT_PREC_BLOCK for the preconditioner's output GEMM).
 //
 // Kernel anatomy (one CTA per SM, persistent over the tiles of all problems):
 //   warps 0-3  epilogue: thread = tile row = TMEM lane; promotes each K-block into the

@@ -149,8 +149,10 @@ def test_precondition_output_block_length(cuda_lib, block):
     (PAPER.md:401-405).  Diagnostic beside it: the components inside span(U_G) x span(U_A),
     U_G^T S U_A = (D_G + l)^-1 (U_G^T J U_A) (D_A + l)^-1, where the low-rank term cancels most
     of J / (l l): fp32 conditioning amplifies the products' error by |J| / (l l |U_G^T S U_A|)
-    (about 500 here), so the bound is 500 x 6e-6 = 3e-3; measured 1.0e-3 with 256-term blocks
-    and 1.8e-3 with one block, which is why one block is not the default."""
+    (about 500 here), so the bound is 500 x 6e-6 = 3e-3.  Measured (tools/prec_block_error.py,
+    profiles/r02s5_prec_block_error.json): 3.0e-4 with 256-term blocks in the projections and
+    in the output GEMM (their accumulate biases largely cancel when the block lengths match),
+    1.2e-3 with one output block -- which is why one block is not the default."""
     import torch
     from paper_2210_08494_b200 import binding
     dG, dA, rG, rA = 700, 1300, 512, 512
@@ -178,7 +180,7 @@ def test_precondition_output_block_length(cuda_lib, block):
     err_sub = np.linalg.norm(Pg - Po) / np.linalg.norm(Po)
     assert err_sub < 3e-3
     if block == 0:
-        assert err_sub < 1.5e-3
+        assert err_sub < 6e-4
     code, bad, _ = ctx.bkfac_check()
     assert code == 0
 

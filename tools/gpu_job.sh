@@ -1,8 +1,9 @@
 # Scratch job for one gpurun call (rewritten per call; the outputs land in gpurun_out/).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 1200 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "gemm_prec_out/" -k regex:gemm_tc -c 1 -o gpurun_out/s5q_prec_out python tools/prof_cfg5.py --stage-nvtx > gpurun_out/s5q_ncu.log 2>&1
-echo "rc=$?" >> gpurun_out/s5q_ncu.log
-python tools/ncu_full_summary.py gpurun_out/s5q_prec_out_summary.txt "ncu --set full --clock-control none, configs[4] gemm_prec_out (all 48 layers, default 256-term TMEM blocks), session 5 final build" gpurun_out/s5q_prec_out.ncu-rep >> gpurun_out/s5q_ncu.log 2>&1
-timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --nvtx --nvtx-include "brand/" --nvtx-include "prec/" --csv --log-file gpurun_out/s5q_launches.csv python tools/prof_cfg5.py > gpurun_out/s5q_ncu1.log 2>&1
-echo "rc=$?" >> gpurun_out/s5q_ncu1.log
+timeout 600 python bench.py > gpurun_out/s5t_cfg5.json 2> gpurun_out/s5t_cfg5.err
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/s5t_gputests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/s5t_gputests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/s5t_smoke.log 2>&1
+timeout 600 python tools/prec_block_error.py > gpurun_out/s5t_prec_block_error.json 2> gpurun_out/s5t_prec_block_error.err
+for C in cfg3 cfg4; do timeout 300 python bench.py --config $C > gpurun_out/s5t_$C.json 2> gpurun_out/s5t_$C.err; done
