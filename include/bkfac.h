@@ -139,8 +139,8 @@ bkfac_status bkfac_init(bkfac_ctx* out, const bkfac_factor_desc* factors, int nf
  *                         in TMEM blocks of 256 terms, each added to a running sum with
  *                         round-to-nearest, like every other contraction; 1..4096: blocks of
  *                         this many 32-term chunks (>= K / 32: one block -- about 7 % faster
- *                         on that GEMM, but the accumulate bias of the longer block no longer
- *                         matches the projections' and the error of S's components inside
+ *                         on that GEMM, but with the accumulate bias of the longer block
+ *                         the error of S's components inside
  *                         span(U_G) x span(U_A), where the low-rank term cancels most of
  *                         J / (lambda lambda), grows 4x: 3.0e-4 -> 1.2e-3 at lambda = 0.01) */
 #define BKFAC_OPT_TWO_STAGE 1

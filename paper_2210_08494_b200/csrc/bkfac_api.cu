@@ -2029,10 +2029,10 @@ bkfac_status bkfac_gaussian_sketch(float* Om, int n, int l, uint64_t seed, uint6
 // ------------------------------------------------------------------------- precondition
 #ifndef BKFAC_PREC_PROJ_PROMO
 // K chunks per TMEM accumulation block of Y = J U_A, Xt = J^T U_G.  The same 256-term blocks
-// as the output GEMM: the accumulate biases of the projections and of the output product
-// largely cancel inside span(U_G) x span(U_A) when the block lengths match (relative error of
-// U_G^T S U_A at lambda = 0.01: 3.0e-4 with 256 / 256, 1.0e-3 with 512-term projections,
-// 0.85e-3 with 256-term projections and 32-term output blocks; tools/prec_block_error.py).
+// as the output GEMM and every other contraction: the accumulate biases of the projections
+// and of the output product partly cancel inside span(U_G) x span(U_A), and 256 / 256 measured
+// best of 18 combinations (relative error of U_G^T S U_A at lambda = 0.01: 3.0e-4; 1.0e-3 with
+// 512-term projections, 0.85e-3 with 32-term output blocks; tools/prec_block_error.py).
 // 16 (512-term blocks) is 1.6 ms faster on gemm_prec_proj and nothing on the power-capped step.
 #define BKFAC_PREC_PROJ_PROMO TC_PROMO
 #endif

@@ -151,7 +151,7 @@ def test_precondition_output_block_length(cuda_lib, block):
     of J / (l l): fp32 conditioning amplifies the products' error by |J| / (l l |U_G^T S U_A|)
     (about 500 here), so the bound is 500 x 6e-6 = 3e-3.  Measured (tools/prec_block_error.py,
     profiles/r02s5_prec_block_error.json): 3.0e-4 with 256-term blocks in the projections and
-    in the output GEMM (their accumulate biases largely cancel when the block lengths match),
+    in the output GEMM (their accumulate biases partly cancel; best measured combination),
     1.2e-3 with one output block -- which is why one block is not the default."""
     import torch
     from paper_2210_08494_b200 import binding
