@@ -1,6 +1,7 @@
 """Error of bkfac_precondition against the fp64 oracle as a function of the output GEMM's TMEM
 accumulation block length (BKFAC_OPT_PREC_BLOCK), on the shape of
-tests/test_gpu_parity.py::test_precondition_output_block_length: normwise on S and on the
+tests/test_gpu_parity.py::test_precondition_output_block_length (or d_G d_A r_G r_A [blocks...]
+from the command line): normwise on S and on the
 components inside span(U_G) x span(U_A).  A measurement tool (it calls the oracle, like the
 tests do); prints one JSON line."""
 import json
@@ -20,7 +21,8 @@ def main():
     g.build()
     from paper_2210_08494_b200 import binding
     from tests.gpu_helpers import to_dev, to_dev_cols
-    dG, dA, rG, rA = 700, 1300, 512, 512
+    dG, dA, rG, rA = [int(a) for a in sys.argv[1:5]] if len(sys.argv) >= 5 else (700, 1300, 512, 512)
+    blocks = [int(a) for a in sys.argv[5:]] or [1, 2, 4, 8, 16, 32]
     rng = np.random.default_rng(99)
     UG, _ = np.linalg.qr(rng.standard_normal((dG, rG)))
     UA, _ = np.linalg.qr(rng.standard_normal((dA, rA)))
@@ -34,7 +36,7 @@ def main():
                         continuation=False, lam_relative=False)
     Po = UGf.T @ So @ UAf
     out = {"shape": [dG, dA, rG, rA], "lambda": lam, "blocks": {}}
-    for block in (1, 2, 4, 8, 16, 32):
+    for block in blocks:
         ctx = binding.Context([], [(dG, dA, rG, rA)], device=0)
         ctx.bkfac_set_option(binding.BKFAC_OPT_PREC_BLOCK, block)
         S = torch.empty((dG, dA), dtype=torch.float32, device="cuda")
